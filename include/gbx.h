@@ -1,0 +1,255 @@
+/*
+ * gbx.h -- C ABI of the B200-native hot path (libgbx.so).
+ *
+ * Drop-in boundary for the reference's (gblite, /root/reference/proj) graph
+ * object and algorithm entry points.  The reference surface is a C++ namespace
+ * API; this header is its C restatement in the LAGraph calling convention the
+ * paper uses: outputs first, then inputs, then
+ * char msg[GBX_MSG_LEN] last; int return 0 = success, < 0 error, > 0 warning.
+ * Return codes are IDENTICAL to gblite::ErrCode (include/gblite/error.hpp:13-41);
+ * codes <= -30 are new (device / runtime failures).  msg is "" on success
+ * (Status::kMaxMessage = 256, error.hpp:67).  No exceptions cross this ABI.
+ *
+ * Ownership: a gbx_graph owns device copies of A and of every cached property
+ * (graph.hpp:27-39).  Host arrays passed in are only read.  Outputs are
+ * caller-allocated host arrays of length n (or ns*n).  Passing NULL for a
+ * result array keeps the result on the device (see gbx_result_device), which
+ * is how device-resident throughput is measured.
+ *
+ * Threading: every handle owns one CUDA stream; calls are synchronous from the
+ * host's view unless every output pointer is NULL.  Calls on one handle are
+ * serialised internally.
+ *
+ * Each entry point cites the reference interface it replaces.
+ */
+#ifndef GBX_H
+#define GBX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GBX_MSG_LEN 256
+
+/* ---- error codes: gblite::ErrCode (error.hpp:13-41) + device codes ------- */
+enum {
+  GBX_SUCCESS = 0,
+  GBX_NO_VALUE = 1,
+  GBX_DIMENSION_MISMATCH = -1,
+  GBX_DOMAIN_MISMATCH = -2,
+  GBX_INDEX_OUT_OF_BOUNDS = -3,
+  GBX_INVALID_MATRIX = -4,
+  GBX_INVALID_GRAPH = -5,
+  GBX_MISSING_PROPERTY = -6,
+  GBX_SOURCE_OUT_OF_RANGE = -7,
+  GBX_EMPTY_BATCH = -8,
+  GBX_NON_POSITIVE_DAMPING = -9,
+  GBX_NON_POSITIVE_DELTA = -10,
+  GBX_NON_POSITIVE_WEIGHT = -11,
+  GBX_PRECONDITION_VIOLATED = -12,
+  GBX_PARSE_ERROR = -13,
+  GBX_DUPLICATE_ENTRY = -14,
+  GBX_IO_FAILURE = -15,
+  GBX_BAD_MAGIC = -16,
+  GBX_UNSUPPORTED_VERSION = -17,
+  GBX_TRUNCATED_STREAM = -18,
+  GBX_LENGTH_MISMATCH = -19,
+  GBX_ALIASED_OUTPUT = -20,
+  GBX_INVALID_VALUE = -21,
+  /* new: failures the CPU reference cannot have */
+  GBX_CUDA_ERROR = -30,
+  GBX_OUT_OF_MEMORY = -31,
+  GBX_UNSUPPORTED = -32,
+  GBX_NULL_ARGUMENT = -33
+};
+
+/* value domains: gblite::Domain (value.hpp:18-23) + int32 weights */
+enum { GBX_BOOL = 0, GBX_INT64 = 1, GBX_UINT64 = 2, GBX_FP64 = 3, GBX_INT32 = 4 };
+/* gblite::Kind (graph.hpp:16-19) */
+enum { GBX_DIRECTED = 0, GBX_UNDIRECTED = 1 };
+/* gblite::TriState (graph.hpp:23) */
+enum { GBX_FALSE = 0, GBX_TRUE = 1, GBX_UNKNOWN = -1 };
+/* algo::BfsConfig::Direction (algorithms.hpp:28) */
+enum { GBX_BFS_AUTO = 0, GBX_BFS_PUSH = 1, GBX_BFS_PULL = 2 };
+/* algo::TriangleCountConfig::Presort (algorithms.hpp:69) */
+enum { GBX_PRESORT_AUTO = 0, GBX_PRESORT_FORCE = 1, GBX_PRESORT_NEVER = 2 };
+
+typedef struct gbx_graph gbx_graph;
+
+/* Library / device.  Returns the library version string in msg. */
+int gbx_init(int device, char msg[GBX_MSG_LEN]);
+const char* gbx_version(void);
+
+/* ---- graph object (graph.hpp:27-60, graph.cpp:16-220) --------------------- */
+
+/* graph_new(SparseMatrix&&, Kind) (graph.cpp:16-28): validates the CSR like
+ * SparseMatrix::validate (containers.cpp:104-124) -> GBX_INVALID_MATRIX, square
+ * only.  vals may be NULL for a Bool pattern; otherwise its element type is
+ * domain (GBX_FP64 / GBX_INT64 / GBX_UINT64 / GBX_INT32 / GBX_BOOL as uint8). */
+int gbx_graph_new(gbx_graph** g, int64_t n, const int64_t* row_ptr,
+                  const int64_t* col_idx, const void* vals, int domain, int kind,
+                  char msg[GBX_MSG_LEN]);
+/* Same, with int32 column indices (saves the host-side widening). */
+int gbx_graph_new32(gbx_graph** g, int64_t n, const int64_t* row_ptr,
+                    const int32_t* col_idx, const void* vals, int domain, int kind,
+                    char msg[GBX_MSG_LEN]);
+int gbx_graph_free(gbx_graph** g, char msg[GBX_MSG_LEN]);
+
+/* Seeded synthetic graphs built directly in HBM (the BASELINE configs):
+ * R-MAT (edge_factor * 2^scale draws, quadrant probabilities a/b/c, optional id
+ * scramble; kind GBX_UNDIRECTED symmetrises) and Erdos-Renyi (degree * 2^logn
+ * uniform draws, int32 weights in [1,255] when weighted).  Self-loops and
+ * duplicates are removed (duplicates keep the minimum weight).  Bit-identical
+ * to oracle/oracle.c's generator. */
+int gbx_generate_rmat(gbx_graph** g, int scale, int edge_factor, double a, double b,
+                      double c, uint64_t seed, int scramble, int kind,
+                      char msg[GBX_MSG_LEN]);
+int gbx_generate_er(gbx_graph** g, int logn, int degree, uint64_t seed, int weighted,
+                    char msg[GBX_MSG_LEN]);
+
+/* n, nnz, kind, value domain. */
+int gbx_graph_info(const gbx_graph* g, int64_t* n, int64_t* nnz, int* kind, int* domain,
+                   char msg[GBX_MSG_LEN]);
+/* Copy A back to the host (row_ptr[n+1], col[nnz]; vals[nnz] in the graph's
+ * domain, may be NULL). */
+int gbx_graph_export(const gbx_graph* g, int64_t* row_ptr, int32_t* col, void* vals,
+                     char msg[GBX_MSG_LEN]);
+
+/* property_at / rowdegree / coldegree / symmetric_pattern / ndiag
+ * (graph.cpp:30-102) and delete_properties (graph.cpp:104-110). */
+int gbx_property_at(gbx_graph* g, char msg[GBX_MSG_LEN]);
+int gbx_property_rowdegree(gbx_graph* g, char msg[GBX_MSG_LEN]);
+int gbx_property_coldegree(gbx_graph* g, char msg[GBX_MSG_LEN]);
+int gbx_property_symmetric_pattern(gbx_graph* g, char msg[GBX_MSG_LEN]);
+int gbx_property_ndiag(gbx_graph* g, char msg[GBX_MSG_LEN]);
+int gbx_delete_properties(gbx_graph* g, char msg[GBX_MSG_LEN]);
+/* Cache status: has_at, has_rowdeg, has_coldeg (0/1), symmetric (TriState),
+ * ndiag (-1 unknown). */
+int gbx_graph_properties(const gbx_graph* g, int* has_at, int* has_rowdeg,
+                         int* has_coldeg, int* symmetric, int64_t* ndiag,
+                         char msg[GBX_MSG_LEN]);
+/* Dense row/column degree (0 for empty rows); requires the cache. */
+int gbx_row_degree(const gbx_graph* g, int64_t* deg, char msg[GBX_MSG_LEN]);
+int gbx_col_degree(const gbx_graph* g, int64_t* deg, char msg[GBX_MSG_LEN]);
+/* check_graph (graph.cpp:112-187): 0 iff every cache is consistent with A,
+ * else GBX_INVALID_GRAPH naming the first violated invariant. */
+int gbx_check_graph(const gbx_graph* g, char msg[GBX_MSG_LEN]);
+/* util::sort_by_degree(g, ascending, by_row) (util.cpp:35-44): stable. */
+int gbx_sort_by_degree(int64_t* perm, const gbx_graph* g, int ascending, int by_row,
+                       char msg[GBX_MSG_LEN]);
+
+/* ---- algorithms: advanced forms (algorithms.hpp:19-86) ---------------------
+ * Advanced calls never touch the caches and fail with GBX_MISSING_PROPERTY when
+ * one is absent; gbx_basic_* compute what is missing, then delegate
+ * (algorithms.hpp:89-104). */
+
+/* algo::bfs_push (bfs.cpp:56-62) / bfs_direction_optimizing (bfs.cpp:64-85).
+ * parent[n]: parent id, parent(source) = source, -1 = unreached.
+ * level[n] (nullable): hop count, -1 = unreached.  Parents are the minimum-id
+ * neighbour on the previous level (the reference's any.secondi in ascending k). */
+int gbx_bfs_push(int64_t* parent, int64_t* level, const gbx_graph* g, uint64_t source,
+                 char msg[GBX_MSG_LEN]);
+int gbx_bfs(int64_t* parent, int64_t* level, const gbx_graph* g, uint64_t source,
+            int direction, uint64_t push_divisor, char msg[GBX_MSG_LEN]);
+/* B200 extension: ns independent BFS runs in one multi-source sweep (64-bit
+ * lanes).  parent/level are [ns][n] row-major. */
+int gbx_bfs_batch(int64_t* parent, int64_t* level, const gbx_graph* g,
+                  const uint64_t* sources, uint64_t ns, char msg[GBX_MSG_LEN]);
+
+/* algo::pagerank_gap (pagerank.cpp:8-81): GAP PageRank, dangling mass lost.
+ * rank[n] (nullable), iterations (nullable).  fp32 ranks, fp64 row sums and
+ * fp64 L1 change (compared against tol exactly as pagerank.cpp:65-74). */
+int gbx_pagerank(double* rank, int* iterations, const gbx_graph* g, double damping,
+                 double tol, int itermax, char msg[GBX_MSG_LEN]);
+
+/* algo::triangle_count (triangle.cpp:30-64).  The count is invariant under the
+ * presort choice; presort/seed are validated and recorded but the device
+ * kernel always orients edges by ascending degree. */
+int gbx_triangle_count(uint64_t* count, const gbx_graph* g, int presort,
+                       uint64_t sample_seed, char msg[GBX_MSG_LEN]);
+
+/* algo::sssp_delta_stepping (sssp.cpp:16-112).  dist[n]: +inf = unreached.
+ * Weights must be positive (GBX_FP64, GBX_INT32 or GBX_INT64 domain). */
+int gbx_sssp(double* dist, const gbx_graph* g, uint64_t source, double delta,
+             char msg[GBX_MSG_LEN]);
+/* algo::sssp_default_delta (sssp.cpp:114-120): max weight / 2, or 1. */
+int gbx_sssp_default_delta(double* delta, const gbx_graph* g, char msg[GBX_MSG_LEN]);
+
+/* algo::betweenness_centrality (betweenness.cpp:11-86): batched Brandes,
+ * centrality[n] = sum over sources of the dependency (no halving). */
+int gbx_betweenness(double* centrality, const gbx_graph* g, const uint64_t* sources,
+                    uint64_t ns, char msg[GBX_MSG_LEN]);
+
+/* algo::connected_components_fastsv (components.cpp:35-106): label[n] = the
+ * minimum vertex id of the component. */
+int gbx_connected_components(int64_t* label, int* iterations, const gbx_graph* g,
+                             char msg[GBX_MSG_LEN]);
+
+/* ---- basic forms (algorithms.hpp:89-104) ---------------------------------- */
+int gbx_basic_bfs_push(int64_t* parent, int64_t* level, gbx_graph* g, uint64_t source,
+                       char msg[GBX_MSG_LEN]);
+int gbx_basic_bfs(int64_t* parent, int64_t* level, gbx_graph* g, uint64_t source,
+                  int direction, uint64_t push_divisor, char msg[GBX_MSG_LEN]);
+int gbx_basic_pagerank(double* rank, int* iterations, gbx_graph* g, double damping,
+                       double tol, int itermax, char msg[GBX_MSG_LEN]);
+int gbx_basic_triangle_count(uint64_t* count, gbx_graph* g, int presort,
+                             uint64_t sample_seed, char msg[GBX_MSG_LEN]);
+/* delta <= 0 means "use sssp_default_delta" (sssp.cpp:124-127). */
+int gbx_basic_sssp(double* dist, gbx_graph* g, uint64_t source, double delta,
+                   char msg[GBX_MSG_LEN]);
+int gbx_basic_betweenness(double* centrality, gbx_graph* g, const uint64_t* sources,
+                          uint64_t ns, char msg[GBX_MSG_LEN]);
+int gbx_basic_connected_components(int64_t* label, int* iterations, gbx_graph* g,
+                                   char msg[GBX_MSG_LEN]);
+
+/* ---- device plumbing (benchmarks, multi-GPU drivers) ---------------------- */
+
+/* The handle's CUDA stream (cudaStream_t) -- record events on it to time calls. */
+int gbx_graph_stream(const gbx_graph* g, void** stream, char msg[GBX_MSG_LEN]);
+/* Build the per-algorithm device layouts ahead of time so the first call does
+ * not pay for them: which = "pagerank" | "tc" | "sssp" | "bfs" | "bc". */
+int gbx_prepare(gbx_graph* g, const char* which, char msg[GBX_MSG_LEN]);
+/* Device pointer + element count of the last result of an algorithm
+ * (which as above, plus "cc"); layout documented in DESIGN.md. */
+int gbx_result_device(const gbx_graph* g, const char* which, void** ptr,
+                      int64_t* count, char msg[GBX_MSG_LEN]);
+/* Launch statistics of the last call: number of kernel launches, and for the
+ * dominant kernel its launch count and algorithmic bytes per launch. */
+typedef struct {
+  int64_t launches;            /* our kernels launched by the last call   */
+  int64_t hot_launches;        /* launches of the dominant kernel         */
+  double hot_bytes_per_launch; /* algorithmic bytes per dominant launch   */
+  int64_t work_units;          /* edges / wedges / relaxations processed  */
+  int iterations;              /* levels / iterations                     */
+} gbx_stats;
+int gbx_last_stats(const gbx_graph* g, gbx_stats* stats, char msg[GBX_MSG_LEN]);
+
+/* ---- sharded PageRank step for the multi-GPU driver (1D row blocks) -------
+ * One process per GPU owns rows [row_begin, row_end) of AT (the in-edges of its
+ * destination vertices) and the full gathered contribution vector x (fp32, n).
+ * gbx_pr_shard_step computes, for its rows, r_new = teleport + sum x(k),
+ * x_new = r_new * damping / outdeg (0 if dangling) and the fp64 L1 partial;
+ * all three stay on the device (device pointers).  The caller all-gathers
+ * x_new (NCCL) and all-reduces the L1 partial. */
+int gbx_pr_shard_prepare(gbx_graph* g, int64_t row_begin, int64_t row_end,
+                         char msg[GBX_MSG_LEN]);
+int gbx_pr_shard_step(gbx_graph* g, const float* x_full_dev, float* r_dev,
+                      float* x_new_dev, double* l1_dev, double damping,
+                      char msg[GBX_MSG_LEN]);
+/* Rows [row_begin,row_end) of a split with balanced nnz + rows (merge-path). */
+int gbx_partition_rows(int64_t* bounds, const gbx_graph* g, int parts, int transposed,
+                       char msg[GBX_MSG_LEN]);
+/* Triangle count restricted to oriented rows [row_begin, row_end) of the
+ * degree-ordered U (for wedge-balanced sharding; sum over shards = count). */
+int gbx_triangle_count_rows(uint64_t* count, const gbx_graph* g, int64_t row_begin,
+                            int64_t row_end, char msg[GBX_MSG_LEN]);
+/* Wedge-balanced split of the oriented rows into parts. */
+int gbx_tc_partition(int64_t* bounds, gbx_graph* g, int parts, char msg[GBX_MSG_LEN]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GBX_H */

@@ -398,21 +398,3 @@ def csr_from_dense(adj):
         vals.extend(a[i, nz].tolist())
         rp[i + 1] = len(cols)
     return rp, np.array(cols, np.int32), np.array(vals, np.float64)
-
-
-def pick_sources(deg, count, seed, stream=7):
-    """Seeded sources among vertices with deg > 0 (distinct while possible)."""
-    L = lib()
-    n = len(deg)
-    s = L.orc_stream(seed, stream)
-    out, seen = [], set()
-    cand_ok = int(np.count_nonzero(deg))
-    i = 0
-    while len(out) < count and cand_ok > 0:
-        r = L.orc_draw(s, i)
-        i += 1
-        c = (r * n) >> 64
-        if deg[c] > 0 and (c not in seen or len(seen) >= cand_ok):
-            out.append(int(c))
-            seen.add(int(c))
-    return np.array(out, np.int64)

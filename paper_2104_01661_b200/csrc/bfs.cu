@@ -1,0 +1,611 @@
+// bfs.cu -- direction-optimizing BFS (algo/bfs.cpp:18-85) and a 64-lane
+// multi-source BFS, each as ONE persistent cooperative kernel: the level loop,
+// the push/pull decision and the frontier swap all run on the device with
+// grid-wide barriers, so a whole traversal costs one launch (scale-16 BFS is
+// latency-bound: SURVEY.md §7 hard part 7).
+//
+// Parent semantics: the reference's any.secondi keeps the first contribution in
+// ascending frontier order (core.cpp:214-222, ops.cpp:170-175), i.e. the
+// minimum-id neighbour on the previous level.  Push reproduces it with
+// atomicMin over every frontier edge into an unvisited vertex; pull scans the
+// ascending AT row and keeps the first frontier hit.  Both are bit-exact.
+//
+// Frontier: queue of (vertex, chunk) entries (push: one warp per <= kChunk
+// edges, so hubs are split) plus a bitmap (pull: 1 bit per vertex, L2/L1
+// resident).  Compaction into the next queue is warp-aggregated (one atomic
+// per warp).  Direction rule = the reference's (bfs.cpp:77-78): push iff the
+// frontier has < n/push_divisor + 1 vertices and is growing.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include "common.cuh"
+#include "plans.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gbx {
+
+constexpr int kBfsThreads = 256;
+constexpr int64_t kChunk = 1024;
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ int n_chunks(int64_t deg) {
+  return deg <= kChunk ? 1 : static_cast<int>((deg + kChunk - 1) / kChunk);
+}
+
+// Append (vertex, chunk) entries for every lane with has=true; whole warp calls.
+__device__ __forceinline__ void warp_append(bool has, int64_t v, int64_t deg, int64_t* q,
+                                            int* cnt_ent, int* cnt_vtx,
+                                            unsigned long long* cnt_edges) {
+  const int lane = threadIdx.x & 31;
+  int k = has ? n_chunks(deg) : 0;
+  int incl = k;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
+  }
+  int tot = __shfl_sync(kFull, incl, 31);
+  if (tot == 0) return;
+  unsigned vb = __ballot_sync(kFull, has);
+  unsigned long long e = has ? static_cast<unsigned long long>(deg) : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
+  int base = 0;
+  if (lane == 0) {
+    base = atomicAdd(cnt_ent, tot);
+    atomicAdd(cnt_vtx, __popc(vb));
+    if (cnt_edges) atomicAdd(cnt_edges, e);
+  }
+  base = __shfl_sync(kFull, base, 0);
+  if (has) {
+    int off = base + incl - k;
+    for (int c = 0; c < k; ++c) q[off + c] = (static_cast<int64_t>(c) << 32) | v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// single source
+// ---------------------------------------------------------------------------
+struct Bfs1Args {
+  const int64_t* rp;
+  const int32_t* col;
+  const int64_t* trp;
+  const int32_t* tcol;
+  int64_t n;
+  int mode;
+  int64_t divisor;
+  int32_t* level;
+  int32_t* parent;
+  int64_t* q0;
+  int64_t* q1;
+  uint32_t* bm0;
+  uint32_t* bm1;
+  int* ctl;  // [0] entries [1] vertices [2] next entries [3] next vertices [4] prev vertices
+             // [5] levels done [6] push levels
+};
+
+__global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t gsize = int64_t(gridDim.x) * blockDim.x;
+  const int64_t nwords = (a.n + 31) >> 5;
+  for (int d = 1; static_cast<int64_t>(d) + 1 <= a.n; ++d) {
+    const int qe = *(volatile int*)&a.ctl[0];
+    const int qv = *(volatile int*)&a.ctl[1];
+    const int pv = *(volatile int*)&a.ctl[4];
+    if (qv == 0) break;
+    const bool push = a.mode == GBX_BFS_PUSH ||
+                      (a.mode == GBX_BFS_AUTO && qv < a.n / a.divisor + 1 && qv > pv);
+    const int p = (d - 1) & 1;
+    const int64_t* qc = p ? a.q1 : a.q0;
+    int64_t* qn = p ? a.q0 : a.q1;
+    const uint32_t* bc = p ? a.bm1 : a.bm0;
+    uint32_t* bn = p ? a.bm0 : a.bm1;
+    if (push) {
+      for (int64_t e = gwarp; e < qe; e += nwarps) {
+        const int64_t ent = qc[e];
+        const int32_t v = static_cast<int32_t>(ent & 0xffffffff);
+        const int64_t c = ent >> 32;
+        const int64_t b0 = a.rp[v] + c * kChunk;
+        const int64_t e0 = min(a.rp[v + 1], b0 + kChunk);
+        for (int64_t base = b0; base < e0; base += 32) {
+          const int64_t q = base + lane;
+          bool has = false;
+          int32_t w = 0;
+          if (q < e0) {
+            w = __ldg(a.col + q);
+            int lw = *(volatile int32_t*)&a.level[w];
+            if (lw == -1 || lw == d) {
+              atomicMin(&a.parent[w], v);
+              if (lw == -1 && atomicCAS(&a.level[w], -1, d) == -1) {
+                has = true;
+                atomicOr(&bn[w >> 5], 1u << (w & 31));
+              }
+            }
+          }
+          const int64_t dw = has ? a.rp[w + 1] - a.rp[w] : 0;
+          warp_append(has, w, dw, qn, &a.ctl[2], &a.ctl[3], nullptr);
+        }
+      }
+    } else {
+      const int grp = lane >> 3, sub = lane & 7;
+      for (int64_t vb = gwarp * 4; vb < a.n; vb += nwarps * 4) {
+        const int64_t w = vb + grp;
+        bool active = w < a.n && a.level[w] == -1;
+        int64_t pp = active ? a.trp[w] : 0, pe = active ? a.trp[w + 1] : 0;
+        int32_t found = -1;
+        while (__any_sync(kFull, active)) {
+          int32_t u = -1;
+          bool hit = false;
+          if (active && pp + sub < pe) {
+            u = __ldg(a.tcol + pp + sub);
+            hit = (__ldg(bc + (u >> 5)) >> (u & 31)) & 1u;
+          }
+          const unsigned bal = __ballot_sync(kFull, hit);
+          const unsigned gb = (bal >> (grp * 8)) & 0xffu;
+          const int src = grp * 8 + (gb ? __ffs(gb) - 1 : 0);
+          const int32_t uu = __shfl_sync(kFull, u, src);
+          if (active) {
+            if (gb) { found = uu; active = false; }
+            else { pp += 8; if (pp >= pe) active = false; }
+          }
+        }
+        const bool has = sub == 0 && found >= 0;
+        if (has) {
+          a.level[w] = d;
+          a.parent[w] = found;
+          atomicOr(&bn[w >> 5], 1u << (w & 31));
+        }
+        const int64_t dw = has ? a.rp[w + 1] - a.rp[w] : 0;
+        warp_append(has, w, dw, qn, &a.ctl[2], &a.ctl[3], nullptr);
+      }
+    }
+    grid.sync();
+    // roll the frontier: the current bitmap is cleared for reuse two levels on
+    uint32_t* bclr = const_cast<uint32_t*>(bc);
+    for (int64_t i = gtid; i < nwords; i += gsize) bclr[i] = 0u;
+    if (gtid == 0) {
+      a.ctl[4] = qv;
+      a.ctl[0] = a.ctl[2];
+      a.ctl[1] = a.ctl[3];
+      a.ctl[2] = 0;
+      a.ctl[3] = 0;
+      a.ctl[5] = d;
+      if (push) a.ctl[6] += 1;
+    }
+    grid.sync();
+  }
+}
+
+__global__ void k_bfs1_init(int32_t* level, int32_t* parent, uint32_t* bm0, uint32_t* bm1,
+                            int64_t n) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) { level[i] = -1; parent[i] = INT_MAX; }
+  if (i < (n + 31) / 32) { bm0[i] = 0; bm1[i] = 0; }
+}
+
+__global__ void k_bfs1_seed(int32_t* level, int32_t* parent, uint32_t* bm0, int64_t* q0,
+                            int* ctl, const int64_t* rp, int32_t s) {
+  level[s] = 0;
+  parent[s] = s;
+  bm0[s >> 5] |= 1u << (s & 31);
+  int64_t deg = rp[s + 1] - rp[s];
+  int k = n_chunks(deg);
+  for (int c = 0; c < k; ++c) q0[c] = (static_cast<int64_t>(c) << 32) | s;
+  for (int i = 0; i < 8; ++i) ctl[i] = 0;
+  ctl[0] = k;
+  ctl[1] = 1;
+}
+
+__global__ void k_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, int32_t none) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = in[i] == none ? -1 : in[i];
+}
+
+static int coop_grid(const void* fn, int threads) {
+  int per_sm = 0;
+  GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));
+  if (per_sm < 1) fail(GBX_CUDA_ERROR, "cooperative kernel does not fit on an SM");
+  return device_sms() * per_sm;
+}
+
+static void ensure_bfs1(gbx_graph* g) {
+  if (!g->bfs) g->bfs = std::make_unique<BfsWork>();
+  BfsWork& W = *g->bfs;
+  const int64_t n = g->A.n;
+  if (W.n == n && W.level.p) return;
+  W.n = n;
+  W.level.alloc(std::max<int64_t>(n, 1));
+  W.parent.alloc(std::max<int64_t>(n, 1));
+  const int64_t qcap = n + g->A.nnz / kChunk + 64;
+  W.queue[0].alloc(2 * qcap);  // int64 entries stored in int32 pairs
+  W.queue[1].alloc(2 * qcap);
+  W.bitmap[0].alloc((n + 31) / 32 + 1);
+  W.bitmap[1].alloc((n + 31) / 32 + 1);
+  W.ctl.alloc(8);
+}
+
+void bfs_prepare(gbx_graph* g) { ensure_bfs1(g); }
+
+static void copy_out_i64(cudaStream_t s, const int32_t* dev, int64_t n, int32_t none,
+                         int64_t* host) {
+  int64_t* tmp = nullptr;
+  GBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), std::max<int64_t>(n, 1) * 8, s));
+  k_i32_to_i64<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, s>>>(dev, tmp, n, none);
+  cudaError_t le = cudaGetLastError();
+  if (le == cudaSuccess)
+    le = cudaMemcpyAsync(host, tmp, n * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(tmp, s);
+  GBX_CUDA(le);
+}
+
+void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor,
+             bool use_at, int64_t* parent, int64_t* level) {
+  const int64_t n = g->A.n;
+  if (source >= static_cast<uint64_t>(n))
+    fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(source) + " with n = " +
+                                      std::to_string(n));
+  if (direction != GBX_BFS_AUTO && direction != GBX_BFS_PUSH && direction != GBX_BFS_PULL)
+    fail(GBX_INVALID_VALUE, "bfs: unknown direction");
+  ensure_bfs1(g);
+  BfsWork& W = *g->bfs;
+  cudaStream_t s = g->stream;
+  const Csr& A = g->A;
+  const Csr* AT = use_at ? &g->AT() : nullptr;
+  k_bfs1_init<<<ceil_div(n, 256), 256, 0, s>>>(W.level.p, W.parent.p, W.bitmap[0].p,
+                                                 W.bitmap[1].p, n);
+  GBX_LAUNCHED();
+  int64_t* q0 = reinterpret_cast<int64_t*>(W.queue[0].p);
+  int64_t* q1 = reinterpret_cast<int64_t*>(W.queue[1].p);
+  k_bfs1_seed<<<1, 1, 0, s>>>(W.level.p, W.parent.p, W.bitmap[0].p, q0, W.ctl.p, A.rp.p,
+                              static_cast<int32_t>(source));
+  GBX_LAUNCHED();
+  Bfs1Args a{};
+  a.rp = A.rp.p;
+  a.col = A.col.p;
+  a.trp = AT ? AT->rp.p : nullptr;
+  a.tcol = AT ? AT->col.p : nullptr;
+  a.n = n;
+  a.mode = use_at ? direction : GBX_BFS_PUSH;
+  a.divisor = push_divisor == 0 ? 1 : static_cast<int64_t>(push_divisor);
+  a.level = W.level.p;
+  a.parent = W.parent.p;
+  a.q0 = q0;
+  a.q1 = q1;
+  a.bm0 = W.bitmap[0].p;
+  a.bm1 = W.bitmap[1].p;
+  a.ctl = W.ctl.p;
+  static int grid = 0;
+  if (!grid) grid = coop_grid(reinterpret_cast<const void*>(k_bfs1), kBfsThreads);
+  void* args[] = {&a};
+  if (n > 1) {
+    GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_bfs1), dim3(grid),
+                                         dim3(kBfsThreads), args, 0, s));
+  }
+  if (parent) copy_out_i64(s, W.parent.p, n, INT_MAX, parent);
+  if (level) copy_out_i64(s, W.level.p, n, -1, level);
+  int hctl[8] = {0};
+  GBX_CUDA(cudaMemcpyAsync(hctl, W.ctl.p, sizeof hctl, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  g->stats = gbx_stats{};
+  g->stats.launches = 3 + (parent ? 1 : 0) + (level ? 1 : 0);
+  g->stats.hot_launches = 1;
+  g->stats.iterations = hctl[5];
+}
+
+// ---------------------------------------------------------------------------
+// multi-source: 64 lanes, one bit per source in seen/frontier words
+// ---------------------------------------------------------------------------
+struct Bfs64Args {
+  const int64_t* rp;
+  const int32_t* col;
+  const int64_t* trp;
+  const int32_t* tcol;
+  int64_t n, nnz;
+  unsigned long long lanes;
+  unsigned long long* seen;
+  unsigned long long* f0;
+  unsigned long long* f1;
+  int32_t* mlevel;   // [n][64]
+  int32_t* mparent;  // [n][64]
+  int64_t* q0;
+  int64_t* q1;
+  int* ctl;  // [0] entries [1] vertices [2] next entries [3] next vertices [5] levels [6] push
+  unsigned long long* edges;  // [0] frontier edges cur, [1] next
+};
+
+__global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int d = 1; static_cast<int64_t>(d) + 1 <= a.n; ++d) {
+    const int qe = *(volatile int*)&a.ctl[0];
+    const int qv = *(volatile int*)&a.ctl[1];
+    const unsigned long long fe = *(volatile unsigned long long*)&a.edges[0];
+    if (qv == 0) break;
+    const bool push = fe * 20ull < static_cast<unsigned long long>(a.nnz) + 20ull;
+    const int p = (d - 1) & 1;
+    const int64_t* qc = p ? a.q1 : a.q0;
+    int64_t* qn = p ? a.q0 : a.q1;
+    unsigned long long* fc = p ? a.f1 : a.f0;
+    unsigned long long* fn = p ? a.f0 : a.f1;
+    if (push) {
+      for (int64_t e = gwarp; e < qe; e += nwarps) {
+        const int64_t ent = qc[e];
+        const int32_t v = static_cast<int32_t>(ent & 0xffffffff);
+        const int64_t c = ent >> 32;
+        const unsigned long long f = fc[v];
+        const int64_t b0 = a.rp[v] + c * kChunk;
+        const int64_t e0 = min(a.rp[v + 1], b0 + kChunk);
+        for (int64_t base = b0; base < e0; base += 32) {
+          const int64_t q = base + lane;
+          bool has = false;
+          int32_t w = 0;
+          if (q < e0) {
+            w = __ldg(a.col + q);
+            unsigned long long bits = f & ~a.seen[w];
+            if (bits) {
+              unsigned long long old = atomicOr(&fn[w], bits);
+              has = old == 0ull;
+              while (bits) {
+                int b = __ffsll(static_cast<long long>(bits)) - 1;
+                bits &= bits - 1;
+                atomicMin(&a.mparent[static_cast<int64_t>(w) * 64 + b], v);
+              }
+            }
+          }
+          const int64_t dw = has ? a.rp[w + 1] - a.rp[w] : 0;
+          warp_append(has, w, dw, qn, &a.ctl[2], &a.ctl[3], &a.edges[1]);
+        }
+      }
+    } else {
+      const int grp = lane >> 3, sub = lane & 7;
+      const unsigned gmask = 0xffu << (grp * 8);
+      for (int64_t vb = gwarp * 4; vb < a.n; vb += nwarps * 4) {
+        const int64_t w = vb + grp;
+        unsigned long long need = w < a.n ? (~a.seen[w] & a.lanes) : 0ull;
+        bool active = need != 0ull;
+        int64_t pp = active ? a.trp[w] : 0, pe = active ? a.trp[w + 1] : 0;
+        unsigned long long found = 0ull;
+        while (__any_sync(kFull, active)) {
+          int32_t u = -1;
+          unsigned long long hit = 0ull;
+          if (active && pp + sub < pe) {
+            u = __ldg(a.tcol + pp + sub);
+            hit = __ldg(fc + u) & need;
+          }
+          // exclusive prefix-OR over the 8 lanes of the group: the lowest
+          // lane (smallest neighbour id) claims each newly found source bit
+          unsigned long long incl = hit;
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) {
+            unsigned long long t = __shfl_up_sync(kFull, incl, o);
+            if (sub >= o) incl |= t;
+          }
+          unsigned long long excl = __shfl_up_sync(kFull, incl, 1);
+          if (sub == 0) excl = 0ull;
+          unsigned long long mine = hit & ~excl;
+          const unsigned long long tot = __shfl_sync(kFull, incl, grp * 8 + 7);
+          (void)gmask;
+          while (mine) {
+            int b = __ffsll(static_cast<long long>(mine)) - 1;
+            mine &= mine - 1;
+            a.mparent[w * 64 + b] = u;
+          }
+          if (active) {
+            found |= tot;
+            need &= ~tot;
+            pp += 8;
+            if (need == 0ull || pp >= pe) active = false;
+          }
+        }
+        const bool has = sub == 0 && found != 0ull;
+        if (has) fn[w] = found;
+        const int64_t dw = has ? a.rp[w + 1] - a.rp[w] : 0;
+        warp_append(has, w, dw, qn, &a.ctl[2], &a.ctl[3], &a.edges[1]);
+      }
+    }
+    grid.sync();
+    // finalize: new frontier bits become seen + level d; old frontier cleared
+    const int qn_e = *(volatile int*)&a.ctl[2];
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < qn_e;
+         e += int64_t(gridDim.x) * blockDim.x) {
+      const int64_t ent = qn[e];
+      if ((ent >> 32) != 0) continue;
+      const int32_t w = static_cast<int32_t>(ent & 0xffffffff);
+      unsigned long long nb = fn[w];
+      a.seen[w] |= nb;
+      while (nb) {
+        int b = __ffsll(static_cast<long long>(nb)) - 1;
+        nb &= nb - 1;
+        a.mlevel[static_cast<int64_t>(w) * 64 + b] = d;
+      }
+    }
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < qe;
+         e += int64_t(gridDim.x) * blockDim.x) {
+      const int64_t ent = qc[e];
+      if ((ent >> 32) == 0) fc[static_cast<int32_t>(ent & 0xffffffff)] = 0ull;
+    }
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.ctl[0] = a.ctl[2];
+      a.ctl[1] = a.ctl[3];
+      a.ctl[2] = 0;
+      a.ctl[3] = 0;
+      a.ctl[5] = d;
+      if (push) a.ctl[6] += 1;
+      a.edges[0] = a.edges[1];
+      a.edges[1] = 0ull;
+    }
+    grid.sync();
+  }
+}
+
+__global__ void k_bfs64_init(unsigned long long* seen, unsigned long long* f0,
+                             unsigned long long* f1, int32_t* mlevel, int32_t* mparent,
+                             int64_t n) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) { seen[i] = 0ull; f0[i] = 0ull; f1[i] = 0ull; }
+  if (i < n * 64) { mlevel[i] = -1; mparent[i] = INT_MAX; }
+}
+
+__global__ void k_bfs64_seed(const int32_t* src, int ns, unsigned long long* seen,
+                             unsigned long long* f0, int32_t* mlevel, int32_t* mparent) {
+  for (int b = 0; b < ns; ++b) {
+    int32_t s = src[b];
+    seen[s] |= 1ull << b;
+    f0[s] |= 1ull << b;
+    mlevel[static_cast<int64_t>(s) * 64 + b] = 0;
+    mparent[static_cast<int64_t>(s) * 64 + b] = s;
+  }
+}
+
+// [n][64] int32 -> [ns][n] int64 (-1 for none)
+__global__ void k_lanes_out(const int32_t* in, int64_t n, int ns, int32_t none, int64_t* out) {
+  __shared__ int32_t tile[32][65];
+  const int64_t v0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    int64_t v = v0 + r;
+    for (int b = threadIdx.x; b < 64; b += blockDim.x)
+      tile[r][b] = v < n ? in[v * 64 + b] : none;
+  }
+  __syncthreads();
+  for (int b = threadIdx.y; b < ns; b += blockDim.y) {
+    int64_t v = v0 + threadIdx.x;
+    if (v < n) {
+      int32_t x = tile[threadIdx.x][b];
+      out[static_cast<int64_t>(b) * n + v] = x == none ? -1 : x;
+    }
+  }
+}
+
+static void ensure_bfs64(gbx_graph* g) {
+  if (!g->bfs) g->bfs = std::make_unique<BfsWork>();
+  BfsWork& W = *g->bfs;
+  const int64_t n = g->A.n;
+  if (W.seen.p && W.seen.n >= static_cast<size_t>(std::max<int64_t>(n, 1))) return;
+  W.seen.alloc(std::max<int64_t>(n, 1));
+  W.front.alloc(std::max<int64_t>(n, 1));
+  W.next.alloc(std::max<int64_t>(n, 1));
+  W.mlevel.alloc(std::max<int64_t>(n, 1) * 64);
+  W.mparent.alloc(std::max<int64_t>(n, 1) * 64);
+  const int64_t qcap = n + g->A.nnz / kChunk + 64;
+  W.mqueue[0].alloc(2 * qcap);
+  W.mqueue[1].alloc(2 * qcap);
+  W.mctl.alloc(12);
+}
+
+void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* parent,
+                   int64_t* level) {
+  require_at(g, "bfs_batch");
+  const int64_t n = g->A.n;
+  if (ns == 0) fail(GBX_EMPTY_BATCH, "empty source batch");
+  for (uint64_t b = 0; b < ns; ++b)
+    if (sources[b] >= static_cast<uint64_t>(n))
+      fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(sources[b]));
+  ensure_bfs64(g);
+  BfsWork& W = *g->bfs;
+  cudaStream_t s = g->stream;
+  const Csr& A = g->A;
+  const Csr& AT = g->AT();
+  static int grid = 0;
+  if (!grid) grid = coop_grid(reinterpret_cast<const void*>(k_bfs64), kBfsThreads);
+  int64_t total_launches = 0;
+  for (uint64_t b0 = 0; b0 < ns; b0 += 64) {
+    const int nb = static_cast<int>(std::min<uint64_t>(64, ns - b0));
+    k_bfs64_init<<<ceil_div(n * 64, 256), 256, 0, s>>>(W.seen.p, W.front.p, W.next.p,
+                                                       W.mlevel.p, W.mparent.p, n);
+    GBX_LAUNCHED();
+    // initial queue: distinct source vertices, chunked by degree
+    std::vector<int32_t> src(nb);
+    for (int b = 0; b < nb; ++b) src[b] = static_cast<int32_t>(sources[b0 + b]);
+    std::vector<int64_t> rph(2);
+    std::vector<int32_t> uniq(src);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    std::vector<int64_t> q;
+    unsigned long long fedges = 0;
+    for (int32_t v : uniq) {
+      int64_t r[2];
+      GBX_CUDA(cudaMemcpyAsync(r, A.rp.p + v, 16, cudaMemcpyDeviceToHost, s));
+      GBX_CUDA(cudaStreamSynchronize(s));
+      int64_t deg = r[1] - r[0];
+      fedges += deg;
+      int64_t k = deg <= kChunk ? 1 : (deg + kChunk - 1) / kChunk;
+      for (int64_t c = 0; c < k; ++c) q.push_back((c << 32) | v);
+    }
+    int32_t* dsrc = nullptr;
+    GBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dsrc), nb * sizeof(int32_t), s));
+    GBX_CUDA(cudaMemcpyAsync(dsrc, src.data(), nb * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    k_bfs64_seed<<<1, 1, 0, s>>>(dsrc, nb, W.seen.p, W.front.p, W.mlevel.p, W.mparent.p);
+    GBX_LAUNCHED();
+    int64_t* q0 = reinterpret_cast<int64_t*>(W.mqueue[0].p);
+    int64_t* q1 = reinterpret_cast<int64_t*>(W.mqueue[1].p);
+    GBX_CUDA(cudaMemcpyAsync(q0, q.data(), q.size() * 8, cudaMemcpyHostToDevice, s));
+    int hctl[12] = {0};
+    hctl[0] = static_cast<int>(q.size());
+    hctl[1] = static_cast<int>(uniq.size());
+    unsigned long long* edges = reinterpret_cast<unsigned long long*>(hctl + 8);
+    edges[0] = fedges;
+    edges[1] = 0;
+    GBX_CUDA(cudaMemcpyAsync(W.mctl.p, hctl, sizeof hctl, cudaMemcpyHostToDevice, s));
+    Bfs64Args a{};
+    a.rp = A.rp.p;
+    a.col = A.col.p;
+    a.trp = AT.rp.p;
+    a.tcol = AT.col.p;
+    a.n = n;
+    a.nnz = A.nnz;
+    a.lanes = nb == 64 ? ~0ull : ((1ull << nb) - 1);
+    a.seen = W.seen.p;
+    a.f0 = W.front.p;
+    a.f1 = W.next.p;
+    a.mlevel = W.mlevel.p;
+    a.mparent = W.mparent.p;
+    a.q0 = q0;
+    a.q1 = q1;
+    a.ctl = W.mctl.p;
+    a.edges = reinterpret_cast<unsigned long long*>(W.mctl.p + 8);
+    void* args[] = {&a};
+    if (n > 1) {
+      GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_bfs64), dim3(grid),
+                                           dim3(kBfsThreads), args, 0, s));
+    }
+    cudaFreeAsync(dsrc, s);
+    total_launches += 3;
+    W.ms_ns = nb;
+    if (parent || level) {
+      int64_t* tmp = nullptr;
+      GBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), std::max<int64_t>(n, 1) * nb * 8, s));
+      dim3 blk(32, 8);
+      if (parent) {
+        k_lanes_out<<<ceil_div(n, 32), blk, 0, s>>>(W.mparent.p, n, nb, INT_MAX, tmp);
+        GBX_LAUNCHED();
+        GBX_CUDA(cudaMemcpyAsync(parent + b0 * n, tmp, n * nb * 8, cudaMemcpyDeviceToHost, s));
+        total_launches++;
+      }
+      if (level) {
+        k_lanes_out<<<ceil_div(n, 32), blk, 0, s>>>(W.mlevel.p, n, nb, -1, tmp);
+        GBX_LAUNCHED();
+        GBX_CUDA(cudaMemcpyAsync(level + b0 * n, tmp, n * nb * 8, cudaMemcpyDeviceToHost, s));
+        total_launches++;
+      }
+      cudaFreeAsync(tmp, s);
+    }
+    GBX_CUDA(cudaMemcpyAsync(hctl, W.mctl.p, sizeof hctl, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+    g->stats.iterations = hctl[5];
+  }
+  g->stats.launches = total_launches;
+  g->stats.hot_launches = (ns + 63) / 64;
+}
+
+}  // namespace gbx

@@ -1,0 +1,180 @@
+// common.cuh -- shared internals of libgbx.so (B200 / sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gbx.h"
+
+namespace gbx {
+
+// Internal error: carries a gblite::ErrCode-compatible code (error.hpp:13-41).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Error(code, m); }
+
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+#define GBX_CUDA(x)                                                     \
+  do {                                                                  \
+    cudaError_t e_ = (x);                                               \
+    if (e_ != cudaSuccess) ::gbx::cuda_fail(e_, #x, __FILE__, __LINE__); \
+  } while (0)
+#define GBX_LAUNCHED() GBX_CUDA(cudaGetLastError())
+
+constexpr int kSMs = 148;  // B200; the runtime value is queried in device_sms()
+int device_sms();
+
+// Owning device array (cudaMalloc / cudaFree).  Persistent graph data and
+// per-plan workspaces; per-call temporaries use the stream-ordered pool.
+template <typename T>
+struct DevArray {
+  T* p = nullptr;
+  size_t n = 0;
+  DevArray() = default;
+  explicit DevArray(size_t count) { alloc(count); }
+  DevArray(const DevArray&) = delete;
+  DevArray& operator=(const DevArray&) = delete;
+  DevArray(DevArray&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevArray& operator=(DevArray&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevArray() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) {
+      cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+      if (e != cudaSuccess) {
+        p = nullptr;
+        n = 0;
+        (void)cudaGetLastError();
+        fail(GBX_OUT_OF_MEMORY, "cudaMalloc of " + std::to_string(count * sizeof(T)) +
+                                    " bytes failed: " + cudaGetErrorString(e));
+      }
+    }
+  }
+  void ensure(size_t count) { if (n < count) alloc(count); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// Device CSR: row_ptr int64[n+1], col int32[nnz] strictly ascending per row
+// (SparseMatrix invariant, containers.cpp:104-124), optional values in `domain`.
+struct Csr {
+  int64_t n = 0;
+  int64_t nnz = 0;
+  int domain = GBX_BOOL;
+  DevArray<int64_t> rp;
+  DevArray<int32_t> col;
+  DevArray<uint8_t> val;  // raw bytes, element type given by domain
+};
+
+size_t domain_size(int domain);
+
+struct PrPlan;
+struct TcPlan;
+struct SsspPlan;
+struct BfsWork;
+struct BcWork;
+struct CcWork;
+struct PrShard;
+
+}  // namespace gbx
+
+// The graph handle (graph.hpp:27-39 restated on the device).
+struct gbx_graph {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  int kind = GBX_DIRECTED;
+  gbx::Csr A;
+  // caches
+  bool has_at = false;
+  gbx::Csr at_own;  // directed: the transpose; undirected graphs alias A
+  bool has_rowdeg = false, has_coldeg = false;
+  gbx::DevArray<int32_t> rowdeg, coldeg;
+  int symmetric = GBX_UNKNOWN;
+  int64_t ndiag = -1;
+  // derived device layouts (plans), rebuilt after delete_properties
+  std::unique_ptr<gbx::PrPlan> pr;
+  std::unique_ptr<gbx::TcPlan> tc;
+  std::unique_ptr<gbx::SsspPlan> sssp;
+  std::unique_ptr<gbx::BfsWork> bfs;
+  std::unique_ptr<gbx::BcWork> bc;
+  std::unique_ptr<gbx::CcWork> cc;
+  std::unique_ptr<gbx::PrShard> prs;
+  gbx_stats stats{};
+
+  const gbx::Csr& AT() const { return kind == GBX_UNDIRECTED ? A : at_own; }
+  ~gbx_graph();
+};
+
+namespace gbx {
+
+// RAII device guard + handle lock for every ABI entry.
+struct Scope {
+  std::unique_lock<std::mutex> lock;
+  explicit Scope(gbx_graph* g);
+};
+
+// ---- graph-level primitives (graph.cu) ------------------------------------
+void build_from_host(gbx_graph* g, int64_t n, const int64_t* rp, const int64_t* col64,
+                     const int32_t* col32, const void* vals, int domain, int kind);
+void compute_transpose(cudaStream_t s, const Csr& A, Csr& T);
+void compute_degrees(cudaStream_t s, const Csr& A, DevArray<int32_t>& out, bool by_row);
+void require_at(const gbx_graph* g, const char* who);
+void require_rowdeg(const gbx_graph* g, const char* who);
+void reset_plans(gbx_graph* g);
+// stable ascending/descending permutation of ids by key (cub radix, LSD = stable)
+void sort_ids_by_key(cudaStream_t s, const int32_t* key, int64_t n, bool ascending,
+                     DevArray<int32_t>& perm);
+// row ids per nonzero (max-scan over row starts)
+void expand_rows(cudaStream_t s, const Csr& A, DevArray<int32_t>& rowid);
+void generate_rmat(gbx_graph* g, int scale, int ef, double a, double b, double c,
+                   uint64_t seed, int scramble, int kind);
+void generate_er(gbx_graph* g, int logn, int degree, uint64_t seed, int weighted);
+int64_t count_ndiag(cudaStream_t s, const Csr& A);
+bool csr_equal(cudaStream_t s, const Csr& X, const Csr& Y);
+void sync(gbx_graph* g);
+
+// ---- algorithms ----------------------------------------------------------------
+void pagerank_run(gbx_graph* g, double damping, double tol, int itermax, double* rank,
+                  int* iters);
+void pagerank_prepare(gbx_graph* g);
+void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor,
+             bool use_at, int64_t* parent, int64_t* level);
+void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* parent,
+                   int64_t* level);
+void bfs_prepare(gbx_graph* g);
+uint64_t tc_run(gbx_graph* g, int64_t row_begin, int64_t row_end);
+void tc_prepare(gbx_graph* g);
+void tc_partition(gbx_graph* g, int parts, int64_t* bounds);
+void sssp_run(gbx_graph* g, uint64_t source, double delta, double* dist);
+double sssp_default_delta(gbx_graph* g);
+void sssp_prepare(gbx_graph* g);
+void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrality);
+void cc_run(gbx_graph* g, int64_t* label, int* iters);
+void pr_shard_prepare(gbx_graph* g, int64_t rb, int64_t re);
+void pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, double* l1,
+                   double damping);
+void partition_rows(const gbx_graph* g, int parts, bool transposed, int64_t* bounds);
+void result_device(const gbx_graph* g, const std::string& which, void** ptr, int64_t* count);
+
+// ---- device helpers ---------------------------------------------------------------
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace gbx

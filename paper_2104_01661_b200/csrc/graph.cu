@@ -1,0 +1,584 @@
+// graph.cu -- the device CSR store and the Graph-object caches.
+//
+// Restates gblite's graph layer (graph.cpp:16-110, containers.cpp:104-169,
+// core.cpp:237-256, util.cpp:35-44) for HBM: CSR with int64 row_ptr and int32
+// columns, transpose / dedup / symmetrise by CUB radix sort instead of the
+// reference's counting sort and std::stable_sort, degrees by one pass over
+// row_ptr (rows) or one atomic histogram (columns).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace gbx {
+
+void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  (void)cudaGetLastError();
+  char buf[256];
+  std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d", cudaGetErrorName(e), what,
+                file, line);
+  fail(e == cudaErrorMemoryAllocation ? GBX_OUT_OF_MEMORY : GBX_CUDA_ERROR, buf);
+}
+
+int device_sms() {
+  int dev = 0, sms = 0;
+  GBX_CUDA(cudaGetDevice(&dev));
+  GBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  return sms;
+}
+
+size_t domain_size(int d) {
+  switch (d) {
+    case GBX_BOOL: return 1;
+    case GBX_INT32: return 4;
+    case GBX_INT64:
+    case GBX_UINT64:
+    case GBX_FP64: return 8;
+  }
+  fail(GBX_DOMAIN_MISMATCH, "unknown value domain " + std::to_string(d));
+}
+
+Scope::Scope(gbx_graph* g) : lock(g->mu) { GBX_CUDA(cudaSetDevice(g->device)); }
+
+void sync(gbx_graph* g) { GBX_CUDA(cudaStreamSynchronize(g->stream)); }
+
+void require_at(const gbx_graph* g, const char* who) {
+  if (!g->has_at) fail(GBX_MISSING_PROPERTY, std::string(who) + " needs G.AT");
+}
+void require_rowdeg(const gbx_graph* g, const char* who) {
+  if (!g->has_rowdeg) fail(GBX_MISSING_PROPERTY, std::string(who) + " needs G.row_degree");
+}
+
+// Stream-ordered temporary (freed on the stream when it goes out of scope).
+template <typename T>
+struct Tmp {
+  T* p = nullptr;
+  cudaStream_t s;
+  Tmp(size_t n, cudaStream_t st) : s(st) {
+    if (n) {
+      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), s);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        fail(GBX_OUT_OF_MEMORY, "cudaMallocAsync of " + std::to_string(n * sizeof(T)) +
+                                    " bytes failed");
+      }
+    }
+  }
+  ~Tmp() { if (p) cudaFreeAsync(p, s); }
+  Tmp(const Tmp&) = delete;
+  Tmp& operator=(const Tmp&) = delete;
+};
+
+static int bits_for(int64_t n) {
+  int b = 1;
+  while ((int64_t(1) << b) < n) ++b;
+  return b;
+}
+
+// ---- validation (containers.cpp:104-124) -------------------------------------
+
+__global__ void k_validate_rows(const int64_t* rp, int64_t n, int64_t nnz, uint8_t* head,
+                                int* bad) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  int64_t b = rp[i], e = rp[i + 1];
+  if (b > e || b < 0 || e > nnz) { atomicOr(bad, 1); return; }
+  if (b < e) head[b] = 1;
+}
+
+__global__ void k_convert_cols(const int64_t* c64, int32_t* c32, int64_t nnz, int64_t n,
+                               int* bad) {
+  int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p >= nnz) return;
+  int64_t c = c64[p];
+  if (c < 0 || c >= n) { atomicOr(bad, 2); c = 0; }
+  c32[p] = static_cast<int32_t>(c);
+}
+
+__global__ void k_validate_cols(const int32_t* col, const uint8_t* head, int64_t nnz,
+                                int64_t n, int* bad) {
+  int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p >= nnz) return;
+  int32_t c = col[p];
+  if (c < 0 || c >= n) atomicOr(bad, 2);
+  if (p > 0 && !head[p] && col[p - 1] >= c) atomicOr(bad, 4);
+}
+
+void build_from_host(gbx_graph* g, int64_t n, const int64_t* rp, const int64_t* col64,
+                     const int32_t* col32, const void* vals, int domain, int kind) {
+  if (n < 0) fail(GBX_INVALID_MATRIX, "graph_new: negative dimension");
+  if (n >= (int64_t(1) << 31) - 1)
+    fail(GBX_UNSUPPORTED, "graph_new: n >= 2^31 is not supported by the int32 column layout");
+  if (kind != GBX_DIRECTED && kind != GBX_UNDIRECTED)
+    fail(GBX_INVALID_VALUE, "graph_new: unknown kind");
+  if (vals) (void)domain_size(domain);
+  else domain = GBX_BOOL;
+  if (!rp) fail(GBX_NULL_ARGUMENT, "graph_new: row_ptr is NULL");
+  if (rp[0] != 0) fail(GBX_INVALID_MATRIX, "graph_new: row_ptr[0] is not 0");
+  int64_t nnz = rp[n];
+  if (nnz < 0) fail(GBX_INVALID_MATRIX, "graph_new: row_ptr[nrows] is negative");
+  if (nnz > 0 && !col64 && !col32) fail(GBX_NULL_ARGUMENT, "graph_new: col_idx is NULL");
+  cudaStream_t s = g->stream;
+  Csr& A = g->A;
+  A.n = n;
+  A.nnz = nnz;
+  A.domain = domain;
+  A.rp.alloc(n + 1);
+  A.col.alloc(std::max<int64_t>(nnz, 1));
+  GBX_CUDA(cudaMemcpyAsync(A.rp.p, rp, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  Tmp<int> bad(1, s);
+  GBX_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+  if (nnz > 0) {
+    if (col64) {
+      Tmp<int64_t> c64(nnz, s);
+      GBX_CUDA(cudaMemcpyAsync(c64.p, col64, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      k_convert_cols<<<ceil_div(nnz, 256), 256, 0, s>>>(c64.p, A.col.p, nnz, n, bad.p);
+      GBX_LAUNCHED();
+    } else {
+      GBX_CUDA(cudaMemcpyAsync(A.col.p, col32, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    }
+  }
+  if (vals && nnz > 0) {
+    size_t es = domain_size(domain);
+    A.val.alloc(nnz * es);
+    GBX_CUDA(cudaMemcpyAsync(A.val.p, vals, nnz * es, cudaMemcpyHostToDevice, s));
+  }
+  if (n > 0) {
+    Tmp<uint8_t> head(std::max<int64_t>(nnz, 1), s);
+    GBX_CUDA(cudaMemsetAsync(head.p, 0, std::max<int64_t>(nnz, 1), s));
+    k_validate_rows<<<ceil_div(n, 256), 256, 0, s>>>(A.rp.p, n, nnz, head.p, bad.p);
+    GBX_LAUNCHED();
+    if (nnz > 0) {
+      k_validate_cols<<<ceil_div(nnz, 256), 256, 0, s>>>(A.col.p, head.p, nnz, n, bad.p);
+      GBX_LAUNCHED();
+    }
+  }
+  int hbad = 0;
+  GBX_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  if (hbad & 1) fail(GBX_INVALID_MATRIX, "graph_new: row_ptr not nondecreasing");
+  if (hbad & 2) fail(GBX_INVALID_MATRIX, "graph_new: column index out of range");
+  if (hbad & 4) fail(GBX_INVALID_MATRIX, "graph_new: row columns not strictly increasing");
+  g->kind = kind;
+}
+
+// ---- row expansion, degrees, transpose ---------------------------------------
+
+__global__ void k_mark_row_starts(const int64_t* rp, int64_t n, int32_t* rowid) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  if (rp[i] < rp[i + 1]) rowid[rp[i]] = static_cast<int32_t>(i);
+}
+
+struct MaxOp {
+  __device__ __forceinline__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
+};
+
+void expand_rows(cudaStream_t s, const Csr& A, DevArray<int32_t>& rowid) {
+  rowid.alloc(std::max<int64_t>(A.nnz, 1));
+  if (A.nnz == 0) return;
+  GBX_CUDA(cudaMemsetAsync(rowid.p, 0, A.nnz * sizeof(int32_t), s));
+  k_mark_row_starts<<<ceil_div(A.n, 256), 256, 0, s>>>(A.rp.p, A.n, rowid.p);
+  GBX_LAUNCHED();
+  size_t tb = 0;
+  GBX_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, rowid.p, rowid.p, MaxOp(), A.nnz, s));
+  Tmp<uint8_t> t(tb, s);
+  GBX_CUDA(cub::DeviceScan::InclusiveScan(t.p, tb, rowid.p, rowid.p, MaxOp(), A.nnz, s));
+}
+
+__global__ void k_row_degree(const int64_t* rp, int64_t n, int32_t* deg) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) deg[i] = static_cast<int32_t>(rp[i + 1] - rp[i]);
+}
+
+__global__ void k_col_count(const int32_t* col, int64_t nnz, int32_t* cnt) {
+  int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p < nnz) atomicAdd(&cnt[col[p]], 1);
+}
+
+void compute_degrees(cudaStream_t s, const Csr& A, DevArray<int32_t>& out, bool by_row) {
+  out.alloc(std::max<int64_t>(A.n, 1));
+  if (A.n == 0) return;
+  if (by_row) {
+    k_row_degree<<<ceil_div(A.n, 256), 256, 0, s>>>(A.rp.p, A.n, out.p);
+  } else {
+    GBX_CUDA(cudaMemsetAsync(out.p, 0, A.n * sizeof(int32_t), s));
+    if (A.nnz) k_col_count<<<ceil_div(A.nnz, 256), 256, 0, s>>>(A.col.p, A.nnz, out.p);
+  }
+  GBX_LAUNCHED();
+}
+
+// row_ptr from a count array (exclusive scan into int64)
+__global__ void k_widen(const int32_t* in, int64_t* out, int64_t n) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
+static void counts_to_rowptr(cudaStream_t s, const int32_t* cnt, int64_t n, int64_t* rp) {
+  GBX_CUDA(cudaMemsetAsync(rp, 0, sizeof(int64_t), s));
+  if (n == 0) return;
+  k_widen<<<ceil_div(n, 256), 256, 0, s>>>(cnt, rp + 1, n);
+  GBX_LAUNCHED();
+  size_t tb = 0;
+  GBX_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, rp + 1, rp + 1, n, s));
+  Tmp<uint8_t> t(tb, s);
+  GBX_CUDA(cub::DeviceScan::InclusiveSum(t.p, tb, rp + 1, rp + 1, n, s));
+}
+
+__global__ void k_pack_transpose_keys(const int32_t* col, const int32_t* rowid, int64_t nnz,
+                                      int bits, uint64_t* keys, int64_t* idx) {
+  int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p >= nnz) return;
+  keys[p] = (static_cast<uint64_t>(col[p]) << bits) | static_cast<uint64_t>(rowid[p]);
+  if (idx) idx[p] = p;
+}
+
+template <int ES>
+__global__ void k_unpack_transpose(const uint64_t* keys, const int64_t* idx, int64_t nnz,
+                                   int bits, int32_t* tcol, const uint8_t* val, uint8_t* tval) {
+  int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p >= nnz) return;
+  uint64_t mask = (uint64_t(1) << bits) - 1;
+  tcol[p] = static_cast<int32_t>(keys[p] & mask);
+  if (ES > 0) {
+    const uint8_t* src = val + idx[p] * ES;
+    uint8_t* dst = tval + p * ES;
+#pragma unroll
+    for (int b = 0; b < ES; ++b) dst[b] = src[b];
+  }
+}
+
+// T = transpose(A): plain_transpose (core.cpp:237-256) as a radix sort of the
+// (col, row) keys -- rows of T come out strictly ascending.
+void compute_transpose(cudaStream_t s, const Csr& A, Csr& T) {
+  T.n = A.n;
+  T.nnz = A.nnz;
+  T.domain = A.domain;
+  T.rp.alloc(A.n + 1);
+  T.col.alloc(std::max<int64_t>(A.nnz, 1));
+  {
+    Tmp<int32_t> cnt(std::max<int64_t>(A.n, 1), s);
+    GBX_CUDA(cudaMemsetAsync(cnt.p, 0, std::max<int64_t>(A.n, 1) * sizeof(int32_t), s));
+    if (A.nnz) {
+      k_col_count<<<ceil_div(A.nnz, 256), 256, 0, s>>>(A.col.p, A.nnz, cnt.p);
+      GBX_LAUNCHED();
+    }
+    counts_to_rowptr(s, cnt.p, A.n, T.rp.p);
+  }
+  if (A.nnz == 0) return;
+  DevArray<int32_t> rowid;
+  expand_rows(s, A, rowid);
+  int bits = bits_for(A.n);
+  bool has_val = A.val.p != nullptr;
+  size_t es = has_val ? domain_size(A.domain) : 0;
+  Tmp<uint64_t> k0(A.nnz, s), k1(A.nnz, s);
+  Tmp<int64_t> i0(has_val ? A.nnz : 0, s), i1(has_val ? A.nnz : 0, s);
+  k_pack_transpose_keys<<<ceil_div(A.nnz, 256), 256, 0, s>>>(A.col.p, rowid.p, A.nnz, bits,
+                                                              k0.p, has_val ? i0.p : nullptr);
+  GBX_LAUNCHED();
+  rowid.release();
+  size_t tb = 0;
+  cub::DoubleBuffer<uint64_t> kb(k0.p, k1.p);
+  cub::DoubleBuffer<int64_t> ib(i0.p, i1.p);
+  if (has_val) {
+    GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, ib, A.nnz, 0, 2 * bits, s));
+  } else {
+    GBX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, A.nnz, 0, 2 * bits, s));
+  }
+  {
+    Tmp<uint8_t> t(tb, s);
+    if (has_val)
+      GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kb, ib, A.nnz, 0, 2 * bits, s));
+    else
+      GBX_CUDA(cub::DeviceRadixSort::SortKeys(t.p, tb, kb, A.nnz, 0, 2 * bits, s));
+  }
+  if (has_val) T.val.alloc(A.nnz * es);
+  int g = ceil_div(A.nnz, 256);
+  switch (es) {
+    case 0: k_unpack_transpose<0><<<g, 256, 0, s>>>(kb.Current(), nullptr, A.nnz, bits, T.col.p, nullptr, nullptr); break;
+    case 1: k_unpack_transpose<1><<<g, 256, 0, s>>>(kb.Current(), ib.Current(), A.nnz, bits, T.col.p, A.val.p, T.val.p); break;
+    case 4: k_unpack_transpose<4><<<g, 256, 0, s>>>(kb.Current(), ib.Current(), A.nnz, bits, T.col.p, A.val.p, T.val.p); break;
+    default: k_unpack_transpose<8><<<g, 256, 0, s>>>(kb.Current(), ib.Current(), A.nnz, bits, T.col.p, A.val.p, T.val.p); break;
+  }
+  GBX_LAUNCHED();
+}
+
+// ---- ndiag / equality ----------------------------------------------------------------
+
+__global__ void k_ndiag(const int64_t* rp, const int32_t* col, int64_t n,
+                        unsigned long long* cnt) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  int hit = 0;
+  if (i < n) {
+    int64_t lo = rp[i], hi = rp[i + 1];
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (col[mid] < i) lo = mid + 1; else hi = mid;
+    }
+    hit = (lo < rp[i + 1] && col[lo] == i) ? 1 : 0;
+  }
+  unsigned b = __ballot_sync(0xffffffffu, hit);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(cnt, static_cast<unsigned long long>(__popc(b)));
+}
+
+int64_t count_ndiag(cudaStream_t s, const Csr& A) {
+  if (A.n == 0) return 0;
+  Tmp<unsigned long long> c(1, s);
+  GBX_CUDA(cudaMemsetAsync(c.p, 0, sizeof(unsigned long long), s));
+  k_ndiag<<<ceil_div(A.n, 256), 256, 0, s>>>(A.rp.p, A.col.p, A.n, c.p);
+  GBX_LAUNCHED();
+  unsigned long long h = 0;
+  GBX_CUDA(cudaMemcpyAsync(&h, c.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  return static_cast<int64_t>(h);
+}
+
+template <typename T>
+__global__ void k_neq(const T* a, const T* b, int64_t n, int* flag) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n && a[i] != b[i]) *flag = 1;
+}
+
+bool csr_equal(cudaStream_t s, const Csr& X, const Csr& Y) {
+  if (X.n != Y.n || X.nnz != Y.nnz) return false;
+  Tmp<int> f(1, s);
+  GBX_CUDA(cudaMemsetAsync(f.p, 0, sizeof(int), s));
+  k_neq<int64_t><<<ceil_div(X.n + 1, 256), 256, 0, s>>>(X.rp.p, Y.rp.p, X.n + 1, f.p);
+  if (X.nnz) k_neq<int32_t><<<ceil_div(X.nnz, 256), 256, 0, s>>>(X.col.p, Y.col.p, X.nnz, f.p);
+  GBX_LAUNCHED();
+  int h = 0;
+  GBX_CUDA(cudaMemcpyAsync(&h, f.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  return h == 0;
+}
+
+// ---- stable sort of ids by a key (util.cpp:35-44) -----------------------------------
+
+__global__ void k_iota(int32_t* p, int64_t n) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) p[i] = static_cast<int32_t>(i);
+}
+__global__ void k_flip_keys(const int32_t* key, uint32_t* out, int64_t n, bool asc) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = asc ? static_cast<uint32_t>(key[i]) : ~static_cast<uint32_t>(key[i]);
+}
+
+void sort_ids_by_key(cudaStream_t s, const int32_t* key, int64_t n, bool ascending,
+                     DevArray<int32_t>& perm) {
+  perm.alloc(std::max<int64_t>(n, 1));
+  if (n == 0) return;
+  Tmp<uint32_t> k0(n, s), k1(n, s);
+  Tmp<int32_t> v0(n, s);
+  k_flip_keys<<<ceil_div(n, 256), 256, 0, s>>>(key, k0.p, n, ascending);
+  k_iota<<<ceil_div(n, 256), 256, 0, s>>>(v0.p, n);
+  GBX_LAUNCHED();
+  size_t tb = 0;
+  GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.p, k1.p, v0.p, perm.p, n, 0, 32, s));
+  Tmp<uint8_t> t(tb, s);
+  GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, k0.p, k1.p, v0.p, perm.p, n, 0, 32, s));
+}
+
+// ---- seeded generators (bit-identical to oracle/oracle.c) -------------------------
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+__host__ __device__ __forceinline__ uint64_t gen_stream(uint64_t seed, uint64_t stream) {
+  return mix64(seed ^ mix64(stream + 0x632BE59BD9B4E019ull));
+}
+__host__ __device__ __forceinline__ uint64_t gen_draw(uint64_t s, uint64_t i) {
+  return mix64(s + (i + 1) * 0x9E3779B97F4A7C15ull);
+}
+__device__ __forceinline__ uint32_t gen_scramble(uint32_t x, int scale, uint64_t add) {
+  uint64_t mask = (scale >= 32) ? 0xFFFFFFFFull : ((1ull << scale) - 1);
+  int sh = scale / 2 + 1;
+  uint64_t y = x;
+  y = (y * 0x9E3779B97F4A7C15ull) & mask;
+  y ^= y >> sh;
+  y = (y + add) & mask;
+  y = (y * 0xBF58476D1CE4E5B9ull) & mask;
+  y ^= y >> sh;
+  return static_cast<uint32_t>(y);
+}
+
+
+__global__ void k_rmat(int scale, int64_t m, uint32_t ta, uint32_t tab, uint32_t tabc,
+                       uint64_t s, int scramble, uint64_t add, int sym, uint64_t* keys) {
+  const uint64_t kDropKey = uint64_t(1) << (2 * scale);
+  int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= m) return;
+  int per = (scale + 1) / 2;
+  uint32_t uu = 0, vv = 0;
+  uint64_t r = 0;
+  for (int l = 0; l < scale; ++l) {
+    if ((l & 1) == 0) r = gen_draw(s, static_cast<uint64_t>(e) * per + (l >> 1));
+    uint32_t x = (l & 1) ? static_cast<uint32_t>(r >> 32) : static_cast<uint32_t>(r);
+    uint32_t ub, vb;
+    if (x < ta) { ub = 0; vb = 0; }
+    else if (x < tab) { ub = 0; vb = 1; }
+    else if (x < tabc) { ub = 1; vb = 0; }
+    else { ub = 1; vb = 1; }
+    uu = (uu << 1) | ub;
+    vv = (vv << 1) | vb;
+  }
+  if (scramble) {
+    uu = gen_scramble(uu, scale, add);
+    vv = gen_scramble(vv, scale, add);
+  }
+  bool loop = uu == vv;
+  if (sym) {
+    keys[2 * e] = loop ? kDropKey : ((uint64_t(uu) << scale) | vv);
+    keys[2 * e + 1] = loop ? kDropKey : ((uint64_t(vv) << scale) | uu);
+  } else {
+    keys[e] = loop ? kDropKey : ((uint64_t(uu) << scale) | vv);
+  }
+}
+
+__global__ void k_er(int logn, int64_t m, uint64_t s, uint64_t* keys, int32_t* w) {
+  const uint64_t kDropKey = uint64_t(1) << (2 * logn);
+  int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= m) return;
+  uint64_t r1 = gen_draw(s, 2 * static_cast<uint64_t>(e));
+  uint64_t r2 = gen_draw(s, 2 * static_cast<uint64_t>(e) + 1);
+  uint32_t u = static_cast<uint32_t>(r1 >> (64 - logn));
+  uint32_t v = static_cast<uint32_t>(r2 >> (64 - logn));
+  keys[e] = (u == v) ? kDropKey : ((uint64_t(u) << logn) | v);
+  if (w) w[e] = 1 + static_cast<int32_t>(((r1 & 0xFFFFFFFFull) * 255ull) >> 32);
+}
+
+// keep the first key of every run (and the minimum weight of the run)
+__global__ void k_run_heads(const uint64_t* keys, const int32_t* w, int64_t m,
+                            uint64_t kDropKey, uint8_t* flag, int32_t* wmin) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= m) return;
+  uint64_t k = keys[i];
+  bool head = k != kDropKey && (i == 0 || keys[i - 1] != k);
+  flag[i] = head ? 1 : 0;
+  if (head && w) {
+    int32_t best = w[i];
+    for (int64_t j = i + 1; j < m && keys[j] == k; ++j) best = min(best, w[j]);
+    wmin[i] = best;
+  }
+}
+
+__global__ void k_split_keys(const uint64_t* keys, int64_t nnz, int bits, int32_t* col,
+                             int32_t* rowcnt) {
+  int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p >= nnz) return;
+  uint64_t k = keys[p];
+  col[p] = static_cast<int32_t>(k & ((uint64_t(1) << bits) - 1));
+  atomicAdd(&rowcnt[k >> bits], 1);
+}
+
+// sorted (u<<bits|v) keys (+ weights) -> CSR in g->A
+static void keys_to_graph(gbx_graph* g, int64_t n, int bits, uint64_t* keys, int32_t* w,
+                          int64_t m, int kind) {
+  cudaStream_t s = g->stream;
+  // sort
+  size_t tb = 0;
+  Tmp<uint64_t> kalt(m, s);
+  Tmp<int32_t> walt(w ? m : 0, s);
+  cub::DoubleBuffer<uint64_t> kb(keys, kalt.p);
+  cub::DoubleBuffer<int32_t> wb(w, walt.p);
+  // drop keys (self-loops) are 1 << 2*bits: they sort after every edge
+  const int end_bit = 2 * bits + 1;
+  const uint64_t drop = uint64_t(1) << (2 * bits);
+  if (w) GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, wb, m, 0, end_bit, s));
+  else GBX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, m, 0, end_bit, s));
+  {
+    Tmp<uint8_t> t(tb, s);
+    if (w) GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kb, wb, m, 0, end_bit, s));
+    else GBX_CUDA(cub::DeviceRadixSort::SortKeys(t.p, tb, kb, m, 0, end_bit, s));
+  }
+  Tmp<uint8_t> flag(m, s);
+  Tmp<int32_t> wmin(w ? m : 0, s);
+  k_run_heads<<<ceil_div(m, 256), 256, 0, s>>>(kb.Current(), w ? wb.Current() : nullptr, m,
+                                                drop, flag.p, wmin.p);
+  GBX_LAUNCHED();
+  Tmp<uint64_t> uk(m, s);
+  Tmp<int64_t> nsel(1, s);
+  tb = 0;
+  GBX_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, kb.Current(), flag.p, uk.p, nsel.p, m, s));
+  int64_t nnz = 0;
+  {
+    Tmp<uint8_t> t(tb, s);
+    GBX_CUDA(cub::DeviceSelect::Flagged(t.p, tb, kb.Current(), flag.p, uk.p, nsel.p, m, s));
+    GBX_CUDA(cudaMemcpyAsync(&nnz, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+  }
+  Csr& A = g->A;
+  A.n = n;
+  A.nnz = nnz;
+  A.domain = w ? GBX_INT32 : GBX_BOOL;
+  A.rp.alloc(n + 1);
+  A.col.alloc(std::max<int64_t>(nnz, 1));
+  {
+    Tmp<int32_t> cnt(n, s);
+    GBX_CUDA(cudaMemsetAsync(cnt.p, 0, n * sizeof(int32_t), s));
+    if (nnz) {
+      k_split_keys<<<ceil_div(nnz, 256), 256, 0, s>>>(uk.p, nnz, bits, A.col.p, cnt.p);
+      GBX_LAUNCHED();
+    }
+    counts_to_rowptr(s, cnt.p, n, A.rp.p);
+  }
+  if (w) {
+    A.val.alloc(std::max<int64_t>(nnz, 1) * sizeof(int32_t));
+    tb = 0;
+    GBX_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, wmin.p, flag.p,
+                                        reinterpret_cast<int32_t*>(A.val.p), nsel.p, m, s));
+    Tmp<uint8_t> t(tb, s);
+    GBX_CUDA(cub::DeviceSelect::Flagged(t.p, tb, wmin.p, flag.p,
+                                        reinterpret_cast<int32_t*>(A.val.p), nsel.p, m, s));
+  }
+  GBX_CUDA(cudaStreamSynchronize(s));
+  g->kind = kind;
+}
+
+void generate_rmat(gbx_graph* g, int scale, int ef, double a, double b, double c,
+                   uint64_t seed, int scramble, int kind) {
+  if (scale < 1 || scale > 30) fail(GBX_INVALID_VALUE, "rmat: scale must be in [1,30]");
+  if (ef < 1) fail(GBX_INVALID_VALUE, "rmat: edge factor must be >= 1");
+  if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0))
+    fail(GBX_INVALID_VALUE, "rmat: need a,b,c >= 0 and a+b+c <= 1");
+  cudaStream_t s = g->stream;
+  int64_t n = int64_t(1) << scale;
+  int64_t m = int64_t(ef) << scale;
+  bool sym = kind == GBX_UNDIRECTED;
+  int64_t mk = sym ? 2 * m : m;
+  uint32_t ta = static_cast<uint32_t>(a * 4294967296.0);
+  uint32_t tab = static_cast<uint32_t>((a + b) * 4294967296.0);
+  double abc = a + b + c;
+  uint32_t tabc = abc >= 1.0 ? 0xFFFFFFFFu : static_cast<uint32_t>(abc * 4294967296.0);
+  uint64_t st = gen_stream(seed, 0);
+  uint64_t mask = (1ull << scale) - 1;
+  uint64_t add = gen_stream(seed, 1) & mask;
+  Tmp<uint64_t> keys(mk, s);
+  k_rmat<<<ceil_div(m, 256), 256, 0, s>>>(scale, m, ta, tab, tabc, st, scramble, add,
+                                           sym ? 1 : 0, keys.p);
+  GBX_LAUNCHED();
+  keys_to_graph(g, n, scale, keys.p, nullptr, mk, kind);
+}
+
+void generate_er(gbx_graph* g, int logn, int degree, uint64_t seed, int weighted) {
+  if (logn < 1 || logn > 30) fail(GBX_INVALID_VALUE, "er: logn must be in [1,30]");
+  if (degree < 1) fail(GBX_INVALID_VALUE, "er: degree must be >= 1");
+  cudaStream_t s = g->stream;
+  int64_t n = int64_t(1) << logn;
+  int64_t m = int64_t(degree) << logn;
+  Tmp<uint64_t> keys(m, s);
+  Tmp<int32_t> w(weighted ? m : 0, s);
+  k_er<<<ceil_div(m, 256), 256, 0, s>>>(logn, m, gen_stream(seed, 2), keys.p,
+                                         weighted ? w.p : nullptr);
+  GBX_LAUNCHED();
+  keys_to_graph(g, n, logn, keys.p, weighted ? w.p : nullptr, m, GBX_DIRECTED);
+}
+
+}  // namespace gbx

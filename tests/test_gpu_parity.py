@@ -1,0 +1,223 @@
+"""Parity of the CUDA library (through the C ABI) against the reference's own
+outputs (tests/golden) and the oracle restatement.  Needs a B200."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2104_01661_b200 as P
+from paper_2104_01661_b200 import algo
+from tests.golden_util import Golden, case_ids
+from tests.gpu_util import graph_of, rel_l1
+
+pytestmark = pytest.mark.gpu
+G = Golden()
+CASES = {c.name: c for c in G.cases}
+
+
+# ---------------------------------------------------------------- BFS
+@pytest.mark.parametrize("name", case_ids("bfs"))
+def test_bfs_golden(name):
+    c = CASES[name]
+    g = graph_of(c)
+    src = c.params["src"]
+    r = algo.bfs_push(g, src, want_level=True)
+    assert np.array_equal(r.parent, c.out["parent_pushonly"])
+    assert np.array_equal(r.level, c.out["level_pushonly"])
+    P.property_at(g)
+    for d, tag in ((algo.Direction.Auto, "auto"), (algo.Direction.ForcePush, "push"),
+                   (algo.Direction.ForcePull, "pull")):
+        r = algo.bfs_direction_optimizing(g, src, algo.BfsConfig(d, 16, True))
+        assert np.array_equal(r.parent, c.out[f"parent_{tag}"]), tag
+        assert np.array_equal(r.level, c.out[f"level_{tag}"]), tag
+
+
+@pytest.mark.parametrize("name", case_ids("bfs"))
+def test_bfs_batch_golden(name):
+    c = CASES[name]
+    g = graph_of(c)
+    P.property_at(g)
+    src = c.params["src"]
+    sources = [src] * 3 + list(range(min(c.n, 5)))
+    parent, level = algo.bfs_batch(g, sources)
+    for b, s in enumerate(sources):
+        wp, wl = O.bfs(c.n, c.rp, c.col, s)
+        assert np.array_equal(parent[b], wp) and np.array_equal(level[b], wl), b
+
+
+def test_bfs_errors():
+    c = CASES["bfs_path3"]
+    g = graph_of(c)
+    with pytest.raises(P.Error) as e:
+        algo.bfs_direction_optimizing(g, 0)
+    assert e.value.code == P.ErrCode.MissingProperty
+    assert not g.has_AT  # no silent computation (test_bfs.cpp:53-64)
+    with pytest.raises(P.Error) as e:
+        algo.bfs_push(g, 3)
+    assert e.value.code == P.ErrCode.SourceOutOfRange
+    r = algo.basic.bfs_direction_optimizing(g, 0, algo.BfsConfig(want_level=True))
+    assert g.has_AT and r.level.tolist() == [0, 1, 2]
+
+
+@pytest.mark.parametrize("scale,seed", [(14, 1), (16, 2)])
+def test_bfs_rmat_vs_oracle(scale, seed):
+    g = P.generate_rmat(scale, 16, seed=seed, kind=P.Kind.UndirectedAdjacency)
+    P.property_at(g)
+    rp, col, _ = g.export()
+    n = len(rp) - 1
+    P.property_rowdegree(g)
+    srcs = P.pick_sources(g.row_degree(), 8, seed)
+    for s in srcs:
+        wp, wl = O.bfs(n, rp, col, s)
+        for d in (algo.Direction.Auto, algo.Direction.ForcePush, algo.Direction.ForcePull):
+            r = algo.bfs_direction_optimizing(g, int(s), algo.BfsConfig(d, 16, True))
+            assert np.array_equal(r.level, wl) and np.array_equal(r.parent, wp)
+    parent, level = algo.bfs_batch(g, srcs)
+    for b, s in enumerate(srcs):
+        wp, wl = O.bfs(n, rp, col, s)
+        assert np.array_equal(parent[b], wp) and np.array_equal(level[b], wl)
+
+
+def test_bfs_batch_64_sources_config1():
+    """BASELINE config 1 shape: R-MAT scale 16 undirected, 64 seeded sources."""
+    g = P.generate_rmat(16, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
+    P.property_at(g)
+    P.property_rowdegree(g)
+    rp, col, _ = g.export()
+    n = len(rp) - 1
+    srcs = P.pick_sources(g.row_degree(), 64, 1)
+    parent, level = algo.bfs_batch(g, srcs)
+    for b in range(0, 64, 7):
+        wp, wl = O.bfs(n, rp, col, srcs[b])
+        assert np.array_equal(parent[b], wp) and np.array_equal(level[b], wl)
+
+
+# ---------------------------------------------------------------- PageRank
+@pytest.mark.parametrize("name", case_ids("pagerank"))
+def test_pagerank_golden(name):
+    c = CASES[name]
+    g = graph_of(c)
+    P.property_at(g)
+    P.property_rowdegree(g)
+    prm = c.params
+    r = algo.pagerank_gap(g, prm["damping"], prm["tol"], prm["itermax"])
+    assert r.iterations == int(c.out["iters"])
+    want = c.out["rank"]
+    assert rel_l1(r.rank, want) <= 1e-4
+    assert np.max(np.abs(r.rank - want)) <= 1e-6
+
+
+def test_pagerank_fixed_points():
+    # test_pr.cpp:24-38: 2- and 3-cycles settle at the uniform fixpoint
+    for name, v in (("pr_cycle2", 0.5), ("pr_cycle3", 1.0 / 3)):
+        g = graph_of(CASES[name])
+        r = algo.basic.pagerank_gap(g, 0.85, 1e-8, 100)
+        assert np.all(np.abs(r.rank - v) <= 1e-7)
+
+
+def test_pagerank_errors_and_cap():
+    g = graph_of(CASES["pr_cycle3"])
+    with pytest.raises(P.Error) as e:
+        algo.pagerank_gap(g)
+    assert e.value.code == P.ErrCode.MissingProperty
+    P.property_at(g)
+    with pytest.raises(P.Error) as e:
+        algo.pagerank_gap(g)
+    assert e.value.code == P.ErrCode.MissingProperty
+    P.property_rowdegree(g)
+    for bad in (0.0, -0.5):
+        with pytest.raises(P.Error) as e:
+            algo.pagerank_gap(g, bad)
+        assert e.value.code == P.ErrCode.NonPositiveDamping
+    assert algo.pagerank_gap(g, 0.85, 0.0, 7).iterations == 7
+
+
+@pytest.mark.parametrize("scale", [16, 18])
+def test_pagerank_rmat_vs_oracle(scale):
+    g = P.generate_rmat(scale, 16, seed=5, kind=P.Kind.DirectedAdjacency)
+    P.property_at(g)
+    P.property_rowdegree(g)
+    r = algo.pagerank_gap(g)
+    rp, col, _ = g.export()
+    n = len(rp) - 1
+    trp, tcol, _ = O.transpose(n, rp, col)
+    want, iters = O.pagerank(n, trp, tcol, np.diff(rp))
+    assert r.iterations == iters
+    assert rel_l1(r.rank, want) <= 1e-4
+
+
+def test_pagerank_repeatable():
+    g = P.generate_rmat(14, 16, seed=9)
+    P.property_at(g)
+    P.property_rowdegree(g)
+    a = algo.pagerank_gap(g)
+    b = algo.pagerank_gap(g)
+    assert a.iterations == b.iterations
+    assert np.array_equal(a.rank, b.rank)
+
+
+# ---------------------------------------------------------------- CC
+@pytest.mark.parametrize("name", case_ids("cc"))
+def test_cc_golden(name):
+    c = CASES[name]
+    g = graph_of(c)
+    r = algo.connected_components_fastsv(g)
+    assert np.array_equal(r.label, c.out["label"])
+
+
+def test_cc_rmat_vs_oracle():
+    g = P.generate_rmat(16, 4, seed=3, kind=P.Kind.UndirectedAdjacency)
+    rp, col, _ = g.export()
+    r = algo.connected_components_fastsv(g)
+    assert np.array_equal(r.label, O.cc(len(rp) - 1, rp, col))
+    again = algo.connected_components_fastsv(g)
+    assert np.array_equal(again.label, r.label)
+
+
+# ---------------------------------------------------------------- graph layer
+@pytest.mark.parametrize("und", [False, True])
+def test_generator_matches_oracle(und):
+    for scale in (8, 12):
+        g = P.generate_rmat(scale, 16, seed=7,
+                            kind=P.Kind.UndirectedAdjacency if und else P.Kind.DirectedAdjacency)
+        rp, col, _ = g.export()
+        wrp, wcol = O.rmat_graph(scale, 16, seed=7, undirected=und)
+        assert np.array_equal(rp, wrp) and np.array_equal(col, wcol)
+    g = P.generate_er(12, 16, seed=3)
+    rp, col, w = g.export()
+    wrp, wcol, ww = O.er_graph(12, 16, seed=3)
+    assert np.array_equal(rp, wrp) and np.array_equal(col, wcol) and np.array_equal(w, ww)
+
+
+def test_graph_object_caches():
+    c = CASES["bfs_randdi0"]
+    g = graph_of(c)
+    props = g.properties()
+    assert not props["AT"] and not props["row_degree"] and props["ndiag"] == -1
+    P.property_at(g)
+    P.property_rowdegree(g)
+    P.property_coldegree(g)
+    P.property_ndiag(g)
+    P.property_symmetric_pattern(g)
+    assert P.check_graph(g)[0] == 0
+    assert np.array_equal(g.row_degree(), np.diff(c.rp))
+    assert np.array_equal(g.col_degree(), np.bincount(c.col, minlength=c.n))
+    P.delete_properties(g)
+    assert not g.has_AT and g.ndiag == -1
+
+
+def test_graph_new_rejects_corrupt_matrix():
+    # test_graph.cpp:24-32: an unsorted row
+    with pytest.raises(P.Error) as e:
+        P.graph_new(np.array([0, 2, 2]), np.array([1, 0]))
+    assert e.value.code == P.ErrCode.InvalidMatrix
+    with pytest.raises(P.Error) as e:
+        P.graph_new(np.array([0, 1, 1]), np.array([5]))
+    assert e.value.code == P.ErrCode.InvalidMatrix
+
+
+@pytest.mark.parametrize("name", case_ids("sort_by_degree"))
+def test_sort_by_degree_golden(name):
+    c = CASES[name]
+    g = graph_of(c)
+    P.property_rowdegree(g)
+    assert np.array_equal(P.sort_by_degree(g, True, True), c.out["perm"])
