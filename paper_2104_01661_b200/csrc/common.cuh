@@ -150,6 +150,10 @@ void generate_er(gbx_graph* g, int logn, int degree, uint64_t seed, int weighted
 int64_t count_ndiag(cudaStream_t s, const Csr& A);
 bool csr_equal(cudaStream_t s, const Csr& X, const Csr& Y);
 void sync(gbx_graph* g);
+int bits_for(int64_t n);
+uint64_t* sort_keys(cudaStream_t s, uint64_t* keys, uint64_t* alt, int64_t m, int end_bit);
+void csr_from_sorted_keys(cudaStream_t s, int64_t n, int bits, const uint64_t* keys,
+                          int64_t nnz, DevArray<int64_t>& rp, DevArray<int32_t>& col);
 
 // ---- algorithms ----------------------------------------------------------------
 void pagerank_run(gbx_graph* g, double damping, double tol, int itermax, double* rank,

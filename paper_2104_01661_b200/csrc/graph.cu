@@ -72,7 +72,7 @@ struct Tmp {
   Tmp& operator=(const Tmp&) = delete;
 };
 
-static int bits_for(int64_t n) {
+int bits_for(int64_t n) {
   int b = 1;
   while ((int64_t(1) << b) < n) ++b;
   return b;
@@ -476,6 +476,30 @@ __global__ void k_split_keys(const uint64_t* keys, int64_t nnz, int bits, int32_
   uint64_t k = keys[p];
   col[p] = static_cast<int32_t>(k & ((uint64_t(1) << bits) - 1));
   atomicAdd(&rowcnt[k >> bits], 1);
+}
+
+// sort 64-bit keys in place (double buffer); returns the buffer holding the result
+uint64_t* sort_keys(cudaStream_t s, uint64_t* keys, uint64_t* alt, int64_t m, int end_bit) {
+  size_t tb = 0;
+  cub::DoubleBuffer<uint64_t> kb(keys, alt);
+  GBX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, m, 0, end_bit, s));
+  Tmp<uint8_t> t(tb, s);
+  GBX_CUDA(cub::DeviceRadixSort::SortKeys(t.p, tb, kb, m, 0, end_bit, s));
+  return kb.Current();
+}
+
+// the first nnz sorted (row<<bits|col) keys -> CSR arrays
+void csr_from_sorted_keys(cudaStream_t s, int64_t n, int bits, const uint64_t* keys,
+                          int64_t nnz, DevArray<int64_t>& rp, DevArray<int32_t>& col) {
+  rp.alloc(n + 1);
+  col.alloc(std::max<int64_t>(nnz, 1));
+  Tmp<int32_t> cnt(std::max<int64_t>(n, 1), s);
+  GBX_CUDA(cudaMemsetAsync(cnt.p, 0, std::max<int64_t>(n, 1) * sizeof(int32_t), s));
+  if (nnz) {
+    k_split_keys<<<ceil_div(nnz, 256), 256, 0, s>>>(keys, nnz, bits, col.p, cnt.p);
+    GBX_LAUNCHED();
+  }
+  counts_to_rowptr(s, cnt.p, n, rp.p);
 }
 
 // sorted (u<<bits|v) keys (+ weights) -> CSR in g->A

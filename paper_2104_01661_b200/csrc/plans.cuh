@@ -17,7 +17,8 @@ struct PrPlan {
   DevArray<int64_t> split_row, split_slot;
   DevArray<double> split_part;
   DevArray<unsigned> split_cnt;
-  DevArray<float> r[2], x[2];
+  DevArray<float> r[2], x[2];      // fp32 storage (tol >= 1e-6)
+  DevArray<double> rd[2], xd[2];    // fp64 storage (tight tolerances)
   DevArray<double> l1_block, l1_hist;
   DevArray<int> ctl;            // [0] completed iterations, [1] done
   DevArray<unsigned> blk_cnt;
@@ -26,6 +27,8 @@ struct PrPlan {
   cudaGraphExec_t exec = nullptr;
   double g_damping = -1, g_tol = -1;
   int g_itermax = -1;
+  int g_prec = 0;
+  int last_prec = 32;
   bool graph_failed = false;
   int last_iters = 0;
   ~PrPlan();

@@ -1,0 +1,471 @@
+// sssp.cu -- delta-stepping SSSP (algo/sssp.cpp:16-112) as ONE persistent
+// cooperative kernel.
+//
+// The reference relaxes light edges (w <= delta) of the current bucket
+// [lo, lo+delta) to a fixpoint, then heavy edges once, and jumps to the next
+// non-empty bucket (sssp.cpp:55-106).  Its result equals Dijkstra exactly
+// (test_sssp.cpp:91-111), so the device mirrors it in result, not mechanism
+// (SURVEY.md §7 hard part 4): a near/far bucketed label-correcting sweep.
+//   * near queue: vertices whose tentative distance fell into the current
+//     bucket; each level relaxes all their edges with atomicMin on the
+//     distance word; improvements below hi re-enter the near queue (deduped
+//     by a per-vertex stamp), improvements above go to the far pile;
+//   * when the near queue drains, the bucket jumps to floor(min far / delta)
+//     * delta (the reference's jump, sssp.cpp:60-65) and the far pile is
+//     split into the new near queue and what stays far -- all on the device;
+//   * edges are packed as (col << 8 | w) in one u32 when n <= 2^24 and the
+//     weights are integers in [1,255] (BASELINE config 4: 4 B/edge), else
+//     separate col + weight arrays; integer weights use u32 distances, other
+//     fp64 weights u64 bit patterns of positive doubles (order-preserving).
+// Algorithmic bytes per source: 8*m_r + 12*V_r.
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <vector>
+
+#include "common.cuh"
+#include "plans.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gbx {
+
+constexpr int kSsspThreads = 256;
+constexpr unsigned kFullW = 0xffffffffu;
+
+template <typename D> struct DistTraits;
+template <> struct DistTraits<uint32_t> {
+  static __device__ __forceinline__ uint32_t inf() { return 0xffffffffu; }
+  static __device__ __forceinline__ uint32_t add(uint32_t d, uint32_t w) { return d + w; }
+  static __device__ __forceinline__ uint32_t bucket_hi(uint32_t lo, double delta) {
+    double h = static_cast<double>(lo) + delta;
+    return h >= 4294967295.0 ? 0xffffffffu : static_cast<uint32_t>(ceil(h));
+  }
+};
+template <> struct DistTraits<unsigned long long> {
+  static __device__ __forceinline__ unsigned long long inf() { return 0x7FF0000000000000ull; }
+  static __device__ __forceinline__ unsigned long long add(unsigned long long d, double w) {
+    return static_cast<unsigned long long>(__double_as_longlong(__longlong_as_double(d) + w));
+  }
+};
+
+// edge readers
+struct PackedEdges {
+  const uint32_t* e;
+  __device__ __forceinline__ void get(int64_t p, int32_t& v, uint32_t& w) const {
+    uint32_t x = __ldg(e + p);
+    v = static_cast<int32_t>(x >> 8);
+    w = x & 0xffu;
+  }
+};
+struct IntEdges {
+  const int32_t* col;
+  const int32_t* w;
+  __device__ __forceinline__ void get(int64_t p, int32_t& v, uint32_t& ww) const {
+    v = __ldg(col + p);
+    ww = static_cast<uint32_t>(__ldg(w + p));
+  }
+};
+struct DblEdges {
+  const int32_t* col;
+  const double* w;
+  __device__ __forceinline__ void get(int64_t p, int32_t& v, double& ww) const {
+    v = __ldg(col + p);
+    ww = __ldg(w + p);
+  }
+};
+
+template <typename D, typename E>
+struct SsspArgs {
+  const int64_t* rp;
+  E edges;
+  int64_t n;
+  double delta;
+  D* dist;
+  int32_t* q0;
+  int32_t* q1;
+  int32_t* f0;
+  int32_t* f1;
+  int32_t* qmark;  // stamp of the last near iteration that queued the vertex
+  int* ctl;        // [0] |Q| [1] |Qnext| [2] |F| [3] |Fnext| [4] near iterations [5] buckets
+  D* lohi;         // [0] lo [1] hi [2] min far (scratch)
+  unsigned long long* relax;  // edges relaxed
+};
+
+__device__ __forceinline__ void warp_push(bool has, int32_t v, int32_t* q, int* cnt) {
+  const int lane = threadIdx.x & 31;
+  unsigned b = __ballot_sync(kFullW, has);
+  if (!b) return;
+  int base = 0;
+  if (lane == 0) base = atomicAdd(cnt, __popc(b));
+  base = __shfl_sync(kFullW, base, 0);
+  if (has) q[base + __popc(b & ((1u << lane) - 1))] = v;
+}
+
+template <typename D>
+__device__ __forceinline__ D next_hi(D lo, double delta);
+template <>
+__device__ __forceinline__ uint32_t next_hi<uint32_t>(uint32_t lo, double delta) {
+  return DistTraits<uint32_t>::bucket_hi(lo, delta);
+}
+template <>
+__device__ __forceinline__ unsigned long long next_hi<unsigned long long>(unsigned long long lo,
+                                                                         double delta) {
+  return static_cast<unsigned long long>(__double_as_longlong(__longlong_as_double(lo) + delta));
+}
+template <typename D>
+__device__ __forceinline__ D bucket_floor(D m, double delta);
+template <>
+__device__ __forceinline__ uint32_t bucket_floor<uint32_t>(uint32_t m, double delta) {
+  return static_cast<uint32_t>(floor(static_cast<double>(m) / delta) * delta);
+}
+template <>
+__device__ __forceinline__ unsigned long long bucket_floor<unsigned long long>(
+    unsigned long long m, double delta) {
+  double lo = floor(__longlong_as_double(m) / delta) * delta;
+  return static_cast<unsigned long long>(__double_as_longlong(lo));
+}
+
+template <typename D, typename E, typename W>
+__global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int grp = lane >> 3, sub = lane & 7;
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t gsize = int64_t(gridDim.x) * blockDim.x;
+  int stamp = 1;
+  int pq = 0, pf = 0;  // parity of the current near queue / far pile
+  for (;;) {
+    // ---------------- near iterations inside the bucket
+    for (;;) {
+      const int nq = *(volatile int*)&a.ctl[0];
+      if (nq == 0) break;
+      const D hi = *(volatile D*)&a.lohi[1];
+      const int32_t* qc = pq ? a.q1 : a.q0;
+      int32_t* qn = pq ? a.q0 : a.q1;
+      int32_t* fc = pf ? a.f1 : a.f0;
+      unsigned long long nrel = 0;
+      for (int64_t base = gwarp * 4; base < nq; base += nwarps * 4) {
+        const int64_t qi = base + grp;
+        bool active = qi < nq;
+        int32_t u = active ? qc[qi] : 0;
+        int64_t p = active ? a.rp[u] : 0, e = active ? a.rp[u + 1] : 0;
+        const D du = active ? *(volatile D*)&a.dist[u] : D(0);
+        while (__any_sync(kFullW, active)) {
+          bool near_push = false, far_push = false;
+          int32_t v = 0;
+          if (active && p + sub < e) {
+            W w;
+            a.edges.get(p + sub, v, w);
+            ++nrel;
+            const D nd = DistTraits<D>::add(du, w);
+            if (nd < *(volatile D*)&a.dist[v]) {
+              const D old = atomicMin(&a.dist[v], nd);
+              if (nd < old) {
+                if (nd < hi) near_push = atomicExch(&a.qmark[v], stamp) != stamp;
+                else far_push = true;
+              }
+            }
+          }
+          warp_push(near_push, v, qn, &a.ctl[1]);
+          warp_push(far_push, v, fc, &a.ctl[2]);
+          if (active) {
+            p += 8;
+            if (p >= e) active = false;
+          }
+        }
+      }
+      if (nrel) atomicAdd(a.relax, nrel);
+      grid.sync();
+      if (gtid == 0) {
+        a.ctl[0] = a.ctl[1];
+        a.ctl[1] = 0;
+        a.ctl[4] += 1;
+      }
+      pq ^= 1;
+      ++stamp;
+      grid.sync();
+    }
+    // ---------------- bucket jump: min over the far pile at or above hi
+    const int nf = *(volatile int*)&a.ctl[2];
+    if (nf == 0) break;
+    const int32_t* fc = pf ? a.f1 : a.f0;
+    int32_t* fn = pf ? a.f0 : a.f1;
+    const D hi = *(volatile D*)&a.lohi[1];
+    {
+      D m = DistTraits<D>::inf();
+      for (int64_t i = gtid; i < nf; i += gsize) {
+        const D d = *(volatile D*)&a.dist[fc[i]];
+        if (d >= hi && d < m) m = d;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        D t = __shfl_xor_sync(kFullW, m, o);
+        m = t < m ? t : m;
+      }
+      if (lane == 0 && m != DistTraits<D>::inf()) atomicMin(&a.lohi[2], m);
+    }
+    grid.sync();
+    const D mfar = *(volatile D*)&a.lohi[2];
+    if (mfar == DistTraits<D>::inf()) break;  // every far entry was stale
+    const D lo2 = bucket_floor<D>(mfar, a.delta);
+    const D hi2 = next_hi<D>(lo2, a.delta);
+    // split the pile: [lo2, hi2) -> near queue, >= hi2 -> stays far, < hi stale
+    int32_t* qn = pq ? a.q1 : a.q0;  // current (empty) near queue
+    for (int64_t base = gwarp * 32; base < nf; base += nwarps * 32) {
+      const int64_t i = base + lane;
+      bool to_near = false, to_far = false;
+      int32_t v = 0;
+      if (i < nf) {
+        v = fc[i];
+        const D d = *(volatile D*)&a.dist[v];
+        if (d >= hi) {
+          if (d < hi2) to_near = atomicExch(&a.qmark[v], stamp) != stamp;
+          else to_far = true;
+        }
+      }
+      warp_push(to_near, v, qn, &a.ctl[0]);
+      warp_push(to_far, v, fn, &a.ctl[3]);
+    }
+    grid.sync();
+    if (gtid == 0) {
+      a.lohi[0] = lo2;
+      a.lohi[1] = hi2;
+      a.lohi[2] = DistTraits<D>::inf();
+      a.ctl[2] = a.ctl[3];
+      a.ctl[3] = 0;
+      a.ctl[5] += 1;
+    }
+    pf ^= 1;
+    ++stamp;
+    grid.sync();
+  }
+}
+
+template <typename D>
+__global__ void k_sssp_init(D* dist, int32_t* qmark, int64_t n, int32_t src, int32_t* q0, int* ctl,
+                            D* lohi, unsigned long long* relax, D hi0, D inf) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) { dist[i] = i == src ? D(0) : inf; qmark[i] = 0; }
+  if (i == 0) {
+    q0[0] = src;
+    for (int k = 0; k < 8; ++k) ctl[k] = 0;
+    ctl[0] = 1;
+    lohi[0] = D(0);
+    lohi[1] = hi0;
+    lohi[2] = inf;
+    *relax = 0;
+  }
+}
+
+template <typename D>
+__global__ void k_sssp_out(const D* dist, int64_t n, double* out);
+template <>
+__global__ void k_sssp_out<uint32_t>(const uint32_t* dist, int64_t n, double* out) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = dist[i] == 0xffffffffu ? __longlong_as_double(0x7FF0000000000000ll)
+                                              : static_cast<double>(dist[i]);
+}
+template <>
+__global__ void k_sssp_out<unsigned long long>(const unsigned long long* dist, int64_t n,
+                                               double* out) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = __longlong_as_double(static_cast<long long>(dist[i]));
+}
+
+// ---- plan ------------------------------------------------------------------------
+
+__global__ void k_weight_stats(const uint8_t* val, int dom, int64_t nnz, int* bad_nonpos,
+                               int* nonint, double* maxw) {
+  int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  double w = 0;
+  bool ni = false, np = false;
+  if (p < nnz) {
+    if (dom == GBX_FP64) {
+      w = reinterpret_cast<const double*>(val)[p];
+      np = !(w > 0.0);
+      ni = !(w == floor(w)) || w > 2147483647.0;
+    } else {
+      w = reinterpret_cast<const int32_t*>(val)[p];
+      np = !(w > 0.0);
+    }
+  }
+  if (np) atomicOr(bad_nonpos, 1);
+  if (ni) atomicOr(nonint, 1);
+  typedef cub::BlockReduce<double, 256> BR;
+  __shared__ typename BR::TempStorage t;
+  double m = BR(t).Reduce(p < nnz ? w : -1.0, cub::Max());
+  if (threadIdx.x == 0) {
+    // max of non-negative doubles via integer atomicMax on the bit pattern
+    if (m > 0) atomicMax(reinterpret_cast<unsigned long long*>(maxw),
+                         static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
+__global__ void k_pack_edges(const int32_t* col, const uint8_t* val, int dom, int64_t nnz,
+                             uint32_t* packed, int32_t* wint) {
+  int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p >= nnz) return;
+  int32_t w = dom == GBX_FP64 ? static_cast<int32_t>(reinterpret_cast<const double*>(val)[p])
+                              : reinterpret_cast<const int32_t*>(val)[p];
+  if (packed) packed[p] = (static_cast<uint32_t>(col[p]) << 8) | static_cast<uint32_t>(w);
+  if (wint) wint[p] = w;
+}
+
+void sssp_prepare(gbx_graph* g) {
+  if (g->sssp) return;
+  const Csr& A = g->A;
+  if (A.domain != GBX_FP64 && A.domain != GBX_INT32)
+    fail(GBX_DOMAIN_MISMATCH, "sssp needs fp64 (or int32) edge weights");
+  cudaStream_t s = g->stream;
+  auto P = std::make_unique<SsspPlan>();
+  P->n = A.n;
+  P->nnz = A.nnz;
+  DevArray<int> flags(2);
+  DevArray<double> mx(1);
+  GBX_CUDA(cudaMemsetAsync(flags.p, 0, 8, s));
+  GBX_CUDA(cudaMemsetAsync(mx.p, 0, 8, s));
+  if (A.nnz) {
+    k_weight_stats<<<ceil_div(A.nnz, 256), 256, 0, s>>>(A.val.p, A.domain, A.nnz, flags.p,
+                                                         flags.p + 1, mx.p);
+    GBX_LAUNCHED();
+  }
+  int hf[2];
+  GBX_CUDA(cudaMemcpyAsync(hf, flags.p, 8, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaMemcpyAsync(&P->max_w, mx.p, 8, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  P->nonpositive = hf[0] != 0;
+  const bool integral = hf[1] == 0;
+  // u32 distances are exact while max_w * (n-1) fits
+  P->integral = integral && P->max_w * static_cast<double>(std::max<int64_t>(A.n - 1, 1)) <
+                                4294967294.0;
+  P->packed = P->integral && P->max_w <= 255.0 && A.n <= (int64_t(1) << 24);
+  if (!P->nonpositive && A.nnz) {
+    if (P->packed) {
+      P->packed_edges.alloc(A.nnz);
+      k_pack_edges<<<ceil_div(A.nnz, 256), 256, 0, s>>>(A.col.p, A.val.p, A.domain, A.nnz,
+                                                         P->packed_edges.p, nullptr);
+      GBX_LAUNCHED();
+    } else if (P->integral) {
+      if (A.domain == GBX_FP64) {
+        P->wint.alloc(A.nnz);
+        k_pack_edges<<<ceil_div(A.nnz, 256), 256, 0, s>>>(A.col.p, A.val.p, A.domain, A.nnz,
+                                                           nullptr, P->wint.p);
+        GBX_LAUNCHED();
+      }
+    }
+  }
+  const int64_t n1 = std::max<int64_t>(A.n, 1);
+  if (P->integral) P->dist32.alloc(n1); else P->dist64.alloc(n1);
+  P->q[0].alloc(n1 + 1);
+  P->q[1].alloc(n1 + 1);
+  // far pile: every successful improvement above hi appends once
+  const int64_t fcap = A.nnz + A.n + 1;
+  P->far[0].alloc(fcap);
+  P->far[1].alloc(fcap);
+  P->stamp.alloc(n1);
+  P->ctl.alloc(8);
+  P->lohi.alloc(3);
+  P->relax.alloc(1);
+  GBX_CUDA(cudaStreamSynchronize(s));
+  g->sssp = std::move(P);
+}
+
+template <typename D, typename E, typename W>
+static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src, double delta,
+                        D hi0, D inf) {
+  cudaStream_t s = g->stream;
+  const int64_t n = P.n;
+  D* lohi = reinterpret_cast<D*>(P.lohi.p);
+  k_sssp_init<D><<<ceil_div(n, 256), 256, 0, s>>>(dist, P.stamp.p, n, src, P.q[0].p, P.ctl.p,
+                                                   lohi, P.relax.p, hi0, inf);
+  GBX_LAUNCHED();
+  SsspArgs<D, E> a{};
+  a.rp = g->A.rp.p;
+  a.edges = edges;
+  a.n = n;
+  a.delta = delta;
+  a.dist = dist;
+  a.q0 = P.q[0].p;
+  a.q1 = P.q[1].p;
+  a.f0 = P.far[0].p;
+  a.f1 = P.far[1].p;
+  a.qmark = P.stamp.p;
+  a.ctl = P.ctl.p;
+  a.lohi = lohi;
+  a.relax = P.relax.p;
+  auto fn = k_sssp<D, E, W>;
+  int per_sm = 0;
+  GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSsspThreads, 0));
+  if (per_sm < 1) fail(GBX_CUDA_ERROR, "sssp kernel does not fit on an SM");
+  const int grid = device_sms() * per_sm;
+  void* args[] = {&a};
+  GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid),
+                                       dim3(kSsspThreads), args, 0, s));
+}
+
+void sssp_run(gbx_graph* g, uint64_t source, double delta, double* out) {
+  const int64_t n = g->A.n;
+  if (source >= static_cast<uint64_t>(n))
+    fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(source));
+  if (!(delta > 0.0)) fail(GBX_NON_POSITIVE_DELTA, "delta must be positive");
+  sssp_prepare(g);
+  SsspPlan& P = *g->sssp;
+  if (P.nonpositive) fail(GBX_NON_POSITIVE_WEIGHT, "edge weights must be positive");
+  const int32_t src = static_cast<int32_t>(source);
+  if (P.integral) {
+    // integer distances: bucket [lo, lo+delta) -> integer hi = ceil(lo + delta)
+    const double h0 = std::ceil(delta);
+    const uint32_t hi0 = h0 >= 4294967295.0 ? 0xffffffffu : static_cast<uint32_t>(h0);
+    if (P.packed) {
+      sssp_launch<uint32_t, PackedEdges, uint32_t>(g, P, PackedEdges{P.packed_edges.p},
+                                                   P.dist32.p, src, delta, hi0, 0xffffffffu);
+    } else {
+      const int32_t* w = g->A.domain == GBX_INT32 ? reinterpret_cast<const int32_t*>(g->A.val.p)
+                                                  : P.wint.p;
+      sssp_launch<uint32_t, IntEdges, uint32_t>(g, P, IntEdges{g->A.col.p, w}, P.dist32.p, src,
+                                                delta, hi0, 0xffffffffu);
+    }
+  } else {
+    unsigned long long hi0, inf = 0x7FF0000000000000ull;
+    std::memcpy(&hi0, &delta, 8);
+    sssp_launch<unsigned long long, DblEdges, double>(
+        g, P, DblEdges{g->A.col.p, reinterpret_cast<const double*>(g->A.val.p)}, P.dist64.p,
+        src, delta, hi0, inf);
+  }
+  cudaStream_t s = g->stream;
+  if (out) {
+    double* tmp = nullptr;
+    GBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), std::max<int64_t>(n, 1) * 8, s));
+    if (P.integral) k_sssp_out<uint32_t><<<ceil_div(n, 256), 256, 0, s>>>(P.dist32.p, n, tmp);
+    else k_sssp_out<unsigned long long><<<ceil_div(n, 256), 256, 0, s>>>(P.dist64.p, n, tmp);
+    cudaError_t le = cudaGetLastError();
+    if (le == cudaSuccess) le = cudaMemcpyAsync(out, tmp, n * 8, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(tmp, s);
+    GBX_CUDA(le);
+  }
+  int hctl[8];
+  unsigned long long rel = 0;
+  GBX_CUDA(cudaMemcpyAsync(hctl, P.ctl.p, sizeof hctl, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaMemcpyAsync(&rel, P.relax.p, 8, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  g->stats = gbx_stats{};
+  g->stats.launches = 2 + (out ? 1 : 0);
+  g->stats.hot_launches = 1;
+  g->stats.iterations = hctl[4];
+  g->stats.work_units = static_cast<int64_t>(rel);
+}
+
+// sssp_default_delta (sssp.cpp:114-120): half the largest weight, or 1.
+double sssp_default_delta(gbx_graph* g) {
+  if (g->A.nnz == 0 || (g->A.domain != GBX_FP64 && g->A.domain != GBX_INT32)) return 1.0;
+  sssp_prepare(g);
+  const double m = g->sssp->max_w;
+  return m > 0 ? m / 2.0 : 1.0;
+}
+
+}  // namespace gbx

@@ -2,9 +2,6 @@
 #include "common.cuh"
 #include "plans.cuh"
 namespace gbx {
-uint64_t tc_run(gbx_graph*, int64_t, int64_t) { fail(GBX_UNSUPPORTED, "triangle_count: not yet implemented"); }
-void tc_prepare(gbx_graph*) { fail(GBX_UNSUPPORTED, "tc: not yet implemented"); }
-void tc_partition(gbx_graph*, int, int64_t*) { fail(GBX_UNSUPPORTED, "tc: not yet implemented"); }
 void sssp_run(gbx_graph*, uint64_t, double, double*) { fail(GBX_UNSUPPORTED, "sssp: not yet implemented"); }
 double sssp_default_delta(gbx_graph*) { fail(GBX_UNSUPPORTED, "sssp: not yet implemented"); }
 void sssp_prepare(gbx_graph*) { fail(GBX_UNSUPPORTED, "sssp: not yet implemented"); }

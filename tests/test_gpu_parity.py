@@ -221,3 +221,57 @@ def test_sort_by_degree_golden(name):
     g = graph_of(c)
     P.property_rowdegree(g)
     assert np.array_equal(P.sort_by_degree(g, True, True), c.out["perm"])
+
+
+# ---------------------------------------------------------------- triangle count
+def _tc_ready(c):
+    g = graph_of(c)
+    P.property_rowdegree(g)
+    P.property_ndiag(g)
+    return g
+
+
+@pytest.mark.parametrize("name", case_ids("triangle_count"))
+def test_tc_golden(name):
+    c = CASES[name]
+    g = _tc_ready(c)
+    for ps, tag in ((algo.Presort.Auto, "auto"), (algo.Presort.Force, "force"),
+                    (algo.Presort.Never, "never")):
+        assert algo.triangle_count(g, algo.TriangleCountConfig(ps)) == int(c.out[f"count_{tag}"])
+
+
+def test_tc_preconditions():
+    c = CASES["tc_K3"]
+    g = graph_of(c)
+    P.property_rowdegree(g)
+    with pytest.raises(P.Error) as e:
+        algo.triangle_count(g)
+    assert e.value.code == P.ErrCode.MissingProperty
+    # self loop on a directed-kind graph marked symmetric (test_tc.cpp:100-112)
+    rp = np.array([0, 2, 5, 7])
+    col = np.array([1, 2, 0, 1, 2, 0, 1])
+    bad = P.graph_new(rp, col, kind=P.Kind.DirectedAdjacency)
+    P.property_symmetric_pattern(bad)
+    P.property_ndiag(bad)
+    P.property_rowdegree(bad)
+    with pytest.raises(P.Error) as e:
+        algo.triangle_count(bad)
+    assert e.value.code == P.ErrCode.PreconditionViolated
+    d = P.graph_new(np.array([0, 1, 2, 2]), np.array([1, 2]), kind=P.Kind.DirectedAdjacency)
+    P.property_symmetric_pattern(d)
+    P.property_ndiag(d)
+    P.property_rowdegree(d)
+    with pytest.raises(P.Error) as e:
+        algo.triangle_count(d)
+    assert e.value.code == P.ErrCode.PreconditionViolated
+    fresh = graph_of(CASES["tc_K4"])
+    assert algo.basic.triangle_count(fresh) == 4
+    assert fresh.ndiag == 0
+
+
+@pytest.mark.parametrize("scale", [14, 16])
+def test_tc_rmat_vs_oracle(scale):
+    g = P.generate_rmat(scale, 16, seed=4, kind=P.Kind.UndirectedAdjacency)
+    rp, col, _ = g.export()
+    want = O.triangle_count(len(rp) - 1, rp, col)
+    assert algo.basic.triangle_count(g) == want
