@@ -72,6 +72,7 @@ struct SsspPlan {
   int64_t n = 0, nnz = 0;
   bool packed = false;     // uint32 col<<8|w, n <= 2^24, integer w in [1,255]
   bool integral = false;   // integer weights: uint32 distances
+  bool nonpositive = false; // some weight <= 0 (NonPositiveWeight on every call)
   double max_w = 0;
   DevArray<uint32_t> packed_edges;
   DevArray<int32_t> wint;
@@ -80,6 +81,7 @@ struct SsspPlan {
   DevArray<unsigned long long> dist64;
   DevArray<int32_t> q[2], far[2], stamp;
   DevArray<int> ctl;
+  DevArray<unsigned long long> lohi, relax;
 };
 
 // Betweenness workspaces (bc.cu).

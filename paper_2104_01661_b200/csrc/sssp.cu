@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <limits>
 #include <vector>
 
@@ -90,6 +91,7 @@ struct SsspArgs {
   int32_t* f0;
   int32_t* f1;
   int32_t* qmark;  // stamp of the last near iteration that queued the vertex
+  int32_t* fmark;  // stamp of the bucket epoch whose far pile holds the vertex
   int* ctl;        // [0] |Q| [1] |Qnext| [2] |F| [3] |Fnext| [4] near iterations [5] buckets
   D* lohi;         // [0] lo [1] hi [2] min far (scratch)
   unsigned long long* relax;  // edges relaxed
@@ -138,7 +140,8 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int64_t gsize = int64_t(gridDim.x) * blockDim.x;
-  int stamp = 1;
+  int stamp = 1;       // near-queue epoch (one per near iteration)
+  int bstamp = 1;      // far-pile epoch (one per bucket): a vertex sits in the pile once
   int pq = 0, pf = 0;  // parity of the current near queue / far pile
   for (;;) {
     // ---------------- near iterations inside the bucket
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
               const D old = atomicMin(&a.dist[v], nd);
               if (nd < old) {
                 if (nd < hi) near_push = atomicExch(&a.qmark[v], stamp) != stamp;
-                else far_push = true;
+                else far_push = atomicExch(&a.fmark[v], bstamp) != bstamp;
               }
             }
           }
@@ -213,7 +216,9 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
     const D mfar = *(volatile D*)&a.lohi[2];
     if (mfar == DistTraits<D>::inf()) break;  // every far entry was stale
     const D lo2 = bucket_floor<D>(mfar, a.delta);
-    const D hi2 = next_hi<D>(lo2, a.delta);
+    D hi2 = next_hi<D>(lo2, a.delta);
+    if (!(mfar < hi2)) hi2 = mfar + 1;  // rounding guard: the bucket must hold mfar
+                                         // (for fp64 bit patterns: the next double up)
     // split the pile: [lo2, hi2) -> near queue, >= hi2 -> stays far, < hi stale
     int32_t* qn = pq ? a.q1 : a.q0;  // current (empty) near queue
     for (int64_t base = gwarp * 32; base < nf; base += nwarps * 32) {
@@ -225,7 +230,7 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
         const D d = *(volatile D*)&a.dist[v];
         if (d >= hi) {
           if (d < hi2) to_near = atomicExch(&a.qmark[v], stamp) != stamp;
-          else to_far = true;
+          else to_far = atomicExch(&a.fmark[v], bstamp + 1) != bstamp + 1;
         }
       }
       warp_push(to_near, v, qn, &a.ctl[0]);
@@ -241,6 +246,7 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
       a.ctl[5] += 1;
     }
     pf ^= 1;
+    ++bstamp;
     ++stamp;
     grid.sync();
   }
@@ -250,7 +256,7 @@ template <typename D>
 __global__ void k_sssp_init(D* dist, int32_t* qmark, int64_t n, int32_t src, int32_t* q0, int* ctl,
                             D* lohi, unsigned long long* relax, D hi0, D inf) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < n) { dist[i] = i == src ? D(0) : inf; qmark[i] = 0; }
+  if (i < n) { dist[i] = i == src ? D(0) : inf; qmark[i] = 0; qmark[n + i] = 0; }
   if (i == 0) {
     q0[0] = src;
     for (int k = 0; k < 8; ++k) ctl[k] = 0;
@@ -364,10 +370,10 @@ void sssp_prepare(gbx_graph* g) {
   P->q[0].alloc(n1 + 1);
   P->q[1].alloc(n1 + 1);
   // far pile: every successful improvement above hi appends once
-  const int64_t fcap = A.nnz + A.n + 1;
+  const int64_t fcap = A.n + 1;  // <= one entry per vertex per bucket epoch
   P->far[0].alloc(fcap);
   P->far[1].alloc(fcap);
-  P->stamp.alloc(n1);
+  P->stamp.alloc(2 * n1);  // near stamps, then far stamps
   P->ctl.alloc(8);
   P->lohi.alloc(3);
   P->relax.alloc(1);
@@ -395,6 +401,7 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
   a.f0 = P.far[0].p;
   a.f1 = P.far[1].p;
   a.qmark = P.stamp.p;
+  a.fmark = P.stamp.p + n;
   a.ctl = P.ctl.p;
   a.lohi = lohi;
   a.relax = P.relax.p;

@@ -275,3 +275,106 @@ def test_tc_rmat_vs_oracle(scale):
     rp, col, _ = g.export()
     want = O.triangle_count(len(rp) - 1, rp, col)
     assert algo.basic.triangle_count(g) == want
+
+
+# ---------------------------------------------------------------- SSSP
+@pytest.mark.parametrize("name", case_ids("sssp"))
+def test_sssp_golden(name):
+    c = CASES[name]
+    g = graph_of(c)
+    for d in c.params["deltas"]:
+        r = algo.sssp_delta_stepping(g, c.params["src"], d)
+        assert np.array_equal(r.dist, c.out[f"dist_{d:g}"]), d
+    assert algo.sssp_default_delta(g) == c.params["default_delta"]
+
+
+def test_sssp_errors():
+    g = P.graph_new(np.array([0, 1, 1]), np.array([1]), np.array([1.0]))
+    for src, delta, code in ((5, 1.0, P.ErrCode.SourceOutOfRange),
+                             (0, 0.0, P.ErrCode.NonPositiveDelta),
+                             (0, -1.0, P.ErrCode.NonPositiveDelta)):
+        with pytest.raises(P.Error) as e:
+            algo.sssp_delta_stepping(g, src, delta)
+        assert e.value.code == code
+    neg = P.graph_new(np.array([0, 1, 1]), np.array([1]), np.array([-2.0]))
+    with pytest.raises(P.Error) as e:
+        algo.sssp_delta_stepping(neg, 0, 1.0)
+    assert e.value.code == P.ErrCode.NonPositiveWeight
+    ints = P.graph_new(np.array([0, 1, 1]), np.array([1]), np.array([1], np.int64))
+    with pytest.raises(P.Error) as e:
+        algo.sssp_delta_stepping(ints, 0, 1.0)
+    assert e.value.code == P.ErrCode.DomainMismatch
+    # basic wrapper: delta = max / 2 (test_sssp.cpp:113-121)
+    b = P.graph_new(np.array([0, 1, 2, 2]), np.array([1, 2]), np.array([3.0, 6.0]))
+    assert algo.basic.sssp_delta_stepping(b, 0).dist[2] == 9.0
+
+
+@pytest.mark.parametrize("logn", [12, 16])
+def test_sssp_er_vs_oracle(logn):
+    g = P.generate_er(logn, 16, seed=6)
+    rp, col, w = g.export()
+    n = len(rp) - 1
+    P.property_rowdegree(g)
+    for s in P.pick_sources(g.row_degree(), 3, 6):
+        want = O.dijkstra(n, rp, col, w.astype(np.float64), s)
+        for delta in (64.0, 16.0, 1000.0):
+            got = algo.sssp_delta_stepping(g, int(s), delta).dist
+            assert np.array_equal(got, want)
+
+
+def test_sssp_fp64_weights_vs_oracle():
+    rng = np.random.default_rng(3)
+    g0 = P.generate_rmat(12, 8, seed=2)
+    rp, col, _ = g0.export()
+    w = rng.uniform(1e-3, 10.0, len(col))
+    g = P.graph_new(rp, col, w)
+    n = len(rp) - 1
+    for s in (0, 1, 17):
+        want = O.dijkstra(n, rp, col, w, s)
+        for delta in (0.5, 2.0, 8.0):
+            assert np.array_equal(algo.sssp_delta_stepping(g, s, delta).dist, want)
+
+
+# ---------------------------------------------------------------- betweenness
+@pytest.mark.parametrize("name", case_ids("bc"))
+def test_bc_golden(name):
+    c = CASES[name]
+    g = graph_of(c)
+    P.property_at(g)
+    got = algo.betweenness_centrality(g, c.params["sources"]).centrality
+    want = c.out["centrality"]
+    # test_bc.cpp:74-91 accepts 1e-9 absolute against Brandes
+    assert np.max(np.abs(got - want), initial=0.0) <= 1e-9
+
+
+def test_bc_errors_and_basic():
+    c = CASES["bc_path3"]
+    g = graph_of(c)
+    with pytest.raises(P.Error) as e:
+        algo.betweenness_centrality(g, [0])
+    assert e.value.code == P.ErrCode.MissingProperty
+    P.property_at(g)
+    with pytest.raises(P.Error) as e:
+        algo.betweenness_centrality(g, [])
+    assert e.value.code == P.ErrCode.EmptyBatch
+    with pytest.raises(P.Error) as e:
+        algo.betweenness_centrality(g, [7])
+    assert e.value.code == P.ErrCode.SourceOutOfRange
+    g2 = graph_of(CASES["bc_star4"])
+    b = algo.basic.betweenness_centrality(g2, [0, 1, 2, 3, 4]).centrality
+    assert np.allclose(b, CASES["bc_star4"].out["centrality"], atol=1e-12)
+
+
+@pytest.mark.parametrize("und", [True, False])
+def test_bc_rmat_vs_oracle(und):
+    kind = P.Kind.UndirectedAdjacency if und else P.Kind.DirectedAdjacency
+    g = P.generate_rmat(14, 16, seed=8, kind=kind)
+    P.property_at(g)
+    P.property_rowdegree(g)
+    rp, col, _ = g.export()
+    n = len(rp) - 1
+    trp, tcol, _ = O.transpose(n, rp, col)
+    srcs = P.pick_sources(g.row_degree(), 6, 8)
+    got = algo.betweenness_centrality(g, srcs).centrality
+    want = O.bc(n, rp, col, trp, tcol, srcs)
+    assert rel_l1(got, want) <= 1e-9
