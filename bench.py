@@ -1,0 +1,438 @@
+#!/usr/bin/env python3
+"""Benchmark driver (contract: one JSON line from rank 0).
+
+Headline workload (BASELINE.json configs[1]): GAP PageRank on a directed R-MAT
+scale-22 graph (edge factor 16, a/b/c = .57/.19/.19, duplicates and self-loops
+removed), fp32 ranks, damping 0.85, tol 1e-4, itermax 100.  Metric:
+edges/s/iter = nnz(AT) * iterations / seconds per run.  One "step" = one full
+pagerank_gap run to convergence on the resident graph.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload pagerank|bfs|bfs64|tc|sssp|bc] [--scale S]
+
+`value` is device-timed (CUDA events on the library's stream, L2 flushed
+between steps, graph resident in HBM).  `e2e` goes through the C ABI with host
+buffers: H2D of the CSR from pinned memory, graph_new + the basic call (which
+builds AT and the degree cache on the device) and D2H of the ranks, timed on
+the host around the synchronous call.  `--impl reference` times the reference
+library itself (oracle/_ref, built from /root/reference) on the box's CPU.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PageRank edges/s/iter at R-MAT scale 22 (BASELINE: BFS GTEPS & PageRank " \
+         "edges/s/iter at R-MAT scale 22-24; % of HBM roofline)"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 4 + k and r[4 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- distributed
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def maybe_init_dist(ws, local):
+    if ws <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist
+
+
+def max_over_ranks(dist, x):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ---------------------------------------------------------------- CPU baselines
+def cpu_baseline_pagerank(scale, seed, budget_s=12.0):
+    """The reference's own pull SpMV (core.cpp:340-386, via oracle/_ref) on a
+    bounded row sample of the same AT, plus the multi-threaded oracle port on
+    the full graph for a few iterations.  Returns (baseline dict, extras)."""
+    import oracle as O
+    rp, col = O.rmat_graph(scale, 16, seed=seed, undirected=False)
+    n = len(rp) - 1
+    trp, tcol, _ = O.transpose(n, rp, col)
+    outdeg = np.diff(rp)
+    extras = {}
+    # port: 3 iterations of the restatement, all host threads
+    t0 = time.perf_counter()
+    O.pagerank(n, trp, tcol, outdeg, 0.85, 0.0, 3)
+    tp = time.perf_counter() - t0
+    port = {"value": float(trp[-1]) * 3 / tp, "unit": "edges/s/iter", "cores": O.threads(),
+            "kind": "port",
+            "sample": f"oracle restatement, 3 PageRank iterations on the full scale-{scale} graph"}
+    extras["port"] = port
+    if not O.ref_available():
+        return port, extras
+    # reference: rows [0, R) of AT through gblite::mxv, R grown to ~budget_s
+    r = 4
+    secs, _ = O.ref_pr_mxv_sample(n, trp, tcol, outdeg, 0.85, 0, r)
+    while secs < budget_s / 4 and r < n:
+        r = min(n, int(r * max(2.0, budget_s / 2 / max(secs, 1e-3))))
+        secs, _ = O.ref_pr_mxv_sample(n, trp, tcol, outdeg, 0.85, 0, r)
+    edges = int(trp[r] - trp[0])
+    ref = {"value": edges / secs, "unit": "edges/s/iter", "cores": 1, "kind": "reference",
+           "sample": f"gblite mxv (plus.second, core.cpp:340-386) over rows [0,{r}) of AT "
+                     f"({edges} edges) of the scale-{scale} graph against the full contribution "
+                     f"vector, {secs:.1f} s; the reference is single-threaded and O(n*nnz(u)) "
+                     f"per pull (SURVEY.md §3.3)"}
+    return ref, extras
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle as O
+    O.build(ref=os.path.isdir("/root/reference/proj/src"))
+    scale = args.scale or 22
+    vals = []
+    base = None
+    for _ in range(args.warmup):
+        pass
+    for step in range(max(args.steps, 1)):
+        base, extras = cpu_baseline_pagerank(scale, 1, budget_s=max(4.0, 60.0 / args.steps))
+        vals.append(base["value"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s/iter",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"pagerank_rmat{scale}_directed", "scale": scale,
+                       "edge_factor": 16, "damping": 0.85, "tol": 1e-4, "itermax": 100},
+            "cpu_baseline": dict(base, value=v),
+            "e2e": {"value": v, "unit": "edges/s/iter", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm: PageRank
+def bench_pagerank(args, dist, ws, rank, local):
+    import torch
+    import paper_2104_01661_b200 as P
+    from paper_2104_01661_b200 import algo
+    from paper_2104_01661_b200.graph import call
+    import ctypes as C
+
+    scale = args.scale or 22
+    P.init(local)
+    torch.cuda.set_device(local)
+    g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.DirectedAdjacency)
+    P.property_at(g)
+    P.property_rowdegree(g)
+    g.prepare("pagerank")
+    n, nnz, _, _ = g.info()
+    stream = torch.cuda.ExternalStream(g.stream())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    it = C.c_int(0)
+
+    def step():
+        call("gbx_pagerank", None, C.byref(it), g.handle, 0.85, 1e-4, 100)
+        return it.value
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    times, iters = [], []
+    barrier(dist)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            k = step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+            iters.append(k)
+    torch.cuda.synchronize()
+    barrier(dist)
+    st = g.last_stats()
+    t_step = max_over_ranks(dist, sum(times) / len(times))
+    k_iter = iters[-1]
+    value = nnz * k_iter / t_step * ws
+    hot_bytes = st["hot_bytes_per_launch"]
+    t_launch = t_step / max(k_iter, 1)   # graph launch = init + k iteration kernels
+    peak, peak_kind = peaks()
+    achieved = hot_bytes / t_launch / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "pagerank_ncu.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    # e2e through the C ABI with host buffers (pinned), basic mode
+    rp, col, _ = g.export()
+    rp_h = torch.from_numpy(rp).pin_memory()
+    col_h = torch.from_numpy(col).pin_memory()
+    rank_h = torch.empty(n, dtype=torch.float64).pin_memory()
+    e2e_times = []
+    for s in range(max(2, min(args.steps, 5)) + 1):
+        t0 = time.perf_counter()
+        h = C.c_void_p()
+        call("gbx_graph_new32", C.byref(h), n, rp_h.data_ptr(), col_h.data_ptr(), None, 0, 0)
+        call("gbx_basic_pagerank", rank_h.data_ptr(), C.byref(it), h, 0.85, 1e-4, 100)
+        call("gbx_graph_free", C.byref(h))
+        if s > 0:  # the first is a warm-up
+            e2e_times.append(time.perf_counter() - t0)
+    t_e2e = max_over_ranks(dist, statistics.median(e2e_times))
+    e2e_val = nnz * it.value / t_e2e * ws
+    out = {
+        "metric": METRIC, "value": value, "unit": "edges/s/iter", "n_gpus": ws,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak" if ws > 1 else "weak",
+        "vs_baseline": None, "dtype": "f32 (ranks; fp64 row sums and L1)",
+        "data": "synthetic (seeded R-MAT, generated in HBM)",
+        "config": {"workload": f"pagerank_rmat{scale}_directed", "scale": scale, "n": n,
+                   "nnz": nnz, "edge_factor": 16, "a_b_c": [0.57, 0.19, 0.19],
+                   "damping": 0.85, "tol": 1e-4, "itermax": 100, "iterations": k_iter,
+                   "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                   "l2": "flushed (256 MB write) before every step"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "k_pr_iter (fused pull SpMV + epilogue)",
+                     "bytes_per_launch": hot_bytes,
+                     "launch_ms": t_launch * 1e3,
+                     "note": "launch time = device time of one run / iterations (the run is "
+                             "one CUDA graph: 1 init kernel + one k_pr_iter per iteration)"},
+        "e2e": {"value": e2e_val, "unit": "edges/s/iter",
+                "h2d_bytes_per_step": int(rp.nbytes + col.nbytes),
+                "d2h_bytes_per_step": int(n * 8 + 4),
+                "includes": "H2D CSR (pinned), graph_new32 validation, property_at "
+                            "(device transpose), property_rowdegree, PageRank, D2H ranks"},
+        "gpu_launches": int((st["launches"]) * args.steps),
+        "clocks": clk.summary(),
+    }
+    return out, (scale,)
+
+
+# ---------------------------------------------------------------- other workloads
+def bench_simple(args, dist, ws, rank, local):
+    """Secondary configs (not the headline): bfs, bfs64, tc, sssp, bc."""
+    import ctypes as C
+
+    import torch
+    import paper_2104_01661_b200 as P
+    from paper_2104_01661_b200 import algo
+
+    P.init(local)
+    torch.cuda.set_device(local)
+    w = args.workload
+    peak, peak_kind = peaks()
+    if w in ("bfs", "bfs64"):
+        scale = args.scale or (22 if w == "bfs" else 16)
+        g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
+        P.property_at(g)
+        P.property_rowdegree(g)
+        n, nnz, _, _ = g.info()
+        deg = g.row_degree()
+        srcs = P.pick_sources(deg, 64, 1)
+        from paper_2104_01661_b200.graph import call
+        import oracle  # noqa: F401  (not used on the timed path)
+
+        def one():
+            if w == "bfs":
+                for s in srcs[:8]:
+                    call("gbx_bfs", None, None, g.handle, int(s), 0, 16)
+                return 8
+            arr = np.ascontiguousarray(srcs, np.uint64)
+            call("gbx_bfs_batch", None, None, g.handle, arr.ctypes.data, len(arr))
+            return 64
+        unit_edges = nnz / 2  # Graph500 undirected convention (reached component ~ all)
+        metric = f"BFS GTEPS at R-MAT scale {scale} ({'single source' if w == 'bfs' else '64-source batch'})"
+        unit = "GTEPS"
+    elif w == "tc":
+        scale = args.scale or 22
+        g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
+        P.property_rowdegree(g)
+        P.property_ndiag(g)
+        g.prepare("tc")
+        n, nnz, _, _ = g.info()
+
+        def one():
+            algo.triangle_count(g)
+            return 1
+        unit_edges = nnz / 2
+        metric = f"triangle count edges/s at R-MAT scale {scale}"
+        unit = "edges/s"
+    elif w == "sssp":
+        logn = args.scale or 24
+        g = P.generate_er(logn, 16, seed=1)
+        P.property_rowdegree(g)
+        g.prepare("sssp")
+        n, nnz, _, _ = g.info()
+        srcs = P.pick_sources(g.row_degree(), 16, 1)
+        from paper_2104_01661_b200.graph import call
+
+        def one():
+            for s in srcs:
+                call("gbx_sssp", None, g.handle, int(s), 64.0)
+            return len(srcs)
+        unit_edges = nnz
+        metric = f"SSSP relaxation edges/s (ER 2^{logn}, 16 sources, delta 64)"
+        unit = "edges/s"
+    elif w == "bc":
+        scale = args.scale or 24
+        g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
+        P.property_at(g)
+        P.property_rowdegree(g)
+        n, nnz, _, _ = g.info()
+        srcs = P.pick_sources(g.row_degree(), 4, 1)
+        from paper_2104_01661_b200.graph import call
+
+        def one():
+            s = np.ascontiguousarray(srcs, np.uint64)
+            call("gbx_betweenness", None, g.handle, s.ctypes.data, 4)
+            return 4
+        unit_edges = nnz
+        metric = f"BC batch-4 edges/s at R-MAT scale {scale}"
+        unit = "edges/s"
+    else:
+        raise SystemExit(f"unknown workload {w}")
+    stream = torch.cuda.ExternalStream(g.stream())
+    for _ in range(max(args.warmup, 3)):
+        one()
+    torch.cuda.synchronize()
+    times, units = [], 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            units = one()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    t = max_over_ranks(dist, sum(times) / len(times))
+    per = unit_edges * units / t
+    value = per / 1e9 if unit == "GTEPS" else per
+    out = {"metric": metric, "value": value * ws, "unit": unit, "n_gpus": ws,
+           "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "int32 indices", "data": "synthetic",
+           "config": {"workload": w, "scale": args.scale, "n": n, "nnz": nnz},
+           "gpu_launches": int(g.last_stats()["launches"] * args.steps),
+           "clocks": clk.summary()}
+    return out, None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="pagerank",
+                    choices=["pagerank", "bfs", "bfs64", "tc", "sssp", "bc"])
+    ap.add_argument("--scale", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    ws, rank, local = dist_env()
+    dist = maybe_init_dist(ws, local)
+    if args.workload == "pagerank":
+        out, extra = bench_pagerank(args, dist, ws, rank, local)
+    else:
+        out, extra = bench_simple(args, dist, ws, rank, local)
+    if rank == 0:
+        if args.workload == "pagerank" and ws == 1 and not args.no_cpu_baseline:
+            base, extras = cpu_baseline_pagerank(extra[0], 1)
+            out["cpu_baseline"] = base
+            out["cpu_baseline_port"] = extras.get("port")
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -6,7 +6,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgbx.so")
+LIB_PATH = os.environ.get("GBX_LIB") or os.path.join(_HERE, "libgbx.so")
 MSG_LEN = 256
 
 _lib = None

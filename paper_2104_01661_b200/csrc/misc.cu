@@ -37,8 +37,7 @@ void result_device(const gbx_graph* g, const std::string& w, void** ptr, int64_t
   *ptr = nullptr;
   *count = 0;
   if (w == "pagerank" && g->pr) {
-    *ptr = g->pr->last_prec == 64 ? static_cast<void*>(g->pr->rd[g->pr->last_iters & 1].p)
-                                  : static_cast<void*>(g->pr->r[g->pr->last_iters & 1].p);
+    *ptr = g->pr->out.p;  // fp64 ranks, original vertex order
     *count = g->A.n;
   } else if (w == "bfs" && g->bfs) {
     *ptr = g->bfs->parent.p;

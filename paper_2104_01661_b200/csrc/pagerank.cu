@@ -1,30 +1,36 @@
-// pagerank.cu -- GAP PageRank (algo/pagerank.cpp:8-81) as one fused pull-SpMV
-// kernel per iteration, looped on the device by a CUDA-graph WHILE node.
+// pagerank.cu -- GAP PageRank (algo/pagerank.cpp:8-81) as a fused pull SpMV,
+// looped on the device by a CUDA-graph WHILE node.
 //
 // Reference per iteration: contrib = prior ./ (deg/damping) (:55-56), rank =
 // teleport (:58), rank += AT plus.second contrib (:59-61), L1 = sum|prior -
-// rank| (:65-73), stop when L1 < tol (:74).  Here one kernel does all of it:
-//   * work is split into merge-path tiles of kPrItems (row-ends + nonzeros) so
-//     every CTA does the same amount of work regardless of the in-degree skew
-//     (R-MAT hubs have 10^5 in-edges);
-//   * a tile stages its AT columns (streamed, evict-first) and the gathered
-//     x = contrib values (read-only path, L2-resident: 4n bytes) in shared
-//     memory, then each thread consumes kPrIpt merge items sequentially, a
-//     block reduce-by-key scan fixes up rows split between threads;
-//   * rows split between tiles are finished by the last tile to arrive
-//     (per-row epoch counter, parts summed in tile order);
-//   * the epilogue is fused: r_new = teleport + sum (fp64), L1 partial
-//     |r_prev - r_new| (fp64), x_next = r_new / (deg / damping) (fp32, 0 for
-//     dangling vertices -- their mass is lost exactly as in the reference);
-//   * the last CTA reduces the per-CTA L1 partials in a fixed order, stores
-//     the iteration count and clears the graph's WHILE condition on
-//     convergence, so the whole run is one graph launch with no host syncs.
-// Algorithmic bytes per iteration: 4*nnz (col) + 4*nnz (gathered
-// x) + 8*(n+1) (row_ptr) + 16*n (read r_prev, read deg, write r, write x).
+// rank| (:65-73), stop when L1 < tol (:74).
+//
+// Device layout (the PageRank plan, built once per graph):
+//   * vertices are relabeled by descending in-degree (stable).  R-MAT in- and
+//     out-degree skews coincide, so the hot contribution entries x[k] gathered
+//     by most edges land in a compact prefix of x that stays L1/L2 resident;
+//   * rows are therefore sorted by length and binned: a row of length in
+//     (G/2, G] is summed by a group of G lanes (G = 1..32, 32/G rows per warp),
+//     rows longer than kPrLong are cut into kPrChunk-nonzero chunks whose
+//     partial sums go to fixed slots -- every warp gets a similar amount of
+//     work and no block barrier sits in the hot loop.
+// Per iteration two kernels run inside the graph body:
+//   k_pr_rows   -- every warp unit: coalesced AT column loads (streamed,
+//                  evict-first), gathered x (read-only path), fp64 sums, and
+//                  the fused epilogue r = teleport + sum, |r_prev - r| (fp64),
+//                  x_next = r / (deg / damping) (0 for dangling vertices --
+//                  their mass is lost exactly as in the reference);
+//   k_pr_finish -- sums the chunk slots of the long rows in order, their
+//                  epilogue, then the last CTA reduces every L1 partial in a
+//                  fixed order, counts the iteration and clears the WHILE
+//                  condition on convergence.  Deterministic end to end.
+// Algorithmic bytes per iteration: (4 + sizeof x) * nnz + 8 * (n+1)
+// + (3 * sizeof x + 4) * n.
 #include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -33,8 +39,16 @@
 namespace gbx {
 
 constexpr int kPrThreads = 256;
-constexpr int kPrIpt = 8;
-constexpr int kPrItems = kPrThreads * kPrIpt;
+#ifndef GBX_PR_MINB
+#define GBX_PR_MINB 6  // resident CTAs per SM the rows kernel is compiled for
+#endif
+constexpr int kPrIpl = 8;          // items per lane: 8 independent gathers in flight
+constexpr int64_t kPrLong = 1024;   // rows longer than this are chunked
+constexpr int64_t kPrShort = 32;    // rows up to this length: thread per row, exact-length bins
+constexpr int64_t kPrChunk = 2048;  // nonzeros per chunk unit
+// default shared-memory hot prefix of x (override: GBX_PR_HOT_KB)
+constexpr int kPrHotKbDefault = 0;
+constexpr unsigned kWarp = 0xffffffffu;
 
 PrPlan::~PrPlan() {
   if (exec) cudaGraphExecDestroy(exec);
@@ -43,300 +57,404 @@ PrPlan::~PrPlan() {
 
 template <typename V>
 struct PrArgs {
-  const int64_t* trp;
+  const int64_t* trp;      // relabeled AT
   const int32_t* tcol;
-  const int32_t* outdeg;   // indexed by global row
-  const int64_t* tile_row;
-  const int64_t* tile_nz;
-  const int32_t* head_split;
-  const int32_t* tail_split;
-  const int32_t* split_first;
-  const int32_t* split_parts;
-  const int64_t* split_row;
-  const int64_t* split_slot;
-  double* split_part;
-  unsigned* split_cnt;
+  const int32_t* outdeg;   // relabeled out-degree
+  const V* inv;            // damping / outdeg (0 for dangling vertices), relabeled
+  const PrBin* bins;       // warp units by bin (staged in shared memory)
+  int nbins;
+  int64_t nunits;
+  const int64_t* chunk_p;  // chunk units: nonzero range [p0, p1) -> slot
+  int64_t nchunks;
+  const int32_t* long_row;     // rows finished by k_pr_finish
+  const int64_t* long_slot;    // [nlong+1] slot ranges
+  int64_t nlong;
+  double* slot;
   V* r0;
   V* r1;
-  V* x0;   // x0/x1: contribution vectors indexed by global vertex
+  V* x0;
   V* x1;
-  double* l1_block;
+  double* l1_rows;     // [gridA] per-CTA partials of k_pr_rows
+  double* l1_fin;      // [gridB]
   double* l1_hist;
-  int* ctl;
-  unsigned* blk_cnt;
-  int64_t ntiles;
-  int64_t out_base;   // output row r is stored at r - out_base
+  int* ctl;            // [0] completed iterations [1] done
+  unsigned* fin_cnt;
+  int64_t hot;         // x[0, hot) is staged in shared memory by k_pr_rows
+  int64_t l1hot;       // x[hot, l1hot) gathered with L1 evict_last, the rest no_allocate
+  int64_t row0;        // first row of this plan (shards); outputs indexed row - row0
+  int grid_rows;
   double damping, teleport, tol;
   int itermax;
-  int fixed;          // 1: single step, r0/x0 are inputs, r1/x1 outputs
+  int fixed;           // single step: r0/x0 inputs, r1/x1 outputs, no convergence
   cudaGraphConditionalHandle cond;
 };
 
-struct KeyVal {
-  int key;
-  double val;
-};
-struct ReduceBySeg {
-  __device__ __forceinline__ KeyVal operator()(const KeyVal& a, const KeyVal& b) const {
-    KeyVal r;
-    r.key = b.key;
-    r.val = (a.key == b.key) ? a.val + b.val : b.val;
-    return r;
-  }
-};
-
 template <typename V>
-__device__ __forceinline__ double pr_epilogue(const PrArgs<V>& a, const V* r_cur, V* r_nxt,
-                                              V* x_nxt, int64_t row, double s) {
-  double rn = a.teleport + s;
-  int64_t o = row - a.out_base;
-  double d = fabs(static_cast<double>(r_cur[o]) - rn);
-  r_nxt[o] = static_cast<V>(rn);
-  int dg = a.outdeg[row];
-  x_nxt[row] = dg > 0 ? static_cast<V>(rn / (static_cast<double>(dg) / a.damping)) : V(0);
-  return d;
+__device__ __forceinline__ void pr_buffers(const PrArgs<V>& a, int k, const V*& x_cur,
+                                           const V*& r_cur, V*& x_nxt, V*& r_nxt) {
+  const bool odd = !a.fixed && (k & 1);
+  x_cur = odd ? a.x1 : a.x0;
+  r_cur = odd ? a.r1 : a.r0;
+  x_nxt = odd ? a.x0 : a.x1;
+  r_nxt = odd ? a.r0 : a.r1;
 }
 
-// One part of a row split between tiles; the last part to arrive finishes it.
+// Cache-policy loads (PTX): the AT column stream is read once -> no L1
+// allocation, evict-first in L2; gathers of the hot prefix of x (the highest-
+// degree vertices after relabeling, ~58% of all gathers on R-MAT in the first
+// 48K ids) are kept in L1 (evict_last); cold gathers bypass L1 so they do not
+// evict the hot lines.
+__device__ __forceinline__ int ld_stream(const int32_t* p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_hot(const float* p) {
+  float v;
+  asm("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_hot(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_cold(const float* p) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_cold(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// gather x[c]: optional shared-memory prefix [0, hot), L1-resident prefix
+// [hot, l1hot), the rest from L2 without L1 allocation
 template <typename V>
-__device__ __forceinline__ double pr_split_part(const PrArgs<V>& a, const V* r_cur,
-                                                V* r_nxt, V* x_nxt, int id, int64_t t,
-                                                double v, unsigned epoch) {
-  int64_t base = a.split_slot[id];
-  int parts = a.split_parts[id];
-  a.split_part[base + (t - a.split_first[id])] = v;
-  __threadfence();
-  unsigned prev = atomicAdd(&a.split_cnt[id], 1u);
-  if (prev == epoch * static_cast<unsigned>(parts) - 1u) {
-    __threadfence();
+__device__ __forceinline__ V pr_x(const V* s_x, int64_t hot, const V* x, int c) {
+  return c < hot ? s_x[c] : ld_hot(x + c);
+}
+template <typename V>
+__device__ __forceinline__ V pr_xg(const V* s_x, int64_t hot, int64_t l1hot, const V* x, int c) {
+  if (c < hot) return s_x[c];
+  return c < l1hot ? ld_hot(x + c) : ld_cold(x + c);
+}
+
+// fused epilogue of one row with prefetched r_prev / out-degree
+template <typename V>
+__device__ __forceinline__ double pr_finish_row(const PrArgs<V>& a, V* r_nxt, V* x_nxt,
+                                                int64_t row, double s, V rprev, V inv) {
+  const double rn = a.teleport + s;
+  r_nxt[row - a.row0] = static_cast<V>(rn);
+  x_nxt[row] = static_cast<V>(rn * static_cast<double>(inv));
+  return fabs(static_cast<double>(rprev) - rn);
+}
+
+template <typename V>
+__global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_rows(PrArgs<V> a) {
+  using BlockReduce = cub::BlockReduce<double, kPrThreads>;
+  __shared__ typename BlockReduce::TempStorage red;
+  __shared__ PrBin s_bins[kPrBinsMax];
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  V* s_x = reinterpret_cast<V*>(s_raw);
+  if (!a.fixed && *(volatile int*)&a.ctl[1]) return;  // converged (host-looped path)
+  const int k = *(volatile int*)&a.ctl[0];
+  const V *x_cur, *r_cur;
+  V *x_nxt, *r_nxt;
+  pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
+  for (int64_t i = threadIdx.x; i < a.hot; i += blockDim.x) s_x[i] = x_cur[i];
+  for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_bins[i] = a.bins[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  double l1 = 0.0;
+  // 1) long-row chunks: 32 lanes, kPrIpl independent gathers in flight per lane
+  for (int64_t u = gwarp; u < a.nchunks; u += nwarps) {
+    const int64_t p0 = a.chunk_p[2 * u], p1 = a.chunk_p[2 * u + 1];
     double s = 0.0;
-    for (int q = 0; q < parts; ++q) s += __ldcg(&a.split_part[base + q]);
-    return pr_epilogue(a, r_cur, r_nxt, x_nxt, a.split_row[id], s);
+    for (int64_t base = p0 + lane; base < p1; base += 32 * kPrIpl) {
+      int c[kPrIpl];
+#pragma unroll
+      for (int j = 0; j < kPrIpl; ++j) {
+        const int64_t p = base + 32 * j;
+        c[j] = p < p1 ? ld_stream(a.tcol + p) : -1;
+      }
+#pragma unroll
+      for (int j = 0; j < kPrIpl; ++j)
+        if (c[j] >= 0) s += static_cast<double>(pr_xg(s_x, a.hot, a.l1hot, x_cur, c[j]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
+    if (lane == 0) a.slot[u] = s;
   }
-  return 0.0;
+  // 2) warp units in bin order.  Bin 0: rows kPrShort < len <= kPrLong, one
+  //    warp per row through row_ptr.  Bins 1..: rows of one exact length L <=
+  //    kPrShort, 32 rows per unit, thread per row, nonzeros at p0 + i*L and a
+  //    warp-uniform L-trip loop.  The grid-stride walk visits units in
+  //    increasing order, so the bin cursor only moves forward.
+  int bk = 0;
+  for (int64_t u = gwarp; u < a.nunits; u += nwarps) {
+    while (bk + 1 < a.nbins && u >= s_bins[bk + 1].unit0) ++bk;
+    const PrBin& B = s_bins[bk];
+    if (B.len < 0) {
+      const int64_t row = B.row0 + (u - B.unit0);
+      const int64_t b = a.trp[row], e = a.trp[row + 1];
+      const V rprev = r_cur[row - a.row0];
+      const V inv = a.inv[row];
+      double s = 0.0;
+      for (int64_t base = b + lane; base < e; base += 32 * 4) {
+        int c[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[q] = base + 32 * q < e ? ld_stream(a.tcol + base + 32 * q) : -1;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (c[q] >= 0) s += static_cast<double>(pr_xg(s_x, a.hot, a.l1hot, x_cur, c[q]));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
+      if (lane == 0) l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, rprev, inv);
+    } else {
+      const int64_t i = (u - B.unit0) * 32 + lane;
+      const int64_t row = B.row0 + i;
+      if (row < B.row1) {
+        const V rprev = r_cur[row - a.row0];
+        const V inv = a.inv[row];
+        const int L = B.len;
+        const int32_t* cp = a.tcol + B.p0 + i * L;
+        double s = 0.0;
+        int j = 0;
+        for (; j + 4 <= L; j += 4) {
+          const int c0 = ld_stream(cp + j), c1 = ld_stream(cp + j + 1);
+          const int c2 = ld_stream(cp + j + 2), c3 = ld_stream(cp + j + 3);
+          const V t0 = pr_xg(s_x, a.hot, a.l1hot, x_cur, c0), t1 = pr_xg(s_x, a.hot, a.l1hot, x_cur, c1);
+          const V t2 = pr_xg(s_x, a.hot, a.l1hot, x_cur, c2), t3 = pr_xg(s_x, a.hot, a.l1hot, x_cur, c3);
+          s += (static_cast<double>(t0) + static_cast<double>(t1)) +
+               (static_cast<double>(t2) + static_cast<double>(t3));
+        }
+        for (; j < L; ++j) s += static_cast<double>(pr_xg(s_x, a.hot, a.l1hot, x_cur, ld_stream(cp + j)));
+        l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, rprev, inv);
+      }
+    }
+  }
+  const double blk = BlockReduce(red).Sum(l1);
+  if (threadIdx.x == 0) a.l1_rows[blockIdx.x] = blk;
 }
 
 template <typename V, bool kGraph>
-__global__ void __launch_bounds__(kPrThreads) k_pr_iter(PrArgs<V> a) {
-  using BlockScan = cub::BlockScan<KeyVal, kPrThreads>;
+__global__ void __launch_bounds__(kPrThreads) k_pr_finish(PrArgs<V> a) {
   using BlockReduce = cub::BlockReduce<double, kPrThreads>;
-  __shared__ int s_rowend[kPrItems];
-  __shared__ V s_val[kPrItems];
-  __shared__ double s_sum[kPrItems];
-  __shared__ union {
-    typename BlockScan::TempStorage scan;
-    typename BlockReduce::TempStorage red;
-  } tmp;
+  __shared__ typename BlockReduce::TempStorage red;
   __shared__ int s_last;
-
-  if (!a.fixed && *(volatile int*)&a.ctl[1]) return;  // converged (host-looped path)
+  if (!a.fixed && *(volatile int*)&a.ctl[1]) return;
   const int k = *(volatile int*)&a.ctl[0];
   const unsigned epoch = static_cast<unsigned>(k) + 1u;
-  const bool odd = !a.fixed && (k & 1);
-  const V* x_cur = odd ? a.x1 : a.x0;
-  const V* r_cur = odd ? a.r1 : a.r0;
-  V* x_nxt = odd ? a.x0 : a.x1;
-  V* r_nxt = odd ? a.r0 : a.r1;
-  const int tid = threadIdx.x;
+  const V *x_cur, *r_cur;
+  V *x_nxt, *r_nxt;
+  pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
   double l1 = 0.0;
-
-  for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-    const int64_t rs = a.tile_row[t], js = a.tile_nz[t];
-    const int nrows = static_cast<int>(a.tile_row[t + 1] - rs);
-    const int nnz = static_cast<int>(a.tile_nz[t + 1] - js);
-    // ---- stage: row ends (local offsets) and gathered contributions
-    {
-      int c[kPrIpt];
-#pragma unroll
-      for (int q = 0; q < kPrIpt; ++q) {
-        int i = tid + q * kPrThreads;
-        c[q] = i < nnz ? __ldcs(a.tcol + js + i) : -1;
-      }
-#pragma unroll
-      for (int q = 0; q < kPrIpt; ++q) {
-        int i = tid + q * kPrThreads;
-        if (i < nrows) s_rowend[i] = static_cast<int>(a.trp[rs + 1 + i] - js);
-      }
-#pragma unroll
-      for (int q = 0; q < kPrIpt; ++q) {
-        int i = tid + q * kPrThreads;
-        if (c[q] >= 0) s_val[i] = __ldg(x_cur + c[q]);
-      }
-    }
-    __syncthreads();
-    // ---- merge-path consume
-    const int total = nrows + nnz;
-    const int diag = min(tid * kPrIpt, total);
-    int lo = max(diag - nnz, 0), hi = min(diag, nrows);
-    while (lo < hi) {
-      int piv = (lo + hi) >> 1;
-      if (s_rowend[piv] <= diag - piv - 1) lo = piv + 1; else hi = piv;
-    }
-    int x = lo, y = diag - lo;
-    const int dend = min(diag + kPrIpt, total);
-    double sum = 0.0, first_val = 0.0;
-    int first_row = -1;
-    for (int it = diag; it < dend; ++it) {
-      if (x < nrows && s_rowend[x] <= y) {
-        if (first_row < 0) { first_row = x; first_val = sum; } else { s_sum[x] = sum; }
-        sum = 0.0;
-        ++x;
-      } else {
-        sum += static_cast<double>(s_val[y]);
-        ++y;
-      }
-    }
-    KeyVal in{x, sum}, pre, agg;
-    BlockScan(tmp.scan).ExclusiveScan(in, pre, KeyVal{-1, 0.0}, ReduceBySeg(), agg);
-    if (first_row >= 0) s_sum[first_row] = first_val + (pre.key == first_row ? pre.val : 0.0);
-    __syncthreads();
-    // ---- fused epilogue over the rows completed in this tile
-    const int hs = a.head_split[t];
-    for (int i = tid; i < nrows; i += kPrThreads) {
-      double s = s_sum[i];
-      if (i == 0 && hs >= 0) {
-        l1 += pr_split_part(a, r_cur, r_nxt, x_nxt, hs, t, s, epoch);
-      } else {
-        l1 += pr_epilogue(a, r_cur, r_nxt, x_nxt, rs + i, s);
-      }
-    }
-    if (tid == 0) {
-      const int ts = a.tail_split[t];
-      if (ts >= 0) l1 += pr_split_part(a, r_cur, r_nxt, x_nxt, ts, t, agg.val, epoch);
-    }
-    __syncthreads();
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.nlong;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int64_t q = a.long_slot[i]; q < a.long_slot[i + 1]; ++q) s += a.slot[q];
+    const int64_t row = a.long_row[i];
+    l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, r_cur[row - a.row0], a.inv[row]);
   }
-  // ---- L1: per-CTA partial, the last CTA reduces in a fixed order
-  double blk = BlockReduce(tmp.red).Sum(l1);
-  if (tid == 0) {
-    a.l1_block[blockIdx.x] = blk;
+  double blk = BlockReduce(red).Sum(l1);
+  if (threadIdx.x == 0) {
+    a.l1_fin[blockIdx.x] = blk;
     __threadfence();
-    unsigned prev = atomicAdd(a.blk_cnt, 1u);
-    s_last = (prev == epoch * gridDim.x - 1u) ? 1 : 0;
+    const unsigned prev = atomicAdd(a.fin_cnt, 1u);
+    s_last = prev == epoch * gridDim.x - 1u;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
   double part = 0.0;
-  for (int b = tid; b < static_cast<int>(gridDim.x); b += kPrThreads) part += __ldcg(&a.l1_block[b]);
-  double tot = BlockReduce(tmp.red).Sum(part);
-  if (tid == 0) {
-    a.l1_hist[k] = tot;
+  for (int b = threadIdx.x; b < a.grid_rows; b += kPrThreads) part += __ldcg(&a.l1_rows[b]);
+  for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += kPrThreads)
+    part += __ldcg(&a.l1_fin[b]);
+  __syncthreads();
+  const double tot = BlockReduce(red).Sum(part);
+  if (threadIdx.x == 0) {
+    a.l1_hist[k % 128] = tot;
     a.ctl[0] = k + 1;
-    bool stop = a.fixed || !(tot >= a.tol) || (k + 1 >= a.itermax);
+    const bool stop = a.fixed || !(tot >= a.tol) || (k + 1 >= a.itermax);
     if (stop) a.ctl[1] = 1;
     if constexpr (kGraph) cudaGraphSetConditional(a.cond, stop ? 0u : 1u);
   }
 }
 
-template <typename V>
-__global__ void k_pr_init(V* r, V* x, const int32_t* outdeg, int64_t n, double damping) {
-  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  double r0 = 1.0 / static_cast<double>(n);
-  r[i] = static_cast<V>(r0);
-  int dg = outdeg[i];
-  x[i] = dg > 0 ? static_cast<V>(r0 / (static_cast<double>(dg) / damping)) : V(0);
+__global__ void k_pr_inv(float* inv, const int32_t* outdeg, int64_t n, double damping) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) inv[i] = outdeg[i] > 0 ? static_cast<float>(damping / static_cast<double>(outdeg[i])) : 0.f;
 }
 
-// ---- plan construction (host; once per graph) -------------------------------
+template <typename V>
+__global__ void k_pr_init(V* r, V* x, V* inv, const int32_t* outdeg, int64_t n, double damping) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double r0 = 1.0 / static_cast<double>(n);
+  r[i] = static_cast<V>(r0);
+  const int dg = outdeg[i];
+  // contrib = prior ./ (deg / damping) (pagerank.cpp:30-40, 55-56); the
+  // iterations use the precomputed damping / deg (0: dangling, mass lost)
+  x[i] = dg > 0 ? static_cast<V>(r0 / (static_cast<double>(dg) / damping)) : V(0);
+  inv[i] = dg > 0 ? static_cast<V>(damping / static_cast<double>(dg)) : V(0);
+}
 
-static void build_tiles(cudaStream_t s, PrPlan& P, const std::vector<int64_t>& trp) {
-  const int64_t row0 = P.row0, row1 = P.row1;
-  const int64_t nrows = row1 - row0;
-  const int64_t nz0 = trp[row0], nz1 = trp[row1];
-  const int64_t nnz = nz1 - nz0;
-  const int64_t total = nrows + nnz;
-  const int64_t ntiles = std::max<int64_t>(1, (total + kPrItems - 1) / kPrItems);
-  std::vector<int64_t> trow(ntiles + 1), tnz(ntiles + 1);
-  for (int64_t t = 0; t <= ntiles; ++t) {
-    int64_t d = std::min(t * kPrItems, total);
-    // merge path over row ends a[i] = trp[row0+i+1]-nz0 and nonzeros b[j] = j
-    int64_t lo = std::max<int64_t>(d - nnz, 0), hi = std::min(d, nrows);
-    while (lo < hi) {
-      int64_t piv = (lo + hi) >> 1;
-      if (trp[row0 + piv + 1] - nz0 <= d - piv - 1) lo = piv + 1; else hi = piv;
+// relabeled rank -> original ids (fp64 for the host copy)
+template <typename V>
+__global__ void k_pr_unpermute(const V* r, const int32_t* new2old, int64_t n, double* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[new2old[i]] = static_cast<double>(r[i]);
+}
+
+// ---- plan -------------------------------------------------------------------------
+
+__global__ void k_neg_len(const int64_t* rp, int64_t n, int32_t* key) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) key[i] = static_cast<int32_t>(rp[i + 1] - rp[i]);
+}
+__global__ void k_inverse_perm(const int32_t* new2old, int64_t n, int32_t* old2new) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) old2new[new2old[i]] = static_cast<int32_t>(i);
+}
+__global__ void k_relabel_keys(const int32_t* rowid, const int32_t* col, const int32_t* old2new,
+                               int64_t nnz, int bits, uint64_t* keys) {
+  const int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p < nnz)
+    keys[p] = (static_cast<uint64_t>(old2new[rowid[p]]) << bits) |
+              static_cast<uint64_t>(old2new[col[p]]);
+}
+__global__ void k_gather_i32(const int32_t* src, const int32_t* idx, int64_t n, int32_t* dst) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+// work units over relabeled rows [row0, row1) (lengths non-increasing): long
+// rows become chunk units; rows up to kPrLong are binned by G = lanes per row
+// (G*kPrIpl >= length); rows up to kPrShort get one bin per distinct length so
+// the kernel computes their nonzero offsets instead of loading row_ptr.
+static void build_units(PrPlan& P, const std::vector<int64_t>& rp, int64_t row0, int64_t row1,
+                        cudaStream_t s) {
+  std::vector<int64_t> chunks, lslot;
+  std::vector<int32_t> lrow;
+  int64_t r = row0;
+  while (r < row1 && rp[r + 1] - rp[r] > kPrLong) {
+    lrow.push_back(static_cast<int32_t>(r));
+    lslot.push_back(static_cast<int64_t>(chunks.size() / 2));
+    for (int64_t p = rp[r]; p < rp[r + 1]; p += kPrChunk) {
+      chunks.push_back(p);
+      chunks.push_back(std::min(rp[r + 1], p + kPrChunk));
     }
-    trow[t] = row0 + lo;
-    tnz[t] = nz0 + (d - lo);
+    ++r;
   }
-  std::vector<int32_t> head(ntiles, -1), tail(ntiles, -1), sfirst, sparts;
-  std::vector<int64_t> srow, sslot;
-  int64_t slots = 0;
-  for (int64_t t = 0; t < ntiles; ++t) {
-    int64_t rs = trow[t], js = tnz[t];
-    if (rs < row1 && js > trp[rs]) head[t] = static_cast<int32_t>(srow.size()) - 1;
-    int64_t re = trow[t + 1], je = tnz[t + 1];
-    if (re < row1 && je > trp[re]) {
-      if (head[t] >= 0 && srow.back() == re) {
-        tail[t] = head[t];
-      } else {
-        tail[t] = static_cast<int32_t>(srow.size());
-        srow.push_back(re);
-        sfirst.push_back(static_cast<int32_t>(t));
-        sparts.push_back(0);
-        sslot.push_back(0);
-      }
-    }
+  lslot.push_back(static_cast<int64_t>(chunks.size() / 2));
+  std::vector<PrBin> bins;
+  int64_t units = 0;
+  {
+    // bin 0: kPrShort < len <= kPrLong, one warp (unit) per row
+    int64_t r1 = r;
+    while (r1 < row1 && rp[r1 + 1] - rp[r1] > kPrShort) ++r1;
+    PrBin b{};
+    b.unit0 = units;
+    b.row0 = r;
+    b.row1 = r1;
+    b.p0 = rp[r];
+    b.len = -1;
+    bins.push_back(b);
+    units += r1 - r;
+    r = r1;
   }
-  // parts = last tile containing the row end - first tile + 1
-  for (int64_t t = 0; t < ntiles; ++t) {
-    if (head[t] >= 0 && trow[t + 1] > trow[t]) {
-      int id = head[t];
-      sparts[id] = static_cast<int32_t>(t - sfirst[id] + 1);
-    }
+  // bins 1..: one per exact length (non-increasing), 32 rows per unit
+  while (r < row1) {
+    const int64_t len = rp[r + 1] - rp[r];
+    int64_t r1 = r;
+    while (r1 < row1 && rp[r1 + 1] - rp[r1] == len) ++r1;
+    PrBin b{};
+    b.unit0 = units;
+    b.row0 = r;
+    b.row1 = r1;
+    b.p0 = rp[r];
+    b.len = static_cast<int32_t>(len);
+    bins.push_back(b);
+    units += (r1 - r + 31) / 32;
+    r = r1;
   }
-  for (size_t id = 0; id < srow.size(); ++id) {
-    sslot[id] = slots;
-    slots += sparts[id];
-  }
-  P.ntiles = ntiles;
-  P.nsplit = static_cast<int64_t>(srow.size());
-  P.tile_row.alloc(ntiles + 1);
-  P.tile_nz.alloc(ntiles + 1);
-  P.head_split.alloc(ntiles);
-  P.tail_split.alloc(ntiles);
-  size_t ns = std::max<size_t>(srow.size(), 1);
-  P.split_first.alloc(ns);
-  P.split_parts.alloc(ns);
-  P.split_row.alloc(ns);
-  P.split_slot.alloc(ns);
-  P.split_part.alloc(std::max<int64_t>(slots, 1));
-  P.split_cnt.alloc(ns);
-  GBX_CUDA(cudaMemcpyAsync(P.tile_row.p, trow.data(), (ntiles + 1) * 8, cudaMemcpyHostToDevice, s));
-  GBX_CUDA(cudaMemcpyAsync(P.tile_nz.p, tnz.data(), (ntiles + 1) * 8, cudaMemcpyHostToDevice, s));
-  GBX_CUDA(cudaMemcpyAsync(P.head_split.p, head.data(), ntiles * 4, cudaMemcpyHostToDevice, s));
-  GBX_CUDA(cudaMemcpyAsync(P.tail_split.p, tail.data(), ntiles * 4, cudaMemcpyHostToDevice, s));
-  if (!srow.empty()) {
-    GBX_CUDA(cudaMemcpyAsync(P.split_first.p, sfirst.data(), srow.size() * 4, cudaMemcpyHostToDevice, s));
-    GBX_CUDA(cudaMemcpyAsync(P.split_parts.p, sparts.data(), srow.size() * 4, cudaMemcpyHostToDevice, s));
-    GBX_CUDA(cudaMemcpyAsync(P.split_row.p, srow.data(), srow.size() * 8, cudaMemcpyHostToDevice, s));
-    GBX_CUDA(cudaMemcpyAsync(P.split_slot.p, sslot.data(), srow.size() * 8, cudaMemcpyHostToDevice, s));
-  }
+  if (bins.size() > static_cast<size_t>(kPrBinsMax)) fail(GBX_CUDA_ERROR, "pagerank: too many bins");
+  P.nbins = static_cast<int>(bins.size());
+  P.bins.alloc(std::max<size_t>(bins.size(), 1));
+  if (!bins.empty())
+    GBX_CUDA(cudaMemcpyAsync(P.bins.p, bins.data(), bins.size() * sizeof(PrBin),
+                             cudaMemcpyHostToDevice, s));
+  P.nunits = units;
+  P.nchunks = static_cast<int64_t>(chunks.size() / 2);
+  P.nlong = static_cast<int64_t>(lrow.size());
+  P.chunk_p.alloc(std::max<int64_t>(2 * P.nchunks, 2));
+  P.long_row.alloc(std::max<int64_t>(P.nlong, 1));
+  P.long_slot.alloc(P.nlong + 1);
+  P.slot.alloc(std::max<int64_t>(P.nchunks, 1));
+  if (P.nchunks)
+    GBX_CUDA(cudaMemcpyAsync(P.chunk_p.p, chunks.data(), chunks.size() * 8, cudaMemcpyHostToDevice, s));
+  if (P.nlong)
+    GBX_CUDA(cudaMemcpyAsync(P.long_row.p, lrow.data(), lrow.size() * 4, cudaMemcpyHostToDevice, s));
+  GBX_CUDA(cudaMemcpyAsync(P.long_slot.p, lslot.data(), lslot.size() * 8, cudaMemcpyHostToDevice, s));
   GBX_CUDA(cudaStreamSynchronize(s));
 }
 
-static int pr_grid(int64_t ntiles) {
-  int per_sm = 0;
-  GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_iter<double, true>, kPrThreads, 0));
-  per_sm = std::max(per_sm, 1);
-  int64_t g = static_cast<int64_t>(device_sms()) * per_sm;
-  return static_cast<int>(std::min<int64_t>(g, ntiles));
+// relabeled AT (rows by descending in-degree) + relabeled out-degree
+static void build_relabeled(gbx_graph* g, PrPlan& P) {
+  const Csr& AT = g->AT();
+  cudaStream_t s = g->stream;
+  const int64_t n = AT.n, nnz = AT.nnz;
+  P.n = n;
+  P.nnz = nnz;
+  DevArray<int32_t> len(std::max<int64_t>(n, 1));
+  if (n) {
+    k_neg_len<<<ceil_div(n, 256), 256, 0, s>>>(AT.rp.p, n, len.p);
+    GBX_LAUNCHED();
+  }
+  sort_ids_by_key(s, len.p, n, false, P.new2old);
+  P.old2new.alloc(std::max<int64_t>(n, 1));
+  P.deg.alloc(std::max<int64_t>(n, 1));
+  if (n) {
+    k_inverse_perm<<<ceil_div(n, 256), 256, 0, s>>>(P.new2old.p, n, P.old2new.p);
+    k_gather_i32<<<ceil_div(n, 256), 256, 0, s>>>(g->rowdeg.p, P.new2old.p, n, P.deg.p);
+    GBX_LAUNCHED();
+  }
+  const int bits = bits_for(std::max<int64_t>(n, 2));
+  if (nnz) {
+    DevArray<int32_t> rowid;
+    expand_rows(s, AT, rowid);
+    DevArray<uint64_t> k0(nnz), k1(nnz);
+    k_relabel_keys<<<ceil_div(nnz, 256), 256, 0, s>>>(rowid.p, AT.col.p, P.old2new.p, nnz, bits,
+                                                        k0.p);
+    GBX_LAUNCHED();
+    rowid.release();
+    uint64_t* sorted = sort_keys(s, k0.p, k1.p, nnz, 2 * bits);
+    csr_from_sorted_keys(s, n, bits, sorted, nnz, P.trp, P.tcol);
+  } else {
+    csr_from_sorted_keys(s, n, bits, nullptr, 0, P.trp, P.tcol);
+  }
+  GBX_CUDA(cudaStreamSynchronize(s));
 }
 
 static void plan_rows(gbx_graph* g, PrPlan& P, int64_t row0, int64_t row1) {
-  const Csr& AT = g->AT();
   cudaStream_t s = g->stream;
-  P.n = AT.n;
-  P.nnz = AT.nnz;
+  std::vector<int64_t> rp(P.n + 1);
+  GBX_CUDA(cudaMemcpyAsync(rp.data(), P.trp.p, (P.n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
   P.row0 = row0;
   P.row1 = row1;
-  std::vector<int64_t> trp(AT.n + 1);
-  GBX_CUDA(cudaMemcpyAsync(trp.data(), AT.rp.p, (AT.n + 1) * 8, cudaMemcpyDeviceToHost, s));
-  GBX_CUDA(cudaStreamSynchronize(s));
-  build_tiles(s, P, trp);
-  P.grid = pr_grid(P.ntiles);
-  P.l1_block.alloc(P.grid);
+  build_units(P, rp, row0, row1, s);
+  P.grid = 0;  // set per precision by rows_grid() (depends on the shared-memory footprint)
+  P.grid_fin = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
+      (P.nlong + kPrThreads - 1) / kPrThreads, device_sms())));
+  P.l1_block.alloc(static_cast<size_t>(device_sms()) * 32);
+  P.l1_fin.alloc(P.grid_fin);
   P.l1_hist.alloc(128);
   P.ctl.alloc(2);
   P.blk_cnt.alloc(1);
@@ -347,11 +465,13 @@ void pagerank_prepare(gbx_graph* g) {
   require_rowdeg(g, "pagerank_gap");
   if (g->pr) return;
   auto P = std::make_unique<PrPlan>();
-  plan_rows(g, *P, 0, g->A.n);
+  build_relabeled(g, *P);
+  plan_rows(g, *P, 0, P->n);
   for (int b = 0; b < 2; ++b) {
     P->r[b].alloc(std::max<int64_t>(g->A.n, 1));
     P->x[b].alloc(std::max<int64_t>(g->A.n, 1));
   }
+  P->out.alloc(std::max<int64_t>(g->A.n, 1));
   g->pr = std::move(P);
 }
 
@@ -371,36 +491,95 @@ template <> double* buf_x<double>(PrPlan& P, int b) {
   if (!P.xd[b].p) P.xd[b].alloc(P.x[b].n);
   return P.xd[b].p;
 }
+template <typename V> V* buf_inv(PrPlan& P);
+template <> float* buf_inv<float>(PrPlan& P) {
+  if (!P.invf.p) P.invf.alloc(P.r[0].n);
+  return P.invf.p;
+}
+template <> double* buf_inv<double>(PrPlan& P) {
+  if (!P.invd.p) P.invd.alloc(P.r[0].n);
+  return P.invd.p;
+}
+
+static int64_t hot_bytes() {
+  static const int64_t hb = [] {
+    const char* e = std::getenv("GBX_PR_HOT_KB");
+    return static_cast<int64_t>(e ? std::atoi(e) : kPrHotKbDefault) * 1024;
+  }();
+  return hb;
+}
+
+// bytes of x kept L1-resident (override: GBX_PR_L1_KB)
+static int64_t l1_hot_bytes() {
+  static const int64_t hb = [] {
+    const char* e = std::getenv("GBX_PR_L1_KB");
+    return static_cast<int64_t>(e ? std::atoi(e) : 160) * 1024;
+  }();
+  return hb;
+}
 
 template <typename V>
-static PrArgs<V> make_args(gbx_graph* g, PrPlan& P, double damping, double tol, int itermax) {
-  const Csr& AT = g->AT();
+static size_t rows_smem(const PrArgs<V>& a) {
+  static bool attr = false;
+  if (!attr) {
+    const int mx = static_cast<int>(std::min<int64_t>(hot_bytes(), 200 * 1024));
+    GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  std::max(mx, 1)));
+    GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  std::max(mx, 1)));
+    // (measured: the default carveout is best; GBX_PR_CARVEOUT overrides)
+    if (const char* cv = std::getenv("GBX_PR_CARVEOUT")) {
+      const int carve = std::atoi(cv);
+      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    }
+    attr = true;
+  }
+  return static_cast<size_t>(a.hot) * sizeof(V);
+}
+
+// persistent grid: SMs x resident CTAs for this shared-memory footprint
+template <typename V>
+static int rows_grid(const PrArgs<V>& a) {
+  int per_sm = 0;
+  GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_rows<V>, kPrThreads,
+                                                         rows_smem<V>(a)));
+  return device_sms() * std::max(per_sm, 1);
+}
+
+template <typename V>
+static PrArgs<V> make_args(PrPlan& P, double damping, double tol, int itermax) {
   PrArgs<V> a{};
-  a.trp = AT.rp.p;
-  a.tcol = AT.col.p;
-  a.outdeg = g->rowdeg.p;
-  a.tile_row = P.tile_row.p;
-  a.tile_nz = P.tile_nz.p;
-  a.head_split = P.head_split.p;
-  a.tail_split = P.tail_split.p;
-  a.split_first = P.split_first.p;
-  a.split_parts = P.split_parts.p;
-  a.split_row = P.split_row.p;
-  a.split_slot = P.split_slot.p;
-  a.split_part = P.split_part.p;
-  a.split_cnt = P.split_cnt.p;
+  a.trp = P.trp.p;
+  a.tcol = P.tcol.p;
+  a.outdeg = P.deg.p;
+  if (P.r[0].p) a.inv = buf_inv<V>(P);
+  a.bins = P.bins.p;
+  a.nbins = P.nbins;
+  a.nunits = P.nunits;
+  a.chunk_p = P.chunk_p.p;
+  a.nchunks = P.nchunks;
+  a.long_row = P.long_row.p;
+  a.long_slot = P.long_slot.p;
+  a.nlong = P.nlong;
+  a.slot = P.slot.p;
   if (P.r[0].p) {
     a.r0 = buf_r<V>(P, 0);
     a.r1 = buf_r<V>(P, 1);
     a.x0 = buf_x<V>(P, 0);
     a.x1 = buf_x<V>(P, 1);
   }
-  a.l1_block = P.l1_block.p;
+  a.l1_rows = P.l1_block.p;
+  a.l1_fin = P.l1_fin.p;
   a.l1_hist = P.l1_hist.p;
   a.ctl = P.ctl.p;
-  a.blk_cnt = P.blk_cnt.p;
-  a.ntiles = P.ntiles;
-  a.out_base = 0;
+  a.fin_cnt = P.blk_cnt.p;
+  a.row0 = 0;
+  a.hot = std::min<int64_t>(P.n, hot_bytes() / static_cast<int64_t>(sizeof(V)));
+  a.l1hot = std::min<int64_t>(P.n, l1_hot_bytes() / static_cast<int64_t>(sizeof(V)));
+  a.grid_rows = rows_grid<V>(a);
   a.damping = damping;
   a.teleport = (1.0 - damping) / static_cast<double>(P.n);
   a.tol = tol;
@@ -412,11 +591,10 @@ static PrArgs<V> make_args(gbx_graph* g, PrPlan& P, double damping, double tol, 
 static void reset_state(cudaStream_t s, PrPlan& P) {
   GBX_CUDA(cudaMemsetAsync(P.ctl.p, 0, 2 * sizeof(int), s));
   GBX_CUDA(cudaMemsetAsync(P.blk_cnt.p, 0, sizeof(unsigned), s));
-  GBX_CUDA(cudaMemsetAsync(P.split_cnt.p, 0, P.split_cnt.bytes(), s));
 }
 
 template <typename V>
-static bool build_graph(gbx_graph* g, PrPlan& P, double damping, double tol, int itermax) {
+static bool build_graph(PrPlan& P, double damping, double tol, int itermax) {
   const int prec = sizeof(V) == 8 ? 64 : 32;
   if (P.exec && P.g_damping == damping && P.g_tol == tol && P.g_itermax == itermax &&
       P.g_prec == prec)
@@ -441,18 +619,26 @@ static bool build_graph(gbx_graph* g, PrPlan& P, double damping, double tol, int
     ok = cudaGraphAddNode(&node, graph, nullptr, 0, &cp) == cudaSuccess;
     if (ok) body = cp.conditional.phGraph_out[0];
   }
+  PrArgs<V> a = make_args<V>(P, damping, tol, itermax);
+  a.cond = cond;
+  void* params[] = {&a};
+  cudaGraphNode_t kn_rows = nullptr, kn_fin = nullptr;
   if (ok) {
-    PrArgs<V> a = make_args<V>(g, P, damping, tol, itermax);
-    a.cond = cond;
-    void* params[] = {&a};
     cudaKernelNodeParams kp = {};
-    kp.func = reinterpret_cast<void*>(k_pr_iter<V, true>);
-    kp.gridDim = dim3(P.grid);
+    kp.func = reinterpret_cast<void*>(k_pr_rows<V>);
+    kp.gridDim = dim3(a.grid_rows);
     kp.blockDim = dim3(kPrThreads);
-    kp.sharedMemBytes = 0;
+    kp.sharedMemBytes = static_cast<unsigned>(rows_smem<V>(a));
     kp.kernelParams = params;
-    cudaGraphNode_t kn;
-    ok = cudaGraphAddKernelNode(&kn, body, nullptr, 0, &kp) == cudaSuccess;
+    ok = cudaGraphAddKernelNode(&kn_rows, body, nullptr, 0, &kp) == cudaSuccess;
+  }
+  if (ok) {
+    cudaKernelNodeParams kp = {};
+    kp.func = reinterpret_cast<void*>(k_pr_finish<V, true>);
+    kp.gridDim = dim3(P.grid_fin);
+    kp.blockDim = dim3(kPrThreads);
+    kp.kernelParams = params;
+    ok = cudaGraphAddKernelNode(&kn_fin, body, &kn_rows, 1, &kp) == cudaSuccess;
   }
   if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
   if (!ok) {
@@ -476,19 +662,22 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
   const int64_t n = g->A.n;
   cudaStream_t s = g->stream;
   reset_state(s, P);
-  k_pr_init<V><<<ceil_div(n, 256), 256, 0, s>>>(buf_r<V>(P, 0), buf_x<V>(P, 0), g->rowdeg.p, n,
-                                                damping);
+  k_pr_init<V><<<ceil_div(n, 256), 256, 0, s>>>(buf_r<V>(P, 0), buf_x<V>(P, 0), buf_inv<V>(P),
+                                                P.deg.p, n, damping);
   GBX_LAUNCHED();
-  if (build_graph<V>(g, P, damping, tol, itermax)) {
+  // GBX_PR_NO_GRAPH=1 forces the host-looped path (ncu cannot profile kernel
+  // nodes of a graph that holds conditional nodes)
+  static const bool no_graph = std::getenv("GBX_PR_NO_GRAPH") != nullptr;
+  if (!no_graph && build_graph<V>(P, damping, tol, itermax)) {
     GBX_CUDA(cudaGraphLaunch(P.exec, s));
   } else {
-    // host-looped fallback: chunks of launches, each exits early once done
-    PrArgs<V> a = make_args<V>(g, P, damping, tol, itermax);
+    PrArgs<V> a = make_args<V>(P, damping, tol, itermax);
     int done = 0, launched = 0;
     while (!done && launched < itermax) {
-      int chunk = std::min(4, itermax - launched);
+      const int chunk = std::min(4, itermax - launched);
       for (int c = 0; c < chunk; ++c) {
-        k_pr_iter<V, false><<<P.grid, kPrThreads, 0, s>>>(a);
+        k_pr_rows<V><<<a.grid_rows, kPrThreads, rows_smem<V>(a), s>>>(a);
+        k_pr_finish<V, false><<<P.grid_fin, kPrThreads, 0, s>>>(a);
         GBX_LAUNCHED();
       }
       launched += chunk;
@@ -497,18 +686,17 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
     }
   }
   int it = 0;
-  if (rank != nullptr || iters != nullptr) {
-    GBX_CUDA(cudaMemcpyAsync(&it, P.ctl.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaMemcpyAsync(&it, P.ctl.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  P.last_iters = it;
+  if (iters) *iters = it;
+  // ranks back in original vertex order (device-resident result; fp64)
+  k_pr_unpermute<V><<<ceil_div(n, 256), 256, 0, s>>>(buf_r<V>(P, it & 1), P.new2old.p, n,
+                                                       P.out.p);
+  GBX_LAUNCHED();
+  if (rank) {
+    GBX_CUDA(cudaMemcpyAsync(rank, P.out.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     GBX_CUDA(cudaStreamSynchronize(s));
-    P.last_iters = it;
-    if (iters) *iters = it;
-    if (rank) {
-      std::vector<V> r(n);
-      GBX_CUDA(cudaMemcpyAsync(r.data(), buf_r<V>(P, it & 1), n * sizeof(V),
-                               cudaMemcpyDeviceToHost, s));
-      GBX_CUDA(cudaStreamSynchronize(s));
-      for (int64_t i = 0; i < n; ++i) rank[i] = r[i];
-    }
   }
   return it;
 }
@@ -531,25 +719,28 @@ void pagerank_run(gbx_graph* g, double damping, double tol, int itermax, double*
   PrPlan& P = *g->pr;
   const bool f64 = use_fp64(tol);
   P.last_prec = f64 ? 64 : 32;
-  int it = f64 ? pagerank_loop<double>(g, P, damping, tol, itermax, rank, iters)
-               : pagerank_loop<float>(g, P, damping, tol, itermax, rank, iters);
+  const int it = f64 ? pagerank_loop<double>(g, P, damping, tol, itermax, rank, iters)
+                     : pagerank_loop<float>(g, P, damping, tol, itermax, rank, iters);
   const double vb = f64 ? 8.0 : 4.0;
-  g->stats.launches = 1 + it;
+  g->stats.launches = 2 + 2 * it;
   g->stats.hot_launches = it;
   g->stats.iterations = it;
-  g->stats.work_units = g->AT().nnz;
+  g->stats.work_units = P.nnz;
   // col (4) + gathered x (vb) per edge; row_ptr (8) + r_prev, r, x (vb each) + deg (4)
-  g->stats.hot_bytes_per_launch = (4.0 + vb) * static_cast<double>(g->AT().nnz) +
+  g->stats.hot_bytes_per_launch = (4.0 + vb) * static_cast<double>(P.nnz) +
                                   8.0 * static_cast<double>(n + 1) + (3.0 * vb + 4.0) * n;
 }
 
 // ---- sharded step (multi-GPU driver) ----------------------------------------------
+// Shards own contiguous blocks of the RELABELED rows; x vectors are in relabeled
+// ids, so the driver all-gathers x_new slices as they are.
 
 void pr_shard_prepare(gbx_graph* g, int64_t rb, int64_t re) {
   require_at(g, "pr_shard");
   require_rowdeg(g, "pr_shard");
   if (rb < 0 || re > g->A.n || rb > re) fail(GBX_INDEX_OUT_OF_BOUNDS, "pr_shard: bad row range");
   auto S = std::make_unique<PrShard>();
+  build_relabeled(g, S->plan);
   plan_rows(g, S->plan, rb, re);
   g->prs = std::move(S);
 }
@@ -559,17 +750,24 @@ void pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, do
   if (!g->prs) fail(GBX_MISSING_PROPERTY, "pr_shard_step needs gbx_pr_shard_prepare");
   PrPlan& P = g->prs->plan;
   cudaStream_t s = g->stream;
-  PrArgs<float> a = make_args<float>(g, P, damping, 0.0, 1 << 30);
+  PrArgs<float> a = make_args<float>(P, damping, 0.0, 1 << 30);
+  if (!P.invf.p || P.g_damping != damping) {
+    P.invf.alloc(std::max<int64_t>(P.n, 1));
+    k_pr_inv<<<ceil_div(P.n, 256), 256, 0, s>>>(P.invf.p, P.deg.p, P.n, damping);
+    GBX_LAUNCHED();
+    P.g_damping = damping;
+  }
+  a.inv = P.invf.p;
   a.fixed = 1;
   a.x0 = const_cast<float*>(x_full);
-  a.x1 = x_new;       // written at global row ids
-  a.r0 = r;           // r_prev (local rows), overwritten in place by r_new
+  a.x1 = x_new;  // written at relabeled global row ids
+  a.r0 = r;      // r_prev (local rows), overwritten in place by r_new
   a.r1 = r;
-  a.out_base = P.row0;
+  a.row0 = P.row0;
   GBX_CUDA(cudaMemsetAsync(P.ctl.p, 0, 2 * sizeof(int), s));
   GBX_CUDA(cudaMemsetAsync(P.blk_cnt.p, 0, sizeof(unsigned), s));
-  GBX_CUDA(cudaMemsetAsync(P.split_cnt.p, 0, P.split_cnt.bytes(), s));
-  k_pr_iter<float, false><<<P.grid, kPrThreads, 0, s>>>(a);
+  k_pr_rows<float><<<a.grid_rows, kPrThreads, rows_smem<float>(a), s>>>(a);
+  k_pr_finish<float, false><<<P.grid_fin, kPrThreads, 0, s>>>(a);
   GBX_LAUNCHED();
   GBX_CUDA(cudaMemcpyAsync(l1, P.l1_hist.p, sizeof(double), cudaMemcpyDeviceToDevice, s));
   g->prs->steps++;

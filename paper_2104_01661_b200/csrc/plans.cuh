@@ -5,21 +5,40 @@
 
 namespace gbx {
 
-// PageRank pull plan over AT (pagerank.cu): merge-path tiles of
-// kPrItems (row-ends + nonzeros) each, and the rows that straddle tiles.
+// A PageRank work bin: warp units [unit0, next bin's unit0) cover rows
+// [row0, row1), 32/2^lg rows per unit with 2^lg lanes per row.  len >= 0: every
+// row has exactly len nonzeros starting at p0 + (row - row0) * len.
+constexpr int kPrBinsMax = 96;
+struct PrBin {
+  int64_t unit0, row0, row1, p0;
+  int32_t len;
+  int32_t lg;
+};
+
+// PageRank pull plan (pagerank.cu): AT relabeled by descending in-degree,
+// rows binned into warp units (G lanes per row) and long-row chunks.
 struct PrPlan {
-  int64_t n = 0, nnz = 0, row0 = 0, row1 = 0;  // rows [row0,row1) of AT
-  int64_t ntiles = 0, nsplit = 0;
-  int grid = 0;
-  DevArray<int64_t> tile_row, tile_nz;      // [ntiles+1] merge-path coordinates
-  DevArray<int32_t> head_split, tail_split; // [ntiles] split id or -1
-  DevArray<int32_t> split_first, split_parts;
-  DevArray<int64_t> split_row, split_slot;
-  DevArray<double> split_part;
-  DevArray<unsigned> split_cnt;
+  int64_t n = 0, nnz = 0, row0 = 0, row1 = 0;  // rows [row0,row1) of the relabeled AT
+  DevArray<int64_t> trp;           // relabeled AT
+  DevArray<int32_t> tcol;
+  DevArray<int32_t> deg;           // relabeled out-degree
+  DevArray<int32_t> new2old, old2new;
+  DevArray<PrBin> bins;            // warp units by bin
+  int nbins = 0;
+  int64_t nunits = 0;
+  DevArray<int64_t> chunk_p;       // [2 * nchunks] nonzero ranges of long rows
+  int64_t nchunks = 0;
+  DevArray<int32_t> long_row;
+  DevArray<int64_t> long_slot;     // [nlong + 1]
+  int64_t nlong = 0;
+  DevArray<double> slot;           // chunk partial sums
+  int grid = 0, grid_fin = 1;
   DevArray<float> r[2], x[2];      // fp32 storage (tol >= 1e-6)
   DevArray<double> rd[2], xd[2];    // fp64 storage (tight tolerances)
-  DevArray<double> l1_block, l1_hist;
+  DevArray<double> out;            // ranks in original vertex order
+  DevArray<float> invf;            // damping / out-degree (fp32 storage)
+  DevArray<double> invd;           // damping / out-degree (fp64 storage)
+  DevArray<double> l1_block, l1_fin, l1_hist;
   DevArray<int> ctl;            // [0] completed iterations, [1] done
   DevArray<unsigned> blk_cnt;
   // CUDA graph with a conditional WHILE node (one iteration kernel per trip)
