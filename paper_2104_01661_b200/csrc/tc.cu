@@ -27,83 +27,85 @@
 
 namespace gbx {
 
-constexpr int kTcWarpCap = 1024;        // max dU(i) for the warp kernel
-constexpr int kTcWarpSlots = 2048;      // hash slots per warp (pow2, load <= 0.5)
-constexpr int kTcWarpsPerCta = 4;
+constexpr int kTcWarpCap = 512;         // max dU(i) for the warp kernel
+constexpr int kTcWarpSlots = 1024;      // hash slots per warp: 256 buckets x 4 (load <= 0.5)
+constexpr int kTcWarpsPerCta = 8;
 constexpr int kTcCtaCap = 16384;        // max dU(i) for the CTA kernel
 constexpr int kTcCtaSlots = 32768;      // 128 KB dynamic shared memory
 constexpr int kTcRowChunk = 8;
 constexpr unsigned kFullMask = 0xffffffffu;
 
-__device__ __forceinline__ uint32_t tc_hash(int32_t k, int log_slots) {
-  return (static_cast<uint32_t>(k) * 0x9E3779B1u) >> (32 - log_slots);
+// Shared-memory hash set of U(i): buckets of 4 int32 slots (one 16-byte load
+// per probe, no divergent probe chains), bucket = Fibonacci hash of the key,
+// linear probing at bucket granularity only when a bucket is full (rare at a
+// load factor <= 1/2).  log_slots counts slots (>= 2).
+__device__ __forceinline__ uint32_t tc_bucket(int32_t k, int log_buckets) {
+  return (static_cast<uint32_t>(k) * 0x9E3779B1u) >> (32 - log_buckets);
 }
 
 __device__ __forceinline__ void tc_insert(int* table, int log_slots, int32_t k) {
-  const uint32_t mask = (1u << log_slots) - 1;
-  uint32_t h = tc_hash(k, log_slots);
+  const int lb = log_slots - 2;
+  const uint32_t bmask = (1u << lb) - 1;
+  uint32_t b = tc_bucket(k, lb);
   for (;;) {
-    int prev = atomicCAS(&table[h], -1, k);
-    if (prev == -1 || prev == k) return;
-    h = (h + 1) & mask;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int prev = atomicCAS(&table[4 * b + q], -1, k);
+      if (prev == -1 || prev == k) return;
+    }
+    b = (b + 1) & bmask;
   }
 }
 
 __device__ __forceinline__ bool tc_lookup(const int* table, int log_slots, int32_t k) {
-  const uint32_t mask = (1u << log_slots) - 1;
-  uint32_t h = tc_hash(k, log_slots);
+  const int lb = log_slots - 2;
+  const uint32_t bmask = (1u << lb) - 1;
+  uint32_t b = tc_bucket(k, lb);
   for (;;) {
-    int v = table[h];
-    if (v == k) return true;
-    if (v == -1) return false;
-    h = (h + 1) & mask;
+    const int4 v = *reinterpret_cast<const int4*>(table + 4 * b);
+    if (v.x == k || v.y == k || v.z == k || v.w == k) return true;
+    if (v.x == -1 || v.y == -1 || v.z == -1 || v.w == -1) return false;
+    b = (b + 1) & bmask;
   }
 }
 
-// Stream the concatenation of U(j) for j in U(i)[jb, je) over `lanes` threads
-// (tid in [0, lanes)), probing every element in the table.  Each round takes
-// 32 j's, prefix-sums their lengths and spreads the elements over the lanes.
+// Stream the concatenation of U(j) for j in U(i)[jb, je) over a warp group,
+// probing every element in the table.  Each round takes 32 j's, prefix-sums
+// their lengths and spreads the elements over the lanes (32-bit offsets:
+// nnz(U) < 2^31 is checked by tc_prepare).
 template <int kWarps>
 __device__ __forceinline__ unsigned long long tc_stream_row(
-    const int64_t* __restrict__ urp, const int32_t* __restrict__ ucol, int64_t jb, int64_t je,
-    const int* table, int log_slots, int lane, int warp_in_group) {
+    const int64_t* __restrict__ urp, const int32_t* __restrict__ ucol, int jb, int je,
+    const int* table, int log_slots, int lane, int warp_in_group, int* s_incl, int* s_sx) {
   unsigned long long cnt = 0;
   // each warp of the group takes every kWarps-th block of 32 j's
-  for (int64_t base = jb + 32 * warp_in_group; base < je; base += 32 * kWarps) {
-    const int64_t p = base + lane;
-    int32_t j = -1;
-    int64_t s = 0, len = 0;
+  for (int base = jb + 32 * warp_in_group; base < je; base += 32 * kWarps) {
+    const int p = base + lane;
+    int s = 0, len = 0;
     if (p < je) {
-      j = __ldg(ucol + p);
-      s = __ldg(urp + j);
-      len = __ldg(urp + j + 1) - s;
+      const int32_t j = __ldg(ucol + p);
+      s = static_cast<int>(__ldg(urp + j));
+      len = static_cast<int>(__ldg(urp + j + 1)) - s;
     }
-    int64_t incl = len;
+    int incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int64_t t = __shfl_up_sync(kFullMask, incl, o);
+      const int t = __shfl_up_sync(kFullMask, incl, o);
       if (lane >= o) incl += t;
     }
-    const int64_t total = __shfl_sync(kFullMask, incl, 31);
-    const int64_t excl = incl - len;
-    for (int64_t e0 = 0; e0 < total; e0 += 32) {
-      const int64_t e = e0 + lane;
-      // owner = the lane whose [excl, incl) contains e
-      int lo = 0, hi = 31;
+    const int total = __shfl_sync(kFullMask, incl, 31);
+    // element e of lane l's list is ucol[sx[l] + e]; owners found in shared memory
+    s_incl[lane] = incl;
+    s_sx[lane] = s - (incl - len);
+    __syncwarp();
+    for (int e = lane; e < total; e += 32) {
+      int lo = 0;
 #pragma unroll
-      for (int step = 0; step < 5; ++step) {
-        int mid = (lo + hi) >> 1;
-        int64_t m_incl = __shfl_sync(kFullMask, incl, mid);
-        if (m_incl <= e) lo = mid + 1; else hi = mid;
-      }
-      const int owner = lo;
-      const int64_t o_s = __shfl_sync(kFullMask, s, owner);
-      const int64_t o_ex = __shfl_sync(kFullMask, excl, owner);
-      if (e < total) {
-        const int32_t k = __ldg(ucol + o_s + (e - o_ex));
-        cnt += tc_lookup(table, log_slots, k) ? 1ull : 0ull;
-      }
+      for (int step = 16; step > 0; step >>= 1)
+        if (s_incl[lo + step - 1] <= e) lo += step;
+      cnt += tc_lookup(table, log_slots, __ldg(ucol + s_sx[lo] + e)) ? 1ull : 0ull;
     }
+    __syncwarp();
   }
   return cnt;
 }
@@ -117,7 +119,8 @@ struct TcArgs {
 };
 
 __global__ void __launch_bounds__(32 * kTcWarpsPerCta) k_tc_warp(TcArgs a) {
-  __shared__ int tables[kTcWarpsPerCta][kTcWarpSlots];
+  __shared__ __align__(16) int tables[kTcWarpsPerCta][kTcWarpSlots];
+  __shared__ int owners[kTcWarpsPerCta][64];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   int* table = tables[wid];
@@ -135,14 +138,15 @@ __global__ void __launch_bounds__(32 * kTcWarpsPerCta) k_tc_warp(TcArgs a) {
       const int64_t b = __ldg(a.urp + i), e = __ldg(a.urp + i + 1);
       const int64_t du = e - b;
       if (du < 2 || du > kTcWarpCap) continue;
-      int log_slots = 6;
+      int log_slots = 5;
       while ((1 << log_slots) < 2 * du) ++log_slots;
       const int slots = 1 << log_slots;
       for (int t = lane; t < slots; t += 32) table[t] = -1;
       __syncwarp();
       for (int64_t q = b + lane; q < e; q += 32) tc_insert(table, log_slots, __ldg(a.ucol + q));
       __syncwarp();
-      cnt += tc_stream_row<1>(a.urp, a.ucol, b, e, table, log_slots, lane, 0);
+      cnt += tc_stream_row<1>(a.urp, a.ucol, static_cast<int>(b), static_cast<int>(e), table,
+                              log_slots, lane, 0, owners[wid], owners[wid] + 32);
       __syncwarp();
     }
   }
@@ -155,7 +159,8 @@ __global__ void __launch_bounds__(32 * kTcWarpsPerCta) k_tc_warp(TcArgs a) {
 __global__ void __launch_bounds__(512) k_tc_cta(const int64_t* urp, const int32_t* ucol,
                                                 const int32_t* rows, int64_t nrows,
                                                 unsigned long long* count) {
-  extern __shared__ int table[];
+  extern __shared__ __align__(16) int table[];
+  __shared__ int owners[16][64];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   constexpr int kW = 16;
@@ -164,14 +169,15 @@ __global__ void __launch_bounds__(512) k_tc_cta(const int64_t* urp, const int32_
     const int64_t i = rows[r];
     const int64_t b = urp[i], e = urp[i + 1];
     const int64_t du = e - b;
-    int log_slots = 6;
+    int log_slots = 5;
     while ((1 << log_slots) < 2 * du) ++log_slots;
     const int slots = 1 << log_slots;
     for (int t = threadIdx.x; t < slots; t += blockDim.x) table[t] = -1;
     __syncthreads();
     for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) tc_insert(table, log_slots, ucol[q]);
     __syncthreads();
-    cnt += tc_stream_row<kW>(urp, ucol, b, e, table, log_slots, lane, wid);
+    cnt += tc_stream_row<kW>(urp, ucol, static_cast<int>(b), static_cast<int>(e), table,
+                             log_slots, lane, wid, owners[wid], owners[wid] + 32);
     __syncthreads();
   }
 #pragma unroll
@@ -268,6 +274,8 @@ void tc_prepare(gbx_graph* g) {
   // the graph is symmetric and loop-free (checked by the caller): exactly half
   // of the entries point up in rank
   const int64_t unnz = m / 2;
+  if (unnz >= (int64_t(1) << 31) - 1)
+    fail(GBX_UNSUPPORTED, "triangle_count: nnz(U) >= 2^31 is not supported (32-bit offsets)");
   csr_from_sorted_keys(s, n, bits, sorted, unnz, P->urp, P->ucol);
   P->nnz = unnz;
   P->count.alloc(1);
