@@ -130,39 +130,72 @@ def barrier(dist):
 
 
 # ---------------------------------------------------------------- CPU baselines
+class RefPagerankSampler:
+    """The reference's own pull SpMV (gblite mxv plus.second, core.cpp:340-386,
+    compiled from /root/reference into oracle/_ref) on a bounded row sample of
+    the same relabel-free AT: one sample = one PageRank pull (pagerank.cpp:59-61)
+    over rows [0, R) against the full contribution vector.  R is calibrated so
+    one sample takes about `budget_s` seconds.  Falls back to the oracle port
+    (multi-threaded restatement, full iterations) when oracle/_ref is absent."""
+
+    def __init__(self, scale, seed=1, budget_s=5.0):
+        import oracle as O
+        self.O = O
+        self.scale = scale
+        rp, col = O.rmat_graph(scale, 16, seed=seed, undirected=False)
+        self.n = len(rp) - 1
+        self.trp, self.tcol, _ = O.transpose(self.n, rp, col)
+        self.outdeg = np.diff(rp)
+        self.kind = "reference" if O.ref_available() else "port"
+        self.rows = 4
+        if self.kind == "reference":
+            secs, _ = O.ref_pr_mxv_sample(self.n, self.trp, self.tcol, self.outdeg, 0.85, 0,
+                                          self.rows)
+            while secs < budget_s / 3 and self.rows < self.n:
+                self.rows = min(self.n, int(self.rows * max(2.0, budget_s / max(secs, 1e-3) / 2)))
+                secs, _ = O.ref_pr_mxv_sample(self.n, self.trp, self.tcol, self.outdeg, 0.85, 0,
+                                              self.rows)
+
+    def step(self):
+        O = self.O
+        if self.kind == "reference":
+            secs, _ = O.ref_pr_mxv_sample(self.n, self.trp, self.tcol, self.outdeg, 0.85, 0,
+                                          self.rows)
+            edges = int(self.trp[self.rows] - self.trp[0])
+            return edges / secs
+        t0 = time.perf_counter()
+        O.pagerank(self.n, self.trp, self.tcol, self.outdeg, 0.85, 0.0, 3)
+        return float(self.trp[-1]) * 3 / (time.perf_counter() - t0)
+
+    def describe(self, value):
+        if self.kind == "reference":
+            edges = int(self.trp[self.rows] - self.trp[0])
+            return {"value": value, "unit": "edges/s/iter", "cores": 1, "kind": "reference",
+                    "sample": f"gblite mxv (plus.second, core.cpp:340-386) over rows "
+                              f"[0,{self.rows}) of AT ({edges} edges) of the scale-{self.scale} "
+                              f"graph against the full contribution vector; the reference is "
+                              f"single-threaded (gapbench.cpp:164-166) and O(n * nnz(u)) per "
+                              f"pull (SURVEY.md 3.3), so the full graph is out of reach"}
+        return {"value": value, "unit": "edges/s/iter", "cores": self.O.threads(), "kind": "port",
+                "sample": f"oracle restatement, 3 PageRank iterations on the full "
+                          f"scale-{self.scale} graph"}
+
+
 def cpu_baseline_pagerank(scale, seed, budget_s=12.0):
-    """The reference's own pull SpMV (core.cpp:340-386, via oracle/_ref) on a
-    bounded row sample of the same AT, plus the multi-threaded oracle port on
-    the full graph for a few iterations.  Returns (baseline dict, extras)."""
+    """cpu_baseline for our arm: the reference sampler, plus the port as an extra."""
     import oracle as O
-    rp, col = O.rmat_graph(scale, 16, seed=seed, undirected=False)
-    n = len(rp) - 1
-    trp, tcol, _ = O.transpose(n, rp, col)
-    outdeg = np.diff(rp)
+    ref = RefPagerankSampler(scale, seed, budget_s=budget_s / 2)
+    v = ref.step()
+    base = ref.describe(v)
     extras = {}
-    # port: 3 iterations of the restatement, all host threads
     t0 = time.perf_counter()
-    O.pagerank(n, trp, tcol, outdeg, 0.85, 0.0, 3)
+    O.pagerank(ref.n, ref.trp, ref.tcol, ref.outdeg, 0.85, 0.0, 3)
     tp = time.perf_counter() - t0
-    port = {"value": float(trp[-1]) * 3 / tp, "unit": "edges/s/iter", "cores": O.threads(),
-            "kind": "port",
-            "sample": f"oracle restatement, 3 PageRank iterations on the full scale-{scale} graph"}
-    extras["port"] = port
-    if not O.ref_available():
-        return port, extras
-    # reference: rows [0, R) of AT through gblite::mxv, R grown to ~budget_s
-    r = 4
-    secs, _ = O.ref_pr_mxv_sample(n, trp, tcol, outdeg, 0.85, 0, r)
-    while secs < budget_s / 4 and r < n:
-        r = min(n, int(r * max(2.0, budget_s / 2 / max(secs, 1e-3))))
-        secs, _ = O.ref_pr_mxv_sample(n, trp, tcol, outdeg, 0.85, 0, r)
-    edges = int(trp[r] - trp[0])
-    ref = {"value": edges / secs, "unit": "edges/s/iter", "cores": 1, "kind": "reference",
-           "sample": f"gblite mxv (plus.second, core.cpp:340-386) over rows [0,{r}) of AT "
-                     f"({edges} edges) of the scale-{scale} graph against the full contribution "
-                     f"vector, {secs:.1f} s; the reference is single-threaded and O(n*nnz(u)) "
-                     f"per pull (SURVEY.md §3.3)"}
-    return ref, extras
+    extras["port"] = {"value": float(ref.trp[-1]) * 3 / tp, "unit": "edges/s/iter",
+                      "cores": O.threads(), "kind": "port",
+                      "sample": f"oracle restatement, 3 PageRank iterations on the full "
+                                f"scale-{scale} graph"}
+    return base, extras
 
 
 def run_reference(args):
@@ -172,20 +205,18 @@ def run_reference(args):
     import oracle as O
     O.build(ref=os.path.isdir("/root/reference/proj/src"))
     scale = args.scale or 22
-    vals = []
-    base = None
+    steps = max(args.steps, 1)
+    sampler = RefPagerankSampler(scale, 1, budget_s=max(0.5, min(5.0, 90.0 / steps)))
     for _ in range(args.warmup):
-        pass
-    for step in range(max(args.steps, 1)):
-        base, extras = cpu_baseline_pagerank(scale, 1, budget_s=max(4.0, 60.0 / args.steps))
-        vals.append(base["value"])
+        sampler.step()
+    vals = [sampler.step() for _ in range(steps)]
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s/iter",
-            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "n_gpus": ws, "steps": steps, "warmup": args.warmup, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"pagerank_rmat{scale}_directed", "scale": scale,
                        "edge_factor": 16, "damping": 0.85, "tol": 1e-4, "itermax": 100},
-            "cpu_baseline": dict(base, value=v),
+            "cpu_baseline": sampler.describe(v),
             "e2e": {"value": v, "unit": "edges/s/iter", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -278,11 +309,14 @@ def bench_pagerank(args, dist, ws, rank, local):
                    "l2": "flushed (256 MB write) before every step"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_pr_iter (fused pull SpMV + epilogue)",
+                     "kernel": "k_pr_rows (fused pull SpMV + epilogue) + k_pr_finish",
                      "bytes_per_launch": hot_bytes,
                      "launch_ms": t_launch * 1e3,
-                     "note": "launch time = device time of one run / iterations (the run is "
-                             "one CUDA graph: 1 init kernel + one k_pr_iter per iteration)"},
+                     "note": "launch time = device time of one run / iterations: an upper "
+                             "bound on the k_pr_rows launch (the run is one CUDA graph: init, then "
+                             "k_pr_rows + k_pr_finish per iteration, then the un-permute)",
+                     "traffic_source": "profiles/pagerank_ncu.json (ncu --set full, cold "
+                                       "cache, one k_pr_rows launch)"},
         "e2e": {"value": e2e_val, "unit": "edges/s/iter",
                 "h2d_bytes_per_step": int(rp.nbytes + col.nbytes),
                 "d2h_bytes_per_step": int(n * 8 + 4),
@@ -407,7 +441,7 @@ def bench_simple(args, dist, ws, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="pagerank",
