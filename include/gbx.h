@@ -227,18 +227,27 @@ typedef struct {
 } gbx_stats;
 int gbx_last_stats(const gbx_graph* g, gbx_stats* stats, char msg[GBX_MSG_LEN]);
 
-/* ---- sharded PageRank step for the multi-GPU driver (1D row blocks) -------
- * One process per GPU owns rows [row_begin, row_end) of AT (the in-edges of its
- * destination vertices) and the full gathered contribution vector x (fp32, n).
- * gbx_pr_shard_step computes, for its rows, r_new = teleport + sum x(k),
- * x_new = r_new * damping / outdeg (0 if dangling) and the fp64 L1 partial;
- * all three stay on the device (device pointers).  The caller all-gathers
- * x_new (NCCL) and all-reduces the L1 partial. */
-int gbx_pr_shard_prepare(gbx_graph* g, int64_t row_begin, int64_t row_end,
-                         char msg[GBX_MSG_LEN]);
+/* ---- sharded PageRank for the multi-GPU driver (1D row blocks) -------------
+ * pagerank.cpp:52-76 split over ranks.  Every rank holds the graph; rank r of
+ * nranks owns rows [row_begin, row_end) of the in-degree-relabeled AT (balanced
+ * by rows + nnz).  Vectors live in relabeled ids:
+ *   gbx_pr_shard_init   x_full[n] = initial contributions, r_local = 1/n;
+ *   gbx_pr_shard_step   for its rows: r = teleport + sum x(k) (fp64), x_new[row]
+ *                       = r * damping / outdeg (written at relabeled ids in a
+ *                       full-length buffer), *l1_dev = fp64 L1 partial;
+ *   the caller all-gathers the x_new slices (NCCL) and all-reduces l1;
+ *   gbx_pr_shard_unpermute maps a gathered relabeled rank vector back to the
+ *                       original vertex order (fp64, host).
+ * All vector arguments are device pointers. */
+int gbx_pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* row_begin,
+                         int64_t* row_end, char msg[GBX_MSG_LEN]);
+int gbx_pr_shard_init(gbx_graph* g, float* x_full_dev, float* r_local_dev, double damping,
+                      char msg[GBX_MSG_LEN]);
 int gbx_pr_shard_step(gbx_graph* g, const float* x_full_dev, float* r_dev,
                       float* x_new_dev, double* l1_dev, double damping,
                       char msg[GBX_MSG_LEN]);
+int gbx_pr_shard_unpermute(gbx_graph* g, const float* r_full_dev, double* rank_out,
+                           char msg[GBX_MSG_LEN]);
 /* Rows [row_begin,row_end) of a split with balanced nnz + rows (merge-path). */
 int gbx_partition_rows(int64_t* bounds, const gbx_graph* g, int parts, int transposed,
                        char msg[GBX_MSG_LEN]);

@@ -67,7 +67,9 @@ _SIGS = {
     "gbx_prepare": [_vp, _cp],
     "gbx_result_device": [_vp, _cp, _pp, _vp],
     "gbx_last_stats": [_vp, C.POINTER(gbx_stats)],
-    "gbx_pr_shard_prepare": [_vp, _i64, _i64],
+    "gbx_pr_shard_prepare": [_vp, _int, _int, _vp, _vp],
+    "gbx_pr_shard_init": [_vp, _vp, _vp, _dbl],
+    "gbx_pr_shard_unpermute": [_vp, _vp, _vp],
     "gbx_pr_shard_step": [_vp, _vp, _vp, _vp, _vp, _dbl],
     "gbx_partition_rows": [_vp, _vp, _int, _int],
     "gbx_triangle_count_rows": [_vp, _vp, _i64, _i64],

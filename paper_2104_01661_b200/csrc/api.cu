@@ -603,11 +603,28 @@ int gbx_last_stats(const gbx_graph* gc, gbx_stats* stats, char* msg) {
   });
 }
 
-int gbx_pr_shard_prepare(gbx_graph* g, int64_t rb, int64_t re, char* msg) {
+int gbx_pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* row_begin,
+                         int64_t* row_end, char* msg) {
   return guard(msg, [&] {
     need(g);
     gbx::Scope sc(g);
-    gbx::pr_shard_prepare(g, rb, re);
+    gbx::pr_shard_prepare(g, rank, nranks, row_begin, row_end);
+  });
+}
+
+int gbx_pr_shard_init(gbx_graph* g, float* x_full, float* r_local, double damping, char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    gbx::Scope sc(g);
+    gbx::pr_shard_init(g, x_full, r_local, damping);
+  });
+}
+
+int gbx_pr_shard_unpermute(gbx_graph* g, const float* r_full, double* out, char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    gbx::Scope sc(g);
+    gbx::pr_shard_unpermute(g, r_full, out);
   });
 }
 

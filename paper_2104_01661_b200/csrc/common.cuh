@@ -172,7 +172,9 @@ double sssp_default_delta(gbx_graph* g);
 void sssp_prepare(gbx_graph* g);
 void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrality);
 void cc_run(gbx_graph* g, int64_t* label, int* iters);
-void pr_shard_prepare(gbx_graph* g, int64_t rb, int64_t re);
+void pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* rb, int64_t* re);
+void pr_shard_init(gbx_graph* g, float* x_full, float* r_local, double damping);
+void pr_shard_unpermute(gbx_graph* g, const float* r_full, double* out_host);
 void pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, double* l1,
                    double damping);
 void partition_rows(const gbx_graph* g, int parts, bool transposed, int64_t* bounds);

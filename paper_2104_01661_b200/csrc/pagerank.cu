@@ -732,17 +732,60 @@ void pagerank_run(gbx_graph* g, double damping, double tol, int itermax, double*
 }
 
 // ---- sharded step (multi-GPU driver) ----------------------------------------------
-// Shards own contiguous blocks of the RELABELED rows; x vectors are in relabeled
-// ids, so the driver all-gathers x_new slices as they are.
+// Shards own contiguous blocks of the RELABELED rows, balanced by rows + nnz
+// (merge-path split); x vectors are in relabeled ids, so the driver all-gathers
+// the x_new slices as they are and un-permutes the final ranks once.
 
-void pr_shard_prepare(gbx_graph* g, int64_t rb, int64_t re) {
+void pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* rb_out, int64_t* re_out) {
   require_at(g, "pr_shard");
   require_rowdeg(g, "pr_shard");
-  if (rb < 0 || re > g->A.n || rb > re) fail(GBX_INDEX_OUT_OF_BOUNDS, "pr_shard: bad row range");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    fail(GBX_INVALID_VALUE, "pr_shard: bad rank / nranks");
   auto S = std::make_unique<PrShard>();
-  build_relabeled(g, S->plan);
-  plan_rows(g, S->plan, rb, re);
+  PrPlan& P = S->plan;
+  build_relabeled(g, P);
+  std::vector<int64_t> rp(P.n + 1);
+  GBX_CUDA(cudaMemcpyAsync(rp.data(), P.trp.p, (P.n + 1) * 8, cudaMemcpyDeviceToHost, g->stream));
+  GBX_CUDA(cudaStreamSynchronize(g->stream));
+  auto split = [&](int q) -> int64_t {
+    if (q <= 0) return 0;
+    if (q >= nranks) return P.n;
+    const int64_t target = (P.n + P.nnz) * q / nranks;
+    int64_t lo = 0, hi = P.n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (mid + rp[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  const int64_t rb = split(rank), re = std::max(rb, split(rank + 1));
+  plan_rows(g, P, rb, re);
+  P.invf.alloc(std::max<int64_t>(P.n, 1));
+  S->nranks = nranks;
+  S->rank = rank;
   g->prs = std::move(S);
+  if (rb_out) *rb_out = rb;
+  if (re_out) *re_out = re;
+}
+
+__global__ void k_pr_shard_init(float* x, float* r_local, float* inv, const int32_t* outdeg,
+                                int64_t n, int64_t rb, int64_t re, double damping) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double r0 = 1.0 / static_cast<double>(n);
+  const int dg = outdeg[i];
+  x[i] = dg > 0 ? static_cast<float>(r0 / (static_cast<double>(dg) / damping)) : 0.f;
+  inv[i] = dg > 0 ? static_cast<float>(damping / static_cast<double>(dg)) : 0.f;
+  if (i >= rb && i < re) r_local[i - rb] = static_cast<float>(r0);
+}
+
+void pr_shard_init(gbx_graph* g, float* x_full, float* r_local, double damping) {
+  if (!g->prs) fail(GBX_MISSING_PROPERTY, "pr_shard_init needs gbx_pr_shard_prepare");
+  PrPlan& P = g->prs->plan;
+  k_pr_shard_init<<<ceil_div(std::max<int64_t>(P.n, 1), 256), 256, 0, g->stream>>>(
+      x_full, r_local, P.invf.p, P.deg.p, P.n, P.row0, P.row1, damping);
+  GBX_LAUNCHED();
+  P.g_damping = damping;
 }
 
 void pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, double* l1,
@@ -750,13 +793,13 @@ void pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, do
   if (!g->prs) fail(GBX_MISSING_PROPERTY, "pr_shard_step needs gbx_pr_shard_prepare");
   PrPlan& P = g->prs->plan;
   cudaStream_t s = g->stream;
-  PrArgs<float> a = make_args<float>(P, damping, 0.0, 1 << 30);
-  if (!P.invf.p || P.g_damping != damping) {
-    P.invf.alloc(std::max<int64_t>(P.n, 1));
-    k_pr_inv<<<ceil_div(P.n, 256), 256, 0, s>>>(P.invf.p, P.deg.p, P.n, damping);
+  if (P.g_damping != damping) {
+    k_pr_inv<<<ceil_div(std::max<int64_t>(P.n, 1), 256), 256, 0, s>>>(P.invf.p, P.deg.p, P.n,
+                                                                      damping);
     GBX_LAUNCHED();
     P.g_damping = damping;
   }
+  PrArgs<float> a = make_args<float>(P, damping, 0.0, 1 << 30);
   a.inv = P.invf.p;
   a.fixed = 1;
   a.x0 = const_cast<float*>(x_full);
@@ -764,13 +807,35 @@ void pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, do
   a.r0 = r;      // r_prev (local rows), overwritten in place by r_new
   a.r1 = r;
   a.row0 = P.row0;
+  a.hot = 0;
+  a.grid_rows = rows_grid<float>(a);
   GBX_CUDA(cudaMemsetAsync(P.ctl.p, 0, 2 * sizeof(int), s));
   GBX_CUDA(cudaMemsetAsync(P.blk_cnt.p, 0, sizeof(unsigned), s));
-  k_pr_rows<float><<<a.grid_rows, kPrThreads, rows_smem<float>(a), s>>>(a);
+  k_pr_rows<float><<<a.grid_rows, kPrThreads, 0, s>>>(a);
   k_pr_finish<float, false><<<P.grid_fin, kPrThreads, 0, s>>>(a);
   GBX_LAUNCHED();
   GBX_CUDA(cudaMemcpyAsync(l1, P.l1_hist.p, sizeof(double), cudaMemcpyDeviceToDevice, s));
   g->prs->steps++;
+}
+
+__global__ void k_pr_unpermute_f(const float* r, const int32_t* new2old, int64_t n, double* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[new2old[i]] = static_cast<double>(r[i]);
+}
+
+void pr_shard_unpermute(gbx_graph* g, const float* r_full, double* out_host) {
+  if (!g->prs) fail(GBX_MISSING_PROPERTY, "pr_shard_unpermute needs gbx_pr_shard_prepare");
+  PrPlan& P = g->prs->plan;
+  cudaStream_t s = g->stream;
+  double* tmp = nullptr;
+  GBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), std::max<int64_t>(P.n, 1) * 8, s));
+  k_pr_unpermute_f<<<ceil_div(std::max<int64_t>(P.n, 1), 256), 256, 0, s>>>(r_full, P.new2old.p,
+                                                                            P.n, tmp);
+  cudaError_t le = cudaGetLastError();
+  if (le == cudaSuccess) le = cudaMemcpyAsync(out_host, tmp, P.n * 8, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(tmp, s);
+  GBX_CUDA(le);
+  GBX_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace gbx

@@ -57,6 +57,7 @@ struct PrPlan {
 struct PrShard {
   PrPlan plan;
   int64_t steps = 0;
+  int rank = 0, nranks = 1;
 };
 
 // BFS workspaces (bfs.cu).

@@ -1,0 +1,149 @@
+"""Multi-GPU drivers: one process per GPU, torch.distributed
+(NCCL over NVLink/NVSwitch) for the exchange, libgbx.so shard kernels for the
+compute.
+
+PageRank (config 2): 1D row blocks of the in-degree-relabeled AT, balanced by
+rows + nnz.  Per iteration every rank runs the fused shard step on its rows
+(gbx_pr_shard_step: sums, teleport, next contributions, fp64 L1 partial), then
+  * all-gather of the x slices (fp32, n/P per rank) -> the full x for the next
+    gather step, and
+  * all-reduce (sum) of the fp64 L1 partial, compared against tol exactly as
+    pagerank.cpp:65-74 does (same iteration count as the single-GPU path).
+Triangle count (config 3): U replicated, oriented rows split by wedge work
+(gbx_tc_partition), one u64 all-reduce at the end.
+
+The drivers only speak to a small backend interface, so the host logic (the
+partition bookkeeping, the exchange, the convergence test) is exercised on CPU
+by tests/test_dist_gloo.py with world_size 2 over gloo and a numpy backend.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+
+def _gather_slices(dist, local, bounds, world, out):
+    """All-gather variable-length 1-D slices: rank p owns out[bounds[p]:bounds[p+1]].
+    NCCL all-gather wants equal sizes, so slices are padded to the longest."""
+    import torch
+    chunk = max(int(bounds[p + 1] - bounds[p]) for p in range(world))
+    send = torch.zeros(chunk, dtype=local.dtype, device=local.device)
+    send[: local.numel()] = local
+    parts = [torch.empty(chunk, dtype=local.dtype, device=local.device) for _ in range(world)]
+    dist.all_gather(parts, send)
+    for p in range(world):
+        b, e = int(bounds[p]), int(bounds[p + 1])
+        if e > b:
+            out[b:e] = parts[p][: e - b]
+    return out
+
+
+def sharded_pagerank(backend, dist, damping=0.85, tol=1e-4, itermax=100):
+    """GAP PageRank over `world` ranks; returns (rank vector on every rank (numpy,
+    original ids), iterations)."""
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    rb, re, n = backend.prepare(rank, world)
+    dev = backend.device
+    b = torch.tensor([rb, re], dtype=torch.int64, device=dev)
+    allb = [torch.empty(2, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(allb, b)
+    bounds = [int(t[0]) for t in allb] + [int(allb[-1][1])]
+    for p in range(world - 1):
+        assert int(allb[p][1]) == int(allb[p + 1][0]), "row blocks must tile [0, n)"
+    assert bounds[0] == 0 and bounds[-1] == n
+    backend.init(damping)
+    k = 0
+    for k in range(1, itermax + 1):
+        l1 = backend.step(damping)                 # device scalar (fp64)
+        dist.all_reduce(l1)                        # sum of the per-shard partials
+        _gather_slices(dist, backend.x_new_slice(), bounds, world, backend.x_full())
+        if not (float(l1.item()) >= tol):          # pagerank.cpp:74: stop when < tol
+            break
+    iters = min(k, itermax)
+    r_full = torch.empty(n, dtype=backend.r_local().dtype, device=dev)
+    _gather_slices(dist, backend.r_local(), bounds, world, r_full)
+    return backend.unpermute(r_full), iters
+
+
+def sharded_triangle_count(backend, dist):
+    """Triangle count with wedge-balanced row blocks of the oriented U."""
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    bounds = backend.tc_partition(world)
+    local = backend.tc_rows(int(bounds[rank]), int(bounds[rank + 1]))
+    t = torch.tensor([local], dtype=torch.int64, device=backend.device)
+    dist.all_reduce(t)
+    return int(t.item())
+
+
+class GpuShardBackend:
+    """libgbx.so shard kernels on this rank's GPU (vectors are torch CUDA tensors)."""
+
+    def __init__(self, graph):
+        import torch
+        self.g = graph
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def prepare(self, rank, world):
+        import torch
+
+        from .graph import call
+        rb, re = C.c_int64(), C.c_int64()
+        call("gbx_pr_shard_prepare", self.g.handle, rank, world, C.byref(rb), C.byref(re))
+        self.rb, self.re = rb.value, re.value
+        self.n = self.g.n()
+        self._x = torch.empty(self.n, dtype=torch.float32, device=self.device)
+        self._xn = torch.empty(self.n, dtype=torch.float32, device=self.device)
+        self._r = torch.empty(max(self.re - self.rb, 1), dtype=torch.float32, device=self.device)
+        self._l1 = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self._stream = torch.cuda.ExternalStream(self.g.stream())
+        return self.rb, self.re, self.n
+
+    def init(self, damping):
+        from .graph import call
+        call("gbx_pr_shard_init", self.g.handle, self._x.data_ptr(), self._r.data_ptr(), damping)
+
+    def step(self, damping):
+        import torch
+
+        from .graph import call
+        # the library stream must see the x gathered on torch's stream
+        self._stream.wait_stream(torch.cuda.current_stream())
+        call("gbx_pr_shard_step", self.g.handle, self._x.data_ptr(), self._r.data_ptr(),
+             self._xn.data_ptr(), self._l1.data_ptr(), damping)
+        # the collectives run on torch's stream: order them after the library's
+        torch.cuda.current_stream().wait_stream(self._stream)
+        return self._l1
+
+    def x_new_slice(self):
+        return self._xn[self.rb:self.re]
+
+    def x_full(self):
+        return self._x
+
+    def r_local(self):
+        return self._r[: self.re - self.rb]
+
+    def unpermute(self, r_full):
+        import torch
+
+        from .graph import call
+        torch.cuda.synchronize()
+        out = np.empty(self.n, np.float64)
+        call("gbx_pr_shard_unpermute", self.g.handle, r_full.data_ptr(), out.ctypes.data)
+        return out
+
+    # ---- triangle count
+    def tc_partition(self, world):
+        from .graph import call
+        b = np.empty(world + 1, np.int64)
+        call("gbx_tc_partition", b.ctypes.data, self.g.handle, world)
+        return b
+
+    def tc_rows(self, rb, re):
+        from .graph import call
+        c = C.c_uint64(0)
+        call("gbx_triangle_count_rows", C.byref(c), self.g.handle, rb, re)
+        return int(c.value)
