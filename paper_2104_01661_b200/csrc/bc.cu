@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "plans.cuh"
+#include "warpqueue.cuh"
 
 namespace gbx {
 
@@ -32,35 +33,6 @@ constexpr unsigned kAll = 0xffffffffu;
 
 __device__ __forceinline__ int bc_chunks(int64_t deg) {
   return deg <= kBcChunk ? 1 : static_cast<int>((deg + kBcChunk - 1) / kBcChunk);
-}
-
-// Append vertex v (once per level, via mark) to the level list and its chunk
-// entries to the entry queue.  Whole warp calls.
-__device__ __forceinline__ void bc_append(bool has, int32_t v, int64_t deg, int32_t* list,
-                                          int64_t* entries, int* cnt) {
-  const int lane = threadIdx.x & 31;
-  int k = has ? bc_chunks(deg) : 0;
-  int incl = k;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(kAll, incl, o);
-    if (lane >= o) incl += t;
-  }
-  const int tot = __shfl_sync(kAll, incl, 31);
-  if (tot == 0) return;
-  const unsigned vb = __ballot_sync(kAll, has);
-  int eb = 0, lb = 0;
-  if (lane == 0) {
-    eb = atomicAdd(&cnt[1], tot);
-    lb = atomicAdd(&cnt[0], __popc(vb));
-  }
-  eb = __shfl_sync(kAll, eb, 0);
-  lb = __shfl_sync(kAll, lb, 0);
-  if (has) {
-    list[lb + __popc(vb & ((1u << lane) - 1))] = v;
-    const int off = eb + incl - k;
-    for (int c = 0; c < k; ++c) entries[off + c] = (static_cast<int64_t>(c) << 32) | v;
-  }
 }
 
 struct BcArgs {
@@ -80,7 +52,13 @@ struct BcArgs {
   int lanes;
 };
 
-__global__ void k_bc_forward(BcArgs a) {
+__global__ void __launch_bounds__(256) k_bc_forward(BcArgs a) {
+  __shared__ int32_t s_buf[8][256];
+  FrontierQueue<256> fq;
+  fq.buf = s_buf[threadIdx.x >> 5];
+  fq.rp = a.rp;
+  fq.chunk = kBcChunk;
+  fq.reset(a.ent_out, &a.cnt[1], &a.cnt[0], nullptr, a.list_out);
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -119,10 +97,10 @@ __global__ void k_bc_forward(BcArgs a) {
         }
       }
       const bool has = claimed && atomicExch(&a.mark[v], d) != d;
-      const int64_t dv = has ? a.rp[v + 1] - a.rp[v] : 0;
-      bc_append(has, v, dv, a.list_out, a.ent_out, a.cnt);
+      fq.push(has, v);
     }
   }
+  fq.flush();
 }
 
 // backward accumulation for the entries of level d

@@ -23,48 +23,19 @@
 
 #include "common.cuh"
 #include "plans.cuh"
+#include "warpqueue.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace gbx {
 
 constexpr int kBfsThreads = 256;
+constexpr int kBfsBuf = 256;  // staged frontier vertices per warp
 constexpr int64_t kChunk = 1024;
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ int n_chunks(int64_t deg) {
   return deg <= kChunk ? 1 : static_cast<int>((deg + kChunk - 1) / kChunk);
-}
-
-// Append (vertex, chunk) entries for every lane with has=true; whole warp calls.
-__device__ __forceinline__ void warp_append(bool has, int64_t v, int64_t deg, int64_t* q,
-                                            int* cnt_ent, int* cnt_vtx,
-                                            unsigned long long* cnt_edges) {
-  const int lane = threadIdx.x & 31;
-  int k = has ? n_chunks(deg) : 0;
-  int incl = k;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += t;
-  }
-  int tot = __shfl_sync(kFull, incl, 31);
-  if (tot == 0) return;
-  unsigned vb = __ballot_sync(kFull, has);
-  unsigned long long e = has ? static_cast<unsigned long long>(deg) : 0ull;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
-  int base = 0;
-  if (lane == 0) {
-    base = atomicAdd(cnt_ent, tot);
-    atomicAdd(cnt_vtx, __popc(vb));
-    if (cnt_edges) atomicAdd(cnt_edges, e);
-  }
-  base = __shfl_sync(kFull, base, 0);
-  if (has) {
-    int off = base + incl - k;
-    for (int c = 0; c < k; ++c) q[off + c] = (static_cast<int64_t>(c) << 32) | v;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -90,6 +61,11 @@ struct Bfs1Args {
 
 __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
   cg::grid_group grid = cg::this_grid();
+  __shared__ int32_t s_buf[kBfsThreads / 32][kBfsBuf];
+  FrontierQueue<kBfsBuf> fq;
+  fq.buf = s_buf[threadIdx.x >> 5];
+  fq.rp = a.rp;
+  fq.chunk = kChunk;
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -108,6 +84,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
     int64_t* qn = p ? a.q0 : a.q1;
     const uint32_t* bc = p ? a.bm1 : a.bm0;
     uint32_t* bn = p ? a.bm0 : a.bm1;
+    fq.reset(qn, &a.ctl[2], &a.ctl[3], nullptr, nullptr);
     if (push) {
       for (int64_t e = gwarp; e < qe; e += nwarps) {
         const int64_t ent = qc[e];
@@ -130,8 +107,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
               }
             }
           }
-          const int64_t dw = has ? a.rp[w + 1] - a.rp[w] : 0;
-          warp_append(has, w, dw, qn, &a.ctl[2], &a.ctl[3], nullptr);
+          fq.push(has, w);
         }
       }
     } else {
@@ -163,10 +139,10 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
           a.parent[w] = found;
           atomicOr(&bn[w >> 5], 1u << (w & 31));
         }
-        const int64_t dw = has ? a.rp[w + 1] - a.rp[w] : 0;
-        warp_append(has, w, dw, qn, &a.ctl[2], &a.ctl[3], nullptr);
+        fq.push(has, static_cast<int32_t>(w));
       }
     }
+    fq.flush();
     grid.sync();
     // roll the frontier: the current bitmap is cleared for reuse two levels on
     uint32_t* bclr = const_cast<uint32_t*>(bc);
@@ -323,6 +299,11 @@ struct Bfs64Args {
 
 __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
   cg::grid_group grid = cg::this_grid();
+  __shared__ int32_t s_buf[kBfsThreads / 32][kBfsBuf];
+  FrontierQueue<kBfsBuf> fq;
+  fq.buf = s_buf[threadIdx.x >> 5];
+  fq.rp = a.rp;
+  fq.chunk = kChunk;
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -337,6 +318,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
     int64_t* qn = p ? a.q0 : a.q1;
     unsigned long long* fc = p ? a.f1 : a.f0;
     unsigned long long* fn = p ? a.f0 : a.f1;
+    fq.reset(qn, &a.ctl[2], &a.ctl[3], &a.edges[1], nullptr);
     if (push) {
       for (int64_t e = gwarp; e < qe; e += nwarps) {
         const int64_t ent = qc[e];
@@ -362,8 +344,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
               }
             }
           }
-          const int64_t dw = has ? a.rp[w + 1] - a.rp[w] : 0;
-          warp_append(has, w, dw, qn, &a.ctl[2], &a.ctl[3], &a.edges[1]);
+          fq.push(has, w);
         }
       }
     } else {
@@ -409,10 +390,10 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
         }
         const bool has = sub == 0 && found != 0ull;
         if (has) fn[w] = found;
-        const int64_t dw = has ? a.rp[w + 1] - a.rp[w] : 0;
-        warp_append(has, w, dw, qn, &a.ctl[2], &a.ctl[3], &a.edges[1]);
+        fq.push(has, static_cast<int32_t>(w));
       }
     }
+    fq.flush();
     grid.sync();
     // finalize: new frontier bits become seen + level d; old frontier cleared
     const int qn_e = *(volatile int*)&a.ctl[2];

@@ -29,12 +29,15 @@
 
 #include "common.cuh"
 #include "plans.cuh"
+#include "warpqueue.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace gbx {
 
 constexpr int kSsspThreads = 256;
+constexpr int kSsspWarps = kSsspThreads / 32;
+constexpr int kSsspBuf = 256;  // staged pushes per warp and queue
 constexpr unsigned kFullW = 0xffffffffu;
 
 template <typename D> struct DistTraits;
@@ -97,16 +100,6 @@ struct SsspArgs {
   unsigned long long* relax;  // edges relaxed
 };
 
-__device__ __forceinline__ void warp_push(bool has, int32_t v, int32_t* q, int* cnt) {
-  const int lane = threadIdx.x & 31;
-  unsigned b = __ballot_sync(kFullW, has);
-  if (!b) return;
-  int base = 0;
-  if (lane == 0) base = atomicAdd(cnt, __popc(b));
-  base = __shfl_sync(kFullW, base, 0);
-  if (has) q[base + __popc(b & ((1u << lane) - 1))] = v;
-}
-
 template <typename D>
 __device__ __forceinline__ D next_hi(D lo, double delta);
 template <>
@@ -134,6 +127,11 @@ __device__ __forceinline__ unsigned long long bucket_floor<unsigned long long>(
 template <typename D, typename E, typename W>
 __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
   cg::grid_group grid = cg::this_grid();
+  __shared__ int32_t s_near[kSsspWarps][kSsspBuf];
+  __shared__ int32_t s_far[kSsspWarps][kSsspBuf];
+  WarpQueue<int32_t, kSsspBuf> nearq, farq;
+  nearq.buf = s_near[threadIdx.x >> 5];
+  farq.buf = s_far[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int grp = lane >> 3, sub = lane & 7;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -153,6 +151,8 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
       int32_t* qn = pq ? a.q0 : a.q1;
       int32_t* fc = pf ? a.f1 : a.f0;
       unsigned long long nrel = 0;
+      nearq.reset(qn, &a.ctl[1]);
+      farq.reset(fc, &a.ctl[2]);
       for (int64_t base = gwarp * 4; base < nq; base += nwarps * 4) {
         const int64_t qi = base + grp;
         bool active = qi < nq;
@@ -175,14 +175,16 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
               }
             }
           }
-          warp_push(near_push, v, qn, &a.ctl[1]);
-          warp_push(far_push, v, fc, &a.ctl[2]);
+          nearq.push(near_push, v);
+          farq.push(far_push, v);
           if (active) {
             p += 8;
             if (p >= e) active = false;
           }
         }
       }
+      nearq.flush();
+      farq.flush();
       if (nrel) atomicAdd(a.relax, nrel);
       grid.sync();
       if (gtid == 0) {
@@ -221,6 +223,8 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
                                          // (for fp64 bit patterns: the next double up)
     // split the pile: [lo2, hi2) -> near queue, >= hi2 -> stays far, < hi stale
     int32_t* qn = pq ? a.q1 : a.q0;  // current (empty) near queue
+    nearq.reset(qn, &a.ctl[0]);
+    farq.reset(fn, &a.ctl[3]);
     for (int64_t base = gwarp * 32; base < nf; base += nwarps * 32) {
       const int64_t i = base + lane;
       bool to_near = false, to_far = false;
@@ -233,9 +237,11 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
           else to_far = atomicExch(&a.fmark[v], bstamp + 1) != bstamp + 1;
         }
       }
-      warp_push(to_near, v, qn, &a.ctl[0]);
-      warp_push(to_far, v, fn, &a.ctl[3]);
+      nearq.push(to_near, v);
+      farq.push(to_far, v);
     }
+    nearq.flush();
+    farq.flush();
     grid.sync();
     if (gtid == 0) {
       a.lohi[0] = lo2;
