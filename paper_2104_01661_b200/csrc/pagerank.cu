@@ -152,9 +152,13 @@ __device__ __forceinline__ double pr_finish_row(const PrArgs<V>& a, V* r_nxt, V*
   return fabs(static_cast<double>(rprev) - rn);
 }
 
-template <typename V>
-__global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_rows(PrArgs<V> a) {
-  using BlockReduce = cub::BlockReduce<double, kPrThreads>;
+// BS = 256: several CTAs per SM, hot prefix in L1 only.  BS = 1024: two CTAs
+// per SM, each with a shared-memory copy of the hot prefix of x (random
+// gathers are L1TEX-tag bound -- one 32-byte sector per cycle per SM; from
+// shared memory they are bank-parallel).
+template <typename V, int BS>
+__global__ void __launch_bounds__(BS, BS == 1024 ? 2 : GBX_PR_MINB) k_pr_rows(PrArgs<V> a) {
+  using BlockReduce = cub::BlockReduce<double, BS>;
   __shared__ typename BlockReduce::TempStorage red;
   __shared__ PrBin s_bins[kPrBinsMax];
   extern __shared__ __align__(16) unsigned char s_raw[];
@@ -164,7 +168,13 @@ __global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_rows(PrArgs<V> a
   const V *x_cur, *r_cur;
   V *x_nxt, *r_nxt;
   pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
-  for (int64_t i = threadIdx.x; i < a.hot; i += blockDim.x) s_x[i] = x_cur[i];
+  {
+    // stage the hot prefix of x (16-byte vector loads; hot is a multiple of 16 B)
+    constexpr int kVec = 16 / sizeof(V);
+    const int4* src = reinterpret_cast<const int4*>(x_cur);
+    int4* dst = reinterpret_cast<int4*>(s_x);
+    for (int64_t i = threadIdx.x; i < a.hot / kVec; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
   for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_bins[i] = a.bins[i];
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -523,16 +533,16 @@ static size_t rows_smem(const PrArgs<V>& a) {
   static bool attr = false;
   if (!attr) {
     const int mx = static_cast<int>(std::min<int64_t>(hot_bytes(), 200 * 1024));
-    GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   std::max(mx, 1)));
-    GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   std::max(mx, 1)));
     // (measured: the default carveout is best; GBX_PR_CARVEOUT overrides)
     if (const char* cv = std::getenv("GBX_PR_CARVEOUT")) {
       const int carve = std::atoi(cv);
-      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float>,
+      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float, 1024>,
                                     cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double>,
+      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double, 1024>,
                                     cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     }
     attr = true;
@@ -540,13 +550,31 @@ static size_t rows_smem(const PrArgs<V>& a) {
   return static_cast<size_t>(a.hot) * sizeof(V);
 }
 
+template <typename V>
+static int rows_block(const PrArgs<V>& a) {
+  return a.hot > 0 ? 1024 : kPrThreads;
+}
+template <typename V>
+static void* rows_fn(const PrArgs<V>& a) {
+  return a.hot > 0 ? reinterpret_cast<void*>(k_pr_rows<V, 1024>)
+                   : reinterpret_cast<void*>(k_pr_rows<V, kPrThreads>);
+}
+
 // persistent grid: SMs x resident CTAs for this shared-memory footprint
 template <typename V>
 static int rows_grid(const PrArgs<V>& a) {
   int per_sm = 0;
-  GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_rows<V>, kPrThreads,
+  GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_fn<V>(a), rows_block<V>(a),
                                                          rows_smem<V>(a)));
   return device_sms() * std::max(per_sm, 1);
+}
+
+template <typename V>
+static void launch_rows(const PrArgs<V>& a, cudaStream_t s) {
+  if (a.hot > 0)
+    k_pr_rows<V, 1024><<<a.grid_rows, 1024, rows_smem<V>(a), s>>>(a);
+  else
+    k_pr_rows<V, kPrThreads><<<a.grid_rows, kPrThreads, 0, s>>>(a);
 }
 
 template <typename V>
@@ -577,7 +605,7 @@ static PrArgs<V> make_args(PrPlan& P, double damping, double tol, int itermax) {
   a.ctl = P.ctl.p;
   a.fin_cnt = P.blk_cnt.p;
   a.row0 = 0;
-  a.hot = std::min<int64_t>(P.n, hot_bytes() / static_cast<int64_t>(sizeof(V)));
+  a.hot = std::min<int64_t>(P.n, hot_bytes() / static_cast<int64_t>(sizeof(V))) & ~int64_t(3);
   a.l1hot = std::min<int64_t>(P.n, l1_hot_bytes() / static_cast<int64_t>(sizeof(V)));
   a.grid_rows = rows_grid<V>(a);
   a.damping = damping;
@@ -625,9 +653,9 @@ static bool build_graph(PrPlan& P, double damping, double tol, int itermax) {
   cudaGraphNode_t kn_rows = nullptr, kn_fin = nullptr;
   if (ok) {
     cudaKernelNodeParams kp = {};
-    kp.func = reinterpret_cast<void*>(k_pr_rows<V>);
+    kp.func = rows_fn<V>(a);
     kp.gridDim = dim3(a.grid_rows);
-    kp.blockDim = dim3(kPrThreads);
+    kp.blockDim = dim3(rows_block<V>(a));
     kp.sharedMemBytes = static_cast<unsigned>(rows_smem<V>(a));
     kp.kernelParams = params;
     ok = cudaGraphAddKernelNode(&kn_rows, body, nullptr, 0, &kp) == cudaSuccess;
@@ -676,7 +704,7 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
     while (!done && launched < itermax) {
       const int chunk = std::min(4, itermax - launched);
       for (int c = 0; c < chunk; ++c) {
-        k_pr_rows<V><<<a.grid_rows, kPrThreads, rows_smem<V>(a), s>>>(a);
+        launch_rows<V>(a, s);
         k_pr_finish<V, false><<<P.grid_fin, kPrThreads, 0, s>>>(a);
         GBX_LAUNCHED();
       }
@@ -811,7 +839,7 @@ void pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, do
   a.grid_rows = rows_grid<float>(a);
   GBX_CUDA(cudaMemsetAsync(P.ctl.p, 0, 2 * sizeof(int), s));
   GBX_CUDA(cudaMemsetAsync(P.blk_cnt.p, 0, sizeof(unsigned), s));
-  k_pr_rows<float><<<a.grid_rows, kPrThreads, 0, s>>>(a);
+  launch_rows<float>(a, s);
   k_pr_finish<float, false><<<P.grid_fin, kPrThreads, 0, s>>>(a);
   GBX_LAUNCHED();
   GBX_CUDA(cudaMemcpyAsync(l1, P.l1_hist.p, sizeof(double), cudaMemcpyDeviceToDevice, s));
