@@ -102,6 +102,11 @@ struct SsspPlan {
   DevArray<int32_t> q[2], far[2], stamp;
   DevArray<int> ctl;
   DevArray<unsigned long long> lohi, relax;
+  // circular buckets (bucketed variant)
+  DevArray<int32_t> bq;
+  DevArray<uint32_t> bbits;
+  DevArray<int> bcnt;
+  int nb_alloc = 0;
 };
 
 // Betweenness workspaces (bc.cu).

@@ -8,8 +8,11 @@
 // (SURVEY.md §7 hard part 4): a near/far bucketed label-correcting sweep.
 //   * near queue: vertices whose tentative distance fell into the current
 //     bucket; each level relaxes all their edges with atomicMin on the
-//     distance word; improvements below hi re-enter the near queue (deduped
-//     by a per-vertex stamp), improvements above go to the far pile;
+//     distance word; improvements below hi re-enter the near queue, the rest
+//     go to the far pile, each deduplicated by a parity-alternating bitmap
+//     (n/8 bytes: L2-resident; the iteration that pops a queue clears its bits);
+//   * the distance array is pinned in L2 with an access-policy window while
+//     the edge stream bypasses L1;
 //   * when the near queue drains, the bucket jumps to floor(min far / delta)
 //     * delta (the reference's jump, sssp.cpp:60-65) and the far pile is
 //     split into the new near queue and what stays far -- all on the device;
@@ -23,6 +26,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <vector>
@@ -60,7 +64,8 @@ template <> struct DistTraits<unsigned long long> {
 struct PackedEdges {
   const uint32_t* e;
   __device__ __forceinline__ void get(int64_t p, int32_t& v, uint32_t& w) const {
-    uint32_t x = __ldg(e + p);
+    uint32_t x;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(x) : "l"(e + p));
     v = static_cast<int32_t>(x >> 8);
     w = x & 0xffu;
   }
@@ -93,8 +98,8 @@ struct SsspArgs {
   int32_t* q1;
   int32_t* f0;
   int32_t* f1;
-  int32_t* qmark;  // stamp of the last near iteration that queued the vertex
-  int32_t* fmark;  // stamp of the bucket epoch whose far pile holds the vertex
+  uint32_t* qbits[2];  // near-queue membership, alternating per near iteration
+  uint32_t* fbits[2];  // far-pile membership, alternating per bucket epoch
   int* ctl;        // [0] |Q| [1] |Qnext| [2] |F| [3] |Fnext| [4] near iterations [5] buckets
   D* lohi;         // [0] lo [1] hi [2] min far (scratch)
   unsigned long long* relax;  // edges relaxed
@@ -138,8 +143,9 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int64_t gsize = int64_t(gridDim.x) * blockDim.x;
-  int stamp = 1;       // near-queue epoch (one per near iteration)
-  int bstamp = 1;      // far-pile epoch (one per bucket): a vertex sits in the pile once
+  int qp = 1;          // parity of the near-queue bitmap receiving pushes (the
+                       // source sits in bitmap 0, released when it is popped)
+  int fp = 0;          // parity of the far-pile bitmap of the current bucket epoch
   int pq = 0, pf = 0;  // parity of the current near queue / far pile
   for (;;) {
     // ---------------- near iterations inside the bucket
@@ -153,32 +159,53 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
       unsigned long long nrel = 0;
       nearq.reset(qn, &a.ctl[1]);
       farq.reset(fc, &a.ctl[2]);
-      for (int64_t base = gwarp * 4; base < nq; base += nwarps * 4) {
-        const int64_t qi = base + grp;
+      // 4 lanes per queued vertex (8 vertices per warp), each lane relaxing 4
+      // edges per round: 4 independent edge -> dist -> atomicMin chains
+      const int g4 = lane >> 2, s4 = lane & 3;
+      for (int64_t base = gwarp * 8; base < nq; base += nwarps * 8) {
+        const int64_t qi = base + g4;
         bool active = qi < nq;
         int32_t u = active ? qc[qi] : 0;
-        int64_t p = active ? a.rp[u] : 0, e = active ? a.rp[u + 1] : 0;
+        // u was queued through the other near bitmap: release its bit
+        if (active && s4 == 0) atomicAnd(&a.qbits[qp ^ 1][u >> 5], ~(1u << (u & 31)));
+        int64_t p = active ? a.rp[u] : 0;
+        const int64_t e = active ? a.rp[u + 1] : 0;
         const D du = active ? *(volatile D*)&a.dist[u] : D(0);
         while (__any_sync(kFullW, active)) {
-          bool near_push = false, far_push = false;
-          int32_t v = 0;
-          if (active && p + sub < e) {
-            W w;
-            a.edges.get(p + sub, v, w);
-            ++nrel;
-            const D nd = DistTraits<D>::add(du, w);
-            if (nd < *(volatile D*)&a.dist[v]) {
-              const D old = atomicMin(&a.dist[v], nd);
-              if (nd < old) {
-                if (nd < hi) near_push = atomicExch(&a.qmark[v], stamp) != stamp;
-                else far_push = atomicExch(&a.fmark[v], bstamp) != bstamp;
+          int32_t v[4];
+          D nd[4];
+          bool ok[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int64_t q = p + s4 + 4 * t;
+            ok[t] = active && q < e;
+            W w = W(0);
+            v[t] = 0;
+            if (ok[t]) a.edges.get(q, v[t], w);
+            nd[t] = DistTraits<D>::add(du, w);
+          }
+          D cur[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) cur[t] = ok[t] ? *(volatile D*)&a.dist[v[t]] : D(0);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            bool near_push = false, far_push = false;
+            if (ok[t]) {
+              ++nrel;
+              if (nd[t] < cur[t]) {
+                const D old = atomicMin(&a.dist[v[t]], nd[t]);
+                if (nd[t] < old) {
+                  const uint32_t bit = 1u << (v[t] & 31);
+                  if (nd[t] < hi) near_push = !(atomicOr(&a.qbits[qp][v[t] >> 5], bit) & bit);
+                  else far_push = !(atomicOr(&a.fbits[fp][v[t] >> 5], bit) & bit);
+                }
               }
             }
+            nearq.push(near_push, v[t]);
+            farq.push(far_push, v[t]);
           }
-          nearq.push(near_push, v);
-          farq.push(far_push, v);
           if (active) {
-            p += 8;
+            p += 16;
             if (p >= e) active = false;
           }
         }
@@ -193,7 +220,7 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
         a.ctl[4] += 1;
       }
       pq ^= 1;
-      ++stamp;
+      qp ^= 1;
       grid.sync();
     }
     // ---------------- bucket jump: min over the far pile at or above hi
@@ -231,10 +258,12 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
       int32_t v = 0;
       if (i < nf) {
         v = fc[i];
+        const uint32_t bit = 1u << (v & 31);
+        atomicAnd(&a.fbits[fp][v >> 5], ~bit);  // leaves this epoch's pile
         const D d = *(volatile D*)&a.dist[v];
         if (d >= hi) {
-          if (d < hi2) to_near = atomicExch(&a.qmark[v], stamp) != stamp;
-          else to_far = atomicExch(&a.fmark[v], bstamp + 1) != bstamp + 1;
+          if (d < hi2) to_near = !(atomicOr(&a.qbits[qp][v >> 5], bit) & bit);
+          else to_far = !(atomicOr(&a.fbits[fp ^ 1][v >> 5], bit) & bit);
         }
       }
       nearq.push(to_near, v);
@@ -252,17 +281,239 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
       a.ctl[5] += 1;
     }
     pf ^= 1;
-    ++bstamp;
-    ++stamp;
+    fp ^= 1;
+    qp ^= 1;  // the new near queue was marked in qbits[qp]: popped next, released there
+    grid.sync();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Circular-bucket variant (used when NB = pow2 >= 2 + max_w / delta <= 64):
+// an improvement nd >= hi goes straight into bucket floor(nd/delta) mod NB (it
+// cannot be more than max_w/delta buckets ahead of the current one), so a
+// bucket jump reads ONE bucket instead of rescanning a far pile.
+// ---------------------------------------------------------------------------
+template <typename D>
+__device__ __forceinline__ int64_t bucket_of(D d, double delta);
+template <>
+__device__ __forceinline__ int64_t bucket_of<uint32_t>(uint32_t d, double delta) {
+  return static_cast<int64_t>(floor(static_cast<double>(d) / delta));
+}
+template <>
+__device__ __forceinline__ int64_t bucket_of<unsigned long long>(unsigned long long d,
+                                                                 double delta) {
+  return static_cast<int64_t>(floor(__longlong_as_double(static_cast<long long>(d)) / delta));
+}
+
+template <typename D, typename E>
+struct SsspBArgs {
+  const int64_t* rp;
+  E edges;
+  int64_t n;
+  double delta;
+  int nb;              // buckets (power of two)
+  int64_t cap;         // entries per bucket array
+  D* dist;
+  int32_t* q0;
+  int32_t* q1;
+  int32_t* bq;         // [nb][cap]
+  int* bcnt;           // [nb]
+  uint32_t* qbits[2];  // near-queue membership (parity per near iteration)
+  uint32_t* bbits;     // [nb][words] bucket membership
+  int64_t words;
+  int* ctl;            // [0] |Q| [1] |Qnext| [4] near iterations [5] buckets
+  unsigned long long* relax;
+  int trace;
+};
+
+// stages (vertex, bucket) pushes; one atomic per distinct bucket per 32 entries
+template <int CAP>
+struct BucketQueue {
+  int32_t* bv;
+  int32_t* bb;
+  int n;
+  __device__ __forceinline__ void flush(int32_t* bq, int64_t cap, int* bcnt) {
+    __syncwarp();
+    const int lane = threadIdx.x & 31;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      const bool ok = i < n;
+      const int32_t v = ok ? bv[i] : 0;
+      const int b = ok ? bb[i] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      const int leader = __ffs(peers) - 1;
+      int base = 0;
+      if (ok && lane == leader) base = atomicAdd(&bcnt[b], __popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (ok) bq[static_cast<int64_t>(b) * cap + base + __popc(peers & ((1u << lane) - 1))] = v;
+    }
+    __syncwarp();
+    n = 0;
+  }
+  __device__ __forceinline__ void push(bool has, int32_t v, int b, int32_t* bq, int64_t cap,
+                                       int* bcnt) {
+    const unsigned m = __ballot_sync(0xffffffffu, has);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    if (has) {
+      const int pos = n + __popc(m & ((1u << lane) - 1));
+      bv[pos] = v;
+      bb[pos] = b;
+    }
+    n += __popc(m);
+    if (n > CAP - 32) flush(bq, cap, bcnt);
+  }
+};
+
+template <typename D, typename E, typename W>
+__global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ int32_t s_near[kSsspWarps][kSsspBuf];
+  __shared__ int32_t s_bv[kSsspWarps][kSsspBuf];
+  __shared__ int32_t s_bb[kSsspWarps][kSsspBuf];
+  WarpQueue<int32_t, kSsspBuf> nearq;
+  BucketQueue<kSsspBuf> bucq;
+  nearq.buf = s_near[threadIdx.x >> 5];
+  bucq.bv = s_bv[threadIdx.x >> 5];
+  bucq.bb = s_bb[threadIdx.x >> 5];
+  bucq.n = 0;
+  const int lane = threadIdx.x & 31;
+  const int g4 = lane >> 2, s4 = lane & 3;
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int nbm = a.nb - 1;
+  int64_t k = 0;      // current bucket (absolute index)
+  int qp = 1, pq = 0;
+  const bool trace = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
+  for (int guard = 0;; ++guard) {
+    if (guard > (1 << 28)) break;
+    // ---------------- near iterations inside bucket k
+    for (;;) {
+      const int nq = *(volatile int*)&a.ctl[0];
+      if (trace) printf("near k=%lld nq=%d pq=%d qp=%d\n", (long long)k, nq, pq, qp);
+      if (nq == 0) break;
+      const int32_t* qc = pq ? a.q1 : a.q0;
+      int32_t* qn = pq ? a.q0 : a.q1;
+      unsigned long long nrel = 0;
+      nearq.reset(qn, &a.ctl[1]);
+      for (int64_t base = gwarp * 8; base < nq; base += nwarps * 8) {
+        const int64_t qi = base + g4;
+        bool active = qi < nq;
+        const int32_t u = active ? qc[qi] : 0;
+        if (active && s4 == 0) atomicAnd(&a.qbits[qp ^ 1][u >> 5], ~(1u << (u & 31)));
+        int64_t p = active ? a.rp[u] : 0;
+        const int64_t e = active ? a.rp[u + 1] : 0;
+        const D du = active ? *(volatile D*)&a.dist[u] : D(0);
+        while (__any_sync(kFullW, active)) {
+          int32_t v[4];
+          D nd[4];
+          bool ok[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int64_t q = p + s4 + 4 * t;
+            ok[t] = active && q < e;
+            W w = W(0);
+            v[t] = 0;
+            if (ok[t]) a.edges.get(q, v[t], w);
+            nd[t] = DistTraits<D>::add(du, w);
+          }
+          D cur[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) cur[t] = ok[t] ? *(volatile D*)&a.dist[v[t]] : D(0);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            bool near_push = false, buck_push = false;
+            int bidx = 0;
+            if (ok[t]) {
+              ++nrel;
+              if (nd[t] < cur[t]) {
+                const D old = atomicMin(&a.dist[v[t]], nd[t]);
+                if (nd[t] < old) {
+                  const uint32_t bit = 1u << (v[t] & 31);
+                  const int64_t kb = bucket_of<D>(nd[t], a.delta);
+                  if (kb <= k) {
+                    near_push = !(atomicOr(&a.qbits[qp][v[t] >> 5], bit) & bit);
+                  } else {
+                    bidx = static_cast<int>(kb & nbm);
+                    buck_push = !(atomicOr(&a.bbits[bidx * a.words + (v[t] >> 5)], bit) & bit);
+                  }
+                }
+              }
+            }
+            nearq.push(near_push, v[t]);
+            bucq.push(buck_push, v[t], bidx, a.bq, a.cap, a.bcnt);
+          }
+          if (active) {
+            p += 16;
+            if (p >= e) active = false;
+          }
+        }
+      }
+      nearq.flush();
+      bucq.flush(a.bq, a.cap, a.bcnt);
+      if (nrel) atomicAdd(a.relax, nrel);
+      grid.sync();
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ctl[0] = a.ctl[1];
+        a.ctl[1] = 0;
+        a.ctl[4] += 1;
+      }
+      pq ^= 1;
+      qp ^= 1;
+      grid.sync();
+    }
+    // ---------------- jump to the next non-empty bucket (at most nb-1 ahead):
+    // one thread decides, everyone reads the decision after a grid barrier
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      int jj = 1;
+      for (; jj < a.nb; ++jj)
+        if (*(volatile int*)&a.bcnt[(k + jj) & nbm] > 0) break;
+      a.ctl[6] = jj;
+      a.ctl[7] = jj < a.nb ? *(volatile int*)&a.bcnt[(k + jj) & nbm] : 0;
+    }
+    grid.sync();
+    const int j = *(volatile int*)&a.ctl[6];
+    if (trace) printf("jump k=%lld j=%d\n", (long long)k, j);
+    if (j >= a.nb) break;
+    k += j;
+    const int b = static_cast<int>(k & nbm);
+    const int cnt = *(volatile int*)&a.ctl[7];
+    const int32_t* src = a.bq + static_cast<int64_t>(b) * a.cap;
+    int32_t* qn = pq ? a.q1 : a.q0;  // current (empty) near queue
+    nearq.reset(qn, &a.ctl[0]);
+    for (int64_t base = gwarp * 32; base < cnt; base += nwarps * 32) {
+      const int64_t i = base + lane;
+      bool to_near = false;
+      int32_t v = 0;
+      if (i < cnt) {
+        v = src[i];
+        const uint32_t bit = 1u << (v & 31);
+        atomicAnd(&a.bbits[b * a.words + (v >> 5)], ~bit);
+        // stale entries (improved into an earlier bucket since) are skipped
+        if (bucket_of<D>(*(volatile D*)&a.dist[v], a.delta) == k)
+          to_near = !(atomicOr(&a.qbits[qp][v >> 5], bit) & bit);
+      }
+      nearq.push(to_near, v);
+    }
+    nearq.flush();
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.bcnt[b] = 0;
+      a.ctl[5] += 1;
+    }
+    qp ^= 1;
     grid.sync();
   }
 }
 
 template <typename D>
-__global__ void k_sssp_init(D* dist, int32_t* qmark, int64_t n, int32_t src, int32_t* q0, int* ctl,
+__global__ void k_sssp_init(D* dist, uint32_t* bits, int64_t n, int32_t src, int32_t* q0, int* ctl,
                             D* lohi, unsigned long long* relax, D hi0, D inf) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < n) { dist[i] = i == src ? D(0) : inf; qmark[i] = 0; qmark[n + i] = 0; }
+  if (i < n) dist[i] = i == src ? D(0) : inf;
+  const int64_t words = (n + 31) / 32;
+  if (i < 4 * words) bits[i] = 0u;
+  if (i == 0) bits[src >> 5] |= 1u << (src & 31);  // the source sits in near queue 0
   if (i == 0) {
     q0[0] = src;
     for (int k = 0; k < 8; ++k) ctl[k] = 0;
@@ -379,7 +630,7 @@ void sssp_prepare(gbx_graph* g) {
   const int64_t fcap = A.n + 1;  // <= one entry per vertex per bucket epoch
   P->far[0].alloc(fcap);
   P->far[1].alloc(fcap);
-  P->stamp.alloc(2 * n1);  // near stamps, then far stamps
+  P->stamp.alloc(4 * ((n1 + 31) / 32));  // 2 near + 2 far membership bitmaps
   P->ctl.alloc(8);
   P->lohi.alloc(3);
   P->relax.alloc(1);
@@ -393,7 +644,9 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
   cudaStream_t s = g->stream;
   const int64_t n = P.n;
   D* lohi = reinterpret_cast<D*>(P.lohi.p);
-  k_sssp_init<D><<<ceil_div(n, 256), 256, 0, s>>>(dist, P.stamp.p, n, src, P.q[0].p, P.ctl.p,
+  uint32_t* bits = reinterpret_cast<uint32_t*>(P.stamp.p);
+  const int64_t words = (n + 31) / 32;
+  k_sssp_init<D><<<ceil_div(std::max<int64_t>(n, 4 * words), 256), 256, 0, s>>>(dist, bits, n, src, P.q[0].p, P.ctl.p,
                                                    lohi, P.relax.p, hi0, inf);
   GBX_LAUNCHED();
   SsspArgs<D, E> a{};
@@ -406,19 +659,85 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
   a.q1 = P.q[1].p;
   a.f0 = P.far[0].p;
   a.f1 = P.far[1].p;
-  a.qmark = P.stamp.p;
-  a.fmark = P.stamp.p + n;
+  a.qbits[0] = bits;
+  a.qbits[1] = bits + words;
+  a.fbits[0] = bits + 2 * words;
+  a.fbits[1] = bits + 3 * words;
   a.ctl = P.ctl.p;
   a.lohi = lohi;
   a.relax = P.relax.p;
-  auto fn = k_sssp<D, E, W>;
-  int per_sm = 0;
-  GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSsspThreads, 0));
-  if (per_sm < 1) fail(GBX_CUDA_ERROR, "sssp kernel does not fit on an SM");
-  const int grid = device_sms() * per_sm;
-  void* args[] = {&a};
-  GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid),
-                                       dim3(kSsspThreads), args, 0, s));
+  // keep the distance array resident in L2 while the edges stream past it
+  {
+    int max_persist = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, g->device);
+    const size_t bytes = static_cast<size_t>(n) * sizeof(D);
+    if (max_persist > 0) {
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, max_persist));
+      cudaStreamAttrValue at = {};
+      at.accessPolicyWindow.base_ptr = dist;
+      at.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, max_persist);
+      at.accessPolicyWindow.hitRatio = 1.0f;
+      at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &at);
+    }
+    (void)cudaGetLastError();  // persistence is an optimisation: never fail on it
+  }
+  // circular buckets when no improvement can land more than nb-1 buckets ahead
+  int nb = 1;
+  const double span = 2.0 + P.max_w / delta;
+  while (nb < span && nb <= 64) nb <<= 1;
+  if (nb <= 64 && !std::getenv("GBX_SSSP_NEARFAR")) {
+    const int64_t cap = n + 1;
+    if (static_cast<int>(P.bcnt.n) < nb || P.nb_alloc < nb) {
+      P.bq.alloc(static_cast<size_t>(nb) * cap);
+      P.bbits.alloc(static_cast<size_t>(nb) * std::max<int64_t>(words, 1));
+      P.bcnt.alloc(nb);
+      P.nb_alloc = nb;
+    }
+    GBX_CUDA(cudaMemsetAsync(P.bbits.p, 0, P.bbits.bytes(), s));
+    GBX_CUDA(cudaMemsetAsync(P.bcnt.p, 0, P.bcnt.bytes(), s));
+    SsspBArgs<D, E> b{};
+    b.rp = a.rp;
+    b.edges = edges;
+    b.n = n;
+    b.delta = delta;
+    b.nb = nb;
+    b.cap = cap;
+    b.dist = dist;
+    b.q0 = a.q0;
+    b.q1 = a.q1;
+    b.bq = P.bq.p;
+    b.bcnt = P.bcnt.p;
+    b.qbits[0] = a.qbits[0];
+    b.qbits[1] = a.qbits[1];
+    b.bbits = P.bbits.p;
+    b.words = words;
+    b.ctl = a.ctl;
+    b.relax = a.relax;
+    b.trace = std::getenv("GBX_SSSP_TRACE") ? 1 : 0;
+    auto fnb = k_sssp_b<D, E, W>;
+    int per_sm = 0;
+    GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fnb, kSsspThreads, 0));
+    if (per_sm < 1) fail(GBX_CUDA_ERROR, "sssp kernel does not fit on an SM");
+    const int grid = device_sms() * per_sm;
+    void* args[] = {&b};
+    GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fnb), dim3(grid),
+                                         dim3(kSsspThreads), args, 0, s));
+  } else {
+    auto fn = k_sssp<D, E, W>;
+    int per_sm = 0;
+    GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSsspThreads, 0));
+    if (per_sm < 1) fail(GBX_CUDA_ERROR, "sssp kernel does not fit on an SM");
+    const int grid = device_sms() * per_sm;
+    void* args[] = {&a};
+    GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid),
+                                         dim3(kSsspThreads), args, 0, s));
+  }
+  cudaStreamAttrValue off = {};
+  off.accessPolicyWindow.num_bytes = 0;
+  cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &off);
+  (void)cudaGetLastError();
 }
 
 void sssp_run(gbx_graph* g, uint64_t source, double delta, double* out) {
