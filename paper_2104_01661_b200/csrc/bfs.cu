@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -295,7 +297,20 @@ struct Bfs64Args {
   int64_t* q1;
   int* ctl;  // [0] entries [1] vertices [2] next entries [3] next vertices [5] levels [6] push
   unsigned long long* edges;  // [0] frontier edges cur, [1] next
+  unsigned long long* tlog;   // optional: %globaltimer at phase boundaries (debug)
+  int pull_div;               // pull once frontier edges >= nnz / pull_div
+  const int32_t* heavy;       // vertices with in-degree > kBfsHeavy
+  int64_t nheavy;
 };
+
+// In-degree above which a pull row goes to a whole warp instead of 8 lanes.
+constexpr int64_t kBfsHeavy = 256;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
   cg::grid_group grid = cg::this_grid();
@@ -312,7 +327,14 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
     const int qv = *(volatile int*)&a.ctl[1];
     const unsigned long long fe = *(volatile unsigned long long*)&a.edges[0];
     if (qv == 0) break;
-    const bool push = fe * 20ull < static_cast<unsigned long long>(a.nnz) + 20ull;
+    // 64 lanes rarely satisfy every source bit early in a pull (and hub rows
+    // straggle in one group), so push until the frontier edges reach nnz/2
+    const bool push = fe * static_cast<unsigned long long>(a.pull_div) <
+                      static_cast<unsigned long long>(a.nnz) + 1ull;
+    if (a.tlog && blockIdx.x == 0 && threadIdx.x == 0) {
+      a.tlog[4 * d] = gtimer();
+      a.tlog[4 * d + 3] = (push ? 1ull : 0ull) | (static_cast<unsigned long long>(qv) << 8);
+    }
     const int p = (d - 1) & 1;
     const int64_t* qc = p ? a.q1 : a.q0;
     int64_t* qn = p ? a.q0 : a.q1;
@@ -355,6 +377,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
         unsigned long long need = w < a.n ? (~a.seen[w] & a.lanes) : 0ull;
         bool active = need != 0ull;
         int64_t pp = active ? a.trp[w] : 0, pe = active ? a.trp[w + 1] : 0;
+        if (pe - pp > kBfsHeavy) active = false;  // hub: the warp pass below
         unsigned long long found = 0ull;
         while (__any_sync(kFull, active)) {
           int32_t u = -1;
@@ -392,9 +415,49 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
         if (has) fn[w] = found;
         fq.push(has, static_cast<int32_t>(w));
       }
+      // hubs: one warp per vertex, 32 in-neighbours per step, lowest lane
+      // (smallest neighbour id) claims each source bit as in the groups above
+      for (int64_t h = gwarp; h < a.nheavy; h += nwarps) {
+        const int32_t w = a.heavy[h];
+        unsigned long long need = ~a.seen[w] & a.lanes;
+        unsigned long long found = 0ull;
+        if (need) {
+          const int64_t pe = a.trp[w + 1];
+          for (int64_t pp = a.trp[w]; pp < pe; pp += 32) {
+            int32_t u = -1;
+            unsigned long long hit = 0ull;
+            if (pp + lane < pe) {
+              u = __ldg(a.tcol + pp + lane);
+              hit = __ldg(fc + u) & need;
+            }
+            unsigned long long incl = hit;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              unsigned long long t = __shfl_up_sync(kFull, incl, o);
+              if (lane >= o) incl |= t;
+            }
+            unsigned long long excl = __shfl_up_sync(kFull, incl, 1);
+            if (lane == 0) excl = 0ull;
+            unsigned long long mine = hit & ~excl;
+            const unsigned long long tot = __shfl_sync(kFull, incl, 31);
+            while (mine) {
+              int b = __ffsll(static_cast<long long>(mine)) - 1;
+              mine &= mine - 1;
+              a.mparent[static_cast<int64_t>(w) * 64 + b] = u;
+            }
+            found |= tot;
+            need &= ~tot;
+            if (need == 0ull) break;
+          }
+        }
+        const bool has = lane == 0 && found != 0ull;
+        if (has) fn[w] = found;
+        fq.push(has, w);
+      }
     }
     fq.flush();
     grid.sync();
+    if (a.tlog && blockIdx.x == 0 && threadIdx.x == 0) a.tlog[4 * d + 1] = gtimer();
     // finalize: new frontier bits become seen + level d; old frontier cleared
     const int qn_e = *(volatile int*)&a.ctl[2];
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < qn_e;
@@ -425,9 +488,15 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
       if (push) a.ctl[6] += 1;
       a.edges[0] = a.edges[1];
       a.edges[1] = 0ull;
+      if (a.tlog) a.tlog[4 * d + 2] = gtimer();
     }
     grid.sync();
   }
+}
+
+__global__ void k_bfs64_heavy(const int64_t* trp, int64_t n, int32_t* out, int* cnt) {
+  int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (v < n && trp[v + 1] - trp[v] > kBfsHeavy) out[atomicAdd(cnt, 1)] = static_cast<int32_t>(v);
 }
 
 __global__ void k_bfs64_init(unsigned long long* seen, unsigned long long* f0,
@@ -438,15 +507,37 @@ __global__ void k_bfs64_init(unsigned long long* seen, unsigned long long* f0,
   if (i < n * 64) { mlevel[i] = -1; mparent[i] = INT_MAX; }
 }
 
-__global__ void k_bfs64_seed(const int32_t* src, int ns, unsigned long long* seen,
-                             unsigned long long* f0, int32_t* mlevel, int32_t* mparent) {
-  for (int b = 0; b < ns; ++b) {
-    int32_t s = src[b];
-    seen[s] |= 1ull << b;
-    f0[s] |= 1ull << b;
-    mlevel[static_cast<int64_t>(s) * 64 + b] = 0;
-    mparent[static_cast<int64_t>(s) * 64 + b] = s;
+// One warp per distinct source: set its lane bits, then emit its degree chunks
+// into the level-1 queue (ctl[0] entries, ctl[1] vertices, edges[0] edges).
+// src[0..ns) are the batch lanes, src[ns..ns+nu) the distinct sources.
+__global__ void k_bfs64_seed(const int32_t* src, int ns, int nu, const int64_t* rp,
+                             unsigned long long* seen, unsigned long long* f0, int32_t* mlevel,
+                             int32_t* mparent, int64_t* q, int* ctl,
+                             unsigned long long* edges) {
+  const int u = blockIdx.x;
+  const int lane = threadIdx.x;
+  const int32_t v = src[ns + u];
+  if (lane == 0) {
+    unsigned long long bits = 0ull;
+    for (int b = 0; b < ns; ++b)
+      if (src[b] == v) {
+        bits |= 1ull << b;
+        mlevel[static_cast<int64_t>(v) * 64 + b] = 0;
+        mparent[static_cast<int64_t>(v) * 64 + b] = v;
+      }
+    seen[v] = bits;
+    f0[v] = bits;
   }
+  const int64_t deg = rp[v + 1] - rp[v];
+  const int64_t k = deg <= kChunk ? 1 : (deg + kChunk - 1) / kChunk;
+  int base = 0;
+  if (lane == 0) {
+    base = atomicAdd(&ctl[0], static_cast<int>(k));
+    atomicAdd(&ctl[1], 1);
+    atomicAdd(edges, static_cast<unsigned long long>(deg));
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int64_t c = lane; c < k; c += 32) q[base + c] = (c << 32) | v;
 }
 
 // [n][64] int32 -> [ns][n] int64 (-1 for none)
@@ -482,6 +573,26 @@ static void ensure_bfs64(gbx_graph* g) {
   W.mqueue[0].alloc(2 * qcap);
   W.mqueue[1].alloc(2 * qcap);
   W.mctl.alloc(12);
+  W.msrc.alloc(128);
+}
+
+// hub list for the pull pass, rebuilt when the transpose changes
+static void ensure_bfs64_heavy(gbx_graph* g, const Csr& AT) {
+  BfsWork& W = *g->bfs;
+  if (W.heavy_key == AT.rp.p && W.heavy_nnz == AT.nnz && W.heavy.p) return;
+  const int64_t n = AT.n;
+  cudaStream_t s = g->stream;
+  W.heavy.alloc(std::max<int64_t>(n, 1));
+  GBX_CUDA(cudaMemsetAsync(W.mctl.p, 0, sizeof(int), s));
+  k_bfs64_heavy<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, s>>>(AT.rp.p, n, W.heavy.p,
+                                                                      W.mctl.p);
+  GBX_LAUNCHED();
+  int c = 0;
+  GBX_CUDA(cudaMemcpyAsync(&c, W.mctl.p, sizeof c, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  W.nheavy = c;
+  W.heavy_key = AT.rp.p;
+  W.heavy_nnz = AT.nnz;
 }
 
 void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* parent,
@@ -497,6 +608,7 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
   cudaStream_t s = g->stream;
   const Csr& A = g->A;
   const Csr& AT = g->AT();
+  ensure_bfs64_heavy(g, AT);
   static int grid = 0;
   if (!grid) grid = coop_grid(reinterpret_cast<const void*>(k_bfs64), kBfsThreads);
   int64_t total_launches = 0;
@@ -505,39 +617,23 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
     k_bfs64_init<<<ceil_div(n * 64, 256), 256, 0, s>>>(W.seen.p, W.front.p, W.next.p,
                                                        W.mlevel.p, W.mparent.p, n);
     GBX_LAUNCHED();
-    // initial queue: distinct source vertices, chunked by degree
+    // lanes then distinct sources; the seed kernel builds the level-1 queue
     std::vector<int32_t> src(nb);
     for (int b = 0; b < nb; ++b) src[b] = static_cast<int32_t>(sources[b0 + b]);
-    std::vector<int64_t> rph(2);
     std::vector<int32_t> uniq(src);
     std::sort(uniq.begin(), uniq.end());
     uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-    std::vector<int64_t> q;
-    unsigned long long fedges = 0;
-    for (int32_t v : uniq) {
-      int64_t r[2];
-      GBX_CUDA(cudaMemcpyAsync(r, A.rp.p + v, 16, cudaMemcpyDeviceToHost, s));
-      GBX_CUDA(cudaStreamSynchronize(s));
-      int64_t deg = r[1] - r[0];
-      fedges += deg;
-      int64_t k = deg <= kChunk ? 1 : (deg + kChunk - 1) / kChunk;
-      for (int64_t c = 0; c < k; ++c) q.push_back((c << 32) | v);
-    }
-    int32_t* dsrc = nullptr;
-    GBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dsrc), nb * sizeof(int32_t), s));
-    GBX_CUDA(cudaMemcpyAsync(dsrc, src.data(), nb * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    k_bfs64_seed<<<1, 1, 0, s>>>(dsrc, nb, W.seen.p, W.front.p, W.mlevel.p, W.mparent.p);
-    GBX_LAUNCHED();
+    const int nu = static_cast<int>(uniq.size());
+    src.insert(src.end(), uniq.begin(), uniq.end());
     int64_t* q0 = reinterpret_cast<int64_t*>(W.mqueue[0].p);
     int64_t* q1 = reinterpret_cast<int64_t*>(W.mqueue[1].p);
-    GBX_CUDA(cudaMemcpyAsync(q0, q.data(), q.size() * 8, cudaMemcpyHostToDevice, s));
-    int hctl[12] = {0};
-    hctl[0] = static_cast<int>(q.size());
-    hctl[1] = static_cast<int>(uniq.size());
-    unsigned long long* edges = reinterpret_cast<unsigned long long*>(hctl + 8);
-    edges[0] = fedges;
-    edges[1] = 0;
-    GBX_CUDA(cudaMemcpyAsync(W.mctl.p, hctl, sizeof hctl, cudaMemcpyHostToDevice, s));
+    GBX_CUDA(cudaMemsetAsync(W.mctl.p, 0, 12 * sizeof(int), s));
+    GBX_CUDA(cudaMemcpyAsync(W.msrc.p, src.data(), src.size() * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, s));
+    k_bfs64_seed<<<nu, 32, 0, s>>>(W.msrc.p, nb, nu, A.rp.p, W.seen.p, W.front.p, W.mlevel.p,
+                                   W.mparent.p, q0, W.mctl.p,
+                                   reinterpret_cast<unsigned long long*>(W.mctl.p + 8));
+    GBX_LAUNCHED();
     Bfs64Args a{};
     a.rp = A.rp.p;
     a.col = A.col.p;
@@ -555,12 +651,21 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
     a.q1 = q1;
     a.ctl = W.mctl.p;
     a.edges = reinterpret_cast<unsigned long long*>(W.mctl.p + 8);
+    static const int pull_div = std::getenv("GBX_BFS64_PULLDIV") ? std::atoi(std::getenv("GBX_BFS64_PULLDIV")) : 2;
+    a.pull_div = pull_div;
+    a.heavy = W.heavy.p;
+    a.nheavy = W.nheavy;
+    static const bool tlog_on = std::getenv("GBX_BFS_TLOG") != nullptr;
+    if (tlog_on) {
+      if (!W.tlog.p) W.tlog.alloc(4 * 256);
+      GBX_CUDA(cudaMemsetAsync(W.tlog.p, 0, W.tlog.bytes(), s));
+      a.tlog = W.tlog.p;
+    }
     void* args[] = {&a};
     if (n > 1) {
       GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_bfs64), dim3(grid),
                                            dim3(kBfsThreads), args, 0, s));
     }
-    cudaFreeAsync(dsrc, s);
     total_launches += 3;
     W.ms_ns = nb;
     if (parent || level) {
@@ -581,9 +686,18 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
       }
       cudaFreeAsync(tmp, s);
     }
+    int hctl[12];
     GBX_CUDA(cudaMemcpyAsync(hctl, W.mctl.p, sizeof hctl, cudaMemcpyDeviceToHost, s));
     GBX_CUDA(cudaStreamSynchronize(s));
     g->stats.iterations = hctl[5];
+    if (tlog_on) {
+      std::vector<unsigned long long> t(4 * 256);
+      GBX_CUDA(cudaMemcpy(t.data(), W.tlog.p, t.size() * 8, cudaMemcpyDeviceToHost));
+      for (int d = 1; d < 256 && t[4 * d]; ++d)
+        std::fprintf(stderr, "bfs64 level %d %s qv=%llu work=%.1fus finalize=%.1fus\n", d,
+                     (t[4 * d + 3] & 1) ? "push" : "pull", t[4 * d + 3] >> 8,
+                     (t[4 * d + 1] - t[4 * d]) / 1e3, (t[4 * d + 2] - t[4 * d + 1]) / 1e3);
+    }
   }
   g->stats.launches = total_launches;
   g->stats.hot_launches = (ns + 63) / 64;

@@ -73,6 +73,13 @@ struct BfsWork {
   int64_t ms_ns = 0;
   DevArray<int32_t> mqueue[2];
   DevArray<int> mctl;
+  DevArray<int32_t> msrc;                   // batch lanes + distinct sources
+  DevArray<unsigned long long> tlog;
+  // pull-mode hubs (in-degree > kBfsHeavy) handled warp-per-vertex
+  DevArray<int32_t> heavy;
+  int64_t nheavy = 0;
+  const void* heavy_key = nullptr;
+  int64_t heavy_nnz = -1;
 };
 
 // Triangle counting plan (tc.cu): degree-ordered upper triangle U.
