@@ -33,11 +33,21 @@ namespace gbx {
 
 constexpr int kBfsThreads = 256;
 constexpr int kBfsBuf = 256;  // staged frontier vertices per warp
-constexpr int64_t kChunk = 1024;
+constexpr int64_t kChunk = 256;  // push: edges per warp entry (latency-bound steps)
 constexpr unsigned kFull = 0xffffffffu;
+// In-degree above which a pull row goes to a whole warp instead of 8 lanes.
+constexpr int64_t kBfsHeavy = 256;
+// Pull: 4-edge rounds a lane scans its own row before handing it to a group.
+constexpr int kThreadRounds = 2;
 
 __device__ __forceinline__ int n_chunks(int64_t deg) {
   return deg <= kChunk ? 1 : static_cast<int>((deg + kChunk - 1) / kChunk);
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 // ---------------------------------------------------------------------------
@@ -48,45 +58,73 @@ struct Bfs1Args {
   const int32_t* col;
   const int64_t* trp;
   const int32_t* tcol;
-  int64_t n;
+  int64_t n, nnz;
   int mode;
   int64_t divisor;
+  int alpha;         // AUTO also pulls once frontier edges * alpha >= nnz (0: off)
   int32_t* level;
   int32_t* parent;
   int64_t* q0;
   int64_t* q1;
   uint32_t* bm0;
   uint32_t* bm1;
+  int32_t* ul0;      // still-unvisited vertices (pull levels only scan these)
+  int32_t* ul1;
+  const int32_t* heavy;  // in-degree > kBfsHeavy: pulled by whole warps, never listed
+  int64_t nheavy;
   int* ctl;  // [0] entries [1] vertices [2] next entries [3] next vertices [4] prev vertices
-             // [5] levels done [6] push levels
+             // [5] levels done [6] push levels [8:10) u64 frontier edges [10:12) next
+             // [12] unvisited-list size (-1: not built) [13] next size [14] list parity
+  unsigned long long* tlog;  // optional: %globaltimer at phase boundaries (debug)
 };
 
 __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ int32_t s_buf[kBfsThreads / 32][kBfsBuf];
+  __shared__ int32_t s_ubuf[kBfsThreads / 32][kBfsBuf];
   FrontierQueue<kBfsBuf> fq;
   fq.buf = s_buf[threadIdx.x >> 5];
   fq.rp = a.rp;
   fq.chunk = kChunk;
+  WarpQueue<int32_t, kBfsBuf> uq;
+  uq.buf = s_ubuf[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int64_t gsize = int64_t(gridDim.x) * blockDim.x;
   const int64_t nwords = (a.n + 31) >> 5;
+  unsigned long long* edges = reinterpret_cast<unsigned long long*>(a.ctl + 8);
+  if (a.tlog && gtid == 0) a.tlog[0] = gtimer();
   for (int d = 1; static_cast<int64_t>(d) + 1 <= a.n; ++d) {
     const int qe = *(volatile int*)&a.ctl[0];
     const int qv = *(volatile int*)&a.ctl[1];
     const int pv = *(volatile int*)&a.ctl[4];
+    const unsigned long long fe = *(volatile unsigned long long*)&edges[0];
     if (qv == 0) break;
-    const bool push = a.mode == GBX_BFS_PUSH ||
-                      (a.mode == GBX_BFS_AUTO && qv < a.n / a.divisor + 1 && qv > pv);
+    // alpha == 0: the reference's rule (bfs.cpp:77-78), push while the frontier
+    // has < n/divisor + 1 vertices and grows.  alpha > 0 (default): Beamer's
+    // edge test replaces "grows" -- push while the frontier's edges are under
+    // nnz/alpha, so a 1-vertex or shrinking frontier is pushed instead of paying
+    // a scan of every unvisited row.  Results are identical either way (min-id
+    // parents in both directions); only the work differs.
+    const bool small = qv < a.n / a.divisor + 1;
+    const bool push =
+        a.mode == GBX_BFS_PUSH ||
+        (a.mode == GBX_BFS_AUTO &&
+         (a.alpha == 0 ? (small && qv > pv)
+                       : (small && fe * static_cast<unsigned long long>(a.alpha) <
+                                       static_cast<unsigned long long>(a.nnz))));
+    if (a.tlog && gtid == 0) {
+      a.tlog[4 * d] = gtimer();
+      a.tlog[4 * d + 3] = (push ? 1ull : 0ull) | (static_cast<unsigned long long>(qv) << 8);
+    }
     const int p = (d - 1) & 1;
     const int64_t* qc = p ? a.q1 : a.q0;
     int64_t* qn = p ? a.q0 : a.q1;
     const uint32_t* bc = p ? a.bm1 : a.bm0;
     uint32_t* bn = p ? a.bm0 : a.bm1;
-    fq.reset(qn, &a.ctl[2], &a.ctl[3], nullptr, nullptr);
+    fq.reset(qn, &a.ctl[2], &a.ctl[3], &edges[1], nullptr);
     if (push) {
       for (int64_t e = gwarp; e < qe; e += nwarps) {
         const int64_t ent = qc[e];
@@ -100,8 +138,11 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
           int32_t w = 0;
           if (q < e0) {
             w = __ldg(a.col + q);
-            int lw = *(volatile int32_t*)&a.level[w];
-            if (lw == -1 || lw == d) {
+            // level and parent loads issued together; min-id parent: skip the
+            // atomic when a smaller one already landed
+            const int lw = *(volatile int32_t*)&a.level[w];
+            const int32_t pw = *(volatile int32_t*)&a.parent[w];
+            if ((lw == -1 || lw == d) && v < pw) {
               atomicMin(&a.parent[w], v);
               if (lw == -1 && atomicCAS(&a.level[w], -1, d) == -1) {
                 has = true;
@@ -113,39 +154,125 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
         }
       }
     } else {
+      // scan every vertex the first time, afterwards only the ones a previous
+      // pull left unvisited (vertices with no in-edges never enter the list)
+      const int ucnt = *(volatile int*)&a.ctl[12];
+      const int upar = *(volatile int*)&a.ctl[14];
+      const int32_t* ucur = upar ? a.ul1 : a.ul0;
+      uq.reset(upar ? a.ul0 : a.ul1, &a.ctl[13]);
+      const int64_t range = ucnt < 0 ? a.n : ucnt;
       const int grp = lane >> 3, sub = lane & 7;
-      for (int64_t vb = gwarp * 4; vb < a.n; vb += nwarps * 4) {
-        const int64_t w = vb + grp;
+      // 32 vertices per warp step, one per lane: the level/row-pointer loads
+      // coalesce and every lane scans its own row 4 edges per round (the 4
+      // neighbour and 4 bitmap loads are independent); rows still unresolved
+      // after kThreadRounds rounds go to 8-lane groups, 4 rows at a time.
+      for (int64_t vb = gwarp * 32; vb < range; vb += nwarps * 32) {
+        const int64_t i = vb + lane;
+        const int64_t w = i < range ? (ucnt < 0 ? i : ucur[i]) : a.n;
         bool active = w < a.n && a.level[w] == -1;
         int64_t pp = active ? a.trp[w] : 0, pe = active ? a.trp[w + 1] : 0;
+        if (pe - pp > kBfsHeavy) active = false;  // hub: the warp pass below
+        const bool cand = active && pe > pp;
+        active = cand;
         int32_t found = -1;
-        while (__any_sync(kFull, active)) {
-          int32_t u = -1;
-          bool hit = false;
-          if (active && pp + sub < pe) {
-            u = __ldg(a.tcol + pp + sub);
-            hit = (__ldg(bc + (u >> 5)) >> (u & 31)) & 1u;
-          }
-          const unsigned bal = __ballot_sync(kFull, hit);
-          const unsigned gb = (bal >> (grp * 8)) & 0xffu;
-          const int src = grp * 8 + (gb ? __ffs(gb) - 1 : 0);
-          const int32_t uu = __shfl_sync(kFull, u, src);
+#pragma unroll 1
+        for (int r = 0; r < kThreadRounds && __any_sync(kFull, active); ++r) {
           if (active) {
-            if (gb) { found = uu; active = false; }
-            else { pp += 8; if (pp >= pe) active = false; }
+            int32_t u[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) u[k] = pp + k < pe ? __ldg(a.tcol + pp + k) : -1;
+            unsigned hits = 0u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (u[k] >= 0 && ((__ldg(bc + (u[k] >> 5)) >> (u[k] & 31)) & 1u)) hits |= 1u << k;
+            if (hits) {
+              const int k = __ffs(hits) - 1;
+              found = k == 0 ? u[0] : k == 1 ? u[1] : k == 2 ? u[2] : u[3];
+              active = false;
+            } else {
+              pp += 4;
+              if (pp >= pe) active = false;
+            }
           }
         }
-        const bool has = sub == 0 && found >= 0;
+        bool has = found >= 0;
         if (has) {
           a.level[w] = d;
           a.parent[w] = found;
           atomicOr(&bn[w >> 5], 1u << (w & 31));
         }
         fq.push(has, static_cast<int32_t>(w));
+        uq.push(cand && !active && found < 0, static_cast<int32_t>(w));
+        // long rows: 8-lane groups, 4 rows at a time, continuing at pp
+        unsigned rest = __ballot_sync(kFull, active);
+        while (rest) {
+          int src = -1;
+          unsigned m = rest;
+          for (int k = 0; k < grp && m; ++k) m &= m - 1;
+          if (m) src = __ffs(m) - 1;
+          for (int k = 0; k < 4 && rest; ++k) rest &= rest - 1;
+          const int64_t gw = __shfl_sync(kFull, w, src < 0 ? 0 : src);
+          int64_t gp = __shfl_sync(kFull, pp, src < 0 ? 0 : src);
+          const int64_t ge = __shfl_sync(kFull, pe, src < 0 ? 0 : src);
+          bool gact = src >= 0;
+          int32_t gfound = -1;
+          while (__any_sync(kFull, gact)) {
+            int32_t u = -1;
+            bool hit = false;
+            if (gact && gp + sub < ge) {
+              u = __ldg(a.tcol + gp + sub);
+              hit = (__ldg(bc + (u >> 5)) >> (u & 31)) & 1u;
+            }
+            const unsigned bal = __ballot_sync(kFull, hit);
+            const unsigned gb = (bal >> (grp * 8)) & 0xffu;
+            const int sl = grp * 8 + (gb ? __ffs(gb) - 1 : 0);
+            const int32_t uu = __shfl_sync(kFull, u, sl);
+            if (gact) {
+              if (gb) { gfound = uu; gact = false; }
+              else { gp += 8; if (gp >= ge) gact = false; }
+            }
+          }
+          const bool ghas = sub == 0 && gfound >= 0;
+          if (ghas) {
+            a.level[gw] = d;
+            a.parent[gw] = gfound;
+            atomicOr(&bn[gw >> 5], 1u << (gw & 31));
+          }
+          fq.push(ghas, static_cast<int32_t>(gw));
+          uq.push(sub == 0 && src >= 0 && gfound < 0, static_cast<int32_t>(gw));
+        }
+      }
+      uq.flush();
+      for (int64_t h = gwarp; h < a.nheavy; h += nwarps) {
+        const int32_t w = a.heavy[h];
+        if (a.level[w] != -1) continue;
+        const int64_t pe = a.trp[w + 1];
+        int32_t found = -1;
+        for (int64_t pp = a.trp[w]; pp < pe; pp += 32) {
+          int32_t u = -1;
+          bool hit = false;
+          if (pp + lane < pe) {
+            u = __ldg(a.tcol + pp + lane);
+            hit = (__ldg(bc + (u >> 5)) >> (u & 31)) & 1u;
+          }
+          const unsigned bal = __ballot_sync(kFull, hit);
+          if (bal) {
+            found = __shfl_sync(kFull, u, __ffs(bal) - 1);
+            break;
+          }
+        }
+        const bool has = lane == 0 && found >= 0;
+        if (has) {
+          a.level[w] = d;
+          a.parent[w] = found;
+          atomicOr(&bn[w >> 5], 1u << (w & 31));
+        }
+        fq.push(has, w);
       }
     }
     fq.flush();
     grid.sync();
+    if (a.tlog && gtid == 0) a.tlog[4 * d + 1] = gtimer();
     // roll the frontier: the current bitmap is cleared for reuse two levels on
     uint32_t* bclr = const_cast<uint32_t*>(bc);
     for (int64_t i = gtid; i < nwords; i += gsize) bclr[i] = 0u;
@@ -156,10 +283,20 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
       a.ctl[2] = 0;
       a.ctl[3] = 0;
       a.ctl[5] = d;
-      if (push) a.ctl[6] += 1;
+      edges[0] = edges[1];
+      edges[1] = 0ull;
+      if (push) {
+        a.ctl[6] += 1;
+      } else {
+        a.ctl[12] = a.ctl[13];
+        a.ctl[13] = 0;
+        a.ctl[14] ^= 1;
+      }
+      if (a.tlog) a.tlog[4 * d + 2] = gtimer();
     }
     grid.sync();
   }
+  if (a.tlog && gtid == 0) a.tlog[1] = gtimer();
 }
 
 __global__ void k_bfs1_init(int32_t* level, int32_t* parent, uint32_t* bm0, uint32_t* bm1,
@@ -177,9 +314,11 @@ __global__ void k_bfs1_seed(int32_t* level, int32_t* parent, uint32_t* bm0, int6
   int64_t deg = rp[s + 1] - rp[s];
   int k = n_chunks(deg);
   for (int c = 0; c < k; ++c) q0[c] = (static_cast<int64_t>(c) << 32) | s;
-  for (int i = 0; i < 8; ++i) ctl[i] = 0;
+  for (int i = 0; i < 16; ++i) ctl[i] = 0;
   ctl[0] = k;
   ctl[1] = 1;
+  *reinterpret_cast<unsigned long long*>(ctl + 8) = static_cast<unsigned long long>(deg);
+  ctl[12] = -1;
 }
 
 __global__ void k_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, int32_t none) {
@@ -187,11 +326,47 @@ __global__ void k_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, int32_t
   if (i < n) out[i] = in[i] == none ? -1 : in[i];
 }
 
+// per-level trace written by the kernels when GBX_BFS_TLOG is set
+static void dump_tlog(BfsWork& W, const char* tag) {
+  std::vector<unsigned long long> t(4 * 256);
+  GBX_CUDA(cudaMemcpy(t.data(), W.tlog.p, t.size() * 8, cudaMemcpyDeviceToHost));
+  if (t[0] && t[1]) std::fprintf(stderr, "%s kernel %.1fus\n", tag, (t[1] - t[0]) / 1e3);
+  for (int d = 1; d < 256 && t[4 * d]; ++d)
+    std::fprintf(stderr, "%s level %d %s qv=%llu work=%.1fus finalize=%.1fus\n", tag, d,
+                 (t[4 * d + 3] & 1) ? "push" : "pull", t[4 * d + 3] >> 8,
+                 (t[4 * d + 1] - t[4 * d]) / 1e3, (t[4 * d + 2] - t[4 * d + 1]) / 1e3);
+}
+
 static int coop_grid(const void* fn, int threads) {
   int per_sm = 0;
   GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));
   if (per_sm < 1) fail(GBX_CUDA_ERROR, "cooperative kernel does not fit on an SM");
   return device_sms() * per_sm;
+}
+
+__global__ void k_bfs_heavy(const int64_t* trp, int64_t n, int32_t* out, int* cnt) {
+  int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (v < n && trp[v + 1] - trp[v] > kBfsHeavy) out[atomicAdd(cnt, 1)] = static_cast<int32_t>(v);
+}
+
+// hub list for the pull passes, rebuilt when the transpose changes
+static void ensure_heavy(gbx_graph* g, const Csr& AT) {
+  BfsWork& W = *g->bfs;
+  if (W.heavy_key == AT.rp.p && W.heavy_nnz == AT.nnz && W.heavy.p) return;
+  const int64_t n = AT.n;
+  cudaStream_t s = g->stream;
+  W.heavy.alloc(std::max<int64_t>(n, 1));
+  if (!W.heavy_cnt.p) W.heavy_cnt.alloc(1);
+  GBX_CUDA(cudaMemsetAsync(W.heavy_cnt.p, 0, sizeof(int), s));
+  k_bfs_heavy<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, s>>>(AT.rp.p, n, W.heavy.p,
+                                                                    W.heavy_cnt.p);
+  GBX_LAUNCHED();
+  int c = 0;
+  GBX_CUDA(cudaMemcpyAsync(&c, W.heavy_cnt.p, sizeof c, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  W.nheavy = c;
+  W.heavy_key = AT.rp.p;
+  W.heavy_nnz = AT.nnz;
 }
 
 static void ensure_bfs1(gbx_graph* g) {
@@ -207,7 +382,9 @@ static void ensure_bfs1(gbx_graph* g) {
   W.queue[1].alloc(2 * qcap);
   W.bitmap[0].alloc((n + 31) / 32 + 1);
   W.bitmap[1].alloc((n + 31) / 32 + 1);
-  W.ctl.alloc(8);
+  W.ulist[0].alloc(std::max<int64_t>(n, 1));
+  W.ulist[1].alloc(std::max<int64_t>(n, 1));
+  W.ctl.alloc(16);
 }
 
 void bfs_prepare(gbx_graph* g) { ensure_bfs1(g); }
@@ -237,6 +414,13 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
   cudaStream_t s = g->stream;
   const Csr& A = g->A;
   const Csr* AT = use_at ? &g->AT() : nullptr;
+  if (AT) ensure_heavy(g, *AT);
+  static const bool tlog_on = std::getenv("GBX_BFS_TLOG") != nullptr;
+  cudaEvent_t ev[4];
+  if (tlog_on) {
+    for (auto& e : ev) GBX_CUDA(cudaEventCreate(&e));
+    GBX_CUDA(cudaEventRecord(ev[0], s));
+  }
   k_bfs1_init<<<ceil_div(n, 256), 256, 0, s>>>(W.level.p, W.parent.p, W.bitmap[0].p,
                                                  W.bitmap[1].p, n);
   GBX_LAUNCHED();
@@ -251,7 +435,14 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
   a.trp = AT ? AT->rp.p : nullptr;
   a.tcol = AT ? AT->col.p : nullptr;
   a.n = n;
+  a.nnz = A.nnz;
   a.mode = use_at ? direction : GBX_BFS_PUSH;
+  static const int alpha = std::getenv("GBX_BFS_ALPHA") ? std::atoi(std::getenv("GBX_BFS_ALPHA")) : 14;
+  a.alpha = alpha;
+  a.ul0 = W.ulist[0].p;
+  a.ul1 = W.ulist[1].p;
+  a.heavy = W.heavy.p;
+  a.nheavy = W.nheavy;
   a.divisor = push_divisor == 0 ? 1 : static_cast<int64_t>(push_divisor);
   a.level = W.level.p;
   a.parent = W.parent.p;
@@ -260,6 +451,12 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
   a.bm0 = W.bitmap[0].p;
   a.bm1 = W.bitmap[1].p;
   a.ctl = W.ctl.p;
+  if (tlog_on) {
+    if (!W.tlog.p) W.tlog.alloc(4 * 256);
+    GBX_CUDA(cudaMemsetAsync(W.tlog.p, 0, W.tlog.bytes(), s));
+    a.tlog = W.tlog.p;
+    GBX_CUDA(cudaEventRecord(ev[1], s));
+  }
   static int grid = 0;
   if (!grid) grid = coop_grid(reinterpret_cast<const void*>(k_bfs1), kBfsThreads);
   void* args[] = {&a};
@@ -267,15 +464,27 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
     GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_bfs1), dim3(grid),
                                          dim3(kBfsThreads), args, 0, s));
   }
+  if (tlog_on) GBX_CUDA(cudaEventRecord(ev[2], s));
   if (parent) copy_out_i64(s, W.parent.p, n, INT_MAX, parent);
   if (level) copy_out_i64(s, W.level.p, n, -1, level);
   int hctl[8] = {0};
   GBX_CUDA(cudaMemcpyAsync(hctl, W.ctl.p, sizeof hctl, cudaMemcpyDeviceToHost, s));
+  if (tlog_on) GBX_CUDA(cudaEventRecord(ev[3], s));
   GBX_CUDA(cudaStreamSynchronize(s));
+  if (tlog_on) {
+    float t01, t12, t23;
+    cudaEventElapsedTime(&t01, ev[0], ev[1]);
+    cudaEventElapsedTime(&t12, ev[1], ev[2]);
+    cudaEventElapsedTime(&t23, ev[2], ev[3]);
+    std::fprintf(stderr, "bfs1 events: setup %.1fus kernel %.1fus out %.1fus\n", t01 * 1e3,
+                 t12 * 1e3, t23 * 1e3);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
   g->stats = gbx_stats{};
   g->stats.launches = 3 + (parent ? 1 : 0) + (level ? 1 : 0);
   g->stats.hot_launches = 1;
   g->stats.iterations = hctl[5];
+  if (tlog_on) dump_tlog(W, "bfs1");
 }
 
 // ---------------------------------------------------------------------------
@@ -303,14 +512,6 @@ struct Bfs64Args {
   int64_t nheavy;
 };
 
-// In-degree above which a pull row goes to a whole warp instead of 8 lanes.
-constexpr int64_t kBfsHeavy = 256;
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
   cg::grid_group grid = cg::this_grid();
@@ -494,11 +695,6 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
   }
 }
 
-__global__ void k_bfs64_heavy(const int64_t* trp, int64_t n, int32_t* out, int* cnt) {
-  int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (v < n && trp[v + 1] - trp[v] > kBfsHeavy) out[atomicAdd(cnt, 1)] = static_cast<int32_t>(v);
-}
-
 __global__ void k_bfs64_init(unsigned long long* seen, unsigned long long* f0,
                              unsigned long long* f1, int32_t* mlevel, int32_t* mparent,
                              int64_t n) {
@@ -576,25 +772,6 @@ static void ensure_bfs64(gbx_graph* g) {
   W.msrc.alloc(128);
 }
 
-// hub list for the pull pass, rebuilt when the transpose changes
-static void ensure_bfs64_heavy(gbx_graph* g, const Csr& AT) {
-  BfsWork& W = *g->bfs;
-  if (W.heavy_key == AT.rp.p && W.heavy_nnz == AT.nnz && W.heavy.p) return;
-  const int64_t n = AT.n;
-  cudaStream_t s = g->stream;
-  W.heavy.alloc(std::max<int64_t>(n, 1));
-  GBX_CUDA(cudaMemsetAsync(W.mctl.p, 0, sizeof(int), s));
-  k_bfs64_heavy<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, s>>>(AT.rp.p, n, W.heavy.p,
-                                                                      W.mctl.p);
-  GBX_LAUNCHED();
-  int c = 0;
-  GBX_CUDA(cudaMemcpyAsync(&c, W.mctl.p, sizeof c, cudaMemcpyDeviceToHost, s));
-  GBX_CUDA(cudaStreamSynchronize(s));
-  W.nheavy = c;
-  W.heavy_key = AT.rp.p;
-  W.heavy_nnz = AT.nnz;
-}
-
 void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* parent,
                    int64_t* level) {
   require_at(g, "bfs_batch");
@@ -608,7 +785,7 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
   cudaStream_t s = g->stream;
   const Csr& A = g->A;
   const Csr& AT = g->AT();
-  ensure_bfs64_heavy(g, AT);
+  ensure_heavy(g, AT);
   static int grid = 0;
   if (!grid) grid = coop_grid(reinterpret_cast<const void*>(k_bfs64), kBfsThreads);
   int64_t total_launches = 0;
@@ -690,14 +867,7 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
     GBX_CUDA(cudaMemcpyAsync(hctl, W.mctl.p, sizeof hctl, cudaMemcpyDeviceToHost, s));
     GBX_CUDA(cudaStreamSynchronize(s));
     g->stats.iterations = hctl[5];
-    if (tlog_on) {
-      std::vector<unsigned long long> t(4 * 256);
-      GBX_CUDA(cudaMemcpy(t.data(), W.tlog.p, t.size() * 8, cudaMemcpyDeviceToHost));
-      for (int d = 1; d < 256 && t[4 * d]; ++d)
-        std::fprintf(stderr, "bfs64 level %d %s qv=%llu work=%.1fus finalize=%.1fus\n", d,
-                     (t[4 * d + 3] & 1) ? "push" : "pull", t[4 * d + 3] >> 8,
-                     (t[4 * d + 1] - t[4 * d]) / 1e3, (t[4 * d + 2] - t[4 * d + 1]) / 1e3);
-    }
+    if (tlog_on) dump_tlog(W, "bfs64");
   }
   g->stats.launches = total_launches;
   g->stats.hot_launches = (ns + 63) / 64;

@@ -66,6 +66,7 @@ struct BfsWork {
   DevArray<int32_t> level, parent;          // single source
   DevArray<int32_t> queue[2];
   DevArray<uint32_t> bitmap[2];
+  DevArray<int32_t> ulist[2];               // unvisited vertices for pull levels
   DevArray<int> ctl;
   // multi-source (64 lanes)
   DevArray<unsigned long long> seen, front, next;
@@ -77,6 +78,7 @@ struct BfsWork {
   DevArray<unsigned long long> tlog;
   // pull-mode hubs (in-degree > kBfsHeavy) handled warp-per-vertex
   DevArray<int32_t> heavy;
+  DevArray<int> heavy_cnt;
   int64_t nheavy = 0;
   const void* heavy_key = nullptr;
   int64_t heavy_nnz = -1;
