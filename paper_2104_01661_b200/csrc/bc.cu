@@ -3,22 +3,32 @@
 // The reference keeps ns x n matrices P (path counts), one boolean pattern per
 // BFS level and B = 1 + dependency, and runs Gustavson mxm per level forward
 // (F<!s(P)> = F plus.first A) and backward (W<s(S[i-1])> = W plus.first AT)
-// (betweenness.cpp:27-72).  On the device the batch rows become lanes of a
-// vertex-major layout -- level[v][b] (int32), sigma[v][b] and delta[v][b]
-// (fp64) -- so one gather of a vertex fetches all sources' state in one
-// sector, and every level of the batch is ONE kernel over the union frontier:
-//   forward: push over A from the (vertex, <=1024-edge chunk) entries of the
-//     previous level; a lane claims an unvisited vertex with atomicCAS on its
-//     level word and adds its sigma with fp64 atomicAdd (path counts are
-//     integers < 2^53, so the sum is exact and order-independent);
-//   backward, level d = D-1..1: for u on level d, acc_b = sum over out-
-//     neighbours v on level d+1 of coef_b(v) = (1 + delta_b(v)) / sigma_b(v);
-//     then delta_b(u) = sigma_b(u) * acc_b, centrality(u) += delta_b(u), and
-//     coef_b(u) replaces delta_b(u) for the next level down.
+// (betweenness.cpp:27-72).  On the device the batch rows become 4 lanes of a
+// vertex-major layout:
+//   level[v][4]  int32 exact BFS depth per lane (-1 unreached)
+//   lv8[v]       uint32, one byte per lane = min(depth, 254), 0xFF unreached
+//   map[v/8]     level map: 4 bits per vertex = membership of ONE depth; the
+//                word every edge gathers (8 MB at scale 24, L2-resident) --
+//                depth d-1 in the forward pull, depth d+1 in the backward
+//   sigma[v][4]  fp64 path counts (integers < 2^53: sums are exact in any order)
+//   coef[v][4]   fp64 (1 + delta) / sigma once v's level is final
+// Forward, level d (direction-optimizing like the BFS, results identical):
+//   push (small frontier): (vertex, <=kBcChunk-edge) entries of level d-1; a
+//     lane claims an unreached neighbour with atomicCAS on its level word and
+//     adds sigma with fp64 atomicAdd;
+//   pull (frontier edges >= nnz/alpha): every vertex still unreached in a live
+//     lane sums sigma over its in-neighbours on level d-1 (AT rows, no atomics);
+//     only vertices a previous pull left unreached are rescanned; rows longer
+//     than kBcHeavy are split into chunks summed with atomics by a side pass.
+// Backward, level d = D-1..1: for u on level d, acc_b = sum over out-neighbours
+//   v on level d+1 of coef_b(v); delta_b(u) = sigma_b(u) * acc_b, centrality(u)
+//   += delta_b(u), coef_b(u) = (1 + delta_b(u)) / sigma_b(u) -- finalised in the
+//   same pass for ordinary rows, by a side pass for chunked hub rows.
 // centrality(j) = sum_b (B(b,j) - 1) = sum_b delta_b(j) (betweenness.cpp:74-79);
 // sources and unreached vertices contribute 0, undirected pairs not halved.
 // Algorithmic bytes per batch: E_r*(8 + 16*ns) + V_r*(16 + 24*ns).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -28,54 +38,158 @@
 namespace gbx {
 
 constexpr int kBcLanes = 4;
-constexpr int64_t kBcChunk = 1024;
+constexpr int64_t kBcChunk = 256;    // push entries: edges per warp
+constexpr int64_t kBcHeavy = 2048;   // rows longer than this are chunked
+constexpr int64_t kBcHChunk = 2048;  // edges per hub-row chunk
+constexpr int kBcBuf = 256;
 constexpr unsigned kAll = 0xffffffffu;
 
 __device__ __forceinline__ int bc_chunks(int64_t deg) {
   return deg <= kBcChunk ? 1 : static_cast<int>((deg + kBcChunk - 1) / kBcChunk);
 }
 
+// lane b of lv8 word x is on depth L (exact: depths >= 254 share byte 254)
+__device__ __forceinline__ bool on_level(uint32_t x, int b, int L, const int32_t* level,
+                                         int64_t v) {
+  const uint32_t byte = (x >> (8 * b)) & 0xFFu;
+  if (L < 254) return byte == static_cast<uint32_t>(L);
+  return byte == 254u && level[v * 4 + b] == L;
+}
+
+__device__ __forceinline__ unsigned lanes_on(uint32_t x, int L, unsigned lanes,
+                                             const int32_t* level, int64_t v) {
+  unsigned m = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (((lanes >> b) & 1u) && on_level(x, b, L, level, v)) m |= 1u << b;
+  return m;
+}
+
+__device__ __forceinline__ unsigned lanes_unreached(uint32_t x, unsigned lanes) {
+  unsigned m = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (((x >> (8 * b)) & 0xFFu) == 0xFFu) m |= 1u << b;
+  return m & lanes;
+}
+
+__device__ __forceinline__ uint32_t lv8_byte(int d) { return d < 254 ? d : 254; }
+
+// Level maps: 4 bits per vertex (one per lane), 8 vertices per word -- the
+// membership of ONE depth (8 MB at scale 24, L2-resident), gathered per edge
+// in place of the 64 MB lv8 array.
+__device__ __forceinline__ unsigned nib(const uint32_t* map, int64_t v) {
+  return (__ldg(map + (v >> 3)) >> ((v & 7) * 4)) & 0xFu;
+}
+__device__ __forceinline__ void nib_or(uint32_t* map, int64_t v, unsigned m) {
+  atomicOr(map + (v >> 3), m << ((v & 7) * 4));
+}
+
+// streamed column index (no L1 allocation: L1 is kept for the map words)
+__device__ __forceinline__ int32_t ld_col(const int32_t* p) {
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// s[b] += val[u][b] over the row entries p, p+st, ... < e whose map nibble is
+// in m; four independent column loads, then four map gathers, per step (the
+// chain col -> map -> val is latency-bound, so each lane keeps 4 in flight)
+__device__ __forceinline__ void row_sum(const int32_t* col, int64_t p, int64_t e, int st,
+                                        const uint32_t* map, const double* val, unsigned m,
+                                        double s[4]) {
+  for (; p < e; p += 4 * st) {
+    int32_t u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u[k] = p + k * st < e ? ld_col(col + p + k * st) : -1;
+    unsigned h[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = u[k] >= 0 ? (nib(map, u[k]) & m) : 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (h[k]) {
+        const double* vp = val + static_cast<int64_t>(u[k]) * 4;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if ((h[k] >> b) & 1u) s[b] += __ldg(vp + b);
+      }
+  }
+}
+
+__device__ __forceinline__ void group_reduce(double s[4]) {
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    s[b] += __shfl_xor_sync(0xffffffffu, s[b], 4);
+    s[b] += __shfl_xor_sync(0xffffffffu, s[b], 2);
+    s[b] += __shfl_xor_sync(0xffffffffu, s[b], 1);
+  }
+}
+
+__device__ __forceinline__ void warp_reduce(double s[4]) {
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s[b] += __shfl_xor_sync(0xffffffffu, s[b], o);
+}
+
+// rows up to kBcShort edges are summed by their own lane, longer ones by an
+// 8-lane group (4 rows at a time per warp)
+constexpr int64_t kBcShort = 8;
+
 struct BcArgs {
-  const int64_t* rp;
+  const int64_t* rp;   // A
   const int32_t* col;
-  int32_t* level;    // [n][4]
-  double* sigma;     // [n][4]
-  double* delta;     // [n][4]: coef (1 + delta) / sigma once final
-  double* acc;       // [n][4]: backward accumulator
-  int32_t* mark;     // [n]: last level that listed the vertex
-  int32_t* list_out; // vertices of the level being built
+  const int64_t* trp;  // AT
+  const int32_t* tcol;
+  int64_t n;
+  int32_t* level;
+  uint32_t* lv8;
+  double* sigma;
+  double* coef;
+  double* cent;
+  double* hacc;          // [nheavy][4] hub-row partial sums (zero between uses)
+  int32_t* mark;         // push: last level that listed the vertex
+  int32_t* list_out;     // vertices of the level being built
+  const int32_t* list_in;
+  int n_list;
   const int64_t* ent_in;
   int64_t* ent_out;
-  int* cnt;          // [0] list size [1] entries size
   int n_ent;
+  const int32_t* ul_in;  // pull: vertices still unreached (-1 count: all)
+  int32_t* ul_out;
+  int ul_cnt;
+  const int32_t* hv;     // hub rows (slot -> vertex) and their chunks (chunk<<32|slot)
+  const int64_t* hent;
+  int nhv, nhent;
+  const uint32_t* map_in;  // level map of depth d-1 (forward) / d+1 (backward)
+  uint32_t* map_out;       // forward: level map of depth d being built
+  int* cnt;  // [0] list [1] entries [2] unreached list [3] lanes discovered
+  unsigned long long* edges;  // frontier edges of the level being built
   int d;
-  int lanes;
+  unsigned lanes;  // lanes still live (their previous level was non-empty)
 };
 
-__global__ void __launch_bounds__(256) k_bc_forward(BcArgs a) {
-  __shared__ int32_t s_buf[8][256];
-  FrontierQueue<256> fq;
+// forward push over A from the entries of level d-1
+__global__ void __launch_bounds__(256) k_bc_push(BcArgs a) {
+  __shared__ int32_t s_buf[8][kBcBuf];
+  FrontierQueue<kBcBuf> fq;
   fq.buf = s_buf[threadIdx.x >> 5];
   fq.rp = a.rp;
   fq.chunk = kBcChunk;
-  fq.reset(a.ent_out, &a.cnt[1], &a.cnt[0], nullptr, a.list_out);
+  fq.reset(a.ent_out, &a.cnt[1], &a.cnt[0], a.edges, a.list_out);
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int d = a.d;
+  unsigned found = 0;
   for (int64_t e = gwarp; e < a.n_ent; e += nwarps) {
     const int64_t ent = a.ent_in[e];
     const int32_t u = static_cast<int32_t>(ent & 0xffffffff);
     const int64_t c = ent >> 32;
-    const int4 lu = *reinterpret_cast<const int4*>(a.level + static_cast<int64_t>(u) * 4);
-    const int lv_u[4] = {lu.x, lu.y, lu.z, lu.w};
+    const unsigned m = lanes_on(a.lv8[u], d - 1, a.lanes, a.level, u);
     double su[4];
-    unsigned m = 0;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      su[b] = a.sigma[static_cast<int64_t>(u) * 4 + b];
-      if (b < a.lanes && lv_u[b] == d - 1) m |= 1u << b;
-    }
+    for (int b = 0; b < 4; ++b) su[b] = (m >> b) & 1u ? a.sigma[static_cast<int64_t>(u) * 4 + b] : 0.0;
     const int64_t b0 = a.rp[u] + c * kBcChunk;
     const int64_t e0 = min(a.rp[u + 1], b0 + kBcChunk);
     for (int64_t base = b0; base < e0; base += 32) {
@@ -87,11 +201,17 @@ __global__ void __launch_bounds__(256) k_bc_forward(BcArgs a) {
         int32_t* lvp = a.level + static_cast<int64_t>(v) * 4;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          if (!(m & (1u << b))) continue;
+          if (!((m >> b) & 1u)) continue;
           int lv = *(volatile int32_t*)&lvp[b];
           if (lv == -1) {
             lv = atomicCAS(&lvp[b], -1, d);
-            if (lv == -1) { claimed = true; lv = d; }
+            if (lv == -1) {
+              claimed = true;
+              lv = d;
+              found |= 1u << b;
+              atomicAnd(&a.lv8[v], ~((0xFFu ^ lv8_byte(d)) << (8 * b)));
+              nib_or(a.map_out, v, 1u << b);
+            }
           }
           if (lv == d) atomicAdd(&a.sigma[static_cast<int64_t>(v) * 4 + b], su[b]);
         }
@@ -101,111 +221,371 @@ __global__ void __launch_bounds__(256) k_bc_forward(BcArgs a) {
     }
   }
   fq.flush();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) found |= __shfl_xor_sync(kAll, found, o);
+  if (lane == 0 && found) atomicOr(&a.cnt[3], static_cast<int>(found));
 }
 
-// backward accumulation for the entries of level d
-__global__ void k_bc_backward(BcArgs a) {
+// forward pull over AT for the vertices still unreached in a live lane
+// settle vertex v with path-count sums s for the unreached live lanes um
+__device__ __forceinline__ unsigned bc_settle(const BcArgs& a, int64_t v, unsigned um,
+                                              const double s[4]) {
+  unsigned nm = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (((um >> b) & 1u) && s[b] > 0.0) nm |= 1u << b;
+  if (nm) {
+    uint32_t x = a.lv8[v];
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if ((nm >> b) & 1u) {
+        a.level[v * 4 + b] = a.d;
+        a.sigma[v * 4 + b] = s[b];
+        x = (x & ~(0xFFu << (8 * b))) | (lv8_byte(a.d) << (8 * b));
+      }
+    a.lv8[v] = x;
+    nib_or(a.map_out, v, nm);
+  }
+  return nm;
+}
+
+__global__ void __launch_bounds__(256) k_bc_pull(BcArgs a) {
+  __shared__ int32_t s_buf[8][kBcBuf];
+  __shared__ int32_t s_ubuf[8][kBcBuf];
+  FrontierQueue<kBcBuf> fq;
+  fq.buf = s_buf[threadIdx.x >> 5];
+  fq.rp = a.rp;
+  fq.chunk = kBcChunk;
+  fq.reset(a.ent_out, &a.cnt[1], &a.cnt[0], a.edges, a.list_out);
+  WarpQueue<int32_t, kBcBuf> uq;
+  uq.buf = s_ubuf[threadIdx.x >> 5];
+  uq.reset(a.ul_out, &a.cnt[2]);
+  const int lane = threadIdx.x & 31;
+  const int grp = lane >> 3, sub = lane & 7;
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t range = a.ul_cnt < 0 ? a.n : a.ul_cnt;
+  unsigned found = 0;
+  for (int64_t vb = gwarp * 32; vb < range; vb += nwarps * 32) {
+    const int64_t i = vb + lane;
+    const int64_t v = i < range ? (a.ul_cnt < 0 ? i : a.ul_in[i]) : -1;
+    unsigned um = 0;
+    int64_t pp = 0, pe = 0;
+    if (v >= 0) {
+      um = lanes_unreached(a.lv8[v], a.lanes);
+      if (um) {
+        pp = a.trp[v];
+        pe = a.trp[v + 1];
+        if (pe - pp > kBcHeavy) um = 0;  // hub: chunked side pass
+      }
+    }
+    const bool keep = um != 0 && pe > pp;
+    const bool mine = keep && pe - pp <= kBcShort;
+    unsigned nm = 0;
+    if (mine) {
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+      row_sum(a.tcol, pp, pe, 1, a.map_in, a.sigma, um, s);
+      nm = bc_settle(a, v, um, s);
+      found |= nm;
+    }
+    fq.push(nm != 0, static_cast<int32_t>(v));
+    uq.push(mine && (um & ~nm) != 0, static_cast<int32_t>(v));
+    unsigned rest = __ballot_sync(kAll, keep && !mine);
+    while (rest) {
+      unsigned m = rest;
+      for (int k = 0; k < grp && m; ++k) m &= m - 1;
+      const int src = m ? __ffs(m) - 1 : -1;
+      for (int k = 0; k < 4 && rest; ++k) rest &= rest - 1;
+      const int sl = src < 0 ? 0 : src;
+      const int64_t gv = __shfl_sync(kAll, v, sl);
+      const int64_t gp = __shfl_sync(kAll, pp, sl);
+      const int64_t ge = __shfl_sync(kAll, pe, sl);
+      const unsigned gum0 = __shfl_sync(kAll, um, sl);
+      const unsigned gum = src < 0 ? 0u : gum0;
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+      if (gum) row_sum(a.tcol, gp + sub, ge, 8, a.map_in, a.sigma, gum, s);
+      group_reduce(s);
+      unsigned gnm = 0;
+      if (sub == 0 && gum) {
+        gnm = bc_settle(a, gv, gum, s);
+        found |= gnm;
+      }
+      fq.push(gnm != 0, static_cast<int32_t>(gv));
+      uq.push(sub == 0 && gum && (gum & ~gnm) != 0, static_cast<int32_t>(gv));
+    }
+  }
+  fq.flush();
+  uq.flush();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) found |= __shfl_xor_sync(kAll, found, o);
+  if (lane == 0 && found) atomicOr(&a.cnt[3], static_cast<int>(found));
+}
+
+// forward pull, hub rows: one warp per chunk, partial sums into hacc[slot]
+__global__ void __launch_bounds__(256) k_bc_pull_hub(BcArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t e = gwarp; e < a.nhent; e += nwarps) {
+    const int64_t ent = a.hent[e];
+    const int slot = static_cast<int>(ent & 0xffffffff);
+    const int64_t c = ent >> 32;
+    const int32_t v = a.hv[slot];
+    const unsigned um = lanes_unreached(a.lv8[v], a.lanes);
+    if (!um) continue;
+    const int64_t b0 = a.trp[v] + c * kBcHChunk;
+    const int64_t e0 = min(a.trp[v + 1], b0 + kBcHChunk);
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    row_sum(a.tcol, b0 + lane, e0, 32, a.map_in, a.sigma, um, s);
+    warp_reduce(s);
+    if (lane < 4 && ((um >> lane) & 1u)) {
+      const double mine = lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3];
+      if (mine != 0.0) atomicAdd(&a.hacc[slot * 4 + lane], mine);
+    }
+  }
+}
+
+// forward pull, hub rows: settle the summed hubs, one warp per 32 slots
+__global__ void __launch_bounds__(256) k_bc_pull_hub_fin(BcArgs a) {
+  __shared__ int32_t s_buf[8][kBcBuf];
+  FrontierQueue<kBcBuf> fq;
+  fq.buf = s_buf[threadIdx.x >> 5];
+  fq.rp = a.rp;
+  fq.chunk = kBcChunk;
+  fq.reset(a.ent_out, &a.cnt[1], &a.cnt[0], a.edges, a.list_out);
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int d = a.d;
-  for (int64_t e = gwarp; e < a.n_ent; e += nwarps) {
-    const int64_t ent = a.ent_in[e];
-    const int32_t u = static_cast<int32_t>(ent & 0xffffffff);
-    const int64_t c = ent >> 32;
-    const int4 lu = *reinterpret_cast<const int4*>(a.level + static_cast<int64_t>(u) * 4);
-    const int lv_u[4] = {lu.x, lu.y, lu.z, lu.w};
+  unsigned found = 0;
+  for (int64_t base = gwarp * 32; base < a.nhv; base += nwarps * 32) {
+    const int64_t slot = base + lane;
+    bool has = false;
+    int32_t v = 0;
+    if (slot < a.nhv) {
+      v = a.hv[slot];
+      uint32_t x = a.lv8[v];
+      const unsigned um = lanes_unreached(x, a.lanes);
+      unsigned nm = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const double sb = a.hacc[slot * 4 + b];
+        if (((um >> b) & 1u) && sb > 0.0) {
+          nm |= 1u << b;
+          a.level[static_cast<int64_t>(v) * 4 + b] = d;
+          a.sigma[static_cast<int64_t>(v) * 4 + b] = sb;
+          x = (x & ~(0xFFu << (8 * b))) | (lv8_byte(d) << (8 * b));
+        }
+        if (sb != 0.0) a.hacc[slot * 4 + b] = 0.0;
+      }
+      if (nm) {
+        a.lv8[v] = x;
+        nib_or(a.map_out, v, nm);
+        found |= nm;
+        has = true;
+      }
+    }
+    fq.push(has, v);
+  }
+  fq.flush();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) found |= __shfl_xor_sync(kAll, found, o);
+  if (lane == 0 && found) atomicOr(&a.cnt[3], static_cast<int>(found));
+}
+
+// backward for the level-d list over A rows (hub rows skipped), finalised inline
+__device__ __forceinline__ void bc_final(const BcArgs& a, int64_t u, unsigned m,
+                                         const double acc[4]) {
+  double c = 0.0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if ((m >> b) & 1u) {
+      const double sg = a.sigma[u * 4 + b];
+      const double dl = sg * acc[b];
+      c += dl;
+      a.coef[u * 4 + b] = (1.0 + dl) / sg;
+    }
+  a.cent[u] += c;
+}
+
+__global__ void __launch_bounds__(256) k_bc_back(BcArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int grp = lane >> 3, sub = lane & 7;
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t vb = gwarp * 32; vb < a.n_list; vb += nwarps * 32) {
+    const int64_t i = vb + lane;
+    int64_t u = 0;
     unsigned m = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-      if (b < a.lanes && lv_u[b] == d) m |= 1u << b;
-    const int64_t b0 = a.rp[u] + c * kBcChunk;
-    const int64_t e0 = min(a.rp[u + 1], b0 + kBcChunk);
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t p = b0 + lane; p < e0; p += 32) {
-      const int32_t v = __ldg(a.col + p);
-      const int4 lvv = *reinterpret_cast<const int4*>(a.level + static_cast<int64_t>(v) * 4);
-      const int lv[4] = {lvv.x, lvv.y, lvv.z, lvv.w};
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-        if ((m & (1u << b)) && lv[b] == d + 1) acc[b] += a.delta[static_cast<int64_t>(v) * 4 + b];
+    int64_t pp = 0, pe = 0;
+    if (i < a.n_list) {
+      u = a.list_in[i];
+      m = lanes_on(a.lv8[u], a.d, a.lanes, a.level, u);
+      pp = a.rp[u];
+      pe = a.rp[u + 1];
+      if (pe - pp > kBcHeavy) m = 0;  // hub: chunked side pass
     }
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(kAll, acc[b], o);
+    const bool mine = m != 0 && pe - pp <= kBcShort;
+    if (mine) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      row_sum(a.col, pp, pe, 1, a.map_in, a.coef, m, acc);
+      bc_final(a, u, m, acc);
     }
-    if (lane == 0) {
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-        if ((m & (1u << b)) && acc[b] != 0.0)
-          atomicAdd(&a.acc[static_cast<int64_t>(u) * 4 + b], acc[b]);
+    unsigned rest = __ballot_sync(kAll, m != 0 && !mine);
+    while (rest) {
+      unsigned r = rest;
+      for (int k = 0; k < grp && r; ++k) r &= r - 1;
+      const int src = r ? __ffs(r) - 1 : -1;
+      for (int k = 0; k < 4 && rest; ++k) rest &= rest - 1;
+      const int sl = src < 0 ? 0 : src;
+      const int64_t gu = __shfl_sync(kAll, u, sl);
+      const int64_t gp = __shfl_sync(kAll, pp, sl);
+      const int64_t ge = __shfl_sync(kAll, pe, sl);
+      const unsigned gm0 = __shfl_sync(kAll, m, sl);
+      const unsigned gm = src < 0 ? 0u : gm0;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      if (gm) row_sum(a.col, gp + sub, ge, 8, a.map_in, a.coef, gm, acc);
+      group_reduce(acc);
+      if (sub == 0 && gm) bc_final(a, gu, gm, acc);
     }
   }
 }
 
-// finalize level d: delta = sigma * acc; centrality += delta; coef replaces delta
-__global__ void k_bc_finalize(const int32_t* list, int nlist, int d, int lanes,
-                              const int32_t* level, const double* sigma, double* delta,
-                              const double* acc, double* cent) {
+// backward, hub rows of A: one warp per chunk, partial sums into hacc[slot]
+__global__ void __launch_bounds__(256) k_bc_back_hub(BcArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int d = a.d;
+  for (int64_t e = gwarp; e < a.nhent; e += nwarps) {
+    const int64_t ent = a.hent[e];
+    const int slot = static_cast<int>(ent & 0xffffffff);
+    const int64_t c = ent >> 32;
+    const int32_t u = a.hv[slot];
+    const unsigned m = lanes_on(a.lv8[u], d, a.lanes, a.level, u);
+    if (!m) continue;
+    const int64_t b0 = a.rp[u] + c * kBcHChunk;
+    const int64_t e0 = min(a.rp[u + 1], b0 + kBcHChunk);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    row_sum(a.col, b0 + lane, e0, 32, a.map_in, a.coef, m, acc);
+    warp_reduce(acc);
+    if (lane < 4 && ((m >> lane) & 1u)) {
+      const double mine = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
+      if (mine != 0.0) atomicAdd(&a.hacc[slot * 4 + lane], mine);
+    }
+  }
+}
+
+__global__ void k_bc_back_hub_fin(BcArgs a) {
+  const int64_t slot = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (slot >= a.nhv) return;
+  const int64_t u = a.hv[slot];
+  const unsigned m = lanes_on(a.lv8[u], a.d, a.lanes, a.level, u);
+  double c = 0.0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const double ab = a.hacc[slot * 4 + b];
+    if ((m >> b) & 1u) {
+      const double sg = a.sigma[u * 4 + b];
+      const double dl = sg * ab;
+      c += dl;
+      a.coef[u * 4 + b] = (1.0 + dl) / sg;
+    }
+    if (ab != 0.0) a.hacc[slot * 4 + b] = 0.0;
+  }
+  if (m) a.cent[u] += c;
+}
+
+// level map of depth d from its list (backward)
+__global__ void k_bc_map(const int32_t* list, int nlist, int d, unsigned lanes,
+                         const int32_t* level, const uint32_t* lv8, uint32_t* map) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= nlist) return;
-  const int64_t u = list[i];
-  double c = 0.0;
-  for (int b = 0; b < lanes; ++b) {
-    if (level[u * 4 + b] != d) continue;
-    const double s = sigma[u * 4 + b];
-    const double dl = s * acc[u * 4 + b];
-    c += dl;
-    delta[u * 4 + b] = (1.0 + dl) / s;
-  }
-  cent[u] += c;
+  const int64_t v = list[i];
+  const unsigned m = lanes_on(lv8[v], d, lanes, level, v);
+  if (m) nib_or(map, v, m);
 }
 
 // deepest level: delta = 0, coef = 1 / sigma
-__global__ void k_bc_leaf(const int32_t* list, int nlist, int d, int lanes, const int32_t* level,
-                          const double* sigma, double* delta) {
+__global__ void k_bc_leaf(const int32_t* list, int nlist, int d, unsigned lanes,
+                          const int32_t* level, const uint32_t* lv8, const double* sigma,
+                          double* coef) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= nlist) return;
   const int64_t u = list[i];
-  for (int b = 0; b < lanes; ++b)
-    if (level[u * 4 + b] == d) delta[u * 4 + b] = 1.0 / sigma[u * 4 + b];
+  const unsigned m = lanes_on(lv8[u], d, lanes, level, u);
+  for (int b = 0; b < 4; ++b)
+    if ((m >> b) & 1u) coef[u * 4 + b] = 1.0 / sigma[u * 4 + b];
 }
 
-// rebuild the chunk entries of a level list
-__global__ void k_bc_entries(const int32_t* list, int nlist, const int64_t* rp, int64_t* ent,
-                             int* cnt) {
+__global__ void k_bc_init(int32_t* level, uint32_t* lv8, double* sigma, int32_t* mark,
+                          int64_t n) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i >= nlist) return;
-  const int32_t v = list[i];
-  const int k = bc_chunks(rp[v + 1] - rp[v]);
-  const int off = atomicAdd(cnt, k);
-  for (int c = 0; c < k; ++c) ent[off + c] = (static_cast<int64_t>(c) << 32) | v;
+  if (i < n * 4) { level[i] = -1; sigma[i] = 0.0; }
+  if (i < n) { mark[i] = -1; lv8[i] = 0xFFFFFFFFu; }
 }
 
-__global__ void k_bc_init(int32_t* level, double* sigma, double* delta, int32_t* mark,
-                          double* acc, int64_t n) {
-  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < n * 4) { level[i] = -1; sigma[i] = 0.0; delta[i] = 0.0; acc[i] = 0.0; }
-  if (i < n) mark[i] = -1;
-}
-
-__global__ void k_bc_seed(const int32_t* src, int ns, int32_t* level, double* sigma,
-                          int32_t* mark, int32_t* list, int64_t* ent, int* cnt, const int64_t* rp) {
+__global__ void k_bc_seed(const int32_t* src, int ns, int32_t* level, uint32_t* lv8,
+                          double* sigma, int32_t* mark, int32_t* list, int64_t* ent, int* cnt,
+                          unsigned long long* edges, const int64_t* rp, uint32_t* map) {
   int nl = 0, ne = 0;
+  unsigned long long fe = 0;
   for (int b = 0; b < ns; ++b) {
     const int64_t s = src[b];
     level[s * 4 + b] = 0;
     sigma[s * 4 + b] = 1.0;
+    lv8[s] &= ~(0xFFu << (8 * b));
+    map[s >> 3] |= (1u << b) << ((s & 7) * 4);
     if (mark[s] != 0) {
       mark[s] = 0;
       list[nl++] = static_cast<int32_t>(s);
-      const int k = bc_chunks(rp[s + 1] - rp[s]);
+      const int64_t deg = rp[s + 1] - rp[s];
+      fe += static_cast<unsigned long long>(deg);
+      const int k = bc_chunks(deg);
       for (int c = 0; c < k; ++c) ent[ne++] = (static_cast<int64_t>(c) << 32) | s;
     }
   }
   cnt[0] = nl;
   cnt[1] = ne;
+  cnt[2] = 0;
+  cnt[3] = (1 << ns) - 1;
+  *edges = fe;
+}
+
+// hub rows (degree > kBcHeavy) of a CSR and their kBcHChunk-edge chunks
+__global__ void k_bc_hubs(const int64_t* rp, int64_t n, int32_t* hv, int64_t* hent, int* cnt) {
+  int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (v >= n) return;
+  const int64_t deg = rp[v + 1] - rp[v];
+  if (deg <= kBcHeavy) return;
+  const int slot = atomicAdd(&cnt[0], 1);
+  hv[slot] = static_cast<int32_t>(v);
+  const int k = static_cast<int>((deg + kBcHChunk - 1) / kBcHChunk);
+  const int off = atomicAdd(&cnt[1], k);
+  for (int c = 0; c < k; ++c) hent[off + c] = (static_cast<int64_t>(c) << 32) | slot;
+}
+
+static void build_hubs(cudaStream_t s, const Csr& M, BcHubs& H) {
+  if (H.key == M.rp.p && H.nnz == M.nnz && H.hv.p) return;
+  const int64_t n1 = std::max<int64_t>(M.n, 1);
+  DevArray<int> cnt(2);
+  GBX_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(int), s));
+  // hubs have > kBcHeavy edges each: at most nnz / kBcHeavy of them
+  const int64_t cap_v = std::min<int64_t>(n1, M.nnz / kBcHeavy + 1);
+  const int64_t cap_e = M.nnz / kBcHChunk + cap_v + 1;
+  H.hv.alloc(cap_v);
+  H.hent.alloc(cap_e);
+  H.hacc.alloc(cap_v * 4);
+  GBX_CUDA(cudaMemsetAsync(H.hacc.p, 0, H.hacc.bytes(), s));
+  k_bc_hubs<<<ceil_div(n1, 256), 256, 0, s>>>(M.rp.p, M.n, H.hv.p, H.hent.p, cnt.p);
+  GBX_LAUNCHED();
+  int hc[2];
+  GBX_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof hc, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  H.nhv = hc[0];
+  H.nhent = hc[1];
+  H.key = M.rp.p;
+  H.nnz = M.nnz;
 }
 
 void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrality) {
@@ -217,71 +597,123 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
   BcWork& W = *g->bc;
   cudaStream_t s = g->stream;
   const Csr& A = g->A;
+  const Csr& AT = g->AT();
   const int64_t n1 = std::max<int64_t>(n, 1);
+  const int64_t ecap = n + A.nnz / kBcChunk + 64;
   if (W.n != n || !W.level.p) {
     W.n = n;
     W.lanes = kBcLanes;
     W.level.alloc(n1 * 4);
+    W.lv8.alloc(n1);
     W.sigma.alloc(n1 * 4);
     W.delta.alloc(n1 * 4);
     W.order.alloc(n1 * 4 + 8);
     W.cent.alloc(n1);
-    W.ctl.alloc(4);
+    W.mark.alloc(n1);
+    W.ulist[0].alloc(n1);
+    W.ulist[1].alloc(n1);
+    W.ent[0].alloc(ecap);
+    W.ent[1].alloc(ecap);
+    W.ctl.alloc(8);
+    W.src.alloc(4);
+    W.map[0].alloc(n1 / 8 + 1);
+    W.map[1].alloc(n1 / 8 + 1);
   }
-  DevArray<int32_t> mark(n1);
-  DevArray<double> acc(n1 * 4);
-  const int64_t ecap = n + A.nnz / kBcChunk + 64;
-  DevArray<int64_t> ent[2];
-  ent[0].alloc(ecap);
-  ent[1].alloc(ecap);
-  DevArray<int32_t> dsrc(4);
+  const size_t map_bytes = (n1 / 8 + 1) * sizeof(uint32_t);
+  build_hubs(s, A, W.hub_a);
+  const bool same = &AT == &A;
+  if (!same) build_hubs(s, AT, W.hub_t);
+  BcHubs& HT = same ? W.hub_a : W.hub_t;
   GBX_CUDA(cudaMemsetAsync(W.cent.p, 0, n1 * 8, s));
-  const int grid = device_sms() * 16;
+  const int grid = device_sms() * 8;
+  static const int alpha = std::getenv("GBX_BC_ALPHA") ? std::atoi(std::getenv("GBX_BC_ALPHA")) : 14;
+  int* ctl = W.ctl.p;
+  unsigned long long* dedges = reinterpret_cast<unsigned long long*>(W.ctl.p + 4);
   int64_t launches = 1, edges = 0;
   int max_levels = 0;
   for (uint64_t b0 = 0; b0 < ns; b0 += kBcLanes) {
     const int nb = static_cast<int>(std::min<uint64_t>(kBcLanes, ns - b0));
     int32_t hs[4];
     for (int b = 0; b < nb; ++b) hs[b] = static_cast<int32_t>(sources[b0 + b]);
-    GBX_CUDA(cudaMemcpyAsync(dsrc.p, hs, nb * 4, cudaMemcpyHostToDevice, s));
-    k_bc_init<<<ceil_div(n * 4, 256), 256, 0, s>>>(W.level.p, W.sigma.p, W.delta.p, mark.p,
-                                                    acc.p, n);
-    k_bc_seed<<<1, 1, 0, s>>>(dsrc.p, nb, W.level.p, W.sigma.p, mark.p, W.order.p, ent[0].p,
-                              W.ctl.p, A.rp.p);
+    GBX_CUDA(cudaMemcpyAsync(W.src.p, hs, nb * 4, cudaMemcpyHostToDevice, s));
+    k_bc_init<<<ceil_div(n1 * 4, 256), 256, 0, s>>>(W.level.p, W.lv8.p, W.sigma.p, W.mark.p, n);
+    GBX_CUDA(cudaMemsetAsync(W.map[0].p, 0, map_bytes, s));
+    GBX_CUDA(cudaMemsetAsync(W.map[1].p, 0, map_bytes, s));
+    k_bc_seed<<<1, 1, 0, s>>>(W.src.p, nb, W.level.p, W.lv8.p, W.sigma.p, W.mark.p, W.order.p,
+                              W.ent[0].p, ctl, dedges, A.rp.p, W.map[0].p);
     GBX_LAUNCHED();
     launches += 2;
     // ---- forward sweep
     std::vector<int64_t> off = {0};
-    int hc[2];
-    GBX_CUDA(cudaMemcpyAsync(hc, W.ctl.p, 8, cudaMemcpyDeviceToHost, s));
+    struct Hc { int c[4]; unsigned long long e; } hc;
+    GBX_CUDA(cudaMemcpyAsync(&hc, W.ctl.p, sizeof hc, cudaMemcpyDeviceToHost, s));
     GBX_CUDA(cudaStreamSynchronize(s));
-    off.push_back(hc[0]);
-    int n_ent = hc[1];
-    int cur = 0;
+    off.push_back(hc.c[0]);
+    int n_ent = hc.c[1];
+    unsigned long long fe = hc.e;
+    unsigned live = static_cast<unsigned>(hc.c[3]);
+    int cur = 0, ucur = 0, ucnt = -1;
     for (int d = 1; static_cast<int64_t>(d) <= n; ++d) {
       if (off.back() == off[off.size() - 2]) break;
-      GBX_CUDA(cudaMemsetAsync(W.ctl.p, 0, 8, s));
+      GBX_CUDA(cudaMemsetAsync(W.ctl.p, 0, sizeof hc, s));
       BcArgs a{};
       a.rp = A.rp.p;
       a.col = A.col.p;
+      a.trp = AT.rp.p;
+      a.tcol = AT.col.p;
+      a.n = n;
       a.level = W.level.p;
+      a.lv8 = W.lv8.p;
       a.sigma = W.sigma.p;
-      a.delta = W.delta.p;
-      a.mark = mark.p;
+      a.mark = W.mark.p;
       a.list_out = W.order.p + off.back();
-      a.ent_in = ent[cur].p;
-      a.ent_out = ent[cur ^ 1].p;
-      a.cnt = W.ctl.p;
+      a.ent_in = W.ent[cur].p;
+      a.ent_out = W.ent[cur ^ 1].p;
       a.n_ent = n_ent;
+      a.cnt = ctl;
+      a.edges = dedges;
       a.d = d;
-      a.lanes = nb;
-      k_bc_forward<<<grid, 256, 0, s>>>(a);
-      GBX_LAUNCHED();
-      ++launches;
-      GBX_CUDA(cudaMemcpyAsync(hc, W.ctl.p, 8, cudaMemcpyDeviceToHost, s));
+      a.lanes = live;
+      a.map_in = W.map[cur].p;
+      a.map_out = W.map[cur ^ 1].p;
+      const bool push = alpha <= 0 || fe * static_cast<unsigned long long>(alpha) <
+                                          static_cast<unsigned long long>(A.nnz);
+      if (push) {
+        k_bc_push<<<grid, 256, 0, s>>>(a);
+        GBX_LAUNCHED();
+        ++launches;
+      } else {
+        // a pull settles every vertex of level d at once, so mark[] (push
+        // dedup) must not see a stale d later: pull never lists twice
+        a.ul_in = W.ulist[ucur].p;
+        a.ul_out = W.ulist[ucur ^ 1].p;
+        a.ul_cnt = ucnt;
+        a.hv = HT.hv.p;
+        a.hent = HT.hent.p;
+        a.nhv = HT.nhv;
+        a.nhent = HT.nhent;
+        a.hacc = HT.hacc.p;
+        k_bc_pull<<<grid, 256, 0, s>>>(a);
+        GBX_LAUNCHED();
+        ++launches;
+        if (HT.nhv) {
+          k_bc_pull_hub<<<grid, 256, 0, s>>>(a);
+          k_bc_pull_hub_fin<<<ceil_div(HT.nhv, 256), 256, 0, s>>>(a);
+          GBX_LAUNCHED();
+          launches += 2;
+        }
+      }
+      GBX_CUDA(cudaMemcpyAsync(&hc, W.ctl.p, sizeof hc, cudaMemcpyDeviceToHost, s));
       GBX_CUDA(cudaStreamSynchronize(s));
-      off.push_back(off.back() + hc[0]);
-      n_ent = hc[1];
+      off.push_back(off.back() + hc.c[0]);
+      n_ent = hc.c[1];
+      fe = hc.e;
+      live = static_cast<unsigned>(hc.c[3]);
+      if (!push) {
+        ucnt = hc.c[2];
+        ucur ^= 1;
+      }
+      GBX_CUDA(cudaMemsetAsync(W.map[cur].p, 0, map_bytes, s));  // depth d-1 map retired
       cur ^= 1;
     }
     // levels: off[d]..off[d+1] lists vertices with some lane at depth d
@@ -289,10 +721,11 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     max_levels = std::max(max_levels, D);
     int deepest = D - 1;
     while (deepest > 0 && off[deepest + 1] == off[deepest]) --deepest;
+    const unsigned all = (1u << nb) - 1;
     if (deepest >= 1) {
       const int nl = static_cast<int>(off[deepest + 1] - off[deepest]);
-      k_bc_leaf<<<ceil_div(nl, 256), 256, 0, s>>>(W.order.p + off[deepest], nl, deepest, nb,
-                                                   W.level.p, W.sigma.p, W.delta.p);
+      k_bc_leaf<<<ceil_div(nl, 256), 256, 0, s>>>(W.order.p + off[deepest], nl, deepest, all,
+                                                   W.level.p, W.lv8.p, W.sigma.p, W.delta.p);
       GBX_LAUNCHED();
       ++launches;
       // the deepest level has delta = 0: nothing to add to the centrality
@@ -300,29 +733,39 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     for (int d = deepest - 1; d >= 1; --d) {
       const int nl = static_cast<int>(off[d + 1] - off[d]);
       if (nl == 0) continue;
-      const int32_t* list = W.order.p + off[d];
-      GBX_CUDA(cudaMemsetAsync(W.ctl.p, 0, 4, s));
-      k_bc_entries<<<ceil_div(nl, 256), 256, 0, s>>>(list, nl, A.rp.p, ent[0].p, W.ctl.p);
-      GBX_LAUNCHED();
-      int ne = 0;
-      GBX_CUDA(cudaMemcpyAsync(&ne, W.ctl.p, 4, cudaMemcpyDeviceToHost, s));
-      GBX_CUDA(cudaStreamSynchronize(s));
       BcArgs a{};
       a.rp = A.rp.p;
       a.col = A.col.p;
+      a.n = n;
       a.level = W.level.p;
+      a.lv8 = W.lv8.p;
       a.sigma = W.sigma.p;
-      a.delta = W.delta.p;
-      a.ent_in = ent[0].p;
-      a.acc = acc.p;
-      a.n_ent = ne;
+      a.coef = W.delta.p;
+      a.cent = W.cent.p;
+      a.list_in = W.order.p + off[d];
+      a.n_list = nl;
+      a.hv = W.hub_a.hv.p;
+      a.hent = W.hub_a.hent.p;
+      a.nhv = W.hub_a.nhv;
+      a.nhent = W.hub_a.nhent;
+      a.hacc = W.hub_a.hacc.p;
       a.d = d;
-      a.lanes = nb;
-      k_bc_backward<<<grid, 256, 0, s>>>(a);
-      k_bc_finalize<<<ceil_div(nl, 256), 256, 0, s>>>(list, nl, d, nb, W.level.p, W.sigma.p,
-                                                       W.delta.p, acc.p, W.cent.p);
+      a.lanes = all;
+      // level map of depth d+1 (the successors' depth) from its list
+      const int nl1 = static_cast<int>(off[d + 2] - off[d + 1]);
+      GBX_CUDA(cudaMemsetAsync(W.map[0].p, 0, map_bytes, s));
+      k_bc_map<<<ceil_div(std::max(nl1, 1), 256), 256, 0, s>>>(W.order.p + off[d + 1], nl1, d + 1,
+                                                               all, W.level.p, W.lv8.p, W.map[0].p);
+      a.map_in = W.map[0].p;
+      k_bc_back<<<std::min<int64_t>(grid, ceil_div(nl, 32)), 256, 0, s>>>(a);
       GBX_LAUNCHED();
-      launches += 3;
+      ++launches;
+      if (W.hub_a.nhv) {
+        k_bc_back_hub<<<grid, 256, 0, s>>>(a);
+        k_bc_back_hub_fin<<<ceil_div(W.hub_a.nhv, 256), 256, 0, s>>>(a);
+        GBX_LAUNCHED();
+        launches += 2;
+      }
     }
     edges += A.nnz;
   }

@@ -119,15 +119,29 @@ struct SsspPlan {
 };
 
 // Betweenness workspaces (bc.cu).
+struct BcHubs {                // rows longer than kBcHeavy, split into chunks
+  DevArray<int32_t> hv;        // slot -> vertex
+  DevArray<int64_t> hent;      // chunk << 32 | slot
+  DevArray<double> hacc;       // [slot][4] partial sums, zero between uses
+  int nhv = 0, nhent = 0;
+  const void* key = nullptr;
+  int64_t nnz = -1;
+};
+
 struct BcWork {
   int64_t n = 0;
   int lanes = 0;
   DevArray<int32_t> level;   // [n][lanes]
+  DevArray<uint32_t> lv8;    // [n]: byte per lane, min(depth, 254), 0xFF unreached
   DevArray<double> sigma;    // [n][lanes]
-  DevArray<double> delta;    // [n][lanes]
+  DevArray<double> delta;    // [n][lanes]: (1 + delta) / sigma once final
   DevArray<int32_t> order;   // vertices by level (union over lanes)
+  DevArray<int32_t> mark, ulist[2], src;
+  DevArray<int64_t> ent[2];
+  DevArray<uint32_t> map[2];  // level maps: 4 bits (lanes) per vertex
   DevArray<double> cent;
   DevArray<int> ctl;
+  BcHubs hub_a, hub_t;       // hub rows of A (backward) and AT (forward pull)
 };
 
 struct CcWork {

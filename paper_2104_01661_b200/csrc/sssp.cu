@@ -138,7 +138,6 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
   nearq.buf = s_near[threadIdx.x >> 5];
   farq.buf = s_far[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
-  const int grp = lane >> 3, sub = lane & 7;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;

@@ -380,6 +380,54 @@ def test_bc_rmat_vs_oracle(und):
     assert rel_l1(got, want) <= 1e-9
 
 
+@pytest.mark.parametrize("und", [True, False])
+def test_bc_rmat16_hubs_vs_oracle(und):
+    """Scale 16: rows longer than the hub threshold take the chunked passes, and
+    the middle levels are pulled."""
+    kind = P.Kind.UndirectedAdjacency if und else P.Kind.DirectedAdjacency
+    g = P.generate_rmat(16, 16, seed=3, kind=kind)
+    P.property_at(g)
+    P.property_rowdegree(g)
+    rp, col, _ = g.export()
+    n = len(rp) - 1
+    trp, tcol, _ = O.transpose(n, rp, col)
+    assert np.diff(rp).max() > 2048 or np.diff(trp).max() > 2048
+    srcs = P.pick_sources(g.row_degree(), 4, 3)
+    got = algo.betweenness_centrality(g, srcs).centrality
+    want = O.bc(n, rp, col, trp, tcol, srcs)
+    assert rel_l1(got, want) <= 1e-9
+
+
+def _undirected(n, edges):
+    import scipy.sparse as sp
+    e = np.asarray(edges, np.int64)
+    r = np.concatenate([e[:, 0], e[:, 1]])
+    c = np.concatenate([e[:, 1], e[:, 0]])
+    m = sp.csr_matrix((np.ones(len(r)), (r, c)), shape=(n, n))
+    m.sum_duplicates()
+    m.sort_indices()
+    return m.indptr.astype(np.int64), m.indices.astype(np.int32)
+
+
+def test_bc_deep_path_and_components():
+    """Depths past 254 (the one-byte level filter saturates) and a lane whose
+    source sits in a small component (its lane dies early)."""
+    n_path = 700
+    edges = [(i, i + 1) for i in range(n_path - 1)]
+    # a second component: a star with a tail, plus an isolated vertex
+    base = n_path
+    edges += [(base, base + k) for k in range(1, 40)] + [(base + 39, base + 40)]
+    n = base + 42
+    rp, col = _undirected(n, edges)
+    g = P.graph_new(rp, col, kind=P.Kind.UndirectedAdjacency)
+    P.property_at(g)
+    trp, tcol = rp, col
+    for srcs in ([0, 350, base + 5, 699], [3, base], [base + 41]):
+        got = algo.betweenness_centrality(g, srcs).centrality
+        want = O.bc(n, rp, col, trp, tcol, np.asarray(srcs, np.int64))
+        assert np.max(np.abs(got - want)) <= 1e-9 * max(1.0, np.abs(want).max())
+
+
 # ---------------------------------------------------------------- multi-GPU shard kernels
 def test_pr_shards_compose_on_one_gpu():
     """Two shard plans (ranks 0 and 1 of 2) stepped in lockstep with the x

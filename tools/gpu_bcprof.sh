@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on --kernel-name-base function -k regex:'^k_bc_pull$' -c 1 -o gpurun_out/bc_pull -f python tools/prof_algo.py bc 24 > gpurun_out/bc_prof1.log 2>&1; echo rc=$?
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on --kernel-name-base function -k regex:'^k_bc_back$' --launch-skip 2 -c 1 -o gpurun_out/bc_back -f python tools/prof_algo.py bc 24 > gpurun_out/bc_prof2.log 2>&1; echo rc=$?
