@@ -27,6 +27,8 @@
 // centrality(j) = sum_b (B(b,j) - 1) = sum_b delta_b(j) (betweenness.cpp:74-79);
 // sources and unreached vertices contribute 0, undirected pairs not halved.
 // Algorithmic bytes per batch: E_r*(8 + 16*ns) + V_r*(16 + 24*ns).
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -93,20 +95,21 @@ __device__ __forceinline__ int32_t ld_col(const int32_t* p) {
 }
 
 // s[b] += val[u][b] over the row entries p, p+st, ... < e whose map nibble is
-// in m; four independent column loads, then four map gathers, per step (the
-// chain col -> map -> val is latency-bound, so each lane keeps 4 in flight)
+// in m; U independent column loads, then U map gathers, per step (the chain
+// col -> map -> val is latency-bound, so each lane keeps U in flight)
+template <int U>
 __device__ __forceinline__ void row_sum(const int32_t* col, int64_t p, int64_t e, int st,
                                         const uint32_t* map, const double* val, unsigned m,
                                         double s[4]) {
-  for (; p < e; p += 4 * st) {
-    int32_t u[4];
+  for (; p < e; p += U * st) {
+    int32_t u[U];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) u[k] = p + k * st < e ? ld_col(col + p + k * st) : -1;
-    unsigned h[4];
+    for (int k = 0; k < U; ++k) u[k] = p + k * st < e ? ld_col(col + p + k * st) : -1;
+    unsigned h[U];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) h[k] = u[k] >= 0 ? (nib(map, u[k]) & m) : 0u;
+    for (int k = 0; k < U; ++k) h[k] = u[k] >= 0 ? (nib(map, u[k]) & m) : 0u;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < U; ++k)
       if (h[k]) {
         const double* vp = val + static_cast<int64_t>(u[k]) * 4;
 #pragma unroll
@@ -132,9 +135,27 @@ __device__ __forceinline__ void warp_reduce(double s[4]) {
     for (int o = 16; o > 0; o >>= 1) s[b] += __shfl_xor_sync(0xffffffffu, s[b], o);
 }
 
-// rows up to kBcShort edges are summed by their own lane, longer ones by an
-// 8-lane group (4 rows at a time per warp)
-constexpr int64_t kBcShort = 8;
+#ifndef GBX_BC_UNROLL
+#define GBX_BC_UNROLL 4
+#endif
+constexpr int kBcUnroll = GBX_BC_UNROLL;  // loads in flight per lane, group/hub rows
+#ifndef GBX_BC_MINB
+#define GBX_BC_MINB 5
+#endif
+constexpr int kBcMinBlocks = GBX_BC_MINB;  // resident 256-thread blocks per SM asked of ptxas
+
+// Row-length bins: rows of a list are partitioned (2-bit radix sort, stable)
+// so a warp step handles rows of one shape -- bin 0 (<= kBin0 edges): one
+// row per lane; bin 1 (<= kBin1): 8-lane groups, 4 rows per warp; bin 2
+// (<= kBcHeavy): one row per warp; bin 3 (hubs): the chunked side passes.
+constexpr int64_t kBin0 = 8, kBin1 = 64;
+__device__ __forceinline__ uint8_t deg_bin(int64_t deg) {
+  return deg <= kBin0 ? 0 : deg <= kBin1 ? 1 : deg <= kBcHeavy ? 2 : 3;
+}
+struct BcBins {
+  const int32_t* list;  // [bin 0 | bin 1 | bin 2 | bin 3]
+  const int* cnt;       // device: sizes of bins 0..3
+};
 
 struct BcArgs {
   const int64_t* rp;   // A
@@ -161,6 +182,7 @@ struct BcArgs {
   const int32_t* hv;     // hub rows (slot -> vertex) and their chunks (chunk<<32|slot)
   const int64_t* hent;
   int nhv, nhent;
+  BcBins bins;             // pull: still-unreached vertices / back: level-d list
   const uint32_t* map_in;  // level map of depth d-1 (forward) / d+1 (backward)
   uint32_t* map_out;       // forward: level map of depth d being built
   int* cnt;  // [0] list [1] entries [2] unreached list [3] lanes discovered
@@ -199,9 +221,15 @@ __global__ void __launch_bounds__(256) k_bc_push(BcArgs a) {
       if (p < e0 && m) {
         v = __ldg(a.col + p);
         int32_t* lvp = a.level + static_cast<int64_t>(v) * 4;
+        // the lv8 word (L2-resident) filters out the lanes where v is already
+        // settled on an earlier depth before touching the int32 level words
+        const uint32_t x = *(volatile uint32_t*)&a.lv8[v];
+        const uint32_t db = lv8_byte(d);
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           if (!((m >> b) & 1u)) continue;
+          const uint32_t xb = (x >> (8 * b)) & 0xFFu;
+          if (xb != 0xFFu && xb != db) continue;
           int lv = *(volatile int32_t*)&lvp[b];
           if (lv == -1) {
             lv = atomicCAS(&lvp[b], -1, d);
@@ -249,7 +277,7 @@ __device__ __forceinline__ unsigned bc_settle(const BcArgs& a, int64_t v, unsign
   return nm;
 }
 
-__global__ void __launch_bounds__(256) k_bc_pull(BcArgs a) {
+__global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_pull(BcArgs a) {
   __shared__ int32_t s_buf[8][kBcBuf];
   __shared__ int32_t s_ubuf[8][kBcBuf];
   FrontierQueue<kBcBuf> fq;
@@ -264,54 +292,54 @@ __global__ void __launch_bounds__(256) k_bc_pull(BcArgs a) {
   const int grp = lane >> 3, sub = lane & 7;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  const int64_t range = a.ul_cnt < 0 ? a.n : a.ul_cnt;
+  const int32_t* L = a.bins.list;
+  const int n0 = a.bins.cnt[0], n1 = a.bins.cnt[1], n2 = a.bins.cnt[2];
+  const int64_t s0 = (n0 + 31) / 32, s1 = (n1 + 3) / 4, tot = s0 + s1 + n2;
   unsigned found = 0;
-  for (int64_t vb = gwarp * 32; vb < range; vb += nwarps * 32) {
-    const int64_t i = vb + lane;
-    const int64_t v = i < range ? (a.ul_cnt < 0 ? i : a.ul_in[i]) : -1;
-    unsigned um = 0;
-    int64_t pp = 0, pe = 0;
-    if (v >= 0) {
-      um = lanes_unreached(a.lv8[v], a.lanes);
-      if (um) {
-        pp = a.trp[v];
-        pe = a.trp[v + 1];
-        if (pe - pp > kBcHeavy) um = 0;  // hub: chunked side pass
+  for (int64_t t = gwarp; t < tot; t += nwarps) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    if (t < s0) {  // bin 0: a row per lane
+      const int64_t i = t * 32 + lane;
+      const int64_t v = i < n0 ? L[i] : -1;
+      unsigned um = 0, nm = 0;
+      int64_t pp = 0, pe = 0;
+      if (v >= 0) {
+        um = lanes_unreached(a.lv8[v], a.lanes);
+        if (um) {
+          pp = a.trp[v];
+          pe = a.trp[v + 1];
+          row_sum<4>(a.tcol, pp, pe, 1, a.map_in, a.sigma, um, s);
+          nm = bc_settle(a, v, um, s);
+          found |= nm;
+        }
       }
-    }
-    const bool keep = um != 0 && pe > pp;
-    const bool mine = keep && pe - pp <= kBcShort;
-    unsigned nm = 0;
-    if (mine) {
-      double s[4] = {0.0, 0.0, 0.0, 0.0};
-      row_sum(a.tcol, pp, pe, 1, a.map_in, a.sigma, um, s);
-      nm = bc_settle(a, v, um, s);
-      found |= nm;
-    }
-    fq.push(nm != 0, static_cast<int32_t>(v));
-    uq.push(mine && (um & ~nm) != 0, static_cast<int32_t>(v));
-    unsigned rest = __ballot_sync(kAll, keep && !mine);
-    while (rest) {
-      unsigned m = rest;
-      for (int k = 0; k < grp && m; ++k) m &= m - 1;
-      const int src = m ? __ffs(m) - 1 : -1;
-      for (int k = 0; k < 4 && rest; ++k) rest &= rest - 1;
-      const int sl = src < 0 ? 0 : src;
-      const int64_t gv = __shfl_sync(kAll, v, sl);
-      const int64_t gp = __shfl_sync(kAll, pp, sl);
-      const int64_t ge = __shfl_sync(kAll, pe, sl);
-      const unsigned gum0 = __shfl_sync(kAll, um, sl);
-      const unsigned gum = src < 0 ? 0u : gum0;
-      double s[4] = {0.0, 0.0, 0.0, 0.0};
-      if (gum) row_sum(a.tcol, gp + sub, ge, 8, a.map_in, a.sigma, gum, s);
+      fq.push(nm != 0, static_cast<int32_t>(v));
+      uq.push(pe > pp && (um & ~nm) != 0, static_cast<int32_t>(v));
+    } else if (t < s0 + s1) {  // bin 1: 8 lanes per row
+      const int64_t i = n0 + (t - s0) * 4 + grp;
+      const int64_t v = i < n0 + n1 ? L[i] : -1;
+      const unsigned um = v >= 0 ? lanes_unreached(a.lv8[v], a.lanes) : 0u;
+      if (um) row_sum<kBcUnroll>(a.tcol, a.trp[v] + sub, a.trp[v + 1], 8, a.map_in, a.sigma, um, s);
       group_reduce(s);
-      unsigned gnm = 0;
-      if (sub == 0 && gum) {
-        gnm = bc_settle(a, gv, gum, s);
-        found |= gnm;
+      unsigned nm = 0;
+      if (sub == 0 && um) {
+        nm = bc_settle(a, v, um, s);
+        found |= nm;
       }
-      fq.push(gnm != 0, static_cast<int32_t>(gv));
-      uq.push(sub == 0 && gum && (gum & ~gnm) != 0, static_cast<int32_t>(gv));
+      fq.push(nm != 0, static_cast<int32_t>(v));
+      uq.push(sub == 0 && (um & ~nm) != 0, static_cast<int32_t>(v));
+    } else {  // bin 2: a warp per row
+      const int64_t v = L[n0 + n1 + (t - s0 - s1)];
+      const unsigned um = lanes_unreached(a.lv8[v], a.lanes);
+      if (um) row_sum<kBcUnroll>(a.tcol, a.trp[v] + lane, a.trp[v + 1], 32, a.map_in, a.sigma, um, s);
+      warp_reduce(s);
+      unsigned nm = 0;
+      if (lane == 0 && um) {
+        nm = bc_settle(a, v, um, s);
+        found |= nm;
+      }
+      fq.push(nm != 0, static_cast<int32_t>(v));
+      uq.push(lane == 0 && (um & ~nm) != 0, static_cast<int32_t>(v));
     }
   }
   fq.flush();
@@ -322,7 +350,7 @@ __global__ void __launch_bounds__(256) k_bc_pull(BcArgs a) {
 }
 
 // forward pull, hub rows: one warp per chunk, partial sums into hacc[slot]
-__global__ void __launch_bounds__(256) k_bc_pull_hub(BcArgs a) {
+__global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_pull_hub(BcArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -336,7 +364,7 @@ __global__ void __launch_bounds__(256) k_bc_pull_hub(BcArgs a) {
     const int64_t b0 = a.trp[v] + c * kBcHChunk;
     const int64_t e0 = min(a.trp[v + 1], b0 + kBcHChunk);
     double s[4] = {0.0, 0.0, 0.0, 0.0};
-    row_sum(a.tcol, b0 + lane, e0, 32, a.map_in, a.sigma, um, s);
+    row_sum<kBcUnroll>(a.tcol, b0 + lane, e0, 32, a.map_in, a.sigma, um, s);
     warp_reduce(s);
     if (lane < 4 && ((um >> lane) & 1u)) {
       const double mine = lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3];
@@ -408,51 +436,45 @@ __device__ __forceinline__ void bc_final(const BcArgs& a, int64_t u, unsigned m,
   a.cent[u] += c;
 }
 
-__global__ void __launch_bounds__(256) k_bc_back(BcArgs a) {
+__global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_back(BcArgs a) {
   const int lane = threadIdx.x & 31;
   const int grp = lane >> 3, sub = lane & 7;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t vb = gwarp * 32; vb < a.n_list; vb += nwarps * 32) {
-    const int64_t i = vb + lane;
-    int64_t u = 0;
-    unsigned m = 0;
-    int64_t pp = 0, pe = 0;
-    if (i < a.n_list) {
-      u = a.list_in[i];
-      m = lanes_on(a.lv8[u], a.d, a.lanes, a.level, u);
-      pp = a.rp[u];
-      pe = a.rp[u + 1];
-      if (pe - pp > kBcHeavy) m = 0;  // hub: chunked side pass
-    }
-    const bool mine = m != 0 && pe - pp <= kBcShort;
-    if (mine) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      row_sum(a.col, pp, pe, 1, a.map_in, a.coef, m, acc);
-      bc_final(a, u, m, acc);
-    }
-    unsigned rest = __ballot_sync(kAll, m != 0 && !mine);
-    while (rest) {
-      unsigned r = rest;
-      for (int k = 0; k < grp && r; ++k) r &= r - 1;
-      const int src = r ? __ffs(r) - 1 : -1;
-      for (int k = 0; k < 4 && rest; ++k) rest &= rest - 1;
-      const int sl = src < 0 ? 0 : src;
-      const int64_t gu = __shfl_sync(kAll, u, sl);
-      const int64_t gp = __shfl_sync(kAll, pp, sl);
-      const int64_t ge = __shfl_sync(kAll, pe, sl);
-      const unsigned gm0 = __shfl_sync(kAll, m, sl);
-      const unsigned gm = src < 0 ? 0u : gm0;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      if (gm) row_sum(a.col, gp + sub, ge, 8, a.map_in, a.coef, gm, acc);
+  const int32_t* L = a.bins.list;
+  const int n0 = a.bins.cnt[0], n1 = a.bins.cnt[1], n2 = a.bins.cnt[2];
+  const int64_t s0 = (n0 + 31) / 32, s1 = (n1 + 3) / 4, tot = s0 + s1 + n2;
+  for (int64_t t = gwarp; t < tot; t += nwarps) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (t < s0) {  // bin 0: a row per lane
+      const int64_t i = t * 32 + lane;
+      if (i < n0) {
+        const int64_t u = L[i];
+        const unsigned m = lanes_on(a.lv8[u], a.d, a.lanes, a.level, u);
+        if (m) {
+          row_sum<4>(a.col, a.rp[u], a.rp[u + 1], 1, a.map_in, a.coef, m, acc);
+          bc_final(a, u, m, acc);
+        }
+      }
+    } else if (t < s0 + s1) {  // bin 1: 8 lanes per row
+      const int64_t i = n0 + (t - s0) * 4 + grp;
+      const int64_t u = i < n0 + n1 ? L[i] : -1;
+      const unsigned m = u >= 0 ? lanes_on(a.lv8[u], a.d, a.lanes, a.level, u) : 0u;
+      if (m) row_sum<kBcUnroll>(a.col, a.rp[u] + sub, a.rp[u + 1], 8, a.map_in, a.coef, m, acc);
       group_reduce(acc);
-      if (sub == 0 && gm) bc_final(a, gu, gm, acc);
+      if (sub == 0 && m) bc_final(a, u, m, acc);
+    } else {  // bin 2: a warp per row
+      const int64_t u = L[n0 + n1 + (t - s0 - s1)];
+      const unsigned m = lanes_on(a.lv8[u], a.d, a.lanes, a.level, u);
+      if (m) row_sum<kBcUnroll>(a.col, a.rp[u] + lane, a.rp[u + 1], 32, a.map_in, a.coef, m, acc);
+      warp_reduce(acc);
+      if (lane == 0 && m) bc_final(a, u, m, acc);
     }
   }
 }
 
 // backward, hub rows of A: one warp per chunk, partial sums into hacc[slot]
-__global__ void __launch_bounds__(256) k_bc_back_hub(BcArgs a) {
+__global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_back_hub(BcArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -467,7 +489,7 @@ __global__ void __launch_bounds__(256) k_bc_back_hub(BcArgs a) {
     const int64_t b0 = a.rp[u] + c * kBcHChunk;
     const int64_t e0 = min(a.rp[u + 1], b0 + kBcHChunk);
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    row_sum(a.col, b0 + lane, e0, 32, a.map_in, a.coef, m, acc);
+    row_sum<kBcUnroll>(a.col, b0 + lane, e0, 32, a.map_in, a.coef, m, acc);
     warp_reduce(acc);
     if (lane < 4 && ((m >> lane) & 1u)) {
       const double mine = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
@@ -565,6 +587,49 @@ __global__ void k_bc_hubs(const int64_t* rp, int64_t n, int32_t* hv, int64_t* he
   for (int c = 0; c < k; ++c) hent[off + c] = (static_cast<int64_t>(c) << 32) | slot;
 }
 
+// keys = row-length bin of each listed vertex (list == nullptr: 0..n-1, also
+// written to iota); cnt[0..3] += bin sizes (block-aggregated: one atomic per
+// bin per block)
+__global__ void __launch_bounds__(256) k_bc_bin_keys(const int32_t* list, int64_t n,
+                                                     const int64_t* rp, uint8_t* keys,
+                                                     int32_t* iota, int* cnt) {
+  __shared__ int s_cnt[4];
+  if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = blockIdx.x * int64_t(blockDim.x); i0 < n; i0 += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    int k = -1;
+    if (i < n) {
+      const int64_t v = list ? list[i] : i;
+      if (!list) iota[i] = static_cast<int32_t>(i);
+      k = deg_bin(rp[v + 1] - rp[v]);
+      keys[i] = static_cast<uint8_t>(k);
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const unsigned bal = __ballot_sync(kAll, k == b);
+      if (lane == 0 && bal) atomicAdd(&s_cnt[b], __popc(bal));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && s_cnt[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], s_cnt[threadIdx.x]);
+}
+
+// stable partition of list[0, n) by row-length bin of M into out; sizes to cnt
+static void bin_list(cudaStream_t s, BcWork& W, const int32_t* list, int64_t n, const Csr& M,
+                     int32_t* out, int* cnt) {
+  GBX_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(int), s));
+  if (n == 0) return;
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), device_sms() * 8));
+  k_bc_bin_keys<<<blocks, 256, 0, s>>>(list, n, M.rp.p, W.bkeys[0].p, W.iota.p, cnt);
+  GBX_LAUNCHED();
+  size_t tb = W.btemp.bytes();
+  GBX_CUDA(cub::DeviceRadixSort::SortPairs(W.btemp.p, tb, W.bkeys[0].p, W.bkeys[1].p,
+                                           list ? list : W.iota.p, out, static_cast<int>(n), 0,
+                                           2, s));
+}
+
 static void build_hubs(cudaStream_t s, const Csr& M, BcHubs& H) {
   if (H.key == M.rp.p && H.nnz == M.nnz && H.hv.p) return;
   const int64_t n1 = std::max<int64_t>(M.n, 1);
@@ -608,6 +673,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     W.sigma.alloc(n1 * 4);
     W.delta.alloc(n1 * 4);
     W.order.alloc(n1 * 4 + 8);
+    W.border.alloc(n1 * 4 + 8);
     W.cent.alloc(n1);
     W.mark.alloc(n1);
     W.ulist[0].alloc(n1);
@@ -618,12 +684,29 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     W.src.alloc(4);
     W.map[0].alloc(n1 / 8 + 1);
     W.map[1].alloc(n1 / 8 + 1);
+    W.bkeys[0].alloc(n1);
+    W.bkeys[1].alloc(n1);
+    W.iota.alloc(n1);
+    W.ucnt.alloc(4);
+    W.allcnt.alloc(4);
+    W.allbin.alloc(n1);
+    size_t tb = 0;
+    GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, W.bkeys[0].p, W.bkeys[1].p, W.iota.p,
+                                             W.order.p, static_cast<int>(n1), 0, 2, s));
+    W.btemp.alloc(tb + 256);
+    W.allbin_key = nullptr;
   }
   const size_t map_bytes = (n1 / 8 + 1) * sizeof(uint32_t);
   build_hubs(s, A, W.hub_a);
   const bool same = &AT == &A;
   if (!same) build_hubs(s, AT, W.hub_t);
   BcHubs& HT = same ? W.hub_a : W.hub_t;
+  // every vertex, binned by in-degree: the first pull's work list
+  if (W.allbin_key != AT.rp.p || W.allbin_nnz != AT.nnz) {
+    bin_list(s, W, nullptr, n, AT, W.allbin.p, W.allcnt.p);
+    W.allbin_key = AT.rp.p;
+    W.allbin_nnz = AT.nnz;
+  }
   GBX_CUDA(cudaMemsetAsync(W.cent.p, 0, n1 * 8, s));
   const int grid = device_sms() * 8;
   static const int alpha = std::getenv("GBX_BC_ALPHA") ? std::atoi(std::getenv("GBX_BC_ALPHA")) : 14;
@@ -652,7 +735,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     int n_ent = hc.c[1];
     unsigned long long fe = hc.e;
     unsigned live = static_cast<unsigned>(hc.c[3]);
-    int cur = 0, ucur = 0, ucnt = -1;
+    int cur = 0, ucnt = -1;
     for (int d = 1; static_cast<int64_t>(d) <= n; ++d) {
       if (off.back() == off[off.size() - 2]) break;
       GBX_CUDA(cudaMemsetAsync(W.ctl.p, 0, sizeof hc, s));
@@ -676,18 +759,29 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       a.lanes = live;
       a.map_in = W.map[cur].p;
       a.map_out = W.map[cur ^ 1].p;
-      const bool push = alpha <= 0 || fe * static_cast<unsigned long long>(alpha) <
-                                          static_cast<unsigned long long>(A.nnz);
+      // push while the frontier's edges are under nnz/alpha -- and, once a pull
+      // has listed the still-unreached vertices, only while the frontier's
+      // edges are under those vertices' (estimated) in-edges
+      const double unreached_edges =
+          ucnt < 0 ? 1e300 : static_cast<double>(ucnt) * A.nnz / std::max<int64_t>(n, 1);
+      const bool push = alpha <= 0 || (fe * static_cast<unsigned long long>(alpha) <
+                                           static_cast<unsigned long long>(A.nnz) &&
+                                       static_cast<double>(fe) < unreached_edges);
       if (push) {
         k_bc_push<<<grid, 256, 0, s>>>(a);
         GBX_LAUNCHED();
         ++launches;
       } else {
-        // a pull settles every vertex of level d at once, so mark[] (push
-        // dedup) must not see a stale d later: pull never lists twice
-        a.ul_in = W.ulist[ucur].p;
-        a.ul_out = W.ulist[ucur ^ 1].p;
-        a.ul_cnt = ucnt;
+        // work list: every vertex (first pull) or the survivors of the last
+        // pull, binned by in-degree; survivors of this pull go to ulist[0]
+        if (ucnt < 0) {
+          a.bins = BcBins{W.allbin.p, W.allcnt.p};
+        } else {
+          bin_list(s, W, W.ulist[0].p, ucnt, AT, W.ulist[1].p, W.ucnt.p);
+          a.bins = BcBins{W.ulist[1].p, W.ucnt.p};
+          launches += 2;
+        }
+        a.ul_out = W.ulist[0].p;
         a.hv = HT.hv.p;
         a.hent = HT.hent.p;
         a.nhv = HT.nhv;
@@ -709,10 +803,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       n_ent = hc.c[1];
       fe = hc.e;
       live = static_cast<unsigned>(hc.c[3]);
-      if (!push) {
-        ucnt = hc.c[2];
-        ucur ^= 1;
-      }
+      if (!push) ucnt = hc.c[2];
       GBX_CUDA(cudaMemsetAsync(W.map[cur].p, 0, map_bytes, s));  // depth d-1 map retired
       cur ^= 1;
     }
@@ -730,6 +821,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       ++launches;
       // the deepest level has delta = 0: nothing to add to the centrality
     }
+    if (static_cast<int64_t>(W.lcnt.n) < 4 * static_cast<int64_t>(D + 1)) W.lcnt.alloc(4 * (D + 1));
     for (int d = deepest - 1; d >= 1; --d) {
       const int nl = static_cast<int>(off[d + 1] - off[d]);
       if (nl == 0) continue;
@@ -742,8 +834,6 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       a.sigma = W.sigma.p;
       a.coef = W.delta.p;
       a.cent = W.cent.p;
-      a.list_in = W.order.p + off[d];
-      a.n_list = nl;
       a.hv = W.hub_a.hv.p;
       a.hent = W.hub_a.hent.p;
       a.nhv = W.hub_a.nhv;
@@ -757,9 +847,12 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       k_bc_map<<<ceil_div(std::max(nl1, 1), 256), 256, 0, s>>>(W.order.p + off[d + 1], nl1, d + 1,
                                                                all, W.level.p, W.lv8.p, W.map[0].p);
       a.map_in = W.map[0].p;
-      k_bc_back<<<std::min<int64_t>(grid, ceil_div(nl, 32)), 256, 0, s>>>(a);
+      // the level-d list binned by out-degree
+      bin_list(s, W, W.order.p + off[d], nl, A, W.border.p + off[d], W.lcnt.p + 4 * d);
+      a.bins = BcBins{W.border.p + off[d], W.lcnt.p + 4 * d};
+      k_bc_back<<<grid, 256, 0, s>>>(a);
       GBX_LAUNCHED();
-      ++launches;
+      launches += 4;
       if (W.hub_a.nhv) {
         k_bc_back_hub<<<grid, 256, 0, s>>>(a);
         k_bc_back_hub_fin<<<ceil_div(W.hub_a.nhv, 256), 256, 0, s>>>(a);

@@ -139,6 +139,15 @@ struct BcWork {
   DevArray<int32_t> mark, ulist[2], src;
   DevArray<int64_t> ent[2];
   DevArray<uint32_t> map[2];  // level maps: 4 bits (lanes) per vertex
+  // row-length binning (stable 2-bit radix partition of a vertex list)
+  DevArray<int32_t> border;   // level lists binned by out-degree
+  DevArray<int32_t> allbin;   // every vertex binned by in-degree (first pull)
+  DevArray<int32_t> iota;
+  DevArray<uint8_t> bkeys[2];
+  DevArray<uint8_t> btemp;
+  DevArray<int> ucnt, allcnt, lcnt;
+  const void* allbin_key = nullptr;
+  int64_t allbin_nnz = -1;
   DevArray<double> cent;
   DevArray<int> ctl;
   BcHubs hub_a, hub_t;       // hub rows of A (backward) and AT (forward pull)

@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "bc" 2>&1 | tail -1
+timeout -s KILL 300 python bench.py --workload bc --steps 3 --warmup 3 2>&1 | tail -1 | cut -c1-200
+timeout -s KILL 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bc_launches.csv python tools/prof_algo.py bc 24 > gpurun_out/bc_ncu.log 2>&1
