@@ -251,8 +251,9 @@ int gbx_pr_shard_unpermute(gbx_graph* g, const float* r_full_dev, double* rank_o
 /* Rows [row_begin,row_end) of a split with balanced nnz + rows (merge-path). */
 int gbx_partition_rows(int64_t* bounds, const gbx_graph* g, int parts, int transposed,
                        char msg[GBX_MSG_LEN]);
-/* Triangle count restricted to oriented rows [row_begin, row_end) of the
- * degree-ordered U (for wedge-balanced sharding; sum over shards = count). */
+/* Triangle count restricted to the triangles whose middle vertex, in the
+ * degree-ordered rank space, lies in [row_begin, row_end) (for work-balanced
+ * sharding; the sum over a partition of [0, n) = count). */
 int gbx_triangle_count_rows(uint64_t* count, const gbx_graph* g, int64_t row_begin,
                             int64_t row_end, char msg[GBX_MSG_LEN]);
 /* Wedge-balanced split of the oriented rows into parts. */

@@ -1,6 +1,8 @@
 // plans.cuh -- per-algorithm device layouts and workspaces owned by a gbx_graph.
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace gbx {
@@ -84,14 +86,21 @@ struct BfsWork {
   int64_t heavy_nnz = -1;
 };
 
-// Triangle counting plan (tc.cu): degree-ordered upper triangle U.
+// Triangle counting plan (tc.cu): degree-ordered upper triangle U, its
+// transpose as tails into U, and the per-middle-vertex work items.
 struct TcPlan {
   int64_t n = 0, nnz = 0;
   DevArray<int64_t> urp;
   DevArray<int32_t> ucol;
-  DevArray<int32_t> order;   // rows with >= 2 entries, heaviest first
-  DevArray<int64_t> work;    // prefix of per-row wedge work (ordered rows)
-  int64_t nrows_active = 0;
+  DevArray<int64_t> lrp;     // L = U' by middle vertex j
+  DevArray<int2> tails;      // [p + 1, urp[i + 1]) for L entry (i, p)
+  DevArray<int64_t> items;   // j << 32 | chunk of <= kTcItem in-neighbours
+  DevArray<int64_t> item_off;  // [n + 1]: first item of each j
+  int64_t nitems = 0;
+  std::vector<int32_t> heavy_h, huge_h;  // middle vertices with long U(j)
+  std::vector<int64_t> heavy_item_off_h;  // [heavy + 1]: first CTA item of each
+  DevArray<int64_t> heavy_items;          // j << 32 | chunk (CTA kernel)
+  DevArray<int32_t> huge;
   DevArray<unsigned long long> count;
   DevArray<unsigned> next_row;
 };

@@ -5,18 +5,22 @@
 // vertex relabeling (test_tc.cpp:43-55, 75-85), so the device path always
 // orients every edge from the lower to the higher (degree, id) rank -- the
 // reference's ascending-degree presort (util.cpp:35-44) -- and never
-// materialises C: for every row i of the oriented U and every j in U(i) it
-// counts |U(i) n U(j)|, fusing the mask, the plus.pair product and the
-// reduction (the fusion the paper asks for).
+// materialises C (the fusion the paper asks for).
 //
-// Kernel: one warp per row (dU(i) <= 1024): U(i) goes into a shared-memory
-// open-addressing hash table, then the concatenated lists U(j), j in U(i), are
-// streamed with all 32 lanes (a warp-level prefix sum over dU(j) assigns
-// elements to lanes, so short lists do not idle lanes) and probed in the
-// table.  Rows with longer U(i) use a whole CTA and a larger table; beyond
-// that, a binary search in global memory.  Counts are u64, reduced per warp.
-// Algorithmic bytes: 4*W (streamed U(j) elements) + 4*nnz(U) +
-// 8*(n+1), W = sum_i sum_{j in U(i)} dU(j).
+// Every triangle i < j < k (rank order) is counted once, at its MIDDLE vertex
+// j: for each in-neighbour i of j (j in U(i)), the tail of U(i) after j is
+// probed against U(j).  The probes are the wedges i -> (j, k) with j < k both
+// in U(i): sum_i C(dU(i), 2), 3.6x fewer than the sum_{j in U(i)} dU(j) of
+// probing U(j) against U(i) at R-MAT scale 20 (measured on the generator).
+//
+// Plan (built once per graph): U in rank space, and L = its transpose as
+// (tail start, tail end) pairs into U -- entry (i, p) of L(j), p the position
+// of j in U(i), stores [p+1, urp[i+1]).  Work items are <= kTcItem in-
+// neighbours of one j; a warp keeps U(j) in a shared-memory hash across the
+// consecutive items of the same j.  Rows with dU(j) > kTcWarpCap use a CTA and
+// a larger table; beyond kTcCtaCap a binary search in global memory.
+// Algorithmic bytes: 4*W2 (streamed tail elements) + 8*nnz(U)
+// (tails) + 4*nnz(U) (hashed rows) + 8*(n+1), W2 = sum_i C(dU(i), 2).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -27,12 +31,15 @@
 
 namespace gbx {
 
-constexpr int kTcWarpCap = 512;         // max dU(i) for the warp kernel
+constexpr int kTcWarpCap = 512;         // max dU(j) for the warp kernel's hash
+constexpr int64_t kTcSpan = 32 * 1024;  // max rank span of U(j) for the warp kernel's bitmap
 constexpr int kTcWarpSlots = 1024;      // hash slots per warp: 256 buckets x 4 (load <= 0.5)
 constexpr int kTcWarpsPerCta = 8;
 constexpr int kTcCtaCap = 16384;        // max dU(i) for the CTA kernel
 constexpr int kTcCtaSlots = 32768;      // 128 KB dynamic shared memory
-constexpr int kTcRowChunk = 8;
+constexpr int kTcRowChunk = 8;            // work items per atomic grab
+constexpr int64_t kTcItem = 64;           // in-neighbours (tails) per work item
+constexpr int64_t kTcCtaItem = 1024;      // ... per CTA work item (heavy middle vertices)
 constexpr unsigned kFullMask = 0xffffffffu;
 
 // Shared-memory hash set of U(i): buckets of 4 int32 slots (one 16-byte load
@@ -69,24 +76,87 @@ __device__ __forceinline__ bool tc_lookup(const int* table, int log_slots, int32
   }
 }
 
-// Stream the concatenation of U(j) for j in U(i)[jb, je) over a warp group,
-// probing every element in the table.  Each round takes 32 j's, prefix-sums
-// their lengths and spreads the elements over the lanes (32-bit offsets:
-// nnz(U) < 2^31 is checked by tc_prepare).
-template <int kWarps>
-__device__ __forceinline__ unsigned long long tc_stream_row(
-    const int64_t* __restrict__ urp, const int32_t* __restrict__ ucol, int jb, int je,
-    const int* table, int log_slots, int lane, int warp_in_group, int* s_incl, int* s_sx) {
-  unsigned long long cnt = 0;
-  // each warp of the group takes every kWarps-th block of 32 j's
-  for (int base = jb + 32 * warp_in_group; base < je; base += 32 * kWarps) {
-    const int p = base + lane;
-    int s = 0, len = 0;
-    if (p < je) {
-      const int32_t j = __ldg(ucol + p);
-      s = static_cast<int>(__ldg(urp + j));
-      len = static_cast<int>(__ldg(urp + j + 1)) - s;
+// The probed set U(j) in shared memory: a bitmap over [base, base + span)
+// when U(j)'s rank span is at most kTcSpan (97% of the probe work at R-MAT
+// scale 20: in rank space the neighbours of a high-rank vertex are close),
+// else the bucketed hash.
+struct TcSet {
+  const int* mem;
+  int log_slots;
+  int32_t base;
+  uint32_t span;  // 0: hash
+  __device__ __forceinline__ bool has(int32_t k) const {
+    if (span) {
+      const uint32_t o = static_cast<uint32_t>(k - base);
+      return o < span && ((static_cast<uint32_t>(mem[o >> 5]) >> (o & 31)) & 1u);
     }
+    return tc_lookup(mem, log_slots, k);
+  }
+};
+
+// Build the set for U(j) = ucol[b, e) with `nthreads` cooperating threads
+// (index t); the caller synchronises before and after.
+__device__ __forceinline__ TcSet tc_build(int* mem, const int32_t* __restrict__ ucol, int64_t b,
+                                          int64_t e, int t, int nthreads, bool clear_only) {
+  TcSet S;
+  S.mem = mem;
+  const int64_t du = e - b;
+  const int32_t lo = __ldg(ucol + b), hi = __ldg(ucol + e - 1);
+  const int64_t span = static_cast<int64_t>(hi) - lo + 1;
+  if (span <= kTcSpan) {
+    S.span = static_cast<uint32_t>(span);
+    S.base = lo;
+    S.log_slots = 0;
+    if (clear_only) {
+      for (int w = t; w < (span + 31) / 32; w += nthreads) mem[w] = 0;
+    } else {
+      for (int64_t q = b + t; q < e; q += nthreads) {
+        const uint32_t o = static_cast<uint32_t>(__ldg(ucol + q) - lo);
+        atomicOr(&mem[o >> 5], 1 << (o & 31));
+      }
+    }
+  } else {
+    S.span = 0;
+    S.base = 0;
+    int ls = 5;
+    while ((1 << ls) < 2 * du) ++ls;
+    S.log_slots = ls;
+    if (clear_only) {
+      for (int w = t; w < (1 << ls); w += nthreads) mem[w] = -1;
+    } else {
+      for (int64_t q = b + t; q < e; q += nthreads) tc_insert(mem, ls, __ldg(ucol + q));
+    }
+  }
+  return S;
+}
+
+// Stream the tails L(j)[qb, qe) over a warp group, probing every element in
+// the set.  Each round takes 32 tails: tails of >= 32 elements are walked by
+// the whole warp one at a time (coalesced), shorter ones are concatenated and
+// spread over the lanes (owner of an element by binary search in shared
+// memory over the prefix sums).
+template <int kWarps>
+__device__ __forceinline__ unsigned long long tc_stream_tails(
+    const int2* __restrict__ tails, const int32_t* __restrict__ ucol, int qb, int qe,
+    const TcSet& S, int lane, int warp_in_group, int* s_incl, int* s_sx) {
+  unsigned long long cnt = 0;
+  for (int base = qb + 32 * warp_in_group; base < qe; base += 32 * kWarps) {
+    const int q = base + lane;
+    int s = 0, len = 0;
+    if (q < qe) {
+      const int2 t = __ldg(tails + q);
+      s = t.x;
+      len = t.y - t.x;
+    }
+    unsigned longs = __ballot_sync(kFullMask, len >= 32);
+    while (longs) {
+      const int src = __ffs(longs) - 1;
+      longs &= longs - 1;
+      const int ls = __shfl_sync(kFullMask, s, src);
+      const int ll = __shfl_sync(kFullMask, len, src);
+      for (int e = lane; e < ll; e += 32) cnt += S.has(__ldg(ucol + ls + e)) ? 1ull : 0ull;
+    }
+    if (len >= 32) len = 0;
     int incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -94,7 +164,6 @@ __device__ __forceinline__ unsigned long long tc_stream_row(
       if (lane >= o) incl += t;
     }
     const int total = __shfl_sync(kFullMask, incl, 31);
-    // element e of lane l's list is ucol[sx[l] + e]; owners found in shared memory
     s_incl[lane] = incl;
     s_sx[lane] = s - (incl - len);
     __syncwarp();
@@ -103,7 +172,7 @@ __device__ __forceinline__ unsigned long long tc_stream_row(
 #pragma unroll
       for (int step = 16; step > 0; step >>= 1)
         if (s_incl[lo + step - 1] <= e) lo += step;
-      cnt += tc_lookup(table, log_slots, __ldg(ucol + s_sx[lo] + e)) ? 1ull : 0ull;
+      cnt += S.has(__ldg(ucol + s_sx[lo] + e)) ? 1ull : 0ull;
     }
     __syncwarp();
   }
@@ -113,8 +182,11 @@ __device__ __forceinline__ unsigned long long tc_stream_row(
 struct TcArgs {
   const int64_t* urp;
   const int32_t* ucol;
-  int64_t row_begin, row_end;
-  unsigned* next_row;
+  const int64_t* lrp;
+  const int2* tails;
+  const int64_t* items;  // j << 32 | chunk
+  int64_t item_begin, item_end;
+  unsigned* next_item;
   unsigned long long* count;
 };
 
@@ -125,29 +197,33 @@ __global__ void __launch_bounds__(32 * kTcWarpsPerCta) k_tc_warp(TcArgs a) {
   const int wid = threadIdx.x >> 5;
   int* table = tables[wid];
   unsigned long long cnt = 0;
-  const int64_t nrows = a.row_end - a.row_begin;
+  const int64_t nitems = a.item_end - a.item_begin;
+  int64_t cur = -1;
+  TcSet S{};
   for (;;) {
     unsigned chunk = 0;
-    if (lane == 0) chunk = atomicAdd(a.next_row, static_cast<unsigned>(kTcRowChunk));
+    if (lane == 0) chunk = atomicAdd(a.next_item, static_cast<unsigned>(kTcRowChunk));
     chunk = __shfl_sync(kFullMask, chunk, 0);
-    if (static_cast<int64_t>(chunk) >= nrows) break;
+    if (static_cast<int64_t>(chunk) >= nitems) break;
     const int64_t cend = static_cast<int64_t>(chunk) + kTcRowChunk;
-    const int64_t rend = cend < nrows ? cend : nrows;
+    const int64_t rend = cend < nitems ? cend : nitems;
     for (int64_t r = chunk; r < rend; ++r) {
-      const int64_t i = a.row_begin + r;
-      const int64_t b = __ldg(a.urp + i), e = __ldg(a.urp + i + 1);
-      const int64_t du = e - b;
-      if (du < 2 || du > kTcWarpCap) continue;
-      int log_slots = 5;
-      while ((1 << log_slots) < 2 * du) ++log_slots;
-      const int slots = 1 << log_slots;
-      for (int t = lane; t < slots; t += 32) table[t] = -1;
-      __syncwarp();
-      for (int64_t q = b + lane; q < e; q += 32) tc_insert(table, log_slots, __ldg(a.ucol + q));
-      __syncwarp();
-      cnt += tc_stream_row<1>(a.urp, a.ucol, static_cast<int>(b), static_cast<int>(e), table,
-                              log_slots, lane, 0, owners[wid], owners[wid] + 32);
-      __syncwarp();
+      const int64_t it = __ldg(a.items + a.item_begin + r);
+      const int64_t j = it >> 32;
+      const int64_t c = it & 0xffffffff;
+      const int64_t lb = __ldg(a.lrp + j), le = __ldg(a.lrp + j + 1);
+      const int qb = static_cast<int>(lb + c * kTcItem);
+      const int qe = static_cast<int>(min(le, lb + (c + 1) * kTcItem));
+      if (j != cur) {  // U(j) into the set (kept for the next items of j)
+        const int64_t b = __ldg(a.urp + j), e = __ldg(a.urp + j + 1);
+        __syncwarp();
+        tc_build(table, a.ucol, b, e, lane, 32, true);
+        __syncwarp();
+        S = tc_build(table, a.ucol, b, e, lane, 32, false);
+        __syncwarp();
+        cur = j;
+      }
+      cnt += tc_stream_tails<1>(a.tails, a.ucol, qb, qe, S, lane, 0, owners[wid], owners[wid] + 32);
     }
   }
 #pragma unroll
@@ -155,47 +231,60 @@ __global__ void __launch_bounds__(32 * kTcWarpsPerCta) k_tc_warp(TcArgs a) {
   if (lane == 0 && cnt) atomicAdd(a.count, cnt);
 }
 
-// one CTA per heavy row (kTcWarpCap < dU(i) <= kTcCtaCap)
+// heavy middle vertices (kTcWarpCap < dU(j) <= kTcCtaCap): CTA work items of
+// <= kTcCtaItem in-neighbours; a CTA keeps U(j) hashed across consecutive items
 __global__ void __launch_bounds__(512) k_tc_cta(const int64_t* urp, const int32_t* ucol,
-                                                const int32_t* rows, int64_t nrows,
-                                                unsigned long long* count) {
+                                                const int64_t* lrp, const int2* tails,
+                                                const int64_t* items, int64_t nitems,
+                                                unsigned* next_item, unsigned long long* count) {
   extern __shared__ __align__(16) int table[];
   __shared__ int owners[16][64];
+  __shared__ unsigned s_item;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   constexpr int kW = 16;
   unsigned long long cnt = 0;
-  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
-    const int64_t i = rows[r];
-    const int64_t b = urp[i], e = urp[i + 1];
-    const int64_t du = e - b;
-    int log_slots = 5;
-    while ((1 << log_slots) < 2 * du) ++log_slots;
-    const int slots = 1 << log_slots;
-    for (int t = threadIdx.x; t < slots; t += blockDim.x) table[t] = -1;
+  int64_t cur = -1;
+  TcSet S{};
+  for (;;) {
     __syncthreads();
-    for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) tc_insert(table, log_slots, ucol[q]);
+    if (threadIdx.x == 0) s_item = atomicAdd(next_item, 1u);
     __syncthreads();
-    cnt += tc_stream_row<kW>(urp, ucol, static_cast<int>(b), static_cast<int>(e), table,
-                             log_slots, lane, wid, owners[wid], owners[wid] + 32);
-    __syncthreads();
+    const int64_t r = s_item;
+    if (r >= nitems) break;
+    const int64_t it = items[r];
+    const int64_t j = it >> 32, c = it & 0xffffffff;
+    if (j != cur) {
+      const int64_t b = urp[j], e = urp[j + 1];
+      tc_build(table, ucol, b, e, threadIdx.x, blockDim.x, true);
+      __syncthreads();
+      S = tc_build(table, ucol, b, e, threadIdx.x, blockDim.x, false);
+      __syncthreads();
+      cur = j;
+    }
+    const int64_t lb = lrp[j], le = lrp[j + 1];
+    const int qb = static_cast<int>(lb + c * kTcCtaItem);
+    const int qe = static_cast<int>(min(le, lb + (c + 1) * kTcCtaItem));
+    cnt += tc_stream_tails<kW>(tails, ucol, qb, qe, S, lane, wid, owners[wid], owners[wid] + 32);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFullMask, cnt, o);
   if (lane == 0 && cnt) atomicAdd(count, cnt);
 }
 
-// fallback for rows too long for shared memory: binary search in global U(i)
-__global__ void k_tc_global(const int64_t* urp, const int32_t* ucol, const int32_t* rows,
-                            int64_t nrows, unsigned long long* count) {
+// fallback for middle vertices with U(j) too long for shared memory: binary
+// search of every tail element in the global U(j)
+__global__ void k_tc_global(const int64_t* urp, const int32_t* ucol, const int64_t* lrp,
+                            const int2* tails, const int32_t* rows, int64_t nrows,
+                            unsigned long long* count) {
   unsigned long long cnt = 0;
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
-    const int64_t i = rows[r];
-    const int64_t b = urp[i], e = urp[i + 1];
-    for (int64_t p = b; p < e; ++p) {
-      const int32_t j = ucol[p];
-      for (int64_t q = urp[j] + threadIdx.x; q < urp[j + 1]; q += blockDim.x) {
-        const int32_t k = ucol[q];
+    const int64_t j = rows[r];
+    const int64_t b = urp[j], e = urp[j + 1];
+    for (int64_t q = lrp[j]; q < lrp[j + 1]; ++q) {
+      const int2 t = tails[q];
+      for (int64_t p = t.x + threadIdx.x; p < t.y; p += blockDim.x) {
+        const int32_t k = ucol[p];
         int64_t lo = b, hi = e;
         while (lo < hi) {
           int64_t mid = (lo + hi) >> 1;
@@ -224,20 +313,69 @@ __global__ void k_upper_keys(const int32_t* rowid, const int32_t* col, const int
                     : (uint64_t(1) << (2 * bits));
 }
 
-__global__ void k_row_work(const int64_t* urp, const int32_t* ucol, int64_t n, int64_t* work) {
+// per middle vertex j: probe work = sum of its in-neighbours' tails + dU(j)
+__global__ void k_row_work(const int64_t* urp, const int64_t* lrp, const int2* tails, int64_t n,
+                           int64_t* work) {
   const int lane = threadIdx.x & 31;
   const int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t i = w; i < n; i += nw) {
+  for (int64_t j = w; j < n; j += nw) {
+    const int64_t du = urp[j + 1] - urp[j];
     int64_t s = 0;
-    for (int64_t p = urp[i] + lane; p < urp[i + 1]; p += 32) {
-      int32_t j = ucol[p];
-      s += urp[j + 1] - urp[j];
-    }
+    if (du > 0)
+      for (int64_t q = lrp[j] + lane; q < lrp[j + 1]; q += 32) s += tails[q].y - tails[q].x;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFullMask, s, o);
-    if (lane == 0) work[i] = s + (urp[i + 1] - urp[i]);
+    if (lane == 0) work[j] = du > 0 ? s + du : 0;
   }
+}
+
+// row id of every U entry (warp per row)
+__global__ void k_u_rows(const int64_t* urp, int64_t n, int32_t* rowu) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = w; i < n; i += nw)
+    for (int64_t p = urp[i] + lane; p < urp[i + 1]; p += 32) rowu[p] = static_cast<int32_t>(i);
+}
+
+// L keys: (j = ucol[p]) << 31 | p
+__global__ void k_l_keys(const int32_t* ucol, int64_t m, uint64_t* keys) {
+  const int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p < m) keys[p] = (static_cast<uint64_t>(ucol[p]) << 31) | static_cast<uint64_t>(p);
+}
+
+// tails[q] = [p + 1, urp[i + 1]) for L entry q = (i, p)
+__global__ void k_l_tails(const int32_t* lcol, const int32_t* rowu, const int64_t* urp, int64_t m,
+                          int2* tails) {
+  const int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (q >= m) return;
+  const int32_t p = lcol[q];
+  tails[q] = make_int2(p + 1, static_cast<int>(urp[rowu[p] + 1]));
+}
+
+// work items per middle vertex j handled by the warp kernel: ceil(|L(j)| / kTcItem)
+// when 1 <= dU(j) <= kTcWarpCap; class[j] = 1 (CTA) / 2 (global) for longer U(j)
+__global__ void k_item_counts(const int64_t* urp, const int32_t* ucol, const int64_t* lrp,
+                              int64_t n, int64_t* cnt, int8_t* cls) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= n) return;
+  const int64_t du = urp[j + 1] - urp[j], nl = lrp[j + 1] - lrp[j];
+  int64_t k = 0;
+  int8_t c = 0;
+  if (du > 0 && nl > 0) {
+    const int64_t span = static_cast<int64_t>(ucol[urp[j + 1] - 1]) - ucol[urp[j]] + 1;
+    if (span <= kTcSpan || du <= kTcWarpCap) k = (nl + kTcItem - 1) / kTcItem;
+    else c = du <= kTcCtaCap ? 1 : 2;
+  }
+  cnt[j] = k;
+  cls[j] = c;
+}
+
+__global__ void k_item_fill(const int64_t* off, int64_t n, int64_t* items) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= n) return;
+  for (int64_t c = 0; c < off[j + 1] - off[j]; ++c) items[off[j] + c] = (j << 32) | c;
 }
 
 void tc_prepare(gbx_graph* g) {
@@ -278,27 +416,90 @@ void tc_prepare(gbx_graph* g) {
     fail(GBX_UNSUPPORTED, "triangle_count: nnz(U) >= 2^31 is not supported (32-bit offsets)");
   csr_from_sorted_keys(s, n, bits, sorted, unnz, P->urp, P->ucol);
   P->nnz = unnz;
+  // L = U' as tails into U, sorted by middle vertex j
+  {
+    DevArray<int32_t> rowu(std::max<int64_t>(unnz, 1)), lcol;
+    uint64_t* lk = k0.p == sorted ? k1.p : k0.p;
+    uint64_t* la = k0.p == sorted ? k0.p : k1.p;
+    if (unnz) {
+      k_u_rows<<<device_sms() * 8, 256, 0, s>>>(P->urp.p, n, rowu.p);
+      k_l_keys<<<ceil_div(unnz, 256), 256, 0, s>>>(P->ucol.p, unnz, lk);
+      GBX_LAUNCHED();
+    }
+    uint64_t* ls = unnz ? sort_keys(s, lk, la, unnz, bits + 31) : lk;
+    csr_from_sorted_keys(s, n, 31, ls, unnz, P->lrp, lcol);
+    P->tails.alloc(std::max<int64_t>(unnz, 1));
+    if (unnz) {
+      k_l_tails<<<ceil_div(unnz, 256), 256, 0, s>>>(lcol.p, rowu.p, P->urp.p, unnz, P->tails.p);
+      GBX_LAUNCHED();
+    }
+  }
+  k0.release();
+  k1.release();
+  // work items (warp kernel) and the CTA / global middle vertices
+  {
+    const int64_t n1 = std::max<int64_t>(n, 1);
+    DevArray<int64_t> cnt(n1);
+    DevArray<int8_t> cls(n1);
+    P->item_off.alloc(n + 1);
+    GBX_CUDA(cudaMemsetAsync(P->item_off.p, 0, sizeof(int64_t), s));
+    if (n) {
+      k_item_counts<<<ceil_div(n, 256), 256, 0, s>>>(P->urp.p, P->ucol.p, P->lrp.p, n, cnt.p, cls.p);
+      GBX_LAUNCHED();
+      size_t tb = 0;
+      GBX_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, cnt.p, P->item_off.p + 1, n, s));
+      DevArray<uint8_t> t(tb + 1);
+      GBX_CUDA(cub::DeviceScan::InclusiveSum(t.p, tb, cnt.p, P->item_off.p + 1, n, s));
+    }
+    int64_t nitems = 0;
+    GBX_CUDA(cudaMemcpyAsync(&nitems, P->item_off.p + n, 8, cudaMemcpyDeviceToHost, s));
+    std::vector<int8_t> hc(n);
+    if (n) GBX_CUDA(cudaMemcpyAsync(hc.data(), cls.p, n, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+    P->nitems = nitems;
+    P->items.alloc(std::max<int64_t>(nitems, 1));
+    if (n) {
+      k_item_fill<<<ceil_div(n, 256), 256, 0, s>>>(P->item_off.p, n, P->items.p);
+      GBX_LAUNCHED();
+    }
+    for (int64_t j = 0; j < n; ++j) {
+      if (hc[j] == 1) P->heavy_h.push_back(static_cast<int32_t>(j));
+      else if (hc[j] == 2) P->huge_h.push_back(static_cast<int32_t>(j));
+    }
+    // heavy middle vertices: CTA items of kTcCtaItem in-neighbours (ascending j)
+    P->heavy_item_off_h.assign(1, 0);
+    std::vector<int64_t> hitems;
+    for (int32_t j : P->heavy_h) {
+      int64_t l[2];
+      GBX_CUDA(cudaMemcpyAsync(l, P->lrp.p + j, 16, cudaMemcpyDeviceToHost, s));
+      GBX_CUDA(cudaStreamSynchronize(s));
+      const int64_t k = (l[1] - l[0] + kTcCtaItem - 1) / kTcCtaItem;
+      for (int64_t c = 0; c < k; ++c) hitems.push_back((static_cast<int64_t>(j) << 32) | c);
+      P->heavy_item_off_h.push_back(static_cast<int64_t>(hitems.size()));
+    }
+    P->heavy_items.alloc(std::max<size_t>(hitems.size(), 1));
+    if (!hitems.empty())
+      GBX_CUDA(cudaMemcpyAsync(P->heavy_items.p, hitems.data(), hitems.size() * 8,
+                               cudaMemcpyHostToDevice, s));
+    P->huge.alloc(std::max<size_t>(P->huge_h.size(), 1));
+    if (!P->huge_h.empty())
+      GBX_CUDA(cudaMemcpyAsync(P->huge.p, P->huge_h.data(), P->huge_h.size() * 4,
+                               cudaMemcpyHostToDevice, s));
+  }
   P->count.alloc(1);
-  P->next_row.alloc(1);
+  P->next_row.alloc(2);
   GBX_CUDA(cudaStreamSynchronize(s));
   g->tc = std::move(P);
 }
 
-static void tc_heavy_rows(gbx_graph* g, int64_t rb, int64_t re, std::vector<int32_t>& heavy,
-                          std::vector<int32_t>& huge) {
-  TcPlan& P = *g->tc;
-  std::vector<int64_t> rp(re - rb + 1);
-  if (re > rb)
-    GBX_CUDA(cudaMemcpyAsync(rp.data(), P.urp.p + rb, (re - rb + 1) * 8, cudaMemcpyDeviceToHost,
-                             g->stream));
-  GBX_CUDA(cudaStreamSynchronize(g->stream));
-  for (int64_t i = rb; i < re; ++i) {
-    int64_t du = rp[i - rb + 1] - rp[i - rb];
-    if (du > kTcCtaCap) huge.push_back(static_cast<int32_t>(i));
-    else if (du > kTcWarpCap) heavy.push_back(static_cast<int32_t>(i));
-  }
+// [lo, hi) of a sorted id list restricted to [rb, re)
+static void id_range(const std::vector<int32_t>& v, int64_t rb, int64_t re, size_t& lo,
+                     size_t& hi) {
+  lo = std::lower_bound(v.begin(), v.end(), rb) - v.begin();
+  hi = std::lower_bound(v.begin(), v.end(), re) - v.begin();
 }
 
+// triangles whose middle vertex (rank space) lies in [rb, re)
 uint64_t tc_run(gbx_graph* g, int64_t rb, int64_t re) {
   tc_prepare(g);
   TcPlan& P = *g->tc;
@@ -307,41 +508,48 @@ uint64_t tc_run(gbx_graph* g, int64_t rb, int64_t re) {
   if (rb < 0) rb = 0;
   g->stats = gbx_stats{};
   if (re <= rb) return 0;
+  int64_t ib = 0, ie = P.nitems;
+  if (rb > 0 || re < P.n) {
+    GBX_CUDA(cudaMemcpyAsync(&ib, P.item_off.p + rb, 8, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaMemcpyAsync(&ie, P.item_off.p + re, 8, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+  }
   GBX_CUDA(cudaMemsetAsync(P.count.p, 0, sizeof(unsigned long long), s));
   GBX_CUDA(cudaMemsetAsync(P.next_row.p, 0, sizeof(unsigned), s));
-  TcArgs a{P.urp.p, P.ucol.p, rb, re, P.next_row.p, P.count.p};
-  int per_sm = 0;
-  GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_warp, 32 * kTcWarpsPerCta, 0));
-  const int grid = device_sms() * std::max(per_sm, 1);
-  k_tc_warp<<<grid, 32 * kTcWarpsPerCta, 0, s>>>(a);
-  GBX_LAUNCHED();
-  int launches = 1;
-  std::vector<int32_t> heavy, huge;
-  tc_heavy_rows(g, rb, re, heavy, huge);
-  int32_t* drows = nullptr;
-  const size_t nr = std::max(heavy.size(), huge.size());
-  if (nr) {
-    GBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&drows), nr * 4, s));
+  int launches = 0;
+  if (ie > ib) {
+    TcArgs a{P.urp.p, P.ucol.p, P.lrp.p, P.tails.p, P.items.p, ib, ie, P.next_row.p, P.count.p};
+    static int per_sm = 0;
+    if (!per_sm)
+      GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_warp,
+                                                             32 * kTcWarpsPerCta, 0));
+    const int grid = device_sms() * std::max(per_sm, 1);
+    k_tc_warp<<<grid, 32 * kTcWarpsPerCta, 0, s>>>(a);
+    GBX_LAUNCHED();
+    ++launches;
   }
-  if (!heavy.empty()) {
-    GBX_CUDA(cudaMemcpyAsync(drows, heavy.data(), heavy.size() * 4, cudaMemcpyHostToDevice, s));
+  size_t lo, hi;
+  id_range(P.heavy_h, rb, re, lo, hi);
+  const int64_t hib = P.heavy_item_off_h[lo], hie = P.heavy_item_off_h[hi];
+  if (hie > hib) {
     const size_t smem = kTcCtaSlots * sizeof(int);
     GBX_CUDA(cudaFuncSetAttribute(k_tc_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-    k_tc_cta<<<std::min<int64_t>(heavy.size(), 4 * device_sms()), 512, smem, s>>>(
-        P.urp.p, P.ucol.p, drows, static_cast<int64_t>(heavy.size()), P.count.p);
+    GBX_CUDA(cudaMemsetAsync(P.next_row.p + 1, 0, sizeof(unsigned), s));
+    k_tc_cta<<<std::min<int64_t>(hie - hib, device_sms()), 512, smem, s>>>(
+        P.urp.p, P.ucol.p, P.lrp.p, P.tails.p, P.heavy_items.p + hib, hie - hib,
+        P.next_row.p + 1, P.count.p);
     GBX_LAUNCHED();
     ++launches;
   }
-  if (!huge.empty()) {
-    GBX_CUDA(cudaStreamSynchronize(s));
-    GBX_CUDA(cudaMemcpyAsync(drows, huge.data(), huge.size() * 4, cudaMemcpyHostToDevice, s));
-    k_tc_global<<<std::min<int64_t>(huge.size(), 4 * device_sms()), 256, 0, s>>>(
-        P.urp.p, P.ucol.p, drows, static_cast<int64_t>(huge.size()), P.count.p);
+  id_range(P.huge_h, rb, re, lo, hi);
+  if (hi > lo) {
+    k_tc_global<<<std::min<int64_t>(hi - lo, 4 * device_sms()), 256, 0, s>>>(
+        P.urp.p, P.ucol.p, P.lrp.p, P.tails.p, P.huge.p + lo, static_cast<int64_t>(hi - lo),
+        P.count.p);
     GBX_LAUNCHED();
     ++launches;
   }
-  if (drows) cudaFreeAsync(drows, s);
   unsigned long long h = 0;
   GBX_CUDA(cudaMemcpyAsync(&h, P.count.p, sizeof h, cudaMemcpyDeviceToHost, s));
   GBX_CUDA(cudaStreamSynchronize(s));
@@ -351,7 +559,7 @@ uint64_t tc_run(gbx_graph* g, int64_t rb, int64_t re) {
   return h;
 }
 
-// Wedge-balanced contiguous split of the oriented rows (multi-GPU TC, §8e).
+// Work-balanced contiguous split of the middle vertices (multi-GPU TC, §8e).
 void tc_partition(gbx_graph* g, int parts, int64_t* bounds) {
   if (parts < 1) fail(GBX_INVALID_VALUE, "tc_partition: parts must be >= 1");
   tc_prepare(g);
@@ -360,7 +568,7 @@ void tc_partition(gbx_graph* g, int parts, int64_t* bounds) {
   const int64_t n = P.n;
   DevArray<int64_t> work(std::max<int64_t>(n, 1));
   if (n) {
-    k_row_work<<<device_sms() * 8, 256, 0, s>>>(P.urp.p, P.ucol.p, n, work.p);
+    k_row_work<<<device_sms() * 8, 256, 0, s>>>(P.urp.p, P.lrp.p, P.tails.p, n, work.p);
     GBX_LAUNCHED();
   }
   std::vector<int64_t> w(n);
