@@ -39,6 +39,14 @@ constexpr int kTcCtaCap = 16384;        // max dU(i) for the CTA kernel
 constexpr int kTcCtaSlots = 32768;      // 128 KB dynamic shared memory
 constexpr int kTcRowChunk = 8;            // work items per atomic grab
 constexpr int64_t kTcItem = 64;           // in-neighbours (tails) per work item
+#ifndef GBX_TC_LONG
+#define GBX_TC_LONG 32
+#endif
+#ifndef GBX_TC_UNROLL
+#define GBX_TC_UNROLL 4
+#endif
+constexpr int kTcLong = GBX_TC_LONG;      // tails this long are walked by the whole warp
+constexpr int kTcUnroll = GBX_TC_UNROLL;  // loads in flight per lane on those walks
 constexpr int64_t kTcCtaItem = 1024;      // ... per CTA work item (heavy middle vertices)
 constexpr unsigned kFullMask = 0xffffffffu;
 
@@ -148,15 +156,24 @@ __device__ __forceinline__ unsigned long long tc_stream_tails(
       s = t.x;
       len = t.y - t.x;
     }
-    unsigned longs = __ballot_sync(kFullMask, len >= 32);
+    unsigned longs = __ballot_sync(kFullMask, len >= kTcLong);
     while (longs) {
       const int src = __ffs(longs) - 1;
       longs &= longs - 1;
       const int ls = __shfl_sync(kFullMask, s, src);
       const int ll = __shfl_sync(kFullMask, len, src);
-      for (int e = lane; e < ll; e += 32) cnt += S.has(__ldg(ucol + ls + e)) ? 1ull : 0ull;
+      // kTcUnroll independent loads in flight per lane
+      for (int e = lane; e < ll; e += 32 * kTcUnroll) {
+        int32_t k[kTcUnroll];
+#pragma unroll
+        for (int u = 0; u < kTcUnroll; ++u)
+          k[u] = e + 32 * u < ll ? __ldg(ucol + ls + e + 32 * u) : 0;
+#pragma unroll
+        for (int u = 0; u < kTcUnroll; ++u)
+          if (e + 32 * u < ll && S.has(k[u])) ++cnt;
+      }
     }
-    if (len >= 32) len = 0;
+    if (len >= kTcLong) len = 0;
     int incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
