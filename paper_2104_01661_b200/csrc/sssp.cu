@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -323,34 +324,52 @@ struct SsspBArgs {
   int* ctl;            // [0] |Q| [1] |Qnext| [4] near iterations [5] buckets
   unsigned long long* relax;
   int trace;
+  unsigned long long* tlog;  // optional: [2i] %globaltimer, [2i+1] kind<<32 | size (debug)
+  int tlog_cap;
 };
 
-// stages (vertex, bucket) pushes; one atomic per distinct bucket per 32 entries
+__device__ __forceinline__ unsigned long long sssp_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// stages (vertex, bucket) pushes; a flush counts the staged entries per
+// bucket in shared memory and reserves each bucket's run with ONE global
+// atomic (the nb bucket counters are the hottest addresses of the kernel:
+// one atomic per 32 entries and bucket serialised in L2)
 template <int CAP>
 struct BucketQueue {
   int32_t* bv;
-  int32_t* bb;
+  int32_t* bb;   // bucket, then bucket | slot << 8 during a flush
+  int* scnt;     // [64] per-bucket counts / bases (warp-private)
   int n;
-  __device__ __forceinline__ void flush(int32_t* bq, int64_t cap, int* bcnt) {
+  __device__ __forceinline__ void flush(int32_t* bq, int64_t cap, int* bcnt, int nb) {
     __syncwarp();
+    if (n == 0) return;
     const int lane = threadIdx.x & 31;
-    for (int i0 = 0; i0 < n; i0 += 32) {
-      const int i = i0 + lane;
-      const bool ok = i < n;
-      const int32_t v = ok ? bv[i] : 0;
-      const int b = ok ? bb[i] : -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, b);
-      const int leader = __ffs(peers) - 1;
-      int base = 0;
-      if (ok && lane == leader) base = atomicAdd(&bcnt[b], __popc(peers));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (ok) bq[static_cast<int64_t>(b) * cap + base + __popc(peers & ((1u << lane) - 1))] = v;
+    for (int t = lane; t < nb; t += 32) scnt[t] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const int b = bb[i];
+      bb[i] = b | (atomicAdd(&scnt[b], 1) << 8);
+    }
+    __syncwarp();
+    for (int t = lane; t < nb; t += 32) {
+      const int c = scnt[t];
+      scnt[t] = c ? atomicAdd(&bcnt[t], c) : 0;
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const int x = bb[i];
+      const int b = x & 0xff;
+      bq[static_cast<int64_t>(b) * cap + scnt[b] + (x >> 8)] = bv[i];
     }
     __syncwarp();
     n = 0;
   }
   __device__ __forceinline__ void push(bool has, int32_t v, int b, int32_t* bq, int64_t cap,
-                                       int* bcnt) {
+                                       int* bcnt, int nb) {
     const unsigned m = __ballot_sync(0xffffffffu, has);
     if (!m) return;
     const int lane = threadIdx.x & 31;
@@ -360,7 +379,7 @@ struct BucketQueue {
       bb[pos] = b;
     }
     n += __popc(m);
-    if (n > CAP - 32) flush(bq, cap, bcnt);
+    if (n > CAP - 32) flush(bq, cap, bcnt, nb);
   }
 };
 
@@ -370,36 +389,59 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
   __shared__ int32_t s_near[kSsspWarps][kSsspBuf];
   __shared__ int32_t s_bv[kSsspWarps][kSsspBuf];
   __shared__ int32_t s_bb[kSsspWarps][kSsspBuf];
+  __shared__ int s_bcnt[kSsspWarps][64];
   WarpQueue<int32_t, kSsspBuf> nearq;
   BucketQueue<kSsspBuf> bucq;
   nearq.buf = s_near[threadIdx.x >> 5];
   bucq.bv = s_bv[threadIdx.x >> 5];
   bucq.bb = s_bb[threadIdx.x >> 5];
+  bucq.scnt = s_bcnt[threadIdx.x >> 5];
   bucq.n = 0;
   const int lane = threadIdx.x & 31;
   const int g4 = lane >> 2, s4 = lane & 3;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int nbm = a.nb - 1;
-  int64_t k = 0;      // current bucket (absolute index)
-  int qp = 1, pq = 0;
+  int64_t k = 0;  // current bucket (absolute index)
+  // near iteration t pops queue t&1 (count ctl[t%3], dedup bits qbits[t&1])
+  // and pushes queue (t+1)&1 (count ctl[(t+1)%3]); ctl[(t+2)%3] -- read by
+  // every thread before the previous barrier -- is zeroed for iteration t+1,
+  // so ONE grid barrier per near iteration suffices
+  int t = 0;
+  int zero_bucket = -1;  // bucket emptied by the last jump, cleared lazily
   const bool trace = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool tl = a.tlog && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  int tn = 0;
   for (int guard = 0;; ++guard) {
     if (guard > (1 << 28)) break;
     // ---------------- near iterations inside bucket k
     for (;;) {
-      const int nq = *(volatile int*)&a.ctl[0];
-      if (trace) printf("near k=%lld nq=%d pq=%d qp=%d\n", (long long)k, nq, pq, qp);
+      const int nq = *(volatile int*)&a.ctl[t % 3];
+      if (trace) printf("near k=%lld nq=%d t=%d\n", (long long)k, nq, t);
+      if (tl && tn < a.tlog_cap) {
+        a.tlog[2 * tn] = sssp_gtimer();
+        a.tlog[2 * tn + 1] = (static_cast<unsigned long long>(k) << 32) | static_cast<unsigned>(nq);
+        ++tn;
+      }
       if (nq == 0) break;
-      const int32_t* qc = pq ? a.q1 : a.q0;
-      int32_t* qn = pq ? a.q0 : a.q1;
+      if (leader) {
+        a.ctl[(t + 2) % 3] = 0;
+        a.ctl[4] += 1;
+        if (zero_bucket >= 0) a.bcnt[zero_bucket] = 0;
+      }
+      zero_bucket = -1;
+      const int32_t* qc = (t & 1) ? a.q1 : a.q0;
+      int32_t* qn = (t & 1) ? a.q0 : a.q1;
+      uint32_t* pop_bits = a.qbits[t & 1];
+      uint32_t* push_bits = a.qbits[(t + 1) & 1];
       unsigned long long nrel = 0;
-      nearq.reset(qn, &a.ctl[1]);
+      nearq.reset(qn, &a.ctl[(t + 1) % 3]);
       for (int64_t base = gwarp * 8; base < nq; base += nwarps * 8) {
         const int64_t qi = base + g4;
         bool active = qi < nq;
         const int32_t u = active ? qc[qi] : 0;
-        if (active && s4 == 0) atomicAnd(&a.qbits[qp ^ 1][u >> 5], ~(1u << (u & 31)));
+        if (active && s4 == 0) atomicAnd(&pop_bits[u >> 5], ~(1u << (u & 31)));
         int64_t p = active ? a.rp[u] : 0;
         const int64_t e = active ? a.rp[u + 1] : 0;
         const D du = active ? *(volatile D*)&a.dist[u] : D(0);
@@ -408,39 +450,39 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
           D nd[4];
           bool ok[4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int64_t q = p + s4 + 4 * t;
-            ok[t] = active && q < e;
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int64_t q = p + s4 + 4 * q4;
+            ok[q4] = active && q < e;
             W w = W(0);
-            v[t] = 0;
-            if (ok[t]) a.edges.get(q, v[t], w);
-            nd[t] = DistTraits<D>::add(du, w);
+            v[q4] = 0;
+            if (ok[q4]) a.edges.get(q, v[q4], w);
+            nd[q4] = DistTraits<D>::add(du, w);
           }
           D cur[4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) cur[t] = ok[t] ? *(volatile D*)&a.dist[v[t]] : D(0);
+          for (int q4 = 0; q4 < 4; ++q4) cur[q4] = ok[q4] ? *(volatile D*)&a.dist[v[q4]] : D(0);
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
+          for (int q4 = 0; q4 < 4; ++q4) {
             bool near_push = false, buck_push = false;
             int bidx = 0;
-            if (ok[t]) {
+            if (ok[q4]) {
               ++nrel;
-              if (nd[t] < cur[t]) {
-                const D old = atomicMin(&a.dist[v[t]], nd[t]);
-                if (nd[t] < old) {
-                  const uint32_t bit = 1u << (v[t] & 31);
-                  const int64_t kb = bucket_of<D>(nd[t], a.delta);
-                  if (kb <= k) {
-                    near_push = !(atomicOr(&a.qbits[qp][v[t] >> 5], bit) & bit);
-                  } else {
-                    bidx = static_cast<int>(kb & nbm);
-                    buck_push = !(atomicOr(&a.bbits[bidx * a.words + (v[t] >> 5)], bit) & bit);
-                  }
+              if (nd[q4] < cur[q4]) {
+                // fire-and-forget min: a push whose value lost the race is a
+                // harmless extra relaxation (stale bucket entries are skipped)
+                atomicMin(&a.dist[v[q4]], nd[q4]);
+                const uint32_t bit = 1u << (v[q4] & 31);
+                const int64_t kb = bucket_of<D>(nd[q4], a.delta);
+                if (kb <= k) {
+                  near_push = !(atomicOr(&push_bits[v[q4] >> 5], bit) & bit);
+                } else {
+                  bidx = static_cast<int>(kb & nbm);
+                  buck_push = !(atomicOr(&a.bbits[bidx * a.words + (v[q4] >> 5)], bit) & bit);
                 }
               }
             }
-            nearq.push(near_push, v[t]);
-            bucq.push(buck_push, v[t], bidx, a.bq, a.cap, a.bcnt);
+            nearq.push(near_push, v[q4]);
+            bucq.push(buck_push, v[q4], bidx, a.bq, a.cap, a.bcnt, a.nb);
           }
           if (active) {
             p += 16;
@@ -449,37 +491,47 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
         }
       }
       nearq.flush();
-      bucq.flush(a.bq, a.cap, a.bcnt);
+      bucq.flush(a.bq, a.cap, a.bcnt, a.nb);
       if (nrel) atomicAdd(a.relax, nrel);
       grid.sync();
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.ctl[0] = a.ctl[1];
-        a.ctl[1] = 0;
-        a.ctl[4] += 1;
-      }
-      pq ^= 1;
-      qp ^= 1;
-      grid.sync();
+      ++t;
     }
     // ---------------- jump to the next non-empty bucket (at most nb-1 ahead):
     // one thread decides, everyone reads the decision after a grid barrier
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (leader) {
+      if (zero_bucket >= 0) a.bcnt[zero_bucket] = 0;  // the near loop ran no iteration
       int jj = 1;
       for (; jj < a.nb; ++jj)
         if (*(volatile int*)&a.bcnt[(k + jj) & nbm] > 0) break;
       a.ctl[6] = jj;
       a.ctl[7] = jj < a.nb ? *(volatile int*)&a.bcnt[(k + jj) & nbm] : 0;
+      a.ctl[5] += 1;
     }
+    zero_bucket = -1;
     grid.sync();
     const int j = *(volatile int*)&a.ctl[6];
     if (trace) printf("jump k=%lld j=%d\n", (long long)k, j);
-    if (j >= a.nb) break;
+    if (tl && tn < a.tlog_cap) {
+      a.tlog[2 * tn] = sssp_gtimer();
+      a.tlog[2 * tn + 1] = (1ull << 63) | static_cast<unsigned>(*(volatile int*)&a.ctl[7]);
+      ++tn;
+    }
+    if (j >= a.nb) {
+      if (tl && tn < a.tlog_cap) {
+        a.tlog[2 * tn] = sssp_gtimer();
+        a.tlog[2 * tn + 1] = 3ull << 62;
+        ++tn;
+      }
+      break;
+    }
     k += j;
     const int b = static_cast<int>(k & nbm);
     const int cnt = *(volatile int*)&a.ctl[7];
     const int32_t* src = a.bq + static_cast<int64_t>(b) * a.cap;
-    int32_t* qn = pq ? a.q1 : a.q0;  // current (empty) near queue
-    nearq.reset(qn, &a.ctl[0]);
+    // the near queue iteration t pops (empty: the loop above ended on it)
+    int32_t* qn = (t & 1) ? a.q1 : a.q0;
+    uint32_t* push_bits = a.qbits[t & 1];
+    nearq.reset(qn, &a.ctl[t % 3]);
     for (int64_t base = gwarp * 32; base < cnt; base += nwarps * 32) {
       const int64_t i = base + lane;
       bool to_near = false;
@@ -490,17 +542,14 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
         atomicAnd(&a.bbits[b * a.words + (v >> 5)], ~bit);
         // stale entries (improved into an earlier bucket since) are skipped
         if (bucket_of<D>(*(volatile D*)&a.dist[v], a.delta) == k)
-          to_near = !(atomicOr(&a.qbits[qp][v >> 5], bit) & bit);
+          to_near = !(atomicOr(&push_bits[v >> 5], bit) & bit);
       }
       nearq.push(to_near, v);
     }
     nearq.flush();
-    grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      a.bcnt[b] = 0;
-      a.ctl[5] += 1;
-    }
-    qp ^= 1;
+    // bcnt[b] is zeroed by the next near iteration's leader: no push can
+    // target bucket b before k moves past it
+    zero_bucket = b;
     grid.sync();
   }
 }
@@ -671,7 +720,13 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, g->device);
     const size_t bytes = static_cast<size_t>(n) * sizeof(D);
     if (max_persist > 0) {
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, max_persist));
+      // the set-aside is a device-wide setting (and costly to change): grow only
+      static size_t set_aside[64] = {0};
+      const size_t want = std::min<size_t>(bytes, max_persist);
+      if (g->device < 64 && set_aside[g->device] < want) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        set_aside[g->device] = want;
+      }
       cudaStreamAttrValue at = {};
       at.accessPolicyWindow.base_ptr = dist;
       at.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, max_persist);
@@ -715,6 +770,14 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     b.ctl = a.ctl;
     b.relax = a.relax;
     b.trace = std::getenv("GBX_SSSP_TRACE") ? 1 : 0;
+    static const bool tlog_on = std::getenv("GBX_SSSP_TLOG") != nullptr;
+    DevArray<unsigned long long> tlog;
+    if (tlog_on) {
+      tlog.alloc(2 * 4096);
+      GBX_CUDA(cudaMemsetAsync(tlog.p, 0, tlog.bytes(), s));
+      b.tlog = tlog.p;
+      b.tlog_cap = 4096;
+    }
     auto fnb = k_sssp_b<D, E, W>;
     int per_sm = 0;
     GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fnb, kSsspThreads, 0));
@@ -723,6 +786,20 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     void* args[] = {&b};
     GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fnb), dim3(grid),
                                          dim3(kSsspThreads), args, 0, s));
+    if (tlog_on) {
+      std::vector<unsigned long long> t(2 * 4096);
+      GBX_CUDA(cudaMemcpyAsync(t.data(), tlog.p, t.size() * 8, cudaMemcpyDeviceToHost, s));
+      GBX_CUDA(cudaStreamSynchronize(s));
+      for (int i = 0; i + 1 < 4096 && t[2 * i + 2]; ++i) {
+        const unsigned long long tag = t[2 * i + 1];
+        const double us = (t[2 * i + 2] - t[2 * i]) / 1e3;
+        if (tag >> 63)
+          std::fprintf(stderr, "sssp jump  cnt=%u %.1fus\n", static_cast<unsigned>(tag), us);
+        else
+          std::fprintf(stderr, "sssp near k=%llu nq=%u %.1fus\n", tag >> 32,
+                       static_cast<unsigned>(tag), us);
+      }
+    }
   } else {
     auto fn = k_sssp<D, E, W>;
     int per_sm = 0;
