@@ -144,6 +144,28 @@ void sort_ids_by_key(cudaStream_t s, const int32_t* key, int64_t n, bool ascendi
                      DevArray<int32_t>& perm);
 // row ids per nonzero (max-scan over row starts)
 void expand_rows(cudaStream_t s, const Csr& A, DevArray<int32_t>& rowid);
+void expand_rows_into(cudaStream_t s, const Csr& A, int32_t* rowid);  // nnz entries
+
+// Stream-ordered temporary from the device pool (freed on the stream when it
+// goes out of scope).
+template <typename T>
+struct Tmp {
+  T* p = nullptr;
+  cudaStream_t s;
+  Tmp(size_t n, cudaStream_t st) : s(st) {
+    if (n) {
+      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), s);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        fail(GBX_OUT_OF_MEMORY, "cudaMallocAsync of " + std::to_string(n * sizeof(T)) +
+                                    " bytes failed");
+      }
+    }
+  }
+  ~Tmp() { if (p) cudaFreeAsync(p, s); }
+  Tmp(const Tmp&) = delete;
+  Tmp& operator=(const Tmp&) = delete;
+};
 void generate_rmat(gbx_graph* g, int scale, int ef, double a, double b, double c,
                    uint64_t seed, int scramble, int kind);
 void generate_er(gbx_graph* g, int logn, int degree, uint64_t seed, int weighted);

@@ -41,7 +41,21 @@ size_t domain_size(int d) {
   fail(GBX_DOMAIN_MISMATCH, "unknown value domain " + std::to_string(d));
 }
 
-Scope::Scope(gbx_graph* g) : lock(g->mu) { GBX_CUDA(cudaSetDevice(g->device)); }
+Scope::Scope(gbx_graph* g) : lock(g->mu) {
+  GBX_CUDA(cudaSetDevice(g->device));
+  // keep freed stream-ordered temporaries cached in the device pool (the default
+  // threshold returns them to the driver at every synchronisation)
+  static bool pooled[64] = {false};
+  if (g->device >= 0 && g->device < 64 && !pooled[g->device]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
+      uint64_t thr = ~uint64_t(0);
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    (void)cudaGetLastError();
+    pooled[g->device] = true;
+  }
+}
 
 void sync(gbx_graph* g) { GBX_CUDA(cudaStreamSynchronize(g->stream)); }
 
@@ -51,26 +65,6 @@ void require_at(const gbx_graph* g, const char* who) {
 void require_rowdeg(const gbx_graph* g, const char* who) {
   if (!g->has_rowdeg) fail(GBX_MISSING_PROPERTY, std::string(who) + " needs G.row_degree");
 }
-
-// Stream-ordered temporary (freed on the stream when it goes out of scope).
-template <typename T>
-struct Tmp {
-  T* p = nullptr;
-  cudaStream_t s;
-  Tmp(size_t n, cudaStream_t st) : s(st) {
-    if (n) {
-      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), s);
-      if (e != cudaSuccess) {
-        (void)cudaGetLastError();
-        fail(GBX_OUT_OF_MEMORY, "cudaMallocAsync of " + std::to_string(n * sizeof(T)) +
-                                    " bytes failed");
-      }
-    }
-  }
-  ~Tmp() { if (p) cudaFreeAsync(p, s); }
-  Tmp(const Tmp&) = delete;
-  Tmp& operator=(const Tmp&) = delete;
-};
 
 int bits_for(int64_t n) {
   int b = 1;
@@ -177,16 +171,20 @@ struct MaxOp {
   __device__ __forceinline__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
 };
 
-void expand_rows(cudaStream_t s, const Csr& A, DevArray<int32_t>& rowid) {
-  rowid.alloc(std::max<int64_t>(A.nnz, 1));
+void expand_rows_into(cudaStream_t s, const Csr& A, int32_t* rowid) {
   if (A.nnz == 0) return;
-  GBX_CUDA(cudaMemsetAsync(rowid.p, 0, A.nnz * sizeof(int32_t), s));
-  k_mark_row_starts<<<ceil_div(A.n, 256), 256, 0, s>>>(A.rp.p, A.n, rowid.p);
+  GBX_CUDA(cudaMemsetAsync(rowid, 0, A.nnz * sizeof(int32_t), s));
+  k_mark_row_starts<<<ceil_div(A.n, 256), 256, 0, s>>>(A.rp.p, A.n, rowid);
   GBX_LAUNCHED();
   size_t tb = 0;
-  GBX_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, rowid.p, rowid.p, MaxOp(), A.nnz, s));
+  GBX_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, rowid, rowid, MaxOp(), A.nnz, s));
   Tmp<uint8_t> t(tb, s);
-  GBX_CUDA(cub::DeviceScan::InclusiveScan(t.p, tb, rowid.p, rowid.p, MaxOp(), A.nnz, s));
+  GBX_CUDA(cub::DeviceScan::InclusiveScan(t.p, tb, rowid, rowid, MaxOp(), A.nnz, s));
+}
+
+void expand_rows(cudaStream_t s, const Csr& A, DevArray<int32_t>& rowid) {
+  rowid.alloc(std::max<int64_t>(A.nnz, 1));
+  expand_rows_into(s, A, rowid.p);
 }
 
 __global__ void k_row_degree(const int64_t* rp, int64_t n, int32_t* deg) {
@@ -257,8 +255,8 @@ void compute_transpose(cudaStream_t s, const Csr& A, Csr& T) {
     GBX_CUDA(cudaMemsetAsync(T.rp.p, 0, (A.n + 1) * sizeof(int64_t), s));
     return;
   }
-  DevArray<int32_t> rowid;
-  expand_rows(s, A, rowid);
+  Tmp<int32_t> rowid(A.nnz, s);
+  expand_rows_into(s, A, rowid.p);
   const int bits = bits_for(A.n);
   const bool has_val = A.val.p != nullptr;
   const size_t es = has_val ? domain_size(A.domain) : 0;

@@ -29,6 +29,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <vector>
@@ -344,55 +346,86 @@ __global__ void k_gather_i32(const int32_t* src, const int32_t* idx, int64_t n, 
   if (i < n) dst[i] = src[idx[i]];
 }
 
+// first row r in [row0, row1) with length(r) <= thr[t] (lengths are
+// non-increasing: binary search), and its row pointer
+__global__ void k_pr_bounds(const int64_t* rp, int64_t row0, int64_t row1, const int64_t* thr,
+                            int nt, int64_t* out_row, int64_t* out_p) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  int64_t lo = row0, hi = row1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (rp[mid + 1] - rp[mid] <= thr[t]) hi = mid; else lo = mid + 1;
+  }
+  out_row[t] = lo;
+  out_p[t] = rp[lo];
+}
+
 // work units over relabeled rows [row0, row1) (lengths non-increasing): long
 // rows become chunk units; rows up to kPrLong are binned by G = lanes per row
 // (G*kPrIpl >= length); rows up to kPrShort get one bin per distinct length so
-// the kernel computes their nonzero offsets instead of loading row_ptr.
-static void build_units(PrPlan& P, const std::vector<int64_t>& rp, int64_t row0, int64_t row1,
-                        cudaStream_t s) {
+// the kernel computes their nonzero offsets instead of loading row_ptr.  The
+// bin boundaries come from device binary searches (no O(n) host pass).
+static void build_units(PrPlan& P, int64_t row0, int64_t row1, cudaStream_t s) {
+  // thresholds: kPrLong, then kPrShort, kPrShort-1, ..., 0
+  std::vector<int64_t> thr = {kPrLong};
+  for (int64_t L = kPrShort; L >= 0; --L) thr.push_back(L);
+  const int nt = static_cast<int>(thr.size());
+  std::vector<int64_t> brow(nt), bp(nt);
+  {
+    DevArray<int64_t> dthr(nt), drow(nt), dp(nt);
+    GBX_CUDA(cudaMemcpyAsync(dthr.p, thr.data(), nt * 8, cudaMemcpyHostToDevice, s));
+    k_pr_bounds<<<1, 64, 0, s>>>(P.trp.p, row0, row1, dthr.p, nt, drow.p, dp.p);
+    GBX_LAUNCHED();
+    GBX_CUDA(cudaMemcpyAsync(brow.data(), drow.p, nt * 8, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaMemcpyAsync(bp.data(), dp.p, nt * 8, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+  }
+  // long rows [row0, brow[0]): their row pointers, cut into chunks
+  const int64_t rlong = brow[0];
+  std::vector<int64_t> lrp(rlong - row0 + 1);
+  if (rlong > row0) {
+    GBX_CUDA(cudaMemcpyAsync(lrp.data(), P.trp.p + row0, lrp.size() * 8, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+  }
   std::vector<int64_t> chunks, lslot;
   std::vector<int32_t> lrow;
-  int64_t r = row0;
-  while (r < row1 && rp[r + 1] - rp[r] > kPrLong) {
+  for (int64_t r = row0; r < rlong; ++r) {
+    const int64_t b = lrp[r - row0], e = lrp[r - row0 + 1];
     lrow.push_back(static_cast<int32_t>(r));
     lslot.push_back(static_cast<int64_t>(chunks.size() / 2));
-    for (int64_t p = rp[r]; p < rp[r + 1]; p += kPrChunk) {
+    for (int64_t p = b; p < e; p += kPrChunk) {
       chunks.push_back(p);
-      chunks.push_back(std::min(rp[r + 1], p + kPrChunk));
+      chunks.push_back(std::min(e, p + kPrChunk));
     }
-    ++r;
   }
   lslot.push_back(static_cast<int64_t>(chunks.size() / 2));
   std::vector<PrBin> bins;
   int64_t units = 0;
   {
     // bin 0: kPrShort < len <= kPrLong, one warp (unit) per row
-    int64_t r1 = r;
-    while (r1 < row1 && rp[r1 + 1] - rp[r1] > kPrShort) ++r1;
     PrBin b{};
     b.unit0 = units;
-    b.row0 = r;
-    b.row1 = r1;
-    b.p0 = rp[r];
+    b.row0 = rlong;
+    b.row1 = brow[1];
+    b.p0 = bp[0];
     b.len = -1;
     bins.push_back(b);
-    units += r1 - r;
-    r = r1;
+    units += b.row1 - b.row0;
   }
   // bins 1..: one per exact length (non-increasing), 32 rows per unit
-  while (r < row1) {
-    const int64_t len = rp[r + 1] - rp[r];
-    int64_t r1 = r;
-    while (r1 < row1 && rp[r1 + 1] - rp[r1] == len) ++r1;
+  for (int t = 1; t < nt; ++t) {
+    const int64_t len = thr[t];
+    const int64_t r0 = brow[t], r1 = t + 1 < nt ? brow[t + 1] : row1;
+    if (r1 <= r0) continue;
     PrBin b{};
     b.unit0 = units;
-    b.row0 = r;
+    b.row0 = r0;
     b.row1 = r1;
-    b.p0 = rp[r];
+    b.p0 = bp[t];
     b.len = static_cast<int32_t>(len);
     bins.push_back(b);
-    units += (r1 - r + 31) / 32;
-    r = r1;
+    units += (r1 - r0 + 31) / 32;
   }
   if (bins.size() > static_cast<size_t>(kPrBinsMax)) fail(GBX_CUDA_ERROR, "pagerank: too many bins");
   P.nbins = static_cast<int>(bins.size());
@@ -435,15 +468,20 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
     k_gather_i32<<<ceil_div(n, 256), 256, 0, s>>>(g->rowdeg.p, P.new2old.p, n, P.deg.p);
     GBX_LAUNCHED();
   }
+  // relabeled AT: one radix sort of (new row, new col) keys -- every row's
+  // columns ascending in the new ids (the thread-per-row bins then read the
+  // hub end of x together at each step: ~2% of the iteration time against a
+  // copy that keeps the old column order)
   const int bits = bits_for(std::max<int64_t>(n, 2));
   if (nnz) {
-    DevArray<int32_t> rowid;
-    expand_rows(s, AT, rowid);
-    DevArray<uint64_t> k0(nnz), k1(nnz);
-    k_relabel_keys<<<ceil_div(nnz, 256), 256, 0, s>>>(rowid.p, AT.col.p, P.old2new.p, nnz, bits,
-                                                        k0.p);
-    GBX_LAUNCHED();
-    rowid.release();
+    Tmp<uint64_t> k0(nnz, s), k1(nnz, s);
+    {
+      Tmp<int32_t> rowid(nnz, s);
+      expand_rows_into(s, AT, rowid.p);
+      k_relabel_keys<<<ceil_div(nnz, 256), 256, 0, s>>>(rowid.p, AT.col.p, P.old2new.p, nnz,
+                                                          bits, k0.p);
+      GBX_LAUNCHED();
+    }
     uint64_t* sorted = sort_keys(s, k0.p, k1.p, nnz, 2 * bits);
     csr_from_sorted_keys(s, n, bits, sorted, nnz, P.trp, P.tcol);
   } else {
@@ -454,12 +492,9 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
 
 static void plan_rows(gbx_graph* g, PrPlan& P, int64_t row0, int64_t row1) {
   cudaStream_t s = g->stream;
-  std::vector<int64_t> rp(P.n + 1);
-  GBX_CUDA(cudaMemcpyAsync(rp.data(), P.trp.p, (P.n + 1) * 8, cudaMemcpyDeviceToHost, s));
-  GBX_CUDA(cudaStreamSynchronize(s));
   P.row0 = row0;
   P.row1 = row1;
-  build_units(P, rp, row0, row1, s);
+  build_units(P, row0, row1, s);
   P.grid = 0;  // set per precision by rows_grid() (depends on the shared-memory footprint)
   P.grid_fin = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
       (P.nlong + kPrThreads - 1) / kPrThreads, device_sms())));
@@ -474,14 +509,27 @@ void pagerank_prepare(gbx_graph* g) {
   require_at(g, "pagerank_gap");
   require_rowdeg(g, "pagerank_gap");
   if (g->pr) return;
+  static const bool timing = std::getenv("GBX_PLAN_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!timing) return;
+    GBX_CUDA(cudaStreamSynchronize(g->stream));
+    auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "pagerank_prepare %s %.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   auto P = std::make_unique<PrPlan>();
   build_relabeled(g, *P);
+  mark("relabel");
   plan_rows(g, *P, 0, P->n);
+  mark("plan_rows");
   for (int b = 0; b < 2; ++b) {
     P->r[b].alloc(std::max<int64_t>(g->A.n, 1));
     P->x[b].alloc(std::max<int64_t>(g->A.n, 1));
   }
   P->out.alloc(std::max<int64_t>(g->A.n, 1));
+  mark("vectors");
   g->pr = std::move(P);
 }
 
