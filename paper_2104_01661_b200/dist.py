@@ -9,8 +9,14 @@ rows + nnz.  Per iteration every rank runs the fused shard step on its rows
     gather step, and
   * all-reduce (sum) of the fp64 L1 partial, compared against tol exactly as
     pagerank.cpp:65-74 does (same iteration count as the single-GPU path).
-Triangle count (config 3): U replicated, oriented rows split by wedge work
+Triangle count (config 3): U replicated, middle vertices split by probe work
 (gbx_tc_partition), one u64 all-reduce at the end.
+Betweenness (config 5): the graph replicated, the sources dealt round-robin
+over the ranks (each rank runs batched Brandes on its share), one fp64
+all-reduce of the centrality partials -- the sum over sources is the
+reference's own reduction (betweenness.cpp:74-79).  With the config's 4 sources
+at most 4 ranks have work; a row-partitioned BC (one exchange per BFS level) is
+the path past that.
 
 The drivers only speak to a small backend interface, so the host logic (the
 partition bookkeeping, the exchange, the convergence test) is exercised on CPU
@@ -76,6 +82,24 @@ def sharded_triangle_count(backend, dist):
     t = torch.tensor([local], dtype=torch.int64, device=backend.device)
     dist.all_reduce(t)
     return int(t.item())
+
+
+def sharded_betweenness(backend, dist, sources):
+    """Batched Brandes over `world` ranks: rank r takes sources[r::world]; returns
+    the centrality (numpy fp64, every rank)."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    mine = [int(s) for s in list(sources)[rank::world]]
+    part = backend.bc_partial(mine)            # fp64 tensor [n] (zeros if no sources)
+    dist.all_reduce(part)
+    return part.cpu().numpy().copy()
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ view of a library-owned device buffer."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": (n,),
+                                         "typestr": typestr, "version": 3}
 
 
 class GpuShardBackend:
@@ -147,3 +171,18 @@ class GpuShardBackend:
         c = C.c_uint64(0)
         call("gbx_triangle_count_rows", C.byref(c), self.g.handle, rb, re)
         return int(c.value)
+
+    # ---- betweenness
+    def bc_partial(self, sources):
+        import torch
+
+        from .graph import call
+        n = self.g.n()
+        if not sources:
+            return torch.zeros(n, dtype=torch.float64, device=self.device)
+        src = np.ascontiguousarray(sources, np.uint64)
+        call("gbx_betweenness", None, self.g.handle, src.ctypes.data, len(src))
+        ptr, cnt = self.g.result_device("bc")
+        # the library's centrality buffer, reduced in place by NCCL (the call
+        # above has synchronised its stream)
+        return torch.as_tensor(_DeviceArray(ptr, cnt, "<f8"), device=self.device)

@@ -1,5 +1,6 @@
 """TEST ONLY: a numpy shard backend with the semantics of libgbx's shard calls
-(gbx_pr_shard_*, gbx_tc_partition, gbx_triangle_count_rows), so the
+(gbx_pr_shard_*, gbx_tc_partition, gbx_triangle_count_rows, gbx_betweenness),
+so the
 multi-process driver logic in paper_2104_01661_b200/dist.py runs over gloo on
 CPU.  Identity relabeling; fp64 storage."""
 import numpy as np
@@ -98,3 +99,11 @@ class CpuShardBackend:
             for j in self._upper(i):
                 c += len(ui.intersection(self._upper(j).tolist()))
         return c
+
+    # ---- betweenness (undirected graph: AT = A)
+    def bc_partial(self, sources):
+        import oracle as O
+        if not sources:
+            return torch.zeros(self.n, dtype=torch.float64)
+        c = O.bc(self.n, self.rp, self.col, self.rp, self.col, np.asarray(sources, np.int64))
+        return torch.from_numpy(np.ascontiguousarray(c, np.float64))

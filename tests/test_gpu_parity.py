@@ -429,6 +429,24 @@ def test_bc_deep_path_and_components():
 
 
 # ---------------------------------------------------------------- multi-GPU shard kernels
+def test_bc_partials_compose_on_one_gpu():
+    """The sharded BC driver's per-rank partials (dist.GpuShardBackend.bc_partial,
+    a view of the library's device buffer) sum to the full batch."""
+    import torch
+    from paper_2104_01661_b200.dist import GpuShardBackend
+    g = P.generate_rmat(13, 16, seed=4, kind=P.Kind.UndirectedAdjacency)
+    P.property_at(g)
+    P.property_rowdegree(g)
+    srcs = [int(x) for x in P.pick_sources(g.row_degree(), 6, 4)]
+    be = GpuShardBackend(g)
+    parts = [be.bc_partial(srcs[r::2]).clone() for r in range(2)]
+    assert parts[0].is_cuda and parts[0].dtype == torch.float64
+    got = (parts[0] + parts[1]).cpu().numpy()
+    want = algo.betweenness_centrality(g, srcs).centrality
+    assert rel_l1(got, want) <= 1e-12
+    assert float(be.bc_partial([]).abs().sum()) == 0.0
+
+
 def test_pr_shards_compose_on_one_gpu():
     """Two shard plans (ranks 0 and 1 of 2) stepped in lockstep with the x
     exchange done by hand equal the single-GPU PageRank: the shard kernels plus
