@@ -385,7 +385,8 @@ def bench_pagerank(args, dist, ws, rank, local):
                 "h2d_bytes_per_step": int(rp.nbytes + col.nbytes),
                 "d2h_bytes_per_step": int(n * 8 + 4),
                 "includes": "H2D CSR (pinned), graph_new32 validation, property_at "
-                            "(device transpose), property_rowdegree, PageRank, D2H ranks"},
+                            "(device transpose), property_rowdegree, PageRank, D2H ranks",
+                "samples_ms": [round(t * 1e3, 2) for t in e2e_times]},
         "gpu_launches": int((st["launches"]) * args.steps),
         "clocks": clk.summary(),
     }

@@ -32,8 +32,10 @@ struct Error : std::runtime_error {
 constexpr int kSMs = 148;  // B200; the runtime value is queried in device_sms()
 int device_sms();
 
-// Owning device array (cudaMalloc / cudaFree).  Persistent graph data and
-// per-plan workspaces; per-call temporaries use the stream-ordered pool.
+// Owning device array.  Persistent graph data and per-plan workspaces, taken
+// from the device's stream-ordered pool (kept cached: see Scope) so building
+// and freeing graphs does not remap hundreds of MB through cudaMalloc/cudaFree
+// each time; allocation and release both synchronise, like cudaMalloc/cudaFree.
 template <typename T>
 struct DevArray {
   T* p = nullptr;
@@ -52,19 +54,23 @@ struct DevArray {
     release();
     n = count;
     if (count) {
-      cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), 0);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(0);
       if (e != cudaSuccess) {
         p = nullptr;
         n = 0;
         (void)cudaGetLastError();
-        fail(GBX_OUT_OF_MEMORY, "cudaMalloc of " + std::to_string(count * sizeof(T)) +
+        fail(GBX_OUT_OF_MEMORY, "device allocation of " + std::to_string(count * sizeof(T)) +
                                     " bytes failed: " + cudaGetErrorString(e));
       }
     }
   }
   void ensure(size_t count) { if (n < count) alloc(count); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaDeviceSynchronize();  // every stream's work on p is done
+      cudaFreeAsync(p, 0);
+    }
     p = nullptr;
     n = 0;
   }
