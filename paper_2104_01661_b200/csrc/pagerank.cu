@@ -45,6 +45,10 @@ constexpr int kPrThreads = 256;
 #define GBX_PR_MINB 6  // resident CTAs per SM the rows kernel is compiled for
 #endif
 constexpr int kPrIpl = 8;          // items per lane: 8 independent gathers in flight
+#ifndef GBX_PR_B0IPL
+#define GBX_PR_B0IPL 4
+#endif
+constexpr int kPrB0Ipl = GBX_PR_B0IPL;  // gathers per lane per step in warp-per-row units
 constexpr int64_t kPrLong = 1024;   // rows longer than this are chunked
 constexpr int64_t kPrShort = 32;    // rows up to this length: thread per row, exact-length bins
 constexpr int64_t kPrChunk = 2048;  // nonzeros per chunk unit
@@ -212,41 +216,66 @@ __global__ void __launch_bounds__(BS, BS == 1024 ? 2 : GBX_PR_MINB) k_pr_rows(Pr
     while (bk + 1 < a.nbins && u >= s_bins[bk + 1].unit0) ++bk;
     const PrBin& B = s_bins[bk];
     if (B.len < 0) {
+      // one warp per row (kPrShort < len <= kPrLong): coalesced column loads,
+      // kPrB0Ipl gathers in flight per lane; the next group of columns is
+      // loaded while the current gathers are outstanding
       const int64_t row = B.row0 + (u - B.unit0);
       const int64_t b = a.trp[row], e = a.trp[row + 1];
       const V rprev = r_cur[row - a.row0];
       const V inv = a.inv[row];
       double s = 0.0;
-      for (int64_t base = b + lane; base < e; base += 32 * 4) {
-        int c[4];
+      int c[kPrB0Ipl];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) c[q] = base + 32 * q < e ? ld_stream(a.tcol + base + 32 * q) : -1;
+      for (int q = 0; q < kPrB0Ipl; ++q) {
+        const int64_t p = b + lane + 32 * q;
+        c[q] = p < e ? ld_stream(a.tcol + p) : -1;
+      }
+      for (int64_t base = b + lane; base < e; base += 32 * kPrB0Ipl) {
+        int nx[kPrB0Ipl];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kPrB0Ipl; ++q) {
+          const int64_t p = base + 32 * (kPrB0Ipl + q);
+          nx[q] = p < e ? ld_stream(a.tcol + p) : -1;
+        }
+#pragma unroll
+        for (int q = 0; q < kPrB0Ipl; ++q)
           if (c[q] >= 0) s += static_cast<double>(pr_xg(s_x, a.hot, a.l1hot, x_cur, c[q]));
+#pragma unroll
+        for (int q = 0; q < kPrB0Ipl; ++q) c[q] = nx[q];
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
       if (lane == 0) l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, rprev, inv);
     } else {
-      const int64_t i = (u - B.unit0) * 32 + lane;
-      const int64_t row = B.row0 + i;
+      // exact-length bin, unit-interleaved columns: element j of the unit's
+      // lane-l row sits at unit base + j * m + l (m = rows in the unit), so
+      // every column load of the warp is one coalesced 4-sector request
+      // instead of 32 scattered sectors.  The next four columns are loaded
+      // while the current four gathers are in flight.
+      const int64_t iu = u - B.unit0;
+      const int64_t row = B.row0 + iu * 32 + lane;
       if (row < B.row1) {
         const V rprev = r_cur[row - a.row0];
         const V inv = a.inv[row];
         const int L = B.len;
-        const int32_t* cp = a.tcol + B.p0 + i * L;
+        const int m = static_cast<int>(min(int64_t(32), B.row1 - B.row0 - iu * 32));
+        const int32_t* cp = a.tcol + B.p0 + iu * 32 * L + lane;
+        int c[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[q] = q < L ? ld_stream(cp + q * m) : -1;
         double s = 0.0;
-        int j = 0;
-        for (; j + 4 <= L; j += 4) {
-          const int c0 = ld_stream(cp + j), c1 = ld_stream(cp + j + 1);
-          const int c2 = ld_stream(cp + j + 2), c3 = ld_stream(cp + j + 3);
-          const V t0 = pr_xg(s_x, a.hot, a.l1hot, x_cur, c0), t1 = pr_xg(s_x, a.hot, a.l1hot, x_cur, c1);
-          const V t2 = pr_xg(s_x, a.hot, a.l1hot, x_cur, c2), t3 = pr_xg(s_x, a.hot, a.l1hot, x_cur, c3);
-          s += (static_cast<double>(t0) + static_cast<double>(t1)) +
-               (static_cast<double>(t2) + static_cast<double>(t3));
+        for (int j = 0; j < L; j += 4) {
+          int nx[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) nx[q] = j + 4 + q < L ? ld_stream(cp + (j + 4 + q) * m) : -1;
+          V t[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) t[q] = c[q] >= 0 ? pr_xg(s_x, a.hot, a.l1hot, x_cur, c[q]) : V(0);
+          s += (static_cast<double>(t[0]) + static_cast<double>(t[1])) +
+               (static_cast<double>(t[2]) + static_cast<double>(t[3]));
+#pragma unroll
+          for (int q = 0; q < 4; ++q) c[q] = nx[q];
         }
-        for (; j < L; ++j) s += static_cast<double>(pr_xg(s_x, a.hot, a.l1hot, x_cur, ld_stream(cp + j)));
         l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, rprev, inv);
       }
     }
@@ -346,6 +375,18 @@ __global__ void k_gather_i32(const int32_t* src, const int32_t* idx, int64_t n, 
   if (i < n) dst[i] = src[idx[i]];
 }
 
+// exact-length bin [row0, row0 + nrows) of length L, row-major -> unit-
+// interleaved (32-row units; element j of unit row l at unit*32*L + j*m + l)
+__global__ void k_pr_interleave(const int32_t* src, int32_t* dst, int64_t nrows, int L) {
+  const int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p >= nrows * L) return;
+  const int64_t i = p / L;
+  const int j = static_cast<int>(p - i * L);
+  const int64_t u = i >> 5;
+  const int m = static_cast<int>(min(int64_t(32), nrows - u * 32));
+  dst[u * 32 * L + int64_t(j) * m + (i & 31)] = src[p];
+}
+
 // first row r in [row0, row1) with length(r) <= thr[t] (lengths are
 // non-increasing: binary search), and its row pointer
 __global__ void k_pr_bounds(const int64_t* rp, int64_t row0, int64_t row1, const int64_t* thr,
@@ -428,6 +469,26 @@ static void build_units(PrPlan& P, int64_t row0, int64_t row1, cudaStream_t s) {
     units += (r1 - r0 + 31) / 32;
   }
   if (bins.size() > static_cast<size_t>(kPrBinsMax)) fail(GBX_CUDA_ERROR, "pagerank: too many bins");
+  // exact-length bins: columns to the unit-interleaved layout k_pr_rows reads
+  {
+    int64_t q0 = -1, q1 = -1;
+    for (const PrBin& b : bins)
+      if (b.len > 0) {
+        if (q0 < 0) q0 = b.p0;
+        q1 = b.p0 + (b.row1 - b.row0) * b.len;
+      }
+    if (q0 >= 0 && q1 > q0) {
+      Tmp<int32_t> cp(q1 - q0, s);
+      GBX_CUDA(cudaMemcpyAsync(cp.p, P.tcol.p + q0, (q1 - q0) * 4, cudaMemcpyDeviceToDevice, s));
+      for (const PrBin& b : bins) {
+        const int64_t cnt = (b.row1 - b.row0) * b.len;
+        if (b.len <= 0 || cnt == 0) continue;
+        k_pr_interleave<<<ceil_div(cnt, 256), 256, 0, s>>>(cp.p + (b.p0 - q0), P.tcol.p + b.p0,
+                                                           b.row1 - b.row0, b.len);
+        GBX_LAUNCHED();
+      }
+    }
+  }
   P.nbins = static_cast<int>(bins.size());
   P.bins.alloc(std::max<size_t>(bins.size(), 1));
   if (!bins.empty())
@@ -591,6 +652,10 @@ static size_t rows_smem(const PrArgs<V>& a) {
       GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float, 1024>,
                                     cudaFuncAttributePreferredSharedMemoryCarveout, carve));
       GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double, 1024>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float, kPrThreads>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double, kPrThreads>,
                                     cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     }
     attr = true;
