@@ -110,6 +110,36 @@ int gbx_generate_rmat(gbx_graph** g, int scale, int edge_factor, double a, doubl
 int gbx_generate_er(gbx_graph** g, int logn, int degree, uint64_t seed, int weighted,
                     char msg[GBX_MSG_LEN]);
 
+/* build_matrix (containers.cpp:128-169) + graph_new on the device: n x n
+ * tuples (rows[k], cols[k], vals[k]) -- host arrays -- sorted stably on the
+ * device, duplicates combined in input order by dup (GBX_DUP_ERROR fails with
+ * GBX_DUPLICATE_ENTRY, as mm_read's trap, io.cpp:143-153); a tuple outside
+ * n x n is GBX_INDEX_OUT_OF_BOUNDS.  vals NULL = Bool pattern. */
+enum { GBX_DUP_ERROR = 0, GBX_DUP_FIRST = 1, GBX_DUP_SECOND = 2, GBX_DUP_MIN = 3,
+       GBX_DUP_MAX = 4, GBX_DUP_PLUS = 5 };
+int gbx_graph_build(gbx_graph** g, int64_t n, int64_t nvals, const int64_t* rows,
+                    const int64_t* cols, const void* vals, int domain, int dup, int kind,
+                    char msg[GBX_MSG_LEN]);
+
+/* gblite::io (io.hpp): read_matrix_file (io.cpp:336-343) + graph_new.
+ * format "bin" = LAGK v1 (bin_read, io.cpp:282-334: GBX_BAD_MAGIC,
+ * GBX_UNSUPPORTED_VERSION, GBX_TRUNCATED_STREAM, GBX_PARSE_ERROR for an invalid
+ * matrix) streamed to HBM through pinned staging; "mm" = Matrix Market
+ * coordinate (mm_read, io.cpp:35-160: pattern/integer/real, general/symmetric,
+ * "%%domain", GBX_PARSE_ERROR / GBX_INDEX_OUT_OF_BOUNDS / GBX_DUPLICATE_ENTRY).
+ * A non-square matrix is GBX_INVALID_MATRIX (graph_new).  GBX_IO_FAILURE when
+ * the file cannot be opened.  The _buffer form parses len bytes in memory. */
+int gbx_graph_read(gbx_graph** g, const char* path, const char* format, int kind,
+                   char msg[GBX_MSG_LEN]);
+int gbx_graph_read_buffer(gbx_graph** g, const void* data, size_t len, const char* format,
+                          int kind, char msg[GBX_MSG_LEN]);
+/* write_matrix_file (io.cpp:345-355): "bin" byte-identical to bin_write
+ * (io.cpp:261-280); "mm" byte-identical to mm_write (io.cpp:162-222), symmetric
+ * != 0 writes the lower triangle and requires a symmetric matrix
+ * (GBX_INVALID_VALUE otherwise). */
+int gbx_graph_write(const gbx_graph* g, const char* path, const char* format, int symmetric,
+                    char msg[GBX_MSG_LEN]);
+
 /* n, nnz, kind, value domain. */
 int gbx_graph_info(const gbx_graph* g, int64_t* n, int64_t* nnz, int* kind, int* domain,
                    char msg[GBX_MSG_LEN]);

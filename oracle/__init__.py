@@ -272,6 +272,8 @@ def ref():
         L.ref_verify_bfs_parents.restype = C.c_int
         L.ref_verify_bfs_parents.argtypes = [C.c_void_p, C.c_int64, _i64p,
                                              C.POINTER(C.c_int)]
+        L.ref_io_convert.restype = C.c_int
+        L.ref_io_convert.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int]
         _ref = L
     return _ref
 

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <limits>
 #include <string>
 #include <vector>
@@ -246,6 +247,28 @@ int ref_verify_bfs_parents(void* gp, int64_t src, const int64_t* parent, int* ok
       }
     pv.adopt(std::move(idx), std::move(vals));
     *ok = verify::check_bfs_parents(g.A, static_cast<Index>(src), pv, nullptr) ? 1 : 0;
+  });
+}
+
+// gblite::io round trip (io.cpp:336-355): read_matrix_file(in, in_fmt), then
+// write_matrix_file(out, out_fmt) -- or mm_write(symmetric) for "mm_sym".
+// Also graph_new's square check (graph.cpp:16-28) when check_graph != 0, so the
+// code matches reading straight into a graph.
+int ref_io_convert(const char* in_path, const char* in_fmt, const char* out_path,
+                   const char* out_fmt, int check_graph) {
+  return guarded([&] {
+    SparseMatrix m = io::read_matrix_file(in_path, in_fmt);
+    if (check_graph) {
+      Graph g = graph_new(SparseMatrix(m), Kind::DirectedAdjacency);
+      (void)g;
+    }
+    if (!out_path) return;
+    if (std::string(out_fmt) == "mm_sym") {
+      std::ofstream out(out_path, std::ios::binary);
+      io::mm_write(m, out, true);
+    } else {
+      io::write_matrix_file(m, out_path, out_fmt);
+    }
   });
 }
 

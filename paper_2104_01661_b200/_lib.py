@@ -74,6 +74,10 @@ _SIGS = {
     "gbx_partition_rows": [_vp, _vp, _int, _int],
     "gbx_triangle_count_rows": [_vp, _vp, _i64, _i64],
     "gbx_tc_partition": [_vp, _vp, _int],
+    "gbx_graph_build": [_pp, _i64, _i64, _vp, _vp, _vp, _int, _int, _int],
+    "gbx_graph_read": [_pp, _cp, _cp, _int],
+    "gbx_graph_read_buffer": [_pp, _vp, C.c_size_t, _cp, _int],
+    "gbx_graph_write": [_vp, _cp, _cp, _int],
 }
 
 

@@ -136,6 +136,39 @@ int gbx_graph_new32(gbx_graph** out, int64_t n, const int64_t* row_ptr, const in
   });
 }
 
+int gbx_graph_build(gbx_graph** out, int64_t n, int64_t nvals, const int64_t* rows,
+                    const int64_t* cols, const void* vals, int domain, int dup, int kind,
+                    char* msg) {
+  return make_graph(out, msg, [&](gbx_graph* g) {
+    gbx::build_from_coo(g, n, n, nvals, rows, cols, vals, domain, dup, kind, true);
+  });
+}
+
+int gbx_graph_read(gbx_graph** out, const char* path, const char* format, int kind, char* msg) {
+  return make_graph(out, msg, [&](gbx_graph* g) {
+    if (!path) gbx::fail(GBX_NULL_ARGUMENT, "path is NULL");
+    gbx::graph_read(g, path, nullptr, 0, format, kind);
+  });
+}
+
+int gbx_graph_read_buffer(gbx_graph** out, const void* data, size_t len, const char* format,
+                          int kind, char* msg) {
+  return make_graph(out, msg, [&](gbx_graph* g) {
+    if (!data && len) gbx::fail(GBX_NULL_ARGUMENT, "data is NULL");
+    static const char empty = 0;
+    gbx::graph_read(g, nullptr, data ? data : &empty, len, format, kind);
+  });
+}
+
+int gbx_graph_write(const gbx_graph* gc, const char* path, const char* format, int symmetric,
+                    char* msg) {
+  return guard(msg, [&] {
+    gbx_graph* g = need(gc);
+    gbx::Scope sc(g);
+    gbx::graph_write(g, path, format, symmetric);
+  });
+}
+
 int gbx_generate_rmat(gbx_graph** out, int scale, int edge_factor, double a, double b,
                       double c, uint64_t seed, int scramble, int kind, char* msg) {
   return make_graph(out, msg, [&](gbx_graph* g) {

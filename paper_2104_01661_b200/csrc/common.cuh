@@ -140,6 +140,12 @@ struct Scope {
 // ---- graph-level primitives (graph.cu) ------------------------------------
 void build_from_host(gbx_graph* g, int64_t n, const int64_t* rp, const int64_t* col64,
                      const int32_t* col32, const void* vals, int domain, int kind);
+void build_from_coo(gbx_graph* g, int64_t nrows, int64_t ncols, int64_t m, const int64_t* rows,
+                    const int64_t* cols, const void* vals, int domain, int dup, int kind,
+                    bool host_ptrs);
+void graph_read(gbx_graph* g, const char* path, const void* data, size_t len, const char* format,
+                int kind);
+void graph_write(gbx_graph* g, const char* path, const char* format, int symmetric);
 void compute_transpose(cudaStream_t s, const Csr& A, Csr& T);
 void compute_degrees(cudaStream_t s, const Csr& A, DevArray<int32_t>& out, bool by_row);
 void require_at(const gbx_graph* g, const char* who);

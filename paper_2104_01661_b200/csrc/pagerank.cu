@@ -20,7 +20,8 @@
 //                  the fused epilogue r = teleport + sum, |r_prev - r| (fp64),
 //                  x_next = r / (deg / damping) (0 for dangling vertices --
 //                  their mass is lost exactly as in the reference);
-//   k_pr_finish -- sums the chunk slots of the long rows in order, their
+//   k_pr_finish -- sums the chunk slots of the long rows (warp per row, fixed
+//                  lane-strided + shuffle-tree order), their
 //                  epilogue, then the last CTA reduces every L1 partial in a
 //                  fixed order, counts the iteration and clears the WHILE
 //                  condition on convergence.  Deterministic end to end.
@@ -46,7 +47,7 @@ constexpr int kPrThreads = 256;
 #endif
 constexpr int kPrIpl = 8;          // items per lane: 8 independent gathers in flight
 #ifndef GBX_PR_B0IPL
-#define GBX_PR_B0IPL 4
+#define GBX_PR_B0IPL 2  // measured: 2 and 4 within 1%, 8 slower (registers)
 #endif
 constexpr int kPrB0Ipl = GBX_PR_B0IPL;  // gathers per lane per step in warp-per-row units
 constexpr int64_t kPrLong = 1024;   // rows longer than this are chunked
@@ -296,12 +297,19 @@ __global__ void __launch_bounds__(kPrThreads) k_pr_finish(PrArgs<V> a) {
   V *x_nxt, *r_nxt;
   pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
   double l1 = 0.0;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.nlong;
-       i += int64_t(gridDim.x) * blockDim.x) {
+  // one warp per long row: lane-strided slot sums, fixed shuffle tree
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < a.nlong; i += nw) {
+    const int64_t q0 = a.long_slot[i], q1 = a.long_slot[i + 1];
     double s = 0.0;
-    for (int64_t q = a.long_slot[i]; q < a.long_slot[i + 1]; ++q) s += a.slot[q];
-    const int64_t row = a.long_row[i];
-    l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, r_cur[row - a.row0], a.inv[row]);
+    for (int64_t q = q0 + lane; q < q1; q += 32) s += a.slot[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
+    if (lane == 0) {
+      const int64_t row = a.long_row[i];
+      l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, r_cur[row - a.row0], a.inv[row]);
+    }
   }
   double blk = BlockReduce(red).Sum(l1);
   if (threadIdx.x == 0) {
@@ -558,7 +566,7 @@ static void plan_rows(gbx_graph* g, PrPlan& P, int64_t row0, int64_t row1) {
   build_units(P, row0, row1, s);
   P.grid = 0;  // set per precision by rows_grid() (depends on the shared-memory footprint)
   P.grid_fin = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
-      (P.nlong + kPrThreads - 1) / kPrThreads, device_sms())));
+      (P.nlong * 32 + kPrThreads - 1) / kPrThreads, 4 * device_sms())));
   P.l1_block.alloc(static_cast<size_t>(device_sms()) * 32);
   P.l1_fin.alloc(P.grid_fin);
   P.l1_hist.alloc(128);

@@ -125,6 +125,12 @@ struct SsspPlan {
   DevArray<uint32_t> bbits;
   DevArray<int> bcnt;
   int nb_alloc = 0;
+  // light-first row partition for delta = split_delta (sssp.cu: k_split_*)
+  double split_delta = -1.0;
+  DevArray<int32_t> nlight, split_col, split_wi;
+  DevArray<double> split_wd;
+  DevArray<int32_t> sq;            // settled list of the current bucket
+  DevArray<uint32_t> sbits;        // its membership bitmap
 };
 
 // Betweenness workspaces (bc.cu).

@@ -321,8 +321,18 @@ struct SsspBArgs {
   uint32_t* qbits[2];  // near-queue membership (parity per near iteration)
   uint32_t* bbits;     // [nb][words] bucket membership
   int64_t words;
-  int* ctl;            // [0] |Q| [1] |Qnext| [4] near iterations [5] buckets
+  int* ctl;            // [0..2] queue counts [4] near iterations [5] buckets [6,7] jump [8] |S|
   unsigned long long* relax;
+  // light/heavy split (Delta-stepping proper, sssp.cpp:30-33, 66-106): every
+  // row holds its light edges (w <= delta) first, nl[u] of them.  Near
+  // iterations relax light edges only; each vertex that entered the bucket is
+  // recorded once in the settled list sq (dedup bitmap sbits) and, when the
+  // bucket drains, its heavy edges are relaxed ONCE from its final distance
+  // (they always land in a later bucket).  nl == nullptr: every edge in the
+  // near phase (label-correcting).
+  const int32_t* nl;
+  int32_t* sq;
+  uint32_t* sbits;
   int trace;
   unsigned long long* tlog;  // optional: [2i] %globaltimer, [2i+1] kind<<32 | size (debug)
   int tlog_cap;
@@ -390,6 +400,7 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
   __shared__ int32_t s_bv[kSsspWarps][kSsspBuf];
   __shared__ int32_t s_bb[kSsspWarps][kSsspBuf];
   __shared__ int s_bcnt[kSsspWarps][64];
+  __shared__ int32_t s_settle[kSsspWarps][kSsspBuf];
   WarpQueue<int32_t, kSsspBuf> nearq;
   BucketQueue<kSsspBuf> bucq;
   nearq.buf = s_near[threadIdx.x >> 5];
@@ -413,6 +424,119 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
   const bool tl = a.tlog && blockIdx.x == 0 && threadIdx.x == 0;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   int tn = 0;
+  // relax the edges of the vertices list[0, cnt): phase 0 all edges, 1 light
+  // edges (and record the vertex in the settled list), 2 heavy edges.  4 lanes
+  // per vertex (8 vertices per warp), each lane 4 edges per round: 4
+  // independent edge -> dist -> atomicMin chains.  pop_bits: the list's
+  // membership bitmap, released as entries are taken.
+  auto relax = [&](const int32_t* list, int cnt, int phase, uint32_t* pop_bits,
+                   uint32_t* push_bits, unsigned long long& nrel) {
+    for (int64_t base = gwarp * 8; base < cnt; base += nwarps * 8) {
+      const int64_t qi = base + g4;
+      bool active = qi < cnt;
+      const int32_t u = active ? list[qi] : 0;
+      const uint32_t ubit = 1u << (u & 31);
+      if (active && s4 == 0 && pop_bits) atomicAnd(&pop_bits[u >> 5], ~ubit);
+      int64_t p = active ? a.rp[u] : 0;
+      int64_t e = active ? a.rp[u + 1] : 0;
+      if (active && phase == 1) e = p + a.nl[u];
+      if (active && phase == 2) p += a.nl[u];
+      if (p >= e) active = false;
+      const D du = active ? *(volatile D*)&a.dist[u] : D(0);
+      while (__any_sync(kFullW, active)) {
+        int32_t v[4];
+        D nd[4];
+        bool ok[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int64_t q = p + s4 + 4 * q4;
+          ok[q4] = active && q < e;
+          W w = W(0);
+          v[q4] = 0;
+          if (ok[q4]) a.edges.get(q, v[q4], w);
+          nd[q4] = DistTraits<D>::add(du, w);
+        }
+        D cur[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) cur[q4] = ok[q4] ? *(volatile D*)&a.dist[v[q4]] : D(0);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          bool near_push = false, buck_push = false;
+          int bidx = 0;
+          if (ok[q4]) {
+            ++nrel;
+            if (nd[q4] < cur[q4]) {
+              // fire-and-forget min: a push whose value lost the race is a
+              // harmless extra relaxation (stale bucket entries are skipped)
+              atomicMin(&a.dist[v[q4]], nd[q4]);
+              const uint32_t bit = 1u << (v[q4] & 31);
+              const int64_t kb = bucket_of<D>(nd[q4], a.delta);
+              if (kb <= k && phase != 2) {  // (a heavy edge always leaves the bucket)
+                near_push = !(atomicOr(&push_bits[v[q4] >> 5], bit) & bit);
+              } else {
+                bidx = static_cast<int>(kb & nbm);
+                buck_push = !(atomicOr(&a.bbits[bidx * a.words + (v[q4] >> 5)], bit) & bit);
+              }
+            }
+          }
+          if (phase != 2) nearq.push(near_push, v[q4]);
+          bucq.push(buck_push, v[q4], bidx, a.bq, a.cap, a.bcnt, a.nb);
+        }
+        if (active) {
+          p += 16;
+          if (p >= e) active = false;
+        }
+      }
+    }
+  };
+  // heavy edges of the vertices win[0, c) (warp-local list, every lane calls)
+  auto relax_local = [&](const int32_t* win, int c, unsigned long long& nrel) {
+    for (int base = 0; base < c; base += 8) {
+      const int qi = base + g4;
+      bool active = qi < c;
+      const int32_t u = active ? win[qi] : 0;
+      int64_t p = active ? a.rp[u] + a.nl[u] : 0;
+      const int64_t e = active ? a.rp[u + 1] : 0;
+      if (p >= e) active = false;
+      const D du = active ? *(volatile D*)&a.dist[u] : D(0);
+      while (__any_sync(kFullW, active)) {
+        int32_t v[4];
+        D nd[4];
+        bool ok[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int64_t q = p + s4 + 4 * q4;
+          ok[q4] = active && q < e;
+          W w = W(0);
+          v[q4] = 0;
+          if (ok[q4]) a.edges.get(q, v[q4], w);
+          nd[q4] = DistTraits<D>::add(du, w);
+        }
+        D cur[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) cur[q4] = ok[q4] ? *(volatile D*)&a.dist[v[q4]] : D(0);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          bool buck_push = false;
+          int bidx = 0;
+          if (ok[q4]) {
+            ++nrel;
+            if (nd[q4] < cur[q4]) {
+              atomicMin(&a.dist[v[q4]], nd[q4]);
+              const uint32_t bit = 1u << (v[q4] & 31);
+              bidx = static_cast<int>(bucket_of<D>(nd[q4], a.delta) & nbm);
+              buck_push = !(atomicOr(&a.bbits[bidx * a.words + (v[q4] >> 5)], bit) & bit);
+            }
+          }
+          bucq.push(buck_push, v[q4], bidx, a.bq, a.cap, a.bcnt, a.nb);
+        }
+        if (active) {
+          p += 16;
+          if (p >= e) active = false;
+        }
+      }
+    }
+  };
   for (int guard = 0;; ++guard) {
     if (guard > (1 << 28)) break;
     // ---------------- near iterations inside bucket k
@@ -437,64 +561,35 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
       uint32_t* push_bits = a.qbits[(t + 1) & 1];
       unsigned long long nrel = 0;
       nearq.reset(qn, &a.ctl[(t + 1) % 3]);
-      for (int64_t base = gwarp * 8; base < nq; base += nwarps * 8) {
-        const int64_t qi = base + g4;
-        bool active = qi < nq;
-        const int32_t u = active ? qc[qi] : 0;
-        if (active && s4 == 0) atomicAnd(&pop_bits[u >> 5], ~(1u << (u & 31)));
-        int64_t p = active ? a.rp[u] : 0;
-        const int64_t e = active ? a.rp[u + 1] : 0;
-        const D du = active ? *(volatile D*)&a.dist[u] : D(0);
-        while (__any_sync(kFullW, active)) {
-          int32_t v[4];
-          D nd[4];
-          bool ok[4];
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const int64_t q = p + s4 + 4 * q4;
-            ok[q4] = active && q < e;
-            W w = W(0);
-            v[q4] = 0;
-            if (ok[q4]) a.edges.get(q, v[q4], w);
-            nd[q4] = DistTraits<D>::add(du, w);
-          }
-          D cur[4];
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) cur[q4] = ok[q4] ? *(volatile D*)&a.dist[v[q4]] : D(0);
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            bool near_push = false, buck_push = false;
-            int bidx = 0;
-            if (ok[q4]) {
-              ++nrel;
-              if (nd[q4] < cur[q4]) {
-                // fire-and-forget min: a push whose value lost the race is a
-                // harmless extra relaxation (stale bucket entries are skipped)
-                atomicMin(&a.dist[v[q4]], nd[q4]);
-                const uint32_t bit = 1u << (v[q4] & 31);
-                const int64_t kb = bucket_of<D>(nd[q4], a.delta);
-                if (kb <= k) {
-                  near_push = !(atomicOr(&push_bits[v[q4] >> 5], bit) & bit);
-                } else {
-                  bidx = static_cast<int>(kb & nbm);
-                  buck_push = !(atomicOr(&a.bbits[bidx * a.words + (v[q4] >> 5)], bit) & bit);
-                }
-              }
-            }
-            nearq.push(near_push, v[q4]);
-            bucq.push(buck_push, v[q4], bidx, a.bq, a.cap, a.bcnt, a.nb);
-          }
-          if (active) {
-            p += 16;
-            if (p >= e) active = false;
-          }
-        }
-      }
+      relax(qc, nq, a.nl ? 1 : 0, pop_bits, push_bits, nrel);
       nearq.flush();
       bucq.flush(a.bq, a.cap, a.bcnt, a.nb);
       if (nrel) atomicAdd(a.relax, nrel);
       grid.sync();
       ++t;
+    }
+    // ---------------- heavy edges of every vertex the bucket settled, once:
+    // a dense pass over dist (4 B/vertex, coalesced) finds the vertices whose
+    // final distance lies in bucket k -- cheaper than recording them (one more
+    // atomic per near visit); each warp compacts its 32-vertex window into
+    // shared memory and relaxes the heavy edges 8 vertices at a time
+    if (a.nl) {
+      unsigned long long nrel = 0;
+      int32_t* win = s_settle[threadIdx.x >> 5];
+      for (int64_t base = gwarp * 32; base < a.n; base += nwarps * 32) {
+        const int64_t v = base + lane;
+        const bool in = v < a.n && bucket_of<D>(*(volatile D*)&a.dist[v], a.delta) == k &&
+                        *(volatile D*)&a.dist[v] != DistTraits<D>::inf();
+        const unsigned m = __ballot_sync(kFullW, in);
+        if (in) win[__popc(m & ((1u << lane) - 1))] = static_cast<int32_t>(v);
+        __syncwarp();
+        const int c = __popc(m);
+        if (c) relax_local(win, c, nrel);
+        __syncwarp();
+      }
+      bucq.flush(a.bq, a.cap, a.bcnt, a.nb);
+      if (nrel) atomicAdd(a.relax, nrel);
+      grid.sync();
     }
     // ---------------- jump to the next non-empty bucket (at most nb-1 ahead):
     // one thread decides, everyone reads the decision after a grid barrier
@@ -506,6 +601,7 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
       a.ctl[6] = jj;
       a.ctl[7] = jj < a.nb ? *(volatile int*)&a.bcnt[(k + jj) & nbm] : 0;
       a.ctl[5] += 1;
+      a.ctl[8] = 0;  // the settled list was consumed by the heavy phase
     }
     zero_bucket = -1;
     grid.sync();
@@ -564,7 +660,7 @@ __global__ void k_sssp_init(D* dist, uint32_t* bits, int64_t n, int32_t src, int
   if (i == 0) bits[src >> 5] |= 1u << (src & 31);  // the source sits in near queue 0
   if (i == 0) {
     q0[0] = src;
-    for (int k = 0; k < 8; ++k) ctl[k] = 0;
+    for (int k = 0; k < 10; ++k) ctl[k] = 0;
     ctl[0] = 1;
     lohi[0] = D(0);
     lohi[1] = hi0;
@@ -627,6 +723,89 @@ __global__ void k_pack_edges(const int32_t* col, const uint8_t* val, int dom, in
   if (wint) wint[p] = w;
 }
 
+// light-first partition of every row for one delta (stable within each side):
+// thread per row, a counting pass then a writing pass.  Light = w <= delta
+// (sssp.cpp:30-33).
+__global__ void k_split_packed(const int64_t* rp, int64_t n, double delta, const uint32_t* src,
+                               uint32_t* dst, int32_t* nl) {
+  const int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (u >= n) return;
+  const int64_t b = rp[u], e = rp[u + 1];
+  int64_t c = 0;
+  for (int64_t p = b; p < e; ++p) c += static_cast<double>(src[p] & 0xffu) <= delta;
+  int64_t lo = b, hi = b + c;
+  for (int64_t p = b; p < e; ++p) {
+    const uint32_t x = src[p];
+    if (static_cast<double>(x & 0xffu) <= delta) dst[lo++] = x; else dst[hi++] = x;
+  }
+  nl[u] = static_cast<int32_t>(c);
+}
+template <typename W>
+__global__ void k_split_cw(const int64_t* rp, int64_t n, double delta, const int32_t* col,
+                           const W* w, int32_t* ocol, W* ow, int32_t* nl) {
+  const int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (u >= n) return;
+  const int64_t b = rp[u], e = rp[u + 1];
+  int64_t c = 0;
+  for (int64_t p = b; p < e; ++p) c += static_cast<double>(w[p]) <= delta;
+  int64_t lo = b, hi = b + c;
+  for (int64_t p = b; p < e; ++p) {
+    const int64_t q = static_cast<double>(w[p]) <= delta ? lo++ : hi++;
+    ocol[q] = col[p];
+    ow[q] = w[p];
+  }
+  nl[u] = static_cast<int32_t>(c);
+}
+
+// (re)partition the plan's edges for delta; any row order is valid for the
+// label-correcting sweep, so the packed edges are partitioned in place of the
+// plan's own copy and re-partitioned when delta changes
+static void ensure_split(gbx_graph* g, SsspPlan& P, double delta) {
+  if (P.split_delta == delta) return;
+  cudaStream_t s = g->stream;
+  const Csr& A = g->A;
+  const int64_t n = A.n, n1 = std::max<int64_t>(n, 1);
+  P.nlight.alloc(n1);
+  if (!P.sq.p) P.sq.alloc(n1 + 1);
+  if (!P.sbits.p) P.sbits.alloc((n1 + 31) / 32);
+  if (n > 0 && A.nnz > 0) {
+    if (P.packed) {
+      DevArray<uint32_t> out(A.nnz);
+      k_split_packed<<<ceil_div(n, 256), 256, 0, s>>>(A.rp.p, n, delta, P.packed_edges.p, out.p,
+                                                      P.nlight.p);
+      GBX_LAUNCHED();
+      GBX_CUDA(cudaStreamSynchronize(s));
+      P.packed_edges = std::move(out);
+    } else if (P.integral) {
+      const int32_t* w = A.domain == GBX_INT32 ? reinterpret_cast<const int32_t*>(A.val.p) : P.wint.p;
+      const int32_t* col = P.split_col.p ? P.split_col.p : A.col.p;
+      const int32_t* ws = P.split_wi.p ? P.split_wi.p : w;
+      DevArray<int32_t> oc(A.nnz), ow(A.nnz);
+      k_split_cw<int32_t><<<ceil_div(n, 256), 256, 0, s>>>(A.rp.p, n, delta, col, ws, oc.p, ow.p,
+                                                           P.nlight.p);
+      GBX_LAUNCHED();
+      GBX_CUDA(cudaStreamSynchronize(s));
+      P.split_col = std::move(oc);
+      P.split_wi = std::move(ow);
+    } else {
+      const int32_t* col = P.split_col.p ? P.split_col.p : A.col.p;
+      const double* ws = P.split_wd.p ? P.split_wd.p : reinterpret_cast<const double*>(A.val.p);
+      DevArray<int32_t> oc(A.nnz);
+      DevArray<double> ow(A.nnz);
+      k_split_cw<double><<<ceil_div(n, 256), 256, 0, s>>>(A.rp.p, n, delta, col, ws, oc.p, ow.p,
+                                                          P.nlight.p);
+      GBX_LAUNCHED();
+      GBX_CUDA(cudaStreamSynchronize(s));
+      P.split_col = std::move(oc);
+      P.split_wd = std::move(ow);
+    }
+  } else if (n > 0) {
+    GBX_CUDA(cudaMemsetAsync(P.nlight.p, 0, n * 4, s));
+  }
+  GBX_CUDA(cudaStreamSynchronize(s));
+  P.split_delta = delta;
+}
+
 void sssp_prepare(gbx_graph* g) {
   if (g->sssp) return;
   const Csr& A = g->A;
@@ -679,7 +858,7 @@ void sssp_prepare(gbx_graph* g) {
   P->far[0].alloc(fcap);
   P->far[1].alloc(fcap);
   P->stamp.alloc(4 * ((n1 + 31) / 32));  // 2 near + 2 far membership bitmaps
-  P->ctl.alloc(8);
+  P->ctl.alloc(10);
   P->lohi.alloc(3);
   P->relax.alloc(1);
   GBX_CUDA(cudaStreamSynchronize(s));
@@ -688,7 +867,7 @@ void sssp_prepare(gbx_graph* g) {
 
 template <typename D, typename E, typename W>
 static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src, double delta,
-                        D hi0, D inf) {
+                        D hi0, D inf, bool split) {
   cudaStream_t s = g->stream;
   const int64_t n = P.n;
   D* lohi = reinterpret_cast<D*>(P.lohi.p);
@@ -769,6 +948,12 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     b.words = words;
     b.ctl = a.ctl;
     b.relax = a.relax;
+    if (split) {
+      b.nl = P.nlight.p;
+      b.sq = P.sq.p;
+      b.sbits = P.sbits.p;
+      GBX_CUDA(cudaMemsetAsync(P.sbits.p, 0, P.sbits.bytes(), s));
+    }
     b.trace = std::getenv("GBX_SSSP_TRACE") ? 1 : 0;
     static const bool tlog_on = std::getenv("GBX_SSSP_TLOG") != nullptr;
     DevArray<unsigned long long> tlog;
@@ -825,25 +1010,38 @@ void sssp_run(gbx_graph* g, uint64_t source, double delta, double* out) {
   SsspPlan& P = *g->sssp;
   if (P.nonpositive) fail(GBX_NON_POSITIVE_WEIGHT, "edge weights must be positive");
   const int32_t src = static_cast<int32_t>(source);
+  // the circular-bucket kernel (nb <= 64) runs proper Delta-stepping on a
+  // light-first row partition; GBX_SSSP_NOSPLIT=1 keeps the label-correcting
+  // all-edges sweep (A/B)
+  int nb = 1;
+  while (nb < 2.0 + P.max_w / delta && nb <= 64) nb <<= 1;
+  static const bool nosplit = std::getenv("GBX_SSSP_NOSPLIT") != nullptr;
+  const bool split = nb <= 64 && !std::getenv("GBX_SSSP_NEARFAR") && !nosplit;
+  if (split) ensure_split(g, P, delta);
+  const bool cw = split && !P.packed;  // partitioned copies of col + weights
   if (P.integral) {
     // integer distances: bucket [lo, lo+delta) -> integer hi = ceil(lo + delta)
     const double h0 = std::ceil(delta);
     const uint32_t hi0 = h0 >= 4294967295.0 ? 0xffffffffu : static_cast<uint32_t>(h0);
     if (P.packed) {
       sssp_launch<uint32_t, PackedEdges, uint32_t>(g, P, PackedEdges{P.packed_edges.p},
-                                                   P.dist32.p, src, delta, hi0, 0xffffffffu);
+                                                   P.dist32.p, src, delta, hi0, 0xffffffffu,
+                                                   split);
     } else {
       const int32_t* w = g->A.domain == GBX_INT32 ? reinterpret_cast<const int32_t*>(g->A.val.p)
                                                   : P.wint.p;
-      sssp_launch<uint32_t, IntEdges, uint32_t>(g, P, IntEdges{g->A.col.p, w}, P.dist32.p, src,
-                                                delta, hi0, 0xffffffffu);
+      sssp_launch<uint32_t, IntEdges, uint32_t>(
+          g, P, IntEdges{cw ? P.split_col.p : g->A.col.p, cw ? P.split_wi.p : w}, P.dist32.p,
+          src, delta, hi0, 0xffffffffu, split);
     }
   } else {
     unsigned long long hi0, inf = 0x7FF0000000000000ull;
     std::memcpy(&hi0, &delta, 8);
     sssp_launch<unsigned long long, DblEdges, double>(
-        g, P, DblEdges{g->A.col.p, reinterpret_cast<const double*>(g->A.val.p)}, P.dist64.p,
-        src, delta, hi0, inf);
+        g, P,
+        DblEdges{cw ? P.split_col.p : g->A.col.p,
+                 cw ? P.split_wd.p : reinterpret_cast<const double*>(g->A.val.p)},
+        P.dist64.p, src, delta, hi0, inf, split);
   }
   cudaStream_t s = g->stream;
   if (out) {
@@ -856,7 +1054,7 @@ void sssp_run(gbx_graph* g, uint64_t source, double delta, double* out) {
     cudaFreeAsync(tmp, s);
     GBX_CUDA(le);
   }
-  int hctl[8];
+  int hctl[10];
   unsigned long long rel = 0;
   GBX_CUDA(cudaMemcpyAsync(hctl, P.ctl.p, sizeof hctl, cudaMemcpyDeviceToHost, s));
   GBX_CUDA(cudaMemcpyAsync(&rel, P.relax.p, 8, cudaMemcpyDeviceToHost, s));
