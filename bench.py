@@ -428,6 +428,17 @@ def bench_simple(args, dist, ws, rank, local):
         unit_edges = nnz / 2  # Graph500 undirected convention (reached component ~ all)
         metric = f"BFS GTEPS at R-MAT scale {scale} ({'single source' if w == 'bfs' else '64-source batch'})"
         unit = "GTEPS"
+        # per source B = 8 E_r + 24 V_r (int64 col once; row_ptr,
+        # parent, level per reached vertex), E_r/V_r from one untimed traversal
+        used = srcs[:8] if w == "bfs" else srcs
+        alg_bytes = 0.0
+        for s0 in used:
+            par = np.empty(n, np.int64)
+            call("gbx_bfs", par.ctypes.data, None, g.handle, int(s0), 0, 16)
+            reached = par >= 0
+            alg_bytes += 8.0 * float(deg[reached].sum()) + 24.0 * float(reached.sum())
+        roof_kernel = "k_bfs1 (cooperative push/pull levels)" if w == "bfs" else "k_bfs64 (64-lane batch)"
+        roof_note = "8*E_r + 24*V_r per source (SURVEY 8d), summed over the step's sources"
     elif w == "tc":
         scale = args.scale or 22
         g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
@@ -442,6 +453,19 @@ def bench_simple(args, dist, ws, rank, local):
         unit_edges = nnz / 2
         metric = f"triangle count edges/s at R-MAT scale {scale}"
         unit = "edges/s"
+        # our probe formulation (DESIGN 5): 4*W2 + 12*nnz(U) + 8*(n+1),
+        # W2 = sum_i C(dU(i), 2) over the (degree, id)-oriented upper triangle U
+        rp_h, col_h, _ = g.export()
+        dg = np.diff(rp_h)
+        rank = np.empty(n, np.int64)
+        rank[np.lexsort((np.arange(n), dg))] = np.arange(n)
+        rows = np.repeat(np.arange(n, dtype=np.int64), dg)
+        du = np.bincount(rows[rank[col_h] > rank[rows]], minlength=n).astype(np.float64)
+        del rows, rp_h, col_h
+        w2 = float((du * (du - 1) / 2).sum())
+        alg_bytes = 4.0 * w2 + 12.0 * float(du.sum()) + 8.0 * (n + 1)
+        roof_kernel = "k_tc_warp / k_tc_cta (middle-vertex probes)"
+        roof_note = f"4*W2 + 12*nnz(U) + 8*(n+1), W2 = {w2:.4g} wedge probes (DESIGN 5)"
     elif w == "sssp":
         logn = args.scale or 24
         g = P.generate_er(logn, 16, seed=1)
@@ -458,6 +482,16 @@ def bench_simple(args, dist, ws, rank, local):
         unit_edges = nnz
         metric = f"SSSP relaxation edges/s (ER 2^{logn}, 16 sources, delta 64)"
         unit = "edges/s"
+        # per source B = 8 m_r + 12 V_r (reached edges / vertices)
+        odeg = g.row_degree()
+        alg_bytes = 0.0
+        for s0 in srcs:
+            dd = np.empty(n, np.float64)
+            call("gbx_sssp", dd.ctypes.data, g.handle, int(s0), 64.0)
+            reached = np.isfinite(dd)
+            alg_bytes += 8.0 * float(odeg[reached].sum()) + 12.0 * float(reached.sum())
+        roof_kernel = "k_sssp_b (cooperative circular delta-buckets)"
+        roof_note = "8*m_r + 12*V_r per source (SURVEY 8d), summed over 16 sources"
     elif w == "bc":
         scale = args.scale or 24
         g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
@@ -474,6 +508,18 @@ def bench_simple(args, dist, ws, rank, local):
         unit_edges = nnz
         metric = f"BC batch-4 edges/s at R-MAT scale {scale}"
         unit = "edges/s"
+        # per batch B = E_r (8 + 16 ns) + V_r (16 + 24 ns), reached =
+        # the union of the sources' components (one untimed BFS each)
+        bdeg = g.row_degree()
+        reach = np.zeros(n, bool)
+        for s0 in srcs:
+            par = np.empty(n, np.int64)
+            call("gbx_bfs", par.ctypes.data, None, g.handle, int(s0), 0, 16)
+            reach |= par >= 0
+        ns = 4
+        alg_bytes = float(bdeg[reach].sum()) * (8 + 16 * ns) + float(reach.sum()) * (16 + 24 * ns)
+        roof_kernel = "k_bc_push/k_bc_pull/k_bc_back (batched Brandes levels)"
+        roof_note = "E_r*(8+16*ns) + V_r*(16+24*ns), ns = 4 (SURVEY 8d)"
     else:
         raise SystemExit(f"unknown workload {w}")
     stream = torch.cuda.ExternalStream(g.stream())
@@ -500,6 +546,12 @@ def bench_simple(args, dist, ws, rank, local):
            "config": {"workload": w, "scale": args.scale, "n": n, "nnz": nnz},
            "gpu_launches": int(g.last_stats()["launches"] * args.steps),
            "clocks": clk.summary()}
+    achieved = alg_bytes / t / 1e9
+    out["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                       "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                       "kernel": roof_kernel, "bytes_per_step": alg_bytes,
+                       "note": roof_note + "; divided by the device time of the whole step "
+                               "(all of the step's launches)"}
     return out, None
 
 

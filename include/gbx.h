@@ -235,6 +235,75 @@ int gbx_basic_betweenness(double* centrality, gbx_graph* g, const uint64_t* sour
 int gbx_basic_connected_components(int64_t* label, int* iterations, gbx_graph* g,
                                    char msg[GBX_MSG_LEN]);
 
+/* ---- GraphBLAS operation layer (core.hpp / core.cpp, ops.cpp) -------------
+ * The operations the paper's algorithms are written in, on the device, with
+ * the reference's semantics bit for bit (every fold in the reference's order):
+ *   gbx_mxv  (core.cpp:340-386)  w<mask> accum= A ⊕.⊗ u
+ *   gbx_vxm  (core.cpp:308-338)  w<mask> accum= u ⊕.⊗ A
+ *   gbx_mxm  (core.cpp:267-306)  C<mask> accum= A ⊕.⊗ B
+ * followed by the shared mask / accumulator / replace post-step
+ * (merge_entries, core.cpp:131-175).  Matrices are gbx_mat handles (device
+ * CSR, any shape, bool/int64/uint64/fp64 values); vectors are host sparse
+ * vectors (ascending indices).  Vector results are written to caller arrays of
+ * capacity w->n; matrix results are new gbx_mat handles.  Errors are the
+ * reference's: DimensionMismatch, DomainMismatch, AliasedOutput,
+ * InvalidMatrix, InvalidValue. */
+typedef struct gbx_mat gbx_mat;
+/* built-in semirings (ops.cpp:362-372); the domain argument is the operand /
+ * result domain (any_secondi is always uint64) */
+enum { GBX_SR_PLUS_TIMES = 0, GBX_SR_ANY_SECONDI = 1, GBX_SR_MIN_PLUS = 2, GBX_SR_PLUS_FIRST = 3,
+       GBX_SR_PLUS_SECOND = 4, GBX_SR_PLUS_PAIR = 5, GBX_SR_MIN_SECOND = 6 };
+/* binary operators (ops.cpp:52-203) for the accumulator; GBX_OP_SECONDI is
+ * the positional multiply of any_secondi only */
+enum { GBX_OP_NONE = 0, GBX_OP_PLUS = 1, GBX_OP_MINUS = 2, GBX_OP_TIMES = 3, GBX_OP_DIV = 4,
+       GBX_OP_MIN = 5, GBX_OP_MAX = 6, GBX_OP_FIRST = 7, GBX_OP_SECOND = 8, GBX_OP_PAIR = 9,
+       GBX_OP_ANY = 10, GBX_OP_LOR = 11, GBX_OP_LAND = 12, GBX_OP_SECONDI = 13 };
+/* SparseVector (containers.hpp): n, nvals, idx[nvals] ascending, vals[nvals]
+ * (bool as uint8, others 8 bytes) */
+typedef struct {
+  int64_t n;
+  int64_t nvals;
+  const int64_t* idx;
+  const void* vals;
+  int domain;
+} gbx_vec;
+/* Descriptor + MaskSpec (core.hpp:15-73); zero-initialised = no mask, merge,
+ * no accumulator, no transposes */
+typedef struct {
+  const gbx_vec* mask_vec;
+  const gbx_mat* mask_mat;
+  int complement;
+  int structural;
+  int replace;
+  int accum;         /* GBX_OP_*; GBX_OP_NONE = no accumulator */
+  int accum_domain;  /* the accumulator operator's domain */
+  int transpose_in1;
+  int transpose_in2;
+} gbx_desc;
+/* SparseMatrix from host CSR (validated like containers.cpp:104-124) */
+int gbx_mat_new(gbx_mat** m, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                const int64_t* col_idx, const void* vals, int domain, char msg[GBX_MSG_LEN]);
+/* a graph's A (which = 0) or cached AT (which = 1) as an operand; pattern
+ * graphs are bool true, int32 weights widen to int64 */
+int gbx_mat_from_graph(gbx_mat** m, const gbx_graph* g, int which, char msg[GBX_MSG_LEN]);
+int gbx_mat_info(const gbx_mat* m, int64_t* nrows, int64_t* ncols, int64_t* nvals, int* domain,
+                 char msg[GBX_MSG_LEN]);
+/* row_ptr[nrows+1], col[nvals] (int64), vals[nvals] (domain element size) */
+int gbx_mat_export(const gbx_mat* m, int64_t* row_ptr, int64_t* col_idx, void* vals,
+                   char msg[GBX_MSG_LEN]);
+int gbx_mat_free(gbx_mat** m, char msg[GBX_MSG_LEN]);
+/* w is the prior output (its entries merge / accumulate); the result replaces
+ * it in (w_idx, w_vals, *w_nvals) */
+int gbx_mxv(int64_t* w_idx, void* w_vals, int64_t* w_nvals, const gbx_vec* w,
+            const gbx_desc* desc, int semiring, int domain, const gbx_mat* A, const gbx_vec* u,
+            char msg[GBX_MSG_LEN]);
+int gbx_vxm(int64_t* w_idx, void* w_vals, int64_t* w_nvals, const gbx_vec* w,
+            const gbx_desc* desc, int semiring, int domain, const gbx_vec* u, const gbx_mat* A,
+            char msg[GBX_MSG_LEN]);
+/* *C_out = post_step(C, A ⊕.⊗ B); C is the prior output (not modified) */
+int gbx_mxm(gbx_mat** C_out, const gbx_mat* C, const gbx_desc* desc, int semiring, int domain,
+            const gbx_mat* A, const gbx_mat* B, char msg[GBX_MSG_LEN]);
+
 /* ---- device plumbing (benchmarks, multi-GPU drivers) ---------------------- */
 
 /* The handle's CUDA stream (cudaStream_t) -- record events on it to time calls. */

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <fstream>
 #include <limits>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -270,6 +271,164 @@ int ref_io_convert(const char* in_path, const char* in_fmt, const char* out_path
       io::write_matrix_file(m, out_path, out_fmt);
     }
   });
+}
+
+}  // extern "C"
+
+// ---- GraphBLAS operation layer (core.cpp:267-386) for the op-layer fixtures ----
+namespace {
+
+Scalar scalar_at(int dom, const void* vals, int64_t p) {
+  switch (dom) {
+    case 0: return static_cast<const uint8_t*>(vals)[p] != 0;
+    case 1: return static_cast<const int64_t*>(vals)[p];
+    case 2: return static_cast<const uint64_t*>(vals)[p];
+    default: return static_cast<const double*>(vals)[p];
+  }
+}
+
+void scalar_put(int dom, const Scalar& v, void* out, int64_t p) {
+  switch (dom) {
+    case 0: static_cast<uint8_t*>(out)[p] = as_bool(v) ? 1 : 0; break;
+    case 1: static_cast<int64_t*>(out)[p] = as_int64(v); break;
+    case 2: static_cast<uint64_t*>(out)[p] = as_uint64(v); break;
+    default: static_cast<double*>(out)[p] = as_fp64(v); break;
+  }
+}
+
+SparseMatrix mat_of(int64_t nr, int64_t nc, const int64_t* rp, const int64_t* col,
+                    const void* vals, int dom) {
+  SparseMatrix m(nr, nc, static_cast<Domain>(dom));
+  const int64_t nnz = rp[nr];
+  std::vector<Index> r(rp, rp + nr + 1), c(col, col + nnz);
+  std::vector<Scalar> v;
+  v.reserve(nnz);
+  for (int64_t p = 0; p < nnz; ++p) v.push_back(scalar_at(dom, vals, p));
+  m.adopt(std::move(r), std::move(c), std::move(v));
+  return m;
+}
+
+SparseVector vec_of(int64_t n, int64_t nv, const int64_t* idx, const void* vals, int dom) {
+  SparseVector w(n, static_cast<Domain>(dom));
+  for (int64_t p = 0; p < nv; ++p) w.set_element(idx[p], scalar_at(dom, vals, p));
+  return w;
+}
+
+Semiring semiring_of(int sr, int dom) {
+  const Domain d = static_cast<Domain>(dom);
+  switch (sr) {
+    case 0: return ops::plus_times(d);
+    case 1: return ops::any_secondi();
+    case 2: return ops::min_plus(d);
+    case 3: return ops::plus_first(d);
+    case 4: return ops::plus_second(d);
+    case 5: return ops::plus_pair(d);
+    default: return ops::min_second(d);
+  }
+}
+
+std::optional<BinaryOp> accum_of(int op, int dom) {
+  const Domain d = static_cast<Domain>(dom);
+  switch (op) {
+    case 1: return ops::plus(d);
+    case 2: return ops::minus(d);
+    case 3: return ops::times(d);
+    case 4: return ops::div(d);
+    case 5: return ops::min(d);
+    case 6: return ops::max(d);
+    case 7: return ops::first(d);
+    case 8: return ops::second(d);
+    case 9: return ops::pair(d);
+    case 10: return ops::any(d);
+    case 11: return ops::lor();
+    case 12: return ops::land();
+    default: return std::nullopt;
+  }
+}
+
+thread_local SparseMatrix g_last_mat;
+
+}  // namespace
+
+extern "C" {
+
+// op: 0 mxv (A, u), 1 vxm (u, A); returns the post-step output vector
+int ref_vec_op(int op, int sr, int sdom, int64_t anr, int64_t anc, const int64_t* arp,
+               const int64_t* acol, const void* aval, int adom, int64_t un, int64_t unv,
+               const int64_t* uidx, const void* uval, int udom, int64_t wn, int64_t wnv,
+               const int64_t* widx, const void* wval, int wdom, int has_mask, int64_t mn,
+               int64_t mnv, const int64_t* midx, const void* mval, int mdom, int comp, int structural,
+               int replace, int accum, int accum_dom, int tr1, int tr2, int64_t* out_idx,
+               void* out_val, int64_t* out_nv) {
+  return guarded([&] {
+    SparseMatrix A = mat_of(anr, anc, arp, acol, aval, adom);
+    SparseVector u = vec_of(un, unv, uidx, uval, udom);
+    SparseVector w = vec_of(wn, wnv, widx, wval, wdom);
+    SparseVector M = has_mask ? vec_of(mn, mnv, midx, mval, mdom) : SparseVector();
+    Descriptor d;
+    if (has_mask) d.mask_of(M);
+    d.mask.complement = comp != 0;
+    d.mask.structural = structural != 0;
+    d.mask.replace = replace != 0;
+    d.accum = accum_of(accum, accum_dom);
+    d.transpose_in1 = tr1 != 0;
+    d.transpose_in2 = tr2 != 0;
+    const Semiring s = semiring_of(sr, sdom);
+    if (op == 0) mxv(w, d, s, A, u);
+    else vxm(w, d, s, u, A);
+    *out_nv = static_cast<int64_t>(w.nvals());
+    for (int64_t p = 0; p < *out_nv; ++p) {
+      out_idx[p] = static_cast<int64_t>(w.indices()[p]);
+      scalar_put(wdom, w.values()[p], out_val, p);
+    }
+  });
+}
+
+int ref_mxm2(int sr, int sdom, int64_t anr, int64_t anc, const int64_t* arp, const int64_t* acol,
+             const void* aval, int adom, int64_t bnr, int64_t bnc, const int64_t* brp,
+             const int64_t* bcol, const void* bval, int bdom, int64_t cnr, int64_t cnc,
+             const int64_t* crp, const int64_t* ccol, const void* cval, int cdom, int has_mask,
+             int64_t mnr, int64_t mnc, const int64_t* mrp, const int64_t* mcol, const void* mval,
+             int mdom, int comp, int structural, int replace, int accum, int accum_dom, int tr1,
+             int tr2, int64_t* out_nnz) {
+  return guarded([&] {
+    SparseMatrix A = mat_of(anr, anc, arp, acol, aval, adom);
+    SparseMatrix B = mat_of(bnr, bnc, brp, bcol, bval, bdom);
+    SparseMatrix C = mat_of(cnr, cnc, crp, ccol, cval, cdom);
+    SparseMatrix M = has_mask ? mat_of(mnr, mnc, mrp, mcol, mval, mdom) : SparseMatrix();
+    Descriptor d;
+    if (has_mask) d.mask_of(M);
+    d.mask.complement = comp != 0;
+    d.mask.structural = structural != 0;
+    d.mask.replace = replace != 0;
+    d.accum = accum_of(accum, accum_dom);
+    d.transpose_in1 = tr1 != 0;
+    d.transpose_in2 = tr2 != 0;
+    mxm(C, d, semiring_of(sr, sdom), A, B);
+    *out_nnz = static_cast<int64_t>(C.nvals());
+    g_last_mat = std::move(C);
+  });
+}
+
+int ref_mxm(int sr, int sdom, int64_t anr, int64_t anc, const int64_t* arp, const int64_t* acol,
+            const void* aval, int adom, int64_t bnr, int64_t bnc, const int64_t* brp,
+            const int64_t* bcol, const void* bval, int bdom, int64_t cnr, int64_t cnc,
+            const int64_t* crp, const int64_t* ccol, const void* cval, int cdom, int has_mask,
+            const int64_t* mrp, const int64_t* mcol, const void* mval, int mdom, int comp,
+            int structural, int replace, int accum, int accum_dom, int tr1, int tr2,
+            int64_t* out_nnz) {
+  return ref_mxm2(sr, sdom, anr, anc, arp, acol, aval, adom, bnr, bnc, brp, bcol, bval, bdom, cnr,
+                  cnc, crp, ccol, cval, cdom, has_mask, cnr, cnc, mrp, mcol, mval, mdom, comp,
+                  structural, replace, accum, accum_dom, tr1, tr2, out_nnz);
+}
+
+void ref_mxm_fetch(int64_t* rp, int64_t* col, void* vals) {
+  const SparseMatrix& C = g_last_mat;
+  for (int64_t i = 0; i <= static_cast<int64_t>(C.nrows()); ++i) rp[i] = C.row_ptr()[i];
+  for (int64_t p = 0; p < static_cast<int64_t>(C.nvals()); ++p) {
+    col[p] = C.col_idx()[p];
+    scalar_put(static_cast<int>(C.domain()), C.values()[p], vals, p);
+  }
 }
 
 }  // extern "C"

@@ -78,6 +78,14 @@ _SIGS = {
     "gbx_graph_read": [_pp, _cp, _cp, _int],
     "gbx_graph_read_buffer": [_pp, _vp, C.c_size_t, _cp, _int],
     "gbx_graph_write": [_vp, _cp, _cp, _int],
+    "gbx_mat_new": [_pp, _i64, _i64, _vp, _vp, _vp, _int],
+    "gbx_mat_from_graph": [_pp, _vp, _int],
+    "gbx_mat_info": [_vp, _vp, _vp, _vp, _vp],
+    "gbx_mat_export": [_vp, _vp, _vp, _vp],
+    "gbx_mat_free": [_pp],
+    "gbx_mxv": [_vp, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp],
+    "gbx_vxm": [_vp, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp],
+    "gbx_mxm": [_pp, _vp, _vp, _int, _int, _vp, _vp],
 }
 
 

@@ -106,6 +106,28 @@ int make_graph(gbx_graph** out, char* msg, Build&& build) {
 
 }  // namespace
 
+namespace {
+template <typename Build>
+int make_mat(gbx_mat** out, char* msg, Build&& build) {
+  return guard(msg, [&] {
+    if (!out) gbx::fail(GBX_NULL_ARGUMENT, "output handle pointer is NULL");
+    *out = nullptr;
+    gbx_mat* m = gbx::mat_alloc();
+    try {
+      build(m);
+    } catch (...) {
+      delete m;
+      throw;
+    }
+    *out = m;
+  });
+}
+gbx_mat* need_mat(const gbx_mat* m) {
+  if (!m) gbx::fail(GBX_NULL_ARGUMENT, "matrix handle is NULL");
+  return const_cast<gbx_mat*>(m);
+}
+}  // namespace
+
 extern "C" {
 
 const char* gbx_version(void) { return GBX_VERSION; }
@@ -166,6 +188,68 @@ int gbx_graph_write(const gbx_graph* gc, const char* path, const char* format, i
     gbx_graph* g = need(gc);
     gbx::Scope sc(g);
     gbx::graph_write(g, path, format, symmetric);
+  });
+}
+
+// ---- GraphBLAS operation layer (ops.cu) ------------------------------------
+
+
+int gbx_mat_new(gbx_mat** out, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                const int64_t* col_idx, const void* vals, int domain, char* msg) {
+  return make_mat(out, msg, [&](gbx_mat* m) {
+    gbx::mat_from_host(m, nrows, ncols, row_ptr, col_idx, vals, domain);
+  });
+}
+
+int gbx_mat_from_graph(gbx_mat** out, const gbx_graph* gc, int which, char* msg) {
+  return make_mat(out, msg, [&](gbx_mat* m) {
+    gbx_graph* g = need(gc);
+    gbx::Scope sc(g);
+    gbx::mat_from_graph(m, g, which);
+  });
+}
+
+int gbx_mat_info(const gbx_mat* mc, int64_t* nrows, int64_t* ncols, int64_t* nvals, int* domain,
+                 char* msg) {
+  return guard(msg, [&] {
+    gbx_mat* m = need_mat(mc);
+    if (nrows) *nrows = m->nrows;
+    if (ncols) *ncols = m->ncols;
+    if (nvals) *nvals = m->nnz;
+    if (domain) *domain = m->domain;
+  });
+}
+
+int gbx_mat_export(const gbx_mat* mc, int64_t* row_ptr, int64_t* col_idx, void* vals, char* msg) {
+  return guard(msg, [&] { gbx::mat_export(need_mat(mc), row_ptr, col_idx, vals); });
+}
+
+int gbx_mat_free(gbx_mat** m, char* msg) {
+  return guard(msg, [&] {
+    if (!m) gbx::fail(GBX_NULL_ARGUMENT, "handle pointer is NULL");
+    delete *m;
+    *m = nullptr;
+  });
+}
+
+int gbx_mxv(int64_t* w_idx, void* w_vals, int64_t* w_nvals, const gbx_vec* w, const gbx_desc* desc,
+            int semiring, int domain, const gbx_mat* A, const gbx_vec* u, char* msg) {
+  return guard(msg, [&] {
+    gbx::mxv_op(w_idx, w_vals, w_nvals, w, desc, semiring, domain, need_mat(A), u);
+  });
+}
+
+int gbx_vxm(int64_t* w_idx, void* w_vals, int64_t* w_nvals, const gbx_vec* w, const gbx_desc* desc,
+            int semiring, int domain, const gbx_vec* u, const gbx_mat* A, char* msg) {
+  return guard(msg, [&] {
+    gbx::vxm_op(w_idx, w_vals, w_nvals, w, desc, semiring, domain, u, need_mat(A));
+  });
+}
+
+int gbx_mxm(gbx_mat** C_out, const gbx_mat* C, const gbx_desc* desc, int semiring, int domain,
+            const gbx_mat* A, const gbx_mat* B, char* msg) {
+  return make_mat(C_out, msg, [&](gbx_mat* out) {
+    gbx::mxm_op(out, need_mat(C), desc, semiring, domain, need_mat(A), need_mat(B));
   });
 }
 
@@ -632,6 +716,14 @@ int gbx_result_device(const gbx_graph* gc, const char* which, void** ptr, int64_
 int gbx_last_stats(const gbx_graph* gc, gbx_stats* stats, char* msg) {
   return guard(msg, [&] {
     gbx_graph* g = need(gc);
+    gbx::Scope sc(g);
+    if (g->pending_iters) {  // an asynchronous call: its count lands with the stream
+      int it = 0;
+      GBX_CUDA(cudaMemcpyAsync(&it, g->pending_iters, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+      GBX_CUDA(cudaStreamSynchronize(g->stream));
+      g->stats.iterations = it;
+      g->pending_iters = nullptr;
+    }
     *stats = g->stats;
   });
 }

@@ -867,6 +867,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
   }
   GBX_CUDA(cudaStreamSynchronize(s));
   g->stats = gbx_stats{};
+  g->pending_iters = nullptr;
   g->stats.launches = launches;
   g->stats.iterations = max_levels;
   g->stats.work_units = edges;

@@ -465,6 +465,17 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
                                          dim3(kBfsThreads), args, 0, s));
   }
   if (tlog_on) GBX_CUDA(cudaEventRecord(ev[2], s));
+  g->stats = gbx_stats{};
+  g->pending_iters = nullptr;
+  g->stats.launches = 3 + (parent ? 1 : 0) + (level ? 1 : 0);
+  g->stats.hot_launches = 1;
+  if (!parent && !level && !tlog_on) {
+    // device-resident result (gbx_result_device): the call stays asynchronous
+    // (gbx.h: synchronous unless every output pointer is NULL), so back-to-back
+    // traversals queue on the stream without a host round trip between them
+    g->pending_iters = W.ctl.p + 5;  // read by gbx_last_stats after a stream sync
+    return;
+  }
   if (parent) copy_out_i64(s, W.parent.p, n, INT_MAX, parent);
   if (level) copy_out_i64(s, W.level.p, n, -1, level);
   int hctl[8] = {0};
@@ -480,9 +491,6 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
                  t12 * 1e3, t23 * 1e3);
     for (auto& e : ev) cudaEventDestroy(e);
   }
-  g->stats = gbx_stats{};
-  g->stats.launches = 3 + (parent ? 1 : 0) + (level ? 1 : 0);
-  g->stats.hot_launches = 1;
   g->stats.iterations = hctl[5];
   if (tlog_on) dump_tlog(W, "bfs1");
 }
@@ -789,6 +797,7 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
   static int grid = 0;
   if (!grid) grid = coop_grid(reinterpret_cast<const void*>(k_bfs64), kBfsThreads);
   int64_t total_launches = 0;
+  g->pending_iters = nullptr;
   for (uint64_t b0 = 0; b0 < ns; b0 += 64) {
     const int nb = static_cast<int>(std::min<uint64_t>(64, ns - b0));
     k_bfs64_init<<<ceil_div(n * 64, 256), 256, 0, s>>>(W.seen.p, W.front.p, W.next.p,

@@ -74,6 +74,7 @@ void cc_run(gbx_graph* g, int64_t* label, int* iters) {
   }
   cudaStream_t s = g->stream;
   g->stats = gbx_stats{};
+  g->pending_iters = nullptr;
   if (n == 0) { if (iters) *iters = 0; return; }
   k_cc_init<<<ceil_div(n, 256), 256, 0, s>>>(W.parent.p, n);
   GBX_LAUNCHED();

@@ -124,9 +124,33 @@ struct gbx_graph {
   std::unique_ptr<gbx::CcWork> cc;
   std::unique_ptr<gbx::PrShard> prs;
   gbx_stats stats{};
+  const int* pending_iters = nullptr;  // device word holding stats.iterations of an async call
 
   const gbx::Csr& AT() const { return kind == GBX_UNDIRECTED ? A : at_own; }
   ~gbx_graph();
+};
+
+// operand matrix of the GraphBLAS operation layer (ops.cu)
+struct gbx_mat {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  int domain = GBX_BOOL;
+  gbx::DevArray<int64_t> rp;
+  gbx::DevArray<int32_t> col;
+  gbx::DevArray<uint64_t> val;  // 8-byte lanes
+  // cached transpose (vxm / transpose flags)
+  gbx::DevArray<int64_t> trp;
+  gbx::DevArray<int32_t> tcol;
+  gbx::DevArray<uint64_t> tval;
+  bool has_t = false;
+  ~gbx_mat() {
+    if (stream) {
+      cudaSetDevice(device);
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+  }
 };
 
 namespace gbx {
@@ -146,6 +170,17 @@ void build_from_coo(gbx_graph* g, int64_t nrows, int64_t ncols, int64_t m, const
 void graph_read(gbx_graph* g, const char* path, const void* data, size_t len, const char* format,
                 int kind);
 void graph_write(gbx_graph* g, const char* path, const char* format, int symmetric);
+gbx_mat* mat_alloc();
+void mat_from_host(gbx_mat* M, int64_t nrows, int64_t ncols, const int64_t* rp, const int64_t* col,
+                   const void* vals, int domain);
+void mat_from_graph(gbx_mat* M, gbx_graph* g, int which);
+void mat_export(gbx_mat* M, int64_t* rp, int64_t* col, void* vals);
+void mxv_op(int64_t* w_idx, void* w_vals, int64_t* w_nvals, const gbx_vec* w, const gbx_desc* d,
+            int sr, int sdom, gbx_mat* A, const gbx_vec* u);
+void vxm_op(int64_t* w_idx, void* w_vals, int64_t* w_nvals, const gbx_vec* w, const gbx_desc* d,
+            int sr, int sdom, const gbx_vec* u, gbx_mat* A);
+void mxm_op(gbx_mat* out, gbx_mat* C, const gbx_desc* desc, int sr, int sdom, gbx_mat* A,
+            gbx_mat* B);
 void compute_transpose(cudaStream_t s, const Csr& A, Csr& T);
 void compute_degrees(cudaStream_t s, const Csr& A, DevArray<int32_t>& out, bool by_row);
 void require_at(const gbx_graph* g, const char* who);

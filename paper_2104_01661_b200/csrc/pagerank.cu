@@ -857,6 +857,7 @@ void pagerank_run(gbx_graph* g, double damping, double tol, int itermax, double*
   if (!(damping > 0.0)) fail(GBX_NON_POSITIVE_DAMPING, "damping must be positive");
   const int64_t n = g->A.n;
   g->stats = gbx_stats{};
+  g->pending_iters = nullptr;
   if (n == 0 || itermax <= 0) {
     if (iters) *iters = itermax <= 0 ? std::max(itermax, 0) : 0;
     if (n > 0 && rank) {

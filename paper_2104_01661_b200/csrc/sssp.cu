@@ -41,6 +41,9 @@ namespace cg = cooperative_groups;
 namespace gbx {
 
 constexpr int kSsspThreads = 256;
+#ifndef GBX_SSSP_MINB
+#define GBX_SSSP_MINB 4  // resident CTAs per SM (measured: 2 -> 160 ms, 3 -> 133, 4 -> 128 for config 4)
+#endif
 constexpr int kSsspWarps = kSsspThreads / 32;
 constexpr int kSsspBuf = 256;  // staged pushes per warp and queue
 constexpr unsigned kFullW = 0xffffffffu;
@@ -394,7 +397,7 @@ struct BucketQueue {
 };
 
 template <typename D, typename E, typename W>
-__global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
+__global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArgs<D, E> a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ int32_t s_near[kSsspWarps][kSsspBuf];
   __shared__ int32_t s_bv[kSsspWarps][kSsspBuf];
@@ -561,7 +564,15 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
       uint32_t* push_bits = a.qbits[(t + 1) & 1];
       unsigned long long nrel = 0;
       nearq.reset(qn, &a.ctl[(t + 1) % 3]);
-      relax(qc, nq, a.nl ? 1 : 0, pop_bits, push_bits, nrel);
+      // large queues release their dedup bitmap wholesale (coalesced stores;
+      // the next push into it is two barriers away) instead of one atomicAnd
+      // per popped entry
+      const bool dense_clear = static_cast<int64_t>(nq) * 8 > a.words;
+      if (dense_clear)
+        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.words;
+             i += int64_t(gridDim.x) * blockDim.x)
+          pop_bits[i] = 0u;
+      relax(qc, nq, a.nl ? 1 : 0, dense_clear ? nullptr : pop_bits, push_bits, nrel);
       nearq.flush();
       bucq.flush(a.bq, a.cap, a.bcnt, a.nb);
       if (nrel) atomicAdd(a.relax, nrel);
@@ -576,14 +587,22 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp_b(SsspBArgs<D, E> a) {
     if (a.nl) {
       unsigned long long nrel = 0;
       int32_t* win = s_settle[threadIdx.x >> 5];
-      for (int64_t base = gwarp * 32; base < a.n; base += nwarps * 32) {
-        const int64_t v = base + lane;
-        const bool in = v < a.n && bucket_of<D>(*(volatile D*)&a.dist[v], a.delta) == k &&
-                        *(volatile D*)&a.dist[v] != DistTraits<D>::inf();
-        const unsigned m = __ballot_sync(kFullW, in);
-        if (in) win[__popc(m & ((1u << lane) - 1))] = static_cast<int32_t>(v);
+      for (int64_t base = gwarp * 128; base < a.n; base += nwarps * 128) {
+        D dv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // 4 independent coalesced loads in flight
+          const int64_t v = base + 32 * j + lane;
+          dv[j] = v < a.n ? __ldcg(&a.dist[v]) : DistTraits<D>::inf();
+        }
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool in = dv[j] != DistTraits<D>::inf() && bucket_of<D>(dv[j], a.delta) == k;
+          const unsigned m = __ballot_sync(kFullW, in);
+          if (in) win[c + __popc(m & ((1u << lane) - 1))] = static_cast<int32_t>(base + 32 * j + lane);
+          c += __popc(m);
+        }
         __syncwarp();
-        const int c = __popc(m);
         if (c) relax_local(win, c, nrel);
         __syncwarp();
       }
@@ -1060,6 +1079,7 @@ void sssp_run(gbx_graph* g, uint64_t source, double delta, double* out) {
   GBX_CUDA(cudaMemcpyAsync(&rel, P.relax.p, 8, cudaMemcpyDeviceToHost, s));
   GBX_CUDA(cudaStreamSynchronize(s));
   g->stats = gbx_stats{};
+  g->pending_iters = nullptr;
   g->stats.launches = 2 + (out ? 1 : 0);
   g->stats.hot_launches = 1;
   g->stats.iterations = hctl[4];

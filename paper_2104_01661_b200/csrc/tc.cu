@@ -524,6 +524,7 @@ uint64_t tc_run(gbx_graph* g, int64_t rb, int64_t re) {
   if (re < 0 || re > P.n) re = P.n;
   if (rb < 0) rb = 0;
   g->stats = gbx_stats{};
+  g->pending_iters = nullptr;
   if (re <= rb) return 0;
   int64_t ib = 0, ie = P.nitems;
   if (rb > 0 || re < P.n) {
