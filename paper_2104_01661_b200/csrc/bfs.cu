@@ -33,7 +33,10 @@ namespace gbx {
 
 constexpr int kBfsThreads = 256;
 constexpr int kBfsBuf = 256;  // staged frontier vertices per warp
-constexpr int64_t kChunk = 256;  // push: edges per warp entry (latency-bound steps)
+#ifndef GBX_BFS_CHUNK
+#define GBX_BFS_CHUNK 256
+#endif
+constexpr int64_t kChunk = GBX_BFS_CHUNK;  // push: edges per warp entry (latency-bound steps)
 constexpr unsigned kFull = 0xffffffffu;
 // In-degree above which a pull row goes to a whole warp instead of 8 lanes.
 constexpr int64_t kBfsHeavy = 256;
@@ -76,6 +79,7 @@ struct Bfs1Args {
              // [5] levels done [6] push levels [8:10) u64 frontier edges [10:12) next
              // [12] unvisited-list size (-1: not built) [13] next size [14] list parity
   unsigned long long* tlog;  // optional: %globaltimer at phase boundaries (debug)
+  int32_t source;
 };
 
 __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
@@ -96,6 +100,33 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
   const int64_t nwords = (a.n + 31) >> 5;
   unsigned long long* edges = reinterpret_cast<unsigned long long*>(a.ctl + 8);
   if (a.tlog && gtid == 0) a.tlog[0] = gtimer();
+  {
+    // initial state, inside the persistent kernel (no init / seed launches):
+    // every vertex unreached except the source, empty bitmaps but the
+    // source's bit, and the source's level-1 queue entries (bfs.cpp:18-55)
+    const int32_t src = a.source;
+    for (int64_t i = gtid; i < a.n || i < nwords; i += gsize) {
+      if (i < a.n) {
+        a.level[i] = i == src ? 0 : -1;
+        a.parent[i] = i == src ? src : INT_MAX;
+      }
+      if (i < nwords) {
+        a.bm0[i] = i == (src >> 5) ? 1u << (src & 31) : 0u;
+        a.bm1[i] = 0u;
+      }
+    }
+    if (gtid == 0) {
+      const int64_t deg = a.rp[src + 1] - a.rp[src];
+      const int k = n_chunks(deg);
+      for (int c = 0; c < k; ++c) a.q0[c] = (static_cast<int64_t>(c) << 32) | src;
+      for (int i = 0; i < 16; ++i) a.ctl[i] = 0;
+      a.ctl[0] = k;
+      a.ctl[1] = 1;
+      *reinterpret_cast<unsigned long long*>(a.ctl + 8) = static_cast<unsigned long long>(deg);
+      a.ctl[12] = -1;
+    }
+    grid.sync();
+  }
   for (int d = 1; static_cast<int64_t>(d) + 1 <= a.n; ++d) {
     const int qe = *(volatile int*)&a.ctl[0];
     const int qv = *(volatile int*)&a.ctl[1];
@@ -299,28 +330,6 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
   if (a.tlog && gtid == 0) a.tlog[1] = gtimer();
 }
 
-__global__ void k_bfs1_init(int32_t* level, int32_t* parent, uint32_t* bm0, uint32_t* bm1,
-                            int64_t n) {
-  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < n) { level[i] = -1; parent[i] = INT_MAX; }
-  if (i < (n + 31) / 32) { bm0[i] = 0; bm1[i] = 0; }
-}
-
-__global__ void k_bfs1_seed(int32_t* level, int32_t* parent, uint32_t* bm0, int64_t* q0,
-                            int* ctl, const int64_t* rp, int32_t s) {
-  level[s] = 0;
-  parent[s] = s;
-  bm0[s >> 5] |= 1u << (s & 31);
-  int64_t deg = rp[s + 1] - rp[s];
-  int k = n_chunks(deg);
-  for (int c = 0; c < k; ++c) q0[c] = (static_cast<int64_t>(c) << 32) | s;
-  for (int i = 0; i < 16; ++i) ctl[i] = 0;
-  ctl[0] = k;
-  ctl[1] = 1;
-  *reinterpret_cast<unsigned long long*>(ctl + 8) = static_cast<unsigned long long>(deg);
-  ctl[12] = -1;
-}
-
 __global__ void k_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, int32_t none) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i < n) out[i] = in[i] == none ? -1 : in[i];
@@ -421,15 +430,10 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
     for (auto& e : ev) GBX_CUDA(cudaEventCreate(&e));
     GBX_CUDA(cudaEventRecord(ev[0], s));
   }
-  k_bfs1_init<<<ceil_div(n, 256), 256, 0, s>>>(W.level.p, W.parent.p, W.bitmap[0].p,
-                                                 W.bitmap[1].p, n);
-  GBX_LAUNCHED();
   int64_t* q0 = reinterpret_cast<int64_t*>(W.queue[0].p);
   int64_t* q1 = reinterpret_cast<int64_t*>(W.queue[1].p);
-  k_bfs1_seed<<<1, 1, 0, s>>>(W.level.p, W.parent.p, W.bitmap[0].p, q0, W.ctl.p, A.rp.p,
-                              static_cast<int32_t>(source));
-  GBX_LAUNCHED();
   Bfs1Args a{};
+  a.source = static_cast<int32_t>(source);
   a.rp = A.rp.p;
   a.col = A.col.p;
   a.trp = AT ? AT->rp.p : nullptr;
@@ -460,14 +464,12 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
   static int grid = 0;
   if (!grid) grid = coop_grid(reinterpret_cast<const void*>(k_bfs1), kBfsThreads);
   void* args[] = {&a};
-  if (n > 1) {
-    GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_bfs1), dim3(grid),
-                                         dim3(kBfsThreads), args, 0, s));
-  }
+  GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_bfs1), dim3(grid),
+                                       dim3(kBfsThreads), args, 0, s));
   if (tlog_on) GBX_CUDA(cudaEventRecord(ev[2], s));
   g->stats = gbx_stats{};
   g->pending_iters = nullptr;
-  g->stats.launches = 3 + (parent ? 1 : 0) + (level ? 1 : 0);
+  g->stats.launches = 1 + (parent ? 1 : 0) + (level ? 1 : 0);
   g->stats.hot_launches = 1;
   if (!parent && !level && !tlog_on) {
     // device-resident result (gbx_result_device): the call stays asynchronous
@@ -521,6 +523,10 @@ struct Bfs64Args {
 };
 
 
+// k_bfs64 control words: triple-buffered queue counters (entries, vertices,
+// frontier edges as u64 at ctl + 8), levels done, push levels
+constexpr int kB64Ent = 0, kB64Vtx = 3, kB64Levels = 6, kB64Push = 7, kB64Words = 16;
+
 __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ int32_t s_buf[kBfsThreads / 32][kBfsBuf];
@@ -531,11 +537,21 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  // level d pops the queue counted in buffer d%3 and pushes into (d+1)%3;
+  // buffer (d+2)%3 -- last read during level d-1, before its closing barrier
+  // -- is zeroed by the leader for level d+1: two grid barriers per level
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   for (int d = 1; static_cast<int64_t>(d) + 1 <= a.n; ++d) {
-    const int qe = *(volatile int*)&a.ctl[0];
-    const int qv = *(volatile int*)&a.ctl[1];
-    const unsigned long long fe = *(volatile unsigned long long*)&a.edges[0];
+    const int bc = d % 3, bn = (d + 1) % 3, bz = (d + 2) % 3;
+    const int qe = *(volatile int*)&a.ctl[kB64Ent + bc];
+    const int qv = *(volatile int*)&a.ctl[kB64Vtx + bc];
+    const unsigned long long fe = *(volatile unsigned long long*)&a.edges[bc];
     if (qv == 0) break;
+    if (leader) {
+      a.ctl[kB64Ent + bz] = 0;
+      a.ctl[kB64Vtx + bz] = 0;
+      a.edges[bz] = 0ull;
+    }
     // 64 lanes rarely satisfy every source bit early in a pull (and hub rows
     // straggle in one group), so push until the frontier edges reach nnz/2
     const bool push = fe * static_cast<unsigned long long>(a.pull_div) <
@@ -549,7 +565,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
     int64_t* qn = p ? a.q0 : a.q1;
     unsigned long long* fc = p ? a.f1 : a.f0;
     unsigned long long* fn = p ? a.f0 : a.f1;
-    fq.reset(qn, &a.ctl[2], &a.ctl[3], &a.edges[1], nullptr);
+    fq.reset(qn, &a.ctl[kB64Ent + bn], &a.ctl[kB64Vtx + bn], &a.edges[bn], nullptr);
     if (push) {
       for (int64_t e = gwarp; e < qe; e += nwarps) {
         const int64_t ent = qc[e];
@@ -667,36 +683,28 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
     fq.flush();
     grid.sync();
     if (a.tlog && blockIdx.x == 0 && threadIdx.x == 0) a.tlog[4 * d + 1] = gtimer();
-    // finalize: new frontier bits become seen + level d; old frontier cleared
-    const int qn_e = *(volatile int*)&a.ctl[2];
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < qn_e;
-         e += int64_t(gridDim.x) * blockDim.x) {
+    // finalize: new frontier bits become seen + level d (a warp per vertex,
+    // lanes b and b+32 write the vertex's 256-byte level row coalesced); the
+    // old frontier words are cleared
+    const int qn_e = *(volatile int*)&a.ctl[kB64Ent + bn];
+    for (int64_t e = gwarp; e < qn_e; e += nwarps) {
       const int64_t ent = qn[e];
       if ((ent >> 32) != 0) continue;
       const int32_t w = static_cast<int32_t>(ent & 0xffffffff);
-      unsigned long long nb = fn[w];
-      a.seen[w] |= nb;
-      while (nb) {
-        int b = __ffsll(static_cast<long long>(nb)) - 1;
-        nb &= nb - 1;
-        a.mlevel[static_cast<int64_t>(w) * 64 + b] = d;
-      }
+      const unsigned long long nb = fn[w];
+      if (lane == 0) a.seen[w] |= nb;
+      int32_t* lv = a.mlevel + static_cast<int64_t>(w) * 64;
+      if ((nb >> lane) & 1ull) lv[lane] = d;
+      if ((nb >> (lane + 32)) & 1ull) lv[lane + 32] = d;
     }
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < qe;
          e += int64_t(gridDim.x) * blockDim.x) {
       const int64_t ent = qc[e];
       if ((ent >> 32) == 0) fc[static_cast<int32_t>(ent & 0xffffffff)] = 0ull;
     }
-    grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      a.ctl[0] = a.ctl[2];
-      a.ctl[1] = a.ctl[3];
-      a.ctl[2] = 0;
-      a.ctl[3] = 0;
-      a.ctl[5] = d;
-      if (push) a.ctl[6] += 1;
-      a.edges[0] = a.edges[1];
-      a.edges[1] = 0ull;
+    if (leader) {
+      a.ctl[kB64Levels] = d;
+      if (push) a.ctl[kB64Push] += 1;
       if (a.tlog) a.tlog[4 * d + 2] = gtimer();
     }
     grid.sync();
@@ -712,7 +720,7 @@ __global__ void k_bfs64_init(unsigned long long* seen, unsigned long long* f0,
 }
 
 // One warp per distinct source: set its lane bits, then emit its degree chunks
-// into the level-1 queue (ctl[0] entries, ctl[1] vertices, edges[0] edges).
+// into the level-1 queue (counter buffer 1: entries, vertices, frontier edges).
 // src[0..ns) are the batch lanes, src[ns..ns+nu) the distinct sources.
 __global__ void k_bfs64_seed(const int32_t* src, int ns, int nu, const int64_t* rp,
                              unsigned long long* seen, unsigned long long* f0, int32_t* mlevel,
@@ -736,9 +744,9 @@ __global__ void k_bfs64_seed(const int32_t* src, int ns, int nu, const int64_t* 
   const int64_t k = deg <= kChunk ? 1 : (deg + kChunk - 1) / kChunk;
   int base = 0;
   if (lane == 0) {
-    base = atomicAdd(&ctl[0], static_cast<int>(k));
-    atomicAdd(&ctl[1], 1);
-    atomicAdd(edges, static_cast<unsigned long long>(deg));
+    base = atomicAdd(&ctl[kB64Ent + 1], static_cast<int>(k));  // level 1 pops buffer 1
+    atomicAdd(&ctl[kB64Vtx + 1], 1);
+    atomicAdd(edges + 1, static_cast<unsigned long long>(deg));
   }
   base = __shfl_sync(0xffffffffu, base, 0);
   for (int64_t c = lane; c < k; c += 32) q[base + c] = (c << 32) | v;
@@ -776,7 +784,7 @@ static void ensure_bfs64(gbx_graph* g) {
   const int64_t qcap = n + g->A.nnz / kChunk + 64;
   W.mqueue[0].alloc(2 * qcap);
   W.mqueue[1].alloc(2 * qcap);
-  W.mctl.alloc(12);
+  W.mctl.alloc(kB64Words);
   W.msrc.alloc(128);
 }
 
@@ -813,7 +821,7 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
     src.insert(src.end(), uniq.begin(), uniq.end());
     int64_t* q0 = reinterpret_cast<int64_t*>(W.mqueue[0].p);
     int64_t* q1 = reinterpret_cast<int64_t*>(W.mqueue[1].p);
-    GBX_CUDA(cudaMemsetAsync(W.mctl.p, 0, 12 * sizeof(int), s));
+    GBX_CUDA(cudaMemsetAsync(W.mctl.p, 0, kB64Words * sizeof(int), s));
     GBX_CUDA(cudaMemcpyAsync(W.msrc.p, src.data(), src.size() * sizeof(int32_t),
                              cudaMemcpyHostToDevice, s));
     k_bfs64_seed<<<nu, 32, 0, s>>>(W.msrc.p, nb, nu, A.rp.p, W.seen.p, W.front.p, W.mlevel.p,
@@ -872,10 +880,10 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
       }
       cudaFreeAsync(tmp, s);
     }
-    int hctl[12];
+    int hctl[kB64Words];
     GBX_CUDA(cudaMemcpyAsync(hctl, W.mctl.p, sizeof hctl, cudaMemcpyDeviceToHost, s));
     GBX_CUDA(cudaStreamSynchronize(s));
-    g->stats.iterations = hctl[5];
+    g->stats.iterations = hctl[kB64Levels];
     if (tlog_on) dump_tlog(W, "bfs64");
   }
   g->stats.launches = total_launches;
