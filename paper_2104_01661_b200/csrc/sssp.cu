@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -336,6 +337,7 @@ struct SsspBArgs {
   const int32_t* nl;
   int32_t* sq;
   uint32_t* sbits;
+  int light_group;     // lanes per vertex in the light (near) phase: 1, 2 or 4
   int trace;
   unsigned long long* tlog;  // optional: [2i] %globaltimer, [2i+1] kind<<32 | size (debug)
   int tlog_cap;
@@ -432,14 +434,17 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
   // per vertex (8 vertices per warp), each lane 4 edges per round: 4
   // independent edge -> dist -> atomicMin chains.  pop_bits: the list's
   // membership bitmap, released as entries are taken.
-  auto relax = [&](const int32_t* list, int cnt, int phase, uint32_t* pop_bits,
+  auto relax = [&](auto gsz, const int32_t* list, int cnt, int phase, uint32_t* pop_bits,
                    uint32_t* push_bits, unsigned long long& nrel) {
-    for (int64_t base = gwarp * 8; base < cnt; base += nwarps * 8) {
-      const int64_t qi = base + g4;
+    constexpr int G = decltype(gsz)::value;  // lanes per vertex
+    constexpr int VPW = 32 / G;              // vertices per warp step
+    const int gi = lane / G, si = lane % G;
+    for (int64_t base = gwarp * VPW; base < cnt; base += nwarps * VPW) {
+      const int64_t qi = base + gi;
       bool active = qi < cnt;
       const int32_t u = active ? list[qi] : 0;
       const uint32_t ubit = 1u << (u & 31);
-      if (active && s4 == 0 && pop_bits) atomicAnd(&pop_bits[u >> 5], ~ubit);
+      if (active && si == 0 && pop_bits) atomicAnd(&pop_bits[u >> 5], ~ubit);
       int64_t p = active ? a.rp[u] : 0;
       int64_t e = active ? a.rp[u + 1] : 0;
       if (active && phase == 1) e = p + a.nl[u];
@@ -452,7 +457,7 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
         bool ok[4];
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          const int64_t q = p + s4 + 4 * q4;
+          const int64_t q = p + si + G * q4;
           ok[q4] = active && q < e;
           W w = W(0);
           v[q4] = 0;
@@ -486,7 +491,7 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
           bucq.push(buck_push, v[q4], bidx, a.bq, a.cap, a.bcnt, a.nb);
         }
         if (active) {
-          p += 16;
+          p += 4 * G;
           if (p >= e) active = false;
         }
       }
@@ -572,7 +577,11 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
         for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.words;
              i += int64_t(gridDim.x) * blockDim.x)
           pop_bits[i] = 0u;
-      relax(qc, nq, a.nl ? 1 : 0, dense_clear ? nullptr : pop_bits, push_bits, nrel);
+      uint32_t* pb = dense_clear ? nullptr : pop_bits;
+      if (!a.nl) relax(std::integral_constant<int, 4>{}, qc, nq, 0, pb, push_bits, nrel);
+      else if (a.light_group == 1) relax(std::integral_constant<int, 1>{}, qc, nq, 1, pb, push_bits, nrel);
+      else if (a.light_group == 2) relax(std::integral_constant<int, 2>{}, qc, nq, 1, pb, push_bits, nrel);
+      else relax(std::integral_constant<int, 4>{}, qc, nq, 1, pb, push_bits, nrel);
       nearq.flush();
       bucq.flush(a.bq, a.cap, a.bcnt, a.nb);
       if (nrel) atomicAdd(a.relax, nrel);
@@ -968,6 +977,8 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     b.ctl = a.ctl;
     b.relax = a.relax;
     if (split) {
+      static const int lg = std::getenv("GBX_SSSP_LG") ? std::atoi(std::getenv("GBX_SSSP_LG")) : 2;
+      b.light_group = lg;
       b.nl = P.nlight.p;
       b.sq = P.sq.p;
       b.sbits = P.sbits.p;
