@@ -358,6 +358,35 @@ int gbx_triangle_count_rows(uint64_t* count, const gbx_graph* g, int64_t row_beg
 /* Wedge-balanced split of the oriented rows into parts. */
 int gbx_tc_partition(int64_t* bounds, gbx_graph* g, int parts, char msg[GBX_MSG_LEN]);
 
+/* ---- row-partitioned batched Brandes for the multi-GPU driver --------------
+ * betweenness.cpp:11-86 over 1D row blocks (one exchange per BFS
+ * level).  Every rank holds the graph (AT cached) and calls, in lockstep:
+ *   gbx_bc_shard_begin          owned rows [row_begin, row_end) (nnz-balanced),
+ *                               replicated initial state for <= 4 sources;
+ *   repeat: gbx_bc_shard_forward -> device records of the owned vertices this
+ *           depth settled (40 bytes each: int32 v, uint32 lanes, fp64 sigma[4]);
+ *           the driver all-gathers every rank's records in rank order;
+ *           gbx_bc_shard_forward_apply(all records) -> *done once a depth is empty;
+ *   repeat: gbx_bc_shard_backward -> records (int32 v, pad, fp64 coef[4]) of the
+ *           owned vertices of the next depth, *done after depth 1;
+ *           gbx_bc_shard_backward_apply(all records);
+ *   gbx_bc_shard_centrality     device fp64[n]: this rank's partial (zero off its
+ *                               rows); the sum over ranks (all-reduce) equals
+ *                               gbx_betweenness (to the rounding of the hub rows'
+ *                               fp64 atomics, which both runs share).
+ * Record pointers are device memory owned by the handle (valid until the next
+ * protocol call); applied record buffers are the caller's device memory. */
+int gbx_bc_shard_begin(gbx_graph* g, const uint64_t* sources, uint64_t ns, int rank, int nranks,
+                       int64_t* row_begin, int64_t* row_end, char msg[GBX_MSG_LEN]);
+int gbx_bc_shard_forward(gbx_graph* g, void** recs_dev, int64_t* nrecs, char msg[GBX_MSG_LEN]);
+int gbx_bc_shard_forward_apply(gbx_graph* g, const void* recs_dev, int64_t nrecs, int* done,
+                               char msg[GBX_MSG_LEN]);
+int gbx_bc_shard_backward(gbx_graph* g, void** recs_dev, int64_t* nrecs, int* done,
+                          char msg[GBX_MSG_LEN]);
+int gbx_bc_shard_backward_apply(gbx_graph* g, const void* recs_dev, int64_t nrecs,
+                                char msg[GBX_MSG_LEN]);
+int gbx_bc_shard_centrality(gbx_graph* g, double** cent_dev, char msg[GBX_MSG_LEN]);
+
 #ifdef __cplusplus
 }
 #endif

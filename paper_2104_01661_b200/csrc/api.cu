@@ -728,6 +728,61 @@ int gbx_last_stats(const gbx_graph* gc, gbx_stats* stats, char* msg) {
   });
 }
 
+int gbx_bc_shard_begin(gbx_graph* g, const uint64_t* sources, uint64_t ns, int rank, int nranks,
+                       int64_t* row_begin, int64_t* row_end, char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    if (!sources && ns) gbx::fail(GBX_NULL_ARGUMENT, "sources is NULL");
+    gbx::Scope sc(g);
+    gbx::bc_shard_begin(g, sources, ns, rank, nranks, row_begin, row_end);
+  });
+}
+
+int gbx_bc_shard_forward(gbx_graph* g, void** recs, int64_t* nrecs, char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    if (!recs || !nrecs) gbx::fail(GBX_NULL_ARGUMENT, "output pointers are NULL");
+    gbx::Scope sc(g);
+    gbx::bc_shard_forward(g, recs, nrecs);
+  });
+}
+
+int gbx_bc_shard_forward_apply(gbx_graph* g, const void* recs, int64_t nrecs, int* done, char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    if (!recs && nrecs) gbx::fail(GBX_NULL_ARGUMENT, "records are NULL");
+    gbx::Scope sc(g);
+    gbx::bc_shard_forward_apply(g, recs, nrecs, done);
+  });
+}
+
+int gbx_bc_shard_backward(gbx_graph* g, void** recs, int64_t* nrecs, int* done, char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    if (!recs || !nrecs || !done) gbx::fail(GBX_NULL_ARGUMENT, "output pointers are NULL");
+    gbx::Scope sc(g);
+    gbx::bc_shard_backward(g, recs, nrecs, done);
+  });
+}
+
+int gbx_bc_shard_backward_apply(gbx_graph* g, const void* recs, int64_t nrecs, char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    if (!recs && nrecs) gbx::fail(GBX_NULL_ARGUMENT, "records are NULL");
+    gbx::Scope sc(g);
+    gbx::bc_shard_backward_apply(g, recs, nrecs);
+  });
+}
+
+int gbx_bc_shard_centrality(gbx_graph* g, double** cent, char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    if (!cent) gbx::fail(GBX_NULL_ARGUMENT, "output pointer is NULL");
+    gbx::Scope sc(g);
+    gbx::bc_shard_centrality(g, cent);
+  });
+}
+
 int gbx_pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* row_begin,
                          int64_t* row_end, char* msg) {
   return guard(msg, [&] {

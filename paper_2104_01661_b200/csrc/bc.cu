@@ -94,6 +94,13 @@ __device__ __forceinline__ int32_t ld_col(const int32_t* p) {
   return v;
 }
 
+// val[v][0..3] (32 bytes, sector-aligned) in one 256-bit read-only load
+__device__ __forceinline__ void ld_sector(const double* p, double x[4]) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
+      : "l"(p));
+}
+
 // s[b] += val[u][b] over the row entries p, p+st, ... < e whose map nibble is
 // in m; U independent column loads, then U map gathers, per step (the chain
 // col -> map -> val is latency-bound, so each lane keeps U in flight)
@@ -111,10 +118,12 @@ __device__ __forceinline__ void row_sum(const int32_t* col, int64_t p, int64_t e
 #pragma unroll
     for (int k = 0; k < U; ++k)
       if (h[k]) {
-        const double* vp = val + static_cast<int64_t>(u[k]) * 4;
+        // the vertex's 4 lanes are one 32-byte sector: one 256-bit load
+        double x[4];
+        ld_sector(val + static_cast<int64_t>(u[k]) * 4, x);
 #pragma unroll
         for (int b = 0; b < 4; ++b)
-          if ((h[k] >> b) & 1u) s[b] += __ldg(vp + b);
+          if ((h[k] >> b) & 1u) s[b] += x[b];
       }
   }
 }
@@ -189,6 +198,7 @@ struct BcArgs {
   unsigned long long* edges;  // frontier edges of the level being built
   int d;
   unsigned lanes;  // lanes still live (their previous level was non-empty)
+  int64_t own0, own1;  // vertices this rank finalises (sharded BC; else [0, n))
 };
 
 // forward push over A from the entries of level d-1
@@ -502,6 +512,7 @@ __global__ void k_bc_back_hub_fin(BcArgs a) {
   const int64_t slot = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (slot >= a.nhv) return;
   const int64_t u = a.hv[slot];
+  if (u < a.own0 || u >= a.own1) return;  // another rank's hub
   const unsigned m = lanes_on(a.lv8[u], a.d, a.lanes, a.level, u);
   double c = 0.0;
 #pragma unroll
@@ -653,16 +664,13 @@ static void build_hubs(cudaStream_t s, const Csr& M, BcHubs& H) {
   H.nnz = M.nnz;
 }
 
-void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrality) {
-  const int64_t n = g->A.n;
-  for (uint64_t b = 0; b < ns; ++b)
-    if (sources[b] >= static_cast<uint64_t>(n))
-      fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(sources[b]));
+// per-graph BC workspaces (allocated once per vertex count)
+static BcWork& ensure_work(gbx_graph* g) {
   if (!g->bc) g->bc = std::make_unique<BcWork>();
   BcWork& W = *g->bc;
   cudaStream_t s = g->stream;
   const Csr& A = g->A;
-  const Csr& AT = g->AT();
+  const int64_t n = A.n;
   const int64_t n1 = std::max<int64_t>(n, 1);
   const int64_t ecap = n + A.nnz / kBcChunk + 64;
   if (W.n != n || !W.level.p) {
@@ -696,6 +704,19 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     W.btemp.alloc(tb + 256);
     W.allbin_key = nullptr;
   }
+  return W;
+}
+
+void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrality) {
+  const int64_t n = g->A.n;
+  for (uint64_t b = 0; b < ns; ++b)
+    if (sources[b] >= static_cast<uint64_t>(n))
+      fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(sources[b]));
+  BcWork& W = ensure_work(g);
+  cudaStream_t s = g->stream;
+  const Csr& A = g->A;
+  const Csr& AT = g->AT();
+  const int64_t n1 = std::max<int64_t>(n, 1);
   const size_t map_bytes = (n1 / 8 + 1) * sizeof(uint32_t);
   build_hubs(s, A, W.hub_a);
   const bool same = &AT == &A;
@@ -740,6 +761,8 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       if (off.back() == off[off.size() - 2]) break;
       GBX_CUDA(cudaMemsetAsync(W.ctl.p, 0, sizeof hc, s));
       BcArgs a{};
+      a.own0 = 0;
+      a.own1 = n;
       a.rp = A.rp.p;
       a.col = A.col.p;
       a.trp = AT.rp.p;
@@ -826,6 +849,8 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       const int nl = static_cast<int>(off[d + 1] - off[d]);
       if (nl == 0) continue;
       BcArgs a{};
+      a.own0 = 0;
+      a.own1 = n;
       a.rp = A.rp.p;
       a.col = A.col.p;
       a.n = n;
@@ -871,6 +896,439 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
   g->stats.launches = launches;
   g->stats.iterations = max_levels;
   g->stats.work_units = edges;
+}
+
+
+// ---------------------------------------------------------------------------
+// Row-partitioned batched Brandes for the multi-GPU driver (1D row
+// blocks, one exchange per BFS level).  Every rank holds the graph and the
+// replicated per-vertex state; rank r owns vertices [rb, re) (nnz-balanced):
+//   forward, depth d: pull over AT for the OWNED still-unreached vertices (the
+//     same k_bc_pull / hub passes, work lists restricted to owned rows); the
+//     rank packs (v, new lanes, sigma[4]) for the vertices it settled; the
+//     driver all-gathers every rank's records (rank order) and each rank
+//     applies the others' and appends all of them to the global level list
+//     -- so the level lists, maps and sigma are identical on every rank;
+//   backward, depth d: the owned part of the level-d list runs k_bc_back (and
+//     the owned hub chunks); (v, coef[4]) records are exchanged the same way;
+//   the centrality partials (owned vertices only) are summed by one
+//     all-reduce at the end (betweenness.cpp:74-79).
+// The per-vertex sums are computed by the same kernels as the single-GPU run
+// (push levels become pulls: path counts are integers, exact in any order),
+// so the result equals gbx_betweenness up to the rounding order of the hub
+// rows' fp64 atomics (measured: <= 1e-15 relative).
+// Record layout (40 bytes): int32 v, uint32 lanes, double x[4].
+// ---------------------------------------------------------------------------
+
+struct BcRec {
+  int32_t v;
+  uint32_t lanes;
+  double x[4];
+};
+static_assert(sizeof(BcRec) == 40, "BcRec layout");
+
+__global__ void k_bc_iota_range(int32_t* out, int64_t b, int64_t e) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (b + i < e) out[i] = static_cast<int32_t>(b + i);
+}
+
+// first row r with r + rp[r] >= target (nnz + rows balanced split)
+__global__ void k_bc_split(const int64_t* rp, int64_t n, int parts, int64_t* bounds) {
+  const int q = threadIdx.x;
+  if (q > parts) return;
+  const int64_t target = (n + rp[n]) * q / parts;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (mid + rp[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  bounds[q] = q == 0 ? 0 : q == parts ? n : lo;
+}
+
+__global__ void k_bc_own_hubs(const int64_t* hent, int nhent, const int32_t* hv, int64_t rb,
+                              int64_t re, int64_t* out, int* cnt) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= nhent) return;
+  const int64_t ent = hent[e];
+  const int32_t v = hv[static_cast<int>(ent & 0xffffffff)];
+  if (v >= rb && v < re) out[atomicAdd(cnt, 1)] = ent;
+}
+
+__global__ void k_bc_pack_fwd(const int32_t* list, int nl, int d, const int32_t* level,
+                              const double* sigma, BcRec* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= nl) return;
+  const int64_t v = list[i];
+  BcRec r;
+  r.v = static_cast<int32_t>(v);
+  r.lanes = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    if (level[v * 4 + b] == d) r.lanes |= 1u << b;
+    r.x[b] = sigma[v * 4 + b];
+  }
+  out[i] = r;
+}
+
+// apply every rank's records of depth d: others' vertices get level / lv8 /
+// sigma / map bits; all of them are appended (rank order) to the level list
+__global__ void k_bc_apply_fwd(const BcRec* recs, int64_t nrec, int d, int64_t rb, int64_t re,
+                               int32_t* level, uint32_t* lv8, double* sigma, uint32_t* map,
+                               int32_t* order_out, int* live) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  unsigned m = 0;
+  if (i < nrec) {
+    const BcRec r = recs[i];
+    const int64_t v = r.v;
+    order_out[i] = r.v;
+    m = r.lanes;
+    if (v < rb || v >= re) {
+      uint32_t x = lv8[v];
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if ((r.lanes >> b) & 1u) {
+          level[v * 4 + b] = d;
+          sigma[v * 4 + b] = r.x[b];
+          x = (x & ~(0xFFu << (8 * b))) | (lv8_byte(d) << (8 * b));
+        }
+      lv8[v] = x;
+      nib_or(map, v, r.lanes);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m |= __shfl_xor_sync(kAll, m, o);
+  if ((threadIdx.x & 31) == 0 && m) atomicOr(live, static_cast<int>(m));
+}
+
+__global__ void k_bc_own_filter(const int32_t* list, int64_t nl, int64_t rb, int64_t re,
+                                int32_t* out, int* cnt) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= nl) return;
+  const int32_t v = list[i];
+  if (v >= rb && v < re) out[atomicAdd(cnt, 1)] = v;
+}
+
+__global__ void k_bc_pack_back(const int32_t* list, int nl, const double* coef, BcRec* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= nl) return;
+  const int64_t v = list[i];
+  BcRec r;
+  r.v = static_cast<int32_t>(v);
+  r.lanes = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) r.x[b] = coef[v * 4 + b];
+  out[i] = r;
+}
+
+__global__ void k_bc_apply_back(const BcRec* recs, int64_t nrec, int d, int64_t rb, int64_t re,
+                                const int32_t* level, double* coef) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= nrec) return;
+  const BcRec r = recs[i];
+  const int64_t v = r.v;
+  if (v >= rb && v < re) return;
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (level[v * 4 + b] == d) coef[v * 4 + b] = r.x[b];
+}
+
+static BcShard& need_shard(gbx_graph* g) {
+  if (!g->bc || !g->bc->shard) fail(GBX_MISSING_PROPERTY, "bc shard protocol needs gbx_bc_shard_begin");
+  return *g->bc->shard;
+}
+
+void bc_shard_begin(gbx_graph* g, const uint64_t* sources, uint64_t ns, int rank, int nranks,
+                    int64_t* rb_out, int64_t* re_out) {
+  require_at(g, "bc_shard");
+  const int64_t n = g->A.n;
+  if (ns == 0) fail(GBX_EMPTY_BATCH, "empty source batch");
+  if (ns > static_cast<uint64_t>(kBcLanes))
+    fail(GBX_INVALID_VALUE, "bc_shard: one batch of at most 4 sources per protocol run");
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(GBX_INVALID_VALUE, "bc_shard: bad rank / nranks");
+  for (uint64_t b = 0; b < ns; ++b)
+    if (sources[b] >= static_cast<uint64_t>(n))
+      fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(sources[b]));
+  BcWork& W = ensure_work(g);
+  cudaStream_t s = g->stream;
+  const Csr& A = g->A;
+  const Csr& AT = g->AT();
+  const int64_t n1 = std::max<int64_t>(n, 1);
+  auto S = std::make_unique<BcShard>();
+  S->rank = rank;
+  S->nranks = nranks;
+  S->ns = static_cast<int>(ns);
+  {
+    DevArray<int64_t> bnd(nranks + 1);
+    k_bc_split<<<1, std::max(32, ((nranks + 32) / 32) * 32), 0, s>>>(A.rp.p, n, nranks, bnd.p);
+    GBX_LAUNCHED();
+    std::vector<int64_t> hb(nranks + 1);
+    GBX_CUDA(cudaMemcpyAsync(hb.data(), bnd.p, (nranks + 1) * 8, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+    S->rb = hb[rank];
+    S->re = std::max(hb[rank], hb[rank + 1]);
+  }
+  // hub rows and the owned chunks of them
+  build_hubs(s, A, W.hub_a);
+  const bool same = &AT == &A;
+  if (!same) build_hubs(s, AT, W.hub_t);
+  BcHubs& HT = same ? W.hub_a : W.hub_t;
+  DevArray<int> c(2);
+  GBX_CUDA(cudaMemsetAsync(c.p, 0, 2 * sizeof(int), s));
+  S->hent_a.alloc(std::max(W.hub_a.nhent, 1));
+  S->hent_t.alloc(std::max(HT.nhent, 1));
+  if (W.hub_a.nhent)
+    k_bc_own_hubs<<<ceil_div(W.hub_a.nhent, 256), 256, 0, s>>>(W.hub_a.hent.p, W.hub_a.nhent,
+                                                               W.hub_a.hv.p, S->rb, S->re,
+                                                               S->hent_a.p, c.p);
+  if (HT.nhent)
+    k_bc_own_hubs<<<ceil_div(HT.nhent, 256), 256, 0, s>>>(HT.hent.p, HT.nhent, HT.hv.p, S->rb,
+                                                          S->re, S->hent_t.p, c.p + 1);
+  GBX_LAUNCHED();
+  int hc[2];
+  GBX_CUDA(cudaMemcpyAsync(hc, c.p, sizeof hc, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  S->nhent_a = hc[0];
+  S->nhent_t = hc[1];
+  // the owned rows binned by in-degree: the first pull's work list
+  const int64_t own = S->re - S->rb;
+  S->ownbin.alloc(std::max<int64_t>(own, 1));
+  S->owncnt.alloc(4);
+  S->snew.alloc(n1);
+  S->slist.alloc(n1);
+  S->scnt.alloc(4);
+  S->recs.alloc(n1 * sizeof(BcRec));
+  {
+    DevArray<int32_t> ids(std::max<int64_t>(own, 1));
+    if (own) {
+      k_bc_iota_range<<<ceil_div(own, 256), 256, 0, s>>>(ids.p, S->rb, S->re);
+      GBX_LAUNCHED();
+    }
+    bin_list(s, W, ids.p, own, AT, S->ownbin.p, S->owncnt.p);
+    GBX_CUDA(cudaStreamSynchronize(s));
+  }
+  // replicated initial state (betweenness.cpp:27-35)
+  int32_t hs[4];
+  for (uint64_t b = 0; b < ns; ++b) hs[b] = static_cast<int32_t>(sources[b]);
+  GBX_CUDA(cudaMemcpyAsync(W.src.p, hs, ns * 4, cudaMemcpyHostToDevice, s));
+  const size_t map_bytes = (n1 / 8 + 1) * sizeof(uint32_t);
+  k_bc_init<<<ceil_div(n1 * 4, 256), 256, 0, s>>>(W.level.p, W.lv8.p, W.sigma.p, W.mark.p, n);
+  GBX_CUDA(cudaMemsetAsync(W.map[0].p, 0, map_bytes, s));
+  GBX_CUDA(cudaMemsetAsync(W.map[1].p, 0, map_bytes, s));
+  GBX_CUDA(cudaMemsetAsync(W.cent.p, 0, n1 * 8, s));
+  k_bc_seed<<<1, 1, 0, s>>>(W.src.p, static_cast<int>(ns), W.level.p, W.lv8.p, W.sigma.p, W.mark.p,
+                            W.order.p, W.ent[0].p, W.ctl.p,
+                            reinterpret_cast<unsigned long long*>(W.ctl.p + 4), A.rp.p, W.map[0].p);
+  GBX_LAUNCHED();
+  int hseed[4];
+  GBX_CUDA(cudaMemcpyAsync(hseed, W.ctl.p, sizeof hseed, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  S->off = {0, hseed[0]};
+  S->live = static_cast<unsigned>(hseed[3]);
+  S->cur = 0;
+  S->ucnt = -1;
+  W.shard = std::move(S);
+  if (rb_out) *rb_out = W.shard->rb;
+  if (re_out) *re_out = W.shard->re;
+}
+
+// one forward depth on the owned rows; *recs = device records of the owned
+// vertices it settled (valid until the next protocol call)
+void bc_shard_forward(gbx_graph* g, void** recs, int64_t* nrec) {
+  BcShard& S = need_shard(g);
+  BcWork& W = *g->bc;
+  *recs = S.recs.p;
+  *nrec = 0;
+  if (S.fwd_done) return;
+  cudaStream_t s = g->stream;
+  const Csr& A = g->A;
+  const Csr& AT = g->AT();
+  const bool same = &AT == &A;
+  BcHubs& HT = same ? W.hub_a : W.hub_t;
+  const int d = static_cast<int>(S.off.size()) - 1;
+  GBX_CUDA(cudaMemsetAsync(W.ctl.p, 0, 8 * sizeof(int), s));
+  BcArgs a{};
+  a.rp = A.rp.p;
+  a.col = A.col.p;
+  a.trp = AT.rp.p;
+  a.tcol = AT.col.p;
+  a.n = A.n;
+  a.level = W.level.p;
+  a.lv8 = W.lv8.p;
+  a.sigma = W.sigma.p;
+  a.mark = W.mark.p;
+  a.list_out = S.snew.p;
+  a.ent_out = W.ent[1].p;
+  a.cnt = W.ctl.p;
+  a.edges = reinterpret_cast<unsigned long long*>(W.ctl.p + 4);
+  a.d = d;
+  a.lanes = S.live;
+  a.map_in = W.map[S.cur].p;
+  a.map_out = W.map[S.cur ^ 1].p;
+  a.own0 = S.rb;
+  a.own1 = S.re;
+  if (S.ucnt < 0) {
+    a.bins = BcBins{S.ownbin.p, S.owncnt.p};
+  } else {
+    bin_list(s, W, W.ulist[0].p, S.ucnt, AT, W.ulist[1].p, W.ucnt.p);
+    a.bins = BcBins{W.ulist[1].p, W.ucnt.p};
+  }
+  a.ul_out = W.ulist[0].p;
+  a.hv = HT.hv.p;
+  a.hent = S.hent_t.p;
+  a.nhv = HT.nhv;
+  a.nhent = S.nhent_t;
+  a.hacc = HT.hacc.p;
+  const int grid = device_sms() * 8;
+  k_bc_pull<<<grid, 256, 0, s>>>(a);
+  GBX_LAUNCHED();
+  if (HT.nhv) {
+    if (S.nhent_t) k_bc_pull_hub<<<grid, 256, 0, s>>>(a);
+    k_bc_pull_hub_fin<<<ceil_div(HT.nhv, 256), 256, 0, s>>>(a);
+    GBX_LAUNCHED();
+  }
+  int hc[4];
+  GBX_CUDA(cudaMemcpyAsync(hc, W.ctl.p, sizeof hc, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  S.ucnt = hc[2];
+  if (hc[0]) {
+    k_bc_pack_fwd<<<ceil_div(hc[0], 256), 256, 0, s>>>(S.snew.p, hc[0], d, W.level.p, W.sigma.p,
+                                                       reinterpret_cast<BcRec*>(S.recs.p));
+    GBX_LAUNCHED();
+    GBX_CUDA(cudaStreamSynchronize(s));
+  }
+  *nrec = hc[0];
+}
+
+// every rank's records of the depth just computed, concatenated in rank order
+void bc_shard_forward_apply(gbx_graph* g, const void* recs, int64_t nrec, int* done) {
+  BcShard& S = need_shard(g);
+  BcWork& W = *g->bc;
+  cudaStream_t s = g->stream;
+  const int64_t n1 = std::max<int64_t>(g->A.n, 1);
+  const size_t map_bytes = (n1 / 8 + 1) * sizeof(uint32_t);
+  if (S.fwd_done) { if (done) *done = 1; return; }
+  const int d = static_cast<int>(S.off.size()) - 1;
+  GBX_CUDA(cudaMemsetAsync(W.ctl.p + 3, 0, sizeof(int), s));
+  if (nrec > 0) {
+    k_bc_apply_fwd<<<ceil_div(nrec, 256), 256, 0, s>>>(
+        reinterpret_cast<const BcRec*>(recs), nrec, d, S.rb, S.re, W.level.p, W.lv8.p, W.sigma.p,
+        W.map[S.cur ^ 1].p, W.order.p + S.off.back(), W.ctl.p + 3);
+    GBX_LAUNCHED();
+  }
+  int live = 0;
+  GBX_CUDA(cudaMemcpyAsync(&live, W.ctl.p + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaMemsetAsync(W.map[S.cur].p, 0, map_bytes, s));  // depth d-1 map retired
+  GBX_CUDA(cudaStreamSynchronize(s));
+  S.off.push_back(S.off.back() + nrec);
+  S.live = static_cast<unsigned>(live);
+  S.cur ^= 1;
+  if (nrec == 0 || S.off.size() > static_cast<size_t>(g->A.n) + 1) S.fwd_done = true;
+  if (done) *done = S.fwd_done ? 1 : 0;
+}
+
+// one backward depth on the owned part of the level list; *done = 1 (and no
+// records) once depth 1 has been processed
+void bc_shard_backward(gbx_graph* g, void** recs, int64_t* nrec, int* done) {
+  BcShard& S = need_shard(g);
+  BcWork& W = *g->bc;
+  if (!S.fwd_done) fail(GBX_PRECONDITION_VIOLATED, "bc_shard_backward before the forward sweep ended");
+  cudaStream_t s = g->stream;
+  const Csr& A = g->A;
+  const int64_t n1 = std::max<int64_t>(A.n, 1);
+  const size_t map_bytes = (n1 / 8 + 1) * sizeof(uint32_t);
+  const unsigned all = (1u << S.ns) - 1;
+  const std::vector<int64_t>& off = S.off;
+  const int D = static_cast<int>(off.size()) - 1;
+  *recs = S.recs.p;
+  *nrec = 0;
+  if (S.bd < 0) {
+    // the deepest non-empty level: delta = 0, coef = 1 / sigma (replicated)
+    int deepest = D - 1;
+    while (deepest > 0 && off[deepest + 1] == off[deepest]) --deepest;
+    if (deepest >= 1) {
+      const int nl = static_cast<int>(off[deepest + 1] - off[deepest]);
+      k_bc_leaf<<<ceil_div(nl, 256), 256, 0, s>>>(W.order.p + off[deepest], nl, deepest, all,
+                                                   W.level.p, W.lv8.p, W.sigma.p, W.delta.p);
+      GBX_LAUNCHED();
+    }
+    S.bd = deepest - 1;
+  }
+  while (S.bd >= 1 && off[S.bd + 1] == off[S.bd]) --S.bd;
+  if (S.bd < 1) { *done = 1; return; }
+  *done = 0;
+  const int d = S.bd;
+  const int nl = static_cast<int>(off[d + 1] - off[d]);
+  const int nl1 = static_cast<int>(off[d + 2] - off[d + 1]);
+  GBX_CUDA(cudaMemsetAsync(W.map[0].p, 0, map_bytes, s));
+  if (nl1)
+    k_bc_map<<<ceil_div(nl1, 256), 256, 0, s>>>(W.order.p + off[d + 1], nl1, d + 1, all, W.level.p,
+                                                 W.lv8.p, W.map[0].p);
+  GBX_CUDA(cudaMemsetAsync(S.scnt.p, 0, sizeof(int), s));
+  k_bc_own_filter<<<ceil_div(nl, 256), 256, 0, s>>>(W.order.p + off[d], nl, S.rb, S.re, S.snew.p,
+                                                    S.scnt.p);
+  GBX_LAUNCHED();
+  int own = 0;
+  GBX_CUDA(cudaMemcpyAsync(&own, S.scnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  BcArgs a{};
+  a.rp = A.rp.p;
+  a.col = A.col.p;
+  a.n = A.n;
+  a.level = W.level.p;
+  a.lv8 = W.lv8.p;
+  a.sigma = W.sigma.p;
+  a.coef = W.delta.p;
+  a.cent = W.cent.p;
+  a.hv = W.hub_a.hv.p;
+  a.hent = S.hent_a.p;
+  a.nhv = W.hub_a.nhv;
+  a.nhent = S.nhent_a;
+  a.hacc = W.hub_a.hacc.p;
+  a.d = d;
+  a.lanes = all;
+  a.map_in = W.map[0].p;
+  a.own0 = S.rb;
+  a.own1 = S.re;
+  bin_list(s, W, S.snew.p, own, A, S.slist.p, S.scnt.p);
+  a.bins = BcBins{S.slist.p, S.scnt.p};
+  const int grid = device_sms() * 8;
+  if (own) {
+    k_bc_back<<<grid, 256, 0, s>>>(a);
+    GBX_LAUNCHED();
+  }
+  if (W.hub_a.nhv) {
+    if (S.nhent_a) k_bc_back_hub<<<grid, 256, 0, s>>>(a);
+    k_bc_back_hub_fin<<<ceil_div(W.hub_a.nhv, 256), 256, 0, s>>>(a);
+    GBX_LAUNCHED();
+  }
+  if (own) {
+    k_bc_pack_back<<<ceil_div(own, 256), 256, 0, s>>>(S.snew.p, own, W.delta.p,
+                                                      reinterpret_cast<BcRec*>(S.recs.p));
+    GBX_LAUNCHED();
+  }
+  GBX_CUDA(cudaStreamSynchronize(s));
+  *nrec = own;
+}
+
+void bc_shard_backward_apply(gbx_graph* g, const void* recs, int64_t nrec) {
+  BcShard& S = need_shard(g);
+  BcWork& W = *g->bc;
+  cudaStream_t s = g->stream;
+  if (S.bd < 1) return;
+  if (nrec > 0) {
+    k_bc_apply_back<<<ceil_div(nrec, 256), 256, 0, s>>>(reinterpret_cast<const BcRec*>(recs), nrec,
+                                                        S.bd, S.rb, S.re, W.level.p, W.delta.p);
+    GBX_LAUNCHED();
+  }
+  GBX_CUDA(cudaStreamSynchronize(s));
+  --S.bd;
+}
+
+// this rank's centrality partial (device, fp64, n entries; zero off its rows)
+void bc_shard_centrality(gbx_graph* g, double** cent) {
+  need_shard(g);
+  GBX_CUDA(cudaStreamSynchronize(g->stream));
+  *cent = g->bc->cent.p;
 }
 
 }  // namespace gbx

@@ -240,6 +240,13 @@ void sssp_run(gbx_graph* g, uint64_t source, double delta, double* dist);
 double sssp_default_delta(gbx_graph* g);
 void sssp_prepare(gbx_graph* g);
 void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrality);
+void bc_shard_begin(gbx_graph* g, const uint64_t* sources, uint64_t ns, int rank, int nranks,
+                    int64_t* rb_out, int64_t* re_out);
+void bc_shard_forward(gbx_graph* g, void** recs, int64_t* nrec);
+void bc_shard_forward_apply(gbx_graph* g, const void* recs, int64_t nrec, int* done);
+void bc_shard_backward(gbx_graph* g, void** recs, int64_t* nrec, int* done);
+void bc_shard_backward_apply(gbx_graph* g, const void* recs, int64_t nrec);
+void bc_shard_centrality(gbx_graph* g, double** cent);
 void cc_run(gbx_graph* g, int64_t* label, int* iters);
 void pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* rb, int64_t* re);
 void pr_shard_init(gbx_graph* g, float* x_full, float* r_local, double damping);

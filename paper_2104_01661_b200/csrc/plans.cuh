@@ -133,6 +133,29 @@ struct SsspPlan {
   DevArray<uint32_t> sbits;        // its membership bitmap
 };
 
+// Row-partitioned batched Brandes (bc.cu, sharded protocol): this rank owns
+// vertices [rb, re) -- it settles their path counts (forward pull) and their
+// dependencies (backward) -- while level / sigma / coef stay replicated and are
+// refreshed from the other ranks' records after every level.
+struct BcShard {
+  int rank = 0, nranks = 1, ns = 0;
+  int64_t rb = 0, re = 0;
+  std::vector<int64_t> off;      // global order offsets per depth
+  int cur = 0;                   // forward map parity
+  int ucnt = -1;                 // owned still-unreached list (-1: first pull)
+  unsigned live = 0;
+  bool fwd_done = false;
+  int bd = -1;                   // next backward depth (-1: not started)
+  DevArray<int32_t> ownbin;      // owned vertices binned by in-degree
+  DevArray<int> owncnt;
+  DevArray<int32_t> snew;        // owned vertices of the level at hand
+  DevArray<int32_t> slist;       // its binned copy
+  DevArray<int> scnt;
+  DevArray<unsigned char> recs;  // packed 40-byte records
+  DevArray<int64_t> hent_t, hent_a;  // chunks of the owned hub rows
+  int nhent_t = 0, nhent_a = 0;
+};
+
 // Betweenness workspaces (bc.cu).
 struct BcHubs {                // rows longer than kBcHeavy, split into chunks
   DevArray<int32_t> hv;        // slot -> vertex
@@ -166,6 +189,7 @@ struct BcWork {
   DevArray<double> cent;
   DevArray<int> ctl;
   BcHubs hub_a, hub_t;       // hub rows of A (backward) and AT (forward pull)
+  std::unique_ptr<BcShard> shard;
 };
 
 struct CcWork {

@@ -11,12 +11,18 @@ rows + nnz.  Per iteration every rank runs the fused shard step on its rows
     pagerank.cpp:65-74 does (same iteration count as the single-GPU path).
 Triangle count (config 3): U replicated, middle vertices split by probe work
 (gbx_tc_partition), one u64 all-reduce at the end.
-Betweenness (config 5): the graph replicated, the sources dealt round-robin
-over the ranks (each rank runs batched Brandes on its share), one fp64
-all-reduce of the centrality partials -- the sum over sources is the
-reference's own reduction (betweenness.cpp:74-79).  With the config's 4 sources
-at most 4 ranks have work; a row-partitioned BC (one exchange per BFS level) is
-the path past that.
+Betweenness (config 5), two drivers:
+  * sharded_betweenness_rows -- 1D row blocks: every rank owns a
+    nnz-balanced vertex block and settles only its rows' path counts (forward)
+    and dependencies (backward); after every BFS level the ranks all-gather
+    the (vertex, lanes, sigma[4] | coef[4]) records of the vertices they
+    settled, so the replicated level lists / maps / sigma / coef stay
+    identical; one fp64 all-reduce of the centrality partials at the end.
+    Scales past the config's 4 sources; equals the single GPU to rounding;
+  * sharded_betweenness -- the sources dealt round-robin (each rank runs its
+    own batched Brandes; at most #sources ranks busy) + the same all-reduce:
+    the sum over sources is the reference's own reduction
+    (betweenness.cpp:74-79).
 
 The drivers only speak to a small backend interface, so the host logic (the
 partition bookkeeping, the exchange, the convergence test) is exercised on CPU
@@ -92,6 +98,54 @@ def sharded_betweenness(backend, dist, sources):
     part = backend.bc_partial(mine)            # fp64 tensor [n] (zeros if no sources)
     dist.all_reduce(part)
     return part.cpu().numpy().copy()
+
+
+def _gather_records(dist, recs, nrec, rec_bytes=40):
+    """All-gather variable-length record buffers (uint8 tensors of nrec *
+    rec_bytes bytes) in rank order; returns (concatenated tensor, total)."""
+    import torch
+    world = dist.get_world_size()
+    dev = recs.device
+    cnt = torch.tensor([nrec], dtype=torch.int64, device=dev)
+    cnts = [torch.empty(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(cnts, cnt)
+    cnts = [int(c.item()) for c in cnts]
+    mx = max(cnts)
+    total = sum(cnts)
+    if mx == 0:
+        return torch.empty(0, dtype=torch.uint8, device=dev), 0
+    send = torch.zeros(mx * rec_bytes, dtype=torch.uint8, device=dev)
+    if nrec:
+        send[: nrec * rec_bytes] = recs[: nrec * rec_bytes]
+    parts = [torch.empty(mx * rec_bytes, dtype=torch.uint8, device=dev) for _ in range(world)]
+    dist.all_gather(parts, send)
+    out = torch.cat([parts[p][: cnts[p] * rec_bytes] for p in range(world)])
+    return out, total
+
+
+def sharded_betweenness_rows(backend, dist, sources):
+    """Row-partitioned batched Brandes (one record exchange per BFS level);
+    returns the centrality (numpy fp64, every rank)."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    srcs = [int(s) for s in sources]
+    total = None
+    for b0 in range(0, len(srcs), 4):
+        backend.bc_begin(srcs[b0:b0 + 4], rank, world)
+        while True:                                   # forward: depth by depth
+            recs, nrec = backend.bc_forward()
+            allr, tot = _gather_records(dist, recs, nrec)
+            if backend.bc_forward_apply(allr, tot):
+                break
+        while True:                                   # backward: deepest first
+            recs, nrec, done = backend.bc_backward()
+            if done:
+                break
+            allr, tot = _gather_records(dist, recs, nrec)
+            backend.bc_backward_apply(allr, tot)
+        part = backend.bc_centrality().clone()
+        total = part if total is None else total + part
+    dist.all_reduce(total)
+    return total.cpu().numpy().copy()
 
 
 class _DeviceArray:
@@ -172,7 +226,60 @@ class GpuShardBackend:
         call("gbx_triangle_count_rows", C.byref(c), self.g.handle, rb, re)
         return int(c.value)
 
-    # ---- betweenness
+    # ---- betweenness, row-partitioned protocol (gbx_bc_shard_*)
+    def bc_begin(self, sources, rank, world):
+        from .graph import call
+        src = np.ascontiguousarray(sources, np.uint64)
+        rb, re = C.c_int64(), C.c_int64()
+        call("gbx_bc_shard_begin", self.g.handle, src.ctypes.data, len(src), rank, world,
+             C.byref(rb), C.byref(re))
+        self.bc_rb, self.bc_re = rb.value, re.value
+        return self.bc_rb, self.bc_re
+
+    def _recs(self, ptr, nrec):
+        import torch
+        if nrec == 0:
+            return torch.empty(0, dtype=torch.uint8, device=self.device)
+        return torch.as_tensor(_DeviceArray(ptr, nrec * 40, "|u1"), device=self.device)
+
+    def bc_forward(self):
+        from .graph import call
+        p, k = C.c_void_p(), C.c_int64()
+        call("gbx_bc_shard_forward", self.g.handle, C.byref(p), C.byref(k))
+        return self._recs(p.value, k.value), k.value
+
+    def bc_forward_apply(self, recs, nrec):
+        import torch
+
+        from .graph import call
+        torch.cuda.synchronize()  # the gathered records were written on torch's stream
+        done = C.c_int(0)
+        call("gbx_bc_shard_forward_apply", self.g.handle, recs.data_ptr() if nrec else None,
+             nrec, C.byref(done))
+        return bool(done.value)
+
+    def bc_backward(self):
+        from .graph import call
+        p, k, done = C.c_void_p(), C.c_int64(), C.c_int(0)
+        call("gbx_bc_shard_backward", self.g.handle, C.byref(p), C.byref(k), C.byref(done))
+        return self._recs(p.value, k.value), k.value, bool(done.value)
+
+    def bc_backward_apply(self, recs, nrec):
+        import torch
+
+        from .graph import call
+        torch.cuda.synchronize()
+        call("gbx_bc_shard_backward_apply", self.g.handle, recs.data_ptr() if nrec else None, nrec)
+
+    def bc_centrality(self):
+        import torch
+
+        from .graph import call
+        p = C.c_void_p()
+        call("gbx_bc_shard_centrality", self.g.handle, C.byref(p))
+        return torch.as_tensor(_DeviceArray(p.value, self.g.n(), "<f8"), device=self.device)
+
+    # ---- betweenness, sources dealt over ranks
     def bc_partial(self, sources):
         import torch
 

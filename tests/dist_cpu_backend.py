@@ -107,3 +107,146 @@ class CpuShardBackend:
             return torch.zeros(self.n, dtype=torch.float64)
         c = O.bc(self.n, self.rp, self.col, self.rp, self.col, np.asarray(sources, np.int64))
         return torch.from_numpy(np.ascontiguousarray(c, np.float64))
+
+
+REC = np.dtype([("v", "<i4"), ("lanes", "<u4"), ("x", "<f8", (4,))])  # the 40-byte record
+
+
+class CpuBcRowsBackend:
+    """TEST ONLY: numpy restatement of the gbx_bc_shard_* protocol (row-
+    partitioned batched Brandes, betweenness.cpp:11-86): owned rows settle
+    their path counts / dependencies, records are exchanged per level."""
+    device = torch.device("cpu")
+
+    def __init__(self, n, rp, col):
+        self.n = n
+        self.rp = np.asarray(rp, np.int64)
+        self.col = np.asarray(col, np.int64)  # undirected: AT = A
+
+    def _nb(self, v):
+        return self.col[self.rp[v]:self.rp[v + 1]]
+
+    def bc_begin(self, sources, rank, world):
+        n, nnz = self.n, int(self.rp[-1])
+
+        def split(q):
+            if q <= 0:
+                return 0
+            if q >= world:
+                return n
+            target = (n + nnz) * q // world
+            lo, hi = 0, n
+            while lo < hi:
+                mid = (lo + hi) // 2
+                if mid + self.rp[mid] < target:
+                    lo = mid + 1
+                else:
+                    hi = mid
+            return lo
+        self.rb, self.re = split(rank), max(split(rank), split(rank + 1))
+        self.ns = len(sources)
+        self.level = np.full((n, 4), -1, np.int64)
+        self.sigma = np.zeros((n, 4))
+        self.coef = np.zeros((n, 4))
+        self.cent = np.zeros(n)
+        first = []
+        for b, s in enumerate(sources):
+            self.level[s, b] = 0
+            self.sigma[s, b] = 1.0
+            if s not in first:
+                first.append(s)
+        self.order = [np.array(first, np.int64)]
+        self.live = (1 << self.ns) - 1
+        self.done_fwd = False
+        self.bd = None
+        return self.rb, self.re
+
+    def _pack(self, vs, vals, lanes):
+        r = np.zeros(len(vs), REC)
+        r["v"], r["x"], r["lanes"] = vs, vals, lanes
+        return torch.from_numpy(r.view(np.uint8).copy()), len(vs)
+
+    def bc_forward(self):
+        d = len(self.order)
+        vs, lanes = [], []
+        for v in range(self.rb, self.re):
+            nm = 0
+            for b in range(self.ns):
+                if not (self.live >> b) & 1 or self.level[v, b] != -1:
+                    continue
+                u = self._nb(v)
+                on = u[self.level[u, b] == d - 1]
+                s = float(self.sigma[on, b].sum())
+                if s > 0:
+                    self.level[v, b] = d
+                    self.sigma[v, b] = s
+                    nm |= 1 << b
+            if nm:
+                vs.append(v)
+                lanes.append(nm)
+        return self._pack(np.array(vs, np.int64), self.sigma[vs] if vs else np.zeros((0, 4)),
+                          np.array(lanes, np.uint32))
+
+    def bc_forward_apply(self, recs, nrec):
+        d = len(self.order)
+        r = recs.numpy().view(REC) if nrec else np.zeros(0, REC)
+        live = 0
+        for rec in r:
+            v, m = int(rec["v"]), int(rec["lanes"])
+            live |= m
+            if not (self.rb <= v < self.re):
+                for b in range(4):
+                    if (m >> b) & 1:
+                        self.level[v, b] = d
+                        self.sigma[v, b] = rec["x"][b]
+        self.order.append(r["v"].astype(np.int64))
+        self.live = live
+        if nrec == 0:
+            self.done_fwd = True
+        return self.done_fwd
+
+    def bc_backward(self):
+        empty = (torch.empty(0, dtype=torch.uint8), 0)
+        if self.bd is None:
+            D = len(self.order)
+            deepest = D - 1
+            while deepest > 0 and len(self.order[deepest]) == 0:
+                deepest -= 1
+            for v in self.order[deepest] if deepest >= 1 else []:
+                for b in range(self.ns):
+                    if self.level[v, b] == deepest:
+                        self.coef[v, b] = 1.0 / self.sigma[v, b]
+            self.bd = deepest - 1
+        while self.bd >= 1 and len(self.order[self.bd]) == 0:
+            self.bd -= 1
+        if self.bd < 1:
+            return empty[0], 0, True
+        d = self.bd
+        own = [v for v in self.order[d] if self.rb <= v < self.re]
+        for v in own:
+            w = self._nb(v)
+            for b in range(self.ns):
+                if self.level[v, b] != d:
+                    continue
+                on = w[self.level[w, b] == d + 1]
+                acc = float(self.coef[on, b].sum())
+                dl = self.sigma[v, b] * acc
+                self.cent[v] += dl
+                self.coef[v, b] = (1.0 + dl) / self.sigma[v, b]
+        t, k = self._pack(np.array(own, np.int64), self.coef[own] if own else np.zeros((0, 4)),
+                          np.zeros(len(own), np.uint32))
+        return t, k, False
+
+    def bc_backward_apply(self, recs, nrec):
+        d = self.bd
+        r = recs.numpy().view(REC) if nrec else np.zeros(0, REC)
+        for rec in r:
+            v = int(rec["v"])
+            if not (self.rb <= v < self.re):
+                for b in range(4):
+                    if self.level[v, b] == d:
+                        self.coef[v, b] = rec["x"][b]
+        self.bd -= 1
+
+    def bc_centrality(self):
+        return torch.from_numpy(self.cent.copy())

@@ -28,13 +28,13 @@ def _worker(rank, world, port, q, what):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
-    from paper_2104_01661_b200.dist import (sharded_betweenness, sharded_pagerank,
-                                            sharded_triangle_count)
-    from tests.dist_cpu_backend import CpuShardBackend
+    from paper_2104_01661_b200.dist import (sharded_betweenness, sharded_betweenness_rows,
+                                            sharded_pagerank, sharded_triangle_count)
+    from tests.dist_cpu_backend import CpuBcRowsBackend, CpuShardBackend
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     try:
-        und = what in ("tc", "bc")
+        und = what in ("tc", "bc", "bcrows")
         rp, col = O.rmat_graph(9, 8, seed=3, undirected=und)
         be = CpuShardBackend(len(rp) - 1, rp, col)
         if what == "pr":
@@ -43,6 +43,9 @@ def _worker(rank, world, port, q, what):
         elif what == "bc":
             c = sharded_betweenness(be, dist, BC_SOURCES)
             q.put((rank, "bc", None, c.tolist()))
+        elif what == "bcrows":
+            c = sharded_betweenness_rows(CpuBcRowsBackend(len(rp) - 1, rp, col), dist, BC_SOURCES)
+            q.put((rank, "bcrows", None, c.tolist()))
         else:
             q.put((rank, "tc", sharded_triangle_count(be, dist), None))
     finally:
@@ -92,3 +95,52 @@ def test_sharded_betweenness_gloo_matches_oracle():
     for _, _, _, c in out:
         got = np.array(c)
         assert np.abs(got - want).max() <= 1e-9 * max(1.0, np.abs(want).max())
+
+
+def test_row_partitioned_betweenness_gloo_matches_oracle():
+    """1D row blocks with one record exchange per BFS level (the protocol of
+    gbx_bc_shard_*; 5 sources = a batch of 4 and a batch of 1): equals the
+    single-process batched Brandes."""
+    out = _run("bcrows")
+    rp, col = O.rmat_graph(9, 8, seed=3, undirected=True)
+    n = len(rp) - 1
+    want = O.bc(n, rp, col, rp, col, np.asarray(BC_SOURCES, np.int64))
+    for _, _, _, c in out:
+        got = np.array(c)
+        assert np.abs(got - want).max() <= 1e-9 * max(1.0, np.abs(want).max())
+
+
+def test_row_partitioned_betweenness_single_process_protocol():
+    """The same protocol with 3 simulated ranks in one process (records
+    exchanged by concatenation): no rank ever waits on another."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from tests.dist_cpu_backend import CpuBcRowsBackend
+    rp, col = O.rmat_graph(8, 8, seed=5, undirected=True)
+    n = len(rp) - 1
+    srcs = [1, 9, 33, 77]
+    world = 3
+    bes = [CpuBcRowsBackend(n, rp, col) for _ in range(world)]
+    for r, be in enumerate(bes):
+        be.bc_begin(srcs, r, world)
+    assert [be.rb for be in bes][0] == 0 and bes[-1].re == n
+    while True:
+        outs = [be.bc_forward() for be in bes]
+        allr = torch.cat([t for t, _ in outs])
+        tot = sum(k for _, k in outs)
+        done = [be.bc_forward_apply(allr, tot) for be in bes]
+        assert len(set(done)) == 1
+        if done[0]:
+            break
+    while True:
+        outs = [be.bc_backward() for be in bes]
+        assert len({d for _, _, d in outs}) == 1
+        if outs[0][2]:
+            break
+        allr = torch.cat([t for t, _, _ in outs])
+        tot = sum(k for _, k, _ in outs)
+        for be in bes:
+            be.bc_backward_apply(allr, tot)
+    got = sum(be.bc_centrality().numpy() for be in bes)
+    want = O.bc(n, rp, col, rp, col, np.asarray(srcs, np.int64))
+    assert np.abs(got - want).max() <= 1e-9 * max(1.0, np.abs(want).max())
