@@ -323,6 +323,8 @@ typedef struct {
   double hot_bytes_per_launch; /* algorithmic bytes per dominant launch   */
   int64_t work_units;          /* edges / wedges / relaxations processed  */
   int iterations;              /* levels / iterations                     */
+  double hot_ms;               /* mean device duration of one dominant-kernel
+                                  launch in the last call (ms; 0 = not measured) */
 } gbx_stats;
 int gbx_last_stats(const gbx_graph* g, gbx_stats* stats, char msg[GBX_MSG_LEN]);
 

@@ -15,7 +15,7 @@ _lib = None
 class gbx_stats(C.Structure):
     _fields_ = [("launches", C.c_int64), ("hot_launches", C.c_int64),
                 ("hot_bytes_per_launch", C.c_double), ("work_units", C.c_int64),
-                ("iterations", C.c_int)]
+                ("iterations", C.c_int), ("hot_ms", C.c_double)]
 
 
 _vp = C.c_void_p

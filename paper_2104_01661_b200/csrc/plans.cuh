@@ -42,6 +42,9 @@ struct PrPlan {
   DevArray<double> invd;           // damping / out-degree (fp64 storage)
   DevArray<double> l1_block, l1_fin, l1_hist;
   DevArray<int> ctl;            // [0] completed iterations, [1] done
+  DevArray<unsigned long long> ktime;  // k_pr_rows launch spans (%globaltimer)
+  double last_rows_ms = 0.0;
+  bool last_persist = false;       // the last run used k_pr_persist
   DevArray<unsigned> blk_cnt;
   // CUDA graph with a conditional WHILE node (one iteration kernel per trip)
   cudaGraph_t graph = nullptr;

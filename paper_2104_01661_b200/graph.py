@@ -161,7 +161,7 @@ class Graph:
         call("gbx_last_stats", self.handle, C.byref(st))
         return {"launches": st.launches, "hot_launches": st.hot_launches,
                 "hot_bytes_per_launch": st.hot_bytes_per_launch,
-                "work_units": st.work_units, "iterations": st.iterations}
+                "work_units": st.work_units, "iterations": st.iterations, "hot_ms": st.hot_ms}
 
     def result_device(self, which: str):
         p = C.c_void_p()
