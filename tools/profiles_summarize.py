@@ -20,7 +20,7 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 from ncu_summary import summarize  # noqa: E402
 
 
-def launch_table(src, dst_txt):
+def launch_table(src, dst_txt, header):
     rows = [r for r in csv.reader(open(src)) if len(r) > 10]
     h = rows[0]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
@@ -31,13 +31,7 @@ def launch_table(src, dst_txt):
         agg[k][1] += float(r[vi].replace(",", "")) / 1e3
     tot = sum(t for _, t in agg.values())
     with open(dst_txt, "w") as f:
-        f.write("# ncu --metrics gpu__time_duration.sum --clock-control none launch list of\n"
-                "# `GBX_PR_NO_GRAPH=1 python bench.py --steps 2 --warmup 1` (the bench runs\n"
-                "# PageRank as a conditional-WHILE CUDA graph whose body kernels ncu does not\n"
-                "# list; the env var launches the same kernels one by one).  Cold,\n"
-                "# serialised launches: the SHARE of each kernel is what compares with the\n"
-                "# bench, not the absolute.  The whole process is listed (graph generation,\n"
-                "# plan builds, the e2e leg and the CPU-baseline setup included).\n")
+        f.write(header)
         f.write(f"{'kernel':70s} {'launches':>8s} {'total_us':>12s} {'avg_us':>10s} {'share':>7s}\n")
         for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
             f.write(f"{k[:70]:70s} {c:8d} {t:12.1f} {t / c:10.1f} {100 * t / tot:6.2f}%\n")
@@ -64,10 +58,23 @@ def main():
     src = os.path.join(ROOT, "gpurun_out", f"prof_{r}")
     dst = os.path.join(ROOT, "profiles", r)
     os.makedirs(dst, exist_ok=True)
-    lc = os.path.join(src, "bench_pagerank_launches.csv")
-    if os.path.exists(lc):
-        shutil.copy(lc, dst)
-        launch_table(lc, os.path.join(dst, "bench_pagerank_launches.txt"))
+    common = ("# Cold, serialised launches: the SHARE of each kernel is what compares with\n"
+              "# the bench, not the absolute.  The whole process is listed (graph\n"
+              "# generation, plan builds, the e2e leg and the CPU-baseline setup included).\n")
+    heads = {
+        "bench_pagerank_launches": "# ncu --metrics gpu__time_duration.sum --clock-control none launch list of\n"
+                                   "# `python bench.py --steps 2 --warmup 1` (PageRank runs as ONE persistent\n"
+                                   "# cooperative kernel per step, k_pr_persist: row phase + long-row finish\n"
+                                   "# + L1 reduction per iteration).\n" + common,
+        "bench_pagerank_launches_split": "# the same with GBX_PR_NO_GRAPH=1: the same row / finish code launched as\n"
+                                         "# one k_pr_rows + k_pr_finish pair per iteration, splitting the shares.\n"
+                                         + common,
+    }
+    for base, head in heads.items():
+        lc = os.path.join(src, base + ".csv")
+        if os.path.exists(lc):
+            shutil.copy(lc, dst)
+            launch_table(lc, os.path.join(dst, base + ".txt"), head)
     for fn in sorted(os.listdir(src)):
         p = os.path.join(src, fn)
         if fn.endswith(".ncu-rep"):
