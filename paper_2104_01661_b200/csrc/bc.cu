@@ -214,7 +214,13 @@ __global__ void __launch_bounds__(256) k_bc_push(BcArgs a) {
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int d = a.d;
   unsigned found = 0;
-  for (int64_t e = gwarp; e < a.n_ent; e += nwarps) {
+  // small queues: every entry split over S warps (S a power of two <= 8)
+  int S = 1;
+  while (S < 8 && static_cast<int64_t>(a.n_ent) * S * 2 <= nwarps) S <<= 1;
+  const int64_t sub = kBcChunk / S;
+  for (int64_t e2 = gwarp; e2 < static_cast<int64_t>(a.n_ent) * S; e2 += nwarps) {
+    const int64_t e = e2 / S;
+    const int part = static_cast<int>(e2 - e * S);
     const int64_t ent = a.ent_in[e];
     const int32_t u = static_cast<int32_t>(ent & 0xffffffff);
     const int64_t c = ent >> 32;
@@ -222,8 +228,10 @@ __global__ void __launch_bounds__(256) k_bc_push(BcArgs a) {
     double su[4];
 #pragma unroll
     for (int b = 0; b < 4; ++b) su[b] = (m >> b) & 1u ? a.sigma[static_cast<int64_t>(u) * 4 + b] : 0.0;
-    const int64_t b0 = a.rp[u] + c * kBcChunk;
-    const int64_t e0 = min(a.rp[u + 1], b0 + kBcChunk);
+    const int64_t cb = a.rp[u] + c * kBcChunk;
+    const int64_t ce = min(a.rp[u + 1], cb + kBcChunk);
+    const int64_t b0 = cb + part * sub;
+    const int64_t e0 = min(ce, b0 + sub);
     for (int64_t base = b0; base < e0; base += 32) {
       const int64_t p = base + lane;
       bool claimed = false;

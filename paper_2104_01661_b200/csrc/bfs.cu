@@ -157,12 +157,22 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
     uint32_t* bn = p ? a.bm0 : a.bm1;
     fq.reset(qn, &a.ctl[2], &a.ctl[3], &edges[1], nullptr);
     if (push) {
-      for (int64_t e = gwarp; e < qe; e += nwarps) {
+      // a small queue (a hub or two) would leave most warps idle and walk each
+      // kChunk-edge entry in kChunk/32 dependent steps: split every entry over
+      // S warps (S = power of two up to 8, uniform over the grid)
+      int S = 1;
+      while (S < 8 && static_cast<int64_t>(qe) * S * 2 <= nwarps) S <<= 1;
+      const int64_t sub = kChunk / S;
+      for (int64_t e2 = gwarp; e2 < static_cast<int64_t>(qe) * S; e2 += nwarps) {
+        const int64_t e = e2 / S;
+        const int part = static_cast<int>(e2 - e * S);
         const int64_t ent = qc[e];
         const int32_t v = static_cast<int32_t>(ent & 0xffffffff);
         const int64_t c = ent >> 32;
-        const int64_t b0 = a.rp[v] + c * kChunk;
-        const int64_t e0 = min(a.rp[v + 1], b0 + kChunk);
+        const int64_t cb = a.rp[v] + c * kChunk;
+        const int64_t ce = min(a.rp[v + 1], cb + kChunk);
+        const int64_t b0 = cb + part * sub;
+        const int64_t e0 = min(ce, b0 + sub);
         for (int64_t base = b0; base < e0; base += 32) {
           const int64_t q = base + lane;
           bool has = false;
@@ -567,13 +577,21 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
     unsigned long long* fn = p ? a.f0 : a.f1;
     fq.reset(qn, &a.ctl[kB64Ent + bn], &a.ctl[kB64Vtx + bn], &a.edges[bn], nullptr);
     if (push) {
-      for (int64_t e = gwarp; e < qe; e += nwarps) {
+      // small queues: every entry split over S warps (as in k_bfs1)
+      int S = 1;
+      while (S < 8 && static_cast<int64_t>(qe) * S * 2 <= nwarps) S <<= 1;
+      const int64_t sub = kChunk / S;
+      for (int64_t e2 = gwarp; e2 < static_cast<int64_t>(qe) * S; e2 += nwarps) {
+        const int64_t e = e2 / S;
+        const int part = static_cast<int>(e2 - e * S);
         const int64_t ent = qc[e];
         const int32_t v = static_cast<int32_t>(ent & 0xffffffff);
         const int64_t c = ent >> 32;
         const unsigned long long f = fc[v];
-        const int64_t b0 = a.rp[v] + c * kChunk;
-        const int64_t e0 = min(a.rp[v + 1], b0 + kChunk);
+        const int64_t cb = a.rp[v] + c * kChunk;
+        const int64_t ce = min(a.rp[v + 1], cb + kChunk);
+        const int64_t b0 = cb + part * sub;
+        const int64_t e0 = min(ce, b0 + sub);
         for (int64_t base = b0; base < e0; base += 32) {
           const int64_t q = base + lane;
           bool has = false;
