@@ -389,6 +389,23 @@ int gbx_bc_shard_backward_apply(gbx_graph* g, const void* recs_dev, int64_t nrec
                                 char msg[GBX_MSG_LEN]);
 int gbx_bc_shard_centrality(gbx_graph* g, double** cent_dev, char msg[GBX_MSG_LEN]);
 
+/* ---- row-sharded single-source BFS for the multi-GPU driver ---------------
+ * bfs.cpp:18-85 over 1D row blocks (scale >= 22): rank r owns the
+ * 32-aligned block [row_begin, row_end) (balanced by AT nnz + rows).  Per level
+ * every rank calls gbx_bfs_shard_level with the GLOBAL frontier bitmap (n bits,
+ * device) and receives its slice of the next bitmap (words [row_begin/32,
+ * ceil(row_end/32)), device) and the number of owned vertices it reached; the
+ * driver all-gathers the slices (NCCL) and stops when no rank found any.
+ * Owned vertices are pulled against the frontier: the first frontier
+ * in-neighbour in the ascending AT row is the parent -- the minimum id, as in
+ * gbx_bfs, whose results these equal.  gbx_bfs_shard_result copies the owned
+ * rows' parent / level (-1 = unreached) to host arrays of row_end - row_begin. */
+int gbx_bfs_shard_begin(gbx_graph* g, uint64_t source, int rank, int nranks, int64_t* row_begin,
+                        int64_t* row_end, char msg[GBX_MSG_LEN]);
+int gbx_bfs_shard_level(gbx_graph* g, const uint32_t* frontier_dev, uint32_t* next_slice_dev,
+                        int64_t* found, char msg[GBX_MSG_LEN]);
+int gbx_bfs_shard_result(gbx_graph* g, int64_t* parent, int64_t* level, char msg[GBX_MSG_LEN]);
+
 #ifdef __cplusplus
 }
 #endif

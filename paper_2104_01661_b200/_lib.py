@@ -87,6 +87,9 @@ _SIGS = {
     "gbx_vxm": [_vp, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp],
     "gbx_mxm": [_pp, _vp, _vp, _int, _int, _vp, _vp],
     "gbx_bc_shard_begin": [_vp, _vp, _u64, _int, _int, _vp, _vp],
+    "gbx_bfs_shard_begin": [_vp, _u64, _int, _int, _vp, _vp],
+    "gbx_bfs_shard_level": [_vp, _vp, _vp, _vp],
+    "gbx_bfs_shard_result": [_vp, _vp, _vp],
     "gbx_bc_shard_forward": [_vp, _pp, _vp],
     "gbx_bc_shard_forward_apply": [_vp, _vp, _i64, _vp],
     "gbx_bc_shard_backward": [_vp, _pp, _vp, _vp],

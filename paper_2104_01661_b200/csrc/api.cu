@@ -728,6 +728,33 @@ int gbx_last_stats(const gbx_graph* gc, gbx_stats* stats, char* msg) {
   });
 }
 
+int gbx_bfs_shard_begin(gbx_graph* g, uint64_t source, int rank, int nranks, int64_t* row_begin,
+                        int64_t* row_end, char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    gbx::Scope sc(g);
+    gbx::bfs_shard_begin(g, source, rank, nranks, row_begin, row_end);
+  });
+}
+
+int gbx_bfs_shard_level(gbx_graph* g, const uint32_t* front, uint32_t* next_slice, int64_t* found,
+                        char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    if (!front || !found) gbx::fail(GBX_NULL_ARGUMENT, "frontier / found is NULL");
+    gbx::Scope sc(g);
+    gbx::bfs_shard_level(g, front, next_slice, found);
+  });
+}
+
+int gbx_bfs_shard_result(gbx_graph* g, int64_t* parent, int64_t* level, char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    gbx::Scope sc(g);
+    gbx::bfs_shard_result(g, parent, level);
+  });
+}
+
 int gbx_bc_shard_begin(gbx_graph* g, const uint64_t* sources, uint64_t ns, int rank, int nranks,
                        int64_t* row_begin, int64_t* row_end, char* msg) {
   return guard(msg, [&] {

@@ -908,4 +908,189 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
   g->stats.hot_launches = (ns + 63) / 64;
 }
 
+
+// ---------------------------------------------------------------------------
+// Row-sharded single-source BFS for the multi-GPU driver (scale >=
+// 22): rank r owns the 32-aligned vertex block [rb, re) (balanced by AT nnz +
+// rows).  Per level every rank pulls its still-unvisited owned vertices
+// against the GLOBAL frontier bitmap (n bits) -- the first frontier
+// in-neighbour in the ascending AT row is the parent, the minimum id exactly
+// as in the single-GPU traversal -- and writes its slice of the next bitmap;
+// the driver all-gathers the slices (the north_star's frontier-bitmap
+// all-gather) and sums the found counts.  Pull-only: results are identical
+// to gbx_bfs (parents are min-id in both directions).
+// ---------------------------------------------------------------------------
+
+// 8 lanes per vertex, 4 vertices per warp step: the group scans its AT row 8
+// edges per step; the lowest lane with a frontier hit holds the min-id parent
+__global__ void __launch_bounds__(256) k_bfs_shard_pull(const int64_t* trp, const int32_t* tcol,
+                                                        int64_t rb, int64_t re,
+                                                        const int32_t* ul_in, int ucnt,
+                                                        const uint32_t* front, int d,
+                                                        int32_t* level, int32_t* parent,
+                                                        uint32_t* next_slice, int32_t* ul_out,
+                                                        int* cnt) {
+  const int lane = threadIdx.x & 31;
+  const int grp = lane >> 3, sub = lane & 7;
+  const unsigned gmask = 0xffu << (grp * 8);
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t range = ucnt < 0 ? re - rb : ucnt;
+  int found = 0;
+  for (int64_t base = gwarp * 4; base < range; base += nwarps * 4) {
+    const int64_t i = base + grp;
+    int64_t v = -1;
+    if (i < range) v = ucnt < 0 ? rb + i : ul_in[i];
+    bool active = v >= 0 && level[v] == -1;
+    int64_t p = active ? trp[v] : 0;
+    const int64_t e = active ? trp[v + 1] : 0;
+    const bool nonempty = e > p;
+    int32_t par = -1;
+    while (__any_sync(kFull, active)) {
+      bool hit = false;
+      int32_t u = 0;
+      if (active && p + sub < e) {
+        u = __ldg(tcol + p + sub);
+        hit = (__ldg(front + (u >> 5)) >> (u & 31)) & 1u;
+      }
+      const unsigned hb = __ballot_sync(kFull, hit) & gmask;
+      if (active) {
+        if (hb) {
+          const int first = __ffs(hb) - 1;  // lowest lane = smallest neighbour id
+          par = __shfl_sync(gmask, u, first, 32);
+          active = false;
+        } else {
+          p += 8;
+          if (p >= e) active = false;
+        }
+      } else {
+        (void)__shfl_sync(gmask, u, grp * 8, 32);
+      }
+    }
+    if (v >= 0 && sub == 0) {
+      if (par >= 0) {
+        level[v] = d;
+        parent[v] = par;
+        const int64_t w = (v >> 5) - (rb >> 5);
+        atomicOr(next_slice + w, 1u << (v & 31));
+        ++found;
+      } else if (nonempty && level[v] == -1) {
+        ul_out[atomicAdd(&cnt[1], 1)] = static_cast<int32_t>(v);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) found += __shfl_xor_sync(kFull, found, o);
+  if (lane == 0 && found) atomicAdd(&cnt[0], found);
+}
+
+__global__ void k_bfs_shard_init(int32_t* level, int32_t* parent, int64_t rb, int64_t re,
+                                 int32_t src) {
+  const int64_t v = rb + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (v >= re) return;
+  level[v] = v == src ? 0 : -1;
+  parent[v] = v == src ? src : -1;
+}
+
+__global__ void k_bfs_shard_split(const int64_t* trp, int64_t n, int parts, int64_t* bounds) {
+  const int q = threadIdx.x;
+  if (q > parts) return;
+  const int64_t target = (n + trp[n]) * q / parts;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (mid + trp[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  // 32-aligned so every rank owns whole bitmap words
+  bounds[q] = q == 0 ? 0 : q == parts ? n : min(n, (lo + 31) & ~int64_t(31));
+}
+
+static BfsShard& need_bfs_shard(gbx_graph* g) {
+  if (!g->bfs || !g->bfs->shard) fail(GBX_MISSING_PROPERTY, "bfs shard protocol needs gbx_bfs_shard_begin");
+  return *g->bfs->shard;
+}
+
+void bfs_shard_begin(gbx_graph* g, uint64_t source, int rank, int nranks, int64_t* rb_out,
+                     int64_t* re_out) {
+  require_at(g, "bfs_shard");
+  const int64_t n = g->A.n;
+  if (source >= static_cast<uint64_t>(n)) fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(source));
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(GBX_INVALID_VALUE, "bfs_shard: bad rank / nranks");
+  ensure_bfs1(g);
+  BfsWork& W = *g->bfs;
+  cudaStream_t s = g->stream;
+  const Csr& AT = g->AT();
+  auto S = std::make_unique<BfsShard>();
+  S->rank = rank;
+  S->nranks = nranks;
+  S->source = static_cast<int32_t>(source);
+  {
+    DevArray<int64_t> b(nranks + 1);
+    k_bfs_shard_split<<<1, ((nranks + 32) / 32) * 32, 0, s>>>(AT.rp.p, n, nranks, b.p);
+    GBX_LAUNCHED();
+    std::vector<int64_t> hb(nranks + 1);
+    GBX_CUDA(cudaMemcpyAsync(hb.data(), b.p, (nranks + 1) * 8, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+    for (int q = 1; q <= nranks; ++q) hb[q] = std::max(hb[q], hb[q - 1]);
+    S->rb = hb[rank];
+    S->re = hb[rank + 1];
+  }
+  S->cnt.alloc(2);
+  if (S->re > S->rb) {
+    k_bfs_shard_init<<<ceil_div(S->re - S->rb, 256), 256, 0, s>>>(W.level.p, W.parent.p, S->rb,
+                                                                   S->re, S->source);
+    GBX_LAUNCHED();
+  }
+  GBX_CUDA(cudaStreamSynchronize(s));
+  W.shard = std::move(S);
+  if (rb_out) *rb_out = W.shard->rb;
+  if (re_out) *re_out = W.shard->re;
+}
+
+// one level: pull the owned unvisited vertices against front (n bits, global);
+// next_slice = this rank's words [rb/32, ceil(re/32)) of the next frontier
+void bfs_shard_level(gbx_graph* g, const uint32_t* front, uint32_t* next_slice, int64_t* found) {
+  BfsShard& S = need_bfs_shard(g);
+  BfsWork& W = *g->bfs;
+  cudaStream_t s = g->stream;
+  const Csr& AT = g->AT();
+  const int64_t words = (S.re + 31) / 32 - S.rb / 32;
+  if (words > 0) GBX_CUDA(cudaMemsetAsync(next_slice, 0, words * 4, s));
+  GBX_CUDA(cudaMemsetAsync(S.cnt.p, 0, 2 * sizeof(int), s));
+  const int d = S.d + 1;
+  const int grid = device_sms() * 8;
+  if (S.re > S.rb && S.ucnt != 0) {
+    k_bfs_shard_pull<<<grid, 256, 0, s>>>(AT.rp.p, AT.col.p, S.rb, S.re, W.ulist[S.ul].p, S.ucnt,
+                                          front, d, W.level.p, W.parent.p, next_slice,
+                                          W.ulist[S.ul ^ 1].p, S.cnt.p);
+    GBX_LAUNCHED();
+  }
+  int hc[2] = {0, 0};
+  GBX_CUDA(cudaMemcpyAsync(hc, S.cnt.p, sizeof hc, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  if (S.re > S.rb && S.ucnt != 0) {
+    S.ucnt = hc[1];
+    S.ul ^= 1;
+  }
+  S.d = d;
+  *found = hc[0];
+}
+
+// owned rows [rb, re): parent / level (-1 = unreached), host arrays of re - rb
+void bfs_shard_result(gbx_graph* g, int64_t* parent, int64_t* level) {
+  BfsShard& S = need_bfs_shard(g);
+  BfsWork& W = *g->bfs;
+  cudaStream_t s = g->stream;
+  const int64_t m = S.re - S.rb;
+  if (m <= 0) return;
+  std::vector<int32_t> tp(m), tl(m);
+  GBX_CUDA(cudaMemcpyAsync(tp.data(), W.parent.p + S.rb, m * 4, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaMemcpyAsync(tl.data(), W.level.p + S.rb, m * 4, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < m; ++i) {
+    if (parent) parent[i] = tl[i] < 0 ? -1 : tp[i];
+    if (level) level[i] = tl[i];
+  }
+}
+
 }  // namespace gbx

@@ -233,6 +233,10 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
 void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* parent,
                    int64_t* level);
 void bfs_prepare(gbx_graph* g);
+void bfs_shard_begin(gbx_graph* g, uint64_t source, int rank, int nranks, int64_t* rb_out,
+                     int64_t* re_out);
+void bfs_shard_level(gbx_graph* g, const uint32_t* front, uint32_t* next_slice, int64_t* found);
+void bfs_shard_result(gbx_graph* g, int64_t* parent, int64_t* level);
 uint64_t tc_run(gbx_graph* g, int64_t row_begin, int64_t row_end);
 void tc_prepare(gbx_graph* g);
 void tc_partition(gbx_graph* g, int parts, int64_t* bounds);

@@ -66,8 +66,22 @@ struct PrShard {
 };
 
 // BFS workspaces (bfs.cu).
+// Row-sharded single-source BFS (bfs.cu, multi-GPU driver): this rank owns
+// vertices [rb, re) (32-aligned), pulls them against the global frontier
+// bitmap each level and contributes its slice of the next bitmap.
+struct BfsShard {
+  int rank = 0, nranks = 1;
+  int64_t rb = 0, re = 0;
+  int32_t source = 0;
+  int d = 0;             // levels done
+  int ucnt = -1;         // owned still-unvisited list (-1: every owned vertex)
+  int ul = 0;            // parity of the list being read
+  DevArray<int> cnt;     // [0] found [1] next list size
+};
+
 struct BfsWork {
   int64_t n = 0;
+  std::unique_ptr<BfsShard> shard;
   DevArray<int32_t> level, parent;          // single source
   DevArray<int32_t> queue[2];
   DevArray<uint32_t> bitmap[2];

@@ -11,6 +11,9 @@ rows + nnz.  Per iteration every rank runs the fused shard step on its rows
     pagerank.cpp:65-74 does (same iteration count as the single-GPU path).
 Triangle count (config 3): U replicated, middle vertices split by probe work
 (gbx_tc_partition), one u64 all-reduce at the end.
+BFS (scale >= 22): 1D row blocks (32-aligned), one frontier-bitmap all-gather
+per level (sharded_bfs): every rank pulls its unvisited rows against the global
+frontier, parents are the min-id frontier in-neighbour exactly as on one GPU.
 Betweenness (config 5), two drivers:
   * sharded_betweenness_rows -- 1D row blocks: every rank owns a
     nnz-balanced vertex block and settles only its rows' path counts (forward)
@@ -98,6 +101,38 @@ def sharded_betweenness(backend, dist, sources):
     part = backend.bc_partial(mine)            # fp64 tensor [n] (zeros if no sources)
     dist.all_reduce(part)
     return part.cpu().numpy().copy()
+
+
+def sharded_bfs(backend, dist, source):
+    """Row-sharded BFS from one source; returns (parent, level) numpy int64
+    arrays (-1 = unreached) on every rank."""
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    rb, re, n = backend.bfs_begin(source, rank, world)
+    dev = backend.device
+    b = torch.tensor([rb, re], dtype=torch.int64, device=dev)
+    allb = [torch.empty(2, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(allb, b)
+    rows = [int(t[0]) for t in allb] + [int(allb[-1][1])]
+    assert rows[0] == 0 and rows[-1] == n
+    words = (n + 31) // 32
+    wb = [r // 32 for r in rows[:-1]] + [words]          # word slices tile [0, words)
+    front = torch.zeros(max(words, 1), dtype=torch.int32, device=dev)
+    front[source >> 5] = torch.tensor(1 << (source & 31), dtype=torch.int64).to(torch.int32)
+    nxt = torch.zeros(max(wb[rank + 1] - wb[rank], 1), dtype=torch.int32, device=dev)
+    while True:
+        found = backend.bfs_level(front, nxt)
+        tot = torch.tensor([found], dtype=torch.int64, device=dev)
+        dist.all_reduce(tot)
+        if int(tot.item()) == 0:
+            break
+        _gather_slices(dist, nxt[: wb[rank + 1] - wb[rank]], wb, world, front)
+    par, lev = backend.bfs_result()
+    p_full = torch.empty(n, dtype=torch.int64, device=dev)
+    l_full = torch.empty(n, dtype=torch.int64, device=dev)
+    _gather_slices(dist, torch.as_tensor(par, device=dev), rows, world, p_full)
+    _gather_slices(dist, torch.as_tensor(lev, device=dev), rows, world, l_full)
+    return p_full.cpu().numpy(), l_full.cpu().numpy()
 
 
 def _gather_records(dist, recs, nrec, rec_bytes=40):
@@ -225,6 +260,32 @@ class GpuShardBackend:
         c = C.c_uint64(0)
         call("gbx_triangle_count_rows", C.byref(c), self.g.handle, rb, re)
         return int(c.value)
+
+    # ---- row-sharded BFS (gbx_bfs_shard_*)
+    def bfs_begin(self, source, rank, world):
+        from .graph import call
+        rb, re = C.c_int64(), C.c_int64()
+        call("gbx_bfs_shard_begin", self.g.handle, int(source), rank, world, C.byref(rb),
+             C.byref(re))
+        self.bfs_rb, self.bfs_re = rb.value, re.value
+        return self.bfs_rb, self.bfs_re, self.g.n()
+
+    def bfs_level(self, front, nxt):
+        import torch
+
+        from .graph import call
+        torch.cuda.synchronize()  # the gathered frontier was written on torch's stream
+        k = C.c_int64()
+        call("gbx_bfs_shard_level", self.g.handle, front.data_ptr(), nxt.data_ptr(), C.byref(k))
+        return k.value
+
+    def bfs_result(self):
+        from .graph import call
+        m = self.bfs_re - self.bfs_rb
+        par = np.empty(max(m, 1), np.int64)
+        lev = np.empty(max(m, 1), np.int64)
+        call("gbx_bfs_shard_result", self.g.handle, par.ctypes.data, lev.ctypes.data)
+        return par[:m], lev[:m]
 
     # ---- betweenness, row-partitioned protocol (gbx_bc_shard_*)
     def bc_begin(self, sources, rank, world):

@@ -250,3 +250,60 @@ class CpuBcRowsBackend:
 
     def bc_centrality(self):
         return torch.from_numpy(self.cent.copy())
+
+
+class CpuBfsRowsBackend:
+    """TEST ONLY: numpy restatement of the gbx_bfs_shard_* protocol (row-
+    sharded BFS, bfs.cpp:18-85): owned 32-aligned rows pulled against the
+    global frontier bitmap; parent = the first (min-id) frontier in-neighbour."""
+    device = torch.device("cpu")
+
+    def __init__(self, n, rp, col):
+        self.n = n
+        self.rp = np.asarray(rp, np.int64)
+        self.col = np.asarray(col, np.int64)  # undirected: AT = A
+
+    def bfs_begin(self, source, rank, world):
+        n, nnz = self.n, int(self.rp[-1])
+        b = [0]
+        for q in range(1, world):
+            target = (n + nnz) * q // world
+            lo, hi = 0, n
+            while lo < hi:
+                mid = (lo + hi) // 2
+                if mid + self.rp[mid] < target:
+                    lo = mid + 1
+                else:
+                    hi = mid
+            b.append(max(b[-1], min(n, (lo + 31) // 32 * 32)))
+        b.append(n)
+        self.rb, self.re = b[rank], b[rank + 1]
+        self.level = np.full(n, -1, np.int64)
+        self.parent = np.full(n, -1, np.int64)
+        if self.rb <= source < self.re:
+            self.level[source] = 0
+            self.parent[source] = source
+        self.d = 0
+        return self.rb, self.re, n
+
+    def bfs_level(self, front, nxt):
+        f = front.numpy().view(np.uint32)
+        d = self.d + 1
+        nxt.zero_()
+        nx = nxt.numpy().view(np.uint32)
+        found = 0
+        for v in range(self.rb, self.re):
+            if self.level[v] != -1:
+                continue
+            for u in self.col[self.rp[v]:self.rp[v + 1]]:
+                if (f[u >> 5] >> (u & 31)) & 1:
+                    self.level[v] = d
+                    self.parent[v] = u
+                    nx[(v >> 5) - (self.rb >> 5)] |= np.uint32(1 << (v & 31))
+                    found += 1
+                    break
+        self.d = d
+        return found
+
+    def bfs_result(self):
+        return self.parent[self.rb:self.re].copy(), self.level[self.rb:self.re].copy()

@@ -22,6 +22,7 @@ def _free_port():
 
 
 BC_SOURCES = [3, 17, 40, 101, 250]
+BFS_SOURCE = 17
 
 
 def _worker(rank, world, port, q, what):
@@ -30,11 +31,12 @@ def _worker(rank, world, port, q, what):
     sys.path.insert(0, root)
     from paper_2104_01661_b200.dist import (sharded_betweenness, sharded_betweenness_rows,
                                             sharded_pagerank, sharded_triangle_count)
-    from tests.dist_cpu_backend import CpuBcRowsBackend, CpuShardBackend
+    from paper_2104_01661_b200.dist import sharded_bfs
+    from tests.dist_cpu_backend import CpuBcRowsBackend, CpuBfsRowsBackend, CpuShardBackend
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     try:
-        und = what in ("tc", "bc", "bcrows")
+        und = what in ("tc", "bc", "bcrows", "bfsrows")
         rp, col = O.rmat_graph(9, 8, seed=3, undirected=und)
         be = CpuShardBackend(len(rp) - 1, rp, col)
         if what == "pr":
@@ -43,6 +45,9 @@ def _worker(rank, world, port, q, what):
         elif what == "bc":
             c = sharded_betweenness(be, dist, BC_SOURCES)
             q.put((rank, "bc", None, c.tolist()))
+        elif what == "bfsrows":
+            p, lv = sharded_bfs(CpuBfsRowsBackend(len(rp) - 1, rp, col), dist, BFS_SOURCE)
+            q.put((rank, "bfsrows", lv.tolist(), p.tolist()))
         elif what == "bcrows":
             c = sharded_betweenness_rows(CpuBcRowsBackend(len(rp) - 1, rp, col), dist, BC_SOURCES)
             q.put((rank, "bcrows", None, c.tolist()))
@@ -144,3 +149,14 @@ def test_row_partitioned_betweenness_single_process_protocol():
     got = sum(be.bc_centrality().numpy() for be in bes)
     want = O.bc(n, rp, col, rp, col, np.asarray(srcs, np.int64))
     assert np.abs(got - want).max() <= 1e-9 * max(1.0, np.abs(want).max())
+
+
+def test_row_sharded_bfs_gloo_matches_oracle():
+    """Row-sharded BFS, one frontier-bitmap all-gather per level: parents and
+    levels bit-exact against the oracle (min-id parents)."""
+    out = _run("bfsrows")
+    rp, col = O.rmat_graph(9, 8, seed=3, undirected=True)
+    n = len(rp) - 1
+    wp, wl = O.bfs(n, rp, col, BFS_SOURCE)
+    for _, _, lv, par in out:
+        assert np.array_equal(np.array(par), wp) and np.array_equal(np.array(lv), wl)
