@@ -27,6 +27,6 @@ $FULL -k regex:'^k_bc_back$' -s 4 -c 1 -o $OUT/bc_k_bc_back -f python tools/prof
 $FULL -k regex:'^k_sssp_b' -c 1 -o $OUT/sssp_k_sssp_b -f python tools/prof_algo.py sssp 24 > $OUT/sssp.log 2>&1; echo sssp rc=$?
 # 3) cooperative-kernel level timing (%globaltimer), not a profiler run
 PYTHONPATH=. GBX_BFS_TLOG=1 timeout -s KILL 300 python tools/bfs_one.py 0 > $OUT/bfs1_levels.txt 2>&1
-GBX_BFS_TLOG=1 timeout -s KILL 300 python bench.py --workload bfs64 --steps 1 --warmup 3 2> $OUT/bfs64_levels.txt > /dev/null
+GBX_BFS_TLOG=1 timeout -s KILL 300 python bench.py --workload bfs64 --steps 1 --warmup 3 2>&1 >/dev/null | grep "^bfs64" > $OUT/bfs64_levels.txt
 PYTHONPATH=. GBX_SSSP_TLOG=1 timeout -s KILL 300 python tools/sssp_diag.py > $OUT/sssp_levels.txt 2>&1
 echo done
