@@ -182,6 +182,8 @@ void vxm_op(int64_t* w_idx, void* w_vals, int64_t* w_nvals, const gbx_vec* w, co
 void mxm_op(gbx_mat* out, gbx_mat* C, const gbx_desc* desc, int sr, int sdom, gbx_mat* A,
             gbx_mat* B);
 void compute_transpose(cudaStream_t s, const Csr& A, Csr& T);
+void rowptr_from_sorted_rows32(cudaStream_t s, int64_t n, const uint32_t* rows, int64_t nnz,
+                               int64_t* rp);
 void compute_degrees(cudaStream_t s, const Csr& A, DevArray<int32_t>& out, bool by_row);
 void require_at(const gbx_graph* g, const char* who);
 void require_rowdeg(const gbx_graph* g, const char* who);

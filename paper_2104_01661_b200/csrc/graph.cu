@@ -501,6 +501,16 @@ void rowptr_from_sorted_keys(cudaStream_t s, int64_t n, int bits, const uint64_t
   max_scan_rowptr(s, rp, n);
 }
 
+// row pointers (n+1) from a row-sorted 32-bit row-id array
+void rowptr_from_sorted_rows32(cudaStream_t s, int64_t n, const uint32_t* rows, int64_t nnz,
+                               int64_t* rp) {
+  GBX_CUDA(cudaMemsetAsync(rp, 0, (n + 1) * sizeof(int64_t), s));
+  if (nnz == 0) return;
+  k_row_ends32<<<ceil_div(nnz, 256), 256, 0, s>>>(rows, nnz, rp);
+  GBX_LAUNCHED();
+  max_scan_rowptr(s, rp, n);
+}
+
 // the first nnz sorted (row<<bits|col) keys -> CSR arrays
 void csr_from_sorted_keys(cudaStream_t s, int64_t n, int bits, const uint64_t* keys,
                           int64_t nnz, DevArray<int64_t>& rp, DevArray<int32_t>& col) {

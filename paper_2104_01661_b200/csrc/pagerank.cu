@@ -462,12 +462,13 @@ __global__ void k_inverse_perm(const int32_t* new2old, int64_t n, int32_t* old2n
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i < n) old2new[new2old[i]] = static_cast<int32_t>(i);
 }
-__global__ void k_relabel_keys(const int32_t* rowid, const int32_t* col, const int32_t* old2new,
-                               int64_t nnz, int bits, uint64_t* keys) {
+__global__ void k_relabel_pairs(const int32_t* rowid, const int32_t* col, const int32_t* old2new,
+                                int64_t nnz, uint32_t* new_col, uint32_t* new_row) {
   const int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (p < nnz)
-    keys[p] = (static_cast<uint64_t>(old2new[rowid[p]]) << bits) |
-              static_cast<uint64_t>(old2new[col[p]]);
+  if (p < nnz) {
+    new_col[p] = static_cast<uint32_t>(old2new[col[p]]);
+    new_row[p] = static_cast<uint32_t>(old2new[rowid[p]]);
+  }
 }
 __global__ void k_gather_i32(const int32_t* src, const int32_t* idx, int64_t n, int32_t* dst) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -628,24 +629,36 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
     k_gather_i32<<<ceil_div(n, 256), 256, 0, s>>>(g->rowdeg.p, P.new2old.p, n, P.deg.p);
     GBX_LAUNCHED();
   }
-  // relabeled AT: one radix sort of (new row, new col) keys -- every row's
-  // columns ascending in the new ids (the thread-per-row bins then read the
-  // hub end of x together at each step: ~2% of the iteration time against a
-  // copy that keeps the old column order)
+  // relabeled AT, every row's columns ascending in the new ids (the thread-
+  // per-row bins then read the hub end of x together at each step): two
+  // stable 32-bit radix sorts -- by new column carrying the new row, then by
+  // new row carrying the column -- instead of one sort of 64-bit (row, col)
+  // keys (2*bits digits): 5.1 -> ~1.5 ms at scale 22
   const int bits = bits_for(std::max<int64_t>(n, 2));
+  P.trp.alloc(n + 1);
+  P.tcol.alloc(std::max<int64_t>(nnz, 1));
   if (nnz) {
-    Tmp<uint64_t> k0(nnz, s), k1(nnz, s);
+    Tmp<uint32_t> kc(nnz, s), kc2(nnz, s), vr(nnz, s), vr2(nnz, s);
     {
       Tmp<int32_t> rowid(nnz, s);
       expand_rows_into(s, AT, rowid.p);
-      k_relabel_keys<<<ceil_div(nnz, 256), 256, 0, s>>>(rowid.p, AT.col.p, P.old2new.p, nnz,
-                                                          bits, k0.p);
+      k_relabel_pairs<<<ceil_div(nnz, 256), 256, 0, s>>>(rowid.p, AT.col.p, P.old2new.p, nnz,
+                                                         kc.p, vr.p);
       GBX_LAUNCHED();
     }
-    uint64_t* sorted = sort_keys(s, k0.p, k1.p, nnz, 2 * bits);
-    csr_from_sorted_keys(s, n, bits, sorted, nnz, P.trp, P.tcol);
+    size_t tb = 0;
+    GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kc.p, kc2.p, vr.p, vr2.p, nnz, 0, bits, s));
+    {
+      Tmp<uint8_t> t(tb, s);
+      GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kc.p, kc2.p, vr.p, vr2.p, nnz, 0, bits, s));
+      // by new row (stable): (row, col) order; the columns land in tcol
+      GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, vr2.p, vr.p, kc2.p,
+                                               reinterpret_cast<uint32_t*>(P.tcol.p), nnz, 0, bits,
+                                               s));
+    }
+    rowptr_from_sorted_rows32(s, n, vr.p, nnz, P.trp.p);
   } else {
-    csr_from_sorted_keys(s, n, bits, nullptr, 0, P.trp, P.tcol);
+    GBX_CUDA(cudaMemsetAsync(P.trp.p, 0, (n + 1) * sizeof(int64_t), s));
   }
   GBX_CUDA(cudaStreamSynchronize(s));
 }
