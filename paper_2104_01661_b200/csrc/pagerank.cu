@@ -316,21 +316,27 @@ __global__ void __launch_bounds__(BS, BS == 1024 ? 2 : GBX_PR_MINB) k_pr_rows(Pr
 // reaches the same convergence decision (pagerank.cpp:65-74).  Replaces the
 // graph's two kernel nodes + conditional per iteration (~20 us of launch gaps
 // per iteration against ~200 us of row work) with two grid barriers.
-template <typename V>
-__global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist(PrArgs<V> a) {
+// BS = kPrThreads: several CTAs per SM, the hot prefix of x in L1 only.  BS =
+// 1024: ONE CTA per SM (64 registers per thread) holding x[0, hot) in shared
+// memory, restaged after every grid barrier -- the hot gathers leave the
+// L1 -> L2 request path (one sector request per cycle per SM, the measured
+// limiter of the L1 variant).
+template <typename V, int BS>
+__global__ void __launch_bounds__(BS, BS == 1024 ? 1 : GBX_PR_MINB) k_pr_persist(PrArgs<V> a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  using BlockReduce = cub::BlockReduce<double, kPrThreads>;
+  using BlockReduce = cub::BlockReduce<double, BS>;
   __shared__ typename BlockReduce::TempStorage red;
   __shared__ PrBin s_bins[kPrBinsMax];
   __shared__ int s_stop;
-  V* s_x = nullptr;  // (no shared-memory hot prefix in this variant: a.hot == 0)
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  V* s_x = reinterpret_cast<V*>(s_raw);  // a.hot entries (0: unused)
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int k = 0;; ++k) {
     if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 2], pr_gtimer());
-    const double blk = pr_rows_phase<V, kPrThreads>(a, k, red, s_bins, s_x);
+    const double blk = pr_rows_phase<V, BS>(a, k, red, s_bins, s_x);
     if (threadIdx.x == 0) {
       a.l1_rows[blockIdx.x] = blk;
       if (a.ktime) atomicMax(&a.ktime[(k % 128) * 2 + 1], pr_gtimer());
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist(PrArgs<V
     grid.sync();
     // every CTA: all partials in a fixed order -> the same total everywhere
     double part = 0.0;
-    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += kPrThreads)
+    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += BS)
       part += __ldcg(&a.l1_rows[b]) + __ldcg(&a.l1_fin[b]);
     __syncthreads();
     const double tot = BlockReduce(red).Sum(part);
@@ -833,7 +839,14 @@ static PrArgs<V> make_args(PrPlan& P, double damping, double tol, int itermax) {
   a.fin_cnt = P.blk_cnt.p;
   a.row0 = 0;
   a.hot = std::min<int64_t>(P.n, hot_bytes() / static_cast<int64_t>(sizeof(V))) & ~int64_t(3);
-  a.l1hot = std::min<int64_t>(P.n, l1_hot_bytes() / static_cast<int64_t>(sizeof(V)));
+  // with a shared-memory prefix, the L1 evict_last window follows it
+  // (GBX_PR_L1X_KB bytes of x past the prefix)
+  static const int64_t l1x = [] {
+    const char* e = std::getenv("GBX_PR_L1X_KB");
+    return static_cast<int64_t>(e ? std::atoi(e) : 48) * 1024;
+  }();
+  a.l1hot = a.hot > 0 ? std::min<int64_t>(P.n, a.hot + l1x / static_cast<int64_t>(sizeof(V)))
+                      : std::min<int64_t>(P.n, l1_hot_bytes() / static_cast<int64_t>(sizeof(V)));
   a.grid_rows = rows_grid<V>(a);
   a.damping = damping;
   a.teleport = (1.0 - damping) / static_cast<double>(P.n);
@@ -917,20 +930,38 @@ static bool build_graph(PrPlan& P, double damping, double tol, int itermax) {
   return true;
 }
 
-// the persistent variant needs every CTA resident (cooperative launch) and
-// no shared-memory hot prefix
+// the persistent variant needs every CTA resident (cooperative launch): one
+// CTA per SM with the shared-memory hot prefix (a.hot > 0), else as many
+// kPrThreads CTAs as fit
 template <typename V>
-static bool persist_ok(PrPlan& P, double damping, double tol, int itermax) {
-  PrArgs<V> a = make_args<V>(P, damping, tol, itermax);
-  if (a.hot > 0) return false;
+static void* persist_fn(const PrArgs<V>& a) {
+  return a.hot > 0 ? reinterpret_cast<void*>(k_pr_persist<V, 1024>)
+                   : reinterpret_cast<void*>(k_pr_persist<V, kPrThreads>);
+}
+
+template <typename V>
+static bool persist_args(PrPlan& P, double damping, double tol, int itermax, PrArgs<V>& a,
+                         int& block, size_t& smem) {
+  a = make_args<V>(P, damping, tol, itermax);
+  block = a.hot > 0 ? 1024 : kPrThreads;
+  smem = static_cast<size_t>(a.hot) * sizeof(V);
+  if (a.hot > 0) {
+    if (smem > 200 * 1024) return false;
+    if (cudaFuncSetAttribute(persist_fn<V>(a), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return false;
+    }
+  }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_persist<V>, kPrThreads, 0) !=
-      cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persist_fn<V>(a), block, smem) !=
+          cudaSuccess || per_sm < 1) {
     (void)cudaGetLastError();
     return false;
   }
-  return static_cast<int64_t>(per_sm) * device_sms() >= a.grid_rows &&
-         static_cast<int64_t>(P.l1_fin.n) >= a.grid_rows;
+  a.grid_rows = device_sms() * per_sm;
+  return static_cast<int64_t>(P.l1_fin.n) >= a.grid_rows &&
+         static_cast<int64_t>(P.l1_block.n) >= a.grid_rows;
 }
 
 template <typename V>
@@ -947,11 +978,13 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
   // nodes of a graph that holds conditional nodes)
   static const bool no_graph = std::getenv("GBX_PR_NO_GRAPH") != nullptr;
   static const bool use_graph = std::getenv("GBX_PR_GRAPH") != nullptr;
-  if (!no_graph && !use_graph && persist_ok<V>(P, damping, tol, itermax)) {
-    PrArgs<V> a = make_args<V>(P, damping, tol, itermax);
-    void* args[] = {&a};
-    GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_pr_persist<V>),
-                                         dim3(a.grid_rows), dim3(kPrThreads), args, 0, s));
+  PrArgs<V> pa{};
+  int pblock = 0;
+  size_t psmem = 0;
+  if (!no_graph && !use_graph && persist_args<V>(P, damping, tol, itermax, pa, pblock, psmem)) {
+    void* args[] = {&pa};
+    GBX_CUDA(cudaLaunchCooperativeKernel(persist_fn<V>(pa), dim3(pa.grid_rows), dim3(pblock), args,
+                                         psmem, s));
     P.last_persist = true;
   } else if (!no_graph && build_graph<V>(P, damping, tol, itermax)) {
     GBX_CUDA(cudaGraphLaunch(P.exec, s));

@@ -148,6 +148,9 @@ struct SsspPlan {
   DevArray<double> split_wd;
   DevArray<int32_t> sq;            // settled list of the current bucket
   DevArray<uint32_t> sbits;        // its membership bitmap
+  // per-vertex edge ranges {begin, light end, end, 0} (nnz < 2^32): one 16-byte
+  // load per popped vertex instead of row_ptr[u], row_ptr[u+1] and nlight[u]
+  DevArray<uint4> vmeta;
 };
 
 // Row-partitioned batched Brandes (bc.cu, sharded protocol): this rank owns

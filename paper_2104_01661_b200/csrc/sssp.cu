@@ -70,7 +70,16 @@ struct PackedEdges {
   const uint32_t* e;
   __device__ __forceinline__ void get(int64_t p, int32_t& v, uint32_t& w) const {
     uint32_t x;
+#ifdef GBX_SSSP_EDGE_EF
+    // the edge stream is read once per relaxation pass: evict-first in L2 so
+    // it does not push the distance array out
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(x) : "l"(e + p), "l"(pol));
+#else
     asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(x) : "l"(e + p));
+#endif
     v = static_cast<int32_t>(x >> 8);
     w = x & 0xffu;
   }
@@ -335,6 +344,7 @@ struct SsspBArgs {
   // (they always land in a later bucket).  nl == nullptr: every edge in the
   // near phase (label-correcting).
   const int32_t* nl;
+  const uint4* vm;     // {begin, light end, end, 0} per vertex, or nullptr
   int32_t* sq;
   uint32_t* sbits;
   int light_group;     // lanes per vertex in the light (near) phase: 1, 2 or 4
@@ -445,10 +455,19 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
       const int32_t u = active ? list[qi] : 0;
       const uint32_t ubit = 1u << (u & 31);
       if (active && si == 0 && pop_bits) atomicAnd(&pop_bits[u >> 5], ~ubit);
-      int64_t p = active ? a.rp[u] : 0;
-      int64_t e = active ? a.rp[u + 1] : 0;
-      if (active && phase == 1) e = p + a.nl[u];
-      if (active && phase == 2) p += a.nl[u];
+      int64_t p = 0, e = 0;
+      if (a.vm) {
+        if (active) {
+          const uint4 m = __ldg(a.vm + u);
+          p = phase == 2 ? m.y : m.x;
+          e = phase == 1 ? m.y : m.z;
+        }
+      } else {
+        p = active ? a.rp[u] : 0;
+        e = active ? a.rp[u + 1] : 0;
+        if (active && phase == 1) e = p + a.nl[u];
+        if (active && phase == 2) p += a.nl[u];
+      }
       if (p >= e) active = false;
       const D du = active ? *(volatile D*)&a.dist[u] : D(0);
       while (__any_sync(kFullW, active)) {
@@ -503,8 +522,17 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
       const int qi = base + g4;
       bool active = qi < c;
       const int32_t u = active ? win[qi] : 0;
-      int64_t p = active ? a.rp[u] + a.nl[u] : 0;
-      const int64_t e = active ? a.rp[u + 1] : 0;
+      int64_t p = 0, e = 0;
+      if (active) {
+        if (a.vm) {
+          const uint4 m = __ldg(a.vm + u);
+          p = m.y;
+          e = m.z;
+        } else {
+          p = a.rp[u] + a.nl[u];
+          e = a.rp[u + 1];
+        }
+      }
       if (p >= e) active = false;
       const D du = active ? *(volatile D*)&a.dist[u] : D(0);
       while (__any_sync(kFullW, active)) {
@@ -785,6 +813,13 @@ __global__ void k_split_cw(const int64_t* rp, int64_t n, double delta, const int
   nl[u] = static_cast<int32_t>(c);
 }
 
+__global__ void k_vmeta(const int64_t* rp, const int32_t* nl, int64_t n, uint4* vm) {
+  const int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (u >= n) return;
+  const uint32_t b = static_cast<uint32_t>(rp[u]);
+  vm[u] = make_uint4(b, b + static_cast<uint32_t>(nl[u]), static_cast<uint32_t>(rp[u + 1]), 0u);
+}
+
 // (re)partition the plan's edges for delta; any row order is valid for the
 // label-correcting sweep, so the packed edges are partitioned in place of the
 // plan's own copy and re-partitioned when delta changes
@@ -829,6 +864,12 @@ static void ensure_split(gbx_graph* g, SsspPlan& P, double delta) {
     }
   } else if (n > 0) {
     GBX_CUDA(cudaMemsetAsync(P.nlight.p, 0, n * 4, s));
+  }
+  static const bool no_vm = std::getenv("GBX_SSSP_NOVM") != nullptr;
+  if (n > 0 && A.nnz < (int64_t(1) << 32) && !no_vm) {
+    if (!P.vmeta.p) P.vmeta.alloc(n);
+    k_vmeta<<<ceil_div(n, 256), 256, 0, s>>>(A.rp.p, P.nlight.p, n, P.vmeta.p);
+    GBX_LAUNCHED();
   }
   GBX_CUDA(cudaStreamSynchronize(s));
   P.split_delta = delta;
@@ -926,7 +967,10 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     int max_persist = 0;
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, g->device);
     const size_t bytes = static_cast<size_t>(n) * sizeof(D);
-    if (max_persist > 0) {
+    static const bool no_persist = std::getenv("GBX_SSSP_NOPERSIST") != nullptr;
+    if (std::getenv("GBX_SSSP_TLOG"))
+      std::fprintf(stderr, "sssp: max persisting L2 %d bytes, dist %zu bytes\n", max_persist, bytes);
+    if (max_persist > 0 && !no_persist) {
       // the set-aside is a device-wide setting (and costly to change): grow only
       static size_t set_aside[64] = {0};
       const size_t want = std::min<size_t>(bytes, max_persist);
@@ -980,6 +1024,7 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
       static const int lg = std::getenv("GBX_SSSP_LG") ? std::atoi(std::getenv("GBX_SSSP_LG")) : 2;
       b.light_group = lg;
       b.nl = P.nlight.p;
+      b.vm = P.vmeta.p;
       b.sq = P.sq.p;
       b.sbits = P.sbits.p;
       GBX_CUDA(cudaMemsetAsync(P.sbits.p, 0, P.sbits.bytes(), s));
