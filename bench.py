@@ -108,8 +108,14 @@ def dist_env():
     return ws, rank, local
 
 
+def force_sharded():
+    """GBX_BENCH_SHARDED=1 under torchrun --nproc-per-node 1: the N>1 code path
+    (NCCL group, sharded driver) on one GPU, for testing it end to end."""
+    return os.environ.get("GBX_BENCH_SHARDED") == "1" and "MASTER_ADDR" in os.environ
+
+
 def maybe_init_dist(ws, local):
-    if ws <= 1:
+    if ws <= 1 and not force_sharded():
         return None
     import torch
     import torch.distributed as dist
@@ -228,12 +234,16 @@ def run_reference(args):
 
 # ---------------------------------------------------------------- our arm: PageRank
 def bench_pagerank_sharded(args, dist, ws, rank, local):
-    """N > 1: one process per GPU, row blocks of the relabeled AT, NCCL all-gather
-    of the contribution slices + all-reduce of the L1 partial per iteration
-    (paper_2104_01661_b200/dist.py).  Total work fixed -> strong scaling."""
+    """N > 1: one process per GPU, row blocks of the relabeled AT, one NCCL
+    all_gather_into_tensor of the padded contribution slices + one fp64 L1
+    all-reduce per iteration (paper_2104_01661_b200/dist.py).  Total work
+    fixed -> strong scaling."""
+    import ctypes as C
+
     import torch
     import paper_2104_01661_b200 as P
     from paper_2104_01661_b200.dist import GpuShardBackend, sharded_pagerank
+    from paper_2104_01661_b200.graph import Graph, call
 
     scale = args.scale or 22
     P.init(local)
@@ -242,6 +252,7 @@ def bench_pagerank_sharded(args, dist, ws, rank, local):
     P.property_at(g)
     P.property_rowdegree(g)
     n, nnz, _, _ = g.info()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     for _ in range(max(args.warmup, 3)):
         be = GpuShardBackend(g)
         _, iters = sharded_pagerank(be, dist, 0.85, 1e-4, 100)
@@ -250,17 +261,41 @@ def bench_pagerank_sharded(args, dist, ws, rank, local):
         for _ in range(args.steps):
             be = GpuShardBackend(g)
             be.prepare(rank, ws)  # plan outside the timed region
+            flush.zero_()
             barrier(dist)
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            _, iters = sharded_pagerank(_Prepared(be), dist, 0.85, 1e-4, 100)
+            _, iters = sharded_pagerank(_Prepared(be), dist, 0.85, 1e-4, 100, to_host=False)
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
     t = max_over_ranks(dist, sum(times) / len(times))
     value = nnz * iters / t
+    # e2e: every rank builds its copy of the graph from pinned host CSR through
+    # the C ABI (H2D + validation), fills AT / degrees (basic mode), plans its
+    # row block and runs the sharded iterations; the ranks come back to the host
+    # (D2H, original order) -- device time max over ranks, wall clock per rank
+    rp, col, _ = g.export()
+    rp_h = torch.from_numpy(rp).pin_memory()
+    col_h = torch.from_numpy(col).pin_memory()
+    e2e_times = []
+    for s_ in range(3):
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = C.c_void_p()
+        call("gbx_graph_new32", C.byref(h), n, rp_h.data_ptr(), col_h.data_ptr(), None, 0, 0)
+        gh = Graph(h)
+        P.property_at(gh)
+        P.property_rowdegree(gh)
+        _, it2 = sharded_pagerank(GpuShardBackend(gh), dist, 0.85, 1e-4, 100)
+        dt = time.perf_counter() - t0
+        gh.free()
+        if s_ > 0:
+            e2e_times.append(dt)
+    t_e2e = max_over_ranks(dist, statistics.median(e2e_times))
     out = {"metric": METRIC, "value": value, "unit": "edges/s/iter", "n_gpus": ws,
            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t * 1e3,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -268,8 +303,17 @@ def bench_pagerank_sharded(args, dist, ws, rank, local):
            "data": "synthetic (seeded R-MAT, generated in HBM)",
            "config": {"workload": f"pagerank_rmat{scale}_directed", "scale": scale, "n": n,
                       "nnz": nnz, "iterations": iters, "parallelism": f"rowblock{ws}",
-                      "exchange": "NCCL all_gather (x slices) + all_reduce (L1) per iteration"},
-           "gpu_launches": int(2 * iters * args.steps), "clocks": clk.summary()}
+                      "exchange": "NCCL all_gather_into_tensor (padded x slices) + "
+                                  "all_reduce (L1) per iteration",
+                      "l2": "flushed (256 MB write) before every step"},
+           "e2e": {"value": nnz * it2 / t_e2e, "unit": "edges/s/iter",
+                   "h2d_bytes_per_step": int(rp.nbytes + col.nbytes),
+                   "d2h_bytes_per_step": int(n * 8),
+                   "includes": "per rank: H2D CSR (pinned), graph_new32 validation, "
+                               "property_at, property_rowdegree, shard plan, sharded "
+                               "iterations, D2H ranks",
+                   "samples_ms": [round(x * 1e3, 2) for x in e2e_times]},
+           "gpu_launches": int(2 * (iters + 1) * args.steps), "clocks": clk.summary()}
     return out, (scale,)
 
 
@@ -595,7 +639,7 @@ def main():
         return run_reference(args)
     ws, rank, local = dist_env()
     dist = maybe_init_dist(ws, local)
-    if args.workload == "pagerank" and ws > 1:
+    if args.workload == "pagerank" and (ws > 1 or force_sharded()):
         out, extra = bench_pagerank_sharded(args, dist, ws, rank, local)
     elif args.workload == "pagerank":
         out, extra = bench_pagerank(args, dist, ws, rank, local)

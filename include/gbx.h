@@ -331,21 +331,31 @@ int gbx_last_stats(const gbx_graph* g, gbx_stats* stats, char msg[GBX_MSG_LEN]);
 /* ---- sharded PageRank for the multi-GPU driver (1D row blocks) -------------
  * pagerank.cpp:52-76 split over ranks.  Every rank holds the graph; rank r of
  * nranks owns rows [row_begin, row_end) of the in-degree-relabeled AT (balanced
- * by rows + nnz).  Vectors live in relabeled ids:
- *   gbx_pr_shard_init   x_full[n] = initial contributions, r_local = 1/n;
- *   gbx_pr_shard_step   for its rows: r = teleport + sum x(k) (fp64), x_new[row]
- *                       = r * damping / outdeg (written at relabeled ids in a
- *                       full-length buffer), *l1_dev = fp64 L1 partial;
- *   the caller all-gathers the x_new slices (NCCL) and all-reduces l1;
- *   gbx_pr_shard_unpermute maps a gathered relabeled rank vector back to the
+ * by rows + nnz; every rank computes the same split).  Exchange layout: rank
+ * q's contributions live at x_full[q * chunk + (row - bounds[q])], chunk = the
+ * longest block rounded up to even + 2 (gbx_pr_shard_layout), so x_full has
+ * nranks * chunk floats; the last 8 bytes of every slot are free for the rank's
+ * fp64 L1 partial (pass l1_dev = (double*)(x_slice + chunk - 2)), so ONE
+ * equal-size all-gather of the chunk-long slices (NCCL all_gather_into_tensor)
+ * per iteration moves the contributions and every partial in place.
+ *   gbx_pr_shard_init   x_full (padded) = initial contributions, r_local = 1/n;
+ *   gbx_pr_shard_step   for its rows: r_new = teleport + sum x(k) (fp64),
+ *                       x_slice[row - row_begin] = r_new * damping / outdeg,
+ *                       *l1_dev = fp64 L1 partial |r_prev - r_new| (r_prev may
+ *                       alias r_new); the caller all-gathers the slices and
+ *                       sums the partials (pagerank.cpp:65-74 on the sum);
+ *   gbx_pr_shard_unpermute maps a gathered (padded) rank vector back to the
  *                       original vertex order (fp64, host).
  * All vector arguments are device pointers. */
 int gbx_pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* row_begin,
                          int64_t* row_end, char msg[GBX_MSG_LEN]);
+/* chunk (slot length of the padded layout) and, if non-NULL, bounds[nranks+1]. */
+int gbx_pr_shard_layout(const gbx_graph* g, int64_t* chunk, int64_t* bounds,
+                        char msg[GBX_MSG_LEN]);
 int gbx_pr_shard_init(gbx_graph* g, float* x_full_dev, float* r_local_dev, double damping,
                       char msg[GBX_MSG_LEN]);
-int gbx_pr_shard_step(gbx_graph* g, const float* x_full_dev, float* r_dev,
-                      float* x_new_dev, double* l1_dev, double damping,
+int gbx_pr_shard_step(gbx_graph* g, const float* x_full_dev, const float* r_prev_dev,
+                      float* r_new_dev, float* x_slice_dev, double* l1_dev, double damping,
                       char msg[GBX_MSG_LEN]);
 int gbx_pr_shard_unpermute(gbx_graph* g, const float* r_full_dev, double* rank_out,
                            char msg[GBX_MSG_LEN]);

@@ -835,12 +835,21 @@ int gbx_pr_shard_unpermute(gbx_graph* g, const float* r_full, double* out, char*
   });
 }
 
-int gbx_pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, double* l1,
-                      double damping, char* msg) {
+int gbx_pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, float* r_new,
+                      float* x_slice, double* l1, double damping, char* msg) {
   return guard(msg, [&] {
     need(g);
+    if (!x_full || !r_prev || !r_new || !x_slice || !l1)
+      gbx::fail(GBX_NULL_ARGUMENT, "pr_shard_step: NULL device buffer");
     gbx::Scope sc(g);
-    gbx::pr_shard_step(g, x_full, r, x_new, l1, damping);
+    gbx::pr_shard_step(g, x_full, r_prev, r_new, x_slice, l1, damping);
+  });
+}
+
+int gbx_pr_shard_layout(const gbx_graph* gc, int64_t* chunk, int64_t* bounds, char* msg) {
+  return guard(msg, [&] {
+    gbx_graph* g = need(gc);
+    gbx::pr_shard_layout(g, chunk, bounds);
   });
 }
 

@@ -257,8 +257,9 @@ void cc_run(gbx_graph* g, int64_t* label, int* iters);
 void pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* rb, int64_t* re);
 void pr_shard_init(gbx_graph* g, float* x_full, float* r_local, double damping);
 void pr_shard_unpermute(gbx_graph* g, const float* r_full, double* out_host);
-void pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, double* l1,
-                   double damping);
+void pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, float* r_new,
+                   float* x_slice, double* l1, double damping);
+void pr_shard_layout(gbx_graph* g, int64_t* chunk, int64_t* bounds);
 void partition_rows(const gbx_graph* g, int parts, bool transposed, int64_t* bounds);
 void result_device(const gbx_graph* g, const std::string& which, void** ptr, int64_t* count);
 

@@ -1067,8 +1067,24 @@ void pagerank_run(gbx_graph* g, double damping, double tol, int itermax, double*
 
 // ---- sharded step (multi-GPU driver) ----------------------------------------------
 // Shards own contiguous blocks of the RELABELED rows, balanced by rows + nnz
-// (merge-path split); x vectors are in relabeled ids, so the driver all-gathers
-// the x_new slices as they are and un-permutes the final ranks once.
+// (merge-path split).  The exchange layout is padded: rank q's rows keep their
+// contributions at x_full[q * chunk + (row - bounds[q])] (chunk = the longest
+// block), so the driver's one equal-size all-gather (NCCL
+// all_gather_into_tensor) lands every slice in place with no unpacking copies;
+// the shard's column indices are remapped to that layout once, at prepare.
+
+__device__ __forceinline__ int64_t pr_pad_index(const int64_t* bounds, int nranks, int64_t chunk,
+                                                int64_t i) {
+  int q = 0;
+  while (q + 1 < nranks && i >= bounds[q + 1]) ++q;
+  return static_cast<int64_t>(q) * chunk + (i - bounds[q]);
+}
+
+__global__ void k_pr_pad_cols(int32_t* col, int64_t nnz, const int64_t* bounds, int nranks,
+                              int64_t chunk) {
+  const int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p < nnz) col[p] = static_cast<int32_t>(pr_pad_index(bounds, nranks, chunk, col[p]));
+}
 
 void pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* rb_out, int64_t* re_out) {
   require_at(g, "pr_shard");
@@ -1092,9 +1108,29 @@ void pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* rb_out, int64
     }
     return lo;
   };
-  const int64_t rb = split(rank), re = std::max(rb, split(rank + 1));
+  // every rank computes the same bounds from the same relabeled AT
+  S->bounds.assign(nranks + 1, 0);
+  for (int q = 1; q <= nranks; ++q) S->bounds[q] = std::max(S->bounds[q - 1], split(q));
+  // slot = the longest block rounded up to even + 2 floats: the slot's last
+  // 8 bytes carry the rank's fp64 L1 partial, so ONE all-gather per
+  // iteration moves both the contributions and every partial
+  int64_t longest = 1;
+  for (int q = 0; q < nranks; ++q) longest = std::max(longest, S->bounds[q + 1] - S->bounds[q]);
+  S->chunk = ((longest + 1) & ~int64_t(1)) + 2;
+  if (S->chunk * nranks >= (int64_t(1) << 31))
+    fail(GBX_INVALID_VALUE, "pr_shard: padded exchange layout exceeds int32 column ids");
+  const int64_t rb = S->bounds[rank], re = S->bounds[rank + 1];
   plan_rows(g, P, rb, re);
+  S->dbounds.alloc(nranks + 1);
+  GBX_CUDA(cudaMemcpyAsync(S->dbounds.p, S->bounds.data(), (nranks + 1) * 8,
+                           cudaMemcpyHostToDevice, g->stream));
+  if (P.nnz) {
+    k_pr_pad_cols<<<ceil_div(P.nnz, 256), 256, 0, g->stream>>>(P.tcol.p, P.nnz, S->dbounds.p,
+                                                                 nranks, S->chunk);
+    GBX_LAUNCHED();
+  }
   P.invf.alloc(std::max<int64_t>(P.n, 1));
+  GBX_CUDA(cudaStreamSynchronize(g->stream));
   S->nranks = nranks;
   S->rank = rank;
   g->prs = std::move(S);
@@ -1102,28 +1138,39 @@ void pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* rb_out, int64
   if (re_out) *re_out = re;
 }
 
+void pr_shard_layout(gbx_graph* g, int64_t* chunk, int64_t* bounds) {
+  if (!g->prs) fail(GBX_MISSING_PROPERTY, "pr_shard_layout needs gbx_pr_shard_prepare");
+  if (chunk) *chunk = g->prs->chunk;
+  if (bounds) std::copy(g->prs->bounds.begin(), g->prs->bounds.end(), bounds);
+}
+
 __global__ void k_pr_shard_init(float* x, float* r_local, float* inv, const int32_t* outdeg,
-                                int64_t n, int64_t rb, int64_t re, double damping) {
+                                int64_t n, int64_t rb, int64_t re, double damping,
+                                const int64_t* bounds, int nranks, int64_t chunk) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const double r0 = 1.0 / static_cast<double>(n);
   const int dg = outdeg[i];
-  x[i] = dg > 0 ? static_cast<float>(r0 / (static_cast<double>(dg) / damping)) : 0.f;
+  x[pr_pad_index(bounds, nranks, chunk, i)] =
+      dg > 0 ? static_cast<float>(r0 / (static_cast<double>(dg) / damping)) : 0.f;
   inv[i] = dg > 0 ? static_cast<float>(damping / static_cast<double>(dg)) : 0.f;
   if (i >= rb && i < re) r_local[i - rb] = static_cast<float>(r0);
 }
 
 void pr_shard_init(gbx_graph* g, float* x_full, float* r_local, double damping) {
   if (!g->prs) fail(GBX_MISSING_PROPERTY, "pr_shard_init needs gbx_pr_shard_prepare");
-  PrPlan& P = g->prs->plan;
+  PrShard& S = *g->prs;
+  PrPlan& P = S.plan;
+  GBX_CUDA(cudaMemsetAsync(x_full, 0, S.chunk * S.nranks * sizeof(float), g->stream));
   k_pr_shard_init<<<ceil_div(std::max<int64_t>(P.n, 1), 256), 256, 0, g->stream>>>(
-      x_full, r_local, P.invf.p, P.deg.p, P.n, P.row0, P.row1, damping);
+      x_full, r_local, P.invf.p, P.deg.p, P.n, P.row0, P.row1, damping, S.dbounds.p, S.nranks,
+      S.chunk);
   GBX_LAUNCHED();
   P.g_damping = damping;
 }
 
-void pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, double* l1,
-                   double damping) {
+void pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, float* r_new,
+                   float* x_slice, double* l1, double damping) {
   if (!g->prs) fail(GBX_MISSING_PROPERTY, "pr_shard_step needs gbx_pr_shard_prepare");
   PrPlan& P = g->prs->plan;
   cudaStream_t s = g->stream;
@@ -1136,10 +1183,10 @@ void pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, do
   PrArgs<float> a = make_args<float>(P, damping, 0.0, 1 << 30);
   a.inv = P.invf.p;
   a.fixed = 1;
-  a.x0 = const_cast<float*>(x_full);
-  a.x1 = x_new;  // written at relabeled global row ids
-  a.r0 = r;      // r_prev (local rows), overwritten in place by r_new
-  a.r1 = r;
+  a.x0 = const_cast<float*>(x_full);  // padded layout (tcol remapped to it)
+  a.x1 = x_slice - P.row0;            // x_nxt[row] -> x_slice[row - row0]
+  a.r0 = const_cast<float*>(r_prev);  // local rows; may alias r_new
+  a.r1 = r_new;
   a.row0 = P.row0;
   a.hot = 0;
   a.grid_rows = rows_grid<float>(a);
@@ -1152,19 +1199,21 @@ void pr_shard_step(gbx_graph* g, const float* x_full, float* r, float* x_new, do
   g->prs->steps++;
 }
 
-__global__ void k_pr_unpermute_f(const float* r, const int32_t* new2old, int64_t n, double* out) {
+__global__ void k_pr_unpermute_f(const float* r, const int32_t* new2old, int64_t n, double* out,
+                                 const int64_t* bounds, int nranks, int64_t chunk) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < n) out[new2old[i]] = static_cast<double>(r[i]);
+  if (i < n) out[new2old[i]] = static_cast<double>(r[pr_pad_index(bounds, nranks, chunk, i)]);
 }
 
 void pr_shard_unpermute(gbx_graph* g, const float* r_full, double* out_host) {
   if (!g->prs) fail(GBX_MISSING_PROPERTY, "pr_shard_unpermute needs gbx_pr_shard_prepare");
-  PrPlan& P = g->prs->plan;
+  PrShard& S = *g->prs;
+  PrPlan& P = S.plan;
   cudaStream_t s = g->stream;
   double* tmp = nullptr;
   GBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), std::max<int64_t>(P.n, 1) * 8, s));
-  k_pr_unpermute_f<<<ceil_div(std::max<int64_t>(P.n, 1), 256), 256, 0, s>>>(r_full, P.new2old.p,
-                                                                            P.n, tmp);
+  k_pr_unpermute_f<<<ceil_div(std::max<int64_t>(P.n, 1), 256), 256, 0, s>>>(
+      r_full, P.new2old.p, P.n, tmp, S.dbounds.p, S.nranks, S.chunk);
   cudaError_t le = cudaGetLastError();
   if (le == cudaSuccess) le = cudaMemcpyAsync(out_host, tmp, P.n * 8, cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(tmp, s);

@@ -63,6 +63,12 @@ struct PrShard {
   PrPlan plan;
   int64_t steps = 0;
   int rank = 0, nranks = 1;
+  // padded exchange layout: rank q's rows [bounds[q], bounds[q+1]) keep their
+  // contributions at x_full[q * chunk + (row - bounds[q])], so one equal-size
+  // all-gather writes every slice in place (tcol is remapped to it)
+  std::vector<int64_t> bounds;
+  int64_t chunk = 1;
+  DevArray<int64_t> dbounds;
 };
 
 // BFS workspaces (bfs.cu).

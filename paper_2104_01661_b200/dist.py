@@ -5,10 +5,12 @@ compute.
 PageRank (config 2): 1D row blocks of the in-degree-relabeled AT, balanced by
 rows + nnz.  Per iteration every rank runs the fused shard step on its rows
 (gbx_pr_shard_step: sums, teleport, next contributions, fp64 L1 partial), then
-  * all-gather of the x slices (fp32, n/P per rank) -> the full x for the next
-    gather step, and
-  * all-reduce (sum) of the fp64 L1 partial, compared against tol exactly as
-    pagerank.cpp:65-74 does (same iteration count as the single-GPU path).
+  * one all_gather_into_tensor of the x slices (fp32, padded to the longest
+    block, so every slice lands in place) -> the full x for the next step; the
+    slots' last 8 bytes carry the fp64 L1 partials, summed in rank order and
+    compared against tol exactly as pagerank.cpp:65-74 does (same iteration
+    count as the single-GPU path), one iteration behind so the host check
+    overlaps the next queued iteration.
 Triangle count (config 3): U replicated, middle vertices split by probe work
 (gbx_tc_partition), one u64 all-reduce at the end.
 BFS (scale >= 22): 1D row blocks (32-aligned), one frontier-bitmap all-gather
@@ -54,31 +56,47 @@ def _gather_slices(dist, local, bounds, world, out):
     return out
 
 
-def sharded_pagerank(backend, dist, damping=0.85, tol=1e-4, itermax=100):
+def sharded_pagerank(backend, dist, damping=0.85, tol=1e-4, itermax=100, to_host=True):
     """GAP PageRank over `world` ranks; returns (rank vector on every rank (numpy,
-    original ids), iterations)."""
+    original ids), iterations).  to_host=False: the gathered (padded,
+    relabeled) rank vector stays on the device and is returned as is.
+
+    Per iteration k: the shard step (library stream), then ONE
+    all_gather_into_tensor of the chunk-long slices straight into the padded x
+    (gbx_pr_shard_layout) -- every slot carries its rank's fp64 L1 partial in
+    its last 8 bytes -- and an async copy of the world partials to the host,
+    summed there in rank order (the same total on every rank).
+    The convergence test of iteration k-1 (pagerank.cpp:74: stop when L1 < tol)
+    runs on the host while iteration k is already queued, so the host never
+    drains the device; r is double-buffered, so when k-1 converged the result
+    is r of k-1 and the speculative step k is discarded.  The iteration count
+    and ranks equal the sequential loop's."""
     import torch
     rank, world = dist.get_rank(), dist.get_world_size()
     rb, re, n = backend.prepare(rank, world)
-    dev = backend.device
-    b = torch.tensor([rb, re], dtype=torch.int64, device=dev)
-    allb = [torch.empty(2, dtype=torch.int64, device=dev) for _ in range(world)]
-    dist.all_gather(allb, b)
-    bounds = [int(t[0]) for t in allb] + [int(allb[-1][1])]
-    for p in range(world - 1):
-        assert int(allb[p][1]) == int(allb[p + 1][0]), "row blocks must tile [0, n)"
-    assert bounds[0] == 0 and bounds[-1] == n
+    chunk = backend.chunk
+    assert re - rb <= chunk
     backend.init(damping)
-    k = 0
+    x_full = backend.x_full()
+    assert x_full.numel() == world * chunk
+    pending = None
+    iters = 0
     for k in range(1, itermax + 1):
-        l1 = backend.step(damping)                 # device scalar (fp64)
-        dist.all_reduce(l1)                        # sum of the per-shard partials
-        _gather_slices(dist, backend.x_new_slice(), bounds, world, backend.x_full())
-        if not (float(l1.item()) >= tol):          # pagerank.cpp:74: stop when < tol
-            break
-    iters = min(k, itermax)
-    r_full = torch.empty(n, dtype=backend.r_local().dtype, device=dev)
-    _gather_slices(dist, backend.r_local(), bounds, world, r_full)
+        backend.step(damping, k)                   # r, x slice + its L1 partial (tail)
+        dist.all_gather_into_tensor(x_full, backend.x_new_slice())
+        tok = backend.l1_post(k)                   # every rank's partial -> host (async)
+        if pending is not None:
+            kk, tk = pending
+            if not (backend.l1_value(tk) >= tol):
+                iters = kk
+                break
+        pending = (k, tok)
+    else:
+        iters = pending[0] if pending is not None else 0
+    r_full = torch.empty(world * chunk, dtype=backend.r_local(iters).dtype, device=backend.device)
+    dist.all_gather_into_tensor(r_full, backend.r_local(iters))
+    if not to_host:
+        return r_full, iters
     return backend.unpermute(r_full), iters
 
 
@@ -203,41 +221,65 @@ class GpuShardBackend:
         import torch
 
         from .graph import call
-        rb, re = C.c_int64(), C.c_int64()
+        rb, re, chunk = C.c_int64(), C.c_int64(), C.c_int64()
         call("gbx_pr_shard_prepare", self.g.handle, rank, world, C.byref(rb), C.byref(re))
-        self.rb, self.re = rb.value, re.value
+        call("gbx_pr_shard_layout", self.g.handle, C.byref(chunk), None)
+        self.rb, self.re, self.chunk = rb.value, re.value, chunk.value
+        self.world = world
         self.n = self.g.n()
-        self._x = torch.empty(self.n, dtype=torch.float32, device=self.device)
-        self._xn = torch.empty(self.n, dtype=torch.float32, device=self.device)
-        self._r = torch.empty(max(self.re - self.rb, 1), dtype=torch.float32, device=self.device)
-        self._l1 = torch.zeros(1, dtype=torch.float64, device=self.device)
+        dev = self.device
+        self._x = torch.empty(world * self.chunk, dtype=torch.float32, device=dev)
+        self._xs = torch.zeros(self.chunk, dtype=torch.float32, device=dev)
+        self._r = [torch.zeros(self.chunk, dtype=torch.float32, device=dev) for _ in range(2)]
+        self._l1h = [torch.zeros(world, 1, dtype=torch.float64).pin_memory() for _ in range(2)]
+        self._ev = [torch.cuda.Event() for _ in range(2)]
         self._stream = torch.cuda.ExternalStream(self.g.stream())
         return self.rb, self.re, self.n
 
     def init(self, damping):
         from .graph import call
-        call("gbx_pr_shard_init", self.g.handle, self._x.data_ptr(), self._r.data_ptr(), damping)
+        call("gbx_pr_shard_init", self.g.handle, self._x.data_ptr(), self._r[0].data_ptr(),
+             damping)
 
-    def step(self, damping):
+    def step(self, damping, k):
+        """Iteration k (1-based): r_prev = buffer (k-1)&1, r_new = buffer k&1; the
+        fp64 L1 partial goes to the slice's last 8 bytes."""
         import torch
 
         from .graph import call
         # the library stream must see the x gathered on torch's stream
         self._stream.wait_stream(torch.cuda.current_stream())
-        call("gbx_pr_shard_step", self.g.handle, self._x.data_ptr(), self._r.data_ptr(),
-             self._xn.data_ptr(), self._l1.data_ptr(), damping)
+        call("gbx_pr_shard_step", self.g.handle, self._x.data_ptr(),
+             self._r[(k - 1) & 1].data_ptr(), self._r[k & 1].data_ptr(), self._xs.data_ptr(),
+             self._xs.data_ptr() + 4 * (self.chunk - 2), damping)
         # the collectives run on torch's stream: order them after the library's
         torch.cuda.current_stream().wait_stream(self._stream)
-        return self._l1
+
+    def l1_post(self, k):
+        """Queue the world's L1 partials of iteration k (gathered slot tails) for
+        the host: one strided async copy into pinned memory."""
+        import torch
+        tails = self._x.view(self.world, self.chunk)[:, self.chunk - 2:].view(torch.float64)
+        self._l1h[k & 1].copy_(tails, non_blocking=True)
+        self._ev[k & 1].record(torch.cuda.current_stream())
+        return k & 1
+
+    def l1_value(self, tok):
+        self._ev[tok].synchronize()
+        parts = self._l1h[tok]
+        tot = 0.0
+        for q in range(self.world):  # rank order: the same sum on every rank
+            tot += float(parts[q, 0])
+        return tot
 
     def x_new_slice(self):
-        return self._xn[self.rb:self.re]
+        return self._xs
 
     def x_full(self):
         return self._x
 
-    def r_local(self):
-        return self._r[: self.re - self.rb]
+    def r_local(self, k):
+        return self._r[k & 1]
 
     def unpermute(self, r_full):
         import torch

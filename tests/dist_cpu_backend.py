@@ -36,41 +36,62 @@ class CpuShardBackend:
                 else:
                     hi = mid
             return lo
-        self.rb, self.re = split(rank), max(split(rank), split(rank + 1))
-        self._x = torch.zeros(self.n, dtype=torch.float64)
-        self._xn = torch.zeros(self.n, dtype=torch.float64)
-        self._r = torch.zeros(max(self.re - self.rb, 1), dtype=torch.float64)
+        self.bounds = [0]
+        for q in range(1, world + 1):
+            self.bounds.append(max(self.bounds[-1], split(q)))
+        self.rb, self.re = self.bounds[rank], self.bounds[rank + 1]
+        # slot: the longest block + 1 fp64 for the rank's L1 partial (the GPU
+        # backend's fp32 slots carry it in their last two floats)
+        self.chunk = max(1, max(self.bounds[q + 1] - self.bounds[q] for q in range(world))) + 1
+        self.world = world
+        # padded exchange layout (gbx_pr_shard_layout): vertex i of owner q at
+        # q * chunk + (i - bounds[q])
+        own = np.searchsorted(np.asarray(self.bounds[1:]), np.arange(self.n), side="right")
+        self.pad = own * self.chunk + (np.arange(self.n) - np.asarray(self.bounds)[own])
+        self._x = torch.zeros(world * self.chunk, dtype=torch.float64)
+        self._xs = torch.zeros(self.chunk, dtype=torch.float64)
+        self._r = [torch.zeros(self.chunk, dtype=torch.float64) for _ in range(2)]
         return self.rb, self.re, self.n
 
     def init(self, damping):
         r0 = 1.0 / self.n
         x = np.where(self.deg > 0, r0 / (np.maximum(self.deg, 1) / damping), 0.0)
-        self._x[:] = torch.from_numpy(x)
-        self._r[: self.re - self.rb] = r0
+        xf = np.zeros(self.world * self.chunk)
+        xf[self.pad] = x
+        self._x[:] = torch.from_numpy(xf)
+        self._r[0][: self.re - self.rb] = r0
 
-    def step(self, damping):
-        x = self._x.numpy()
+    def step(self, damping, k):
+        x = self._x.numpy()[self.pad]
         teleport = (1 - damping) / self.n
+        rp, rn_buf = self._r[(k - 1) & 1], self._r[k & 1]
         l1 = 0.0
         for i in range(self.rb, self.re):
             s = float(x[self.tcol[self.trp[i]:self.trp[i + 1]]].sum())
             rn = teleport + s
-            l1 += abs(float(self._r[i - self.rb]) - rn)
-            self._r[i - self.rb] = rn
-            self._xn[i] = rn * damping / self.deg[i] if self.deg[i] > 0 else 0.0
-        return torch.tensor([l1], dtype=torch.float64)
+            l1 += abs(float(rp[i - self.rb]) - rn)
+            rn_buf[i - self.rb] = rn
+            self._xs[i - self.rb] = rn * damping / self.deg[i] if self.deg[i] > 0 else 0.0
+        self._xs[self.chunk - 1] = l1
+
+    def l1_post(self, k):
+        parts = self._x.view(self.world, self.chunk)[:, self.chunk - 1]
+        return sum(float(parts[q]) for q in range(self.world))
+
+    def l1_value(self, tok):
+        return tok
 
     def x_new_slice(self):
-        return self._xn[self.rb:self.re]
+        return self._xs
 
     def x_full(self):
         return self._x
 
-    def r_local(self):
-        return self._r[: self.re - self.rb]
+    def r_local(self, k):
+        return self._r[k & 1]
 
     def unpermute(self, r_full):
-        return r_full.numpy().copy()
+        return r_full.numpy()[self.pad].copy()
 
     # ---- triangle count (rows of the id-oriented U)
     def _upper(self, i):

@@ -447,38 +447,49 @@ def test_bc_partials_compose_on_one_gpu():
     assert float(be.bc_partial([]).abs().sum()) == 0.0
 
 
-def test_pr_shards_compose_on_one_gpu():
-    """Two shard plans (ranks 0 and 1 of 2) stepped in lockstep with the x
-    exchange done by hand equal the single-GPU PageRank: the shard kernels plus
-    the driver's bookkeeping (dist.py) without NCCL."""
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_pr_shards_compose_on_one_gpu(world):
+    """`world` shard plans stepped in lockstep with the padded all-gather done
+    by hand equal the single-GPU PageRank: the shard kernels plus the
+    driver's padded layout, double-buffered r and the lagged convergence test
+    (dist.sharded_pagerank) without NCCL (the ranks never wait on each other)."""
     import torch
     from paper_2104_01661_b200.dist import GpuShardBackend
-    world = 2
-    gs, bes, bounds = [], [], []
+    bes = []
     for r in range(world):
         g = P.generate_rmat(14, 16, seed=5)
         P.property_at(g)
         P.property_rowdegree(g)
         be = GpuShardBackend(g)
+        be.g_keep = g
         rb, re, n = be.prepare(r, world)
-        gs.append(g)
         bes.append(be)
-        bounds.append((rb, re))
-    assert bounds[0][0] == 0 and bounds[0][1] == bounds[1][0] and bounds[1][1] == n
+    chunk = bes[0].chunk
+    assert all(be.chunk == chunk for be in bes)
+    assert bes[0].rb == 0 and bes[-1].re == n
+    assert all(bes[q].re == bes[q + 1].rb for q in range(world - 1))
+    assert all(be.re - be.rb <= chunk for be in bes)
     for be in bes:
         be.init(0.85)
-    iters = 0
+    pending, iters = None, 0
     for k in range(1, 101):
-        l1 = sum(float(be.step(0.85).item()) for be in bes)
+        for be in bes:
+            be.step(0.85, k)
         torch.cuda.synchronize()
-        for be in bes:  # the all-gather, by hand
-            for src in bes:
-                be.x_full()[src.rb:src.re] = src.x_new_slice()
+        for be in bes:  # all_gather_into_tensor, by hand
+            for q, src in enumerate(bes):
+                be.x_full()[q * chunk:(q + 1) * chunk] = src.x_new_slice()
         torch.cuda.synchronize()
-        iters = k
-        if not (l1 >= 1e-4):
+        l1s = [be.l1_value(be.l1_post(k)) for be in bes]
+        assert all(v == l1s[0] for v in l1s)  # the same rank-order sum everywhere
+        l1 = l1s[0]
+        if pending is not None and not (pending[1] >= 1e-4):
+            iters = pending[0]
             break
-    r_full = torch.cat([be.r_local() for be in bes])
+        pending = (k, l1)
+    else:
+        iters = pending[0]
+    r_full = torch.cat([be.r_local(iters) for be in bes])
     got = bes[0].unpermute(r_full)
     ref = P.generate_rmat(14, 16, seed=5)
     P.property_at(ref)
