@@ -242,8 +242,32 @@ def bench_pagerank_sharded(args, dist, ws, rank, local):
 
     import torch
     import paper_2104_01661_b200 as P
-    from paper_2104_01661_b200.dist import GpuShardBackend, sharded_pagerank
+    from paper_2104_01661_b200.dist import (GpuShardBackend, sharded_pagerank,
+                                            sharded_pagerank_p2p)
     from paper_2104_01661_b200.graph import Graph, call
+
+    # the exchange: "p2p" (default) fuses it into one cooperative kernel per
+    # rank (peer stores over NVLink via symmetric memory, device-side barrier);
+    # "nccl" = one all_gather_into_tensor per iteration from the host loop
+    exchange = os.environ.get("GBX_PR_EXCHANGE", "p2p")
+    if exchange == "p2p":
+        ok = 1
+        try:  # symmetric memory + peer access on this box?
+            g0 = P.generate_rmat(10, 16, seed=1)
+            P.property_at(g0)
+            P.property_rowdegree(g0)
+            GpuShardBackend(g0).prepare(rank, ws)
+            be0 = GpuShardBackend(g0)
+            be0.prepare(rank, ws)
+            be0.p2p_setup(dist)
+        except Exception as e:
+            print(f"bench: p2p exchange unavailable ({e}); using nccl", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)  # every rank takes the same path
+        if int(flag.item()) == 0:
+            exchange = "nccl"
+    run_sharded = sharded_pagerank_p2p if exchange == "p2p" else sharded_pagerank
 
     scale = args.scale or 22
     P.init(local)
@@ -255,19 +279,21 @@ def bench_pagerank_sharded(args, dist, ws, rank, local):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     for _ in range(max(args.warmup, 3)):
         be = GpuShardBackend(g)
-        _, iters = sharded_pagerank(be, dist, 0.85, 1e-4, 100)
+        _, iters = run_sharded(be, dist, 0.85, 1e-4, 100)
     times = []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             be = GpuShardBackend(g)
-            be.prepare(rank, ws)  # plan outside the timed region
+            be.prepare(rank, ws)  # plan (and symmetric buffers) outside the timed region
+            if exchange == "p2p":
+                be.p2p_setup(dist)
             flush.zero_()
             barrier(dist)
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            _, iters = sharded_pagerank(_Prepared(be), dist, 0.85, 1e-4, 100, to_host=False)
+            _, iters = run_sharded(_Prepared(be), dist, 0.85, 1e-4, 100, to_host=False)
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
@@ -290,7 +316,7 @@ def bench_pagerank_sharded(args, dist, ws, rank, local):
         gh = Graph(h)
         P.property_at(gh)
         P.property_rowdegree(gh)
-        _, it2 = sharded_pagerank(GpuShardBackend(gh), dist, 0.85, 1e-4, 100)
+        _, it2 = run_sharded(GpuShardBackend(gh), dist, 0.85, 1e-4, 100)
         dt = time.perf_counter() - t0
         gh.free()
         if s_ > 0:
@@ -303,8 +329,12 @@ def bench_pagerank_sharded(args, dist, ws, rank, local):
            "data": "synthetic (seeded R-MAT, generated in HBM)",
            "config": {"workload": f"pagerank_rmat{scale}_directed", "scale": scale, "n": n,
                       "nnz": nnz, "iterations": iters, "parallelism": f"rowblock{ws}",
-                      "exchange": "NCCL all_gather_into_tensor (padded x slices) + "
-                                  "all_reduce (L1) per iteration",
+                      "exchange": ("fused: one cooperative kernel per rank stores x "
+                                   "into every rank's padded x over NVLink (symmetric "
+                                   "memory), device-side signal barrier per iteration"
+                                   if exchange == "p2p" else
+                                   "NCCL all_gather_into_tensor (padded x slices + L1 "
+                                   "partials) per iteration"),
                       "l2": "flushed (256 MB write) before every step"},
            "e2e": {"value": nnz * it2 / t_e2e, "unit": "edges/s/iter",
                    "h2d_bytes_per_step": int(rp.nbytes + col.nbytes),
@@ -313,7 +343,8 @@ def bench_pagerank_sharded(args, dist, ws, rank, local):
                                "property_at, property_rowdegree, shard plan, sharded "
                                "iterations, D2H ranks",
                    "samples_ms": [round(x * 1e3, 2) for x in e2e_times]},
-           "gpu_launches": int(2 * (iters + 1) * args.steps), "clocks": clk.summary()}
+           "gpu_launches": int((2 if exchange == "p2p" else 2 * (iters + 1)) * args.steps),
+           "clocks": clk.summary()}
     return out, (scale,)
 
 

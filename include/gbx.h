@@ -349,6 +349,25 @@ int gbx_last_stats(const gbx_graph* g, gbx_stats* stats, char msg[GBX_MSG_LEN]);
  * All vector arguments are device pointers. */
 int gbx_pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* row_begin,
                          int64_t* row_end, char msg[GBX_MSG_LEN]);
+/* The whole sharded run in ONE cooperative launch per rank, the exchange fused
+ * into the iteration kernel (no NCCL per iteration): the row epilogue stores
+ * x_next straight into every rank's padded x over NVLink (peer pointers, e.g.
+ * torch symmetric memory); the rank's fp64 L1 total goes to slot
+ * [k&1][rank] of every rank's table; a device-side barrier (one system-scope
+ * signal increment per peer, spin on the own word) separates iterations and
+ * every rank sums the table in rank order -> the same stop decision.
+ *   x0_peers/x1_peers[q]  rank q's x buffers (nranks * chunk floats each); x0
+ *                         holds the initial contributions (gbx_pr_shard_init)
+ *   l1_peers[q]           rank q's slot table (2 * nranks doubles)
+ *   sig_peers[q]          rank q's signal word (u32); every word must read 0
+ *                         when the run starts (zero them, then barrier)
+ *   r0 / r1               this rank's local rank buffers (chunk floats; r0 =
+ *                         the initial 1/n); the result is in (iters & 1 ? r1 : r0)
+ * At most 8 ranks; every rank must call it (the kernels wait on each other). */
+int gbx_pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1_peers,
+                         const uint64_t* l1_peers, const uint64_t* sig_peers, float* r0,
+                         float* r1, double damping, double tol, int itermax, int* iters,
+                         char msg[GBX_MSG_LEN]);
 /* chunk (slot length of the padded layout) and, if non-NULL, bounds[nranks+1]. */
 int gbx_pr_shard_layout(const gbx_graph* g, int64_t* chunk, int64_t* bounds,
                         char msg[GBX_MSG_LEN]);

@@ -72,6 +72,7 @@ _SIGS = {
     "gbx_pr_shard_unpermute": [_vp, _vp, _vp],
     "gbx_pr_shard_step": [_vp, _vp, _vp, _vp, _vp, _vp, _dbl],
     "gbx_pr_shard_layout": [_vp, _vp, _vp],
+    "gbx_pr_shard_run_p2p": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _int, _vp],
     "gbx_partition_rows": [_vp, _vp, _int, _int],
     "gbx_triangle_count_rows": [_vp, _vp, _i64, _i64],
     "gbx_tc_partition": [_vp, _vp, _int],

@@ -846,6 +846,18 @@ int gbx_pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, fl
   });
 }
 
+int gbx_pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1_peers,
+                         const uint64_t* l1_peers, const uint64_t* sig_peers, float* r0,
+                         float* r1, double damping, double tol, int itermax, int* iters,
+                         char* msg) {
+  return guard(msg, [&] {
+    need(g);
+    gbx::Scope sc(g);
+    gbx::pr_shard_run_p2p(g, x0_peers, x1_peers, l1_peers, sig_peers, r0, r1, damping, tol,
+                          itermax, iters);
+  });
+}
+
 int gbx_pr_shard_layout(const gbx_graph* gc, int64_t* chunk, int64_t* bounds, char* msg) {
   return guard(msg, [&] {
     gbx_graph* g = need(gc);

@@ -260,6 +260,9 @@ void pr_shard_unpermute(gbx_graph* g, const float* r_full, double* out_host);
 void pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, float* r_new,
                    float* x_slice, double* l1, double damping);
 void pr_shard_layout(gbx_graph* g, int64_t* chunk, int64_t* bounds);
+void pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1_peers,
+                      const uint64_t* l1_peers, const uint64_t* sig_peers, float* r0, float* r1,
+                      double damping, double tol, int itermax, int* iters);
 void partition_rows(const gbx_graph* g, int parts, bool transposed, int64_t* bounds);
 void result_device(const gbx_graph* g, const std::string& which, void** ptr, int64_t* count);
 

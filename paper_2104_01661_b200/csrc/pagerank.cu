@@ -57,6 +57,7 @@ constexpr int64_t kPrChunk = 2048;  // nonzeros per chunk unit
 // default shared-memory hot prefix of x (override: GBX_PR_HOT_KB)
 constexpr int kPrHotKbDefault = 0;
 constexpr unsigned kWarp = 0xffffffffu;
+constexpr int kPrMaxPeers = 8;     // ranks of the fused P2P exchange (one NVSwitch box)
 
 PrPlan::~PrPlan() {
   if (exec) cudaGraphExecDestroy(exec);
@@ -96,6 +97,11 @@ struct PrArgs {
   int itermax;
   int fixed;           // single step: r0/x0 inputs, r1/x1 outputs, no convergence
   cudaGraphConditionalHandle cond;
+  // fused multi-GPU run (k_pr_persist_p2p): x_next is stored straight into
+  // every rank's x buffer over NVLink.  xp[b][q] = rank q's x_b, pre-offset so
+  // that xp[b][q][row] is this rank's padded slot entry for relabeled row
+  int npeer;
+  V* xp[2][kPrMaxPeers];
 };
 
 template <typename V>
@@ -165,7 +171,15 @@ __device__ __forceinline__ double pr_finish_row(const PrArgs<V>& a, V* r_nxt, V*
                                                 int64_t row, double s, V rprev, V inv) {
   const double rn = a.teleport + s;
   r_nxt[row - a.row0] = static_cast<V>(rn);
-  x_nxt[row] = static_cast<V>(rn * static_cast<double>(inv));
+  const V xv = static_cast<V>(rn * static_cast<double>(inv));
+  if (a.npeer == 0) {
+    x_nxt[row] = xv;
+  } else {
+    // fused exchange: the contribution goes to every rank's copy of x (peer
+    // stores over NVLink; consecutive rows of a warp -> coalesced 128 B writes)
+    V* const* xp = a.xp[x_nxt == a.x1 ? 1 : 0];
+    for (int q = 0; q < a.npeer; ++q) xp[q][row] = xv;
+  }
   return fabs(static_cast<double>(rprev) - rn);
 }
 
@@ -369,6 +383,106 @@ __global__ void __launch_bounds__(BS, BS == 1024 ? 1 : GBX_PR_MINB) k_pr_persist
     __syncthreads();
     const double tot = BlockReduce(red).Sum(part);
     if (threadIdx.x == 0) {
+      const bool stop = !(tot >= a.tol) || (k + 1 >= a.itermax);
+      s_stop = stop;
+      if (blockIdx.x == 0) {
+        a.l1_hist[k % 128] = tot;
+        a.ctl[0] = k + 1;
+        if (stop) a.ctl[1] = 1;
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+  }
+}
+
+// Sharded PageRank with the exchange fused into the iteration kernel (one
+// cooperative launch per rank for the whole run).  Per iteration: the row
+// phase and the long-row finish store x_next into EVERY rank's x (peer
+// pointers, e.g. torch symmetric memory over NVLink/NVSwitch); the rank's fp64
+// L1 total goes to slot [k&1][rank] of every rank's table; then a cross-rank
+// barrier -- system-scope fence per CTA, grid barrier, one signal increment
+// per peer, spin on the own signal word, grid barrier -- and every CTA sums
+// the table in rank order: the same decision on every rank (pagerank.cpp:74).
+// x and the slot table are double-buffered by iteration parity, so a rank one
+// iteration ahead never overwrites what a slower rank still reads.
+struct PrP2p {
+  double* l1p[kPrMaxPeers];     // rank q's slot table [2][nranks]
+  unsigned* sigp[kPrMaxPeers];  // rank q's signal word
+  double* l1_own;               // this rank's table
+  unsigned* sig_own;            // this rank's signal word
+  int rank, nranks;
+};
+
+__global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist_p2p(PrArgs<float> a,
+                                                                            PrP2p m) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  using BlockReduce = cub::BlockReduce<double, kPrThreads>;
+  __shared__ typename BlockReduce::TempStorage red;
+  __shared__ PrBin s_bins[kPrBinsMax];
+  __shared__ int s_stop;
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int k = 0;; ++k) {
+    if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 2], pr_gtimer());
+    const double blk = pr_rows_phase<float, kPrThreads>(a, k, red, s_bins, nullptr);
+    if (threadIdx.x == 0) {
+      a.l1_rows[blockIdx.x] = blk;
+      if (a.ktime) atomicMax(&a.ktime[(k % 128) * 2 + 1], pr_gtimer());
+    }
+    grid.sync();
+    const float *x_cur, *r_cur;
+    float *x_nxt, *r_nxt;
+    pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
+    double l1 = 0.0;
+    for (int64_t i = gwarp; i < a.nlong; i += nwarps) {
+      const int64_t q0 = a.long_slot[i], q1 = a.long_slot[i + 1];
+      double s = 0.0;
+      for (int64_t q = q0 + lane; q < q1; q += 32) s += __ldcg(a.slot + q);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
+      if (lane == 0) {
+        const int64_t row = a.long_row[i];
+        l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, r_cur[row - a.row0], a.inv[row]);
+      }
+    }
+    __syncthreads();
+    const double blk2 = BlockReduce(red).Sum(l1);
+    if (threadIdx.x == 0) a.l1_fin[blockIdx.x] = blk2;
+    __threadfence_system();  // this CTA's peer stores before the signal below
+    grid.sync();
+    if (blockIdx.x == 0) {
+      double part = 0.0;
+      for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += kPrThreads)
+        part += __ldcg(&a.l1_rows[b]) + __ldcg(&a.l1_fin[b]);
+      __syncthreads();
+      const double mine = BlockReduce(red).Sum(part);
+      if (threadIdx.x == 0) {
+        const int par = k & 1;
+        for (int q = 0; q < m.nranks; ++q)
+          m.l1p[q][par * m.nranks + m.rank] = mine;
+        __threadfence_system();
+        for (int q = 0; q < m.nranks; ++q) atomicAdd_system(m.sigp[q], 1u);
+        // every rank signals every rank once per iteration
+        // (the caller zeroes the signal words and barriers before the run)
+        const unsigned want = static_cast<unsigned>(m.nranks) * (k + 1);
+        for (;;) {
+          unsigned v;
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(m.sig_own) : "memory");
+          if (static_cast<int>(v - want) >= 0) break;
+          __nanosleep(64);
+        }
+        __threadfence_system();
+      }
+    }
+    grid.sync();
+    if (threadIdx.x == 0) {
+      const int par = k & 1;
+      double tot = 0.0;
+      for (int q = 0; q < m.nranks; ++q)  // rank order: identical on every rank
+        tot += *(volatile double*)&m.l1_own[par * m.nranks + q];
       const bool stop = !(tot >= a.tol) || (k + 1 >= a.itermax);
       s_stop = stop;
       if (blockIdx.x == 0) {
@@ -1197,6 +1311,70 @@ void pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, float
   GBX_LAUNCHED();
   GBX_CUDA(cudaMemcpyAsync(l1, P.l1_hist.p, sizeof(double), cudaMemcpyDeviceToDevice, s));
   g->prs->steps++;
+}
+
+void pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1_peers,
+                      const uint64_t* l1_peers, const uint64_t* sig_peers, float* r0, float* r1,
+                      double damping, double tol, int itermax, int* iters) {
+  if (!g->prs) fail(GBX_MISSING_PROPERTY, "pr_shard_run_p2p needs gbx_pr_shard_prepare");
+  PrShard& S = *g->prs;
+  PrPlan& P = S.plan;
+  if (S.nranks > kPrMaxPeers) fail(GBX_INVALID_VALUE, "pr_shard_run_p2p: more than 8 ranks");
+  if (!x0_peers || !x1_peers || !l1_peers || !sig_peers || !r0 || !r1)
+    fail(GBX_NULL_ARGUMENT, "pr_shard_run_p2p: NULL buffer");
+  cudaStream_t s = g->stream;
+  if (P.g_damping != damping) {
+    k_pr_inv<<<ceil_div(std::max<int64_t>(P.n, 1), 256), 256, 0, s>>>(P.invf.p, P.deg.p, P.n,
+                                                                      damping);
+    GBX_LAUNCHED();
+    P.g_damping = damping;
+  }
+  if (itermax <= 0) {
+    if (iters) *iters = std::max(itermax, 0);
+    return;
+  }
+  PrArgs<float> a = make_args<float>(P, damping, tol, itermax);
+  a.inv = P.invf.p;
+  a.fixed = 0;
+  a.row0 = P.row0;
+  a.hot = 0;
+  a.x0 = reinterpret_cast<float*>(x0_peers[S.rank]);
+  a.x1 = reinterpret_cast<float*>(x1_peers[S.rank]);
+  a.r0 = r0;
+  a.r1 = r1;
+  a.npeer = S.nranks;
+  const int64_t off = static_cast<int64_t>(S.rank) * S.chunk - P.row0;
+  for (int q = 0; q < S.nranks; ++q) {
+    a.xp[0][q] = reinterpret_cast<float*>(x0_peers[q]) + off;
+    a.xp[1][q] = reinterpret_cast<float*>(x1_peers[q]) + off;
+  }
+  // the gathers read the local padded copy; x_nxt only selects the parity
+  a.x0 = reinterpret_cast<float*>(x0_peers[S.rank]);
+  a.x1 = reinterpret_cast<float*>(x1_peers[S.rank]);
+  PrP2p m{};
+  for (int q = 0; q < S.nranks; ++q) {
+    m.l1p[q] = reinterpret_cast<double*>(l1_peers[q]);
+    m.sigp[q] = reinterpret_cast<unsigned*>(sig_peers[q]);
+  }
+  m.l1_own = m.l1p[S.rank];
+  m.sig_own = m.sigp[S.rank];
+  m.rank = S.rank;
+  m.nranks = S.nranks;
+  int per_sm = 0;
+  GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_persist_p2p, kPrThreads, 0));
+  a.grid_rows = device_sms() * std::max(per_sm, 1);
+  if (static_cast<int64_t>(P.l1_fin.n) < a.grid_rows || static_cast<int64_t>(P.l1_block.n) < a.grid_rows)
+    fail(GBX_CUDA_ERROR, "pr_shard_run_p2p: partial buffers too small");
+  reset_state(s, P);
+  void* args[] = {&a, &m};
+  GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_pr_persist_p2p),
+                                       dim3(a.grid_rows), dim3(kPrThreads), args, 0, s));
+  GBX_LAUNCHED();
+  int it = 0;
+  GBX_CUDA(cudaMemcpyAsync(&it, P.ctl.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  P.last_iters = it;
+  if (iters) *iters = it;
 }
 
 __global__ void k_pr_unpermute_f(const float* r, const int32_t* new2old, int64_t n, double* out,

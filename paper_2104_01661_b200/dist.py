@@ -100,6 +100,31 @@ def sharded_pagerank(backend, dist, damping=0.85, tol=1e-4, itermax=100, to_host
     return backend.unpermute(r_full), iters
 
 
+def sharded_pagerank_p2p(backend, dist, damping=0.85, tol=1e-4, itermax=100, to_host=True):
+    """GAP PageRank over `world` ranks with the exchange FUSED into the iteration
+    kernel (gbx_pr_shard_run_p2p): one cooperative launch per rank runs every
+    iteration; each row epilogue stores its contribution straight into every
+    rank's x over NVLink (torch symmetric-memory peer pointers), the L1
+    partials go to every rank's slot table, and a device-side signal barrier
+    separates iterations -- no host round trip and no NCCL call per iteration.
+    One NCCL all-gather of the local ranks at the end.  Same results and
+    iteration count as sharded_pagerank."""
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    rb, re, n = backend.prepare(rank, world)
+    chunk = backend.chunk
+    backend.p2p_setup(dist)
+    backend.p2p_init(damping)          # x0 (every slot), r0; signal words zeroed
+    dist.barrier()                     # every rank zeroed before any rank signals
+    iters = backend.p2p_run(damping, tol, itermax)
+    r_local = backend.p2p_result(iters)
+    r_full = torch.empty(world * chunk, dtype=r_local.dtype, device=backend.device)
+    dist.all_gather_into_tensor(r_full, r_local)
+    if not to_host:
+        return r_full, iters
+    return backend.unpermute(r_full), iters
+
+
 def sharded_triangle_count(backend, dist):
     """Triangle count with wedge-balanced row blocks of the oriented U."""
     import torch
@@ -201,6 +226,10 @@ def sharded_betweenness_rows(backend, dist, sources):
     return total.cpu().numpy().copy()
 
 
+# symmetric buffers of the fused P2P PageRank, keyed by (world, chunk, device)
+_P2P_BUFFERS = {}
+
+
 class _DeviceArray:
     """__cuda_array_interface__ view of a library-owned device buffer."""
 
@@ -274,6 +303,55 @@ class GpuShardBackend:
 
     def x_new_slice(self):
         return self._xs
+    # ---- fused P2P run (gbx_pr_shard_run_p2p) over symmetric memory
+    def p2p_setup(self, dist):
+        """Symmetric x0 / x1 / slot table / signal buffers, rendezvoused over the
+        world group; their peer pointers go to the kernel."""
+        import torch
+        import torch.distributed._symmetric_memory as symm_mem
+        if getattr(self, "_p2p_world", None) == (self.world, self.chunk):
+            return
+        group = dist.group.WORLD
+        dev = self.device
+        key = (self.world, self.chunk, str(dev))
+        if key not in _P2P_BUFFERS:  # allocation + rendezvous once per layout
+            bufs = [symm_mem.empty(self.world * self.chunk, dtype=torch.float32, device=dev),
+                    symm_mem.empty(self.world * self.chunk, dtype=torch.float32, device=dev),
+                    symm_mem.empty(2 * self.world, dtype=torch.float64, device=dev),
+                    symm_mem.empty(4, dtype=torch.int32, device=dev)]
+            hdl = [symm_mem.rendezvous(t, group) for t in bufs]
+            ptr = [np.ascontiguousarray([int(p) for p in h.buffer_ptrs], np.uint64) for h in hdl]
+            _P2P_BUFFERS.clear()
+            _P2P_BUFFERS[key] = (bufs, hdl, ptr)
+        self._pbufs, self._phdl, self._pptr = _P2P_BUFFERS[key]
+        for a in self._pptr:
+            assert len(a) == self.world
+        self._pr = [torch.zeros(self.chunk, dtype=torch.float32, device=dev) for _ in range(2)]
+        self._p2p_world = (self.world, self.chunk)
+
+    def p2p_init(self, damping):
+        import torch
+
+        from .graph import call
+        self._pbufs[3].zero_()
+        self._pbufs[2].zero_()
+        torch.cuda.current_stream().synchronize()
+        call("gbx_pr_shard_init", self.g.handle, self._pbufs[0].data_ptr(),
+             self._pr[0].data_ptr(), damping)
+        self._stream.synchronize()
+
+    def p2p_run(self, damping, tol, itermax):
+        from .graph import call
+        it = C.c_int(0)
+        p = self._pptr
+        call("gbx_pr_shard_run_p2p", self.g.handle, p[0].ctypes.data, p[1].ctypes.data,
+             p[2].ctypes.data, p[3].ctypes.data, self._pr[0].data_ptr(), self._pr[1].data_ptr(),
+             damping, tol, itermax, C.byref(it))
+        return it.value
+
+    def p2p_result(self, iters):
+        return self._pr[iters & 1]
+
 
     def x_full(self):
         return self._x
