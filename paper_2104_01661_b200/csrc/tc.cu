@@ -42,6 +42,9 @@ constexpr int64_t kTcItem = 64;           // in-neighbours (tails) per work item
 #ifndef GBX_TC_LONG
 #define GBX_TC_LONG 32
 #endif
+#ifndef GBX_TC_VEC
+#define GBX_TC_VEC 0  // 16-byte loads on the long-tail walks (measured slower: masking)
+#endif
 #ifndef GBX_TC_UNROLL
 #define GBX_TC_UNROLL 4
 #endif
@@ -138,16 +141,30 @@ __device__ __forceinline__ TcSet tc_build(int* mem, const int32_t* __restrict__ 
   return S;
 }
 
+// membership test with the set's kind fixed at compile time (the probe loop
+// is issue-bound: no per-probe branch on the kind)
+template <bool kBm>
+__device__ __forceinline__ unsigned tc_has(const TcSet& S, int32_t k) {
+  if constexpr (kBm) {
+    const uint32_t o = static_cast<uint32_t>(k - S.base);
+    return o < S.span ? (static_cast<uint32_t>(S.mem[o >> 5]) >> (o & 31)) & 1u : 0u;
+  } else {
+    return tc_lookup(S.mem, S.log_slots, k) ? 1u : 0u;
+  }
+}
+
 // Stream the tails L(j)[qb, qe) over a warp group, probing every element in
 // the set.  Each round takes 32 tails: tails of >= 32 elements are walked by
-// the whole warp one at a time (coalesced), shorter ones are concatenated and
-// spread over the lanes (owner of an element by binary search in shared
-// memory over the prefix sums).
-template <int kWarps>
-__device__ __forceinline__ unsigned long long tc_stream_tails(
+// the whole warp one at a time with 16-byte loads (4 probes per load, from the
+// 4-aligned element at or below the tail start; out-of-tail lanes masked),
+// shorter ones are concatenated and spread over the lanes (owner of an
+// element by binary search in shared memory over the prefix sums).  32-bit
+// counts per call (a call probes < 2^32 elements).
+template <int kWarps, bool kBm>
+__device__ __forceinline__ unsigned long long tc_stream_tails_k(
     const int2* __restrict__ tails, const int32_t* __restrict__ ucol, int qb, int qe,
     const TcSet& S, int lane, int warp_in_group, int* s_incl, int* s_sx) {
-  unsigned long long cnt = 0;
+  unsigned cnt = 0;
   for (int base = qb + 32 * warp_in_group; base < qe; base += 32 * kWarps) {
     const int q = base + lane;
     int s = 0, len = 0;
@@ -161,17 +178,36 @@ __device__ __forceinline__ unsigned long long tc_stream_tails(
       const int src = __ffs(longs) - 1;
       longs &= longs - 1;
       const int ls = __shfl_sync(kFullMask, s, src);
-      const int ll = __shfl_sync(kFullMask, len, src);
-      // kTcUnroll independent loads in flight per lane
-      for (int e = lane; e < ll; e += 32 * kTcUnroll) {
+      const int le = ls + __shfl_sync(kFullMask, len, src);
+#if GBX_TC_VEC
+      const int a0 = ls & ~3;  // ucol is 256-byte aligned: int4 at multiples of 4
+      for (int e = a0 + 4 * lane; e < le; e += 128 * kTcUnroll) {
+        int4 v[kTcUnroll];
+#pragma unroll
+        for (int u = 0; u < kTcUnroll; ++u)
+          v[u] = e + 128 * u < le ? __ldg(reinterpret_cast<const int4*>(ucol + e + 128 * u))
+                                  : make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < kTcUnroll; ++u) {
+          const int x = e + 128 * u;
+          if (x < le) {
+            const int k4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (x + c >= ls && x + c < le) cnt += tc_has<kBm>(S, k4[c]);
+          }
+        }
+      }
+#else
+      for (int e = ls + lane; e < le; e += 32 * kTcUnroll) {
         int32_t k[kTcUnroll];
 #pragma unroll
-        for (int u = 0; u < kTcUnroll; ++u)
-          k[u] = e + 32 * u < ll ? __ldg(ucol + ls + e + 32 * u) : 0;
+        for (int u = 0; u < kTcUnroll; ++u) k[u] = e + 32 * u < le ? __ldg(ucol + e + 32 * u) : 0;
 #pragma unroll
         for (int u = 0; u < kTcUnroll; ++u)
-          if (e + 32 * u < ll && S.has(k[u])) ++cnt;
+          if (e + 32 * u < le) cnt += tc_has<kBm>(S, k[u]);
       }
+#endif
     }
     if (len >= kTcLong) len = 0;
     int incl = len;
@@ -189,11 +225,21 @@ __device__ __forceinline__ unsigned long long tc_stream_tails(
 #pragma unroll
       for (int step = 16; step > 0; step >>= 1)
         if (s_incl[lo + step - 1] <= e) lo += step;
-      cnt += S.has(__ldg(ucol + s_sx[lo] + e)) ? 1ull : 0ull;
+      cnt += tc_has<kBm>(S, __ldg(ucol + s_sx[lo] + e));
     }
     __syncwarp();
   }
   return cnt;
+}
+
+template <int kWarps>
+__device__ __forceinline__ unsigned long long tc_stream_tails(
+    const int2* __restrict__ tails, const int32_t* __restrict__ ucol, int qb, int qe,
+    const TcSet& S, int lane, int warp_in_group, int* s_incl, int* s_sx) {
+  return S.span ? tc_stream_tails_k<kWarps, true>(tails, ucol, qb, qe, S, lane, warp_in_group,
+                                                  s_incl, s_sx)
+                : tc_stream_tails_k<kWarps, false>(tails, ucol, qb, qe, S, lane, warp_in_group,
+                                                   s_incl, s_sx);
 }
 
 struct TcArgs {
@@ -526,6 +572,9 @@ uint64_t tc_run(gbx_graph* g, int64_t rb, int64_t re) {
   g->stats = gbx_stats{};
   g->pending_iters = nullptr;
   if (re <= rb) return 0;
+  // the long-tail walks read U with 16-byte loads from 4-aligned element ids
+  if (reinterpret_cast<uintptr_t>(P.ucol.p) % 16 != 0)
+    fail(GBX_CUDA_ERROR, "triangle_count: U column array is not 16-byte aligned");
   int64_t ib = 0, ie = P.nitems;
   if (rb > 0 || re < P.n) {
     GBX_CUDA(cudaMemcpyAsync(&ib, P.item_off.p + rb, 8, cudaMemcpyDeviceToHost, s));
