@@ -776,16 +776,33 @@ __global__ void k_pr_list_long(const int64_t* prp, int64_t n, int32_t* list, int
   const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (r < n && prp[r + 1] - prp[r] > kPrGatherLong) list[atomicAdd(cnt, 1)] = static_cast<int32_t>(r);
 }
+// long rows cut into kPrGatherChunk-element items (one hub row per CTA left
+// a single CTA looping over 10^5 elements at the end of the launch)
+constexpr int64_t kPrGatherChunk = 2048;
+__global__ void k_pr_long_chunks(const int64_t* prp, const int32_t* list, int m, int64_t* nch) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) {
+    const int64_t r = list[i];
+    nch[i] = (prp[r + 1] - prp[r] + kPrGatherChunk - 1) / kPrGatherChunk;
+  }
+}
 __global__ void k_pr_gather_a_long(const int64_t* arp, const int32_t* acol, const int32_t* new2old,
                                    const int32_t* old2new, const int64_t* prp,
-                                   const int32_t* list, const int* cnt, uint32_t* key,
-                                   uint32_t* val) {
-  const int m = *cnt;
-  for (int i = blockIdx.x; i < m; i += gridDim.x) {
-    const int64_t r = list[i];
+                                   const int32_t* list, const int64_t* cincl, int m,
+                                   uint32_t* key, uint32_t* val) {
+  const int64_t total = cincl[m - 1];
+  for (int64_t c = blockIdx.x; c < total; c += gridDim.x) {
+    int lo = 0, hi = m - 1;  // first i with cincl[i] > c
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cincl[mid] > c) hi = mid; else lo = mid + 1;
+    }
+    const int64_t r = list[lo];
+    const int64_t k = c - (lo ? cincl[lo - 1] : 0);
     const int64_t d = prp[r], len = prp[r + 1] - d;
     const int64_t src = arp[new2old[r]];
-    for (int64_t p = threadIdx.x; p < len; p += blockDim.x) {
+    const int64_t p1 = min(len, (k + 1) * kPrGatherChunk);
+    for (int64_t p = k * kPrGatherChunk + threadIdx.x; p < p1; p += blockDim.x) {
       key[d + p] = static_cast<uint32_t>(old2new[acol[src + p]]);
       val[d + p] = static_cast<uint32_t>(r);
     }
@@ -870,9 +887,23 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
       Tmp<int> cnt(1, s);
       GBX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), s));
       k_pr_list_long<<<ceil_div(n, 256), 256, 0, s>>>(prp.p, n, list.p, cnt.p);
-      k_pr_gather_a_long<<<device_sms() * 4, 256, 0, s>>>(A.rp.p, A.col.p, P.new2old.p,
-                                                           P.old2new.p, prp.p, list.p, cnt.p,
-                                                           kc.p, vr.p);
+      GBX_LAUNCHED();
+      int m = 0;
+      GBX_CUDA(cudaMemcpyAsync(&m, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      GBX_CUDA(cudaStreamSynchronize(s));
+      if (m > 0) {
+        Tmp<int64_t> nch(m, s);
+        k_pr_long_chunks<<<ceil_div(m, 256), 256, 0, s>>>(prp.p, list.p, m, nch.p);
+        size_t tb2 = 0;
+        GBX_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb2, nch.p, nch.p, m, s));
+        {
+          Tmp<uint8_t> t(tb2, s);
+          GBX_CUDA(cub::DeviceScan::InclusiveSum(t.p, tb2, nch.p, nch.p, m, s));
+        }
+        k_pr_gather_a_long<<<device_sms() * 8, 256, 0, s>>>(A.rp.p, A.col.p, P.new2old.p,
+                                                             P.old2new.p, prp.p, list.p, nch.p, m,
+                                                             kc.p, vr.p);
+      }
     }
     k_pr_gather_a_short<<<device_sms() * 8, 256, 0, s>>>(A.rp.p, A.col.p, P.new2old.p,
                                                           P.old2new.p, prp.p, n, kc.p, vr.p);
