@@ -42,6 +42,12 @@ namespace cg = cooperative_groups;
 namespace gbx {
 
 constexpr int kSsspThreads = 256;
+#ifndef GBX_SSSP_IBUCKET
+#define GBX_SSSP_IBUCKET 1  // integer bucket index (shift / u32 division) for integral delta
+#endif
+#ifndef GBX_SSSP_PRECHECK
+#define GBX_SSSP_PRECHECK 0  // plain load of the dedup word before its atomicOr
+#endif
 #ifndef GBX_SSSP_MINB
 #define GBX_SSSP_MINB 4  // resident CTAs per SM (measured: 2 -> 160 ms, 3 -> 133, 4 -> 128 for config 4)
 #endif
@@ -318,12 +324,27 @@ __device__ __forceinline__ int64_t bucket_of<unsigned long long>(unsigned long l
   return static_cast<int64_t>(floor(__longlong_as_double(static_cast<long long>(d)) / delta));
 }
 
+// bucket index of an integer distance without the fp64 division when delta is
+// an integer (a shift for a power of two: config 4's delta = 64)
+template <typename D, typename A>
+__device__ __forceinline__ int64_t bucket_k(D d, const A& a) {
+#if GBX_SSSP_IBUCKET
+  if constexpr (std::is_same<D, uint32_t>::value) {
+    if (a.dshift >= 0) return static_cast<int64_t>(d >> a.dshift);
+    if (a.idelta) return static_cast<int64_t>(d / a.idelta);
+  }
+#endif
+  return bucket_of<D>(d, a.delta);
+}
+
 template <typename D, typename E>
 struct SsspBArgs {
   const int64_t* rp;
   E edges;
   int64_t n;
   double delta;
+  int dshift;          // delta = 2^dshift (integer distances), else -1
+  uint32_t idelta;     // integral delta (integer distances), else 0
   int nb;              // buckets (power of two)
   int64_t cap;         // entries per bucket array
   D* dist;
@@ -497,11 +518,17 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
               // harmless extra relaxation (stale bucket entries are skipped)
               atomicMin(&a.dist[v[q4]], nd[q4]);
               const uint32_t bit = 1u << (v[q4] & 31);
-              const int64_t kb = bucket_of<D>(nd[q4], a.delta);
+              const int64_t kb = bucket_k<D>(nd[q4], a);
               if (kb <= k && phase != 2) {  // (a heavy edge always leaves the bucket)
+#if GBX_SSSP_PRECHECK
+                if (!(*(volatile uint32_t*)&push_bits[v[q4] >> 5] & bit))
+#endif
                 near_push = !(atomicOr(&push_bits[v[q4] >> 5], bit) & bit);
               } else {
                 bidx = static_cast<int>(kb & nbm);
+#if GBX_SSSP_PRECHECK
+                if (!(*(volatile uint32_t*)&a.bbits[bidx * a.words + (v[q4] >> 5)] & bit))
+#endif
                 buck_push = !(atomicOr(&a.bbits[bidx * a.words + (v[q4] >> 5)], bit) & bit);
               }
             }
@@ -560,7 +587,7 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
             if (nd[q4] < cur[q4]) {
               atomicMin(&a.dist[v[q4]], nd[q4]);
               const uint32_t bit = 1u << (v[q4] & 31);
-              bidx = static_cast<int>(bucket_of<D>(nd[q4], a.delta) & nbm);
+              bidx = static_cast<int>(bucket_k<D>(nd[q4], a) & nbm);
               buck_push = !(atomicOr(&a.bbits[bidx * a.words + (v[q4] >> 5)], bit) & bit);
             }
           }
@@ -634,7 +661,7 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
         int c = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const bool in = dv[j] != DistTraits<D>::inf() && bucket_of<D>(dv[j], a.delta) == k;
+          const bool in = dv[j] != DistTraits<D>::inf() && bucket_k<D>(dv[j], a) == k;
           const unsigned m = __ballot_sync(kFullW, in);
           if (in) win[c + __popc(m & ((1u << lane) - 1))] = static_cast<int32_t>(base + 32 * j + lane);
           c += __popc(m);
@@ -693,7 +720,7 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
         const uint32_t bit = 1u << (v & 31);
         atomicAnd(&a.bbits[b * a.words + (v >> 5)], ~bit);
         // stale entries (improved into an earlier bucket since) are skipped
-        if (bucket_of<D>(*(volatile D*)&a.dist[v], a.delta) == k)
+        if (bucket_k<D>(*(volatile D*)&a.dist[v], a) == k)
           to_near = !(atomicOr(&push_bits[v >> 5], bit) & bit);
       }
       nearq.push(to_near, v);
@@ -1007,6 +1034,17 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     b.edges = edges;
     b.n = n;
     b.delta = delta;
+    b.dshift = -1;
+    b.idelta = 0;
+    if (std::is_same<D, uint32_t>::value && delta == std::floor(delta) && delta >= 1.0 &&
+        delta < 4294967296.0) {
+      b.idelta = static_cast<uint32_t>(delta);
+      if ((b.idelta & (b.idelta - 1)) == 0) {
+        int sh = 0;
+        while ((1u << sh) < b.idelta) ++sh;
+        b.dshift = sh;
+      }
+    }
     b.nb = nb;
     b.cap = cap;
     b.dist = dist;
