@@ -71,13 +71,14 @@ struct Bfs1Args {
   int64_t* q1;
   uint32_t* bm0;
   uint32_t* bm1;
+  uint32_t* bm2;
   int32_t* ul0;      // still-unvisited vertices (pull levels only scan these)
   int32_t* ul1;
   const int32_t* heavy;  // in-degree > kBfsHeavy: pulled by whole warps, never listed
   int64_t nheavy;
-  int* ctl;  // [0] entries [1] vertices [2] next entries [3] next vertices [4] prev vertices
-             // [5] levels done [6] push levels [8:10) u64 frontier edges [10:12) next
-             // [12] unvisited-list size (-1: not built) [13] next size [14] list parity
+  int* ctl;  // [5] levels done [6] push levels; slot j = ctl + 16 + 8 * (j & 3) describes
+             // the frontier level j produced: [0] queue entries [1] vertices [2:4) u64
+             // frontier edges [4] unvisited-list size (-1: not built) [5] list parity
   unsigned long long* tlog;  // optional: %globaltimer at phase boundaries (debug)
   int32_t source;
 };
@@ -98,7 +99,13 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int64_t gsize = int64_t(gridDim.x) * blockDim.x;
   const int64_t nwords = (a.n + 31) >> 5;
-  unsigned long long* edges = reinterpret_cast<unsigned long long*>(a.ctl + 8);
+  // one grid barrier per level: the per-level counters live in a ring of 4
+  // slots (level d reads slot d-1 and d-2, accumulates slot d and zeroes slot
+  // d+1, last read at the start of level d-2) and the frontier bitmaps in a
+  // ring of 3 (level d reads bm[d-1], writes bm[d], clears bm[d+1], which level
+  // d-1 read) -- nothing a level touches is still in use by the previous one
+  auto slot = [&](int j) { return a.ctl + 16 + 8 * (j & 3); };
+  uint32_t* bms[3] = {a.bm0, a.bm1, a.bm2};
   if (a.tlog && gtid == 0) a.tlog[0] = gtimer();
   {
     // initial state, inside the persistent kernel (no init / seed launches):
@@ -119,19 +126,23 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
       const int64_t deg = a.rp[src + 1] - a.rp[src];
       const int k = n_chunks(deg);
       for (int c = 0; c < k; ++c) a.q0[c] = (static_cast<int64_t>(c) << 32) | src;
-      for (int i = 0; i < 16; ++i) a.ctl[i] = 0;
-      a.ctl[0] = k;
-      a.ctl[1] = 1;
-      *reinterpret_cast<unsigned long long*>(a.ctl + 8) = static_cast<unsigned long long>(deg);
-      a.ctl[12] = -1;
+      for (int i = 0; i < 48; ++i) a.ctl[i] = 0;
+      int* s0 = slot(0);
+      s0[0] = k;
+      s0[1] = 1;
+      *reinterpret_cast<unsigned long long*>(s0 + 2) = static_cast<unsigned long long>(deg);
+      s0[4] = -1;
+      s0[5] = 0;
     }
     grid.sync();
   }
   for (int d = 1; static_cast<int64_t>(d) + 1 <= a.n; ++d) {
-    const int qe = *(volatile int*)&a.ctl[0];
-    const int qv = *(volatile int*)&a.ctl[1];
-    const int pv = *(volatile int*)&a.ctl[4];
-    const unsigned long long fe = *(volatile unsigned long long*)&edges[0];
+    const int* sc = slot(d - 1);
+    int* sn = slot(d);
+    const int qe = *(volatile const int*)&sc[0];
+    const int qv = *(volatile const int*)&sc[1];
+    const int pv = d >= 2 ? *(volatile const int*)&slot(d - 2)[1] : 0;
+    const unsigned long long fe = *(volatile const unsigned long long*)(sc + 2);
     if (qv == 0) break;
     // alpha == 0: the reference's rule (bfs.cpp:77-78), push while the frontier
     // has < n/divisor + 1 vertices and grows.  alpha > 0 (default): Beamer's
@@ -153,9 +164,28 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
     const int p = (d - 1) & 1;
     const int64_t* qc = p ? a.q1 : a.q0;
     int64_t* qn = p ? a.q0 : a.q1;
-    const uint32_t* bc = p ? a.bm1 : a.bm0;
-    uint32_t* bn = p ? a.bm0 : a.bm1;
-    fq.reset(qn, &a.ctl[2], &a.ctl[3], &edges[1], nullptr);
+    const uint32_t* bc = bms[(d - 1) % 3];
+    uint32_t* bn = bms[d % 3];
+    {
+      // the bitmap level d+1 writes (level d-1 read it) and slot d+1
+      uint32_t* bclr = bms[(d + 1) % 3];
+      for (int64_t i = gtid; i < nwords; i += gsize) bclr[i] = 0u;
+      if (gtid == 0) {
+        int* sz = slot(d + 1);
+        for (int i = 0; i < 8; ++i) sz[i] = 0;
+      }
+    }
+    const int ucnt = *(volatile const int*)&sc[4];
+    const int upar = *(volatile const int*)&sc[5];
+    if (gtid == 0) {
+      // the unvisited list this level leaves behind: a pull builds the other
+      // buffer (its size accumulates in sn[4], zeroed two levels ago), a push
+      // keeps the current one
+      if (push) sn[4] = ucnt;
+      sn[5] = push ? upar : (upar ^ 1);
+    }
+    unsigned long long* edges_n = reinterpret_cast<unsigned long long*>(sn + 2);
+    fq.reset(qn, &sn[0], &sn[1], edges_n, nullptr);
     if (push) {
       // a small queue (a hub or two) would leave most warps idle and walk each
       // kChunk-edge entry in kChunk/32 dependent steps: split every entry over
@@ -197,10 +227,8 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
     } else {
       // scan every vertex the first time, afterwards only the ones a previous
       // pull left unvisited (vertices with no in-edges never enter the list)
-      const int ucnt = *(volatile int*)&a.ctl[12];
-      const int upar = *(volatile int*)&a.ctl[14];
       const int32_t* ucur = upar ? a.ul1 : a.ul0;
-      uq.reset(upar ? a.ul0 : a.ul1, &a.ctl[13]);
+      uq.reset(upar ? a.ul0 : a.ul1, &sn[4]);
       const int64_t range = ucnt < 0 ? a.n : ucnt;
       const int grp = lane >> 3, sub = lane & 7;
       // 32 vertices per warp step, one per lane: the level/row-pointer loads
@@ -312,30 +340,13 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
       }
     }
     fq.flush();
-    grid.sync();
     if (a.tlog && gtid == 0) a.tlog[4 * d + 1] = gtimer();
-    // roll the frontier: the current bitmap is cleared for reuse two levels on
-    uint32_t* bclr = const_cast<uint32_t*>(bc);
-    for (int64_t i = gtid; i < nwords; i += gsize) bclr[i] = 0u;
     if (gtid == 0) {
-      a.ctl[4] = qv;
-      a.ctl[0] = a.ctl[2];
-      a.ctl[1] = a.ctl[3];
-      a.ctl[2] = 0;
-      a.ctl[3] = 0;
       a.ctl[5] = d;
-      edges[0] = edges[1];
-      edges[1] = 0ull;
-      if (push) {
-        a.ctl[6] += 1;
-      } else {
-        a.ctl[12] = a.ctl[13];
-        a.ctl[13] = 0;
-        a.ctl[14] ^= 1;
-      }
-      if (a.tlog) a.tlog[4 * d + 2] = gtimer();
+      if (push) a.ctl[6] += 1;
     }
     grid.sync();
+    if (a.tlog && gtid == 0) a.tlog[4 * d + 2] = gtimer();
   }
   if (a.tlog && gtid == 0) a.tlog[1] = gtimer();
 }
@@ -401,9 +412,10 @@ static void ensure_bfs1(gbx_graph* g) {
   W.queue[1].alloc(2 * qcap);
   W.bitmap[0].alloc((n + 31) / 32 + 1);
   W.bitmap[1].alloc((n + 31) / 32 + 1);
+  W.bitmap[2].alloc((n + 31) / 32 + 1);
   W.ulist[0].alloc(std::max<int64_t>(n, 1));
   W.ulist[1].alloc(std::max<int64_t>(n, 1));
-  W.ctl.alloc(16);
+  W.ctl.alloc(64);
 }
 
 void bfs_prepare(gbx_graph* g) { ensure_bfs1(g); }
@@ -464,6 +476,7 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
   a.q1 = q1;
   a.bm0 = W.bitmap[0].p;
   a.bm1 = W.bitmap[1].p;
+  a.bm2 = W.bitmap[2].p;
   a.ctl = W.ctl.p;
   if (tlog_on) {
     if (!W.tlog.p) W.tlog.alloc(4 * 256);

@@ -90,7 +90,7 @@ struct BfsWork {
   std::unique_ptr<BfsShard> shard;
   DevArray<int32_t> level, parent;          // single source
   DevArray<int32_t> queue[2];
-  DevArray<uint32_t> bitmap[2];
+  DevArray<uint32_t> bitmap[3];             // frontier bitmaps: read, write, clear per level
   DevArray<int32_t> ulist[2];               // unvisited vertices for pull levels
   DevArray<int> ctl;
   // multi-source (64 lanes)
