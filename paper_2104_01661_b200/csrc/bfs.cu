@@ -533,6 +533,7 @@ struct Bfs64Args {
   unsigned long long* seen;
   unsigned long long* f0;
   unsigned long long* f1;
+  unsigned long long* f2;
   int32_t* mlevel;   // [n][64]
   int32_t* mparent;  // [n][64]
   int64_t* q0;
@@ -562,9 +563,15 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   // level d pops the queue counted in buffer d%3 and pushes into (d+1)%3;
   // buffer (d+2)%3 -- last read during level d-1, before its closing barrier
-  // -- is zeroed by the leader for level d+1: two grid barriers per level
+  // -- is zeroed by the leader for level d+1.  ONE grid barrier per level:
+  // the frontier words are a ring of 3 (level d reads f[d-1], writes f[d],
+  // clears f[d+1], which only level d-1 read) and "seen" lags one level --
+  // level d folds level d-1's frontier into seen (and writes its level rows)
+  // while testing visits against seen | f[d-1], which is exact either way
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-  for (int d = 1; static_cast<int64_t>(d) + 1 <= a.n; ++d) {
+  unsigned long long* fr[3] = {a.f0, a.f1, a.f2};
+  // (depth <= n - 1, so level n always finds an empty frontier and stops)
+  for (int d = 1; static_cast<int64_t>(d) <= a.n; ++d) {
     const int bc = d % 3, bn = (d + 1) % 3, bz = (d + 2) % 3;
     const int qe = *(volatile int*)&a.ctl[kB64Ent + bc];
     const int qv = *(volatile int*)&a.ctl[kB64Vtx + bc];
@@ -586,8 +593,26 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
     const int p = (d - 1) & 1;
     const int64_t* qc = p ? a.q1 : a.q0;
     int64_t* qn = p ? a.q0 : a.q1;
-    unsigned long long* fc = p ? a.f1 : a.f0;
-    unsigned long long* fn = p ? a.f0 : a.f1;
+    unsigned long long* fc = fr[(d - 1) % 3];
+    unsigned long long* fn = fr[d % 3];
+    {
+      unsigned long long* fz = fr[(d + 1) % 3];  // written by level d+1
+      for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.n;
+           i += int64_t(gridDim.x) * blockDim.x)
+        fz[i] = 0ull;
+    }
+    // level d-1's frontier into seen + its level rows (a warp per vertex,
+    // lanes b and b+32 write the vertex's 256-byte level row coalesced)
+    for (int64_t e = gwarp; e < qe; e += nwarps) {
+      const int64_t ent = qc[e];
+      if ((ent >> 32) != 0) continue;
+      const int32_t w = static_cast<int32_t>(ent & 0xffffffff);
+      const unsigned long long nb = fc[w];
+      if (lane == 0) a.seen[w] |= nb;
+      int32_t* lv = a.mlevel + static_cast<int64_t>(w) * 64;
+      if ((nb >> lane) & 1ull) lv[lane] = d - 1;
+      if ((nb >> (lane + 32)) & 1ull) lv[lane + 32] = d - 1;
+    }
     fq.reset(qn, &a.ctl[kB64Ent + bn], &a.ctl[kB64Vtx + bn], &a.edges[bn], nullptr);
     if (push) {
       // small queues: every entry split over S warps (as in k_bfs1)
@@ -611,7 +636,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
           int32_t w = 0;
           if (q < e0) {
             w = __ldg(a.col + q);
-            unsigned long long bits = f & ~a.seen[w];
+            unsigned long long bits = f & ~(a.seen[w] | fc[w]);
             if (bits) {
               unsigned long long old = atomicOr(&fn[w], bits);
               has = old == 0ull;
@@ -630,7 +655,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
       const unsigned gmask = 0xffu << (grp * 8);
       for (int64_t vb = gwarp * 4; vb < a.n; vb += nwarps * 4) {
         const int64_t w = vb + grp;
-        unsigned long long need = w < a.n ? (~a.seen[w] & a.lanes) : 0ull;
+        unsigned long long need = w < a.n ? (~(a.seen[w] | fc[w]) & a.lanes) : 0ull;
         bool active = need != 0ull;
         int64_t pp = active ? a.trp[w] : 0, pe = active ? a.trp[w + 1] : 0;
         if (pe - pp > kBfsHeavy) active = false;  // hub: the warp pass below
@@ -675,7 +700,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
       // (smallest neighbour id) claims each source bit as in the groups above
       for (int64_t h = gwarp; h < a.nheavy; h += nwarps) {
         const int32_t w = a.heavy[h];
-        unsigned long long need = ~a.seen[w] & a.lanes;
+        unsigned long long need = ~(a.seen[w] | fc[w]) & a.lanes;
         unsigned long long found = 0ull;
         if (need) {
           const int64_t pe = a.trp[w + 1];
@@ -712,41 +737,21 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
       }
     }
     fq.flush();
-    grid.sync();
     if (a.tlog && blockIdx.x == 0 && threadIdx.x == 0) a.tlog[4 * d + 1] = gtimer();
-    // finalize: new frontier bits become seen + level d (a warp per vertex,
-    // lanes b and b+32 write the vertex's 256-byte level row coalesced); the
-    // old frontier words are cleared
-    const int qn_e = *(volatile int*)&a.ctl[kB64Ent + bn];
-    for (int64_t e = gwarp; e < qn_e; e += nwarps) {
-      const int64_t ent = qn[e];
-      if ((ent >> 32) != 0) continue;
-      const int32_t w = static_cast<int32_t>(ent & 0xffffffff);
-      const unsigned long long nb = fn[w];
-      if (lane == 0) a.seen[w] |= nb;
-      int32_t* lv = a.mlevel + static_cast<int64_t>(w) * 64;
-      if ((nb >> lane) & 1ull) lv[lane] = d;
-      if ((nb >> (lane + 32)) & 1ull) lv[lane + 32] = d;
-    }
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < qe;
-         e += int64_t(gridDim.x) * blockDim.x) {
-      const int64_t ent = qc[e];
-      if ((ent >> 32) == 0) fc[static_cast<int32_t>(ent & 0xffffffff)] = 0ull;
-    }
     if (leader) {
       a.ctl[kB64Levels] = d;
       if (push) a.ctl[kB64Push] += 1;
-      if (a.tlog) a.tlog[4 * d + 2] = gtimer();
     }
     grid.sync();
+    if (a.tlog && blockIdx.x == 0 && threadIdx.x == 0) a.tlog[4 * d + 2] = gtimer();
   }
 }
 
 __global__ void k_bfs64_init(unsigned long long* seen, unsigned long long* f0,
-                             unsigned long long* f1, int32_t* mlevel, int32_t* mparent,
-                             int64_t n) {
+                             unsigned long long* f1, unsigned long long* f2, int32_t* mlevel,
+                             int32_t* mparent, int64_t n) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < n) { seen[i] = 0ull; f0[i] = 0ull; f1[i] = 0ull; }
+  if (i < n) { seen[i] = 0ull; f0[i] = 0ull; f1[i] = 0ull; f2[i] = 0ull; }
   if (i < n * 64) { mlevel[i] = -1; mparent[i] = INT_MAX; }
 }
 
@@ -810,6 +815,7 @@ static void ensure_bfs64(gbx_graph* g) {
   W.seen.alloc(std::max<int64_t>(n, 1));
   W.front.alloc(std::max<int64_t>(n, 1));
   W.next.alloc(std::max<int64_t>(n, 1));
+  W.third.alloc(std::max<int64_t>(n, 1));
   W.mlevel.alloc(std::max<int64_t>(n, 1) * 64);
   W.mparent.alloc(std::max<int64_t>(n, 1) * 64);
   const int64_t qcap = n + g->A.nnz / kChunk + 64;
@@ -840,7 +846,7 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
   for (uint64_t b0 = 0; b0 < ns; b0 += 64) {
     const int nb = static_cast<int>(std::min<uint64_t>(64, ns - b0));
     k_bfs64_init<<<ceil_div(n * 64, 256), 256, 0, s>>>(W.seen.p, W.front.p, W.next.p,
-                                                       W.mlevel.p, W.mparent.p, n);
+                                                       W.third.p, W.mlevel.p, W.mparent.p, n);
     GBX_LAUNCHED();
     // lanes then distinct sources; the seed kernel builds the level-1 queue
     std::vector<int32_t> src(nb);
@@ -870,6 +876,7 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
     a.seen = W.seen.p;
     a.f0 = W.front.p;
     a.f1 = W.next.p;
+    a.f2 = W.third.p;
     a.mlevel = W.mlevel.p;
     a.mparent = W.mparent.p;
     a.q0 = q0;

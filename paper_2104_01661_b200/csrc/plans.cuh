@@ -94,7 +94,7 @@ struct BfsWork {
   DevArray<int32_t> ulist[2];               // unvisited vertices for pull levels
   DevArray<int> ctl;
   // multi-source (64 lanes)
-  DevArray<unsigned long long> seen, front, next;
+  DevArray<unsigned long long> seen, front, next, third;  // seen + a ring of 3 frontiers
   DevArray<int32_t> mlevel, mparent;        // [n][64] vertex-major
   int64_t ms_ns = 0;
   DevArray<int32_t> mqueue[2];

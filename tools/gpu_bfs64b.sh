@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out/bfs
+timeout -s KILL 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "bfs" > gpurun_out/bfs/pytest.log 2>&1; echo pytest rc=$?; tail -1 gpurun_out/bfs/pytest.log
+for i in 1 2 3; do
+timeout -s KILL 300 python bench.py --workload bfs64 --steps 20 --warmup 3 > gpurun_out/bfs/b64.json 2> gpurun_out/bfs/b64.err
+python -c "import json; d=json.load(open('gpurun_out/bfs/b64.json')); print('bfs64', round(d['ms_per_step'],4), 'ms', round(d['value'],1), 'GTEPS frac', round(d['roofline']['frac'],3))" || tail -3 gpurun_out/bfs/b64.err
+done
+GBX_BFS_TLOG=1 timeout -s KILL 300 python bench.py --workload bfs64 --steps 1 --warmup 3 2>&1 >/dev/null | grep "^bfs64" | head -8
