@@ -643,7 +643,8 @@ def bench_simple(args, dist, ws, rank, local):
            "ms_per_step": t * 1e3, "higher_is_better": True,
            "scaling": "strong" if strong else "weak", "vs_baseline": None,
            "dtype": "int32 indices", "data": "synthetic",
-           "config": {"workload": w, "scale": args.scale, "n": n, "nnz": nnz},
+           "config": {"workload": w, "scale": scale if w != "sssp" else logn, "n": n,
+                      "nnz": nnz},
            "gpu_launches": int(g.last_stats()["launches"] * args.steps),
            "clocks": clk.summary()}
     achieved = alg_bytes / t / 1e9
