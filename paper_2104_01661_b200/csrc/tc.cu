@@ -114,12 +114,13 @@ __device__ __forceinline__ TcSet tc_build(int* mem, const int32_t* __restrict__ 
   const int64_t du = e - b;
   const int32_t lo = __ldg(ucol + b), hi = __ldg(ucol + e - 1);
   const int64_t span = static_cast<int64_t>(hi) - lo + 1;
-  if (span <= kTcSpan) {
+  if (span < kTcSpan) {
     S.span = static_cast<uint32_t>(span);
     S.base = lo;
     S.log_slots = 0;
     if (clear_only) {
-      for (int w = t; w < (span + 31) / 32; w += nthreads) mem[w] = 0;
+      // words [0, span/32]: bit `span` stays 0, the clamp target of tc_has
+      for (int w = t; w <= span / 32; w += nthreads) mem[w] = 0;
     } else {
       for (int64_t q = b + t; q < e; q += nthreads) {
         const uint32_t o = static_cast<uint32_t>(__ldg(ucol + q) - lo);
@@ -146,8 +147,10 @@ __device__ __forceinline__ TcSet tc_build(int* mem, const int32_t* __restrict__ 
 template <bool kBm>
 __device__ __forceinline__ unsigned tc_has(const TcSet& S, int32_t k) {
   if constexpr (kBm) {
-    const uint32_t o = static_cast<uint32_t>(k - S.base);
-    return o < S.span ? (static_cast<uint32_t>(S.mem[o >> 5]) >> (o & 31)) & 1u : 0u;
+    // branch-free: an offset outside the span is clamped onto bit `span`,
+    // which the build keeps 0
+    const uint32_t o = min(static_cast<uint32_t>(k - S.base), S.span);
+    return (static_cast<uint32_t>(S.mem[o >> 5]) >> (o & 31)) & 1u;
   } else {
     return tc_lookup(S.mem, S.log_slots, k) ? 1u : 0u;
   }
@@ -201,11 +204,19 @@ __device__ __forceinline__ unsigned long long tc_stream_tails_k(
 #else
       for (int e = ls + lane; e < le; e += 32 * kTcUnroll) {
         int32_t k[kTcUnroll];
+        if (e - lane + 32 * kTcUnroll <= le) {
+          // a full round (warp-uniform): no per-probe bounds
 #pragma unroll
-        for (int u = 0; u < kTcUnroll; ++u) k[u] = e + 32 * u < le ? __ldg(ucol + e + 32 * u) : 0;
+          for (int u = 0; u < kTcUnroll; ++u) k[u] = __ldg(ucol + e + 32 * u);
 #pragma unroll
-        for (int u = 0; u < kTcUnroll; ++u)
-          if (e + 32 * u < le) cnt += tc_has<kBm>(S, k[u]);
+          for (int u = 0; u < kTcUnroll; ++u) cnt += tc_has<kBm>(S, k[u]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < kTcUnroll; ++u) k[u] = e + 32 * u < le ? __ldg(ucol + e + 32 * u) : 0;
+#pragma unroll
+          for (int u = 0; u < kTcUnroll; ++u)
+            if (e + 32 * u < le) cnt += tc_has<kBm>(S, k[u]);
+        }
       }
 #endif
     }
@@ -428,7 +439,7 @@ __global__ void k_item_counts(const int64_t* urp, const int32_t* ucol, const int
   int8_t c = 0;
   if (du > 0 && nl > 0) {
     const int64_t span = static_cast<int64_t>(ucol[urp[j + 1] - 1]) - ucol[urp[j]] + 1;
-    if (span <= kTcSpan || du <= kTcWarpCap) k = (nl + kTcItem - 1) / kTcItem;
+    if (span < kTcSpan || du <= kTcWarpCap) k = (nl + kTcItem - 1) / kTcItem;
     else c = du <= kTcCtaCap ? 1 : 2;
   }
   cnt[j] = k;
