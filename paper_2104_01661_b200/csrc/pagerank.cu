@@ -195,6 +195,9 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k,
                                                 typename cub::BlockReduce<double, BS>::TempStorage& red,
                                                 PrBin* s_bins, V* s_x) {
   using BlockReduce = cub::BlockReduce<double, BS>;
+  // the shared-memory prefix exists only in the 1024-thread variant: for 256
+  // threads the bound is a compile-time 0 and the per-gather test folds away
+  const int64_t hot = BS == 1024 ? a.hot : 0;
   const V *x_cur, *r_cur;
   V *x_nxt, *r_nxt;
   pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
@@ -224,7 +227,7 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k,
       }
 #pragma unroll
       for (int j = 0; j < kPrIpl; ++j)
-        if (c[j] >= 0) s += static_cast<double>(pr_xg(s_x, a.hot, a.l1hot, x_cur, c[j]));
+        if (c[j] >= 0) s += static_cast<double>(pr_xg(s_x, hot, a.l1hot, x_cur, c[j]));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
@@ -263,7 +266,7 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k,
         }
 #pragma unroll
         for (int q = 0; q < kPrB0Ipl; ++q)
-          if (c[q] >= 0) s += static_cast<double>(pr_xg(s_x, a.hot, a.l1hot, x_cur, c[q]));
+          if (c[q] >= 0) s += static_cast<double>(pr_xg(s_x, hot, a.l1hot, x_cur, c[q]));
 #pragma unroll
         for (int q = 0; q < kPrB0Ipl; ++q) c[q] = nx[q];
       }
@@ -294,7 +297,7 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k,
           for (int q = 0; q < 4; ++q) nx[q] = j + 4 + q < L ? ld_stream(cp + (j + 4 + q) * m) : -1;
           V t[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) t[q] = c[q] >= 0 ? pr_xg(s_x, a.hot, a.l1hot, x_cur, c[q]) : V(0);
+          for (int q = 0; q < 4; ++q) t[q] = c[q] >= 0 ? pr_xg(s_x, hot, a.l1hot, x_cur, c[q]) : V(0);
           s += (static_cast<double>(t[0]) + static_cast<double>(t[1])) +
                (static_cast<double>(t[2]) + static_cast<double>(t[3]));
 #pragma unroll
