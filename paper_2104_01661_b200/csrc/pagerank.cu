@@ -1519,8 +1519,8 @@ void pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1
     GBX_LAUNCHED();
     P.g_damping = damping;
   }
-  if (itermax <= 0) {
-    if (iters) *iters = std::max(itermax, 0);
+  if (itermax <= 0 || P.n == 0) {  // as pagerank_run: nothing to iterate
+    if (iters) *iters = itermax <= 0 ? std::max(itermax, 0) : 0;
     return;
   }
   PrArgs<float> a = make_args<float>(P, damping, tol, itermax);
