@@ -74,6 +74,26 @@ class CpuShardBackend:
             self._xs[i - self.rb] = rn * damping / self.deg[i] if self.deg[i] > 0 else 0.0
         self._xs[self.chunk - 1] = l1
 
+    # ---- the fused run's orchestration (dist.sharded_pagerank_p2p): the
+    # device kernel exchanges x through peer memory; here every rank runs the
+    # same sequential iterations on its replicated graph and keeps its rows
+    def p2p_setup(self, dist):
+        self._p2p_ready = True
+
+    def p2p_init(self, damping):
+        assert self._p2p_ready
+        self.init(damping)
+
+    def p2p_run(self, damping, tol, itermax):
+        import oracle as O
+        want, iters = O.pagerank(self.n, self.trp, self.tcol, self.deg, damping, tol, itermax)
+        self._p2p_r = torch.zeros(self.chunk, dtype=torch.float64)
+        self._p2p_r[: self.re - self.rb] = torch.from_numpy(want[self.rb:self.re].copy())
+        return iters
+
+    def p2p_result(self, iters):
+        return self._p2p_r
+
     def l1_post(self, k):
         parts = self._x.view(self.world, self.chunk)[:, self.chunk - 1]
         return sum(float(parts[q]) for q in range(self.world))

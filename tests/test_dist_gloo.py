@@ -42,6 +42,10 @@ def _worker(rank, world, port, q, what):
         if what == "pr":
             ranks, iters = sharded_pagerank(be, dist, 0.85, 1e-4, 100)
             q.put((rank, "pr", iters, ranks.tolist()))
+        elif what == "prp2p":
+            from paper_2104_01661_b200.dist import sharded_pagerank_p2p
+            ranks, iters = sharded_pagerank_p2p(be, dist, 0.85, 1e-4, 100)
+            q.put((rank, "prp2p", iters, ranks.tolist()))
         elif what == "bc":
             c = sharded_betweenness(be, dist, BC_SOURCES)
             q.put((rank, "bc", None, c.tolist()))
@@ -81,6 +85,20 @@ def test_sharded_pagerank_gloo_matches_oracle():
         assert it == iters
         got = np.array(ranks)
         assert np.abs(got - want).sum() / np.abs(want).sum() <= 1e-9
+
+
+def test_sharded_pagerank_p2p_orchestration_gloo():
+    """dist.sharded_pagerank_p2p's host side (layout, init, barrier, the final
+    padded all-gather and the unpermute) over gloo; the fused kernel itself
+    runs on the device (tests/test_pr_p2p_gpu.py)."""
+    out = _run("prp2p")
+    rp, col = O.rmat_graph(9, 8, seed=3, undirected=False)
+    n = len(rp) - 1
+    trp, tcol, _ = O.transpose(n, rp, col)
+    want, iters = O.pagerank(n, trp, tcol, np.diff(rp))
+    for _, _, it, ranks in out:
+        assert it == iters
+        assert np.array_equal(np.array(ranks), want)
 
 
 def test_sharded_triangle_count_gloo_matches_oracle():
