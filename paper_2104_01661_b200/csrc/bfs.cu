@@ -87,6 +87,8 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ int32_t s_buf[kBfsThreads / 32][kBfsBuf];
   __shared__ int32_t s_ubuf[kBfsThreads / 32][kBfsBuf];
+  __shared__ int32_t s_kbuf[kBfsThreads / 32][kBfsBuf];
+  __shared__ __align__(8) int s_red[6];
   FrontierQueue<kBfsBuf> fq;
   fq.buf = s_buf[threadIdx.x >> 5];
   fq.rp = a.rp;
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
         fq.push(has, w);
       }
     }
-    fq.flush();
+    fq.flush_block(s_kbuf[threadIdx.x >> 5], s_red);
     if (a.tlog && gtid == 0) a.tlog[4 * d + 1] = gtimer();
     if (gtid == 0) {
       a.ctl[5] = d;
@@ -554,6 +556,8 @@ constexpr int kB64Ent = 0, kB64Vtx = 3, kB64Levels = 6, kB64Push = 7, kB64Words 
 __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ int32_t s_buf[kBfsThreads / 32][kBfsBuf];
+  __shared__ int32_t s_kbuf[kBfsThreads / 32][kBfsBuf];
+  __shared__ __align__(8) int s_red[6];
   FrontierQueue<kBfsBuf> fq;
   fq.buf = s_buf[threadIdx.x >> 5];
   fq.rp = a.rp;
@@ -736,7 +740,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
         fq.push(has, w);
       }
     }
-    fq.flush();
+    fq.flush_block(s_kbuf[threadIdx.x >> 5], s_red);
     if (a.tlog && blockIdx.x == 0 && threadIdx.x == 0) a.tlog[4 * d + 1] = gtimer();
     if (leader) {
       a.ctl[kB64Levels] = d;

@@ -142,6 +142,79 @@ struct FrontierQueue {
     n += __popc(b);
     if (n > CAP - 32) flush();
   }
+
+  // End-of-level flush called by EVERY thread of the CTA (block-uniform): the
+  // warps' totals meet in shared memory and ONE thread per CTA reserves the
+  // CTA's runs with the global atomics (every warp flushing at the same moment
+  // piled ~10^4 atomics onto the same three addresses at the end of a level).
+  // The per-vertex chunk counts of pass 1 are kept in kbuf (CAP ints per
+  // warp), so pass 2 re-reads no row pointers.  s_red: 6 ints of CTA shared
+  // memory, 8-byte aligned.
+  __device__ __forceinline__ void flush_block(int* kbuf, int* s_red) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    unsigned long long* s_edges = reinterpret_cast<unsigned long long*>(s_red + 4);
+    if (threadIdx.x == 0) {
+      s_red[0] = 0;
+      s_red[1] = 0;
+      *s_edges = 0ull;
+    }
+    __syncthreads();
+    int ent = 0;
+    unsigned long long edges = 0;
+    for (int i = lane; i < n; i += 32) {
+      const int32_t v = buf[i];
+      const int64_t d = rp[v + 1] - rp[v];
+      const int k = nchunks(d, chunk);
+      kbuf[i] = k;
+      ent += k;
+      edges += static_cast<unsigned long long>(d);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ent += __shfl_xor_sync(full, ent, o);
+      edges += __shfl_xor_sync(full, edges, o);
+    }
+    int eoff = 0, voff = 0;
+    if (lane == 0 && n > 0) {
+      eoff = atomicAdd(&s_red[0], ent);
+      voff = atomicAdd(&s_red[1], n);
+      if (cnt_edges) atomicAdd(s_edges, edges);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int te = s_red[0], tv = s_red[1];
+      s_red[2] = te ? atomicAdd(cnt_ent, te) : 0;
+      s_red[3] = tv ? atomicAdd(cnt_vtx, tv) : 0;
+      if (cnt_edges && tv) atomicAdd(cnt_edges, *s_edges);
+    }
+    __syncthreads();
+    const int ebase = s_red[2] + __shfl_sync(full, eoff, 0);
+    const int vbase = s_red[3] + __shfl_sync(full, voff, 0);
+    int off = ebase;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      int32_t v = 0;
+      int k = 0;
+      if (i < n) {
+        v = buf[i];
+        k = kbuf[i];
+        if (list) list[vbase + i] = v;
+      }
+      int incl = k;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(full, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int tot = __shfl_sync(full, incl, 31);
+      for (int c = 0; c < k; ++c)
+        q[off + incl - k + c] = (static_cast<int64_t>(c) << 32) | static_cast<uint32_t>(v);
+      off += tot;
+    }
+    __syncwarp();
+    n = 0;
+  }
 };
 
 }  // namespace gbx
