@@ -204,6 +204,8 @@ struct BcArgs {
 // forward push over A from the entries of level d-1
 __global__ void __launch_bounds__(256) k_bc_push(BcArgs a) {
   __shared__ int32_t s_buf[8][kBcBuf];
+  __shared__ int32_t s_kbuf[8][kBcBuf];
+  __shared__ __align__(8) int s_red[8];
   FrontierQueue<kBcBuf> fq;
   fq.buf = s_buf[threadIdx.x >> 5];
   fq.rp = a.rp;
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(256) k_bc_push(BcArgs a) {
       fq.push(has, v);
     }
   }
-  fq.flush();
+  fq.flush_block(s_kbuf[threadIdx.x >> 5], s_red);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) found |= __shfl_xor_sync(kAll, found, o);
   if (lane == 0 && found) atomicOr(&a.cnt[3], static_cast<int>(found));
@@ -298,6 +300,8 @@ __device__ __forceinline__ unsigned bc_settle(const BcArgs& a, int64_t v, unsign
 __global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_pull(BcArgs a) {
   __shared__ int32_t s_buf[8][kBcBuf];
   __shared__ int32_t s_ubuf[8][kBcBuf];
+  __shared__ int32_t s_kbuf[8][kBcBuf];
+  __shared__ __align__(8) int s_red[8];
   FrontierQueue<kBcBuf> fq;
   fq.buf = s_buf[threadIdx.x >> 5];
   fq.rp = a.rp;
@@ -360,7 +364,7 @@ __global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_pull(BcArgs a) {
       uq.push(lane == 0 && (um & ~nm) != 0, static_cast<int32_t>(v));
     }
   }
-  fq.flush();
+  fq.flush_block(s_kbuf[threadIdx.x >> 5], s_red);
   uq.flush();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) found |= __shfl_xor_sync(kAll, found, o);
