@@ -345,6 +345,18 @@ __device__ __forceinline__ int64_t bucket_k(D d, const A& a) {
   return bucket_of<D>(d, a.delta);
 }
 
+// lower dist[v] to nd (an improvement landing in the later bucket kb) and
+// report whether v must be appended to kb's queue: exactly when the distance
+// it replaced was not already in bucket kb (infinite, or a later bucket --
+// that entry goes stale).  One returning atomic replaces the fire-and-forget
+// min + the returning atomicOr on a per-bucket membership bitmap.
+template <typename D, typename A>
+__device__ __forceinline__ bool bucket_enter(D* dist, D nd, int64_t kb, const A& a) {
+  const D old = atomicMin(dist, nd);
+  if (!(nd < old)) return false;
+  return old == DistTraits<D>::inf() || bucket_k<D>(old, a) != kb;
+}
+
 template <typename D, typename E>
 struct SsspBArgs {
   const int64_t* rp;
@@ -522,22 +534,18 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
           if (ok[q4]) {
             ++nrel;
             if (nd[q4] < cur[q4]) {
-              // fire-and-forget min: a push whose value lost the race is a
-              // harmless extra relaxation (stale bucket entries are skipped)
-              atomicMin(&a.dist[v[q4]], nd[q4]);
               const uint32_t bit = 1u << (v[q4] & 31);
               const int64_t kb = bucket_k<D>(nd[q4], a);
               if (kb <= k && phase != 2) {  // (a heavy edge always leaves the bucket)
-#if GBX_SSSP_PRECHECK
-                if (!(*(volatile uint32_t*)&push_bits[v[q4] >> 5] & bit))
-#endif
+                // fire-and-forget min: a push whose value lost the race is a
+                // harmless extra relaxation; the near queue dedups by bitmap
+                atomicMin(&a.dist[v[q4]], nd[q4]);
                 near_push = !(atomicOr(&push_bits[v[q4] >> 5], bit) & bit);
               } else {
+                // a later bucket: the returned old distance is the dedup -- v
+                // already sits in bucket kb's queue iff its old distance did
                 bidx = static_cast<int>(kb & nbm);
-#if GBX_SSSP_PRECHECK
-                if (!(*(volatile uint32_t*)&a.bbits[bidx * a.words + (v[q4] >> 5)] & bit))
-#endif
-                buck_push = !(atomicOr(&a.bbits[bidx * a.words + (v[q4] >> 5)], bit) & bit);
+                buck_push = bucket_enter<D>(&a.dist[v[q4]], nd[q4], kb, a);
               }
             }
           }
@@ -593,10 +601,9 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
           if (ok[q4]) {
             ++nrel;
             if (nd[q4] < cur[q4]) {
-              atomicMin(&a.dist[v[q4]], nd[q4]);
-              const uint32_t bit = 1u << (v[q4] & 31);
-              bidx = static_cast<int>(bucket_k<D>(nd[q4], a) & nbm);
-              buck_push = !(atomicOr(&a.bbits[bidx * a.words + (v[q4] >> 5)], bit) & bit);
+              const int64_t kb = bucket_k<D>(nd[q4], a);
+              bidx = static_cast<int>(kb & nbm);
+              buck_push = bucket_enter<D>(&a.dist[v[q4]], nd[q4], kb, a);
             }
           }
           bucq.push(buck_push, v[q4], bidx, a.bq, a.cap, a.bcnt, a.nb);
@@ -726,7 +733,6 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
       if (i < cnt) {
         v = src[i];
         const uint32_t bit = 1u << (v & 31);
-        atomicAnd(&a.bbits[b * a.words + (v >> 5)], ~bit);
         // stale entries (improved into an earlier bucket since) are skipped
         if (bucket_k<D>(*(volatile D*)&a.dist[v], a) == k)
           to_near = !(atomicOr(&push_bits[v >> 5], bit) & bit);
