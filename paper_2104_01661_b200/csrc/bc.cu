@@ -963,7 +963,7 @@ __global__ void k_bc_own_hubs(const int64_t* hent, int nhent, const int32_t* hv,
   if (e >= nhent) return;
   const int64_t ent = hent[e];
   const int32_t v = hv[static_cast<int>(ent & 0xffffffff)];
-  if (v >= rb && v < re) out[atomicAdd(cnt, 1)] = ent;
+  if (v >= rb && v < re) out[agg_append(cnt)] = ent;
 }
 
 __global__ void k_bc_pack_fwd(const int32_t* list, int nl, int d, const int32_t* level,
@@ -1017,7 +1017,7 @@ __global__ void k_bc_own_filter(const int32_t* list, int64_t nl, int64_t rb, int
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= nl) return;
   const int32_t v = list[i];
-  if (v >= rb && v < re) out[atomicAdd(cnt, 1)] = v;
+  if (v >= rb && v < re) out[agg_append(cnt)] = v;
 }
 
 __global__ void k_bc_pack_back(const int32_t* list, int nl, const double* coef, BcRec* out) {

@@ -999,7 +999,7 @@ __global__ void __launch_bounds__(256) k_bfs_shard_pull(const int64_t* trp, cons
         atomicOr(next_slice + w, 1u << (v & 31));
         ++found;
       } else if (nonempty && level[v] == -1) {
-        ul_out[atomicAdd(&cnt[1], 1)] = static_cast<int32_t>(v);
+        ul_out[agg_append(&cnt[1])] = static_cast<int32_t>(v);
       }
     }
   }

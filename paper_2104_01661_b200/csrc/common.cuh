@@ -1,6 +1,7 @@
 // common.cuh -- shared internals of libgbx.so (B200 / sm_100a).
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -152,6 +153,21 @@ struct gbx_mat {
     }
   }
 };
+
+namespace gbx {
+
+// Warp-aggregated list append: the threads that call it together (coalesced)
+// reserve their slots with ONE atomic on the shared counter -- per-thread
+// atomics on a single address serialise in L2 (10^5-10^6 per pass).
+__device__ __forceinline__ int agg_append(int* cnt) {
+  namespace cg = cooperative_groups;
+  cg::coalesced_group g = cg::coalesced_threads();
+  int base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(cnt, static_cast<int>(g.size()));
+  return g.shfl(base, 0) + static_cast<int>(g.thread_rank());
+}
+
+}  // namespace gbx
 
 namespace gbx {
 

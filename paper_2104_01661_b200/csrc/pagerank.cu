@@ -777,7 +777,7 @@ __global__ void k_pr_gather_short(const int64_t* atrp, const int32_t* atcol,
 // (A's rows are not in length order here: the long ones are listed first)
 __global__ void k_pr_list_long(const int64_t* prp, int64_t n, int32_t* list, int* cnt) {
   const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (r < n && prp[r + 1] - prp[r] > kPrGatherLong) list[atomicAdd(cnt, 1)] = static_cast<int32_t>(r);
+  if (r < n && prp[r + 1] - prp[r] > kPrGatherLong) list[agg_append(cnt)] = static_cast<int32_t>(r);
 }
 // long rows cut into kPrGatherChunk-element items (one hub row per CTA left
 // a single CTA looping over 10^5 elements at the end of the launch)
