@@ -47,7 +47,10 @@ constexpr int kPrThreads = 256;
 #ifndef GBX_PR_MINB
 #define GBX_PR_MINB 6  // resident CTAs per SM the rows kernel is compiled for
 #endif
-constexpr int kPrIpl = 8;          // items per lane: 8 independent gathers in flight
+#ifndef GBX_PR_IPL
+#define GBX_PR_IPL 16  // measured: 4 / 8 / 16 -> 219.1 / 215.8 / 215.0 us per iteration
+#endif
+constexpr int kPrIpl = GBX_PR_IPL;  // chunk walks: independent gathers in flight per lane
 #ifndef GBX_PR_B0IPL
 #define GBX_PR_B0IPL 2  // measured: 2 and 4 within 1%, 8 slower (registers)
 #endif
