@@ -1246,6 +1246,17 @@ static void* persist_fn(const PrArgs<V>& a) {
                    : reinterpret_cast<void*>(k_pr_persist<V, kPrThreads>);
 }
 
+#ifndef GBX_PR_PERSIST_CARVEOUT
+#define GBX_PR_PERSIST_CARVEOUT -1
+#endif
+static int persist_carveout() {
+  static const int c = [] {
+    const char* cv = std::getenv("GBX_PR_CARVEOUT");
+    return cv ? std::atoi(cv) : GBX_PR_PERSIST_CARVEOUT;
+  }();
+  return c;
+}
+
 template <typename V>
 static bool persist_args(PrPlan& P, double damping, double tol, int itermax, PrArgs<V>& a,
                          int& block, size_t& smem) {
@@ -1260,6 +1271,11 @@ static bool persist_args(PrPlan& P, double damping, double tol, int itermax, PrA
       return false;
     }
   }
+  // shared-memory carveout of the persistent kernel (percent of the maximum;
+  // GBX_PR_CARVEOUT overrides, < 0 leaves the driver's choice)
+  if (const int carve = persist_carveout(); carve >= 0)
+    (void)cudaFuncSetAttribute(persist_fn<V>(a), cudaFuncAttributePreferredSharedMemoryCarveout,
+                               carve);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persist_fn<V>(a), block, smem) !=
           cudaSuccess || per_sm < 1) {

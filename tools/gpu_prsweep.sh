@@ -1,7 +1,7 @@
 #!/bin/bash
 # PageRank A/B sweep: variant libraries x cache knobs, bench line per run.
 mkdir -p gpurun_out/sweep
-timeout -s KILL 600 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "pagerank or pr_" > gpurun_out/sweep/pytest.log 2>&1; echo pytest rc=$?; tail -1 gpurun_out/sweep/pytest.log
+[ -n "$NOTEST" ] || timeout -s KILL 600 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "pagerank or pr_" > gpurun_out/sweep/pytest.log 2>&1; echo pytest rc=$?; tail -1 gpurun_out/sweep/pytest.log
 run() {  # name, env...
   local name=$1; shift
   env "$@" timeout -s KILL 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/sweep/$name.json 2> gpurun_out/sweep/$name.err
