@@ -1578,6 +1578,8 @@ void pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1
   m.rank = S.rank;
   m.nranks = S.nranks;
   int per_sm = 0;
+  if (const int carve = persist_carveout(); carve >= 0)  // same L1 split as k_pr_persist
+    (void)cudaFuncSetAttribute(k_pr_persist_p2p, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
   GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_persist_p2p, kPrThreads, 0));
   a.grid_rows = device_sms() * std::max(per_sm, 1);
   if (static_cast<int64_t>(P.l1_fin.n) < a.grid_rows || static_cast<int64_t>(P.l1_block.n) < a.grid_rows)
