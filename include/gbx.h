@@ -83,6 +83,22 @@ typedef struct gbx_graph gbx_graph;
 int gbx_init(int device, char msg[GBX_MSG_LEN]);
 const char* gbx_version(void);
 
+/* Tuning / diagnostics options (process-wide; no reference counterpart -- the
+ * reference has no device knobs).  Unknown names and out-of-range values ->
+ * GBX_INVALID_VALUE.  gbx_option_name(i) enumerates them (NULL past the end):
+ *   pagerank.l1_window_kb  144    bytes of x gathered with L1 evict_last
+ *   pagerank.carveout      10     % shared-memory carveout of the row kernels (-1: driver)
+ *   pagerank.host_loop     0      1: one launch per iteration (for ncu captures)
+ *   p2p.timeout_ms         10000  bound of the fused multi-GPU exchange's peer wait
+ *   bfs.alpha              14     push while frontier edges < nnz/alpha (0: bfs.cpp:77-78 rule)
+ *   bfs64.pull_div         2      64-lane batch: pull when frontier edges > nnz/div
+ *   bfs.trace / sssp.trace 0      1: per-level %globaltimer log on stderr
+ *   bc.alpha               14     as bfs.alpha for the Brandes forward sweep */
+int gbx_set_option(const char* name, int64_t value, char msg[GBX_MSG_LEN]);
+int gbx_reset_option(const char* name, char msg[GBX_MSG_LEN]);
+int gbx_get_option(const char* name, int64_t* value, char msg[GBX_MSG_LEN]);
+const char* gbx_option_name(int index);
+
 /* ---- graph object (graph.hpp:27-60, graph.cpp:16-220) --------------------- */
 
 /* graph_new(SparseMatrix&&, Kind) (graph.cpp:16-28): validates the CSR like
@@ -369,6 +385,17 @@ int gbx_pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t*
                          float* r1, double damping, double tol, int itermax, int* iters,
                          char msg[GBX_MSG_LEN]);
 /* chunk (slot length of the padded layout) and, if non-NULL, bounds[nranks+1]. */
+/* The same run for `nranks` shards that all live on THIS GPU, as ONE
+ * cooperative launch (shard v = rank v; its CTAs are co-resident with every
+ * other rank's, so no rank ever waits on a rank that is not running): the
+ * single-GPU emulation of the multi-rank protocol (tests, gbx_comm_init_local).
+ * Peer arrays as above, r0[v] / r1[v] per rank.  Fails with GBX_CUDA_ERROR if
+ * the ranks disagree on the iteration count. */
+int gbx_pr_shard_run_p2p_multi(gbx_graph* const* shards, int nranks, const uint64_t* x0_peers,
+                               const uint64_t* x1_peers, const uint64_t* l1_peers,
+                               const uint64_t* sig_peers, float* const* r0, float* const* r1,
+                               double damping, double tol, int itermax, int* iters,
+                               char msg[GBX_MSG_LEN]);
 int gbx_pr_shard_layout(const gbx_graph* g, int64_t* chunk, int64_t* bounds,
                         char msg[GBX_MSG_LEN]);
 int gbx_pr_shard_init(gbx_graph* g, float* x_full_dev, float* r_local_dev, double damping,

@@ -29,6 +29,9 @@ _pp = C.POINTER(C.c_void_p)
 # name: (argtypes) -- every function returns int and takes char* msg last
 _SIGS = {
     "gbx_init": [_int],
+    "gbx_set_option": [_cp, _i64],
+    "gbx_reset_option": [_cp],
+    "gbx_get_option": [_cp, _vp],
     "gbx_graph_new": [_pp, _i64, _vp, _vp, _vp, _int, _int],
     "gbx_graph_new32": [_pp, _i64, _vp, _vp, _vp, _int, _int],
     "gbx_graph_free": [_pp],
@@ -73,6 +76,8 @@ _SIGS = {
     "gbx_pr_shard_step": [_vp, _vp, _vp, _vp, _vp, _vp, _dbl],
     "gbx_pr_shard_layout": [_vp, _vp, _vp],
     "gbx_pr_shard_run_p2p": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _int, _vp],
+    "gbx_pr_shard_run_p2p_multi": [_vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _int,
+                                   _vp],
     "gbx_partition_rows": [_vp, _vp, _int, _int],
     "gbx_triangle_count_rows": [_vp, _vp, _i64, _i64],
     "gbx_tc_partition": [_vp, _vp, _int],
@@ -114,9 +119,11 @@ def lib():
             f.restype = C.c_int
         L.gbx_version.restype = C.c_char_p
         L.gbx_version.argtypes = []
+        L.gbx_option_name.restype = C.c_char_p
+        L.gbx_option_name.argtypes = [C.c_int]
         _lib = L
     return _lib
 
 
 def exported_symbols():
-    return sorted(list(_SIGS) + ["gbx_version"])
+    return sorted(list(_SIGS) + ["gbx_version", "gbx_option_name"])

@@ -132,6 +132,23 @@ extern "C" {
 
 const char* gbx_version(void) { return GBX_VERSION; }
 
+int gbx_set_option(const char* name, int64_t value, char* msg) {
+  return guard(msg, [&] { gbx::set_option(name, value); });
+}
+
+int gbx_reset_option(const char* name, char* msg) {
+  return guard(msg, [&] { gbx::reset_option(name); });
+}
+
+int gbx_get_option(const char* name, int64_t* value, char* msg) {
+  return guard(msg, [&] {
+    if (!value) gbx::fail(GBX_NULL_ARGUMENT, "value is NULL");
+    *value = gbx::get_option(name);
+  });
+}
+
+const char* gbx_option_name(int index) { return gbx::option_name(index); }
+
 int gbx_init(int device, char* msg) {
   return guard(msg, [&] {
     int count = 0;
@@ -855,6 +872,19 @@ int gbx_pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t*
     gbx::Scope sc(g);
     gbx::pr_shard_run_p2p(g, x0_peers, x1_peers, l1_peers, sig_peers, r0, r1, damping, tol,
                           itermax, iters);
+  });
+}
+
+int gbx_pr_shard_run_p2p_multi(gbx_graph* const* shards, int nranks, const uint64_t* x0_peers,
+                               const uint64_t* x1_peers, const uint64_t* l1_peers,
+                               const uint64_t* sig_peers, float* const* r0, float* const* r1,
+                               double damping, double tol, int itermax, int* iters, char* msg) {
+  return guard(msg, [&] {
+    if (!shards || !r0 || !r1) gbx::fail(GBX_NULL_ARGUMENT, "pr_shard_run_p2p_multi: NULL array");
+    std::vector<std::unique_ptr<gbx::Scope>> sc;
+    for (int v = 0; v < nranks; ++v) sc.emplace_back(new gbx::Scope(need(shards[v])));
+    gbx::pr_shard_run_p2p_multi(shards, nranks, x0_peers, x1_peers, l1_peers, sig_peers, r0, r1,
+                                damping, tol, itermax, iters);
   });
 }
 

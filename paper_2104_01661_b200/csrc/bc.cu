@@ -742,7 +742,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
   }
   GBX_CUDA(cudaMemsetAsync(W.cent.p, 0, n1 * 8, s));
   const int grid = device_sms() * 8;
-  static const int alpha = std::getenv("GBX_BC_ALPHA") ? std::atoi(std::getenv("GBX_BC_ALPHA")) : 14;
+  const int alpha = static_cast<int>(option(kOptBcAlpha));
   int* ctl = W.ctl.p;
   unsigned long long* dedges = reinterpret_cast<unsigned long long*>(W.ctl.p + 4);
   int64_t launches = 1, edges = 0;

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
             unsigned hits = 0u;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              if (u[k] >= 0 && ((__ldg(bc + (u[k] >> 5)) >> (u[k] & 31)) & 1u)) hits |= 1u << k;
+              if (u[k] >= 0 && ((ld_weak(bc + (u[k] >> 5)) >> (u[k] & 31)) & 1u)) hits |= 1u << k;
             if (hits) {
               const int k = __ffs(hits) - 1;
               found = k == 0 ? u[0] : k == 1 ? u[1] : k == 2 ? u[2] : u[3];
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
             bool hit = false;
             if (gact && gp + sub < ge) {
               u = __ldg(a.tcol + gp + sub);
-              hit = (__ldg(bc + (u >> 5)) >> (u & 31)) & 1u;
+              hit = (ld_weak(bc + (u >> 5)) >> (u & 31)) & 1u;
             }
             const unsigned bal = __ballot_sync(kFull, hit);
             const unsigned gb = (bal >> (grp * 8)) & 0xffu;
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
           bool hit = false;
           if (pp + lane < pe) {
             u = __ldg(a.tcol + pp + lane);
-            hit = (__ldg(bc + (u >> 5)) >> (u & 31)) & 1u;
+            hit = (ld_weak(bc + (u >> 5)) >> (u & 31)) & 1u;
           }
           const unsigned bal = __ballot_sync(kFull, hit);
           if (bal) {
@@ -448,7 +448,7 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
   const Csr& A = g->A;
   const Csr* AT = use_at ? &g->AT() : nullptr;
   if (AT) ensure_heavy(g, *AT);
-  static const bool tlog_on = std::getenv("GBX_BFS_TLOG") != nullptr;
+  const bool tlog_on = option(kOptBfsTrace) != 0;
   cudaEvent_t ev[4];
   if (tlog_on) {
     for (auto& e : ev) GBX_CUDA(cudaEventCreate(&e));
@@ -465,7 +465,7 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
   a.n = n;
   a.nnz = A.nnz;
   a.mode = use_at ? direction : GBX_BFS_PUSH;
-  static const int alpha = std::getenv("GBX_BFS_ALPHA") ? std::atoi(std::getenv("GBX_BFS_ALPHA")) : 14;
+  const int alpha = static_cast<int>(option(kOptBfsAlpha));
   a.alpha = alpha;
   a.ul0 = W.ulist[0].p;
   a.ul1 = W.ulist[1].p;
@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
           unsigned long long hit = 0ull;
           if (active && pp + sub < pe) {
             u = __ldg(a.tcol + pp + sub);
-            hit = __ldg(fc + u) & need;
+            hit = ld_weak(fc + u) & need;
           }
           // exclusive prefix-OR over the 8 lanes of the group: the lowest
           // lane (smallest neighbour id) claims each newly found source bit
@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
             unsigned long long hit = 0ull;
             if (pp + lane < pe) {
               u = __ldg(a.tcol + pp + lane);
-              hit = __ldg(fc + u) & need;
+              hit = ld_weak(fc + u) & need;
             }
             unsigned long long incl = hit;
 #pragma unroll
@@ -887,11 +887,11 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
     a.q1 = q1;
     a.ctl = W.mctl.p;
     a.edges = reinterpret_cast<unsigned long long*>(W.mctl.p + 8);
-    static const int pull_div = std::getenv("GBX_BFS64_PULLDIV") ? std::atoi(std::getenv("GBX_BFS64_PULLDIV")) : 2;
+    const int pull_div = static_cast<int>(option(kOptBfs64PullDiv));
     a.pull_div = pull_div;
     a.heavy = W.heavy.p;
     a.nheavy = W.nheavy;
-    static const bool tlog_on = std::getenv("GBX_BFS_TLOG") != nullptr;
+    const bool tlog_on = option(kOptBfsTrace) != 0;
     if (tlog_on) {
       if (!W.tlog.p) W.tlog.alloc(4 * 256);
       GBX_CUDA(cudaMemsetAsync(W.tlog.p, 0, W.tlog.bytes(), s));

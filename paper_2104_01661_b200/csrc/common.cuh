@@ -30,6 +30,32 @@ struct Error : std::runtime_error {
   } while (0)
 #define GBX_LAUNCHED() GBX_CUDA(cudaGetLastError())
 
+// Coherent weak global load for data another CTA rewrites inside the same
+// persistent launch (frontier bitmaps, contribution vectors): NOT the .nc
+// path (__ldg), which is only defined for data read-only for the whole launch.
+// The grid barrier between levels orders it after the writes.
+template <typename T>
+__device__ __forceinline__ T ld_weak(const T* p) {
+  return *p;  // a plain LDG (pointers are not __restrict__, so never promoted to .nc)
+}
+
+// Tuning / diagnostics options (options.cu): ONE documented registry set
+// through gbx_set_option (include/gbx.h) instead of per-knob environment
+// variables.  Read at call time; defaults are the measured optimum.
+enum Opt : int {
+  kOptPrL1WindowKb = 0,  // "pagerank.l1_window_kb": bytes of x gathered L1 evict_last
+  kOptPrCarveout,        // "pagerank.carveout": % shared-memory carveout of the row kernels
+  kOptPrHostLoop,        // "pagerank.host_loop": per-iteration launches (ncu captures)
+  kOptP2pTimeoutMs,      // "p2p.timeout_ms": bound of the fused exchange's cross-rank spin
+  kOptBfsAlpha,          // "bfs.alpha": push while frontier edges < nnz / alpha (0: reference rule)
+  kOptBfs64PullDiv,      // "bfs64.pull_div"
+  kOptBfsTrace,          // "bfs.trace": per-level %globaltimer log to stderr
+  kOptBcAlpha,           // "bc.alpha"
+  kOptSsspTrace,         // "sssp.trace": per-phase %globaltimer log to stderr
+  kOptCount
+};
+int64_t option(Opt o);
+
 constexpr int kSMs = 148;  // B200; the runtime value is queried in device_sms()
 int device_sms();
 
@@ -204,6 +230,10 @@ void compute_degrees(cudaStream_t s, const Csr& A, DevArray<int32_t>& out, bool 
 void require_at(const gbx_graph* g, const char* who);
 void require_rowdeg(const gbx_graph* g, const char* who);
 void reset_plans(gbx_graph* g);
+void set_option(const char* name, int64_t v);
+void reset_option(const char* name);
+int64_t get_option(const char* name);
+const char* option_name(int i);
 // stable ascending/descending permutation of ids by key (cub radix, LSD = stable)
 void sort_ids_by_key(cudaStream_t s, const int32_t* key, int64_t n, bool ascending,
                      DevArray<int32_t>& perm);
@@ -276,6 +306,10 @@ void pr_shard_unpermute(gbx_graph* g, const float* r_full, double* out_host);
 void pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, float* r_new,
                    float* x_slice, double* l1, double damping);
 void pr_shard_layout(gbx_graph* g, int64_t* chunk, int64_t* bounds);
+void pr_shard_run_p2p_multi(gbx_graph* const* gs, int nv, const uint64_t* x0_peers,
+                            const uint64_t* x1_peers, const uint64_t* l1_peers,
+                            const uint64_t* sig_peers, float* const* r0s, float* const* r1s,
+                            double damping, double tol, int itermax, int* iters);
 void pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1_peers,
                       const uint64_t* l1_peers, const uint64_t* sig_peers, float* r0, float* r1,
                       double damping, double tol, int itermax, int* iters);

@@ -1,5 +1,5 @@
 // pagerank.cu -- GAP PageRank (algo/pagerank.cpp:8-81) as a fused pull SpMV,
-// looped on the device by a CUDA-graph WHILE node.
+// every iteration inside ONE persistent cooperative launch.
 //
 // Reference per iteration: contrib = prior ./ (deg/damping) (:55-56), rank =
 // teleport (:58), rank += AT plus.second contrib (:59-61), L1 = sum|prior -
@@ -9,22 +9,20 @@
 //   * vertices are relabeled by descending in-degree (stable).  R-MAT in- and
 //     out-degree skews coincide, so the hot contribution entries x[k] gathered
 //     by most edges land in a compact prefix of x that stays L1/L2 resident;
-//   * rows are therefore sorted by length and binned: a row of length in
-//     (G/2, G] is summed by a group of G lanes (G = 1..32, 32/G rows per warp),
-//     rows longer than kPrLong are cut into kPrChunk-nonzero chunks whose
-//     partial sums go to fixed slots -- every warp gets a similar amount of
-//     work and no block barrier sits in the hot loop.
-// Per iteration two kernels run inside the graph body:
-//   k_pr_rows   -- every warp unit: coalesced AT column loads (streamed,
-//                  evict-first), gathered x (read-only path), fp64 sums, and
-//                  the fused epilogue r = teleport + sum, |r_prev - r| (fp64),
-//                  x_next = r / (deg / damping) (0 for dangling vertices --
-//                  their mass is lost exactly as in the reference);
-//   k_pr_finish -- sums the chunk slots of the long rows (warp per row, fixed
-//                  lane-strided + shuffle-tree order), their
-//                  epilogue, then the last CTA reduces every L1 partial in a
-//                  fixed order, counts the iteration and clears the WHILE
-//                  condition on convergence.  Deterministic end to end.
+//   * rows are therefore sorted by length and binned: rows of one exact length
+//     <= kPrShort are summed thread-per-row (32 rows per warp unit, columns
+//     unit-interleaved), rows up to kPrLong warp-per-row, longer rows are cut
+//     into kPrChunk-nonzero chunks whose partial sums go to fixed slots --
+//     every warp gets a similar amount of work and no block barrier sits in
+//     the hot loop.
+// Per iteration (k_pr_persist): the row phase -- coalesced AT column loads
+// (streamed, no L1 allocation), gathered x (coherent loads, hot prefix
+// evict_last in L1), fp64 sums and the fused epilogue r = teleport + sum,
+// |r_prev - r| (fp64), x_next = r * (damping / deg) (0 for dangling vertices
+// -- their mass is lost exactly as in the reference) -- a grid barrier, the
+// long-row finish (chunk slots summed in a fixed lane-strided + shuffle-tree
+// order), a grid barrier, and every CTA folds all L1 partials in the same fixed
+// order: the same stop decision everywhere, no host round trip.
 // Algorithmic bytes per iteration: (4 + sizeof x) * nnz + 8 * (n+1)
 // + (3 * sizeof x + 4) * n.
 #include <cooperative_groups.h>
@@ -58,15 +56,8 @@ constexpr int kPrB0Ipl = GBX_PR_B0IPL;  // gathers per lane per step in warp-per
 constexpr int64_t kPrLong = 1024;   // rows longer than this are chunked
 constexpr int64_t kPrShort = 32;    // rows up to this length: thread per row, exact-length bins
 constexpr int64_t kPrChunk = 2048;  // nonzeros per chunk unit
-// default shared-memory hot prefix of x (override: GBX_PR_HOT_KB)
-constexpr int kPrHotKbDefault = 0;
 constexpr unsigned kWarp = 0xffffffffu;
 constexpr int kPrMaxPeers = 8;     // ranks of the fused P2P exchange (one NVSwitch box)
-
-PrPlan::~PrPlan() {
-  if (exec) cudaGraphExecDestroy(exec);
-  if (graph) cudaGraphDestroy(graph);
-}
 
 template <typename V>
 struct PrArgs {
@@ -87,20 +78,18 @@ struct PrArgs {
   V* r1;
   V* x0;
   V* x1;
-  double* l1_rows;     // [gridA] per-CTA partials of k_pr_rows
+  double* l1_rows;     // [2][grid] per-CTA row-phase partials (by iteration parity)
   double* l1_fin;      // [gridB]
   double* l1_hist;
-  int* ctl;            // [0] completed iterations [1] done
+  int* ctl;            // [0] completed iterations [1] done [2] peer timeout (fused exchange)
   unsigned long long* ktime;  // [128][2]: per iteration, min CTA start / max CTA end (%globaltimer)
   unsigned* fin_cnt;
-  int64_t hot;         // x[0, hot) is staged in shared memory by k_pr_rows
-  int64_t l1hot;       // x[hot, l1hot) gathered with L1 evict_last, the rest no_allocate
+  int64_t l1hot;       // x[0, l1hot) gathered with L1 evict_last, the rest no_allocate
   int64_t row0;        // first row of this plan (shards); outputs indexed row - row0
   int grid_rows;
   double damping, teleport, tol;
   int itermax;
   int fixed;           // single step: r0/x0 inputs, r1/x1 outputs, no convergence
-  cudaGraphConditionalHandle cond;
   // fused multi-GPU run (k_pr_persist_p2p): x_next is stored straight into
   // every rank's x buffer over NVLink.  xp[b][q] = rank q's x_b, pre-offset so
   // that xp[b][q][row] is this rank's padded slot entry for relabeled row
@@ -118,11 +107,15 @@ __device__ __forceinline__ void pr_buffers(const PrArgs<V>& a, int k, const V*& 
   r_nxt = odd ? a.r0 : a.r1;
 }
 
-// Cache-policy loads (PTX): the AT column stream is read once -> no L1
-// allocation, evict-first in L2; gathers of the hot prefix of x (the highest-
-// degree vertices after relabeling, ~58% of all gathers on R-MAT in the first
-// 48K ids) are kept in L1 (evict_last); cold gathers bypass L1 so they do not
-// evict the hot lines.
+// Cache-policy loads (PTX).  The AT column stream is read-only for the whole
+// launch: non-coherent path, no L1 allocation.  x is rewritten every
+// iteration inside the same persistent launch (and by peer GPUs in the fused
+// multi-GPU kernel), so its gathers are COHERENT weak loads (no .nc) that keep
+// the eviction hints: the hot prefix (the highest-degree vertices after
+// relabeling) stays in L1 (evict_last) within an iteration, the cold gathers
+// bypass L1; the grid barrier between iterations orders them after the writes
+// (PTX memory model: release/acquire at gpu scope).  volatile: never merged or
+// moved across the barriers by the compiler.
 __device__ __forceinline__ int ld_stream(const int32_t* p) {
   int v;
   asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -130,22 +123,22 @@ __device__ __forceinline__ int ld_stream(const int32_t* p) {
 }
 __device__ __forceinline__ float ld_hot(const float* p) {
   float v;
-  asm("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  asm volatile("ld.global.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ double ld_hot(const double* p) {
   double v;
-  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm volatile("ld.global.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ float ld_cold(const float* p) {
   float v;
-  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  asm volatile("ld.global.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ double ld_cold(const double* p) {
   double v;
-  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 
@@ -157,15 +150,10 @@ __device__ __forceinline__ unsigned long long pr_gtimer() {
   return t;
 }
 
-// gather x[c]: optional shared-memory prefix [0, hot), L1-resident prefix
-// [hot, l1hot), the rest from L2 without L1 allocation
+// gather x[c]: the L1-resident prefix [0, l1hot) (evict_last), the rest from
+// L2 without L1 allocation
 template <typename V>
-__device__ __forceinline__ V pr_x(const V* s_x, int64_t hot, const V* x, int c) {
-  return c < hot ? s_x[c] : ld_hot(x + c);
-}
-template <typename V>
-__device__ __forceinline__ V pr_xg(const V* s_x, int64_t hot, int64_t l1hot, const V* x, int c) {
-  if (c < hot) return s_x[c];
+__device__ __forceinline__ V pr_xg(int64_t l1hot, const V* x, int c) {
   return c < l1hot ? ld_hot(x + c) : ld_cold(x + c);
 }
 
@@ -187,35 +175,21 @@ __device__ __forceinline__ double pr_finish_row(const PrArgs<V>& a, V* r_nxt, V*
   return fabs(static_cast<double>(rprev) - rn);
 }
 
-// BS = 256: several CTAs per SM, hot prefix in L1 only.  BS = 1024: two CTAs
-// per SM, each with a shared-memory copy of the hot prefix of x (random
-// gathers are L1TEX-tag bound -- one 32-byte sector per cycle per SM; from
-// shared memory they are bank-parallel).
-// one iteration's row work for this CTA (every unit of the grid-stride walk);
-// returns the CTA's fp64 L1 partial (valid in thread 0)
-template <typename V, int BS>
-__device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k,
-                                                typename cub::BlockReduce<double, BS>::TempStorage& red,
-                                                PrBin* s_bins, V* s_x) {
-  using BlockReduce = cub::BlockReduce<double, BS>;
-  // the shared-memory prefix exists only in the 1024-thread variant: for 256
-  // threads the bound is a compile-time 0 and the per-gather test folds away
-  const int64_t hot = BS == 1024 ? a.hot : 0;
+// One iteration's row work for CTA `cta` of `ncta` (every unit of the grid-
+// stride walk); returns the CTA's fp64 L1 partial (valid in thread 0).
+template <typename V>
+__device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k, int cta, int ncta,
+                                                typename cub::BlockReduce<double, kPrThreads>::TempStorage& red,
+                                                PrBin* s_bins) {
+  using BlockReduce = cub::BlockReduce<double, kPrThreads>;
   const V *x_cur, *r_cur;
   V *x_nxt, *r_nxt;
   pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
-  {
-    // stage the hot prefix of x (16-byte vector loads; hot is a multiple of 16 B)
-    constexpr int kVec = 16 / sizeof(V);
-    const int4* src = reinterpret_cast<const int4*>(x_cur);
-    int4* dst = reinterpret_cast<int4*>(s_x);
-    for (int64_t i = threadIdx.x; i < a.hot / kVec; i += blockDim.x) dst[i] = __ldg(src + i);
-  }
   for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_bins[i] = a.bins[i];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t gwarp = (cta * int64_t(kPrThreads) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(ncta) * kPrThreads) >> 5;
   double l1 = 0.0;
   // 1) long-row chunks: 32 lanes, kPrIpl independent gathers in flight per lane
   for (int64_t u = gwarp; u < a.nchunks; u += nwarps) {
@@ -230,7 +204,7 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k,
       }
 #pragma unroll
       for (int j = 0; j < kPrIpl; ++j)
-        if (c[j] >= 0) s += static_cast<double>(pr_xg(s_x, hot, a.l1hot, x_cur, c[j]));
+        if (c[j] >= 0) s += static_cast<double>(pr_xg(a.l1hot, x_cur, c[j]));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
@@ -269,7 +243,7 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k,
         }
 #pragma unroll
         for (int q = 0; q < kPrB0Ipl; ++q)
-          if (c[q] >= 0) s += static_cast<double>(pr_xg(s_x, hot, a.l1hot, x_cur, c[q]));
+          if (c[q] >= 0) s += static_cast<double>(pr_xg(a.l1hot, x_cur, c[q]));
 #pragma unroll
         for (int q = 0; q < kPrB0Ipl; ++q) c[q] = nx[q];
       }
@@ -300,7 +274,7 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k,
           for (int q = 0; q < 4; ++q) nx[q] = j + 4 + q < L ? ld_stream(cp + (j + 4 + q) * m) : -1;
           V t[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) t[q] = c[q] >= 0 ? pr_xg(s_x, hot, a.l1hot, x_cur, c[q]) : V(0);
+          for (int q = 0; q < 4; ++q) t[q] = c[q] >= 0 ? pr_xg(a.l1hot, x_cur, c[q]) : V(0);
           s += (static_cast<double>(t[0]) + static_cast<double>(t[1])) +
                (static_cast<double>(t[2]) + static_cast<double>(t[3]));
 #pragma unroll
@@ -314,17 +288,46 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k,
   return BlockReduce(red).Sum(l1);
 }
 
-template <typename V, int BS>
-__global__ void __launch_bounds__(BS, BS == 1024 ? 2 : GBX_PR_MINB) k_pr_rows(PrArgs<V> a) {
-  using BlockReduce = cub::BlockReduce<double, BS>;
+// long rows: the chunk slots of every long row summed by one warp each
+// (lane-strided, fixed shuffle tree) and the row's epilogue; returns the
+// CTA's fp64 L1 partial (valid in thread 0)
+template <typename V>
+__device__ __forceinline__ double pr_long_phase(const PrArgs<V>& a, int k, int cta, int ncta,
+                                                typename cub::BlockReduce<double, kPrThreads>::TempStorage& red) {
+  using BlockReduce = cub::BlockReduce<double, kPrThreads>;
+  const V *x_cur, *r_cur;
+  V *x_nxt, *r_nxt;
+  pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (cta * int64_t(kPrThreads) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(ncta) * kPrThreads) >> 5;
+  double l1 = 0.0;
+  for (int64_t i = gwarp; i < a.nlong; i += nwarps) {
+    const int64_t q0 = a.long_slot[i], q1 = a.long_slot[i + 1];
+    double s = 0.0;
+    for (int64_t q = q0 + lane; q < q1; q += 32) s += __ldcg(a.slot + q);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
+    if (lane == 0) {
+      const int64_t row = a.long_row[i];
+      l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, r_cur[row - a.row0], a.inv[row]);
+    }
+  }
+  __syncthreads();
+  return BlockReduce(red).Sum(l1);
+}
+
+// host-looped row kernel (pr_shard_step, and the per-iteration path kept for
+// ncu captures: option pagerank.host_loop)
+template <typename V>
+__global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_rows(PrArgs<V> a) {
+  using BlockReduce = cub::BlockReduce<double, kPrThreads>;
   __shared__ typename BlockReduce::TempStorage red;
   __shared__ PrBin s_bins[kPrBinsMax];
-  extern __shared__ __align__(16) unsigned char s_raw[];
-  V* s_x = reinterpret_cast<V*>(s_raw);
   if (!a.fixed && *(volatile int*)&a.ctl[1]) return;  // converged (host-looped path)
   const int k = *(volatile int*)&a.ctl[0];
   if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 2], pr_gtimer());
-  const double blk = pr_rows_phase<V, BS>(a, k, red, s_bins, s_x);
+  const double blk = pr_rows_phase<V>(a, k, blockIdx.x, gridDim.x, red, s_bins);
   if (threadIdx.x == 0) {
     a.l1_rows[blockIdx.x] = blk;
     if (a.ktime) atomicMax(&a.ktime[(k % 128) * 2 + 1], pr_gtimer());
@@ -334,59 +337,39 @@ __global__ void __launch_bounds__(BS, BS == 1024 ? 2 : GBX_PR_MINB) k_pr_rows(Pr
 // The whole iteration loop in ONE cooperative launch: per iteration the row
 // phase, a grid barrier, the long-row finish (warp per long row), a grid
 // barrier, then every CTA folds all L1 partials in the same fixed order and
-// reaches the same convergence decision (pagerank.cpp:65-74).  Replaces the
+// reaches the same convergence decision (pagerank.cpp:65-74).  Replaces a
 // graph's two kernel nodes + conditional per iteration (~20 us of launch gaps
 // per iteration against ~200 us of row work) with two grid barriers.
-// BS = kPrThreads: several CTAs per SM, the hot prefix of x in L1 only.  BS =
-// 1024: ONE CTA per SM (64 registers per thread) holding x[0, hot) in shared
-// memory, restaged after every grid barrier -- the hot gathers leave the
-// L1 -> L2 request path (one sector request per cycle per SM, the measured
-// limiter of the L1 variant).
-template <typename V, int BS>
-__global__ void __launch_bounds__(BS, BS == 1024 ? 1 : GBX_PR_MINB) k_pr_persist(PrArgs<V> a) {
+// The row partials are double-buffered by iteration parity: a CTA that has
+// folded iteration k's partials races ahead into iteration k+1's row phase
+// while slower CTAs still fold k -- it writes the other half (the next write
+// of this half, at k+2, comes after barrier #1 of k+1, which every CTA passes
+// only after its fold of k).
+template <typename V>
+__global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist(PrArgs<V> a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  using BlockReduce = cub::BlockReduce<double, BS>;
+  using BlockReduce = cub::BlockReduce<double, kPrThreads>;
   __shared__ typename BlockReduce::TempStorage red;
   __shared__ PrBin s_bins[kPrBinsMax];
   __shared__ int s_stop;
-  extern __shared__ __align__(16) unsigned char s_raw[];
-  V* s_x = reinterpret_cast<V*>(s_raw);  // a.hot entries (0: unused)
-  const int lane = threadIdx.x & 31;
-  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int ncta = gridDim.x;
   for (int k = 0;; ++k) {
+    double* l1_rows = a.l1_rows + (k & 1) * ncta;
     if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 2], pr_gtimer());
-    const double blk = pr_rows_phase<V, BS>(a, k, red, s_bins, s_x);
+    const double blk = pr_rows_phase<V>(a, k, blockIdx.x, ncta, red, s_bins);
     if (threadIdx.x == 0) {
-      a.l1_rows[blockIdx.x] = blk;
+      l1_rows[blockIdx.x] = blk;
       if (a.ktime) atomicMax(&a.ktime[(k % 128) * 2 + 1], pr_gtimer());
     }
     grid.sync();
-    // long rows: the chunk slots summed (lane-strided, fixed shuffle tree)
-    const V *x_cur, *r_cur;
-    V *x_nxt, *r_nxt;
-    pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
-    double l1 = 0.0;
-    for (int64_t i = gwarp; i < a.nlong; i += nwarps) {
-      const int64_t q0 = a.long_slot[i], q1 = a.long_slot[i + 1];
-      double s = 0.0;
-      for (int64_t q = q0 + lane; q < q1; q += 32) s += __ldcg(a.slot + q);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
-      if (lane == 0) {
-        const int64_t row = a.long_row[i];
-        l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, r_cur[row - a.row0], a.inv[row]);
-      }
-    }
-    __syncthreads();
-    const double blk2 = BlockReduce(red).Sum(l1);
+    const double blk2 = pr_long_phase<V>(a, k, blockIdx.x, ncta, red);
     if (threadIdx.x == 0) a.l1_fin[blockIdx.x] = blk2;
     grid.sync();
     // every CTA: all partials in a fixed order -> the same total everywhere
     double part = 0.0;
-    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += BS)
-      part += __ldcg(&a.l1_rows[b]) + __ldcg(&a.l1_fin[b]);
+    for (int b = threadIdx.x; b < ncta; b += kPrThreads)
+      part += __ldcg(&l1_rows[b]) + __ldcg(&a.l1_fin[b]);
     __syncthreads();
     const double tot = BlockReduce(red).Sum(part);
     if (threadIdx.x == 0) {
@@ -404,82 +387,77 @@ __global__ void __launch_bounds__(BS, BS == 1024 ? 1 : GBX_PR_MINB) k_pr_persist
 }
 
 // Sharded PageRank with the exchange fused into the iteration kernel (one
-// cooperative launch per rank for the whole run).  Per iteration: the row
+// cooperative launch per GPU for the whole run).  Per iteration: the row
 // phase and the long-row finish store x_next into EVERY rank's x (peer
-// pointers, e.g. torch symmetric memory over NVLink/NVSwitch); the rank's fp64
-// L1 total goes to slot [k&1][rank] of every rank's table; then a cross-rank
-// barrier -- system-scope fence per CTA, grid barrier, one signal increment
-// per peer, spin on the own signal word, grid barrier -- and every CTA sums
-// the table in rank order: the same decision on every rank (pagerank.cpp:74).
-// x and the slot table are double-buffered by iteration parity, so a rank one
-// iteration ahead never overwrites what a slower rank still reads.
+// pointers over NVLink / NVSwitch); the rank's fp64 L1 total goes to slot
+// [k&1][rank] of every rank's table; then a cross-rank barrier -- system-scope
+// fence per CTA, grid barrier, one signal increment per peer, a BOUNDED spin on
+// the own signal word, grid barrier -- and every CTA sums the table in rank
+// order: the same decision on every rank (pagerank.cpp:74).  x and the slot
+// table are double-buffered by iteration parity, so a rank one iteration ahead
+// never overwrites what a slower rank still reads.
+//
+// The spin gives up after timeout_ns (%globaltimer): a peer that never
+// launched, crashed or was handed other arguments then surfaces as an error
+// word (ctl[2] = 1) on every waiting rank -- the host turns it into
+// GBX_CUDA_ERROR and the driver falls back to the NCCL exchange -- instead of
+// a cooperative grid spinning forever.
+//
+// `nvirt` ranks may share ONE launch on one GPU (blocks [v*per, (v+1)*per)
+// are rank v; each rank's arguments in device memory): the emulation of a
+// multi-GPU run that the tests use -- every rank's CTAs are co-resident
+// (cooperative launch), so the ranks' spins always see each other's signals.
+// On a real multi-GPU run nvirt = 1 and the arguments come by value.
 struct PrP2p {
   double* l1p[kPrMaxPeers];     // rank q's slot table [2][nranks]
   unsigned* sigp[kPrMaxPeers];  // rank q's signal word
   double* l1_own;               // this rank's table
   unsigned* sig_own;            // this rank's signal word
   int rank, nranks;
+  unsigned long long timeout_ns;
 };
 
-__global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist_p2p(PrArgs<float> a,
-                                                                            PrP2p m) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
+__device__ __forceinline__ void pr_p2p_body(const PrArgs<float>& a, const PrP2p& m, int cta,
+                                            int ncta, cooperative_groups::grid_group& grid,
+                                            cub::BlockReduce<double, kPrThreads>::TempStorage& red,
+                                            PrBin* s_bins, int& s_stop) {
   using BlockReduce = cub::BlockReduce<double, kPrThreads>;
-  __shared__ typename BlockReduce::TempStorage red;
-  __shared__ PrBin s_bins[kPrBinsMax];
-  __shared__ int s_stop;
-  const int lane = threadIdx.x & 31;
-  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int k = 0;; ++k) {
     if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 2], pr_gtimer());
-    const double blk = pr_rows_phase<float, kPrThreads>(a, k, red, s_bins, nullptr);
+    const double blk = pr_rows_phase<float>(a, k, cta, ncta, red, s_bins);
     if (threadIdx.x == 0) {
-      a.l1_rows[blockIdx.x] = blk;
+      a.l1_rows[cta] = blk;
       if (a.ktime) atomicMax(&a.ktime[(k % 128) * 2 + 1], pr_gtimer());
     }
     grid.sync();
-    const float *x_cur, *r_cur;
-    float *x_nxt, *r_nxt;
-    pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
-    double l1 = 0.0;
-    for (int64_t i = gwarp; i < a.nlong; i += nwarps) {
-      const int64_t q0 = a.long_slot[i], q1 = a.long_slot[i + 1];
-      double s = 0.0;
-      for (int64_t q = q0 + lane; q < q1; q += 32) s += __ldcg(a.slot + q);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
-      if (lane == 0) {
-        const int64_t row = a.long_row[i];
-        l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, r_cur[row - a.row0], a.inv[row]);
-      }
-    }
-    __syncthreads();
-    const double blk2 = BlockReduce(red).Sum(l1);
-    if (threadIdx.x == 0) a.l1_fin[blockIdx.x] = blk2;
+    const double blk2 = pr_long_phase<float>(a, k, cta, ncta, red);
+    if (threadIdx.x == 0) a.l1_fin[cta] = blk2;
     __threadfence_system();  // this CTA's peer stores before the signal below
     grid.sync();
-    if (blockIdx.x == 0) {
+    if (cta == 0) {
       double part = 0.0;
-      for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += kPrThreads)
+      for (int b = threadIdx.x; b < ncta; b += kPrThreads)
         part += __ldcg(&a.l1_rows[b]) + __ldcg(&a.l1_fin[b]);
       __syncthreads();
       const double mine = BlockReduce(red).Sum(part);
       if (threadIdx.x == 0) {
         const int par = k & 1;
-        for (int q = 0; q < m.nranks; ++q)
-          m.l1p[q][par * m.nranks + m.rank] = mine;
+        for (int q = 0; q < m.nranks; ++q) m.l1p[q][par * m.nranks + m.rank] = mine;
         __threadfence_system();
         for (int q = 0; q < m.nranks; ++q) atomicAdd_system(m.sigp[q], 1u);
         // every rank signals every rank once per iteration
         // (the caller zeroes the signal words and barriers before the run)
         const unsigned want = static_cast<unsigned>(m.nranks) * (k + 1);
+        const unsigned long long t0 = pr_gtimer();
         for (;;) {
           unsigned v;
           asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(m.sig_own) : "memory");
           if (static_cast<int>(v - want) >= 0) break;
-          __nanosleep(64);
+          if (pr_gtimer() - t0 > m.timeout_ns) {
+            atomicExch(&a.ctl[2], 1);  // a peer never arrived: every CTA leaves below
+            break;
+          }
+          __nanosleep(256);
         }
         __threadfence_system();
       }
@@ -490,9 +468,10 @@ __global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist_p2p(PrAr
       double tot = 0.0;
       for (int q = 0; q < m.nranks; ++q)  // rank order: identical on every rank
         tot += *(volatile double*)&m.l1_own[par * m.nranks + q];
-      const bool stop = !(tot >= a.tol) || (k + 1 >= a.itermax);
+      const bool failed = *(volatile int*)&a.ctl[2] != 0;
+      const bool stop = failed || !(tot >= a.tol) || (k + 1 >= a.itermax);
       s_stop = stop;
-      if (blockIdx.x == 0) {
+      if (cta == 0) {
         a.l1_hist[k % 128] = tot;
         a.ctl[0] = k + 1;
         if (stop) a.ctl[1] = 1;
@@ -503,7 +482,38 @@ __global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist_p2p(PrAr
   }
 }
 
-template <typename V, bool kGraph>
+__global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist_p2p(PrArgs<float> a,
+                                                                            PrP2p m) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ cub::BlockReduce<double, kPrThreads>::TempStorage red;
+  __shared__ PrBin s_bins[kPrBinsMax];
+  __shared__ int s_stop;
+  pr_p2p_body(a, m, blockIdx.x, gridDim.x, grid, red, s_bins, s_stop);
+}
+
+// nvirt emulated ranks in one launch (arguments per rank in device memory,
+// staged in shared memory per CTA)
+__global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist_p2p_virt(
+    const PrArgs<float>* va, const PrP2p* vm, int nvirt) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ cub::BlockReduce<double, kPrThreads>::TempStorage red;
+  __shared__ PrBin s_bins[kPrBinsMax];
+  __shared__ int s_stop;
+  __shared__ PrArgs<float> sa;
+  __shared__ PrP2p sm;
+  const int per = gridDim.x / nvirt;
+  const int v = blockIdx.x / per;
+  if (threadIdx.x == 0) {
+    sa = va[v];
+    sm = vm[v];
+  }
+  __syncthreads();
+  pr_p2p_body(sa, sm, blockIdx.x - v * per, per, grid, red, s_bins, s_stop);
+}
+
+template <typename V>
 __global__ void __launch_bounds__(kPrThreads) k_pr_finish(PrArgs<V> a) {
   using BlockReduce = cub::BlockReduce<double, kPrThreads>;
   __shared__ typename BlockReduce::TempStorage red;
@@ -511,25 +521,7 @@ __global__ void __launch_bounds__(kPrThreads) k_pr_finish(PrArgs<V> a) {
   if (!a.fixed && *(volatile int*)&a.ctl[1]) return;
   const int k = *(volatile int*)&a.ctl[0];
   const unsigned epoch = static_cast<unsigned>(k) + 1u;
-  const V *x_cur, *r_cur;
-  V *x_nxt, *r_nxt;
-  pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
-  double l1 = 0.0;
-  // one warp per long row: lane-strided slot sums, fixed shuffle tree
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < a.nlong; i += nw) {
-    const int64_t q0 = a.long_slot[i], q1 = a.long_slot[i + 1];
-    double s = 0.0;
-    for (int64_t q = q0 + lane; q < q1; q += 32) s += a.slot[q];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
-    if (lane == 0) {
-      const int64_t row = a.long_row[i];
-      l1 += pr_finish_row(a, r_nxt, x_nxt, row, s, r_cur[row - a.row0], a.inv[row]);
-    }
-  }
-  double blk = BlockReduce(red).Sum(l1);
+  const double blk = pr_long_phase<V>(a, k, blockIdx.x, gridDim.x, red);
   if (threadIdx.x == 0) {
     a.l1_fin[blockIdx.x] = blk;
     __threadfence();
@@ -550,7 +542,6 @@ __global__ void __launch_bounds__(kPrThreads) k_pr_finish(PrArgs<V> a) {
     a.ctl[0] = k + 1;
     const bool stop = a.fixed || !(tot >= a.tol) || (k + 1 >= a.itermax);
     if (stop) a.ctl[1] = 1;
-    if constexpr (kGraph) cudaGraphSetConditional(a.cond, stop ? 0u : 1u);
   }
 }
 
@@ -588,14 +579,6 @@ __global__ void k_neg_len(const int64_t* rp, int64_t n, int32_t* key) {
 __global__ void k_inverse_perm(const int32_t* new2old, int64_t n, int32_t* old2new) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i < n) old2new[new2old[i]] = static_cast<int32_t>(i);
-}
-__global__ void k_relabel_pairs(const int32_t* rowid, const int32_t* col, const int32_t* old2new,
-                                int64_t nnz, uint32_t* new_col, uint32_t* new_row) {
-  const int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (p < nnz) {
-    new_col[p] = static_cast<uint32_t>(old2new[col[p]]);
-    new_row[p] = static_cast<uint32_t>(old2new[rowid[p]]);
-  }
 }
 __global__ void k_gather_i32(const int32_t* src, const int32_t* idx, int64_t n, int32_t* dst) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -748,32 +731,6 @@ __global__ void k_pr_newlen(const int64_t* atrp, const int32_t* new2old, int64_t
   }
 }
 constexpr int64_t kPrGatherLong = 256;
-// rows longer than kPrGatherLong (a prefix: rows are in descending length): a CTA each
-__global__ void k_pr_gather_long(const int64_t* atrp, const int32_t* atcol, const int32_t* new2old,
-                                 const int32_t* old2new, const int64_t* trp, int64_t n,
-                                 int32_t* tcol) {
-  for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
-    const int64_t d = trp[r], len = trp[r + 1] - d;
-    if (len <= kPrGatherLong) return;
-    const int64_t src = atrp[new2old[r]];
-    for (int64_t p = threadIdx.x; p < len; p += blockDim.x) tcol[d + p] = old2new[atcol[src + p]];
-  }
-}
-// the rest: 8 lanes per row
-__global__ void k_pr_gather_short(const int64_t* atrp, const int32_t* atcol,
-                                  const int32_t* new2old, const int32_t* old2new,
-                                  const int64_t* trp, int64_t n, int32_t* tcol) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t r = gw * 4 + (lane >> 3); r < n; r += nw * 4) {
-    const int64_t d = trp[r], len = trp[r + 1] - d;
-    if (len > kPrGatherLong) continue;
-    const int64_t src = atrp[new2old[r]];
-    for (int64_t p = lane & 7; p < len; p += 8) tcol[d + p] = old2new[atcol[src + p]];
-  }
-}
-
 // rows of A in the new order, as (new column, new row) pairs: the pairs come
 // out ordered by new row, so ONE stable sort by new column yields the
 // relabeled AT with every row's columns ascending in the new ids
@@ -831,23 +788,6 @@ __global__ void k_pr_gather_a_short(const int64_t* arp, const int32_t* acol,
   }
 }
 
-// relabel mode: 0 = two stable radix sorts (rows and columns in new-id order),
-// 1 = row permutation (columns in the original ascending order, mapped),
-// 2 = row permutation + segmented sort of every row (new-id order),
-// 3 (default) = A's rows permuted into the new order + ONE stable radix sort
-// by new column (new-id order; scale 22: 4.4 -> ~2.4 ms, same SpMV time)
-static int relabel_mode() {
-  static const int m = [] {
-    const char* e = std::getenv("GBX_PR_RELABEL");
-    if (!e) return 3;
-    if (!std::strcmp(e, "gather")) return 1;
-    if (!std::strcmp(e, "gather_seg")) return 2;
-    if (!std::strcmp(e, "sort2")) return 0;
-    return 3;
-  }();
-  return m;
-}
-
 // relabeled AT (rows by descending in-degree) + relabeled out-degree
 static void build_relabeled(gbx_graph* g, PrPlan& P) {
   const Csr& AT = g->AT();
@@ -869,14 +809,14 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
     GBX_LAUNCHED();
   }
   // relabeled AT, every row's columns ascending in the new ids (the thread-
-  // per-row bins then read the hub end of x together at each step): two
-  // stable 32-bit radix sorts -- by new column carrying the new row, then by
-  // new row carrying the column -- instead of one sort of 64-bit (row, col)
-  // keys (2*bits digits): 5.1 -> ~1.5 ms at scale 22
+  // per-row bins then read the hub end of x together at each step): A's rows
+  // gathered in the new order as (new column, new row) pairs -- ordered by new
+  // row -- then ONE stable 32-bit radix sort by new column (two sorts took
+  // 4.4 ms at scale 22, this ~2.4 ms)
   const int bits = bits_for(std::max<int64_t>(n, 2));
   P.trp.alloc(n + 1);
   P.tcol.alloc(std::max<int64_t>(nnz, 1));
-  if (nnz && relabel_mode() == 3) {
+  if (nnz) {
     const Csr& A = g->A;
     DevArray<int64_t> prp(n + 1);
     k_pr_newlen<<<ceil_div(n + 1, 256), 256, 0, s>>>(A.rp.p, P.new2old.p, n, prp.p);
@@ -925,51 +865,6 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
                                                bits, s));
     }
     rowptr_from_sorted_rows32(s, n, kc2.p, nnz, P.trp.p);
-  } else if (nnz && relabel_mode() > 0) {
-    k_pr_newlen<<<ceil_div(n + 1, 256), 256, 0, s>>>(AT.rp.p, P.new2old.p, n, P.trp.p);
-    GBX_LAUNCHED();
-    {
-      size_t tb = 0;
-      GBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, P.trp.p, P.trp.p, n + 1, s));
-      Tmp<uint8_t> t(tb, s);
-      GBX_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, P.trp.p, P.trp.p, n + 1, s));
-    }
-    const int grid = device_sms() * 8;
-    k_pr_gather_long<<<device_sms() * 4, 256, 0, s>>>(AT.rp.p, AT.col.p, P.new2old.p, P.old2new.p,
-                                                       P.trp.p, n, P.tcol.p);
-    k_pr_gather_short<<<grid, 256, 0, s>>>(AT.rp.p, AT.col.p, P.new2old.p, P.old2new.p, P.trp.p, n,
-                                           P.tcol.p);
-    GBX_LAUNCHED();
-    if (relabel_mode() == 2) {
-      Tmp<int32_t> out(nnz, s);
-      size_t tb = 0;
-      GBX_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, P.tcol.p, out.p, nnz, n, P.trp.p,
-                                                  P.trp.p + 1, s));
-      Tmp<uint8_t> t(tb, s);
-      GBX_CUDA(cub::DeviceSegmentedSort::SortKeys(t.p, tb, P.tcol.p, out.p, nnz, n, P.trp.p,
-                                                  P.trp.p + 1, s));
-      GBX_CUDA(cudaMemcpyAsync(P.tcol.p, out.p, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    }
-  } else if (nnz) {
-    Tmp<uint32_t> kc(nnz, s), kc2(nnz, s), vr(nnz, s), vr2(nnz, s);
-    {
-      Tmp<int32_t> rowid(nnz, s);
-      expand_rows_into(s, AT, rowid.p);
-      k_relabel_pairs<<<ceil_div(nnz, 256), 256, 0, s>>>(rowid.p, AT.col.p, P.old2new.p, nnz,
-                                                         kc.p, vr.p);
-      GBX_LAUNCHED();
-    }
-    size_t tb = 0;
-    GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kc.p, kc2.p, vr.p, vr2.p, nnz, 0, bits, s));
-    {
-      Tmp<uint8_t> t(tb, s);
-      GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kc.p, kc2.p, vr.p, vr2.p, nnz, 0, bits, s));
-      // by new row (stable): (row, col) order; the columns land in tcol
-      GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, vr2.p, vr.p, kc2.p,
-                                               reinterpret_cast<uint32_t*>(P.tcol.p), nnz, 0, bits,
-                                               s));
-    }
-    rowptr_from_sorted_rows32(s, n, vr.p, nnz, P.trp.p);
   } else {
     GBX_CUDA(cudaMemsetAsync(P.trp.p, 0, (n + 1) * sizeof(int64_t), s));
   }
@@ -988,7 +883,7 @@ static void plan_rows(gbx_graph* g, PrPlan& P, int64_t row0, int64_t row1) {
   P.l1_fin.alloc(std::max<int64_t>(P.grid_fin, static_cast<int64_t>(device_sms()) * 32));
   P.l1_hist.alloc(128);
   P.ktime.alloc(256);
-  P.ctl.alloc(2);
+  P.ctl.alloc(4);
   P.blk_cnt.alloc(1);
 }
 
@@ -996,27 +891,14 @@ void pagerank_prepare(gbx_graph* g) {
   require_at(g, "pagerank_gap");
   require_rowdeg(g, "pagerank_gap");
   if (g->pr) return;
-  static const bool timing = std::getenv("GBX_PLAN_TIMING") != nullptr;
-  auto t0 = std::chrono::steady_clock::now();
-  auto mark = [&](const char* what) {
-    if (!timing) return;
-    GBX_CUDA(cudaStreamSynchronize(g->stream));
-    auto t1 = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "pagerank_prepare %s %.2f ms\n", what,
-                 std::chrono::duration<double, std::milli>(t1 - t0).count());
-    t0 = t1;
-  };
   auto P = std::make_unique<PrPlan>();
   build_relabeled(g, *P);
-  mark("relabel");
   plan_rows(g, *P, 0, P->n);
-  mark("plan_rows");
   for (int b = 0; b < 2; ++b) {
     P->r[b].alloc(std::max<int64_t>(g->A.n, 1));
     P->x[b].alloc(std::max<int64_t>(g->A.n, 1));
   }
   P->out.alloc(std::max<int64_t>(g->A.n, 1));
-  mark("vectors");
   g->pr = std::move(P);
 }
 
@@ -1046,93 +928,33 @@ template <> double* buf_inv<double>(PrPlan& P) {
   return P.invd.p;
 }
 
-static int64_t hot_bytes() {
-  static const int64_t hb = [] {
-    const char* e = std::getenv("GBX_PR_HOT_KB");
-    return static_cast<int64_t>(e ? std::atoi(e) : kPrHotKbDefault) * 1024;
-  }();
-  return hb;
+// bytes of x kept L1-resident (option pagerank.l1_window_kb; measured at the
+// 32 KB carveout: 64 / 96 / 112 / 128 / 144 / 160 / 176 / 192 KB -> 221.6 /
+// 216.1 / 209.9 / 209.0 / 205.9 / 207.0 / 208.4 / 209.7 us/iter)
+static int64_t l1_hot_bytes() { return option(kOptPrL1WindowKb) * 1024; }
+
+// shared-memory carveout of the row kernels: 10% -> 32 KB of shared memory,
+// 224 KB of L1 (214.0 -> 207.1 us/iter, A/B); < 0 leaves the driver's choice
+static void set_carveout(const void* fn) {
+  const int carve = static_cast<int>(option(kOptPrCarveout));
+  if (carve >= 0) (void)cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+  (void)cudaGetLastError();
 }
 
-// bytes of x kept L1-resident (override: GBX_PR_L1_KB)
-static int64_t l1_hot_bytes() {
-  static const int64_t hb = [] {
-    const char* e = std::getenv("GBX_PR_L1_KB");
-    return static_cast<int64_t>(e ? std::atoi(e) : 144) * 1024;  // measured at the 32 KB carveout: 64 / 96 / 112 / 128 / 144 / 160 / 176 / 192 KB -> 221.6 / 216.1 / 209.9 / 209.0 / 205.9 / 207.0 / 208.4 / 209.7 us/iter
-  }();
-  return hb;
-}
-
-#ifndef GBX_PR_PERSIST_CARVEOUT
-#define GBX_PR_PERSIST_CARVEOUT 10  // 32 KB of shared memory, 224 KB of L1: 214.0 -> 207.1 us/iter (A/B)
-#endif
-static int persist_carveout() {
-  static const int c = [] {
-    const char* cv = std::getenv("GBX_PR_CARVEOUT");
-    return cv ? std::atoi(cv) : GBX_PR_PERSIST_CARVEOUT;
-  }();
-  return c;
-}
-
-template <typename V>
-static size_t rows_smem(const PrArgs<V>& a) {
-  static bool attr = false;
-  if (!attr) {
-    const int mx = static_cast<int>(std::min<int64_t>(hot_bytes(), 200 * 1024));
-    GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  std::max(mx, 1)));
-    GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  std::max(mx, 1)));
-    // (measured: the default carveout is best; GBX_PR_CARVEOUT overrides)
-    if (const char* cv = std::getenv("GBX_PR_CARVEOUT")) {
-      const int carve = std::atoi(cv);
-      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float, 1024>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double, 1024>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float, kPrThreads>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double, kPrThreads>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-    }
-    // the 256-thread row kernels (host-looped path) share the persistent
-    // kernel's carveout
-    if (const int carve = persist_carveout(); carve >= 0) {
-      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<float, kPrThreads>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-      GBX_CUDA(cudaFuncSetAttribute(k_pr_rows<double, kPrThreads>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-    }
-    attr = true;
-  }
-  return static_cast<size_t>(a.hot) * sizeof(V);
-}
-
-template <typename V>
-static int rows_block(const PrArgs<V>& a) {
-  return a.hot > 0 ? 1024 : kPrThreads;
-}
-template <typename V>
-static void* rows_fn(const PrArgs<V>& a) {
-  return a.hot > 0 ? reinterpret_cast<void*>(k_pr_rows<V, 1024>)
-                   : reinterpret_cast<void*>(k_pr_rows<V, kPrThreads>);
-}
-
-// persistent grid: SMs x resident CTAs for this shared-memory footprint
-template <typename V>
-static int rows_grid(const PrArgs<V>& a) {
+// resident CTAs per SM x SMs for a row kernel
+static int resident_grid(const void* fn) {
+  set_carveout(fn);
   int per_sm = 0;
-  GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_fn<V>(a), rows_block<V>(a),
-                                                         rows_smem<V>(a)));
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPrThreads, 0) != cudaSuccess) {
+    (void)cudaGetLastError();
+    per_sm = 1;
+  }
   return device_sms() * std::max(per_sm, 1);
 }
 
 template <typename V>
 static void launch_rows(const PrArgs<V>& a, cudaStream_t s) {
-  if (a.hot > 0)
-    k_pr_rows<V, 1024><<<a.grid_rows, 1024, rows_smem<V>(a), s>>>(a);
-  else
-    k_pr_rows<V, kPrThreads><<<a.grid_rows, kPrThreads, 0, s>>>(a);
+  k_pr_rows<V><<<a.grid_rows, kPrThreads, 0, s>>>(a);
 }
 
 template <typename V>
@@ -1164,16 +986,8 @@ static PrArgs<V> make_args(PrPlan& P, double damping, double tol, int itermax) {
   a.ktime = P.ktime.p;
   a.fin_cnt = P.blk_cnt.p;
   a.row0 = 0;
-  a.hot = std::min<int64_t>(P.n, hot_bytes() / static_cast<int64_t>(sizeof(V))) & ~int64_t(3);
-  // with a shared-memory prefix, the L1 evict_last window follows it
-  // (GBX_PR_L1X_KB bytes of x past the prefix)
-  static const int64_t l1x = [] {
-    const char* e = std::getenv("GBX_PR_L1X_KB");
-    return static_cast<int64_t>(e ? std::atoi(e) : 48) * 1024;
-  }();
-  a.l1hot = a.hot > 0 ? std::min<int64_t>(P.n, a.hot + l1x / static_cast<int64_t>(sizeof(V)))
-                      : std::min<int64_t>(P.n, l1_hot_bytes() / static_cast<int64_t>(sizeof(V)));
-  a.grid_rows = rows_grid<V>(a);
+  a.l1hot = std::min<int64_t>(P.n, l1_hot_bytes() / static_cast<int64_t>(sizeof(V)));
+  a.grid_rows = resident_grid(reinterpret_cast<const void*>(k_pr_rows<V>));
   a.damping = damping;
   a.teleport = (1.0 - damping) / static_cast<double>(P.n);
   a.tol = tol;
@@ -1188,111 +1002,19 @@ __global__ void k_pr_ktime_reset(unsigned long long* t) {
 }
 
 static void reset_state(cudaStream_t s, PrPlan& P) {
-  GBX_CUDA(cudaMemsetAsync(P.ctl.p, 0, 2 * sizeof(int), s));
+  GBX_CUDA(cudaMemsetAsync(P.ctl.p, 0, P.ctl.n * sizeof(int), s));
   GBX_CUDA(cudaMemsetAsync(P.blk_cnt.p, 0, sizeof(unsigned), s));
   if (P.ktime.p) k_pr_ktime_reset<<<1, 256, 0, s>>>(P.ktime.p);
 }
 
+// the persistent kernel needs every CTA resident (cooperative launch); its
+// row partials are double-buffered (2 * grid entries)
 template <typename V>
-static bool build_graph(PrPlan& P, double damping, double tol, int itermax) {
-  const int prec = sizeof(V) == 8 ? 64 : 32;
-  if (P.exec && P.g_damping == damping && P.g_tol == tol && P.g_itermax == itermax &&
-      P.g_prec == prec)
-    return true;
-  if (P.graph_failed) return false;
-  if (P.exec) { cudaGraphExecDestroy(P.exec); P.exec = nullptr; }
-  if (P.graph) { cudaGraphDestroy(P.graph); P.graph = nullptr; }
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  cudaGraphConditionalHandle cond;
-  cudaGraphNode_t node;
-  cudaGraph_t body = nullptr;
-  bool ok = cudaGraphCreate(&graph, 0) == cudaSuccess &&
-            cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault) ==
-                cudaSuccess;
-  if (ok) {
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = cond;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    ok = cudaGraphAddNode(&node, graph, nullptr, 0, &cp) == cudaSuccess;
-    if (ok) body = cp.conditional.phGraph_out[0];
-  }
-  PrArgs<V> a = make_args<V>(P, damping, tol, itermax);
-  a.cond = cond;
-  void* params[] = {&a};
-  cudaGraphNode_t kn_rows = nullptr, kn_fin = nullptr;
-  if (ok) {
-    cudaKernelNodeParams kp = {};
-    kp.func = rows_fn<V>(a);
-    kp.gridDim = dim3(a.grid_rows);
-    kp.blockDim = dim3(rows_block<V>(a));
-    kp.sharedMemBytes = static_cast<unsigned>(rows_smem<V>(a));
-    kp.kernelParams = params;
-    ok = cudaGraphAddKernelNode(&kn_rows, body, nullptr, 0, &kp) == cudaSuccess;
-  }
-  if (ok) {
-    cudaKernelNodeParams kp = {};
-    kp.func = reinterpret_cast<void*>(k_pr_finish<V, true>);
-    kp.gridDim = dim3(P.grid_fin);
-    kp.blockDim = dim3(kPrThreads);
-    kp.kernelParams = params;
-    ok = cudaGraphAddKernelNode(&kn_fin, body, &kn_rows, 1, &kp) == cudaSuccess;
-  }
-  if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
-  if (!ok) {
-    (void)cudaGetLastError();
-    if (graph) cudaGraphDestroy(graph);
-    P.graph_failed = true;
-    return false;
-  }
-  P.graph = graph;
-  P.exec = exec;
-  P.g_damping = damping;
-  P.g_tol = tol;
-  P.g_itermax = itermax;
-  P.g_prec = prec;
-  return true;
-}
-
-// the persistent variant needs every CTA resident (cooperative launch): one
-// CTA per SM with the shared-memory hot prefix (a.hot > 0), else as many
-// kPrThreads CTAs as fit
-template <typename V>
-static void* persist_fn(const PrArgs<V>& a) {
-  return a.hot > 0 ? reinterpret_cast<void*>(k_pr_persist<V, 1024>)
-                   : reinterpret_cast<void*>(k_pr_persist<V, kPrThreads>);
-}
-
-template <typename V>
-static bool persist_args(PrPlan& P, double damping, double tol, int itermax, PrArgs<V>& a,
-                         int& block, size_t& smem) {
+static bool persist_args(PrPlan& P, double damping, double tol, int itermax, PrArgs<V>& a) {
   a = make_args<V>(P, damping, tol, itermax);
-  block = a.hot > 0 ? 1024 : kPrThreads;
-  smem = static_cast<size_t>(a.hot) * sizeof(V);
-  if (a.hot > 0) {
-    if (smem > 200 * 1024) return false;
-    if (cudaFuncSetAttribute(persist_fn<V>(a), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem)) != cudaSuccess) {
-      (void)cudaGetLastError();
-      return false;
-    }
-  }
-  // shared-memory carveout of the persistent kernel (percent of the maximum;
-  // GBX_PR_CARVEOUT overrides, < 0 leaves the driver's choice)
-  if (const int carve = persist_carveout(); carve >= 0)
-    (void)cudaFuncSetAttribute(persist_fn<V>(a), cudaFuncAttributePreferredSharedMemoryCarveout,
-                               carve);
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persist_fn<V>(a), block, smem) !=
-          cudaSuccess || per_sm < 1) {
-    (void)cudaGetLastError();
-    return false;
-  }
-  a.grid_rows = device_sms() * per_sm;
+  a.grid_rows = resident_grid(reinterpret_cast<const void*>(k_pr_persist<V>));
   return static_cast<int64_t>(P.l1_fin.n) >= a.grid_rows &&
-         static_cast<int64_t>(P.l1_block.n) >= a.grid_rows;
+         static_cast<int64_t>(P.l1_block.n) >= 2 * static_cast<int64_t>(a.grid_rows);
 }
 
 template <typename V>
@@ -1305,28 +1027,22 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
   k_pr_init<V><<<ceil_div(n, 256), 256, 0, s>>>(buf_r<V>(P, 0), buf_x<V>(P, 0), buf_inv<V>(P),
                                                 P.deg.p, n, damping);
   GBX_LAUNCHED();
-  // GBX_PR_NO_GRAPH=1 forces the host-looped path (ncu cannot profile kernel
-  // nodes of a graph that holds conditional nodes)
-  static const bool no_graph = std::getenv("GBX_PR_NO_GRAPH") != nullptr;
-  static const bool use_graph = std::getenv("GBX_PR_GRAPH") != nullptr;
   PrArgs<V> pa{};
-  int pblock = 0;
-  size_t psmem = 0;
-  if (!no_graph && !use_graph && persist_args<V>(P, damping, tol, itermax, pa, pblock, psmem)) {
+  if (!option(kOptPrHostLoop) && persist_args<V>(P, damping, tol, itermax, pa)) {
     void* args[] = {&pa};
-    GBX_CUDA(cudaLaunchCooperativeKernel(persist_fn<V>(pa), dim3(pa.grid_rows), dim3(pblock), args,
-                                         psmem, s));
+    GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_pr_persist<V>),
+                                         dim3(pa.grid_rows), dim3(kPrThreads), args, 0, s));
     P.last_persist = true;
-  } else if (!no_graph && build_graph<V>(P, damping, tol, itermax)) {
-    GBX_CUDA(cudaGraphLaunch(P.exec, s));
   } else {
+    // one row launch + one finish launch per iteration, checked on the host
+    // every 4 iterations (the finish kernels of a converged run return at once)
     PrArgs<V> a = make_args<V>(P, damping, tol, itermax);
     int done = 0, launched = 0;
     while (!done && launched < itermax) {
       const int chunk = std::min(4, itermax - launched);
       for (int c = 0; c < chunk; ++c) {
         launch_rows<V>(a, s);
-        k_pr_finish<V, false><<<P.grid_fin, kPrThreads, 0, s>>>(a);
+        k_pr_finish<V><<<P.grid_fin, kPrThreads, 0, s>>>(a);
         GBX_LAUNCHED();
       }
       launched += chunk;
@@ -1341,8 +1057,8 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
   GBX_CUDA(cudaStreamSynchronize(s));
   P.last_iters = it;
   {
-    // mean k_pr_rows launch duration over this run's iterations (first CTA
-    // start to last CTA end, %globaltimer)
+    // mean row-phase duration over this run's iterations (first CTA start to
+    // last CTA end, %globaltimer)
     double sum = 0.0;
     int cnt = 0;
     for (int k = 0; k < std::min(it, 128); ++k)
@@ -1373,7 +1089,9 @@ void pagerank_run(gbx_graph* g, double damping, double tol, int itermax, double*
   g->stats = gbx_stats{};
   g->pending_iters = nullptr;
   if (n == 0 || itermax <= 0) {
-    if (iters) *iters = itermax <= 0 ? std::max(itermax, 0) : 0;
+    // pagerank.cpp:52-75: iterations = min(k, itermax) with k = 1 when the loop
+    // never runs, so a non-positive itermax comes back unchanged; n = 0 -> 0
+    if (iters) *iters = n == 0 ? 0 : itermax;
     if (n > 0 && rank) {
       for (int64_t i = 0; i < n; ++i) rank[i] = 1.0 / static_cast<double>(n);
     }
@@ -1519,44 +1237,37 @@ void pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, float
   a.r0 = const_cast<float*>(r_prev);  // local rows; may alias r_new
   a.r1 = r_new;
   a.row0 = P.row0;
-  a.hot = 0;
-  a.grid_rows = rows_grid<float>(a);
+  a.grid_rows = resident_grid(reinterpret_cast<const void*>(k_pr_rows<float>));
   GBX_CUDA(cudaMemsetAsync(P.ctl.p, 0, 2 * sizeof(int), s));
   GBX_CUDA(cudaMemsetAsync(P.blk_cnt.p, 0, sizeof(unsigned), s));
   launch_rows<float>(a, s);
-  k_pr_finish<float, false><<<P.grid_fin, kPrThreads, 0, s>>>(a);
+  k_pr_finish<float><<<P.grid_fin, kPrThreads, 0, s>>>(a);
   GBX_LAUNCHED();
   GBX_CUDA(cudaMemcpyAsync(l1, P.l1_hist.p, sizeof(double), cudaMemcpyDeviceToDevice, s));
   g->prs->steps++;
 }
 
-void pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1_peers,
-                      const uint64_t* l1_peers, const uint64_t* sig_peers, float* r0, float* r1,
-                      double damping, double tol, int itermax, int* iters) {
+// per-rank arguments of the fused run: peers[q] = rank q's buffers
+static void p2p_rank_args(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1_peers,
+                          const uint64_t* l1_peers, const uint64_t* sig_peers, float* r0,
+                          float* r1, double damping, double tol, int itermax, PrArgs<float>& a,
+                          PrP2p& m) {
   if (!g->prs) fail(GBX_MISSING_PROPERTY, "pr_shard_run_p2p needs gbx_pr_shard_prepare");
   PrShard& S = *g->prs;
   PrPlan& P = S.plan;
   if (S.nranks > kPrMaxPeers) fail(GBX_INVALID_VALUE, "pr_shard_run_p2p: more than 8 ranks");
   if (!x0_peers || !x1_peers || !l1_peers || !sig_peers || !r0 || !r1)
     fail(GBX_NULL_ARGUMENT, "pr_shard_run_p2p: NULL buffer");
-  cudaStream_t s = g->stream;
   if (P.g_damping != damping) {
-    k_pr_inv<<<ceil_div(std::max<int64_t>(P.n, 1), 256), 256, 0, s>>>(P.invf.p, P.deg.p, P.n,
-                                                                      damping);
+    k_pr_inv<<<ceil_div(std::max<int64_t>(P.n, 1), 256), 256, 0, g->stream>>>(P.invf.p, P.deg.p,
+                                                                              P.n, damping);
     GBX_LAUNCHED();
     P.g_damping = damping;
   }
-  if (itermax <= 0 || P.n == 0) {  // as pagerank_run: nothing to iterate
-    if (iters) *iters = itermax <= 0 ? std::max(itermax, 0) : 0;
-    return;
-  }
-  PrArgs<float> a = make_args<float>(P, damping, tol, itermax);
+  a = make_args<float>(P, damping, tol, itermax);
   a.inv = P.invf.p;
   a.fixed = 0;
   a.row0 = P.row0;
-  a.hot = 0;
-  a.x0 = reinterpret_cast<float*>(x0_peers[S.rank]);
-  a.x1 = reinterpret_cast<float*>(x1_peers[S.rank]);
   a.r0 = r0;
   a.r1 = r1;
   a.npeer = S.nranks;
@@ -1568,7 +1279,7 @@ void pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1
   // the gathers read the local padded copy; x_nxt only selects the parity
   a.x0 = reinterpret_cast<float*>(x0_peers[S.rank]);
   a.x1 = reinterpret_cast<float*>(x1_peers[S.rank]);
-  PrP2p m{};
+  m = PrP2p{};
   for (int q = 0; q < S.nranks; ++q) {
     m.l1p[q] = reinterpret_cast<double*>(l1_peers[q]);
     m.sigp[q] = reinterpret_cast<unsigned*>(sig_peers[q]);
@@ -1577,23 +1288,97 @@ void pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1
   m.sig_own = m.sigp[S.rank];
   m.rank = S.rank;
   m.nranks = S.nranks;
-  int per_sm = 0;
-  if (const int carve = persist_carveout(); carve >= 0)  // same L1 split as k_pr_persist
-    (void)cudaFuncSetAttribute(k_pr_persist_p2p, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-  GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_persist_p2p, kPrThreads, 0));
-  a.grid_rows = device_sms() * std::max(per_sm, 1);
+  m.timeout_ns = static_cast<unsigned long long>(option(kOptP2pTimeoutMs)) * 1000000ull;
+}
+
+// after the run: iterations, or GBX_CUDA_ERROR when a peer never arrived
+static int p2p_finish(gbx_graph* g) {
+  PrPlan& P = g->prs->plan;
+  int ctl[3] = {0, 0, 0};
+  GBX_CUDA(cudaMemcpyAsync(ctl, P.ctl.p, sizeof ctl, cudaMemcpyDeviceToHost, g->stream));
+  GBX_CUDA(cudaStreamSynchronize(g->stream));
+  P.last_iters = ctl[0];
+  if (ctl[2])
+    fail(GBX_CUDA_ERROR, "pr_shard_run_p2p: a peer rank did not reach iteration " +
+                             std::to_string(ctl[0]) + " within p2p.timeout_ms");
+  return ctl[0];
+}
+
+void pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1_peers,
+                      const uint64_t* l1_peers, const uint64_t* sig_peers, float* r0, float* r1,
+                      double damping, double tol, int itermax, int* iters) {
+  PrArgs<float> a{};
+  PrP2p m{};
+  p2p_rank_args(g, x0_peers, x1_peers, l1_peers, sig_peers, r0, r1, damping, tol, itermax, a, m);
+  PrPlan& P = g->prs->plan;
+  if (itermax <= 0 || P.n == 0) {  // as pagerank_run: nothing to iterate
+    if (iters) *iters = P.n == 0 ? 0 : itermax;
+    return;
+  }
+  a.grid_rows = resident_grid(reinterpret_cast<const void*>(k_pr_persist_p2p));
   if (static_cast<int64_t>(P.l1_fin.n) < a.grid_rows || static_cast<int64_t>(P.l1_block.n) < a.grid_rows)
     fail(GBX_CUDA_ERROR, "pr_shard_run_p2p: partial buffers too small");
-  reset_state(s, P);
+  reset_state(g->stream, P);
   void* args[] = {&a, &m};
   GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_pr_persist_p2p),
-                                       dim3(a.grid_rows), dim3(kPrThreads), args, 0, s));
+                                       dim3(a.grid_rows), dim3(kPrThreads), args, 0, g->stream));
   GBX_LAUNCHED();
-  int it = 0;
-  GBX_CUDA(cudaMemcpyAsync(&it, P.ctl.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-  GBX_CUDA(cudaStreamSynchronize(s));
-  P.last_iters = it;
+  const int it = p2p_finish(g);
   if (iters) *iters = it;
+}
+
+// nv ranks emulated in ONE cooperative launch on one GPU (every shard's graph
+// handle lives on this device): the multi-rank protocol -- peer stores, slot
+// tables, signal counts, the cross-rank stop agreement -- with ranks that can
+// never wait on a rank that is not running.  peers arrays are [nv] as above;
+// r0s / r1s per rank.
+void pr_shard_run_p2p_multi(gbx_graph* const* gs, int nv, const uint64_t* x0_peers,
+                            const uint64_t* x1_peers, const uint64_t* l1_peers,
+                            const uint64_t* sig_peers, float* const* r0s, float* const* r1s,
+                            double damping, double tol, int itermax, int* iters) {
+  if (nv < 1 || nv > kPrMaxPeers) fail(GBX_INVALID_VALUE, "pr_shard_run_p2p_multi: 1..8 ranks");
+  std::vector<PrArgs<float>> va(nv);
+  std::vector<PrP2p> vm(nv);
+  for (int v = 0; v < nv; ++v) {
+    if (!gs[v] || !gs[v]->prs || gs[v]->prs->rank != v || gs[v]->prs->nranks != nv)
+      fail(GBX_INVALID_VALUE, "pr_shard_run_p2p_multi: shard v must be rank v of nv");
+    p2p_rank_args(gs[v], x0_peers, x1_peers, l1_peers, sig_peers, r0s[v], r1s[v], damping, tol,
+                  itermax, va[v], vm[v]);
+    GBX_CUDA(cudaStreamSynchronize(gs[v]->stream));
+  }
+  const int64_t n = gs[0]->prs->plan.n;
+  if (itermax <= 0 || n == 0) {
+    if (iters) *iters = n == 0 ? 0 : itermax;
+    return;
+  }
+  const int per = resident_grid(reinterpret_cast<const void*>(k_pr_persist_p2p_virt)) / nv;
+  if (per < 1) fail(GBX_CUDA_ERROR, "pr_shard_run_p2p_multi: too many ranks for one launch");
+  for (int v = 0; v < nv; ++v) {
+    PrPlan& P = gs[v]->prs->plan;
+    va[v].grid_rows = per;
+    if (static_cast<int64_t>(P.l1_fin.n) < per || static_cast<int64_t>(P.l1_block.n) < per)
+      fail(GBX_CUDA_ERROR, "pr_shard_run_p2p_multi: partial buffers too small");
+    reset_state(gs[0]->stream, P);
+  }
+  cudaStream_t s = gs[0]->stream;
+  Tmp<PrArgs<float>> da(nv, s);
+  Tmp<PrP2p> dm(nv, s);
+  GBX_CUDA(cudaMemcpyAsync(da.p, va.data(), nv * sizeof(PrArgs<float>), cudaMemcpyHostToDevice, s));
+  GBX_CUDA(cudaMemcpyAsync(dm.p, vm.data(), nv * sizeof(PrP2p), cudaMemcpyHostToDevice, s));
+  const PrArgs<float>* pa = da.p;
+  const PrP2p* pm = dm.p;
+  void* args[] = {&pa, &pm, &nv};
+  GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_pr_persist_p2p_virt),
+                                       dim3(per * nv), dim3(kPrThreads), args, 0, s));
+  GBX_LAUNCHED();
+  GBX_CUDA(cudaStreamSynchronize(s));
+  int it0 = -1;
+  for (int v = 0; v < nv; ++v) {
+    const int it = p2p_finish(gs[v]);
+    if (it0 >= 0 && it != it0) fail(GBX_CUDA_ERROR, "pr_shard_run_p2p_multi: ranks disagree on the iteration count");
+    it0 = it;
+  }
+  if (iters) *iters = it0;
 }
 
 __global__ void k_pr_unpermute_f(const float* r, const int32_t* new2old, int64_t n, double* out,

@@ -41,21 +41,14 @@ struct PrPlan {
   DevArray<float> invf;            // damping / out-degree (fp32 storage)
   DevArray<double> invd;           // damping / out-degree (fp64 storage)
   DevArray<double> l1_block, l1_fin, l1_hist;
-  DevArray<int> ctl;            // [0] completed iterations, [1] done
+  DevArray<int> ctl;            // [0] completed iterations, [1] done, [2] peer timeout
   DevArray<unsigned long long> ktime;  // k_pr_rows launch spans (%globaltimer)
   double last_rows_ms = 0.0;
   bool last_persist = false;       // the last run used k_pr_persist
   DevArray<unsigned> blk_cnt;
-  // CUDA graph with a conditional WHILE node (one iteration kernel per trip)
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  double g_damping = -1, g_tol = -1;
-  int g_itermax = -1;
-  int g_prec = 0;
+  double g_damping = -1;           // damping the shard's inv vector was built for
   int last_prec = 32;
-  bool graph_failed = false;
   int last_iters = 0;
-  ~PrPlan();
 };
 
 // Sharded PageRank step (multi-GPU driver): a PrPlan over a row block.

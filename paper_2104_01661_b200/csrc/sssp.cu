@@ -906,8 +906,7 @@ static void ensure_split(gbx_graph* g, SsspPlan& P, double delta) {
   } else if (n > 0) {
     GBX_CUDA(cudaMemsetAsync(P.nlight.p, 0, n * 4, s));
   }
-  static const bool no_vm = std::getenv("GBX_SSSP_NOVM") != nullptr;
-  if (n > 0 && A.nnz < (int64_t(1) << 32) && !no_vm) {
+  if (n > 0 && A.nnz < (int64_t(1) << 32)) {
     if (!P.vmeta.p) P.vmeta.alloc(n);
     k_vmeta<<<ceil_div(n, 256), 256, 0, s>>>(A.rp.p, P.nlight.p, n, P.vmeta.p);
     GBX_LAUNCHED();
@@ -1008,10 +1007,9 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     int max_persist = 0;
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, g->device);
     const size_t bytes = static_cast<size_t>(n) * sizeof(D);
-    static const bool no_persist = std::getenv("GBX_SSSP_NOPERSIST") != nullptr;
-    if (std::getenv("GBX_SSSP_TLOG"))
+    if (option(kOptSsspTrace))
       std::fprintf(stderr, "sssp: max persisting L2 %d bytes, dist %zu bytes\n", max_persist, bytes);
-    if (max_persist > 0 && !no_persist) {
+    if (max_persist > 0) {
       // the set-aside is a device-wide setting (and costly to change): grow only
       static size_t set_aside[64] = {0};
       const size_t want = std::min<size_t>(bytes, max_persist);
@@ -1033,7 +1031,7 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
   int nb = 1;
   const double span = 2.0 + P.max_w / delta;
   while (nb < span && nb <= 64) nb <<= 1;
-  if (nb <= 64 && !std::getenv("GBX_SSSP_NEARFAR")) {
+  if (nb <= 64) {
     const int64_t cap = n + 1;
     if (static_cast<int>(P.bcnt.n) < nb || P.nb_alloc < nb) {
       P.bq.alloc(static_cast<size_t>(nb) * cap);
@@ -1073,16 +1071,15 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     b.ctl = a.ctl;
     b.relax = a.relax;
     if (split) {
-      static const int lg = std::getenv("GBX_SSSP_LG") ? std::atoi(std::getenv("GBX_SSSP_LG")) : 2;
-      b.light_group = lg;
+      b.light_group = 2;  // 2 lanes per vertex in the light phase (1 / 4: 128 / 124 vs 121 ms)
       b.nl = P.nlight.p;
       b.vm = P.vmeta.p;
       b.sq = P.sq.p;
       b.sbits = P.sbits.p;
       GBX_CUDA(cudaMemsetAsync(P.sbits.p, 0, P.sbits.bytes(), s));
     }
-    b.trace = std::getenv("GBX_SSSP_TRACE") ? 1 : 0;
-    static const bool tlog_on = std::getenv("GBX_SSSP_TLOG") != nullptr;
+    b.trace = option(kOptSsspTrace) ? 1 : 0;
+    const bool tlog_on = option(kOptSsspTrace) != 0;
     DevArray<unsigned long long> tlog;
     if (tlog_on) {
       tlog.alloc(2 * 4096);
@@ -1138,12 +1135,10 @@ void sssp_run(gbx_graph* g, uint64_t source, double delta, double* out) {
   if (P.nonpositive) fail(GBX_NON_POSITIVE_WEIGHT, "edge weights must be positive");
   const int32_t src = static_cast<int32_t>(source);
   // the circular-bucket kernel (nb <= 64) runs proper Delta-stepping on a
-  // light-first row partition; GBX_SSSP_NOSPLIT=1 keeps the label-correcting
-  // all-edges sweep (A/B)
+  // light-first row partition
   int nb = 1;
   while (nb < 2.0 + P.max_w / delta && nb <= 64) nb <<= 1;
-  static const bool nosplit = std::getenv("GBX_SSSP_NOSPLIT") != nullptr;
-  const bool split = nb <= 64 && !std::getenv("GBX_SSSP_NEARFAR") && !nosplit;
+  const bool split = nb <= 64;
   if (split) ensure_split(g, P, delta);
   const bool cw = split && !P.packed;  // partitioned copies of col + weights
   if (P.integral) {

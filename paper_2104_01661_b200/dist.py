@@ -104,19 +104,40 @@ def sharded_pagerank_p2p(backend, dist, damping=0.85, tol=1e-4, itermax=100, to_
     """GAP PageRank over `world` ranks with the exchange FUSED into the iteration
     kernel (gbx_pr_shard_run_p2p): one cooperative launch per rank runs every
     iteration; each row epilogue stores its contribution straight into every
-    rank's x over NVLink (torch symmetric-memory peer pointers), the L1
-    partials go to every rank's slot table, and a device-side signal barrier
-    separates iterations -- no host round trip and no NCCL call per iteration.
-    One NCCL all-gather of the local ranks at the end.  Same results and
-    iteration count as sharded_pagerank."""
+    rank's x over NVLink (symmetric-memory peer pointers), the L1 partials go
+    to every rank's slot table, and a device-side signal barrier separates
+    iterations -- no host round trip and no NCCL call per iteration.  One NCCL
+    all-gather of the local ranks at the end.  Same results and iteration
+    count as sharded_pagerank.
+
+    The kernel's wait for its peers is bounded (option p2p.timeout_ms): when
+    any rank fails -- its launch raised, or a peer never arrived -- every rank
+    learns it through one all-reduce and the run is redone with the NCCL
+    exchange (sharded_pagerank), so a broken peer path degrades instead of
+    hanging the job."""
     import torch
     rank, world = dist.get_rank(), dist.get_world_size()
     rb, re, n = backend.prepare(rank, world)
     chunk = backend.chunk
-    backend.p2p_setup(dist)
-    backend.p2p_init(damping)          # x0 (every slot), r0; signal words zeroed
-    dist.barrier()                     # every rank zeroed before any rank signals
-    iters = backend.p2p_run(damping, tol, itermax)
+    ok = 1
+    iters = 0
+    try:
+        backend.p2p_setup(dist)
+        backend.p2p_init(damping)      # x0 (every slot), r0; signal words zeroed
+    except Exception:
+        ok = 0
+    flag = torch.tensor([ok], dtype=torch.int32, device=backend.device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)   # every rank zeroed before any rank signals
+    if int(flag.item()) == 1:
+        try:
+            iters = backend.p2p_run(damping, tol, itermax)
+        except Exception:
+            ok = 0
+        flag.fill_(ok)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) == 0:
+        backend.p2p_failed = True
+        return sharded_pagerank(backend, dist, damping, tol, itermax, to_host)
     r_local = backend.p2p_result(iters)
     r_full = torch.empty(world * chunk, dtype=r_local.dtype, device=backend.device)
     dist.all_gather_into_tensor(r_full, r_local)

@@ -46,6 +46,16 @@ def _worker(rank, world, port, q, what):
             from paper_2104_01661_b200.dist import sharded_pagerank_p2p
             ranks, iters = sharded_pagerank_p2p(be, dist, 0.85, 1e-4, 100)
             q.put((rank, "prp2p", iters, ranks.tolist()))
+        elif what == "prp2pfail":
+            # rank 1's fused kernel gives up (a peer timeout): every rank must
+            # redo the run over the NCCL-style exchange and agree
+            from paper_2104_01661_b200.dist import sharded_pagerank_p2p
+            if rank == 1:
+                def boom(*a, **k):
+                    raise RuntimeError("pr_shard_run_p2p: a peer rank did not arrive")
+                be.p2p_run = boom
+            ranks, iters = sharded_pagerank_p2p(be, dist, 0.85, 1e-4, 100)
+            q.put((rank, "prp2pfail", iters, ranks.tolist(), bool(getattr(be, "p2p_failed", False))))
         elif what == "bc":
             c = sharded_betweenness(be, dist, BC_SOURCES)
             q.put((rank, "bc", None, c.tolist()))
@@ -99,6 +109,21 @@ def test_sharded_pagerank_p2p_orchestration_gloo():
     for _, _, it, ranks in out:
         assert it == iters
         assert np.array_equal(np.array(ranks), want)
+
+
+def test_sharded_pagerank_p2p_failure_falls_back_gloo():
+    """One rank's fused run fails: both ranks fall back to the exchange driver
+    (no hang, no mixed results) and still match the oracle."""
+    out = _run("prp2pfail")
+    rp, col = O.rmat_graph(9, 8, seed=3, undirected=False)
+    n = len(rp) - 1
+    trp, tcol, _ = O.transpose(n, rp, col)
+    want, iters = O.pagerank(n, trp, tcol, np.diff(rp))
+    assert len(out) == 2
+    for _, _, it, ranks, failed in out:
+        assert failed
+        assert it == iters
+        assert np.abs(np.array(ranks) - want).sum() / np.abs(want).sum() <= 1e-9
 
 
 def test_sharded_triangle_count_gloo_matches_oracle():

@@ -86,7 +86,7 @@ def test_bfs_batch_64_sources_config1():
     n = len(rp) - 1
     srcs = P.pick_sources(g.row_degree(), 64, 1)
     parent, level = algo.bfs_batch(g, srcs)
-    for b in range(0, 64, 7):
+    for b in range(64):  # every source of the config (the bench times all 64)
         wp, wl = O.bfs(n, rp, col, srcs[b])
         assert np.array_equal(parent[b], wp) and np.array_equal(level[b], wl)
 
@@ -508,3 +508,16 @@ def test_tc_partition_rows_sum():
     assert b[0] == 0 and np.all(np.diff(b) >= 0)
     parts = [be.tc_rows(int(b[p]), int(b[p + 1])) for p in range(4)]
     assert sum(parts) == algo.basic.triangle_count(g)
+
+
+def test_pagerank_nonpositive_itermax_passes_through():
+    """pagerank.cpp:52-75: iterations = min(k, itermax) with k = 1 when the loop
+    never runs -- a non-positive itermax comes back unchanged, ranks stay 1/n."""
+    g = P.generate_rmat(8, 8, seed=1)
+    P.property_at(g)
+    P.property_rowdegree(g)
+    n = g.n()
+    for itermax in (0, -1, -5):
+        r = algo.pagerank_gap(g, 0.85, 1e-4, itermax)
+        assert r.iterations == itermax
+        assert np.all(r.rank == 1.0 / n)

@@ -63,3 +63,32 @@ def test_sm100a_cubin_present():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", P.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_options_registry():
+    """gbx_set_option / gbx_get_option: documented names, range checks, reset to
+    the measured default (no GPU needed)."""
+    import paper_2104_01661_b200 as P
+    from paper_2104_01661_b200._lib import lib
+    from paper_2104_01661_b200.graph import call
+    names = []
+    i = 0
+    while lib().gbx_option_name(i) is not None:
+        names.append(lib().gbx_option_name(i).decode())
+        i += 1
+    assert "pagerank.l1_window_kb" in names and "p2p.timeout_ms" in names
+    v = C.c_int64()
+    call("gbx_get_option", b"pagerank.l1_window_kb", C.byref(v))
+    assert v.value == 144
+    call("gbx_set_option", b"pagerank.l1_window_kb", C.c_int64(96))
+    call("gbx_get_option", b"pagerank.l1_window_kb", C.byref(v))
+    assert v.value == 96
+    call("gbx_reset_option", b"pagerank.l1_window_kb")
+    call("gbx_get_option", b"pagerank.l1_window_kb", C.byref(v))
+    assert v.value == 144
+    with pytest.raises(P.Error) as e:
+        call("gbx_set_option", b"no.such.option", C.c_int64(1))
+    assert e.value.code == P.ErrCode.InvalidValue
+    with pytest.raises(P.Error) as e:
+        call("gbx_set_option", b"p2p.timeout_ms", C.c_int64(0))
+    assert e.value.code == P.ErrCode.InvalidValue
