@@ -234,91 +234,60 @@ def run_reference(args):
 
 # ---------------------------------------------------------------- our arm: PageRank
 def bench_pagerank_sharded(args, dist, ws, rank, local):
-    """N > 1: one process per GPU, row blocks of the relabeled AT, one NCCL
-    all_gather_into_tensor of the padded contribution slices + one fp64 L1
-    all-reduce per iteration (paper_2104_01661_b200/dist.py).  Total work
-    fixed -> strong scaling."""
-    import ctypes as C
-
+    """N > 1: one process per GPU; the library's own NCCL communicator
+    (gbx_comm_init), a distributed graph every rank builds LOCALLY (its slice of
+    the R-MAT edge stream, shuffled to the row owners: no full replica), and
+    gbx_pagerank_mg -- row blocks of the relabeled AT with the exchange fused
+    into the iteration kernel (peer stores over NVLink, bounded device
+    barrier; NCCL all-gather fallback).  Total work fixed -> strong scaling."""
     import torch
     import paper_2104_01661_b200 as P
-    from paper_2104_01661_b200.dist import (GpuShardBackend, sharded_pagerank,
-                                            sharded_pagerank_p2p)
-    from paper_2104_01661_b200.graph import Graph, call
-
-    # the exchange: "p2p" (default) fuses it into one cooperative kernel per
-    # rank (peer stores over NVLink via symmetric memory, device-side barrier);
-    # "nccl" = one all_gather_into_tensor per iteration from the host loop
-    exchange = os.environ.get("GBX_PR_EXCHANGE", "p2p")
-    if exchange == "p2p":
-        ok = 1
-        try:  # symmetric memory + peer access on this box?
-            g0 = P.generate_rmat(10, 16, seed=1)
-            P.property_at(g0)
-            P.property_rowdegree(g0)
-            GpuShardBackend(g0).prepare(rank, ws)
-            be0 = GpuShardBackend(g0)
-            be0.prepare(rank, ws)
-            be0.p2p_setup(dist)
-        except Exception as e:
-            print(f"bench: p2p exchange unavailable ({e}); using nccl", file=sys.stderr)
-            ok = 0
-        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)  # every rank takes the same path
-        if int(flag.item()) == 0:
-            exchange = "nccl"
-    run_sharded = sharded_pagerank_p2p if exchange == "p2p" else sharded_pagerank
+    from paper_2104_01661_b200.mg import MG_AUTO, Comm, DGraph
 
     scale = args.scale or 22
     P.init(local)
     torch.cuda.set_device(local)
-    g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.DirectedAdjacency)
-    P.property_at(g)
-    P.property_rowdegree(g)
-    n, nnz, _, _ = g.info()
+    comm = Comm.from_torch(dist, local)
+    g = DGraph.rmat(comm, scale, 16, seed=1, kind=P.Kind.DirectedAdjacency)
+    n, nnz = g.n, g.nnz
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     for _ in range(max(args.warmup, 3)):
-        be = GpuShardBackend(g)
-        _, iters = run_sharded(be, dist, 0.85, 1e-4, 100)
+        _, iters = g.pagerank(0.85, 1e-4, 100, MG_AUTO, to_host=False)
     times = []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            be = GpuShardBackend(g)
-            be.prepare(rank, ws)  # plan (and symmetric buffers) outside the timed region
-            if exchange == "p2p":
-                be.p2p_setup(dist)
             flush.zero_()
             barrier(dist)
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            _, iters = run_sharded(_Prepared(be), dist, 0.85, 1e-4, 100, to_host=False)
+            _, iters = g.pagerank(0.85, 1e-4, 100, MG_AUTO, to_host=False)  # host-synchronous
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
+    st = g.last_stats()
     t = max_over_ranks(dist, sum(times) / len(times))
     value = nnz * iters / t
-    # e2e: every rank builds its copy of the graph from pinned host CSR through
-    # the C ABI (H2D + validation), fills AT / degrees (basic mode), plans its
-    # row block and runs the sharded iterations; the ranks come back to the host
-    # (D2H, original order) -- device time max over ranks, wall clock per rank
-    rp, col, _ = g.export()
-    rp_h = torch.from_numpy(rp).pin_memory()
-    col_h = torch.from_numpy(col).pin_memory()
+    # e2e: every rank hands the library ITS row slice of the host CSR (pinned);
+    # the library shuffles it to its layout, plans, runs and returns the full
+    # rank vector to the host -- device time max over ranks
+    ref = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.DirectedAdjacency)
+    rp, col, _ = ref.export()
+    ref.free()
+    rb, re = n * rank // ws, n * (rank + 1) // ws
+    rp_h = torch.from_numpy(rp[rb:re + 1] - rp[rb]).pin_memory()
+    col_h = torch.from_numpy(col[rp[rb]:rp[re]]).pin_memory()
     e2e_times = []
     for s_ in range(3):
         barrier(dist)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        h = C.c_void_p()
-        call("gbx_graph_new32", C.byref(h), n, rp_h.data_ptr(), col_h.data_ptr(), None, 0, 0)
-        gh = Graph(h)
-        P.property_at(gh)
-        P.property_rowdegree(gh)
-        _, it2 = run_sharded(GpuShardBackend(gh), dist, 0.85, 1e-4, 100)
+        ge = DGraph.from_blocks(comm, n, [(rb, re, rp_h.numpy(), col_h.numpy())],
+                                kind=P.Kind.DirectedAdjacency)
+        _, it2 = ge.pagerank(0.85, 1e-4, 100, MG_AUTO, to_host=True)
+        ge.free()
         dt = time.perf_counter() - t0
-        gh.free()
         if s_ > 0:
             e2e_times.append(dt)
     t_e2e = max_over_ranks(dist, statistics.median(e2e_times))
@@ -326,40 +295,26 @@ def bench_pagerank_sharded(args, dist, ws, rank, local):
            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t * 1e3,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
            "dtype": "f32 (ranks; fp64 row sums and L1)",
-           "data": "synthetic (seeded R-MAT, generated in HBM)",
+           "data": "synthetic (seeded R-MAT, each rank generates its edge slice in HBM)",
            "config": {"workload": f"pagerank_rmat{scale}_directed", "scale": scale, "n": n,
                       "nnz": nnz, "iterations": iters, "parallelism": f"rowblock{ws}",
-                      "exchange": ("fused: one cooperative kernel per rank stores x "
-                                   "into every rank's padded x over NVLink (symmetric "
-                                   "memory), device-side signal barrier per iteration"
-                                   if exchange == "p2p" else
-                                   "NCCL all_gather_into_tensor (padded x slices + L1 "
-                                   "partials) per iteration"),
+                      "exchange": ("fused: one cooperative kernel per rank stores x into every "
+                                   "rank's padded x over NVLink (IPC-mapped peer buffers), "
+                                   "device-side signal barrier per iteration"
+                                   if st["hot_launches"] <= 1 else
+                                   "NCCL all-gather of the padded x slices + L1 partials per "
+                                   "iteration (fused exchange fell back)"),
+                      "graph": "built locally per rank (gbx_dgraph_generate_rmat)",
                       "l2": "flushed (256 MB write) before every step"},
            "e2e": {"value": nnz * it2 / t_e2e, "unit": "edges/s/iter",
-                   "h2d_bytes_per_step": int(rp.nbytes + col.nbytes),
+                   "h2d_bytes_per_step": int(rp_h.numel() * 8 + col_h.numel() * 4),
                    "d2h_bytes_per_step": int(n * 8),
-                   "includes": "per rank: H2D CSR (pinned), graph_new32 validation, "
-                               "property_at, property_rowdegree, shard plan, sharded "
-                               "iterations, D2H ranks",
+                   "includes": "per rank: H2D of its CSR row slice, all-to-all to the owners, "
+                               "relabel + shard plan, sharded iterations, D2H of the full ranks",
                    "samples_ms": [round(x * 1e3, 2) for x in e2e_times]},
-           "gpu_launches": int((2 if exchange == "p2p" else 2 * (iters + 1)) * args.steps),
+           "gpu_launches": int(st["launches"] * args.steps),
            "clocks": clk.summary()}
     return out, (scale,)
-
-
-class _Prepared:
-    """A backend whose prepare() already ran (keeps the plan build untimed)."""
-
-    def __init__(self, be):
-        self.be = be
-        self.device = be.device
-
-    def prepare(self, rank, world):
-        return self.be.rb, self.be.re, self.be.n
-
-    def __getattr__(self, k):
-        return getattr(self.be, k)
 
 
 # ---------------------------------------------------------------- our arm: PageRank, one GPU
@@ -481,152 +436,21 @@ def bench_pagerank(args, dist, ws, rank, local):
 
 
 # ---------------------------------------------------------------- other workloads
-def bench_simple(args, dist, ws, rank, local):
-    """Secondary configs (not the headline): bfs, bfs64, tc, sssp, bc."""
-    import ctypes as C
-
+def _timed(stream, one, steps, warmup, local, flush=None):
+    """W untimed warm-up calls, then K calls each bracketed by CUDA events on
+    the library's stream (optionally after an L2 flush on that stream), under
+    a clock sampler.  Returns (mean seconds per step, units of the last step,
+    clocks)."""
     import torch
-    import paper_2104_01661_b200 as P
-    from paper_2104_01661_b200 import algo
-
-    P.init(local)
-    torch.cuda.set_device(local)
-    w = args.workload
-    peak, peak_kind = peaks()
-    if w in ("bfs", "bfs64"):
-        scale = args.scale or (22 if w == "bfs" else 16)
-        g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
-        P.property_at(g)
-        P.property_rowdegree(g)
-        n, nnz, _, _ = g.info()
-        deg = g.row_degree()
-        srcs = P.pick_sources(deg, 64, 1)
-        from paper_2104_01661_b200.graph import call
-        import oracle  # noqa: F401  (not used on the timed path)
-
-        def one():
-            if w == "bfs":
-                for s in srcs[:8]:
-                    call("gbx_bfs", None, None, g.handle, int(s), 0, 16)
-                return 8
-            arr = np.ascontiguousarray(srcs, np.uint64)
-            call("gbx_bfs_batch", None, None, g.handle, arr.ctypes.data, len(arr))
-            return 64
-        unit_edges = nnz / 2  # Graph500 undirected convention (reached component ~ all)
-        metric = f"BFS GTEPS at R-MAT scale {scale} ({'single source' if w == 'bfs' else '64-source batch'})"
-        unit = "GTEPS"
-        # SURVEY 8d: per source B = 8 E_r + 24 V_r (int64 col once; row_ptr,
-        # parent, level per reached vertex), E_r/V_r from one untimed traversal
-        used = srcs[:8] if w == "bfs" else srcs
-        alg_bytes = 0.0
-        for s0 in used:
-            par = np.empty(n, np.int64)
-            call("gbx_bfs", par.ctypes.data, None, g.handle, int(s0), 0, 16)
-            reached = par >= 0
-            alg_bytes += 8.0 * float(deg[reached].sum()) + 24.0 * float(reached.sum())
-        roof_kernel = "k_bfs1 (cooperative push/pull levels)" if w == "bfs" else "k_bfs64 (64-lane batch)"
-        roof_note = "8*E_r + 24*V_r per source (SURVEY 8d), summed over the step's sources"
-    elif w == "tc":
-        scale = args.scale or 22
-        g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
-        P.property_rowdegree(g)
-        P.property_ndiag(g)
-        g.prepare("tc")
-        n, nnz, _, _ = g.info()
-
-        def one():
-            algo.triangle_count(g)
-            return 1
-        unit_edges = nnz / 2
-        metric = f"triangle count edges/s at R-MAT scale {scale}"
-        unit = "edges/s"
-        # our probe formulation (DESIGN 5): 4*W2 + 12*nnz(U) + 8*(n+1),
-        # W2 = sum_i C(dU(i), 2) over the (degree, id)-oriented upper triangle U
-        rp_h, col_h, _ = g.export()
-        dg = np.diff(rp_h)
-        rank = np.empty(n, np.int64)
-        rank[np.lexsort((np.arange(n), dg))] = np.arange(n)
-        rows = np.repeat(np.arange(n, dtype=np.int64), dg)
-        du = np.bincount(rows[rank[col_h] > rank[rows]], minlength=n).astype(np.float64)
-        del rows, rp_h, col_h
-        w2 = float((du * (du - 1) / 2).sum())
-        alg_bytes = 4.0 * w2 + 12.0 * float(du.sum()) + 8.0 * (n + 1)
-        roof_kernel = "k_tc_warp / k_tc_cta (middle-vertex probes)"
-        roof_note = f"4*W2 + 12*nnz(U) + 8*(n+1), W2 = {w2:.4g} wedge probes (DESIGN 5)"
-    elif w == "sssp":
-        logn = args.scale or 24
-        g = P.generate_er(logn, 16, seed=1)
-        P.property_rowdegree(g)
-        g.prepare("sssp")
-        n, nnz, _, _ = g.info()
-        srcs = P.pick_sources(g.row_degree(), 16, 1)
-        from paper_2104_01661_b200.graph import call
-
-        def one():
-            for s in srcs:
-                call("gbx_sssp", None, g.handle, int(s), 64.0)
-            return len(srcs)
-        unit_edges = nnz
-        metric = f"SSSP relaxation edges/s (ER 2^{logn}, 16 sources, delta 64)"
-        unit = "edges/s"
-        # SURVEY 8d: per source B = 8 m_r + 12 V_r (reached edges / vertices)
-        odeg = g.row_degree()
-        alg_bytes = 0.0
-        for s0 in srcs:
-            dd = np.empty(n, np.float64)
-            call("gbx_sssp", dd.ctypes.data, g.handle, int(s0), 64.0)
-            reached = np.isfinite(dd)
-            alg_bytes += 8.0 * float(odeg[reached].sum()) + 12.0 * float(reached.sum())
-        roof_kernel = "k_sssp_b (cooperative circular delta-buckets)"
-        roof_note = "8*m_r + 12*V_r per source (SURVEY 8d), summed over 16 sources"
-    elif w == "bc":
-        scale = args.scale or 24
-        g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
-        P.property_at(g)
-        P.property_rowdegree(g)
-        n, nnz, _, _ = g.info()
-        srcs = P.pick_sources(g.row_degree(), 4, 1)
-        from paper_2104_01661_b200.graph import call
-
-        if ws > 1:
-            # 1D row blocks over the ranks, one record all-gather per BFS level
-            # (dist.sharded_betweenness_rows): the same batch, strong scaling
-            from paper_2104_01661_b200.dist import GpuShardBackend, sharded_betweenness_rows
-            be = GpuShardBackend(g)
-
-            def one():
-                sharded_betweenness_rows(be, dist, [int(x) for x in srcs])
-                torch.cuda.synchronize()  # the final all-reduce ran on torch's stream
-                return 4
-        else:
-            def one():
-                s = np.ascontiguousarray(srcs, np.uint64)
-                call("gbx_betweenness", None, g.handle, s.ctypes.data, 4)
-                return 4
-        unit_edges = nnz
-        metric = f"BC batch-4 edges/s at R-MAT scale {scale}"
-        unit = "edges/s"
-        # SURVEY 8d: per batch B = E_r (8 + 16 ns) + V_r (16 + 24 ns), reached =
-        # the union of the sources' components (one untimed BFS each)
-        bdeg = g.row_degree()
-        reach = np.zeros(n, bool)
-        for s0 in srcs:
-            par = np.empty(n, np.int64)
-            call("gbx_bfs", par.ctypes.data, None, g.handle, int(s0), 0, 16)
-            reach |= par >= 0
-        ns = 4
-        alg_bytes = float(bdeg[reach].sum()) * (8 + 16 * ns) + float(reach.sum()) * (16 + 24 * ns)
-        roof_kernel = "k_bc_push/k_bc_pull/k_bc_back (batched Brandes levels)"
-        roof_note = "E_r*(8+16*ns) + V_r*(16+24*ns), ns = 4 (SURVEY 8d)"
-    else:
-        raise SystemExit(f"unknown workload {w}")
-    stream = torch.cuda.ExternalStream(g.stream())
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(max(warmup, 3)):
         one()
     torch.cuda.synchronize()
     times, units = [], 0
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
+        for _ in range(steps):
+            if flush is not None:
+                with torch.cuda.stream(stream):
+                    flush.zero_()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -634,25 +458,309 @@ def bench_simple(args, dist, ws, rank, local):
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
+    return sum(times) / len(times), units, clk.summary()
+
+
+def _roof(bytes_8d, bytes_actual, t, peak, peak_kind, kernel, note):
+    a = bytes_8d / t / 1e9
+    b = bytes_actual / t / 1e9
+    return {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak,
+            "traffic": None, "peak_kind": peak_kind, "kernel": kernel,
+            "bytes_per_step": bytes_8d, "bytes_per_step_actual": bytes_actual,
+            "achieved_actual": b, "frac_actual": b / peak,
+            "note": note + "; divided by the device time of the whole step (every launch of "
+                           "the step, CUDA events on the library stream)"}
+
+
+def secondary_bfs(g, srcs, steps, warmup, local, peak, peak_kind, scale, batch64=False,
+                  flush=None):
+    """BFS GTEPS: 8 single-source traversals (gbx_bfs, direction-optimizing) or
+    one 64-source batch (gbx_bfs_batch, config 1)."""
+    import torch
+    from paper_2104_01661_b200.graph import call
+    n, nnz, _, _ = g.info()
+    deg = g.row_degree()
+    if batch64:
+        arr = np.ascontiguousarray(srcs, np.uint64)
+
+        def one():
+            call("gbx_bfs_batch", None, None, g.handle, arr.ctypes.data, len(arr))
+            return len(arr)
+    else:
+        def one():
+            for s0 in srcs:
+                call("gbx_bfs", None, None, g.handle, int(s0), 0, 16)
+            return len(srcs)
+    # E_r / V_r per source from untimed traversals (SURVEY 8d)
+    er = vr = 0.0
+    for s0 in srcs:
+        par = np.empty(n, np.int64)
+        call("gbx_bfs", par.ctypes.data, None, g.handle, int(s0), 0, 16)
+        reached = par >= 0
+        er += float(deg[reached].sum())
+        vr += float(reached.sum())
+    stream = torch.cuda.ExternalStream(g.stream())
+    t, units, clk = _timed(stream, one, steps, warmup, local, flush)
+    launches = g.last_stats()["launches"]
+    gteps = nnz / 2 * units / t / 1e9
+    return {"metric": f"BFS GTEPS at R-MAT scale {scale} "
+                      f"({'64-source batch, BASELINE config 1' if batch64 else f'{len(srcs)} single-source traversals'})",
+            "value": gteps, "unit": "GTEPS", "steps": steps, "warmup": max(warmup, 3),
+            "ms_per_step": t * 1e3, "sources": len(srcs),
+            "config": {"scale": scale, "n": n, "nnz": nnz, "undirected": True,
+                       "teps_edges": "nnz/2 per source (Graph500 undirected convention)",
+                       "l2": "flushed (256 MB write) before every step" if flush is not None
+                             else "graph larger than L2 (not flushed)"},
+            "roofline": _roof(8 * er + 24 * vr, 4 * er + 16 * vr, t, peak, peak_kind,
+                              "k_bfs64 (64-lane batch)" if batch64 else "k_bfs1 (cooperative push/pull levels)",
+                              "SURVEY 8d bytes 8*E_r + 24*V_r (int64 col) summed over the sources; "
+                              "actual: 4*E_r + 16*V_r (int32 col, int64 row_ptr, int32 level+parent)"),
+            "gpu_launches": int(launches * steps), "clocks": clk}
+
+
+def secondary_tc(g, steps, warmup, local, peak, peak_kind, scale):
+    import torch
+    from paper_2104_01661_b200 import algo
+    n, nnz, _, _ = g.info()
+    P_ = __import__("paper_2104_01661_b200")
+    P_.property_rowdegree(g)
+    P_.property_ndiag(g)
+    g.prepare("tc")
+
+    def one():
+        algo.triangle_count(g)
+        return 1
+    # SURVEY 8d: W = sum_v dL(v) dU(v) (row-stationary wedge probes) -> B =
+    # 4W + 4 nnz(U) + 8(n+1); actual (middle-vertex probes, DESIGN 5):
+    # W2 = sum_i C(dU(i), 2) -> 4 W2 + 12 nnz(U) + 8(n+1)
+    rp_h, col_h, _ = g.export()
+    dg = np.diff(rp_h)
+    rank = np.empty(n, np.int64)
+    rank[np.lexsort((np.arange(n), dg))] = np.arange(n)
+    rows = np.repeat(np.arange(n, dtype=np.int64), dg)
+    du = np.bincount(rows[rank[col_h] > rank[rows]], minlength=n).astype(np.float64)
+    del rows, rp_h, col_h
+    dl = dg.astype(np.float64) - du
+    w8d = float((dl * du).sum())
+    w2 = float((du * (du - 1) / 2).sum())
+    unnz = float(du.sum())
+    stream = torch.cuda.ExternalStream(g.stream())
+    t, _, clk = _timed(stream, one, steps, warmup, local)
+    launches = g.last_stats()["launches"]
+    return {"metric": f"triangle count edges/s at R-MAT scale {scale} (BASELINE config 3)",
+            "value": nnz / 2 / t, "unit": "edges/s", "steps": steps, "warmup": max(warmup, 3),
+            "ms_per_step": t * 1e3, "triangles": int(algo.triangle_count(g)),
+            "config": {"scale": scale, "n": n, "nnz": nnz, "W_8d": w8d, "W2_probes": w2,
+                       "l2": "graph larger than L2 (not flushed)"},
+            "roofline": _roof(4 * w8d + 4 * unnz + 8 * (n + 1), 4 * w2 + 12 * unnz + 8 * (n + 1),
+                              t, peak, peak_kind, "k_tc_warp / k_tc_cta (middle-vertex probes)",
+                              "SURVEY 8d bytes 4*W + 4*nnz(U) + 8*(n+1), W = sum dL*dU; actual: "
+                              "this kernel's probes, 4*W2 + 12*nnz(U) + 8*(n+1), W2 = sum C(dU,2)"),
+            "gpu_launches": int(launches * steps), "clocks": clk}
+
+
+def secondary_sssp(g, srcs, steps, warmup, local, peak, peak_kind, logn, delta=64.0):
+    import torch
+    from paper_2104_01661_b200.graph import call
+    n, nnz, _, _ = g.info()
+    odeg = g.row_degree()
+
+    def one():
+        for s0 in srcs:
+            call("gbx_sssp", None, g.handle, int(s0), delta)
+        return len(srcs)
+    mr = vr = 0.0
+    for s0 in srcs:
+        dd = np.empty(n, np.float64)
+        call("gbx_sssp", dd.ctypes.data, g.handle, int(s0), delta)
+        reached = np.isfinite(dd)
+        mr += float(odeg[reached].sum())
+        vr += float(reached.sum())
+    stream = torch.cuda.ExternalStream(g.stream())
+    t, units, clk = _timed(stream, one, steps, warmup, local)
+    launches = g.last_stats()["launches"]
+    return {"metric": f"SSSP relaxation edges/s (ER 2^{logn}, {len(srcs)} sources, delta {delta:g}; "
+                      f"BASELINE config 4)",
+            "value": mr / t, "unit": "edges/s", "steps": steps, "warmup": max(warmup, 3),
+            "ms_per_step": t * 1e3, "ms_per_source": t * 1e3 / len(srcs),
+            "config": {"logn": logn, "n": n, "nnz": nnz, "delta": delta, "sources": len(srcs),
+                       "l2": "graph larger than L2 (not flushed)"},
+            "roofline": _roof(8 * mr + 12 * vr, 4 * mr + 20 * vr, t, peak, peak_kind,
+                              "k_sssp_b (cooperative circular delta-buckets)",
+                              "SURVEY 8d bytes 8*m_r + 12*V_r per source, summed; actual: packed "
+                              "(col:24|w:8) edges 4*m_r + 20*V_r (16-byte row record + u32 dist)"),
+            "gpu_launches": int(launches * steps), "clocks": clk}
+
+
+def secondary_bc(g, srcs, steps, warmup, local, peak, peak_kind, scale):
+    import torch
+    from paper_2104_01661_b200.graph import call
+    n, nnz, _, _ = g.info()
+    ns = len(srcs)
+    s = np.ascontiguousarray(srcs, np.uint64)
+
+    def one():
+        call("gbx_betweenness", None, g.handle, s.ctypes.data, ns)
+        return ns
+    bdeg = g.row_degree()
+    reach = np.zeros(n, bool)
+    for s0 in srcs:
+        par = np.empty(n, np.int64)
+        call("gbx_bfs", par.ctypes.data, None, g.handle, int(s0), 0, 16)
+        reach |= par >= 0
+    er, vr = float(bdeg[reach].sum()), float(reach.sum())
+    b8d = er * (8 + 16 * ns) + vr * (16 + 24 * ns)
+    stream = torch.cuda.ExternalStream(g.stream())
+    t, _, clk = _timed(stream, one, steps, warmup, local)
+    launches = g.last_stats()["launches"]
+    return {"metric": f"BC batch-{ns} edges/s at R-MAT scale {scale} (BASELINE config 5)",
+            "value": nnz / t, "unit": "edges/s", "steps": steps, "warmup": max(warmup, 3),
+            "ms_per_step": t * 1e3,
+            "config": {"scale": scale, "n": n, "nnz": nnz, "sources": ns,
+                       "l2": "graph larger than L2 (not flushed)"},
+            "roofline": _roof(b8d, b8d, t, peak, peak_kind,
+                              "k_bc_push/k_bc_pull/k_bc_back (batched Brandes levels)",
+                              "SURVEY 8d bytes E_r*(8+16*ns) + V_r*(16+24*ns) (int32 col: the same "
+                              "formula is the actual)"),
+            "gpu_launches": int(launches * steps), "clocks": clk}
+
+
+def run_secondaries(args, local, which=None):
+    """BASELINE's other configs, each timed on its own (BFS GTEPS is half of
+    BASELINE's metric): {name: entry}."""
+    import torch
+    import paper_2104_01661_b200 as P
+    peak, peak_kind = peaks()
+    steps = max(3, min(args.steps, 10))
+    out = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    want = set(which or ["bfs22", "bfs16_64", "tc22", "sssp24", "bc24"])
+    if want & {"bfs22", "tc22"}:
+        g = P.generate_rmat(22, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
+        P.property_at(g)
+        P.property_rowdegree(g)
+        if "bfs22" in want:
+            srcs = P.pick_sources(g.row_degree(), 64, 1)[:8]
+            out["bfs22"] = secondary_bfs(g, srcs, steps, args.warmup, local, peak, peak_kind, 22)
+        if "tc22" in want:
+            out["tc22"] = secondary_tc(g, steps, args.warmup, local, peak, peak_kind, 22)
+        g.free()
+    if "bfs16_64" in want:
+        g = P.generate_rmat(16, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
+        P.property_at(g)
+        P.property_rowdegree(g)
+        srcs = P.pick_sources(g.row_degree(), 64, 1)
+        out["bfs16_64"] = secondary_bfs(g, srcs, steps, args.warmup, local, peak, peak_kind, 16,
+                                        batch64=True, flush=flush)
+        g.free()
+    if "bc24" in want:
+        g = P.generate_rmat(24, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
+        P.property_at(g)
+        P.property_rowdegree(g)
+        srcs = P.pick_sources(g.row_degree(), 4, 1)
+        out["bc24"] = secondary_bc(g, srcs, steps, args.warmup, local, peak, peak_kind, 24)
+        g.free()
+    if "sssp24" in want:  # last: its persisting-L2 window is device-wide
+        g = P.generate_er(24, 16, seed=1)
+        P.property_rowdegree(g)
+        g.prepare("sssp")
+        srcs = P.pick_sources(g.row_degree(), 16, 1)
+        out["sssp24"] = secondary_sssp(g, srcs, max(3, min(steps, 5)), args.warmup, local, peak,
+                                       peak_kind, 24)
+        g.free()
+    del flush
+    torch.cuda.synchronize()
+    return out
+
+
+def bench_simple(args, dist, ws, rank, local):
+    """One secondary config as the whole line (--workload bfs|bfs64|tc|sssp|bc);
+    N > 1: TC / BFS / BC through the library's multi-GPU calls (gbx_*_mg on a
+    distributed graph each rank builds locally), SSSP as replicas."""
+    import paper_2104_01661_b200 as P
+    P.init(local)
+    import torch
+    torch.cuda.set_device(local)
+    w = args.workload
+    if ws > 1 or force_sharded():
+        return bench_simple_mg(args, dist, ws, rank, local)
+    name = {"bfs": "bfs22", "bfs64": "bfs16_64", "tc": "tc22", "sssp": "sssp24", "bc": "bc24"}[w]
+    if args.scale:
+        raise SystemExit("--scale is fixed per BASELINE config for the secondary workloads")
+    e = run_secondaries(args, local, [name])[name]
+    out = {"metric": e["metric"], "value": e["value"], "unit": e["unit"], "n_gpus": ws,
+           "steps": e["steps"], "warmup": e["warmup"], "ms_per_step": e["ms_per_step"],
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "int32 indices", "data": "synthetic", "config": dict(e["config"], workload=name),
+           "roofline": e["roofline"], "gpu_launches": e["gpu_launches"], "clocks": e["clocks"]}
+    return out, None
+
+
+def bench_simple_mg(args, dist, ws, rank, local):
+    """Secondary configs at N GPUs through the C++ multi-GPU path."""
+    import torch
+    import paper_2104_01661_b200 as P
+    from paper_2104_01661_b200.mg import Comm, DGraph
+    w = args.workload
+    comm = Comm.from_torch(dist, local)
+    steps = max(3, min(args.steps, 10))
+    if w == "sssp":
+        raise SystemExit("sssp runs as replicas only (SURVEY 8e): use --gpus 1")
+    scale = {"tc": 22, "bfs": 22, "bfs64": 16, "bc": 24}[w]
+    kind = P.Kind.UndirectedAdjacency
+    g = DGraph.rmat(comm, scale, 16, seed=1, kind=kind)
+    if w in ("bfs", "bfs64", "bc"):
+        # the sources the single-GPU line uses: degrees from a local full graph
+        # would need the replica; the seeded draw over non-isolated vertices
+        # needs only the global degree array (one all-reduce, small)
+        deg = torch.zeros(g.n, dtype=torch.int64, device="cuda")
+        rb, re, _ = g.block(0)
+        _, _, brp, _ = g.export_block(0)
+        deg[rb:re] = torch.from_numpy(np.diff(brp)).cuda()
+        dist.all_reduce(deg)
+        deg = deg.cpu().numpy()
+    if w == "tc":
+        def one():
+            g.triangle_count()
+            return 1
+        metric, unit, per = f"triangle count edges/s at R-MAT scale {scale} (multi-GPU)", "edges/s", g.nnz / 2
+    elif w in ("bfs", "bfs64"):
+        srcs = P.pick_sources(deg, 64, 1)[:8]
+
+        def one():
+            for s0 in srcs:
+                g.bfs(int(s0), to_host=False)
+            return len(srcs)
+        metric, unit, per = f"BFS GTEPS at R-MAT scale {scale} (row-sharded pull levels)", "GTEPS", g.nnz / 2 / 1e9
+    else:
+        srcs = P.pick_sources(deg, 4, 1)
+
+        def one():
+            g.betweenness(srcs, to_host=False)
+            return 1
+        metric, unit, per = f"BC batch-4 edges/s at R-MAT scale {scale} (row-partitioned)", "edges/s", g.nnz
+    for _ in range(max(args.warmup, 3)):
+        one()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(steps):
+            barrier(dist)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            units = one()  # host-synchronous library call (its streams drained)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
     t = max_over_ranks(dist, sum(times) / len(times))
-    per = unit_edges * units / t
-    value = per / 1e9 if unit == "GTEPS" else per
-    strong = w == "bc" and ws > 1  # one batch split over the ranks' row blocks
-    out = {"metric": metric, "value": value if strong else value * ws, "unit": unit,
-           "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3),
-           "ms_per_step": t * 1e3, "higher_is_better": True,
-           "scaling": "strong" if strong else "weak", "vs_baseline": None,
-           "dtype": "int32 indices", "data": "synthetic",
-           "config": {"workload": w, "scale": scale if w != "sssp" else logn, "n": n,
-                      "nnz": nnz},
-           "gpu_launches": int(g.last_stats()["launches"] * args.steps),
-           "clocks": clk.summary()}
-    achieved = alg_bytes / t / 1e9
-    out["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                       "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                       "kernel": roof_kernel, "bytes_per_step": alg_bytes,
-                       "note": roof_note + "; divided by the device time of the whole step "
-                               "(all of the step's launches)"}
+    out = {"metric": metric, "value": per * units / t, "unit": unit, "n_gpus": ws, "steps": steps,
+           "warmup": max(args.warmup, 3), "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "int32 indices", "data": "synthetic",
+           "config": {"workload": w, "scale": scale, "n": g.n, "nnz": g.nnz,
+                      "parallelism": f"rowblock{ws}", "graph": "built locally per rank "
+                      "(gbx_dgraph_generate_rmat: edge slices + all-to-all to the owners)"},
+           "gpu_launches": int(g.last_stats()["launches"] * steps), "clocks": clk.summary()}
     return out, None
 
 
@@ -666,6 +774,8 @@ def main():
                     choices=["pagerank", "bfs", "bfs64", "tc", "sssp", "bc"])
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the other BASELINE configs in the default line")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -675,6 +785,10 @@ def main():
         out, extra = bench_pagerank_sharded(args, dist, ws, rank, local)
     elif args.workload == "pagerank":
         out, extra = bench_pagerank(args, dist, ws, rank, local)
+        if ws == 1 and not args.no_secondary:
+            # the rest of BASELINE's metric (BFS GTEPS) and configs, each with
+            # its own roofline and clock record
+            out["secondary"] = run_secondaries(args, local)
     else:
         out, extra = bench_simple(args, dist, ws, rank, local)
     if rank == 0:

@@ -63,7 +63,8 @@ enum {
   GBX_CUDA_ERROR = -30,
   GBX_OUT_OF_MEMORY = -31,
   GBX_UNSUPPORTED = -32,
-  GBX_NULL_ARGUMENT = -33
+  GBX_NULL_ARGUMENT = -33,
+  GBX_COMM_ERROR = -34  /* NCCL / peer-memory failure of a multi-GPU call */
 };
 
 /* value domains: gblite::Domain (value.hpp:18-23) + int32 weights */
@@ -461,6 +462,77 @@ int gbx_bfs_shard_begin(gbx_graph* g, uint64_t source, int rank, int nranks, int
 int gbx_bfs_shard_level(gbx_graph* g, const uint32_t* frontier_dev, uint32_t* next_slice_dev,
                         int64_t* found, char msg[GBX_MSG_LEN]);
 int gbx_bfs_shard_result(gbx_graph* g, int64_t* parent, int64_t* level, char msg[GBX_MSG_LEN]);
+
+/* ---- multi-GPU: communicator, distributed graph, algorithms ---------------
+ * SURVEY.md §8e.  The reference is single-threaded (no counterpart); the
+ * entry points mirror its algorithm signatures (algorithms.hpp:19-104) with a
+ * distributed graph in place of the Graph, and every rank receives the same
+ * full result the reference returns.
+ *
+ * Communicator: one NCCL rank per process / GPU (gbx_comm_init, the unique id
+ * from gbx_comm_unique_id on one rank, passed to the others by the caller), or
+ * nranks in-process ranks on ONE GPU (gbx_comm_init_local: the same protocols,
+ * the exchange as device copies -- used to test the multi-rank paths on one
+ * B200).  NCCL is bound at run time (the copy already loaded in the process,
+ * else the system libnccl.so.2).  NCCL failures -> GBX_COMM_ERROR. */
+#define GBX_COMM_ID_BYTES 128
+typedef struct gbx_comm gbx_comm;
+typedef struct gbx_dgraph gbx_dgraph;
+int gbx_comm_unique_id(void* id, char msg[GBX_MSG_LEN]);
+int gbx_comm_init(gbx_comm** comm, int nranks, int rank, const void* id, int device,
+                  char msg[GBX_MSG_LEN]);
+int gbx_comm_init_local(gbx_comm** comm, int nranks, int device, char msg[GBX_MSG_LEN]);
+int gbx_comm_free(gbx_comm** comm, char msg[GBX_MSG_LEN]);
+int gbx_comm_info(const gbx_comm* comm, int* nranks, int* rank, int* nlocal,
+                  char msg[GBX_MSG_LEN]);
+
+/* Distributed graph: rank q owns rows [b_q, b_{q+1}) (32-aligned, balanced by
+ * rows + entries) of A -- and of AT for a directed graph -- and nothing else;
+ * every rank builds its block LOCALLY (graph_new, graph.cpp:16-41, split over
+ * the ranks): generated edges [q*m/P, (q+1)*m/P) of the seeded R-MAT stream
+ * (the same graph as gbx_generate_rmat), or the CSR rows each rank passes
+ * (host arrays, global column ids, int32), shuffled to their owners with one
+ * all-to-all; self-loops dropped, duplicates combined (Bool pattern).
+ * With a local communicator the block arrays have nlocal entries (one per
+ * in-process rank), with NCCL one.  gbx_dgraph_block / _export_block read back
+ * local rank `local`'s block (row_ptr: re - rb + 1 entries). */
+int gbx_dgraph_generate_rmat(gbx_dgraph** g, gbx_comm* comm, int scale, int edge_factor,
+                             double a, double b, double c, uint64_t seed, int scramble, int kind,
+                             char msg[GBX_MSG_LEN]);
+int gbx_dgraph_from_blocks(gbx_dgraph** g, gbx_comm* comm, int64_t n, const int64_t* row_begin,
+                           const int64_t* row_end, const int64_t* const* row_ptr,
+                           const int32_t* const* col, int kind, char msg[GBX_MSG_LEN]);
+int gbx_dgraph_free(gbx_dgraph** g, char msg[GBX_MSG_LEN]);
+int gbx_dgraph_info(const gbx_dgraph* g, int64_t* n, int64_t* nnz, int* kind,
+                    char msg[GBX_MSG_LEN]);
+int gbx_dgraph_block(const gbx_dgraph* g, int local, int64_t* row_begin, int64_t* row_end,
+                     int64_t* nnz, char msg[GBX_MSG_LEN]);
+int gbx_dgraph_export_block(const gbx_dgraph* g, int local, int64_t* row_ptr, int32_t* col,
+                            char msg[GBX_MSG_LEN]);
+int gbx_dgraph_last_stats(const gbx_dgraph* g, gbx_stats* stats, char msg[GBX_MSG_LEN]);
+
+/* pagerank_gap (pagerank.cpp:8-81) over the ranks: 1D row blocks of the
+ * in-degree-relabeled AT; exchange GBX_MG_P2P = fused into the iteration
+ * kernel (peer stores over NVLink, device-side barrier bounded by option
+ * p2p.timeout_ms), GBX_MG_NCCL = one all-gather of the x slices per iteration,
+ * GBX_MG_AUTO = fused, falling back to NCCL on every rank when any rank's
+ * fused run fails.  rank: n doubles (NULL: keep on the device). */
+enum { GBX_MG_AUTO = 0, GBX_MG_NCCL = 1, GBX_MG_P2P = 2 };
+int gbx_pagerank_mg(double* rank, int* iterations, gbx_dgraph* g, double damping, double tol,
+                    int itermax, int exchange, char msg[GBX_MSG_LEN]);
+/* triangle_count (triangle.cpp:30-64), undirected: U replicated, middle
+ * vertices split by probe work, one u64 all-reduce. */
+int gbx_triangle_count_mg(uint64_t* count, gbx_dgraph* g, char msg[GBX_MSG_LEN]);
+/* bfs (bfs.cpp:18-85): parents / levels as gbx_bfs (n each, -1 unreached,
+ * NULL allowed), pull levels over the owned rows + one frontier-bitmap
+ * all-gather per level. */
+int gbx_bfs_mg(int64_t* parent, int64_t* level, gbx_dgraph* g, uint64_t source,
+               char msg[GBX_MSG_LEN]);
+/* betweenness_centrality (betweenness.cpp:11-86): row-partitioned Brandes
+ * in batches of 4 sources, one record all-gather per BFS level, one fp64
+ * all-reduce of the centrality (n doubles, NULL allowed). */
+int gbx_betweenness_mg(double* centrality, gbx_dgraph* g, const uint64_t* sources, uint64_t ns,
+                       char msg[GBX_MSG_LEN]);
 
 #ifdef __cplusplus
 }

@@ -102,6 +102,22 @@ _SIGS = {
     "gbx_bc_shard_backward": [_vp, _pp, _vp, _vp],
     "gbx_bc_shard_backward_apply": [_vp, _vp, _i64],
     "gbx_bc_shard_centrality": [_vp, _pp],
+    "gbx_comm_unique_id": [_vp],
+    "gbx_comm_init": [_pp, _int, _int, _vp, _int],
+    "gbx_comm_init_local": [_pp, _int, _int],
+    "gbx_comm_free": [_pp],
+    "gbx_comm_info": [_vp, _vp, _vp, _vp],
+    "gbx_dgraph_generate_rmat": [_pp, _vp, _int, _int, _dbl, _dbl, _dbl, _u64, _int, _int],
+    "gbx_dgraph_from_blocks": [_pp, _vp, _i64, _vp, _vp, _vp, _vp, _int],
+    "gbx_dgraph_free": [_pp],
+    "gbx_dgraph_info": [_vp, _vp, _vp, _vp],
+    "gbx_dgraph_block": [_vp, _int, _vp, _vp, _vp],
+    "gbx_dgraph_export_block": [_vp, _int, _vp, _vp],
+    "gbx_dgraph_last_stats": [_vp, C.POINTER(gbx_stats)],
+    "gbx_pagerank_mg": [_vp, _vp, _vp, _dbl, _dbl, _int, _int],
+    "gbx_triangle_count_mg": [_vp, _vp],
+    "gbx_bfs_mg": [_vp, _vp, _vp, _u64],
+    "gbx_betweenness_mg": [_vp, _vp, _vp, _u64],
 }
 
 

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "comm.cuh"
 #include "plans.cuh"
 
 #ifndef GBX_VERSION
@@ -30,9 +31,21 @@ gbx_graph::~gbx_graph() {
   rowdeg.release();
   coldeg.release();
   if (stream) cudaStreamDestroy(stream);
+  (void)cudaGetLastError();  // never leave a destructor's error for the next call
 }
 
 namespace gbx {
+
+gbx_graph* graph_handle() {
+  auto* g = new gbx_graph();
+  cudaError_t e = cudaGetDevice(&g->device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete g;
+    gbx::fail(GBX_CUDA_ERROR, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  }
+  return g;
+}
 
 void reset_plans(gbx_graph* g) {
   g->pr.reset();
@@ -76,16 +89,7 @@ gbx_graph* need(const gbx_graph* g) {
   return const_cast<gbx_graph*>(g);
 }
 
-gbx_graph* new_handle() {
-  auto* g = new gbx_graph();
-  cudaError_t e = cudaGetDevice(&g->device);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
-  if (e != cudaSuccess) {
-    delete g;
-    gbx::fail(GBX_CUDA_ERROR, std::string("no CUDA device: ") + cudaGetErrorString(e));
-  }
-  return g;
-}
+gbx_graph* new_handle() { return gbx::graph_handle(); }
 
 template <typename Build>
 int make_graph(gbx_graph** out, char* msg, Build&& build) {
@@ -905,3 +909,162 @@ int gbx_partition_rows(int64_t* bounds, const gbx_graph* gc, int parts, int tran
 }
 
 }  // extern "C"
+
+// ---- multi-GPU: communicator, distributed graph, algorithms ----------------------
+
+namespace {
+
+gbx_comm* need_comm(const gbx_comm* c) {
+  if (!c) gbx::fail(GBX_NULL_ARGUMENT, "communicator handle is NULL");
+  return const_cast<gbx_comm*>(c);
+}
+gbx_dgraph* need_dg(const gbx_dgraph* g) {
+  if (!g) gbx::fail(GBX_NULL_ARGUMENT, "distributed graph handle is NULL");
+  return const_cast<gbx_dgraph*>(g);
+}
+void check_local(const gbx_dgraph* g, int l) {
+  if (l < 0 || l >= g->comm->nlocal) gbx::fail(GBX_INVALID_VALUE, "local rank out of range");
+}
+
+}  // namespace
+
+int gbx_comm_unique_id(void* id, char* msg) {
+  return guard(msg, [&] {
+    if (!id) gbx::fail(GBX_NULL_ARGUMENT, "id is NULL");
+    gbx::comm_unique_id(id);
+  });
+}
+
+int gbx_comm_init(gbx_comm** c, int nranks, int rank, const void* id, int device, char* msg) {
+  return guard(msg, [&] {
+    if (!c) gbx::fail(GBX_NULL_ARGUMENT, "comm out-pointer is NULL");
+    *c = nullptr;
+    *c = gbx::comm_new_nccl(nranks, rank, id, device);
+  });
+}
+
+int gbx_comm_init_local(gbx_comm** c, int nranks, int device, char* msg) {
+  return guard(msg, [&] {
+    if (!c) gbx::fail(GBX_NULL_ARGUMENT, "comm out-pointer is NULL");
+    *c = nullptr;
+    *c = gbx::comm_new_local(nranks, device);
+  });
+}
+
+int gbx_comm_free(gbx_comm** c, char* msg) {
+  return guard(msg, [&] {
+    if (c && *c) {
+      delete *c;
+      *c = nullptr;
+    }
+  });
+}
+
+int gbx_comm_info(const gbx_comm* c, int* nranks, int* rank, int* nlocal, char* msg) {
+  return guard(msg, [&] {
+    need_comm(c);
+    if (nranks) *nranks = c->nranks;
+    if (rank) *rank = c->rank;
+    if (nlocal) *nlocal = c->nlocal;
+  });
+}
+
+int gbx_dgraph_generate_rmat(gbx_dgraph** g, gbx_comm* c, int scale, int edge_factor, double a,
+                             double b, double cc, uint64_t seed, int scramble, int kind,
+                             char* msg) {
+  return guard(msg, [&] {
+    if (!g) gbx::fail(GBX_NULL_ARGUMENT, "graph out-pointer is NULL");
+    *g = nullptr;
+    need_comm(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    *g = gbx::dgraph_generate_rmat(c, scale, edge_factor, a, b, cc, seed, scramble, kind);
+  });
+}
+
+int gbx_dgraph_from_blocks(gbx_dgraph** g, gbx_comm* c, int64_t n, const int64_t* row_begin,
+                           const int64_t* row_end, const int64_t* const* row_ptr,
+                           const int32_t* const* col, int kind, char* msg) {
+  return guard(msg, [&] {
+    if (!g) gbx::fail(GBX_NULL_ARGUMENT, "graph out-pointer is NULL");
+    *g = nullptr;
+    need_comm(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    *g = gbx::dgraph_from_blocks(c, n, row_begin, row_end, row_ptr, col, kind);
+  });
+}
+
+int gbx_dgraph_free(gbx_dgraph** g, char* msg) {
+  return guard(msg, [&] {
+    if (g && *g) {
+      // the communicator must still be alive (free graphs before their comm)
+      GBX_CUDA(cudaSetDevice((*g)->device));
+      delete *g;
+      *g = nullptr;
+    }
+  });
+}
+
+int gbx_dgraph_info(const gbx_dgraph* g, int64_t* n, int64_t* nnz, int* kind, char* msg) {
+  return guard(msg, [&] {
+    need_dg(g);
+    if (n) *n = g->n;
+    if (nnz) *nnz = g->nnz;
+    if (kind) *kind = g->kind;
+  });
+}
+
+int gbx_dgraph_block(const gbx_dgraph* g, int local, int64_t* rb, int64_t* re, int64_t* nnz,
+                     char* msg) {
+  return guard(msg, [&] {
+    need_dg(g);
+    check_local(g, local);
+    int64_t b, e;
+    gbx::dgraph_block(g, local, &b, &e);
+    if (rb) *rb = b;
+    if (re) *re = e;
+    if (nnz) *nnz = g->local_nnz[local];
+  });
+}
+
+int gbx_dgraph_export_block(const gbx_dgraph* g, int local, int64_t* row_ptr, int32_t* col,
+                            char* msg) {
+  return guard(msg, [&] {
+    need_dg(g);
+    check_local(g, local);
+    int64_t b, e;
+    gbx::dgraph_block(g, local, &b, &e);
+    const gbx_graph* s = g->shard[local];
+    GBX_CUDA(cudaSetDevice(g->comm->device));
+    if (row_ptr) GBX_CUDA(cudaMemcpy(row_ptr, s->A.rp.p + b, (e - b + 1) * 8, cudaMemcpyDeviceToHost));
+    if (col && s->A.nnz) GBX_CUDA(cudaMemcpy(col, s->A.col.p, s->A.nnz * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int gbx_dgraph_last_stats(const gbx_dgraph* g, gbx_stats* st, char* msg) {
+  return guard(msg, [&] {
+    need_dg(g);
+    if (!st) gbx::fail(GBX_NULL_ARGUMENT, "stats is NULL");
+    *st = g->stats;
+  });
+}
+
+int gbx_pagerank_mg(double* rank, int* iters, gbx_dgraph* g, double damping, double tol,
+                    int itermax, int exchange, char* msg) {
+  return guard(msg, [&] { gbx::pagerank_mg(need_dg(g), damping, tol, itermax, exchange, rank, iters); });
+}
+
+int gbx_triangle_count_mg(uint64_t* count, gbx_dgraph* g, char* msg) {
+  return guard(msg, [&] {
+    const uint64_t t = gbx::triangle_count_mg(need_dg(g));
+    if (count) *count = t;
+  });
+}
+
+int gbx_bfs_mg(int64_t* parent, int64_t* level, gbx_dgraph* g, uint64_t source, char* msg) {
+  return guard(msg, [&] { gbx::bfs_mg(need_dg(g), source, parent, level); });
+}
+
+int gbx_betweenness_mg(double* centrality, gbx_dgraph* g, const uint64_t* sources, uint64_t ns,
+                       char* msg) {
+  return guard(msg, [&] { gbx::betweenness_mg(need_dg(g), sources, ns, centrality); });
+}

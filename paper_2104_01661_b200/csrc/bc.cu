@@ -1050,7 +1050,7 @@ static BcShard& need_shard(gbx_graph* g) {
 }
 
 void bc_shard_begin(gbx_graph* g, const uint64_t* sources, uint64_t ns, int rank, int nranks,
-                    int64_t* rb_out, int64_t* re_out) {
+                    int64_t* rb_out, int64_t* re_out, const int64_t* bounds) {
   require_at(g, "bc_shard");
   const int64_t n = g->A.n;
   if (ns == 0) fail(GBX_EMPTY_BATCH, "empty source batch");
@@ -1069,7 +1069,10 @@ void bc_shard_begin(gbx_graph* g, const uint64_t* sources, uint64_t ns, int rank
   S->rank = rank;
   S->nranks = nranks;
   S->ns = static_cast<int>(ns);
-  {
+  if (bounds) {
+    S->rb = bounds[rank];
+    S->re = std::max(bounds[rank], bounds[rank + 1]);
+  } else {
     DevArray<int64_t> bnd(nranks + 1);
     k_bc_split<<<1, std::max(32, ((nranks + 32) / 32) * 32), 0, s>>>(A.rp.p, n, nranks, bnd.p);
     GBX_LAUNCHED();

@@ -1035,7 +1035,7 @@ static BfsShard& need_bfs_shard(gbx_graph* g) {
 }
 
 void bfs_shard_begin(gbx_graph* g, uint64_t source, int rank, int nranks, int64_t* rb_out,
-                     int64_t* re_out) {
+                     int64_t* re_out, const int64_t* bounds) {
   require_at(g, "bfs_shard");
   const int64_t n = g->A.n;
   if (source >= static_cast<uint64_t>(n)) fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(source));
@@ -1048,7 +1048,13 @@ void bfs_shard_begin(gbx_graph* g, uint64_t source, int rank, int nranks, int64_
   S->rank = rank;
   S->nranks = nranks;
   S->source = static_cast<int32_t>(source);
-  {
+  if (bounds) {
+    // the distributed graph's ownership (32-aligned; its shard holds only these rows)
+    S->rb = bounds[rank];
+    S->re = bounds[rank + 1];
+    if ((S->rb & 31) || (S->re < n && (S->re & 31)))
+      fail(GBX_INVALID_VALUE, "bfs_shard: row blocks must be 32-aligned");
+  } else {
     DevArray<int64_t> b(nranks + 1);
     k_bfs_shard_split<<<1, ((nranks + 32) / 32) * 32, 0, s>>>(AT.rp.p, n, nranks, b.p);
     GBX_LAUNCHED();

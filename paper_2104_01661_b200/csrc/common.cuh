@@ -264,6 +264,11 @@ struct Tmp {
 void generate_rmat(gbx_graph* g, int scale, int ef, double a, double b, double c,
                    uint64_t seed, int scramble, int kind);
 void generate_er(gbx_graph* g, int logn, int degree, uint64_t seed, int weighted);
+void rmat_keys(cudaStream_t s, int scale, int ef, double a, double b, double c, uint64_t seed,
+               int scramble, bool sym, int64_t e0, int64_t e1, uint64_t* keys);
+void csr_from_keys_unique(cudaStream_t s, int64_t n, int bits, const uint64_t* sorted, int64_t m,
+                          Csr& A);
+gbx_graph* graph_handle();  // a new empty graph handle on the current device
 int64_t count_ndiag(cudaStream_t s, const Csr& A);
 bool csr_equal(cudaStream_t s, const Csr& X, const Csr& Y);
 void sync(gbx_graph* g);
@@ -282,18 +287,22 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
                    int64_t* level);
 void bfs_prepare(gbx_graph* g);
 void bfs_shard_begin(gbx_graph* g, uint64_t source, int rank, int nranks, int64_t* rb_out,
-                     int64_t* re_out);
+                     int64_t* re_out, const int64_t* bounds = nullptr);
 void bfs_shard_level(gbx_graph* g, const uint32_t* front, uint32_t* next_slice, int64_t* found);
 void bfs_shard_result(gbx_graph* g, int64_t* parent, int64_t* level);
 uint64_t tc_run(gbx_graph* g, int64_t row_begin, int64_t row_end);
 void tc_prepare(gbx_graph* g);
 void tc_partition(gbx_graph* g, int parts, int64_t* bounds);
+void tc_upper_keys(cudaStream_t s, const Csr& A, const int32_t* deg, int64_t n, int bits,
+                   uint64_t* keys);
+void tc_plan_from_upper(gbx_graph* g, int64_t n, int bits, const uint64_t* sorted, int64_t unnz,
+                        uint64_t* scratch, uint64_t* scratch2);
 void sssp_run(gbx_graph* g, uint64_t source, double delta, double* dist);
 double sssp_default_delta(gbx_graph* g);
 void sssp_prepare(gbx_graph* g);
 void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrality);
 void bc_shard_begin(gbx_graph* g, const uint64_t* sources, uint64_t ns, int rank, int nranks,
-                    int64_t* rb_out, int64_t* re_out);
+                    int64_t* rb_out, int64_t* re_out, const int64_t* bounds = nullptr);
 void bc_shard_forward(gbx_graph* g, void** recs, int64_t* nrec);
 void bc_shard_forward_apply(gbx_graph* g, const void* recs, int64_t nrec, int* done);
 void bc_shard_backward(gbx_graph* g, void** recs, int64_t* nrec, int* done);
@@ -306,6 +315,9 @@ void pr_shard_unpermute(gbx_graph* g, const float* r_full, double* out_host);
 void pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, float* r_new,
                    float* x_slice, double* l1, double damping);
 void pr_shard_layout(gbx_graph* g, int64_t* chunk, int64_t* bounds);
+std::vector<int64_t> pr_bounds(const int64_t* rp, int64_t n, int64_t nnz, int nranks);
+void pr_shard_from_block(gbx_graph* g, int rank, int nranks, Csr& block, DevArray<int32_t>& deg,
+                         DevArray<int32_t>& new2old, const std::vector<int64_t>& bounds);
 void pr_shard_run_p2p_multi(gbx_graph* const* gs, int nv, const uint64_t* x0_peers,
                             const uint64_t* x1_peers, const uint64_t* l1_peers,
                             const uint64_t* sig_peers, float* const* r0s, float* const* r1s,

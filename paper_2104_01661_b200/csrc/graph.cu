@@ -422,11 +422,14 @@ __device__ __forceinline__ uint32_t gen_scramble(uint32_t x, int scale, uint64_t
 }
 
 
+// edges [e0, e0 + m) of the seeded stream; key slot i = e - e0
 __global__ void k_rmat(int scale, int64_t m, uint32_t ta, uint32_t tab, uint32_t tabc,
-                       uint64_t s, int scramble, uint64_t add, int sym, uint64_t* keys) {
+                       uint64_t s, int scramble, uint64_t add, int sym, uint64_t* keys,
+                       int64_t e0) {
   const uint64_t kDropKey = uint64_t(1) << (2 * scale);
-  int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (e >= m) return;
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= m) return;
+  const int64_t e = e0 + i;
   int per = (scale + 1) / 2;
   uint32_t uu = 0, vv = 0;
   uint64_t r = 0;
@@ -447,10 +450,10 @@ __global__ void k_rmat(int scale, int64_t m, uint32_t ta, uint32_t tab, uint32_t
   }
   bool loop = uu == vv;
   if (sym) {
-    keys[2 * e] = loop ? kDropKey : ((uint64_t(uu) << scale) | vv);
-    keys[2 * e + 1] = loop ? kDropKey : ((uint64_t(vv) << scale) | uu);
+    keys[2 * i] = loop ? kDropKey : ((uint64_t(uu) << scale) | vv);
+    keys[2 * i + 1] = loop ? kDropKey : ((uint64_t(vv) << scale) | uu);
   } else {
-    keys[e] = loop ? kDropKey : ((uint64_t(uu) << scale) | vv);
+    keys[i] = loop ? kDropKey : ((uint64_t(uu) << scale) | vv);
   }
 }
 
@@ -575,17 +578,20 @@ static void keys_to_graph(gbx_graph* g, int64_t n, int bits, uint64_t* keys, int
   g->kind = kind;
 }
 
-void generate_rmat(gbx_graph* g, int scale, int ef, double a, double b, double c,
-                   uint64_t seed, int scramble, int kind) {
+static void rmat_check(int scale, int ef, double a, double b, double c) {
   if (scale < 1 || scale > 30) fail(GBX_INVALID_VALUE, "rmat: scale must be in [1,30]");
   if (ef < 1) fail(GBX_INVALID_VALUE, "rmat: edge factor must be >= 1");
   if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0))
     fail(GBX_INVALID_VALUE, "rmat: need a,b,c >= 0 and a+b+c <= 1");
-  cudaStream_t s = g->stream;
-  int64_t n = int64_t(1) << scale;
-  int64_t m = int64_t(ef) << scale;
-  bool sym = kind == GBX_UNDIRECTED;
-  int64_t mk = sym ? 2 * m : m;
+}
+
+// keys (u << scale | v) of edges [e0, e1) of the seeded R-MAT stream (both
+// directions when sym: 2 keys per edge); self-loops are the drop key 1 << 2*scale
+void rmat_keys(cudaStream_t s, int scale, int ef, double a, double b, double c, uint64_t seed,
+               int scramble, bool sym, int64_t e0, int64_t e1, uint64_t* keys) {
+  rmat_check(scale, ef, a, b, c);
+  const int64_t m = e1 - e0;
+  if (m <= 0) return;
   uint32_t ta = static_cast<uint32_t>(a * 4294967296.0);
   uint32_t tab = static_cast<uint32_t>((a + b) * 4294967296.0);
   double abc = a + b + c;
@@ -593,11 +599,51 @@ void generate_rmat(gbx_graph* g, int scale, int ef, double a, double b, double c
   uint64_t st = gen_stream(seed, 0);
   uint64_t mask = (1ull << scale) - 1;
   uint64_t add = gen_stream(seed, 1) & mask;
-  Tmp<uint64_t> keys(mk, s);
   k_rmat<<<ceil_div(m, 256), 256, 0, s>>>(scale, m, ta, tab, tabc, st, scramble, add,
-                                           sym ? 1 : 0, keys.p);
+                                           sym ? 1 : 0, keys, e0);
   GBX_LAUNCHED();
+}
+
+void generate_rmat(gbx_graph* g, int scale, int ef, double a, double b, double c,
+                   uint64_t seed, int scramble, int kind) {
+  rmat_check(scale, ef, a, b, c);
+  cudaStream_t s = g->stream;
+  int64_t n = int64_t(1) << scale;
+  int64_t m = int64_t(ef) << scale;
+  bool sym = kind == GBX_UNDIRECTED;
+  int64_t mk = sym ? 2 * m : m;
+  Tmp<uint64_t> keys(mk, s);
+  rmat_keys(s, scale, ef, a, b, c, seed, scramble, sym, 0, m, keys.p);
   keys_to_graph(g, n, scale, keys.p, nullptr, mk, kind);
+}
+
+// sorted (row << bits | col) keys, drop keys (1 << 2*bits) last -> CSR over n
+// rows with duplicates removed (pattern)
+void csr_from_keys_unique(cudaStream_t s, int64_t n, int bits, const uint64_t* sorted, int64_t m,
+                          Csr& A) {
+  const uint64_t drop = uint64_t(1) << (2 * bits);
+  int64_t nnz = 0;
+  Tmp<uint64_t> uk(std::max<int64_t>(m, 1), s);
+  if (m > 0) {
+    Tmp<uint8_t> flag(m, s);
+    k_run_heads<<<ceil_div(m, 256), 256, 0, s>>>(sorted, nullptr, m, drop, flag.p, nullptr);
+    GBX_LAUNCHED();
+    Tmp<int64_t> nsel(1, s);
+    size_t tb = 0;
+    GBX_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, sorted, flag.p, uk.p, nsel.p, m, s));
+    Tmp<uint8_t> t(tb, s);
+    GBX_CUDA(cub::DeviceSelect::Flagged(t.p, tb, sorted, flag.p, uk.p, nsel.p, m, s));
+    GBX_CUDA(cudaMemcpyAsync(&nnz, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+  }
+  A.n = n;
+  A.nnz = nnz;
+  A.domain = GBX_BOOL;
+  A.rp.alloc(n + 1);
+  A.col.alloc(std::max<int64_t>(nnz, 1));
+  A.val.release();
+  rowptr_from_sorted_keys(s, n, bits, uk.p, nnz, A.rp.p, A.col.p);
+  GBX_CUDA(cudaStreamSynchronize(s));
 }
 
 void generate_er(gbx_graph* g, int logn, int degree, uint64_t seed, int weighted) {

@@ -1135,31 +1135,31 @@ __global__ void k_pr_pad_cols(int32_t* col, int64_t nnz, const int64_t* bounds, 
   if (p < nnz) col[p] = static_cast<int32_t>(pr_pad_index(bounds, nranks, chunk, col[p]));
 }
 
-void pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* rb_out, int64_t* re_out) {
-  require_at(g, "pr_shard");
-  require_rowdeg(g, "pr_shard");
-  if (nranks < 1 || rank < 0 || rank >= nranks)
-    fail(GBX_INVALID_VALUE, "pr_shard: bad rank / nranks");
-  auto S = std::make_unique<PrShard>();
-  PrPlan& P = S->plan;
-  build_relabeled(g, P);
-  std::vector<int64_t> rp(P.n + 1);
-  GBX_CUDA(cudaMemcpyAsync(rp.data(), P.trp.p, (P.n + 1) * 8, cudaMemcpyDeviceToHost, g->stream));
-  GBX_CUDA(cudaStreamSynchronize(g->stream));
+// row blocks of the relabeled AT balanced by rows + nnz (merge-path split of
+// the row-pointer prefix rp[0..n]); every rank computes the same bounds
+std::vector<int64_t> pr_bounds(const int64_t* rp, int64_t n, int64_t nnz, int nranks) {
   auto split = [&](int q) -> int64_t {
     if (q <= 0) return 0;
-    if (q >= nranks) return P.n;
-    const int64_t target = (P.n + P.nnz) * q / nranks;
-    int64_t lo = 0, hi = P.n;
+    if (q >= nranks) return n;
+    const int64_t target = (n + nnz) * q / nranks;
+    int64_t lo = 0, hi = n;
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
       if (mid + rp[mid] < target) lo = mid + 1; else hi = mid;
     }
     return lo;
   };
-  // every rank computes the same bounds from the same relabeled AT
-  S->bounds.assign(nranks + 1, 0);
-  for (int q = 1; q <= nranks; ++q) S->bounds[q] = std::max(S->bounds[q - 1], split(q));
+  std::vector<int64_t> bounds(nranks + 1, 0);
+  for (int q = 1; q <= nranks; ++q) bounds[q] = std::max(bounds[q - 1], split(q));
+  return bounds;
+}
+
+// the padded exchange layout + this rank's plan over its rows
+static void pr_shard_finish(gbx_graph* g, std::unique_ptr<PrShard> S, int rank, int nranks,
+                            const std::vector<int64_t>& bounds, int64_t* rb_out,
+                            int64_t* re_out) {
+  PrPlan& P = S->plan;
+  S->bounds = bounds;
   // slot = the longest block rounded up to even + 2 floats: the slot's last
   // 8 bytes carry the rank's fp64 L1 partial, so ONE all-gather per
   // iteration moves both the contributions and every partial
@@ -1185,6 +1185,39 @@ void pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* rb_out, int64
   g->prs = std::move(S);
   if (rb_out) *rb_out = rb;
   if (re_out) *re_out = re;
+}
+
+void pr_shard_prepare(gbx_graph* g, int rank, int nranks, int64_t* rb_out, int64_t* re_out) {
+  require_at(g, "pr_shard");
+  require_rowdeg(g, "pr_shard");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    fail(GBX_INVALID_VALUE, "pr_shard: bad rank / nranks");
+  auto S = std::make_unique<PrShard>();
+  PrPlan& P = S->plan;
+  build_relabeled(g, P);
+  std::vector<int64_t> rp(P.n + 1);
+  GBX_CUDA(cudaMemcpyAsync(rp.data(), P.trp.p, (P.n + 1) * 8, cudaMemcpyDeviceToHost, g->stream));
+  GBX_CUDA(cudaStreamSynchronize(g->stream));
+  // every rank computes the same bounds from the same relabeled AT
+  const std::vector<int64_t> bounds = pr_bounds(rp.data(), P.n, P.nnz, nranks);
+  pr_shard_finish(g, std::move(S), rank, nranks, bounds, rb_out, re_out);
+}
+
+// A shard from this rank's block of the RELABELED AT built by the distributed
+// graph (mg.cu): rows [bounds[rank], bounds[rank+1]) of an n-row CSR whose
+// other rows are empty, columns in new ids; deg = relabeled out-degree (n),
+// new2old = the relabeling -- both identical on every rank.
+void pr_shard_from_block(gbx_graph* g, int rank, int nranks, Csr& block, DevArray<int32_t>& deg,
+                         DevArray<int32_t>& new2old, const std::vector<int64_t>& bounds) {
+  auto S = std::make_unique<PrShard>();
+  PrPlan& P = S->plan;
+  P.n = block.n;
+  P.nnz = block.nnz;
+  P.trp = std::move(block.rp);
+  P.tcol = std::move(block.col);
+  P.deg = std::move(deg);
+  P.new2old = std::move(new2old);
+  pr_shard_finish(g, std::move(S), rank, nranks, bounds, nullptr, nullptr);
 }
 
 void pr_shard_layout(gbx_graph* g, int64_t* chunk, int64_t* bounds) {

@@ -452,19 +452,10 @@ __global__ void k_item_fill(const int64_t* off, int64_t n, int64_t* items) {
   for (int64_t c = 0; c < off[j + 1] - off[j]; ++c) items[off[j] + c] = (j << 32) | c;
 }
 
-void tc_prepare(gbx_graph* g) {
-  if (g->tc) return;
-  cudaStream_t s = g->stream;
-  const Csr& A = g->A;
-  const int64_t n = A.n;
-  auto P = std::make_unique<TcPlan>();
-  P->n = n;
-  DevArray<int32_t> deg_tmp;
-  const int32_t* deg = g->has_rowdeg ? g->rowdeg.p : nullptr;
-  if (!deg) {
-    compute_degrees(s, A, deg_tmp, true);
-    deg = deg_tmp.p;
-  }
+// U keys (rank(i) << bits | rank(j)) for every entry pointing up in rank
+// (the rest: drop keys); rank = stable ascending (degree, id) order
+void tc_upper_keys(cudaStream_t s, const Csr& A, const int32_t* deg, int64_t n, int bits,
+                   uint64_t* keys) {
   DevArray<int32_t> perm, rank, rowid;
   sort_ids_by_key(s, deg, n, true, perm);
   rank.alloc(std::max<int64_t>(n, 1));
@@ -473,19 +464,47 @@ void tc_prepare(gbx_graph* g) {
     GBX_LAUNCHED();
   }
   perm.release();
+  const int64_t m = A.nnz;
+  if (m) {
+    expand_rows(s, A, rowid);
+    k_upper_keys<<<ceil_div(m, 256), 256, 0, s>>>(rowid.p, A.col.p, rank.p, m, bits, keys);
+    GBX_LAUNCHED();
+  }
+  GBX_CUDA(cudaStreamSynchronize(s));
+}
+
+void tc_plan_from_upper(gbx_graph* g, int64_t n, int bits, const uint64_t* sorted, int64_t unnz,
+                        uint64_t* scratch, uint64_t* scratch2);
+
+void tc_prepare(gbx_graph* g) {
+  if (g->tc) return;
+  cudaStream_t s = g->stream;
+  const Csr& A = g->A;
+  const int64_t n = A.n;
+  DevArray<int32_t> deg_tmp;
+  const int32_t* deg = g->has_rowdeg ? g->rowdeg.p : nullptr;
+  if (!deg) {
+    compute_degrees(s, A, deg_tmp, true);
+    deg = deg_tmp.p;
+  }
   const int bits = bits_for(std::max<int64_t>(n, 2));
   int64_t m = A.nnz;
   DevArray<uint64_t> k0(std::max<int64_t>(m, 1)), k1(std::max<int64_t>(m, 1));
-  if (m) {
-    expand_rows(s, A, rowid);
-    k_upper_keys<<<ceil_div(m, 256), 256, 0, s>>>(rowid.p, A.col.p, rank.p, m, bits, k0.p);
-    GBX_LAUNCHED();
-    rowid.release();
-  }
+  tc_upper_keys(s, A, deg, n, bits, k0.p);
   uint64_t* sorted = m ? sort_keys(s, k0.p, k1.p, m, 2 * bits + 1) : k0.p;
   // the graph is symmetric and loop-free (checked by the caller): exactly half
   // of the entries point up in rank
-  const int64_t unnz = m / 2;
+  tc_plan_from_upper(g, n, bits, sorted, m / 2, sorted == k0.p ? k1.p : k0.p,
+                     const_cast<uint64_t*>(sorted));
+}
+
+// the plan from U's sorted keys (unnz of them); scratch, scratch2: buffers of
+// >= unnz keys (scratch2 may be `sorted` itself: it is consumed first)
+void tc_plan_from_upper(gbx_graph* g, int64_t n, int bits, const uint64_t* sorted, int64_t unnz,
+                        uint64_t* scratch, uint64_t* scratch2) {
+  cudaStream_t s = g->stream;
+  auto P = std::make_unique<TcPlan>();
+  P->n = n;
   if (unnz >= (int64_t(1) << 31) - 1)
     fail(GBX_UNSUPPORTED, "triangle_count: nnz(U) >= 2^31 is not supported (32-bit offsets)");
   csr_from_sorted_keys(s, n, bits, sorted, unnz, P->urp, P->ucol);
@@ -493,14 +512,13 @@ void tc_prepare(gbx_graph* g) {
   // L = U' as tails into U, sorted by middle vertex j
   {
     DevArray<int32_t> rowu(std::max<int64_t>(unnz, 1)), lcol;
-    uint64_t* lk = k0.p == sorted ? k1.p : k0.p;
-    uint64_t* la = k0.p == sorted ? k0.p : k1.p;
+    uint64_t* lk = scratch;
     if (unnz) {
       k_u_rows<<<device_sms() * 8, 256, 0, s>>>(P->urp.p, n, rowu.p);
       k_l_keys<<<ceil_div(unnz, 256), 256, 0, s>>>(P->ucol.p, unnz, lk);
       GBX_LAUNCHED();
     }
-    uint64_t* ls = unnz ? sort_keys(s, lk, la, unnz, bits + 31) : lk;
+    uint64_t* ls = unnz ? sort_keys(s, lk, scratch2, unnz, bits + 31) : lk;
     csr_from_sorted_keys(s, n, 31, ls, unnz, P->lrp, lcol);
     P->tails.alloc(std::max<int64_t>(unnz, 1));
     if (unnz) {
@@ -508,8 +526,6 @@ void tc_prepare(gbx_graph* g) {
       GBX_LAUNCHED();
     }
   }
-  k0.release();
-  k1.release();
   // work items (warp kernel) and the CTA / global middle vertices
   {
     const int64_t n1 = std::max<int64_t>(n, 1);

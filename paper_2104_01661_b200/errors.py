@@ -30,6 +30,7 @@ class ErrCode(IntEnum):
     OutOfMemory = -31
     Unsupported = -32
     NullArgument = -33
+    CommError = -34
 
 
 class Error(RuntimeError):
