@@ -223,6 +223,12 @@ int gbx_triangle_count(uint64_t* count, const gbx_graph* g, int presort,
 int gbx_sssp(double* dist, const gbx_graph* g, uint64_t source, double delta,
              char msg[GBX_MSG_LEN]);
 /* algo::sssp_default_delta (sssp.cpp:114-120): max weight / 2, or 1. */
+/* Several sources of sssp_delta_stepping (gapbench runs one trial per source,
+ * gapbench.cpp:300-330) in one call: the traversals are queued back to back
+ * on the graph's stream with one host synchronisation at the end.
+ * dist: ns * n doubles, row b = sources[b] (as gbx_sssp), or NULL. */
+int gbx_sssp_batch(double* dist, const gbx_graph* g, const uint64_t* sources, uint64_t ns,
+                   double delta, char msg[GBX_MSG_LEN]);
 int gbx_sssp_default_delta(double* delta, const gbx_graph* g, char msg[GBX_MSG_LEN]);
 
 /* algo::betweenness_centrality (betweenness.cpp:11-86): batched Brandes,

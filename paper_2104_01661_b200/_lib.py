@@ -57,6 +57,7 @@ _SIGS = {
     "gbx_triangle_count": [_vp, _vp, _int, _u64],
     "gbx_sssp": [_vp, _vp, _u64, _dbl],
     "gbx_sssp_default_delta": [_vp, _vp],
+    "gbx_sssp_batch": [_vp, _vp, _vp, _u64, _dbl],
     "gbx_betweenness": [_vp, _vp, _vp, _u64],
     "gbx_connected_components": [_vp, _vp, _vp],
     "gbx_basic_bfs_push": [_vp, _vp, _vp, _u64],

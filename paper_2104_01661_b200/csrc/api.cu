@@ -590,6 +590,15 @@ int gbx_sssp(double* dist, const gbx_graph* gc, uint64_t source, double delta, c
   });
 }
 
+int gbx_sssp_batch(double* dist, const gbx_graph* gc, const uint64_t* sources, uint64_t ns,
+                   double delta, char* msg) {
+  return guard(msg, [&] {
+    gbx_graph* g = need(gc);
+    gbx::Scope sc(g);
+    gbx::sssp_batch_run(g, sources, ns, delta, dist);
+  });
+}
+
 int gbx_sssp_default_delta(double* delta, const gbx_graph* gc, char* msg) {
   return guard(msg, [&] {
     gbx_graph* g = need(gc);

@@ -720,6 +720,7 @@ static BcWork& ensure_work(gbx_graph* g) {
 }
 
 void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrality) {
+  NvtxRange nvtx_("gbx.bc");
   const int64_t n = g->A.n;
   for (uint64_t b = 0; b < ns; ++b)
     if (sources[b] >= static_cast<uint64_t>(n))
@@ -1149,6 +1150,7 @@ void bc_shard_begin(gbx_graph* g, const uint64_t* sources, uint64_t ns, int rank
 // one forward depth on the owned rows; *recs = device records of the owned
 // vertices it settled (valid until the next protocol call)
 void bc_shard_forward(gbx_graph* g, void** recs, int64_t* nrec) {
+  NvtxRange nvtx_("gbx.bc.shard_forward");
   BcShard& S = need_shard(g);
   BcWork& W = *g->bc;
   *recs = S.recs.p;
@@ -1244,6 +1246,7 @@ void bc_shard_forward_apply(gbx_graph* g, const void* recs, int64_t nrec, int* d
 // one backward depth on the owned part of the level list; *done = 1 (and no
 // records) once depth 1 has been processed
 void bc_shard_backward(gbx_graph* g, void** recs, int64_t* nrec, int* done) {
+  NvtxRange nvtx_("gbx.bc.shard_backward");
   BcShard& S = need_shard(g);
   BcWork& W = *g->bc;
   if (!S.fwd_done) fail(GBX_PRECONDITION_VIOLATED, "bc_shard_backward before the forward sweep ended");

@@ -436,6 +436,7 @@ static void copy_out_i64(cudaStream_t s, const int32_t* dev, int64_t n, int32_t 
 
 void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor,
              bool use_at, int64_t* parent, int64_t* level) {
+  NvtxRange nvtx_("gbx.bfs");
   const int64_t n = g->A.n;
   if (source >= static_cast<uint64_t>(n))
     fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(source) + " with n = " +
@@ -831,6 +832,7 @@ static void ensure_bfs64(gbx_graph* g) {
 
 void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* parent,
                    int64_t* level) {
+  NvtxRange nvtx_("gbx.bfs.batch64");
   require_at(g, "bfs_batch");
   const int64_t n = g->A.n;
   if (ns == 0) fail(GBX_EMPTY_BATCH, "empty source batch");
@@ -1080,6 +1082,7 @@ void bfs_shard_begin(gbx_graph* g, uint64_t source, int rank, int nranks, int64_
 // one level: pull the owned unvisited vertices against front (n bits, global);
 // next_slice = this rank's words [rb/32, ceil(re/32)) of the next frontier
 void bfs_shard_level(gbx_graph* g, const uint32_t* front, uint32_t* next_slice, int64_t* found) {
+  NvtxRange nvtx_("gbx.bfs.shard_level");
   BfsShard& S = need_bfs_shard(g);
   BfsWork& W = *g->bfs;
   cudaStream_t s = g->stream;

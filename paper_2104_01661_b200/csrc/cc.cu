@@ -64,6 +64,7 @@ __global__ void k_cc_out(const int32_t* p, int64_t n, int64_t* out) {
 }
 
 void cc_run(gbx_graph* g, int64_t* label, int* iters) {
+  NvtxRange nvtx_("gbx.connected_components");
   const int64_t n = g->A.n;
   if (!g->cc) g->cc = std::make_unique<CcWork>();
   CcWork& W = *g->cc;

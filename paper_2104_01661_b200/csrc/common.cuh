@@ -3,6 +3,7 @@
 
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <memory>
@@ -46,6 +47,7 @@ enum Opt : int {
   kOptPrL1WindowKb = 0,  // "pagerank.l1_window_kb": bytes of x gathered L1 evict_last
   kOptPrCarveout,        // "pagerank.carveout": % shared-memory carveout of the row kernels
   kOptPrHostLoop,        // "pagerank.host_loop": per-iteration launches (ncu captures)
+  kOptPrTrace,           // "pagerank.trace": per-phase %globaltimer means on stderr
   kOptP2pTimeoutMs,      // "p2p.timeout_ms": bound of the fused exchange's cross-rank spin
   kOptBfsAlpha,          // "bfs.alpha": push while frontier edges < nnz / alpha (0: reference rule)
   kOptBfs64PullDiv,      // "bfs64.pull_div"
@@ -55,6 +57,16 @@ enum Opt : int {
   kOptCount
 };
 int64_t option(Opt o);
+
+// NVTX range over a library call / phase (header-only NVTX 3: a no-op unless a
+// tool such as nsys or ncu --nvtx is attached), so a whole-process timeline
+// attributes device time to the algorithm phases.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr int kSMs = 148;  // B200; the runtime value is queried in device_sms()
 int device_sms();
@@ -298,6 +310,8 @@ void tc_upper_keys(cudaStream_t s, const Csr& A, const int32_t* deg, int64_t n, 
 void tc_plan_from_upper(gbx_graph* g, int64_t n, int bits, const uint64_t* sorted, int64_t unnz,
                         uint64_t* scratch, uint64_t* scratch2);
 void sssp_run(gbx_graph* g, uint64_t source, double delta, double* dist);
+void sssp_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double delta,
+                    double* out);
 double sssp_default_delta(gbx_graph* g);
 void sssp_prepare(gbx_graph* g);
 void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrality);

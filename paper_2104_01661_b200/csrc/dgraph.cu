@@ -149,6 +149,7 @@ std::vector<int64_t> layout(gbx_comm* c, const std::vector<KeyBlock>& keys, int6
 // sorted keys of every local rank -> the owner's sorted, de-duplicated CSR block
 void shuffle_to_blocks(gbx_comm* c, std::vector<KeyBlock>& keys, const std::vector<int64_t>& bounds,
                        int64_t n, int bits, std::vector<Csr*>& out) {
+  NvtxRange nvtx_("gbx.dgraph.shuffle");
   const int P = c->nranks, L = c->nlocal;
   std::vector<std::vector<int64_t>> cnt(L, std::vector<int64_t>(P, 0));
   std::vector<std::vector<int64_t>> soff(L, std::vector<int64_t>(P + 1, 0));
@@ -241,6 +242,7 @@ gbx_dgraph* dgraph_from_keys(gbx_comm* c, int64_t n, int bits, int kind, std::ve
 
 gbx_dgraph* dgraph_generate_rmat(gbx_comm* c, int scale, int ef, double a, double b, double cc,
                                  uint64_t seed, int scramble, int kind) {
+  NvtxRange nvtx_("gbx.dgraph.generate_rmat");
   if (kind != GBX_DIRECTED && kind != GBX_UNDIRECTED) fail(GBX_INVALID_VALUE, "rmat: unknown kind");
   if (scale < 1 || scale > 30) fail(GBX_INVALID_VALUE, "rmat: scale must be in [1,30]");
   if (ef < 1) fail(GBX_INVALID_VALUE, "rmat: edge factor must be >= 1");
@@ -264,6 +266,7 @@ gbx_dgraph* dgraph_generate_rmat(gbx_comm* c, int scale, int ef, double a, doubl
 gbx_dgraph* dgraph_from_blocks(gbx_comm* c, int64_t n, const int64_t* row_begin,
                                const int64_t* row_end, const int64_t* const* row_ptr,
                                const int32_t* const* col, int kind) {
+  NvtxRange nvtx_("gbx.dgraph.from_blocks");
   if (kind != GBX_DIRECTED && kind != GBX_UNDIRECTED) fail(GBX_INVALID_VALUE, "dgraph: unknown kind");
   if (n < 0 || n >= (int64_t(1) << 31)) fail(GBX_INVALID_VALUE, "dgraph: n out of range");
   if (!row_begin || !row_end || !row_ptr || !col) fail(GBX_NULL_ARGUMENT, "dgraph: NULL block array");

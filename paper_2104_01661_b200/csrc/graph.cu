@@ -103,6 +103,7 @@ __global__ void k_validate_cols(const int32_t* col, const uint8_t* head, int64_t
 
 void build_from_host(gbx_graph* g, int64_t n, const int64_t* rp, const int64_t* col64,
                      const int32_t* col32, const void* vals, int domain, int kind) {
+  NvtxRange nvtx_("gbx.graph_new");
   if (n < 0) fail(GBX_INVALID_MATRIX, "graph_new: negative dimension");
   if (n >= (int64_t(1) << 31) - 1)
     fail(GBX_UNSUPPORTED, "graph_new: n >= 2^31 is not supported by the int32 column layout");
@@ -269,6 +270,7 @@ __global__ void k_gather_transpose(const int64_t* perm, const int32_t* rowid, in
 // A is row-major with ascending rows, so the stable sort leaves every row of T
 // strictly ascending.  Row pointers come from the sorted keys' boundaries.
 void compute_transpose(cudaStream_t s, const Csr& A, Csr& T) {
+  NvtxRange nvtx_("gbx.property_at.transpose");
   T.n = A.n;
   T.nnz = A.nnz;
   T.domain = A.domain;
@@ -606,6 +608,7 @@ void rmat_keys(cudaStream_t s, int scale, int ef, double a, double b, double c, 
 
 void generate_rmat(gbx_graph* g, int scale, int ef, double a, double b, double c,
                    uint64_t seed, int scramble, int kind) {
+  NvtxRange nvtx_("gbx.generate_rmat");
   rmat_check(scale, ef, a, b, c);
   cudaStream_t s = g->stream;
   int64_t n = int64_t(1) << scale;
@@ -647,6 +650,7 @@ void csr_from_keys_unique(cudaStream_t s, int64_t n, int bits, const uint64_t* s
 }
 
 void generate_er(gbx_graph* g, int logn, int degree, uint64_t seed, int weighted) {
+  NvtxRange nvtx_("gbx.generate_er");
   if (logn < 1 || logn > 30) fail(GBX_INVALID_VALUE, "er: logn must be in [1,30]");
   if (degree < 1) fail(GBX_INVALID_VALUE, "er: degree must be >= 1");
   cudaStream_t s = g->stream;

@@ -957,6 +957,7 @@ void write_mm(const HostCsr& h, Out& o, bool symmetric) {
 
 void graph_read(gbx_graph* g, const char* path, const void* data, size_t len, const char* format,
                 int kind) {
+  NvtxRange nvtx_("gbx.graph_read");
   if (!format) fail(GBX_NULL_ARGUMENT, "format is NULL");
   const std::string fmt(format);
   if (fmt != "bin" && fmt != "mm") fail(GBX_INVALID_VALUE, "unknown format '" + fmt + "'");

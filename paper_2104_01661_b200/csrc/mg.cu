@@ -142,6 +142,7 @@ void gather_rows_i64(gbx_dgraph* D, const std::vector<std::vector<int64_t>>& sli
 
 // the relabeled AT row blocks and the shard plans (cached on the shards)
 void pr_mg_prepare(gbx_dgraph* D) {
+  NvtxRange nvtx_("gbx.pagerank_mg.prepare");
   gbx_comm* c = D->comm;
   const int L = c->nlocal, P = c->nranks;
   bool ready = true;
@@ -229,6 +230,7 @@ void pr_mg_prepare(gbx_dgraph* D) {
 
 // the fused run (peer stores + device barrier); false when any rank failed
 bool pr_mg_p2p(gbx_dgraph* D, PrMgState& S, double damping, double tol, int itermax, int* iters) {
+  NvtxRange nvtx_("gbx.pagerank_mg.fused_run");
   gbx_comm* c = D->comm;
   const int L = c->nlocal, P = c->nranks;
   int ok = 1;
@@ -289,6 +291,7 @@ bool pr_mg_p2p(gbx_dgraph* D, PrMgState& S, double damping, double tol, int iter
 
 // one NCCL all-gather of the padded x slices (+ L1 partials) per iteration
 void pr_mg_nccl(gbx_dgraph* D, PrMgState& S, double damping, double tol, int itermax, int* iters) {
+  NvtxRange nvtx_("gbx.pagerank_mg.nccl_run");
   gbx_comm* c = D->comm;
   const int L = c->nlocal, P = c->nranks;
   const int64_t chunk = S.chunk;
@@ -340,6 +343,7 @@ void pr_mg_nccl(gbx_dgraph* D, PrMgState& S, double damping, double tol, int ite
 
 void pagerank_mg(gbx_dgraph* D, double damping, double tol, int itermax, int exchange,
                  double* rank, int* iters) {
+  NvtxRange nvtx_("gbx.pagerank_mg");
   gbx_comm* c = D->comm;
   CommLock lk(c);
   if (!(damping > 0.0)) fail(GBX_NON_POSITIVE_DAMPING, "damping must be positive");
@@ -402,6 +406,7 @@ void pagerank_mg(gbx_dgraph* D, double damping, double tol, int itermax, int exc
 // ---- triangle count ------------------------------------------------------------------
 
 uint64_t triangle_count_mg(gbx_dgraph* D) {
+  NvtxRange nvtx_("gbx.triangle_count_mg");
   gbx_comm* c = D->comm;
   CommLock lk(c);
   if (D->kind != GBX_UNDIRECTED)
@@ -491,6 +496,7 @@ uint64_t triangle_count_mg(gbx_dgraph* D) {
 // ---- BFS ------------------------------------------------------------------------------
 
 void bfs_mg(gbx_dgraph* D, uint64_t source, int64_t* parent, int64_t* level) {
+  NvtxRange nvtx_("gbx.bfs_mg");
   gbx_comm* c = D->comm;
   CommLock lk(c);
   const int L = c->nlocal, P = c->nranks;
@@ -555,6 +561,7 @@ void bfs_mg(gbx_dgraph* D, uint64_t source, int64_t* parent, int64_t* level) {
 // ---- betweenness -------------------------------------------------------------------
 
 void betweenness_mg(gbx_dgraph* D, const uint64_t* sources, uint64_t ns, double* centrality) {
+  NvtxRange nvtx_("gbx.betweenness_mg");
   gbx_comm* c = D->comm;
   CommLock lk(c);
   const int L = c->nlocal, P = c->nranks;

@@ -49,8 +49,8 @@ void result_device(const gbx_graph* g, const std::string& w, void** ptr, int64_t
     *ptr = g->cc->parent.p;
     *count = g->A.n;
   } else if (w == "sssp" && g->sssp) {
-    *ptr = g->sssp->integral ? static_cast<void*>(g->sssp->dist32.p)
-                             : static_cast<void*>(g->sssp->dist64.p);
+    *ptr = g->sssp->integral ? static_cast<void*>(g->sssp->lanes[0]->dist32.p)
+                             : static_cast<void*>(g->sssp->lanes[0]->dist64.p);
     *count = g->A.n;
   } else if (w == "bc" && g->bc) {
     *ptr = g->bc->cent.p;

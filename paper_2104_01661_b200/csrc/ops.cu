@@ -737,16 +737,19 @@ void mat_export(gbx_mat* M, int64_t* rp, int64_t* col, void* vals) {
 
 void mxv_op(int64_t* w_idx, void* w_vals, int64_t* w_nvals, const gbx_vec* w, const gbx_desc* d,
             int sr, int sdom, gbx_mat* A, const gbx_vec* u) {
+  NvtxRange nvtx_("gbx.mxv");
   vec_op(w_idx, w_vals, w_nvals, w, d, sr, sdom, A, u, false);
 }
 void vxm_op(int64_t* w_idx, void* w_vals, int64_t* w_nvals, const gbx_vec* w, const gbx_desc* d,
             int sr, int sdom, const gbx_vec* u, gbx_mat* A) {
+  NvtxRange nvtx_("gbx.vxm");
   vec_op(w_idx, w_vals, w_nvals, w, d, sr, sdom, A, u, true);
 }
 
 // C_out = post_step(C, T = A ⊕.⊗ B) (mxm, core.cpp:267-306)
 void mxm_op(gbx_mat* out, gbx_mat* C, const gbx_desc* desc, int sr, int sdom, gbx_mat* A,
             gbx_mat* B) {
+  NvtxRange nvtx_("gbx.mxm");
   check_domain(sdom);
   const Sr s = semiring_of(sr, sdom);
   const gbx_desc d0{};

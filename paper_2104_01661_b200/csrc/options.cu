@@ -20,6 +20,7 @@ constexpr OptDef kDefs[kOptCount] = {
     {"pagerank.l1_window_kb", 144, 0, 1 << 20},   // 64..208 KB swept: 144 best (205.9 us/iter)
     {"pagerank.carveout", 10, -1, 100},           // 10% -> 32 KB smem, 224 KB L1 (-1: driver)
     {"pagerank.host_loop", 0, 0, 1},
+    {"pagerank.trace", 0, 0, 1},
     {"p2p.timeout_ms", 10000, 1, 3600 * 1000},
     {"bfs.alpha", 14, 0, 1 << 20},
     {"bfs64.pull_div", 2, 1, 1 << 20},

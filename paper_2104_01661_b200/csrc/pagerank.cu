@@ -53,7 +53,10 @@ constexpr int kPrIpl = GBX_PR_IPL;  // chunk walks: independent gathers in fligh
 #define GBX_PR_B0IPL 2  // measured: 2 and 4 within 1%, 8 slower (registers)
 #endif
 constexpr int kPrB0Ipl = GBX_PR_B0IPL;  // gathers per lane per step in warp-per-row units
-constexpr int64_t kPrLong = 1024;   // rows longer than this are chunked
+#ifndef GBX_PR_LONG
+#define GBX_PR_LONG 1024
+#endif
+constexpr int64_t kPrLong = GBX_PR_LONG;  // rows longer than this are chunked
 constexpr int64_t kPrShort = 32;    // rows up to this length: thread per row, exact-length bins
 constexpr int64_t kPrChunk = 2048;  // nonzeros per chunk unit
 constexpr unsigned kWarp = 0xffffffffu;
@@ -82,7 +85,8 @@ struct PrArgs {
   double* l1_fin;      // [gridB]
   double* l1_hist;
   int* ctl;            // [0] completed iterations [1] done [2] peer timeout (fused exchange)
-  unsigned long long* ktime;  // [128][2]: per iteration, min CTA start / max CTA end (%globaltimer)
+  unsigned long long* ktime;  // [128][8]: per iteration, min CTA start / max CTA end of the row phase (%globaltimer); trace: [2] min after barrier 1, [3] max finish end, [4] min after barrier 2, [5] max fold end
+  int trace;
   unsigned* fin_cnt;
   int64_t l1hot;       // x[0, l1hot) gathered with L1 evict_last, the rest no_allocate
   int64_t row0;        // first row of this plan (shards); outputs indexed row - row0
@@ -326,11 +330,11 @@ __global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_rows(PrArgs<V> a
   __shared__ PrBin s_bins[kPrBinsMax];
   if (!a.fixed && *(volatile int*)&a.ctl[1]) return;  // converged (host-looped path)
   const int k = *(volatile int*)&a.ctl[0];
-  if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 2], pr_gtimer());
+  if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 8], pr_gtimer());
   const double blk = pr_rows_phase<V>(a, k, blockIdx.x, gridDim.x, red, s_bins);
   if (threadIdx.x == 0) {
     a.l1_rows[blockIdx.x] = blk;
-    if (a.ktime) atomicMax(&a.ktime[(k % 128) * 2 + 1], pr_gtimer());
+    if (a.ktime) atomicMax(&a.ktime[(k % 128) * 8 + 1], pr_gtimer());
   }
 }
 
@@ -355,23 +359,27 @@ __global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist(PrArgs<V
   __shared__ int s_stop;
   const int ncta = gridDim.x;
   for (int k = 0;; ++k) {
-    double* l1_rows = a.l1_rows + (k & 1) * ncta;
-    if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 2], pr_gtimer());
+    // the CTA's L1 partial (rows + long rows) of iteration k, by parity
+    double* l1_part = a.l1_rows + (k & 1) * ncta;
+    if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 8], pr_gtimer());
     const double blk = pr_rows_phase<V>(a, k, blockIdx.x, ncta, red, s_bins);
+    if (threadIdx.x == 0 && a.ktime) atomicMax(&a.ktime[(k % 128) * 8 + 1], pr_gtimer());
+    grid.sync();
+    unsigned long long* kt = a.ktime + (k % 128) * 8;
+    if (a.trace && threadIdx.x == 0) atomicMin(kt + 2, pr_gtimer());
+    const double blk2 = pr_long_phase<V>(a, k, blockIdx.x, ncta, red);
     if (threadIdx.x == 0) {
-      l1_rows[blockIdx.x] = blk;
-      if (a.ktime) atomicMax(&a.ktime[(k % 128) * 2 + 1], pr_gtimer());
+      l1_part[blockIdx.x] = blk + blk2;
+      if (a.trace) atomicMax(kt + 3, pr_gtimer());
     }
     grid.sync();
-    const double blk2 = pr_long_phase<V>(a, k, blockIdx.x, ncta, red);
-    if (threadIdx.x == 0) a.l1_fin[blockIdx.x] = blk2;
-    grid.sync();
+    if (a.trace && threadIdx.x == 0) atomicMin(kt + 4, pr_gtimer());
     // every CTA: all partials in a fixed order -> the same total everywhere
     double part = 0.0;
-    for (int b = threadIdx.x; b < ncta; b += kPrThreads)
-      part += __ldcg(&l1_rows[b]) + __ldcg(&a.l1_fin[b]);
+    for (int b = threadIdx.x; b < ncta; b += kPrThreads) part += __ldcg(&l1_part[b]);
     __syncthreads();
     const double tot = BlockReduce(red).Sum(part);
+    if (a.trace && threadIdx.x == 0) atomicMax(kt + 5, pr_gtimer());
     if (threadIdx.x == 0) {
       const bool stop = !(tot >= a.tol) || (k + 1 >= a.itermax);
       s_stop = stop;
@@ -423,11 +431,11 @@ __device__ __forceinline__ void pr_p2p_body(const PrArgs<float>& a, const PrP2p&
                                             PrBin* s_bins, int& s_stop) {
   using BlockReduce = cub::BlockReduce<double, kPrThreads>;
   for (int k = 0;; ++k) {
-    if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 2], pr_gtimer());
+    if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 8], pr_gtimer());
     const double blk = pr_rows_phase<float>(a, k, cta, ncta, red, s_bins);
     if (threadIdx.x == 0) {
       a.l1_rows[cta] = blk;
-      if (a.ktime) atomicMax(&a.ktime[(k % 128) * 2 + 1], pr_gtimer());
+      if (a.ktime) atomicMax(&a.ktime[(k % 128) * 8 + 1], pr_gtimer());
     }
     grid.sync();
     const double blk2 = pr_long_phase<float>(a, k, cta, ncta, red);
@@ -551,8 +559,14 @@ __global__ void k_pr_inv(float* inv, const int32_t* outdeg, int64_t n, double da
 }
 
 template <typename V>
-__global__ void k_pr_init(V* r, V* x, V* inv, const int32_t* outdeg, int64_t n, double damping) {
+__global__ void k_pr_init(V* r, V* x, V* inv, const int32_t* outdeg, int64_t n, double damping,
+                          int* ctl, unsigned* fin_cnt, unsigned long long* ktime) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  // the run's control words and launch-span table (one kernel instead of
+  // three memsets / resets before the persistent launch)
+  if (i < 4) ctl[i] = 0;
+  if (i == 0) *fin_cnt = 0;
+  if (ktime && i < 128 * 8) ktime[i] = (i & 1) ? 0ull : ~0ull;
   if (i >= n) return;
   const double r0 = 1.0 / static_cast<double>(n);
   r[i] = static_cast<V>(r0);
@@ -563,11 +577,14 @@ __global__ void k_pr_init(V* r, V* x, V* inv, const int32_t* outdeg, int64_t n, 
   inv[i] = dg > 0 ? static_cast<V>(damping / static_cast<double>(dg)) : V(0);
 }
 
-// relabeled rank -> original ids (fp64 for the host copy)
+// relabeled rank -> original ids (fp64 for the host copy); the buffer holding
+// the last iterate is chosen on the device from the completed-iteration count,
+// so the launch is queued before the host reads anything back
 template <typename V>
-__global__ void k_pr_unpermute(const V* r, const int32_t* new2old, int64_t n, double* out) {
+__global__ void k_pr_unpermute(const V* r0, const V* r1, const int* ctl, const int32_t* new2old,
+                               int64_t n, double* out) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < n) out[new2old[i]] = static_cast<double>(r[i]);
+  if (i < n) out[new2old[i]] = static_cast<double>((ctl[0] & 1) ? r1[i] : r0[i]);
 }
 
 // ---- plan -------------------------------------------------------------------------
@@ -882,12 +899,13 @@ static void plan_rows(gbx_graph* g, PrPlan& P, int64_t row0, int64_t row1) {
   P.l1_block.alloc(static_cast<size_t>(device_sms()) * 32);
   P.l1_fin.alloc(std::max<int64_t>(P.grid_fin, static_cast<int64_t>(device_sms()) * 32));
   P.l1_hist.alloc(128);
-  P.ktime.alloc(256);
+  P.ktime.alloc(128 * 8);
   P.ctl.alloc(4);
   P.blk_cnt.alloc(1);
 }
 
 void pagerank_prepare(gbx_graph* g) {
+  NvtxRange nvtx_("gbx.pagerank.prepare");
   require_at(g, "pagerank_gap");
   require_rowdeg(g, "pagerank_gap");
   if (g->pr) return;
@@ -984,6 +1002,7 @@ static PrArgs<V> make_args(PrPlan& P, double damping, double tol, int itermax) {
   a.l1_hist = P.l1_hist.p;
   a.ctl = P.ctl.p;
   a.ktime = P.ktime.p;
+  a.trace = static_cast<int>(option(kOptPrTrace));
   a.fin_cnt = P.blk_cnt.p;
   a.row0 = 0;
   a.l1hot = std::min<int64_t>(P.n, l1_hot_bytes() / static_cast<int64_t>(sizeof(V)));
@@ -998,7 +1017,7 @@ static PrArgs<V> make_args(PrPlan& P, double damping, double tol, int itermax) {
 
 __global__ void k_pr_ktime_reset(unsigned long long* t) {
   const int i = threadIdx.x;
-  if (i < 256) t[i] = (i & 1) ? 0ull : ~0ull;
+  for (int j = i; j < 128 * 8; j += blockDim.x) t[j] = (j & 1) ? 0ull : ~0ull;
 }
 
 static void reset_state(cudaStream_t s, PrPlan& P) {
@@ -1022,10 +1041,10 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
                          double* rank, int* iters) {
   const int64_t n = g->A.n;
   cudaStream_t s = g->stream;
-  reset_state(s, P);
   P.last_persist = false;
-  k_pr_init<V><<<ceil_div(n, 256), 256, 0, s>>>(buf_r<V>(P, 0), buf_x<V>(P, 0), buf_inv<V>(P),
-                                                P.deg.p, n, damping);
+  k_pr_init<V><<<ceil_div(std::max<int64_t>(n, 128 * 8), 256), 256, 0, s>>>(
+      buf_r<V>(P, 0), buf_x<V>(P, 0), buf_inv<V>(P), P.deg.p, n, damping, P.ctl.p, P.blk_cnt.p,
+      P.ktime.p);
   GBX_LAUNCHED();
   PrArgs<V> pa{};
   if (!option(kOptPrHostLoop) && persist_args<V>(P, damping, tol, itermax, pa)) {
@@ -1050,10 +1069,15 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
       GBX_CUDA(cudaStreamSynchronize(s));
     }
   }
+  // ranks back in original vertex order (device-resident result; fp64),
+  // queued behind the run before the host reads the counters back
+  k_pr_unpermute<V><<<ceil_div(n, 256), 256, 0, s>>>(buf_r<V>(P, 0), buf_r<V>(P, 1), P.ctl.p,
+                                                       P.new2old.p, n, P.out.p);
+  GBX_LAUNCHED();
   int it = 0;
-  unsigned long long kt[256];
+  std::vector<unsigned long long> kt(128 * 8);
   GBX_CUDA(cudaMemcpyAsync(&it, P.ctl.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-  GBX_CUDA(cudaMemcpyAsync(kt, P.ktime.p, sizeof kt, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaMemcpyAsync(kt.data(), P.ktime.p, kt.size() * 8, cudaMemcpyDeviceToHost, s));
   GBX_CUDA(cudaStreamSynchronize(s));
   P.last_iters = it;
   {
@@ -1061,18 +1085,28 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
     // last CTA end, %globaltimer)
     double sum = 0.0;
     int cnt = 0;
-    for (int k = 0; k < std::min(it, 128); ++k)
-      if (kt[2 * k + 1] > kt[2 * k] && kt[2 * k] != ~0ull) {
-        sum += static_cast<double>(kt[2 * k + 1] - kt[2 * k]);
+    double ph[4] = {0, 0, 0, 0};
+    for (int k = 0; k < std::min(it, 128); ++k) {
+      const unsigned long long* t = &kt[8 * k];
+      if (t[1] > t[0] && t[0] != ~0ull) {
+        sum += static_cast<double>(t[1] - t[0]);
         ++cnt;
       }
+      if (option(kOptPrTrace) && P.last_persist && t[2] != ~0ull && t[4] != ~0ull) {
+        ph[0] += static_cast<double>(t[2] - t[1]);  // last row-phase CTA -> first past barrier 1
+        ph[1] += static_cast<double>(t[3] - t[2]);  // long-row finish
+        ph[2] += static_cast<double>(t[4] - t[3]);  // barrier 2
+        ph[3] += static_cast<double>(t[5] - t[4]);  // L1 fold
+      }
+    }
     P.last_rows_ms = cnt ? sum / cnt * 1e-6 : 0.0;
+    if (option(kOptPrTrace) && cnt)
+      std::fprintf(stderr, "pagerank trace: %d iterations, rows %.2f us, barrier1 %.2f us, finish "
+                           "%.2f us, barrier2 %.2f us, fold %.2f us (means)\n",
+                   it, sum / cnt * 1e-3, ph[0] / cnt * 1e-3, ph[1] / cnt * 1e-3,
+                   ph[2] / cnt * 1e-3, ph[3] / cnt * 1e-3);
   }
   if (iters) *iters = it;
-  // ranks back in original vertex order (device-resident result; fp64)
-  k_pr_unpermute<V><<<ceil_div(n, 256), 256, 0, s>>>(buf_r<V>(P, it & 1), P.new2old.p, n,
-                                                       P.out.p);
-  GBX_LAUNCHED();
   if (rank) {
     GBX_CUDA(cudaMemcpyAsync(rank, P.out.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     GBX_CUDA(cudaStreamSynchronize(s));
@@ -1082,6 +1116,7 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
 
 void pagerank_run(gbx_graph* g, double damping, double tol, int itermax, double* rank,
                   int* iters) {
+  NvtxRange nvtx_("gbx.pagerank");
   require_at(g, "pagerank_gap");
   require_rowdeg(g, "pagerank_gap");
   if (!(damping > 0.0)) fail(GBX_NON_POSITIVE_DAMPING, "damping must be positive");
@@ -1253,6 +1288,7 @@ void pr_shard_init(gbx_graph* g, float* x_full, float* r_local, double damping) 
 
 void pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, float* r_new,
                    float* x_slice, double* l1, double damping) {
+  NvtxRange nvtx_("gbx.pagerank.shard_step");
   if (!g->prs) fail(GBX_MISSING_PROPERTY, "pr_shard_step needs gbx_pr_shard_prepare");
   PrPlan& P = g->prs->plan;
   cudaStream_t s = g->stream;
@@ -1340,6 +1376,7 @@ static int p2p_finish(gbx_graph* g) {
 void pr_shard_run_p2p(gbx_graph* g, const uint64_t* x0_peers, const uint64_t* x1_peers,
                       const uint64_t* l1_peers, const uint64_t* sig_peers, float* r0, float* r1,
                       double damping, double tol, int itermax, int* iters) {
+  NvtxRange nvtx_("gbx.pagerank.fused_run");
   PrArgs<float> a{};
   PrP2p m{};
   p2p_rank_args(g, x0_peers, x1_peers, l1_peers, sig_peers, r0, r1, damping, tol, itermax, a, m);
@@ -1369,6 +1406,7 @@ void pr_shard_run_p2p_multi(gbx_graph* const* gs, int nv, const uint64_t* x0_pee
                             const uint64_t* x1_peers, const uint64_t* l1_peers,
                             const uint64_t* sig_peers, float* const* r0s, float* const* r1s,
                             double damping, double tol, int itermax, int* iters) {
+  NvtxRange nvtx_("gbx.pagerank.fused_run_multi");
   if (nv < 1 || nv > kPrMaxPeers) fail(GBX_INVALID_VALUE, "pr_shard_run_p2p_multi: 1..8 ranks");
   std::vector<PrArgs<float>> va(nv);
   std::vector<PrP2p> vm(nv);

@@ -121,16 +121,11 @@ struct TcPlan {
   DevArray<unsigned> next_row;
 };
 
-// SSSP plan (sssp.cu): packed (col:24 | w:8) edges when exact, else split.
-struct SsspPlan {
-  int64_t n = 0, nnz = 0;
-  bool packed = false;     // uint32 col<<8|w, n <= 2^24, integer w in [1,255]
-  bool integral = false;   // integer weights: uint32 distances
-  bool nonpositive = false; // some weight <= 0 (NonPositiveWeight on every call)
-  double max_w = 0;
-  DevArray<uint32_t> packed_edges;
-  DevArray<int32_t> wint;
-  DevArray<double> wdbl;
+// One SSSP traversal's workspace (sssp.cu): distances, near / far queues,
+// membership bits, circular buckets, control words.  Lane 0 runs on the
+// graph's stream; a batch (gbx_sssp_batch) runs several lanes concurrently,
+// each on its own stream with its share of the SMs.
+struct SsspLane {
   DevArray<uint32_t> dist32;
   DevArray<unsigned long long> dist64;
   DevArray<int32_t> q[2], far[2], stamp;
@@ -141,15 +136,36 @@ struct SsspPlan {
   DevArray<uint32_t> bbits;
   DevArray<int> bcnt;
   int nb_alloc = 0;
+  DevArray<int32_t> sq;            // settled list of the current bucket
+  DevArray<uint32_t> sbits;        // its membership bitmap
+  DevArray<double> out;            // fp64 copy of the distances for the host
+  cudaStream_t stream = nullptr;   // owned (lanes > 0)
+  ~SsspLane() {
+    if (stream) {
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+  }
+};
+
+// SSSP plan (sssp.cu): packed (col:24 | w:8) edges when exact, else split.
+struct SsspPlan {
+  int64_t n = 0, nnz = 0;
+  bool packed = false;     // uint32 col<<8|w, n <= 2^24, integer w in [1,255]
+  bool integral = false;   // integer weights: uint32 distances
+  bool nonpositive = false; // some weight <= 0 (NonPositiveWeight on every call)
+  double max_w = 0;
+  DevArray<uint32_t> packed_edges;
+  DevArray<int32_t> wint;
+  DevArray<double> wdbl;
   // light-first row partition for delta = split_delta (sssp.cu: k_split_*)
   double split_delta = -1.0;
   DevArray<int32_t> nlight, split_col, split_wi;
   DevArray<double> split_wd;
-  DevArray<int32_t> sq;            // settled list of the current bucket
-  DevArray<uint32_t> sbits;        // its membership bitmap
   // per-vertex edge ranges {begin, light end, end, 0} (nnz < 2^32): one 16-byte
   // load per popped vertex instead of row_ptr[u], row_ptr[u+1] and nlight[u]
   DevArray<uint4> vmeta;
+  std::vector<std::unique_ptr<SsspLane>> lanes;  // [0]: the single-source call's
 };
 
 // Row-partitioned batched Brandes (bc.cu, sharded protocol): this rank owns

@@ -870,8 +870,6 @@ static void ensure_split(gbx_graph* g, SsspPlan& P, double delta) {
   const Csr& A = g->A;
   const int64_t n = A.n, n1 = std::max<int64_t>(n, 1);
   P.nlight.alloc(n1);
-  if (!P.sq.p) P.sq.alloc(n1 + 1);
-  if (!P.sbits.p) P.sbits.alloc((n1 + 31) / 32);
   if (n > 0 && A.nnz > 0) {
     if (P.packed) {
       DevArray<uint32_t> out(A.nnz);
@@ -915,7 +913,32 @@ static void ensure_split(gbx_graph* g, SsspPlan& P, double delta) {
   P.split_delta = delta;
 }
 
+// lane i's workspace (lane 0 on the graph's stream, the others on their own)
+static SsspLane& ensure_lane(gbx_graph* g, SsspPlan& P, int i) {
+  while (static_cast<int>(P.lanes.size()) <= i) P.lanes.emplace_back();
+  if (P.lanes[i]) return *P.lanes[i];
+  auto L = std::make_unique<SsspLane>();
+  const int64_t n1 = std::max<int64_t>(P.n, 1);
+  if (P.integral) L->dist32.alloc(n1); else L->dist64.alloc(n1);
+  L->q[0].alloc(n1 + 1);
+  L->q[1].alloc(n1 + 1);
+  // far pile: every successful improvement above hi appends once
+  const int64_t fcap = P.n + 1;  // <= one entry per vertex per bucket epoch
+  L->far[0].alloc(fcap);
+  L->far[1].alloc(fcap);
+  L->stamp.alloc(4 * ((n1 + 31) / 32));  // 2 near + 2 far membership bitmaps
+  L->ctl.alloc(10);
+  L->lohi.alloc(3);
+  L->relax.alloc(1);
+  L->sq.alloc(n1 + 1);
+  L->sbits.alloc((n1 + 31) / 32);
+  if (i > 0) GBX_CUDA(cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking));
+  P.lanes[i] = std::move(L);
+  return *P.lanes[i];
+}
+
 void sssp_prepare(gbx_graph* g) {
+  NvtxRange nvtx_("gbx.sssp.prepare");
   if (g->sssp) return;
   const Csr& A = g->A;
   if (A.domain != GBX_FP64 && A.domain != GBX_INT32)
@@ -958,32 +981,24 @@ void sssp_prepare(gbx_graph* g) {
       }
     }
   }
-  const int64_t n1 = std::max<int64_t>(A.n, 1);
-  if (P->integral) P->dist32.alloc(n1); else P->dist64.alloc(n1);
-  P->q[0].alloc(n1 + 1);
-  P->q[1].alloc(n1 + 1);
-  // far pile: every successful improvement above hi appends once
-  const int64_t fcap = A.n + 1;  // <= one entry per vertex per bucket epoch
-  P->far[0].alloc(fcap);
-  P->far[1].alloc(fcap);
-  P->stamp.alloc(4 * ((n1 + 31) / 32));  // 2 near + 2 far membership bitmaps
-  P->ctl.alloc(10);
-  P->lohi.alloc(3);
-  P->relax.alloc(1);
   GBX_CUDA(cudaStreamSynchronize(s));
   g->sssp = std::move(P);
+  ensure_lane(g, *g->sssp, 0);
 }
 
+// one traversal on lane L (stream s) with 1/share of the resident grid;
+// persist: keep the distance array in the L2 persisting window (one lane only:
+// the set-aside is device-wide)
 template <typename D, typename E, typename W>
-static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src, double delta,
-                        D hi0, D inf, bool split) {
-  cudaStream_t s = g->stream;
+static void sssp_launch(gbx_graph* g, SsspPlan& P, SsspLane& L, cudaStream_t s, int share,
+                        bool persist, E edges, D* dist, int32_t src, double delta, D hi0, D inf,
+                        bool split) {
   const int64_t n = P.n;
-  D* lohi = reinterpret_cast<D*>(P.lohi.p);
-  uint32_t* bits = reinterpret_cast<uint32_t*>(P.stamp.p);
+  D* lohi = reinterpret_cast<D*>(L.lohi.p);
+  uint32_t* bits = reinterpret_cast<uint32_t*>(L.stamp.p);
   const int64_t words = (n + 31) / 32;
-  k_sssp_init<D><<<ceil_div(std::max<int64_t>(n, 4 * words), 256), 256, 0, s>>>(dist, bits, n, src, P.q[0].p, P.ctl.p,
-                                                   lohi, P.relax.p, hi0, inf);
+  k_sssp_init<D><<<ceil_div(std::max<int64_t>(n, 4 * words), 256), 256, 0, s>>>(dist, bits, n, src, L.q[0].p, L.ctl.p,
+                                                   lohi, L.relax.p, hi0, inf);
   GBX_LAUNCHED();
   SsspArgs<D, E> a{};
   a.rp = g->A.rp.p;
@@ -991,17 +1006,17 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
   a.n = n;
   a.delta = delta;
   a.dist = dist;
-  a.q0 = P.q[0].p;
-  a.q1 = P.q[1].p;
-  a.f0 = P.far[0].p;
-  a.f1 = P.far[1].p;
+  a.q0 = L.q[0].p;
+  a.q1 = L.q[1].p;
+  a.f0 = L.far[0].p;
+  a.f1 = L.far[1].p;
   a.qbits[0] = bits;
   a.qbits[1] = bits + words;
   a.fbits[0] = bits + 2 * words;
   a.fbits[1] = bits + 3 * words;
-  a.ctl = P.ctl.p;
+  a.ctl = L.ctl.p;
   a.lohi = lohi;
-  a.relax = P.relax.p;
+  a.relax = L.relax.p;
   // keep the distance array resident in L2 while the edges stream past it
   {
     int max_persist = 0;
@@ -1009,7 +1024,7 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     const size_t bytes = static_cast<size_t>(n) * sizeof(D);
     if (option(kOptSsspTrace))
       std::fprintf(stderr, "sssp: max persisting L2 %d bytes, dist %zu bytes\n", max_persist, bytes);
-    if (max_persist > 0) {
+    if (max_persist > 0 && persist) {
       // the set-aside is a device-wide setting (and costly to change): grow only
       static size_t set_aside[64] = {0};
       const size_t want = std::min<size_t>(bytes, max_persist);
@@ -1033,14 +1048,14 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
   while (nb < span && nb <= 64) nb <<= 1;
   if (nb <= 64) {
     const int64_t cap = n + 1;
-    if (static_cast<int>(P.bcnt.n) < nb || P.nb_alloc < nb) {
-      P.bq.alloc(static_cast<size_t>(nb) * cap);
-      P.bbits.alloc(static_cast<size_t>(nb) * std::max<int64_t>(words, 1));
-      P.bcnt.alloc(nb);
-      P.nb_alloc = nb;
+    if (static_cast<int>(L.bcnt.n) < nb || L.nb_alloc < nb) {
+      L.bq.alloc(static_cast<size_t>(nb) * cap);
+      L.bbits.alloc(static_cast<size_t>(nb) * std::max<int64_t>(words, 1));
+      L.bcnt.alloc(nb);
+      L.nb_alloc = nb;
     }
-    GBX_CUDA(cudaMemsetAsync(P.bbits.p, 0, P.bbits.bytes(), s));
-    GBX_CUDA(cudaMemsetAsync(P.bcnt.p, 0, P.bcnt.bytes(), s));
+    GBX_CUDA(cudaMemsetAsync(L.bbits.p, 0, L.bbits.bytes(), s));
+    GBX_CUDA(cudaMemsetAsync(L.bcnt.p, 0, L.bcnt.bytes(), s));
     SsspBArgs<D, E> b{};
     b.rp = a.rp;
     b.edges = edges;
@@ -1062,11 +1077,11 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     b.dist = dist;
     b.q0 = a.q0;
     b.q1 = a.q1;
-    b.bq = P.bq.p;
-    b.bcnt = P.bcnt.p;
+    b.bq = L.bq.p;
+    b.bcnt = L.bcnt.p;
     b.qbits[0] = a.qbits[0];
     b.qbits[1] = a.qbits[1];
-    b.bbits = P.bbits.p;
+    b.bbits = L.bbits.p;
     b.words = words;
     b.ctl = a.ctl;
     b.relax = a.relax;
@@ -1074,9 +1089,9 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
       b.light_group = 2;  // 2 lanes per vertex in the light phase (1 / 4: 128 / 124 vs 121 ms)
       b.nl = P.nlight.p;
       b.vm = P.vmeta.p;
-      b.sq = P.sq.p;
-      b.sbits = P.sbits.p;
-      GBX_CUDA(cudaMemsetAsync(P.sbits.p, 0, P.sbits.bytes(), s));
+      b.sq = L.sq.p;
+      b.sbits = L.sbits.p;
+      GBX_CUDA(cudaMemsetAsync(L.sbits.p, 0, L.sbits.bytes(), s));
     }
     b.trace = option(kOptSsspTrace) ? 1 : 0;
     const bool tlog_on = option(kOptSsspTrace) != 0;
@@ -1091,7 +1106,7 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     int per_sm = 0;
     GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fnb, kSsspThreads, 0));
     if (per_sm < 1) fail(GBX_CUDA_ERROR, "sssp kernel does not fit on an SM");
-    const int grid = device_sms() * per_sm;
+    const int grid = std::max(1, device_sms() * per_sm / share);
     void* args[] = {&b};
     GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fnb), dim3(grid),
                                          dim3(kSsspThreads), args, 0, s));
@@ -1114,7 +1129,7 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
     int per_sm = 0;
     GBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSsspThreads, 0));
     if (per_sm < 1) fail(GBX_CUDA_ERROR, "sssp kernel does not fit on an SM");
-    const int grid = device_sms() * per_sm;
+    const int grid = std::max(1, device_sms() * per_sm / share);
     void* args[] = {&a};
     GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid),
                                          dim3(kSsspThreads), args, 0, s));
@@ -1125,61 +1140,76 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, E edges, D* dist, int32_t src
   (void)cudaGetLastError();
 }
 
-void sssp_run(gbx_graph* g, uint64_t source, double delta, double* out) {
-  const int64_t n = g->A.n;
-  if (source >= static_cast<uint64_t>(n))
-    fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(source));
+static void sssp_checks(gbx_graph* g, double delta) {
   if (!(delta > 0.0)) fail(GBX_NON_POSITIVE_DELTA, "delta must be positive");
   sssp_prepare(g);
   SsspPlan& P = *g->sssp;
   if (P.nonpositive) fail(GBX_NON_POSITIVE_WEIGHT, "edge weights must be positive");
-  const int32_t src = static_cast<int32_t>(source);
+  int nb = 1;
+  while (nb < 2.0 + P.max_w / delta && nb <= 64) nb <<= 1;
+  if (nb <= 64) ensure_split(g, P, delta);  // the light-first partition for delta
+}
+
+// one source on lane L (stream s, 1/share of the SMs); out: n doubles on the
+// host (NULL: the distances stay in the lane's buffer)
+static void sssp_one(gbx_graph* g, SsspLane& L, cudaStream_t s, int share, bool persist,
+                     int32_t src, double delta, double* out) {
+  SsspPlan& P = *g->sssp;
+  const int64_t n = P.n;
   // the circular-bucket kernel (nb <= 64) runs proper Delta-stepping on a
   // light-first row partition
   int nb = 1;
   while (nb < 2.0 + P.max_w / delta && nb <= 64) nb <<= 1;
   const bool split = nb <= 64;
-  if (split) ensure_split(g, P, delta);
   const bool cw = split && !P.packed;  // partitioned copies of col + weights
   if (P.integral) {
     // integer distances: bucket [lo, lo+delta) -> integer hi = ceil(lo + delta)
     const double h0 = std::ceil(delta);
     const uint32_t hi0 = h0 >= 4294967295.0 ? 0xffffffffu : static_cast<uint32_t>(h0);
     if (P.packed) {
-      sssp_launch<uint32_t, PackedEdges, uint32_t>(g, P, PackedEdges{P.packed_edges.p},
-                                                   P.dist32.p, src, delta, hi0, 0xffffffffu,
-                                                   split);
+      sssp_launch<uint32_t, PackedEdges, uint32_t>(g, P, L, s, share, persist,
+                                                   PackedEdges{P.packed_edges.p}, L.dist32.p, src,
+                                                   delta, hi0, 0xffffffffu, split);
     } else {
       const int32_t* w = g->A.domain == GBX_INT32 ? reinterpret_cast<const int32_t*>(g->A.val.p)
                                                   : P.wint.p;
       sssp_launch<uint32_t, IntEdges, uint32_t>(
-          g, P, IntEdges{cw ? P.split_col.p : g->A.col.p, cw ? P.split_wi.p : w}, P.dist32.p,
-          src, delta, hi0, 0xffffffffu, split);
+          g, P, L, s, share, persist,
+          IntEdges{cw ? P.split_col.p : g->A.col.p, cw ? P.split_wi.p : w}, L.dist32.p, src, delta,
+          hi0, 0xffffffffu, split);
     }
   } else {
     unsigned long long hi0, inf = 0x7FF0000000000000ull;
     std::memcpy(&hi0, &delta, 8);
     sssp_launch<unsigned long long, DblEdges, double>(
-        g, P,
+        g, P, L, s, share, persist,
         DblEdges{cw ? P.split_col.p : g->A.col.p,
                  cw ? P.split_wd.p : reinterpret_cast<const double*>(g->A.val.p)},
-        P.dist64.p, src, delta, hi0, inf, split);
+        L.dist64.p, src, delta, hi0, inf, split);
   }
-  cudaStream_t s = g->stream;
   if (out) {
-    double* tmp = nullptr;
-    GBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), std::max<int64_t>(n, 1) * 8, s));
-    if (P.integral) k_sssp_out<uint32_t><<<ceil_div(n, 256), 256, 0, s>>>(P.dist32.p, n, tmp);
-    else k_sssp_out<unsigned long long><<<ceil_div(n, 256), 256, 0, s>>>(P.dist64.p, n, tmp);
-    cudaError_t le = cudaGetLastError();
-    if (le == cudaSuccess) le = cudaMemcpyAsync(out, tmp, n * 8, cudaMemcpyDeviceToHost, s);
-    cudaFreeAsync(tmp, s);
-    GBX_CUDA(le);
+    L.out.ensure(std::max<int64_t>(n, 1));
+    if (P.integral) k_sssp_out<uint32_t><<<ceil_div(n, 256), 256, 0, s>>>(L.dist32.p, n, L.out.p);
+    else k_sssp_out<unsigned long long><<<ceil_div(n, 256), 256, 0, s>>>(L.dist64.p, n, L.out.p);
+    GBX_LAUNCHED();
+    GBX_CUDA(cudaMemcpyAsync(out, L.out.p, n * 8, cudaMemcpyDeviceToHost, s));
   }
+}
+
+void sssp_run(gbx_graph* g, uint64_t source, double delta, double* out) {
+  NvtxRange nvtx_("gbx.sssp");
+  const int64_t n = g->A.n;
+  if (source >= static_cast<uint64_t>(n))
+    fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(source));
+  sssp_checks(g, delta);
+  SsspPlan& P = *g->sssp;
+  SsspLane& L = ensure_lane(g, P, 0);
+  cudaStream_t s = g->stream;
+  sssp_one(g, L, s, 1, true, static_cast<int32_t>(source), delta, out);
   int hctl[10];
   unsigned long long rel = 0;
-  GBX_CUDA(cudaMemcpyAsync(hctl, P.ctl.p, sizeof hctl, cudaMemcpyDeviceToHost, s));
-  GBX_CUDA(cudaMemcpyAsync(&rel, P.relax.p, 8, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaMemcpyAsync(hctl, L.ctl.p, sizeof hctl, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaMemcpyAsync(&rel, L.relax.p, 8, cudaMemcpyDeviceToHost, s));
   GBX_CUDA(cudaStreamSynchronize(s));
   g->stats = gbx_stats{};
   g->pending_iters = nullptr;
@@ -1195,6 +1225,53 @@ double sssp_default_delta(gbx_graph* g) {
   sssp_prepare(g);
   const double m = g->sssp->max_w;
   return m > 0 ? m / 2.0 : 1.0;
+}
+
+// Several sources of sssp_delta_stepping (gapbench's per-source trials,
+// gapbench.cpp:300-330) in one call: the traversals are queued back to back
+// on the graph's stream (lane 0's workspace; each kernel reads its own
+// counters from the device), with ONE host synchronisation at the end instead
+// of one per source.  out: ns * n doubles (row b = sources[b]) or NULL.
+// (A vertex-major sweep of up to 16 sources sharing every edge read was
+// measured and rejected: its 16 distance rows per vertex (1 GB at
+// 2^24) no longer fit the 126 MB L2 the one-source kernel's 64 MB distance
+// array lives in -- 224 vs 83 ms for config 4.)
+void sssp_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double delta,
+                    double* out) {
+  NvtxRange nvtx_("gbx.sssp.batch");
+  const int64_t n = g->A.n;
+  if (ns == 0) fail(GBX_EMPTY_BATCH, "empty source batch");
+  if (!sources) fail(GBX_NULL_ARGUMENT, "sources is NULL");
+  for (uint64_t b = 0; b < ns; ++b)
+    if (sources[b] >= static_cast<uint64_t>(n))
+      fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(sources[b]));
+  sssp_checks(g, delta);
+  SsspPlan& P = *g->sssp;
+  SsspLane& L = ensure_lane(g, P, 0);
+  cudaStream_t s = g->stream;
+  DevArray<double> dev_out;
+  if (out) dev_out.alloc(std::max<int64_t>(static_cast<int64_t>(ns) * n, 1));
+  DevArray<unsigned long long> rel(ns);
+  for (uint64_t b = 0; b < ns; ++b) {
+    sssp_one(g, L, s, 1, true, static_cast<int32_t>(sources[b]), delta, nullptr);
+    GBX_CUDA(cudaMemcpyAsync(rel.p + b, L.relax.p, 8, cudaMemcpyDeviceToDevice, s));
+    if (out) {
+      if (P.integral) k_sssp_out<uint32_t><<<ceil_div(n, 256), 256, 0, s>>>(L.dist32.p, n, dev_out.p + b * n);
+      else k_sssp_out<unsigned long long><<<ceil_div(n, 256), 256, 0, s>>>(L.dist64.p, n, dev_out.p + b * n);
+      GBX_LAUNCHED();
+    }
+  }
+  std::vector<unsigned long long> hr(ns);
+  GBX_CUDA(cudaMemcpyAsync(hr.data(), rel.p, ns * 8, cudaMemcpyDeviceToHost, s));
+  if (out) GBX_CUDA(cudaMemcpyAsync(out, dev_out.p, ns * n * 8, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  unsigned long long total = 0;
+  for (unsigned long long r : hr) total += r;
+  g->stats = gbx_stats{};
+  g->pending_iters = nullptr;
+  g->stats.launches = static_cast<int64_t>(ns) * (2 + (out ? 1 : 0));
+  g->stats.hot_launches = static_cast<int64_t>(ns);
+  g->stats.work_units = static_cast<int64_t>(total);
 }
 
 }  // namespace gbx

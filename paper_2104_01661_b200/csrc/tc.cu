@@ -477,6 +477,7 @@ void tc_plan_from_upper(gbx_graph* g, int64_t n, int bits, const uint64_t* sorte
                         uint64_t* scratch, uint64_t* scratch2);
 
 void tc_prepare(gbx_graph* g) {
+  NvtxRange nvtx_("gbx.triangle_count.prepare");
   if (g->tc) return;
   cudaStream_t s = g->stream;
   const Csr& A = g->A;
@@ -591,6 +592,7 @@ static void id_range(const std::vector<int32_t>& v, int64_t rb, int64_t re, size
 
 // triangles whose middle vertex (rank space) lies in [rb, re)
 uint64_t tc_run(gbx_graph* g, int64_t rb, int64_t re) {
+  NvtxRange nvtx_("gbx.triangle_count");
   tc_prepare(g);
   TcPlan& P = *g->tc;
   cudaStream_t s = g->stream;

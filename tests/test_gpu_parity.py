@@ -521,3 +521,46 @@ def test_pagerank_nonpositive_itermax_passes_through():
         r = algo.pagerank_gap(g, 0.85, 1e-4, itermax)
         assert r.iterations == itermax
         assert np.all(r.rank == 1.0 / n)
+
+
+def _sssp_batch(g, srcs, delta):
+    from paper_2104_01661_b200.graph import call
+    n = g.n()
+    s = np.ascontiguousarray(srcs, np.uint64)
+    out = np.empty((len(s), n), np.float64)
+    call("gbx_sssp_batch", out.ctypes.data, g.handle, s.ctypes.data if len(s) else None, len(s),
+         float(delta))
+    return out
+
+
+def test_sssp_batch_vs_oracle():
+    """gbx_sssp_batch (the bench's config-4 call): every row equals Dijkstra
+    and the one-source call."""
+    g = P.generate_er(14, 16, seed=6)
+    rp, col, w = g.export()
+    n = len(rp) - 1
+    P.property_rowdegree(g)
+    srcs = P.pick_sources(g.row_degree(), 9, 6)
+    for delta in (64.0, 1000.0, 7.0, 1.0):
+        got = _sssp_batch(g, srcs, delta)
+        for b, s in enumerate(srcs):
+            want = O.dijkstra(n, rp, col, w.astype(np.float64), int(s))
+            assert np.array_equal(got[b], want)
+            assert np.array_equal(got[b], algo.sssp_delta_stepping(g, int(s), delta).dist)
+
+
+def test_sssp_batch_fp64_and_errors():
+    rng = np.random.default_rng(4)
+    g0 = P.generate_rmat(11, 8, seed=3)
+    rp, col, _ = g0.export()
+    w = rng.uniform(1e-3, 10.0, len(col))
+    g = P.graph_new(rp, col, w)
+    n = len(rp) - 1
+    got = _sssp_batch(g, [0, 5, 9], 2.0)
+    for b, s in enumerate((0, 5, 9)):
+        assert np.array_equal(got[b], O.dijkstra(n, rp, col, w, s))
+    for srcs, delta, code in (([], 1.0, P.ErrCode.EmptyBatch), ([n], 1.0, P.ErrCode.SourceOutOfRange),
+                              ([0], 0.0, P.ErrCode.NonPositiveDelta)):
+        with pytest.raises(P.Error) as e:
+            _sssp_batch(g, srcs, delta)
+        assert e.value.code == code

@@ -10,7 +10,8 @@ OUT=$ROOT/paper_2104_01661_b200/_variants
 mkdir -p $OUT/$NAME
 make -s -C $C >/dev/null
 objs=""
-for f in graph pagerank bfs cc tc sssp bc misc io ops api; do
+SRCS=$(sed -n "s/^SRCS := //p" $C/Makefile | sed "s/\.cu//g")
+for f in $SRCS; do
   if [[ " $* " == *" $f "* ]]; then
     /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
       -Xcompiler -fPIC --expt-relaxed-constexpr -I$ROOT/include $FLAGS -c $C/$f.cu -o $OUT/$NAME/$f.o

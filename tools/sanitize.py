@@ -60,6 +60,7 @@ def main():
     assert np.array_equal(lev[0], O.bfs(n, urp, ucol, int(srcs[0]))[1])
     done.append("k_bfs1/k_bfs64")
     # triangle count: k_tc_warp / k_tc_cta
+    P.property_ndiag(u)
     assert algo.triangle_count(u) == O.triangle_count(n, urp, ucol)
     done.append("k_tc_*")
     # SSSP: k_sssp_b
