@@ -777,9 +777,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the other BASELINE configs in the default line")
+    ap.add_argument("--option", action="append", default=[],
+                    help="library option name=value (gbx_set_option), e.g. pagerank.host_loop=1")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.option:
+        import ctypes as C
+        from paper_2104_01661_b200.graph import call
+        for kv in args.option:
+            k, v = kv.split("=", 1)
+            call("gbx_set_option", k.encode(), C.c_int64(int(v)))
     ws, rank, local = dist_env()
     dist = maybe_init_dist(ws, local)
     if args.workload == "pagerank" and (ws > 1 or force_sharded()):

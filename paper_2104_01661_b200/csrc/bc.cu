@@ -105,13 +105,16 @@ __device__ __forceinline__ void ld_sector(const double* p, double x[4]) {
 // in m; U independent column loads, then U map gathers, per step (the chain
 // col -> map -> val is latency-bound, so each lane keeps U in flight)
 template <int U>
-__device__ __forceinline__ void row_sum(const int32_t* col, int64_t p, int64_t e, int st,
+__device__ __forceinline__ void row_sum(const int32_t* col, int64_t n, int64_t p, int64_t e, int st,
                                         const uint32_t* map, const double* val, unsigned m,
                                         double s[4]) {
   for (; p < e; p += U * st) {
     int32_t u[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) u[k] = p + k * st < e ? ld_col(col + p + k * st) : -1;
+    for (int k = 0; k < U; ++k) {
+      u[k] = p + k * st < e ? ld_col(col + p + k * st) : -1;
+      GBX_DCHECK(u[k] < n, "bc column", u[k]);
+    }
     unsigned h[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) h[k] = u[k] >= 0 ? (nib(map, u[k]) & m) : 0u;
@@ -240,6 +243,7 @@ __global__ void __launch_bounds__(256) k_bc_push(BcArgs a) {
       int32_t v = 0;
       if (p < e0 && m) {
         v = __ldg(a.col + p);
+        GBX_DCHECK(v >= 0 && v < a.n, "bc push column", v);
         int32_t* lvp = a.level + static_cast<int64_t>(v) * 4;
         // the lv8 word (L2-resident) filters out the lanes where v is already
         // settled on an earlier depth before touching the int32 level words
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_pull(BcArgs a) {
         if (um) {
           pp = a.trp[v];
           pe = a.trp[v + 1];
-          row_sum<4>(a.tcol, pp, pe, 1, a.map_in, a.sigma, um, s);
+          row_sum<4>(a.tcol, a.n, pp, pe, 1, a.map_in, a.sigma, um, s);
           nm = bc_settle(a, v, um, s);
           found |= nm;
         }
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_pull(BcArgs a) {
       const int64_t i = n0 + (t - s0) * 4 + grp;
       const int64_t v = i < n0 + n1 ? L[i] : -1;
       const unsigned um = v >= 0 ? lanes_unreached(a.lv8[v], a.lanes) : 0u;
-      if (um) row_sum<kBcUnroll>(a.tcol, a.trp[v] + sub, a.trp[v + 1], 8, a.map_in, a.sigma, um, s);
+      if (um) row_sum<kBcUnroll>(a.tcol, a.n, a.trp[v] + sub, a.trp[v + 1], 8, a.map_in, a.sigma, um, s);
       group_reduce(s);
       unsigned nm = 0;
       if (sub == 0 && um) {
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_pull(BcArgs a) {
     } else {  // bin 2: a warp per row
       const int64_t v = L[n0 + n1 + (t - s0 - s1)];
       const unsigned um = lanes_unreached(a.lv8[v], a.lanes);
-      if (um) row_sum<kBcUnroll>(a.tcol, a.trp[v] + lane, a.trp[v + 1], 32, a.map_in, a.sigma, um, s);
+      if (um) row_sum<kBcUnroll>(a.tcol, a.n, a.trp[v] + lane, a.trp[v + 1], 32, a.map_in, a.sigma, um, s);
       warp_reduce(s);
       unsigned nm = 0;
       if (lane == 0 && um) {
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_pull_hub(BcArgs a) {
     const int64_t b0 = a.trp[v] + c * kBcHChunk;
     const int64_t e0 = min(a.trp[v + 1], b0 + kBcHChunk);
     double s[4] = {0.0, 0.0, 0.0, 0.0};
-    row_sum<kBcUnroll>(a.tcol, b0 + lane, e0, 32, a.map_in, a.sigma, um, s);
+    row_sum<kBcUnroll>(a.tcol, a.n, b0 + lane, e0, 32, a.map_in, a.sigma, um, s);
     warp_reduce(s);
     if (lane < 4 && ((um >> lane) & 1u)) {
       const double mine = lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3];
@@ -474,7 +478,7 @@ __global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_back(BcArgs a) {
         const int64_t u = L[i];
         const unsigned m = lanes_on(a.lv8[u], a.d, a.lanes, a.level, u);
         if (m) {
-          row_sum<4>(a.col, a.rp[u], a.rp[u + 1], 1, a.map_in, a.coef, m, acc);
+          row_sum<4>(a.col, a.n, a.rp[u], a.rp[u + 1], 1, a.map_in, a.coef, m, acc);
           bc_final(a, u, m, acc);
         }
       }
@@ -482,13 +486,13 @@ __global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_back(BcArgs a) {
       const int64_t i = n0 + (t - s0) * 4 + grp;
       const int64_t u = i < n0 + n1 ? L[i] : -1;
       const unsigned m = u >= 0 ? lanes_on(a.lv8[u], a.d, a.lanes, a.level, u) : 0u;
-      if (m) row_sum<kBcUnroll>(a.col, a.rp[u] + sub, a.rp[u + 1], 8, a.map_in, a.coef, m, acc);
+      if (m) row_sum<kBcUnroll>(a.col, a.n, a.rp[u] + sub, a.rp[u + 1], 8, a.map_in, a.coef, m, acc);
       group_reduce(acc);
       if (sub == 0 && m) bc_final(a, u, m, acc);
     } else {  // bin 2: a warp per row
       const int64_t u = L[n0 + n1 + (t - s0 - s1)];
       const unsigned m = lanes_on(a.lv8[u], a.d, a.lanes, a.level, u);
-      if (m) row_sum<kBcUnroll>(a.col, a.rp[u] + lane, a.rp[u + 1], 32, a.map_in, a.coef, m, acc);
+      if (m) row_sum<kBcUnroll>(a.col, a.n, a.rp[u] + lane, a.rp[u + 1], 32, a.map_in, a.coef, m, acc);
       warp_reduce(acc);
       if (lane == 0 && m) bc_final(a, u, m, acc);
     }
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_back_hub(BcArgs a) {
     const int64_t b0 = a.rp[u] + c * kBcHChunk;
     const int64_t e0 = min(a.rp[u + 1], b0 + kBcHChunk);
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    row_sum<kBcUnroll>(a.col, b0 + lane, e0, 32, a.map_in, a.coef, m, acc);
+    row_sum<kBcUnroll>(a.col, a.n, b0 + lane, e0, 32, a.map_in, a.coef, m, acc);
     warp_reduce(acc);
     if (lane < 4 && ((m >> lane) & 1u)) {
       const double mine = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];

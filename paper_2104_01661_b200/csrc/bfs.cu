@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
           int32_t w = 0;
           if (q < e0) {
             w = __ldg(a.col + q);
+            GBX_DCHECK(w >= 0 && w < a.n, "bfs push column", w);
             // level and parent loads issued together; min-id parent: skip the
             // atomic when a smaller one already landed
             const int lw = *(volatile int32_t*)&a.level[w];
@@ -251,7 +252,10 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
           if (active) {
             int32_t u[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) u[k] = pp + k < pe ? __ldg(a.tcol + pp + k) : -1;
+            for (int k = 0; k < 4; ++k) {
+              u[k] = pp + k < pe ? __ldg(a.tcol + pp + k) : -1;
+              GBX_DCHECK(u[k] < a.n, "bfs pull column", u[k]);
+            }
             unsigned hits = 0u;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -292,6 +296,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
             bool hit = false;
             if (gact && gp + sub < ge) {
               u = __ldg(a.tcol + gp + sub);
+              GBX_DCHECK(u >= 0 && u < a.n, "bfs pull column", u);
               hit = (ld_weak(bc + (u >> 5)) >> (u & 31)) & 1u;
             }
             const unsigned bal = __ballot_sync(kFull, hit);
@@ -324,6 +329,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
           bool hit = false;
           if (pp + lane < pe) {
             u = __ldg(a.tcol + pp + lane);
+            GBX_DCHECK(u >= 0 && u < a.n, "bfs pull column", u);
             hit = (ld_weak(bc + (u >> 5)) >> (u & 31)) & 1u;
           }
           const unsigned bal = __ballot_sync(kFull, hit);
@@ -641,6 +647,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
           int32_t w = 0;
           if (q < e0) {
             w = __ldg(a.col + q);
+            GBX_DCHECK(w >= 0 && w < a.n, "bfs push column", w);
             unsigned long long bits = f & ~(a.seen[w] | fc[w]);
             if (bits) {
               unsigned long long old = atomicOr(&fn[w], bits);
@@ -670,6 +677,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
           unsigned long long hit = 0ull;
           if (active && pp + sub < pe) {
             u = __ldg(a.tcol + pp + sub);
+            GBX_DCHECK(u >= 0 && u < a.n, "bfs pull column", u);
             hit = ld_weak(fc + u) & need;
           }
           // exclusive prefix-OR over the 8 lanes of the group: the lowest
@@ -714,6 +722,8 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
             unsigned long long hit = 0ull;
             if (pp + lane < pe) {
               u = __ldg(a.tcol + pp + lane);
+              GBX_DCHECK(u >= 0 && u < a.n, "bfs pull column", u);
+            GBX_DCHECK(u >= 0 && u < a.n, "bfs pull column", u);
               hit = ld_weak(fc + u) & need;
             }
             unsigned long long incl = hit;

@@ -31,6 +31,25 @@ struct Error : std::runtime_error {
   } while (0)
 #define GBX_LAUNCHED() GBX_CUDA(cudaGetLastError())
 
+// Device checks (GBX_DEVICE_CHECKS builds, tools/build_variant.sh): bounds of
+// every column-derived gather index in the hot kernels.  compute-sanitizer is
+// closed on this GPU pool, so the GPU test suite runs against such a build
+// instead (profiles/r02/device_checks.txt).  Compiled out otherwise.
+#ifdef GBX_DEVICE_CHECKS
+#define GBX_DCHECK(cond, what, val_)                                                       \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("gbx device check failed: %s (%lld) at %s:%d block %d thread %d\n", what,      \
+             static_cast<long long>(val_), __FILE__, __LINE__, blockIdx.x, threadIdx.x);    \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define GBX_DCHECK(cond, what, val_) \
+  do {                               \
+  } while (0)
+#endif
+
 // Coherent weak global load for data another CTA rewrites inside the same
 // persistent launch (frontier bitmaps, contribution vectors): NOT the .nc
 // path (__ldg), which is only defined for data read-only for the whole launch.

@@ -89,6 +89,7 @@ struct PrArgs {
   int trace;
   unsigned* fin_cnt;
   int64_t l1hot;       // x[0, l1hot) gathered with L1 evict_last, the rest no_allocate
+  int64_t nx;          // entries of x (device checks)
   int64_t row0;        // first row of this plan (shards); outputs indexed row - row0
   int grid_rows;
   double damping, teleport, tol;
@@ -160,12 +161,14 @@ template <typename V>
 __device__ __forceinline__ V pr_xg(int64_t l1hot, const V* x, int c) {
   return c < l1hot ? ld_hot(x + c) : ld_cold(x + c);
 }
+#define PR_CHECK_COL(a, c) GBX_DCHECK((c) < (a).nx, "pagerank column", (c))
 
 // fused epilogue of one row with prefetched r_prev / out-degree
 template <typename V>
 __device__ __forceinline__ double pr_finish_row(const PrArgs<V>& a, V* r_nxt, V* x_nxt,
                                                 int64_t row, double s, V rprev, V inv) {
   const double rn = a.teleport + s;
+  GBX_DCHECK(row >= a.row0 && row < a.nx, "pagerank row", row);
   r_nxt[row - a.row0] = static_cast<V>(rn);
   const V xv = static_cast<V>(rn * static_cast<double>(inv));
   if (a.npeer == 0) {
@@ -208,7 +211,10 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k, int c
       }
 #pragma unroll
       for (int j = 0; j < kPrIpl; ++j)
-        if (c[j] >= 0) s += static_cast<double>(pr_xg(a.l1hot, x_cur, c[j]));
+        if (c[j] >= 0) {
+          PR_CHECK_COL(a, c[j]);
+          s += static_cast<double>(pr_xg(a.l1hot, x_cur, c[j]));
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kWarp, s, o);
@@ -247,7 +253,10 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k, int c
         }
 #pragma unroll
         for (int q = 0; q < kPrB0Ipl; ++q)
-          if (c[q] >= 0) s += static_cast<double>(pr_xg(a.l1hot, x_cur, c[q]));
+          if (c[q] >= 0) {
+            PR_CHECK_COL(a, c[q]);
+            s += static_cast<double>(pr_xg(a.l1hot, x_cur, c[q]));
+          }
 #pragma unroll
         for (int q = 0; q < kPrB0Ipl; ++q) c[q] = nx[q];
       }
@@ -278,7 +287,10 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k, int c
           for (int q = 0; q < 4; ++q) nx[q] = j + 4 + q < L ? ld_stream(cp + (j + 4 + q) * m) : -1;
           V t[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) t[q] = c[q] >= 0 ? pr_xg(a.l1hot, x_cur, c[q]) : V(0);
+          for (int q = 0; q < 4; ++q) {
+            if (c[q] >= 0) PR_CHECK_COL(a, c[q]);
+            t[q] = c[q] >= 0 ? pr_xg(a.l1hot, x_cur, c[q]) : V(0);
+          }
           s += (static_cast<double>(t[0]) + static_cast<double>(t[1])) +
                (static_cast<double>(t[2]) + static_cast<double>(t[3]));
 #pragma unroll
@@ -1006,6 +1018,7 @@ static PrArgs<V> make_args(PrPlan& P, double damping, double tol, int itermax) {
   a.fin_cnt = P.blk_cnt.p;
   a.row0 = 0;
   a.l1hot = std::min<int64_t>(P.n, l1_hot_bytes() / static_cast<int64_t>(sizeof(V)));
+  a.nx = P.n;
   a.grid_rows = resident_grid(reinterpret_cast<const void*>(k_pr_rows<V>));
   a.damping = damping;
   a.teleport = (1.0 - damping) / static_cast<double>(P.n);
@@ -1302,6 +1315,7 @@ void pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, float
   a.inv = P.invf.p;
   a.fixed = 1;
   a.x0 = const_cast<float*>(x_full);  // padded layout (tcol remapped to it)
+  a.nx = g->prs->chunk * g->prs->nranks;
   a.x1 = x_slice - P.row0;            // x_nxt[row] -> x_slice[row - row0]
   a.r0 = const_cast<float*>(r_prev);  // local rows; may alias r_new
   a.r1 = r_new;
@@ -1340,6 +1354,7 @@ static void p2p_rank_args(gbx_graph* g, const uint64_t* x0_peers, const uint64_t
   a.r0 = r0;
   a.r1 = r1;
   a.npeer = S.nranks;
+  a.nx = S.chunk * S.nranks;
   const int64_t off = static_cast<int64_t>(S.rank) * S.chunk - P.row0;
   for (int q = 0; q < S.nranks; ++q) {
     a.xp[0][q] = reinterpret_cast<float*>(x0_peers[q]) + off;

@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kSsspThreads) k_sssp(SsspArgs<D, E> a) {
             W w = W(0);
             v[t] = 0;
             if (ok[t]) a.edges.get(q, v[t], w);
+            GBX_DCHECK(v[t] >= 0 && v[t] < a.n, "sssp edge target", v[t]);
             nd[t] = DistTraits<D>::add(du, w);
           }
           D cur[4];
@@ -522,6 +523,7 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
           W w = W(0);
           v[q4] = 0;
           if (ok[q4]) a.edges.get(q, v[q4], w);
+          GBX_DCHECK(v[q4] >= 0 && v[q4] < a.n, "sssp edge target", v[q4]);
           nd[q4] = DistTraits<D>::add(du, w);
         }
         D cur[4];
@@ -589,6 +591,7 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
           W w = W(0);
           v[q4] = 0;
           if (ok[q4]) a.edges.get(q, v[q4], w);
+          GBX_DCHECK(v[q4] >= 0 && v[q4] < a.n, "sssp edge target", v[q4]);
           nd[q4] = DistTraits<D>::add(du, w);
         }
         D cur[4];

@@ -1,7 +1,23 @@
 """SSSP diagnostics: stats (near iterations, relaxations) and wall time per source."""
 import sys, time
+import ctypes as C
 import paper_2104_01661_b200 as P
 from paper_2104_01661_b200.graph import call
+
+
+def opt_args(argv):
+    """name=value arguments -> library options (gbx_set_option); the rest returned"""
+    rest = []
+    for a in argv:
+        if "=" in a:
+            k, v = a.split("=", 1)
+            call("gbx_set_option", k.encode(), C.c_int64(int(v)))
+        else:
+            rest.append(a)
+    return rest
+
+
+sys.argv = [sys.argv[0]] + opt_args(sys.argv[1:])
 
 logn = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 P.init(0)
