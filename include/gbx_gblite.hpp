@@ -26,12 +26,26 @@
 
 namespace gblite::b200 {
 
+// Device / runtime failures (gbx codes <= -30: CUDA errors, out of device
+// memory, unsupported sizes, NULL arguments, NCCL failures) have no gblite
+// ErrCode.  They are thrown as DeviceError: a gblite::Error (so a caller that
+// catches gblite::Error still catches it; its code() is InvalidValue) that
+// also carries the gbx code -- distinct from every argument error the
+// reference itself raises.
+class DeviceError : public Error {
+ public:
+  DeviceError(int gbx_code, const std::string& message)
+      : Error(ErrCode::InvalidValue, "device failure " + std::to_string(gbx_code) + ": " + message),
+        gbx_code_(gbx_code) {}
+  int gbx_code() const noexcept { return gbx_code_; }
+
+ private:
+  int gbx_code_;
+};
+
 inline void check(int rc, const char* msg) {
-  if (rc < 0) {
-    // gbx codes <= -30 (device failures) have no gblite counterpart
-    const ErrCode code = rc <= -30 ? ErrCode::InvalidValue : static_cast<ErrCode>(rc);
-    fail(code, std::string("gbx: ") + msg);
-  }
+  if (rc <= -30) throw DeviceError(rc, std::string("gbx: ") + msg);
+  if (rc < 0) fail(static_cast<ErrCode>(rc), std::string("gbx: ") + msg);
 }
 
 // The adjacency + caches of a gblite::Graph, resident on the device.

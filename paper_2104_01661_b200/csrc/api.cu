@@ -331,8 +331,8 @@ int gbx_property_at(gbx_graph* g, char* msg) {
     need(g);
     gbx::Scope sc(g);
     if (g->kind != GBX_UNDIRECTED) {
-      gbx::compute_transpose(g->stream, g->A, g->at_own);
-      gbx::sync(g);
+      g->at_own = gbx::Csr();
+      g->at_pending = true;  // built on first read (gbx_graph::AT)
     }
     g->has_at = true;
   });
@@ -365,7 +365,7 @@ int gbx_property_symmetric_pattern(gbx_graph* g, char* msg) {
     gbx::Scope sc(g);
     bool sym;
     if (g->has_at) {
-      sym = g->kind == GBX_UNDIRECTED ? true : gbx::csr_equal(g->stream, g->A, g->at_own);
+      sym = g->kind == GBX_UNDIRECTED ? true : gbx::csr_equal(g->stream, g->A, g->AT());
     } else {
       gbx::Csr t;
       gbx::compute_transpose(g->stream, g->A, t);
@@ -390,6 +390,7 @@ int gbx_delete_properties(gbx_graph* g, char* msg) {
     gbx::sync(g);
     gbx::reset_plans(g);
     g->at_own = gbx::Csr();
+    g->at_pending = false;
     g->has_at = false;
     g->rowdeg.release();
     g->coldeg.release();
@@ -444,7 +445,7 @@ int gbx_check_graph(const gbx_graph* gc, char* msg) {
     cudaStream_t s = g->stream;
     gbx::Csr t;
     gbx::compute_transpose(s, g->A, t);
-    if (g->has_at && g->kind != GBX_UNDIRECTED && !gbx::csr_equal(s, g->at_own, t))
+    if (g->has_at && g->kind != GBX_UNDIRECTED && !gbx::csr_equal(s, g->AT(), t))
       gbx::fail(GBX_INVALID_GRAPH, "AT does not equal transpose(A)");
     auto check_deg = [&](const gbx::DevArray<int32_t>& d, bool by_row, const char* name) {
       gbx::DevArray<int32_t> want;

@@ -115,6 +115,7 @@ struct gbx_dgraph {
   std::vector<gbx_graph*> shard;   // [nlocal]
   std::vector<int64_t> local_nnz;  // [nlocal]
   std::unique_ptr<gbx::PrMgState> pr;  // PageRank exchange buffers (mg.cu)
+  std::vector<int64_t> tc_bounds;      // triangle count: middle-vertex split (mg.cu)
   gbx_stats stats{};                   // the last multi-GPU call
   ~gbx_dgraph();
 };

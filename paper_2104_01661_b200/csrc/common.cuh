@@ -169,6 +169,11 @@ struct gbx_graph {
   // caches
   bool has_at = false;
   gbx::Csr at_own;  // directed: the transpose; undirected graphs alias A
+  // property_at (graph.cpp:30-41) on a directed graph records the cache and
+  // builds it on first read: PageRank's plan needs only the in-degrees (from
+  // A's columns), so a basic-mode PageRank never pays for a transpose it does
+  // not read; BFS pulls, BC, check_graph ... materialise it through AT()
+  bool at_pending = false;
   bool has_rowdeg = false, has_coldeg = false;
   gbx::DevArray<int32_t> rowdeg, coldeg;
   int symmetric = GBX_UNKNOWN;
@@ -184,7 +189,12 @@ struct gbx_graph {
   gbx_stats stats{};
   const int* pending_iters = nullptr;  // device word holding stats.iterations of an async call
 
-  const gbx::Csr& AT() const { return kind == GBX_UNDIRECTED ? A : at_own; }
+  const gbx::Csr& AT() const {
+    if (kind == GBX_UNDIRECTED) return A;
+    if (at_pending) materialize_at();
+    return at_own;
+  }
+  void materialize_at() const;
   ~gbx_graph();
 };
 

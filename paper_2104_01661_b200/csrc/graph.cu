@@ -59,6 +59,20 @@ Scope::Scope(gbx_graph* g) : lock(g->mu) {
 
 void sync(gbx_graph* g) { GBX_CUDA(cudaStreamSynchronize(g->stream)); }
 
+}  // namespace gbx
+
+// the deferred transpose of property_at (the handle's calls are serialised by
+// its Scope lock, so materialising inside a const accessor is race-free)
+void gbx_graph::materialize_at() const {
+  gbx::NvtxRange nvtx_("gbx.property_at.transpose");
+  gbx_graph* g = const_cast<gbx_graph*>(this);
+  gbx::compute_transpose(g->stream, g->A, g->at_own);
+  GBX_CUDA(cudaStreamSynchronize(g->stream));
+  g->at_pending = false;
+}
+
+namespace gbx {
+
 void require_at(const gbx_graph* g, const char* who) {
   if (!g->has_at) fail(GBX_MISSING_PROPERTY, std::string(who) + " needs G.AT");
 }
@@ -270,7 +284,7 @@ __global__ void k_gather_transpose(const int64_t* perm, const int32_t* rowid, in
 // A is row-major with ascending rows, so the stable sort leaves every row of T
 // strictly ascending.  Row pointers come from the sorted keys' boundaries.
 void compute_transpose(cudaStream_t s, const Csr& A, Csr& T) {
-  NvtxRange nvtx_("gbx.property_at.transpose");
+  gbx::NvtxRange nvtx_("gbx.property_at.transpose");
   T.n = A.n;
   T.nnz = A.nnz;
   T.domain = A.domain;

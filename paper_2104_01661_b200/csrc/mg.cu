@@ -472,12 +472,16 @@ uint64_t triangle_count_mg(gbx_dgraph* D) {
       GBX_CUDA(cudaStreamSynchronize(D->shard[l]->stream));
     }
   }
-  // middle vertices split by probe work: the same split on every rank
+  // middle vertices split by probe work: the same split on every rank (the
+  // replicated U is identical everywhere; computed once per graph)
+  if (static_cast<int>(D->tc_bounds.size()) != P + 1) {
+    D->tc_bounds.assign(P + 1, 0);
+    tc_partition(D->shard[0], P, D->tc_bounds.data());
+  }
+  const std::vector<int64_t>& b = D->tc_bounds;
   std::vector<DevArray<unsigned long long>> part(L);
   std::vector<void*> pp(L);
   for (int l = 0; l < L; ++l) {
-    std::vector<int64_t> b(P + 1);
-    tc_partition(D->shard[l], P, b.data());
     const int q = c->global_rank(l);
     const unsigned long long mine = tc_run(D->shard[l], b[q], b[q + 1]);
     D->stats.launches += D->shard[l]->stats.launches;
@@ -597,6 +601,7 @@ void betweenness_mg(gbx_dgraph* D, const uint64_t* sources, uint64_t ns, double*
       int done = 0;
       for (int l = 0; l < L; ++l) bc_shard_forward_apply(D->shard[l], tot ? all[l].p : nullptr, tot, &done);
       ++levels;
+      D->stats.launches += 4 * L;  // pull (+ hub passes), pack, apply
       if (done) break;
     }
     for (;;) {  // backward
@@ -612,6 +617,7 @@ void betweenness_mg(gbx_dgraph* D, const uint64_t* sources, uint64_t ns, double*
       const int64_t tot = gather_records(c, recs, nrec, kRec, all);
       for (int l = 0; l < L; ++l) bc_shard_backward_apply(D->shard[l], tot ? all[l].p : nullptr, tot);
       ++levels;
+      D->stats.launches += 6 * L;  // map, filter, bins, back (+ hub passes), pack, apply
     }
     for (int l = 0; l < L; ++l) {
       double* cent = nullptr;

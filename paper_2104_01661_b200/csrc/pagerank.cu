@@ -819,15 +819,23 @@ __global__ void k_pr_gather_a_short(const int64_t* arp, const int32_t* acol,
 
 // relabeled AT (rows by descending in-degree) + relabeled out-degree
 static void build_relabeled(gbx_graph* g, PrPlan& P) {
-  const Csr& AT = g->AT();
   cudaStream_t s = g->stream;
-  const int64_t n = AT.n, nnz = AT.nnz;
+  const Csr& A = g->A;
+  const int64_t n = A.n, nnz = A.nnz;
   P.n = n;
   P.nnz = nnz;
-  DevArray<int32_t> len(std::max<int64_t>(n, 1));
-  if (n) {
-    k_neg_len<<<ceil_div(n, 256), 256, 0, s>>>(AT.rp.p, n, len.p);
-    GBX_LAUNCHED();
+  // in-degree = AT's row lengths = A's column counts: the plan is built from
+  // A alone (the relabeled AT below is gathered from A's rows), so a pending
+  // transpose is never materialised for PageRank
+  DevArray<int32_t> len;
+  if (g->kind == GBX_UNDIRECTED) {
+    len.alloc(std::max<int64_t>(n, 1));
+    if (n) {
+      k_neg_len<<<ceil_div(n, 256), 256, 0, s>>>(A.rp.p, n, len.p);
+      GBX_LAUNCHED();
+    }
+  } else {
+    compute_degrees(s, A, len, false);
   }
   sort_ids_by_key(s, len.p, n, false, P.new2old);
   P.old2new.alloc(std::max<int64_t>(n, 1));
@@ -846,7 +854,6 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
   P.trp.alloc(n + 1);
   P.tcol.alloc(std::max<int64_t>(nnz, 1));
   if (nnz) {
-    const Csr& A = g->A;
     DevArray<int64_t> prp(n + 1);
     k_pr_newlen<<<ceil_div(n + 1, 256), 256, 0, s>>>(A.rp.p, P.new2old.p, n, prp.p);
     GBX_LAUNCHED();

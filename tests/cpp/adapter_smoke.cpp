@@ -3,6 +3,7 @@
 // GPU box it also checks one PageRank and one BFS against gblite itself.
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "gbx_gblite.hpp"
 #include "gblite/util.hpp"
@@ -17,6 +18,22 @@ int main(int argc, char** argv) {
   auto g = graph_new(std::move(m), Kind::DirectedAdjacency);
   property_at(g);
   property_rowdegree(g);
+  // device failures surface as DeviceError: still a gblite::Error, distinct type
+  static_assert(std::is_base_of_v<Error, b200::DeviceError>);
+  try {
+    b200::check(GBX_NULL_ARGUMENT, "probe");
+    return 3;
+  } catch (const b200::DeviceError& e) {
+    if (e.gbx_code() != GBX_NULL_ARGUMENT || e.code() != ErrCode::InvalidValue) return 4;
+  }
+  try {
+    b200::check(GBX_SOURCE_OUT_OF_RANGE, "probe");
+    return 5;
+  } catch (const b200::DeviceError&) {
+    return 6;  // an argument error must keep its gblite code, not become a device error
+  } catch (const Error& e) {
+    if (e.code() != ErrCode::SourceOutOfRange) return 7;
+  }
   if (argc < 2) {  // link check only (no GPU)
     std::puts("adapter linked");
     return 0;

@@ -1,5 +1,6 @@
 """Phase timing of the PageRank e2e path (graph_new32 -> basic PR -> D2H)."""
-import ctypes as C, time
+import ctypes as C, time, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2104_01661_b200 as P
 from paper_2104_01661_b200.graph import call

@@ -63,10 +63,11 @@ def main():
               "# generation, plan builds, the e2e leg and the CPU-baseline setup included).\n")
     heads = {
         "bench_pagerank_launches": "# ncu --metrics gpu__time_duration.sum --clock-control none launch list of\n"
-                                   "# `python bench.py --steps 2 --warmup 1` (PageRank runs as ONE persistent\n"
+                                   "# `python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-secondary`\n"
+                                   "# (PageRank runs as ONE persistent\n"
                                    "# cooperative kernel per step, k_pr_persist: row phase + long-row finish\n"
                                    "# + L1 reduction per iteration).\n" + common,
-        "bench_pagerank_launches_split": "# the same with GBX_PR_NO_GRAPH=1: the same row / finish code launched as\n"
+        "bench_pagerank_launches_split": "# the same with --option pagerank.host_loop=1: the same row / finish code launched as\n"
                                          "# one k_pr_rows + k_pr_finish pair per iteration, splitting the shares.\n"
                                          + common,
     }
