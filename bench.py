@@ -698,20 +698,87 @@ def bench_simple(args, dist, ws, rank, local):
     return out, None
 
 
+def bench_replicas(args, dist, ws, rank, local):
+    """SURVEY 8e "replicas only" configs at N GPUs: config 1 (64 independent
+    BFS sources) and config 4 (16 SSSP sources) dealt round-robin over the
+    ranks, each rank running its share on its own copy of the (small / one-
+    GPU-sized) graph with no data-path collective; total work fixed (strong),
+    time = max over ranks."""
+    import ctypes as C
+
+    import torch
+    import paper_2104_01661_b200 as P
+    from paper_2104_01661_b200.graph import call
+    w = args.workload
+    steps = max(3, min(args.steps, 10))
+    if w == "bfs64":
+        scale = 16
+        g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
+        P.property_at(g)
+        P.property_rowdegree(g)
+        srcs = P.pick_sources(g.row_degree(), 64, 1)
+        mine = np.ascontiguousarray(srcs[rank::ws], np.uint64)
+
+        def one():
+            if len(mine):
+                call("gbx_bfs_batch", None, None, g.handle, mine.ctypes.data, len(mine))
+            return len(srcs)
+        metric, unit, per = f"BFS GTEPS at R-MAT scale {scale} (64 sources, replicas)", "GTEPS", \
+            g.info()[1] / 2 / 1e9
+    else:
+        scale = 24
+        g = P.generate_er(scale, 16, seed=1)
+        P.property_rowdegree(g)
+        g.prepare("sssp")
+        srcs = P.pick_sources(g.row_degree(), 16, 1)
+        mine = np.ascontiguousarray(srcs[rank::ws], np.uint64)
+
+        def one():
+            if len(mine):
+                call("gbx_sssp_batch", None, g.handle, mine.ctypes.data, len(mine), 64.0)
+            return len(srcs)
+        metric, unit, per = f"SSSP relaxation edges/s (ER 2^{scale}, 16 sources, replicas)", \
+            "edges/s", float(g.info()[1])
+    stream = torch.cuda.ExternalStream(g.stream())
+    for _ in range(max(args.warmup, 3)):
+        one()
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(steps):
+            barrier(dist)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            units = one()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    t = max_over_ranks(dist, sum(times) / len(times))
+    out = {"metric": metric, "value": per * units / t, "unit": unit, "n_gpus": ws, "steps": steps,
+           "warmup": max(args.warmup, 3), "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "int32 indices", "data": "synthetic",
+           "config": {"workload": w, "scale": scale, "parallelism": f"replicas{ws}",
+                      "sources_per_rank": len(mine)},
+           "gpu_launches": int(g.last_stats()["launches"] * steps), "clocks": clk.summary()}
+    return out, None
+
+
 def bench_simple_mg(args, dist, ws, rank, local):
-    """Secondary configs at N GPUs through the C++ multi-GPU path."""
+    """Secondary configs at N GPUs through the C++ multi-GPU path (TC, BFS-22,
+    BC); config 1 and SSSP as replicas."""
     import torch
     import paper_2104_01661_b200 as P
     from paper_2104_01661_b200.mg import Comm, DGraph
     w = args.workload
+    if w in ("sssp", "bfs64"):
+        return bench_replicas(args, dist, ws, rank, local)
     comm = Comm.from_torch(dist, local)
     steps = max(3, min(args.steps, 10))
-    if w == "sssp":
-        raise SystemExit("sssp runs as replicas only (SURVEY 8e): use --gpus 1")
-    scale = {"tc": 22, "bfs": 22, "bfs64": 16, "bc": 24}[w]
+    scale = {"tc": 22, "bfs": 22, "bc": 24}[w]
     kind = P.Kind.UndirectedAdjacency
     g = DGraph.rmat(comm, scale, 16, seed=1, kind=kind)
-    if w in ("bfs", "bfs64", "bc"):
+    if w in ("bfs", "bc"):
         # the sources the single-GPU line uses: degrees from a local full graph
         # would need the replica; the seeded draw over non-isolated vertices
         # needs only the global degree array (one all-reduce, small)
@@ -726,14 +793,15 @@ def bench_simple_mg(args, dist, ws, rank, local):
             g.triangle_count()
             return 1
         metric, unit, per = f"triangle count edges/s at R-MAT scale {scale} (multi-GPU)", "edges/s", g.nnz / 2
-    elif w in ("bfs", "bfs64"):
+    elif w == "bfs":
         srcs = P.pick_sources(deg, 64, 1)[:8]
 
         def one():
             for s0 in srcs:
                 g.bfs(int(s0), to_host=False)
             return len(srcs)
-        metric, unit, per = f"BFS GTEPS at R-MAT scale {scale} (row-sharded pull levels)", "GTEPS", g.nnz / 2 / 1e9
+        metric, unit, per = (f"BFS GTEPS at R-MAT scale {scale} (row-sharded: push / pull levels, "
+                             f"frontier all-gather)"), "GTEPS", g.nnz / 2 / 1e9
     else:
         srcs = P.pick_sources(deg, 4, 1)
 

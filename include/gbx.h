@@ -90,9 +90,12 @@ const char* gbx_version(void);
  *   pagerank.l1_window_kb  144    bytes of x gathered with L1 evict_last
  *   pagerank.carveout      10     % shared-memory carveout of the row kernels (-1: driver)
  *   pagerank.host_loop     0      1: one launch per iteration (for ncu captures)
+ *   pagerank.trace         0      1: per-iteration phase means (%globaltimer) on stderr
  *   p2p.timeout_ms         10000  bound of the fused multi-GPU exchange's peer wait
  *   bfs.alpha              14     push while frontier edges < nnz/alpha (0: bfs.cpp:77-78 rule)
  *   bfs64.pull_div         2      64-lane batch: pull when frontier edges > nnz/div
+ *   bfs_mg.push_div        0      gbx_bfs_mg: 0 = push while frontier edges < nnz/bfs.alpha,
+ *                                 else push while the frontier < n/div (bfs.cpp:77-78)
  *   bfs.trace / sssp.trace 0      1: per-level %globaltimer log on stderr
  *   bc.alpha               14     as bfs.alpha for the Brandes forward sweep */
 int gbx_set_option(const char* name, int64_t value, char msg[GBX_MSG_LEN]);

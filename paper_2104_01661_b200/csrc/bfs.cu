@@ -1119,6 +1119,154 @@ void bfs_shard_level(gbx_graph* g, const uint32_t* front, uint32_t* next_slice, 
   *found = hc[0];
 }
 
+// ---- push levels of the row-sharded BFS (small frontiers): the owned
+// frontier vertices mark their out-neighbours as candidates (a byte per
+// vertex, max-reduced over the ranks by the driver); each rank then pulls
+// only its owned unvisited candidates -- the same min-id parent as a full
+// pull (the first frontier hit in the ascending AT row), at the cost of the
+// frontier's edges instead of every unvisited row.
+
+// owned frontier vertices (bits of front in [rb, re)) -> light list (a warp
+// each) and heavy list (rows longer than kBfsMarkHeavy: the whole grid)
+constexpr int64_t kBfsMarkHeavy = 2048;
+__global__ void k_bfs_owned_front(const uint32_t* front, const int64_t* rp, int64_t rb, int64_t re,
+                                  int32_t* list, int* cnt, int32_t* heavy, int* hcnt) {
+  const int64_t v = rb + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const bool on = v < re && ((front[v >> 5] >> (v & 31)) & 1u);
+  if (!on) return;
+  if (rp[v + 1] - rp[v] > kBfsMarkHeavy) heavy[agg_append(hcnt)] = static_cast<int32_t>(v);
+  else list[agg_append(cnt)] = static_cast<int32_t>(v);
+}
+
+// a warp per light frontier vertex, then every thread of the grid over the
+// heavy ones' edges: every out-neighbour becomes a candidate
+__global__ void __launch_bounds__(256) k_bfs_shard_mark(const int64_t* rp, const int32_t* col,
+                                                        int64_t n, const int32_t* list,
+                                                        const int* cnt, const int32_t* heavy,
+                                                        const int* hcnt, uint8_t* cand) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int m = *cnt;
+  for (int64_t i = gw; i < m; i += nw) {
+    const int32_t u = list[i];
+    for (int64_t p = rp[u] + lane; p < rp[u + 1]; p += 32) {
+      const int32_t v = __ldg(col + p);
+      GBX_DCHECK(v >= 0 && v < n, "bfs push column", v);
+      cand[v] = 1;  // idempotent plain store
+    }
+  }
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t nt = int64_t(gridDim.x) * blockDim.x;
+  const int mh = *hcnt;
+  for (int h = 0; h < mh; ++h) {
+    const int32_t u = heavy[h];
+    for (int64_t p = rp[u] + t; p < rp[u + 1]; p += nt) {
+      const int32_t v = __ldg(col + p);
+      GBX_DCHECK(v >= 0 && v < n, "bfs push column", v);
+      cand[v] = 1;
+    }
+  }
+}
+
+// owned unvisited candidates -> list
+__global__ void k_bfs_cand_list(const uint8_t* cand, const int32_t* level, int64_t rb, int64_t re,
+                                int32_t* list, int* cnt) {
+  const int64_t v = rb + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const bool on = v < re && cand[v] && level[v] == -1;
+  if (on) list[agg_append(cnt)] = static_cast<int32_t>(v);
+}
+
+// edges of the owned frontier vertices (the direction rule's measure)
+__global__ void k_bfs_front_edges(const uint32_t* front, const int64_t* rp, int64_t rb, int64_t re,
+                                  unsigned long long* out) {
+  const int64_t v = rb + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  unsigned long long e = 0;
+  if (v < re && ((front[v >> 5] >> (v & 31)) & 1u)) e = static_cast<unsigned long long>(rp[v + 1] - rp[v]);
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  if ((threadIdx.x & 31) == 0 && e) atomicAdd(out, e);
+}
+
+int64_t bfs_shard_front_edges(gbx_graph* g, const uint32_t* front) {
+  BfsShard& S = need_bfs_shard(g);
+  cudaStream_t s = g->stream;
+  if (S.re <= S.rb) return 0;
+  Tmp<unsigned long long> e(1, s);
+  GBX_CUDA(cudaMemsetAsync(e.p, 0, 8, s));
+  k_bfs_front_edges<<<ceil_div(S.re - S.rb, 256), 256, 0, s>>>(front, g->A.rp.p, S.rb, S.re, e.p);
+  GBX_LAUNCHED();
+  unsigned long long h = 0;
+  GBX_CUDA(cudaMemcpyAsync(&h, e.p, 8, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  return static_cast<int64_t>(h);
+}
+
+// this rank's level / parent words of its owned rows (device, int32; -1 =
+// unreached): the driver gathers them on the device
+void bfs_shard_result_device(gbx_graph* g, const int32_t** level, const int32_t** parent) {
+  need_bfs_shard(g);
+  *level = g->bfs->level.p;
+  *parent = g->bfs->parent.p;
+}
+
+// mark phase: cand (n bytes, zeroed by the caller) gets this rank's owned
+// frontier vertices' out-neighbours
+void bfs_shard_push_mark(gbx_graph* g, const uint32_t* front, uint8_t* cand) {
+  NvtxRange nvtx_("gbx.bfs.shard_push_mark");
+  BfsShard& S = need_bfs_shard(g);
+  BfsWork& W = *g->bfs;
+  cudaStream_t s = g->stream;
+  const Csr& A = g->A;
+  if (S.re <= S.rb) return;
+  int32_t* list = reinterpret_cast<int32_t*>(W.queue[0].p);
+  int32_t* heavy = reinterpret_cast<int32_t*>(W.queue[1].p);
+  GBX_CUDA(cudaMemsetAsync(S.cnt.p, 0, 2 * sizeof(int), s));
+  k_bfs_owned_front<<<ceil_div(S.re - S.rb, 256), 256, 0, s>>>(front, A.rp.p, S.rb, S.re, list,
+                                                               S.cnt.p, heavy, S.cnt.p + 1);
+  k_bfs_shard_mark<<<device_sms() * 8, 256, 0, s>>>(A.rp.p, A.col.p, A.n, list, S.cnt.p, heavy,
+                                                    S.cnt.p + 1, cand);
+  GBX_LAUNCHED();
+  GBX_CUDA(cudaStreamSynchronize(s));
+}
+
+// pull phase of a push level: only the owned unvisited candidates (every
+// rank's marks max-reduced into cand); the owned still-unvisited list of the
+// pull levels is left as it is (the pull kernel skips vertices visited since)
+void bfs_shard_push_level(gbx_graph* g, const uint8_t* cand, const uint32_t* front,
+                          uint32_t* next_slice, int64_t* found) {
+  NvtxRange nvtx_("gbx.bfs.shard_push_level");
+  BfsShard& S = need_bfs_shard(g);
+  BfsWork& W = *g->bfs;
+  cudaStream_t s = g->stream;
+  const Csr& AT = g->AT();
+  const int64_t words = (S.re + 31) / 32 - S.rb / 32;
+  if (words > 0) GBX_CUDA(cudaMemsetAsync(next_slice, 0, words * 4, s));
+  const int d = S.d + 1;
+  int hc[2] = {0, 0};
+  if (S.re > S.rb) {
+    int32_t* clist = reinterpret_cast<int32_t*>(W.queue[0].p);
+    int32_t* scratch = reinterpret_cast<int32_t*>(W.queue[1].p);
+    GBX_CUDA(cudaMemsetAsync(S.cnt.p, 0, 2 * sizeof(int), s));
+    k_bfs_cand_list<<<ceil_div(S.re - S.rb, 256), 256, 0, s>>>(cand, W.level.p, S.rb, S.re, clist,
+                                                               S.cnt.p + 1);
+    GBX_LAUNCHED();
+    int nc = 0;
+    GBX_CUDA(cudaMemcpyAsync(&nc, S.cnt.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+    GBX_CUDA(cudaMemsetAsync(S.cnt.p, 0, 2 * sizeof(int), s));
+    if (nc > 0) {
+      k_bfs_shard_pull<<<device_sms() * 8, 256, 0, s>>>(AT.rp.p, AT.col.p, S.rb, S.re, clist, nc,
+                                                        front, d, W.level.p, W.parent.p,
+                                                        next_slice, scratch, S.cnt.p);
+      GBX_LAUNCHED();
+    }
+    GBX_CUDA(cudaMemcpyAsync(hc, S.cnt.p, sizeof hc, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+  }
+  S.d = d;
+  *found = hc[0];
+}
+
 // owned rows [rb, re): parent / level (-1 = unreached), host arrays of re - rb
 void bfs_shard_result(gbx_graph* g, int64_t* parent, int64_t* level) {
   BfsShard& S = need_bfs_shard(g);

@@ -217,6 +217,10 @@ void c_allreduce(gbx_comm* c, void* const* buf, size_t count, CollType t, CollOp
       k_reduce_local<uint32_t><<<grid, 256, 0, c->stream>>>(reinterpret_cast<const uint32_t* const*>(src.p),
                                                             c->nlocal, count, reinterpret_cast<uint32_t*>(out.p), o);
       break;
+    case CollType::U8:
+      k_reduce_local<uint8_t><<<grid, 256, 0, c->stream>>>(reinterpret_cast<const uint8_t* const*>(src.p),
+                                                           c->nlocal, count, reinterpret_cast<uint8_t*>(out.p), o);
+      break;
     default:
       fail(GBX_INVALID_VALUE, "allreduce: unsupported type");
   }

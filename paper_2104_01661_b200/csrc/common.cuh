@@ -71,6 +71,7 @@ enum Opt : int {
   kOptBfsAlpha,          // "bfs.alpha": push while frontier edges < nnz / alpha (0: reference rule)
   kOptBfs64PullDiv,      // "bfs64.pull_div"
   kOptBfsTrace,          // "bfs.trace": per-level %globaltimer log to stderr
+  kOptBfsMgPushDiv,      // "bfs_mg.push_div": multi-GPU BFS pushes while the frontier < n/div
   kOptBcAlpha,           // "bc.alpha"
   kOptSsspTrace,         // "sssp.trace": per-phase %globaltimer log to stderr
   kOptCount
@@ -331,6 +332,11 @@ void bfs_shard_begin(gbx_graph* g, uint64_t source, int rank, int nranks, int64_
                      int64_t* re_out, const int64_t* bounds = nullptr);
 void bfs_shard_level(gbx_graph* g, const uint32_t* front, uint32_t* next_slice, int64_t* found);
 void bfs_shard_result(gbx_graph* g, int64_t* parent, int64_t* level);
+void bfs_shard_push_mark(gbx_graph* g, const uint32_t* front, uint8_t* cand);
+int64_t bfs_shard_front_edges(gbx_graph* g, const uint32_t* front);
+void bfs_shard_result_device(gbx_graph* g, const int32_t** level, const int32_t** parent);
+void bfs_shard_push_level(gbx_graph* g, const uint8_t* cand, const uint32_t* front,
+                          uint32_t* next_slice, int64_t* found);
 uint64_t tc_run(gbx_graph* g, int64_t row_begin, int64_t row_end);
 void tc_prepare(gbx_graph* g);
 void tc_partition(gbx_graph* g, int parts, int64_t* bounds);

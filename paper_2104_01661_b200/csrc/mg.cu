@@ -19,6 +19,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 
 #include "comm.cuh"
@@ -110,32 +112,6 @@ int64_t gather_records(gbx_comm* c, const std::vector<const void*>& recs,
   }
   comm_sync(c);
   return total;
-}
-
-// full length-n int64 arrays from every rank's owned slice [bounds[q], bounds[q+1])
-void gather_rows_i64(gbx_dgraph* D, const std::vector<std::vector<int64_t>>& slice, int64_t* out) {
-  gbx_comm* c = D->comm;
-  const int L = c->nlocal, P = c->nranks;
-  int64_t mx = 1;
-  for (int q = 0; q < P; ++q) mx = std::max(mx, D->bounds[q + 1] - D->bounds[q]);
-  std::vector<DevArray<int64_t>> send(L), recv(L);
-  std::vector<const void*> sp(L);
-  std::vector<void*> rp(L);
-  for (int l = 0; l < L; ++l) {
-    send[l].alloc(mx);
-    recv[l].alloc(mx * P);
-    if (!slice[l].empty())
-      GBX_CUDA(cudaMemcpy(send[l].p, slice[l].data(), slice[l].size() * 8, cudaMemcpyHostToDevice));
-    sp[l] = send[l].p;
-    rp[l] = recv[l].p;
-  }
-  c_allgather(c, sp.data(), rp.data(), mx * 8);
-  if (!out) return;
-  std::vector<int64_t> all(mx * P);
-  GBX_CUDA(cudaMemcpy(all.data(), recv[0].p, all.size() * 8, cudaMemcpyDeviceToHost));
-  for (int q = 0; q < P; ++q)
-    std::copy(all.begin() + q * mx, all.begin() + q * mx + (D->bounds[q + 1] - D->bounds[q]),
-              out + D->bounds[q]);
 }
 
 // ---- PageRank ---------------------------------------------------------------------
@@ -499,6 +475,69 @@ uint64_t triangle_count_mg(gbx_dgraph* D) {
 
 // ---- BFS ------------------------------------------------------------------------------
 
+namespace {
+
+__global__ void k_pack_rows(const int32_t* lev, const int32_t* par, int64_t rb, int64_t re,
+                            int32_t* out) {  // out[2][mx]: level then parent of the owned rows
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (rb + i >= re) return;
+  out[i] = lev[rb + i];
+  out[(re - rb) + i] = par[rb + i];
+}
+
+__global__ void k_unpack_rows(const int32_t* in, int64_t mx, const int64_t* bounds, int P,
+                              int64_t n, int64_t* lev, int64_t* par) {
+  const int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (v >= n) return;
+  int q = 0;
+  while (q + 1 < P && v >= bounds[q + 1]) ++q;
+  const int64_t m = bounds[q + 1] - bounds[q];
+  const int32_t* blk = in + q * 2 * mx;
+  const int32_t L = blk[v - bounds[q]], Pa = blk[m + (v - bounds[q])];
+  lev[v] = L;
+  par[v] = L < 0 ? -1 : Pa;
+}
+
+void gather_bfs_result(gbx_dgraph* D, int64_t* parent, int64_t* level) {
+  gbx_comm* c = D->comm;
+  const int L = c->nlocal, P = c->nranks;
+  const int64_t n = D->n;
+  int64_t mx = 1;
+  for (int q = 0; q < P; ++q) mx = std::max(mx, D->bounds[q + 1] - D->bounds[q]);
+  std::vector<DevArray<int32_t>> send(L), recv(L);
+  std::vector<const void*> sp(L);
+  std::vector<void*> rp(L);
+  for (int l = 0; l < L; ++l) {
+    int64_t rb, re;
+    dgraph_block(D, l, &rb, &re);
+    const int32_t *lev, *par;
+    bfs_shard_result_device(D->shard[l], &lev, &par);
+    send[l].alloc(2 * mx);
+    recv[l].alloc(2 * mx * P);
+    if (re > rb) {
+      k_pack_rows<<<ceil_div(re - rb, 256), 256, 0, c->stream>>>(lev, par, rb, re, send[l].p);
+      GBX_LAUNCHED();
+    }
+    sp[l] = send[l].p;
+    rp[l] = recv[l].p;
+  }
+  sync_shards(D);
+  comm_sync(c);
+  c_allgather(c, sp.data(), rp.data(), 2 * mx * sizeof(int32_t));
+  DevArray<int64_t> db(P + 1), out(2 * std::max<int64_t>(n, 1));
+  GBX_CUDA(cudaMemcpyAsync(db.p, D->bounds.data(), (P + 1) * 8, cudaMemcpyHostToDevice, c->stream));
+  if (n) {
+    k_unpack_rows<<<ceil_div(n, 256), 256, 0, c->stream>>>(recv[0].p, mx, db.p, P, n, out.p,
+                                                           out.p + n);
+    GBX_LAUNCHED();
+  }
+  if (level) GBX_CUDA(cudaMemcpyAsync(level, out.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (parent) GBX_CUDA(cudaMemcpyAsync(parent, out.p + n, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  comm_sync(c);
+}
+
+}  // namespace
+
 void bfs_mg(gbx_dgraph* D, uint64_t source, int64_t* parent, int64_t* level) {
   NvtxRange nvtx_("gbx.bfs_mg");
   gbx_comm* c = D->comm;
@@ -529,15 +568,58 @@ void bfs_mg(gbx_dgraph* D, uint64_t source, int64_t* parent, int64_t* level) {
     rp[l] = gat[l].p;
   }
   comm_sync(c);
-  int levels = 0;
+  int levels = 0, pushes = 0;
+  int64_t fcount = 1;  // frontier vertices (all ranks)
+  std::vector<DevArray<uint8_t>> cand(L);
+  std::vector<void*> cp(L);
+  // direction: Beamer's edge rule as in gbx_bfs (push while the frontier's
+  // edges are under nnz/alpha, option bfs.alpha), or bfs.cpp:77-78's vertex
+  // rule (push while the frontier has fewer than n/div vertices) when the
+  // option bfs_mg.push_div is set
+  const int64_t div = option(kOptBfsMgPushDiv);
+  const int64_t alpha = option(kOptBfsAlpha);
+  const bool trace = option(kOptBfsTrace) != 0;
   for (;;) {
+    const auto t0 = std::chrono::steady_clock::now();
+    bool pushed = false;
     std::vector<int64_t> found(L, 0);
-    for (int l = 0; l < L; ++l) bfs_shard_level(D->shard[l], front[l].p, nxt[l].p, &found[l]);
+    bool push;
+    if (div > 0 || alpha <= 0) {
+      push = fcount * (div > 0 ? div : 16) < n;
+    } else {
+      std::vector<int64_t> fe(L, 0);
+      for (int l = 0; l < L; ++l) fe[l] = bfs_shard_front_edges(D->shard[l], front[l].p);
+      int64_t tot_e = 0;
+      for (int64_t x : c_allgather_host(c, fe)) tot_e += x;  // the same sum on every rank
+      push = tot_e * alpha < D->nnz;
+    }
+    if (push) {
+      for (int l = 0; l < L; ++l) {
+        if (!cand[l].p) cand[l].alloc(std::max<int64_t>(n, 1));
+        GBX_CUDA(cudaMemsetAsync(cand[l].p, 0, n, c->stream));
+        cp[l] = cand[l].p;
+      }
+      comm_sync(c);
+      for (int l = 0; l < L; ++l) bfs_shard_push_mark(D->shard[l], front[l].p, cand[l].p);
+      c_allreduce(c, cp.data(), n, CollType::U8, CollOp::Max);  // the OR of every rank's marks
+      for (int l = 0; l < L; ++l)
+        bfs_shard_push_level(D->shard[l], cand[l].p, front[l].p, nxt[l].p, &found[l]);
+      ++pushes;
+      pushed = true;
+    } else {
+      for (int l = 0; l < L; ++l) bfs_shard_level(D->shard[l], front[l].p, nxt[l].p, &found[l]);
+    }
     const std::vector<int64_t> all = c_allgather_host(c, found);
     int64_t tot = 0;
     for (int64_t x : all) tot += x;
     ++levels;
+    if (trace)
+      std::fprintf(stderr, "bfs_mg level %d %s frontier %lld -> found %lld  %.1f us\n", levels,
+                   pushed ? "push" : "pull", static_cast<long long>(fcount),
+                   static_cast<long long>(tot),
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
     if (tot == 0) break;
+    fcount = tot;
     // the frontier-bitmap all-gather (north_star): every rank's slice in place
     c_allgather(c, sp.data(), rp.data(), mw * 4);
     for (int l = 0; l < L; ++l)
@@ -548,18 +630,11 @@ void bfs_mg(gbx_dgraph* D, uint64_t source, int64_t* parent, int64_t* level) {
     comm_sync(c);
   }
   D->stats.iterations = levels;
-  D->stats.launches = 2 * levels * L;
+  D->stats.launches = (2 * levels + 3 * pushes) * L;
   D->stats.hot_launches = levels * L;
-  std::vector<std::vector<int64_t>> ps(L), ls(L);
-  for (int l = 0; l < L; ++l) {
-    int64_t rb, re;
-    dgraph_block(D, l, &rb, &re);
-    ps[l].resize(re - rb);
-    ls[l].resize(re - rb);
-    bfs_shard_result(D->shard[l], ps[l].data(), ls[l].data());
-  }
-  gather_rows_i64(D, ps, parent);
-  gather_rows_i64(D, ls, level);
+  if (!parent && !level) return;  // the result stays distributed over the ranks
+  // every rank's owned slice of level / parent, gathered on the device
+  gather_bfs_result(D, parent, level);
 }
 
 // ---- betweenness -------------------------------------------------------------------

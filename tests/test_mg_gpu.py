@@ -107,10 +107,19 @@ def test_triangle_count_mg_rejects_directed():
     assert e.value.code == P.ErrCode.InvalidGraph
 
 
+@pytest.mark.parametrize("push_div", [0, 1, 1 << 30])
 @pytest.mark.parametrize("kind", [U, D])
 @pytest.mark.parametrize("nr", [1, 2, 4, 8])
-def test_bfs_mg(kind, nr):
+def test_bfs_mg(kind, nr, push_div):
+    """push levels (candidate marks + a pull over the candidates) while the
+    frontier is small, pull levels otherwise; push_div 0 = the edge rule, 1 =
+    push (almost) every level, 2^30 = pull only: the same parents and levels
+    as the oracle."""
+    import ctypes as C
+
+    from paper_2104_01661_b200.graph import call
     P.init(0)
+    call("gbx_set_option", b"bfs_mg.push_div", C.c_int64(push_div))
     g = DGraph.rmat(Comm.local(nr), 13, 16, seed=4, kind=kind)
     ref = P.generate_rmat(13, 16, seed=4, kind=kind)
     P.property_rowdegree(ref)
@@ -122,6 +131,7 @@ def test_bfs_mg(kind, nr):
         wp, wl = O.bfs(n, rp, col, int(s))
         assert np.array_equal(lev, wl)
         assert np.array_equal(par, wp)
+    call("gbx_reset_option", b"bfs_mg.push_div")
 
 
 @pytest.mark.parametrize("nr", [1, 2, 3, 4])
