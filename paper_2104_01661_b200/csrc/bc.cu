@@ -30,6 +30,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <vector>
 
@@ -774,8 +775,14 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     unsigned long long fe = hc.e;
     unsigned live = static_cast<unsigned>(hc.c[3]);
     int cur = 0, ucnt = -1;
+    const bool trace = option(kOptBcTrace) != 0;
+    auto tnow = [] { return std::chrono::steady_clock::now(); };
+    auto us = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+      return std::chrono::duration<double, std::micro>(b - a).count();
+    };
     for (int d = 1; static_cast<int64_t>(d) <= n; ++d) {
       if (off.back() == off[off.size() - 2]) break;
+      const auto t0 = tnow();
       GBX_CUDA(cudaMemsetAsync(W.ctl.p, 0, sizeof hc, s));
       BcArgs a{};
       a.own0 = 0;
@@ -846,6 +853,9 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       if (!push) ucnt = hc.c[2];
       GBX_CUDA(cudaMemsetAsync(W.map[cur].p, 0, map_bytes, s));  // depth d-1 map retired
       cur ^= 1;
+      if (trace)
+        std::fprintf(stderr, "bc forward depth %d %s: %d settled, %.1f us\n", d, push ? "push" : "pull",
+                     hc.c[0], us(t0, tnow()));
     }
     // levels: off[d]..off[d+1] lists vertices with some lane at depth d
     const int D = static_cast<int>(off.size()) - 1;  // depths 0..D-1 (last list may be empty)
@@ -865,6 +875,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     for (int d = deepest - 1; d >= 1; --d) {
       const int nl = static_cast<int>(off[d + 1] - off[d]);
       if (nl == 0) continue;
+      const auto t0 = tnow();
       BcArgs a{};
       a.own0 = 0;
       a.own1 = n;
@@ -900,6 +911,10 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
         k_bc_back_hub_fin<<<ceil_div(W.hub_a.nhv, 256), 256, 0, s>>>(a);
         GBX_LAUNCHED();
         launches += 2;
+      }
+      if (trace) {
+        GBX_CUDA(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "bc backward depth %d: %d vertices, %.1f us\n", d, nl, us(t0, tnow()));
       }
     }
     edges += A.nnz;

@@ -73,6 +73,7 @@ enum Opt : int {
   kOptBfsTrace,          // "bfs.trace": per-level %globaltimer log to stderr
   kOptBfsMgPushDiv,      // "bfs_mg.push_div": multi-GPU BFS pushes while the frontier < n/div
   kOptBcAlpha,           // "bc.alpha"
+  kOptBcTrace,           // "bc.trace": per-depth host timing on stderr
   kOptSsspTrace,         // "sssp.trace": per-phase %globaltimer log to stderr
   kOptCount
 };

@@ -27,6 +27,7 @@ constexpr OptDef kDefs[kOptCount] = {
     {"bfs.trace", 0, 0, 1},
     {"bfs_mg.push_div", 0, 0, 1 << 30},        // 0: Beamer's edge rule (bfs.alpha); else bfs.cpp:77-78's vertex rule
     {"bc.alpha", 14, 1, 1 << 20},
+    {"bc.trace", 0, 0, 1},
     {"sssp.trace", 0, 0, 1},
 };
 

@@ -76,16 +76,9 @@ struct PackedEdges {
   const uint32_t* e;
   __device__ __forceinline__ void get(int64_t p, int32_t& v, uint32_t& w) const {
     uint32_t x;
-#ifdef GBX_SSSP_EDGE_EF
-    // the edge stream is read once per relaxation pass: evict-first in L2 so
-    // it does not push the distance array out
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
-                 : "=r"(x) : "l"(e + p), "l"(pol));
-#else
+    // the edge stream bypasses L1 (read once per relaxation pass; measured:
+    // an L1-allocating load 83.5 vs 83.1 ms, an L2 evict-first policy 134 vs 121)
     asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(x) : "l"(e + p));
-#endif
     v = static_cast<int32_t>(x >> 8);
     w = x & 0xffu;
   }
