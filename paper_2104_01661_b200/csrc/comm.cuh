@@ -71,6 +71,7 @@ struct PrMgState {
   std::vector<DevArray<float>> r0, r1;       // [nlocal] local ranks, chunk each
   std::vector<DevArray<float>> xfull, xs;    // NCCL exchange: padded x, own slice
   bool p2p_failed = false;                   // the fused run fell back this call
+  DevArray<int32_t> flag;                    // the ranks' agreement word
 };
 
 // (row << bits | col) keys of one local rank; drop keys (1 << 2*bits) sort last

@@ -204,6 +204,18 @@ void pr_mg_prepare(gbx_dgraph* D) {
     pr_shard_from_block(D->shard[l], c->global_rank(l), P, blocks[l], deg_new[l], new2old[l], nb);
 }
 
+// every rank's flag min-reduced (a barrier as well: no rank returns before
+// every rank arrived); one persistent word, no allocation per call
+int agree(gbx_comm* c, PrMgState& S, int ok) {
+  if (!c->nccl) return ok;  // in-process ranks: one host thread, nothing to agree on
+  if (!S.flag.p) S.flag.alloc(1);
+  GBX_CUDA(cudaMemcpyAsync(S.flag.p, &ok, 4, cudaMemcpyHostToDevice, c->stream));
+  void* fp = S.flag.p;
+  c_allreduce(c, &fp, 1, CollType::I32, CollOp::Min);
+  GBX_CUDA(cudaMemcpy(&ok, S.flag.p, 4, cudaMemcpyDeviceToHost));
+  return ok;
+}
+
 // the fused run (peer stores + device barrier); false when any rank failed
 bool pr_mg_p2p(gbx_dgraph* D, PrMgState& S, double damping, double tol, int itermax, int* iters) {
   NvtxRange nvtx_("gbx.pagerank_mg.fused_run");
@@ -228,13 +240,7 @@ bool pr_mg_p2p(gbx_dgraph* D, PrMgState& S, double damping, double tol, int iter
     ok = 0;
   }
   // every rank zeroed its words before any rank signals; agree on the setup
-  {
-    DevArray<int32_t> f(1);
-    GBX_CUDA(cudaMemcpy(f.p, &ok, 4, cudaMemcpyHostToDevice));
-    std::vector<void*> fp(L, f.p);
-    if (c->nccl) c_allreduce(c, fp.data(), 1, CollType::I32, CollOp::Min);
-    GBX_CUDA(cudaMemcpy(&ok, f.p, 4, cudaMemcpyDeviceToHost));
-  }
+  ok = agree(c, S, ok);
   if (!ok) return false;
   int it = 0;
   try {
@@ -254,13 +260,7 @@ bool pr_mg_p2p(gbx_dgraph* D, PrMgState& S, double damping, double tol, int iter
   } catch (const Error&) {
     ok = 0;  // e.g. a peer timeout: the words are re-zeroed by the next setup
   }
-  {
-    DevArray<int32_t> f(1);
-    GBX_CUDA(cudaMemcpy(f.p, &ok, 4, cudaMemcpyHostToDevice));
-    std::vector<void*> fp(L, f.p);
-    if (c->nccl) c_allreduce(c, fp.data(), 1, CollType::I32, CollOp::Min);
-    GBX_CUDA(cudaMemcpy(&ok, f.p, 4, cudaMemcpyDeviceToHost));
-  }
+  ok = agree(c, S, ok);
   *iters = it;
   return ok != 0;
 }

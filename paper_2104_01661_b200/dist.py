@@ -1,6 +1,16 @@
-"""Multi-GPU drivers: one process per GPU, torch.distributed
-(NCCL over NVLink/NVSwitch) for the exchange, libgbx.so shard kernels for the
-compute.
+"""Multi-GPU drivers written over torch.distributed.
+
+The product multi-GPU path is the C++ one inside libgbx.so -- its own NCCL
+communicator, distributed graphs built locally, gbx_*_mg -- wrapped by
+paper_2104_01661_b200/mg.py (Comm / DGraph) and used by bench.py --gpus N.
+This module keeps the same protocols as Python drivers over the lower-level
+shard calls (gbx_pr_shard_*, gbx_bfs_shard_*, gbx_bc_shard_*): their host
+logic is what tests/test_dist_gloo.py runs on CPU (world size 2 over gloo with
+a numpy backend), and they serve callers that already hold a torch process
+group and a replicated graph.
+
+One process per GPU, torch.distributed (NCCL over NVLink/NVSwitch) for the
+exchange, libgbx.so shard kernels for the compute.
 
 PageRank (config 2): 1D row blocks of the in-degree-relabeled AT, balanced by
 rows + nnz.  Per iteration every rank runs the fused shard step on its rows
