@@ -203,6 +203,7 @@ struct BcArgs {
   int d;
   unsigned lanes;  // lanes still live (their previous level was non-empty)
   int64_t own0, own1;  // vertices this rank finalises (sharded BC; else [0, n))
+  const uint8_t* cand;  // candidate levels of the sharded forward: only these hubs (else NULL)
 };
 
 // forward push over A from the entries of level d-1
@@ -386,6 +387,7 @@ __global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_pull_hub(BcArgs a) {
     const int slot = static_cast<int>(ent & 0xffffffff);
     const int64_t c = ent >> 32;
     const int32_t v = a.hv[slot];
+    if (a.cand && !a.cand[v]) continue;  // no frontier in-neighbour: nothing to sum
     const unsigned um = lanes_unreached(a.lv8[v], a.lanes);
     if (!um) continue;
     const int64_t b0 = a.trp[v] + c * kBcHChunk;
@@ -1064,6 +1066,65 @@ __global__ void k_bc_apply_back(const BcRec* recs, int64_t nrec, int d, int64_t 
     if (level[v * 4 + b] == d) coef[v * 4 + b] = r.x[b];
 }
 
+// ---- candidate levels of the sharded forward sweep (small frontiers): the
+// owned depth-(d-1) vertices mark their out-neighbours (a byte per vertex,
+// max-reduced over the ranks by the driver); each rank pulls only its owned
+// marked vertices -- the same sums as a full pull (a vertex without a
+// frontier in-neighbour sums to nothing), at the frontier's edge count.
+constexpr int64_t kBcMarkHeavy = 2048;
+
+__global__ void k_bc_front_split(const int32_t* list, int64_t nl, int64_t rb, int64_t re,
+                                 const int64_t* rp, int32_t* light, int* nlight, int32_t* heavy,
+                                 int* nheavy, unsigned long long* edges) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  unsigned long long e = 0;
+  if (i < nl) {
+    const int32_t v = list[i];
+    if (v >= rb && v < re) {
+      const int64_t deg = rp[v + 1] - rp[v];
+      e = static_cast<unsigned long long>(deg);
+      if (deg > kBcMarkHeavy) heavy[agg_append(nheavy)] = v;
+      else light[agg_append(nlight)] = v;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kAll, e, o);
+  if ((threadIdx.x & 31) == 0 && e) atomicAdd(edges, e);
+}
+
+__global__ void __launch_bounds__(256) k_bc_mark(const int64_t* rp, const int32_t* col, int64_t n,
+                                                 const int32_t* light, const int* nlight,
+                                                 const int32_t* heavy, const int* nheavy,
+                                                 uint8_t* cand) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int m = *nlight;
+  for (int64_t i = gw; i < m; i += nw) {
+    const int32_t u = light[i];
+    for (int64_t p = rp[u] + lane; p < rp[u + 1]; p += 32) {
+      const int32_t v = __ldg(col + p);
+      GBX_DCHECK(v >= 0 && v < n, "bc mark column", v);
+      cand[v] = 1;
+    }
+  }
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t nt = int64_t(gridDim.x) * blockDim.x;
+  const int mh = *nheavy;
+  for (int h = 0; h < mh; ++h) {
+    const int32_t u = heavy[h];
+    for (int64_t p = rp[u] + t; p < rp[u + 1]; p += nt) {
+      const int32_t v = __ldg(col + p);
+      GBX_DCHECK(v >= 0 && v < n, "bc mark column", v);
+      cand[v] = 1;
+    }
+  }
+}
+
+__global__ void k_bc_cand_list(const uint8_t* cand, int64_t rb, int64_t re, int32_t* out, int* cnt) {
+  const int64_t v = rb + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (v < re && cand[v]) out[agg_append(cnt)] = static_cast<int32_t>(v);
+}
+
 static BcShard& need_shard(gbx_graph* g) {
   if (!g->bc || !g->bc->shard) fail(GBX_MISSING_PROPERTY, "bc shard protocol needs gbx_bc_shard_begin");
   return *g->bc->shard;
@@ -1166,9 +1227,47 @@ void bc_shard_begin(gbx_graph* g, const uint64_t* sources, uint64_t ns, int rank
   if (re_out) *re_out = W.shard->re;
 }
 
+// edges of the owned vertices of the last settled depth (the direction rule's
+// measure) and, with cand != NULL (n bytes, zeroed by the caller), the marks
+// of their out-neighbours
+int64_t bc_shard_mark(gbx_graph* g, uint8_t* cand) {
+  NvtxRange nvtx_("gbx.bc.shard_mark");
+  BcShard& S = need_shard(g);
+  BcWork& W = *g->bc;
+  if (S.fwd_done) return 0;
+  cudaStream_t s = g->stream;
+  const Csr& A = g->A;
+  const int64_t n1 = std::max<int64_t>(A.n, 1);
+  const int d = static_cast<int>(S.off.size()) - 1;  // the depth being built; d-1 settled
+  const int64_t b = S.off[d - 1], nl = S.off[d] - S.off[d - 1];
+  if (!S.ccnt.p) {
+    S.ccnt.alloc(4);
+    S.flight.alloc(n1);
+    S.fheavy.alloc(n1);
+  }
+  Tmp<unsigned long long> e(1, s);
+  GBX_CUDA(cudaMemsetAsync(e.p, 0, 8, s));
+  GBX_CUDA(cudaMemsetAsync(S.ccnt.p, 0, 4 * sizeof(int), s));
+  if (nl > 0) {
+    k_bc_front_split<<<ceil_div(nl, 256), 256, 0, s>>>(W.order.p + b, nl, S.rb, S.re, A.rp.p,
+                                                       S.flight.p, S.ccnt.p, S.fheavy.p,
+                                                       S.ccnt.p + 1, e.p);
+    GBX_LAUNCHED();
+    if (cand) {
+      k_bc_mark<<<device_sms() * 8, 256, 0, s>>>(A.rp.p, A.col.p, A.n, S.flight.p, S.ccnt.p,
+                                                 S.fheavy.p, S.ccnt.p + 1, cand);
+      GBX_LAUNCHED();
+    }
+  }
+  unsigned long long h = 0;
+  GBX_CUDA(cudaMemcpyAsync(&h, e.p, 8, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  return static_cast<int64_t>(h);
+}
+
 // one forward depth on the owned rows; *recs = device records of the owned
 // vertices it settled (valid until the next protocol call)
-void bc_shard_forward(gbx_graph* g, void** recs, int64_t* nrec) {
+void bc_shard_forward(gbx_graph* g, void** recs, int64_t* nrec, const uint8_t* cand) {
   NvtxRange nvtx_("gbx.bc.shard_forward");
   BcShard& S = need_shard(g);
   BcWork& W = *g->bc;
@@ -1202,13 +1301,37 @@ void bc_shard_forward(gbx_graph* g, void** recs, int64_t* nrec) {
   a.map_out = W.map[S.cur ^ 1].p;
   a.own0 = S.rb;
   a.own1 = S.re;
-  if (S.ucnt < 0) {
+  a.cand = cand;
+  const int64_t n1 = std::max<int64_t>(A.n, 1);
+  if (cand) {
+    // candidate level: the owned marked vertices only; their survivors go to
+    // scratch (the owned still-unreached list of the pull levels stays as it
+    // is: the pull skips vertices settled since)
+    if (!S.clist.p) {
+      S.clist.alloc(n1);
+      S.cbin.alloc(n1);
+      S.cscr.alloc(n1);
+    }
+    if (!S.ccnt.p) S.ccnt.alloc(4);
+    GBX_CUDA(cudaMemsetAsync(S.ccnt.p + 2, 0, sizeof(int), s));
+    if (S.re > S.rb)
+      k_bc_cand_list<<<ceil_div(S.re - S.rb, 256), 256, 0, s>>>(cand, S.rb, S.re, S.clist.p,
+                                                                S.ccnt.p + 2);
+    GBX_LAUNCHED();
+    int nc = 0;
+    GBX_CUDA(cudaMemcpyAsync(&nc, S.ccnt.p + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+    bin_list(s, W, S.clist.p, nc, AT, S.cbin.p, W.ucnt.p);
+    a.bins = BcBins{S.cbin.p, W.ucnt.p};
+    a.ul_out = S.cscr.p;
+  } else if (S.ucnt < 0) {
     a.bins = BcBins{S.ownbin.p, S.owncnt.p};
+    a.ul_out = W.ulist[0].p;
   } else {
     bin_list(s, W, W.ulist[0].p, S.ucnt, AT, W.ulist[1].p, W.ucnt.p);
     a.bins = BcBins{W.ulist[1].p, W.ucnt.p};
+    a.ul_out = W.ulist[0].p;
   }
-  a.ul_out = W.ulist[0].p;
   a.hv = HT.hv.p;
   a.hent = S.hent_t.p;
   a.nhv = HT.nhv;
@@ -1225,7 +1348,7 @@ void bc_shard_forward(gbx_graph* g, void** recs, int64_t* nrec) {
   int hc[4];
   GBX_CUDA(cudaMemcpyAsync(hc, W.ctl.p, sizeof hc, cudaMemcpyDeviceToHost, s));
   GBX_CUDA(cudaStreamSynchronize(s));
-  S.ucnt = hc[2];
+  if (!cand) S.ucnt = hc[2];
   if (hc[0]) {
     k_bc_pack_fwd<<<ceil_div(hc[0], 256), 256, 0, s>>>(S.snew.p, hc[0], d, W.level.p, W.sigma.p,
                                                        reinterpret_cast<BcRec*>(S.recs.p));

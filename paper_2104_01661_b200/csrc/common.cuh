@@ -353,7 +353,8 @@ void sssp_prepare(gbx_graph* g);
 void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrality);
 void bc_shard_begin(gbx_graph* g, const uint64_t* sources, uint64_t ns, int rank, int nranks,
                     int64_t* rb_out, int64_t* re_out, const int64_t* bounds = nullptr);
-void bc_shard_forward(gbx_graph* g, void** recs, int64_t* nrec);
+void bc_shard_forward(gbx_graph* g, void** recs, int64_t* nrec, const uint8_t* cand = nullptr);
+int64_t bc_shard_mark(gbx_graph* g, uint8_t* cand);
 void bc_shard_forward_apply(gbx_graph* g, const void* recs, int64_t nrec, int* done);
 void bc_shard_backward(gbx_graph* g, void** recs, int64_t* nrec, int* done);
 void bc_shard_backward_apply(gbx_graph* g, const void* recs, int64_t nrec);

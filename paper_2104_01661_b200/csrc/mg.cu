@@ -657,8 +657,10 @@ void betweenness_mg(gbx_dgraph* D, const uint64_t* sources, uint64_t ns, double*
     GBX_CUDA(cudaMemsetAsync(acc[l].p, 0, acc[l].bytes(), c->stream));
   }
   comm_sync(c);
-  int levels = 0;
-  std::vector<DevArray<uint8_t>> all;
+  int levels = 0, cand_levels = 0;
+  std::vector<DevArray<uint8_t>> all, cand(L);
+  std::vector<void*> cp(L);
+  const int64_t alpha = option(kOptBcAlpha);
   for (uint64_t b0 = 0; b0 < ns; b0 += 4) {  // batches of 4 (the lane width)
     const uint64_t nb = std::min<uint64_t>(4, ns - b0);
     for (int l = 0; l < L; ++l)
@@ -667,9 +669,27 @@ void betweenness_mg(gbx_dgraph* D, const uint64_t* sources, uint64_t ns, double*
     for (;;) {  // forward: one record exchange per depth
       std::vector<const void*> recs(L);
       std::vector<int64_t> nrec(L);
+      // direction: while the settled depth's edges are under nnz/alpha (the
+      // single-GPU push rule) the ranks pull only the marked candidates
+      std::vector<int64_t> fe(L, 0);
+      for (int l = 0; l < L; ++l) fe[l] = bc_shard_mark(D->shard[l], nullptr);
+      int64_t tot_e = 0;
+      for (int64_t x : c_allgather_host(c, fe)) tot_e += x;
+      const bool candidates = alpha > 0 && tot_e * alpha < D->nnz;
+      if (candidates) {
+        for (int l = 0; l < L; ++l) {
+          if (!cand[l].p) cand[l].alloc(std::max<int64_t>(n, 1));
+          GBX_CUDA(cudaMemsetAsync(cand[l].p, 0, n, c->stream));
+          cp[l] = cand[l].p;
+        }
+        comm_sync(c);
+        for (int l = 0; l < L; ++l) bc_shard_mark(D->shard[l], cand[l].p);
+        c_allreduce(c, cp.data(), n, CollType::U8, CollOp::Max);
+        ++cand_levels;
+      }
       for (int l = 0; l < L; ++l) {
         void* p = nullptr;
-        bc_shard_forward(D->shard[l], &p, &nrec[l]);
+        bc_shard_forward(D->shard[l], &p, &nrec[l], candidates ? cand[l].p : nullptr);
         recs[l] = p;
       }
       const int64_t tot = gather_records(c, recs, nrec, kRec, all);
@@ -708,6 +728,7 @@ void betweenness_mg(gbx_dgraph* D, const uint64_t* sources, uint64_t ns, double*
   for (int l = 0; l < L; ++l) ap[l] = acc[l].p;
   c_allreduce(c, ap.data(), n, CollType::F64, CollOp::Sum);
   D->stats.iterations = levels;
+  D->stats.hot_launches = cand_levels;
   D->stats.work_units = D->nnz;
   if (centrality && n) GBX_CUDA(cudaMemcpy(centrality, acc[0].p, n * 8, cudaMemcpyDeviceToHost));
 }

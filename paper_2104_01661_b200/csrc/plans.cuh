@@ -189,6 +189,10 @@ struct BcShard {
   DevArray<unsigned char> recs;  // packed 40-byte records
   DevArray<int64_t> hent_t, hent_a;  // chunks of the owned hub rows
   int nhent_t = 0, nhent_a = 0;
+  // candidate levels (small frontiers): marked owned candidates, their binned
+  // copy, the pull's survivor scratch, the frontier lists of the mark pass
+  DevArray<int32_t> clist, cbin, cscr, flight, fheavy;
+  DevArray<int> ccnt;
 };
 
 // Betweenness workspaces (bc.cu).
