@@ -12,6 +12,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "sort.cuh"
 
 namespace gbx {
 
@@ -301,24 +302,13 @@ void compute_transpose(cudaStream_t s, const Csr& A, Csr& T) {
   const size_t es = has_val ? domain_size(A.domain) : 0;
   const uint32_t* kin = reinterpret_cast<const uint32_t*>(A.col.p);
   Tmp<uint32_t> kout(A.nnz, s);
-  size_t tb = 0;
   if (!has_val) {
-    GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout.p, rowid.p, T.col.p, A.nnz, 0,
-                                             bits, s));
-    Tmp<uint8_t> t(tb, s);
-    GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kin, kout.p, rowid.p, T.col.p, A.nnz, 0,
-                                             bits, s));
+    radix_sort_pairs<uint32_t, int32_t>(s, kin, kout.p, rowid.p, T.col.p, A.nnz, 0, bits);
   } else {
     Tmp<int64_t> pin(A.nnz, s), pout(A.nnz, s);
     k_iota64<<<ceil_div(A.nnz, 256), 256, 0, s>>>(pin.p, A.nnz);
     GBX_LAUNCHED();
-    GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout.p, pin.p, pout.p, A.nnz, 0,
-                                             bits, s));
-    {
-      Tmp<uint8_t> t(tb, s);
-      GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kin, kout.p, pin.p, pout.p, A.nnz, 0,
-                                               bits, s));
-    }
+    radix_sort_pairs<uint32_t, int64_t>(s, kin, kout.p, pin.p, pout.p, A.nnz, 0, bits);
     T.val.alloc(A.nnz * es);
     const int g = ceil_div(A.nnz, 256);
     switch (es) {
@@ -403,10 +393,7 @@ void sort_ids_by_key(cudaStream_t s, const int32_t* key, int64_t n, bool ascendi
   k_flip_keys<<<ceil_div(n, 256), 256, 0, s>>>(key, k0.p, n, ascending);
   k_iota<<<ceil_div(n, 256), 256, 0, s>>>(v0.p, n);
   GBX_LAUNCHED();
-  size_t tb = 0;
-  GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.p, k1.p, v0.p, perm.p, n, 0, 32, s));
-  Tmp<uint8_t> t(tb, s);
-  GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, k0.p, k1.p, v0.p, perm.p, n, 0, 32, s));
+  radix_sort_pairs<uint32_t, int32_t>(s, k0.p, k1.p, v0.p, perm.p, n, 0, 32);
 }
 
 // ---- seeded generators (bit-identical to oracle/oracle.c) -------------------------
@@ -503,11 +490,8 @@ __global__ void k_run_heads(const uint64_t* keys, const int32_t* w, int64_t m,
 
 // sort 64-bit keys in place (double buffer); returns the buffer holding the result
 uint64_t* sort_keys(cudaStream_t s, uint64_t* keys, uint64_t* alt, int64_t m, int end_bit) {
-  size_t tb = 0;
   cub::DoubleBuffer<uint64_t> kb(keys, alt);
-  GBX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, m, 0, end_bit, s));
-  Tmp<uint8_t> t(tb, s);
-  GBX_CUDA(cub::DeviceRadixSort::SortKeys(t.p, tb, kb, m, 0, end_bit, s));
+  radix_sort_keys(s, kb, m, 0, end_bit);
   return kb.Current();
 }
 
@@ -543,7 +527,6 @@ static void keys_to_graph(gbx_graph* g, int64_t n, int bits, uint64_t* keys, int
                           int64_t m, int kind) {
   cudaStream_t s = g->stream;
   // sort
-  size_t tb = 0;
   Tmp<uint64_t> kalt(m, s);
   Tmp<int32_t> walt(w ? m : 0, s);
   cub::DoubleBuffer<uint64_t> kb(keys, kalt.p);
@@ -551,13 +534,8 @@ static void keys_to_graph(gbx_graph* g, int64_t n, int bits, uint64_t* keys, int
   // drop keys (self-loops) are 1 << 2*bits: they sort after every edge
   const int end_bit = 2 * bits + 1;
   const uint64_t drop = uint64_t(1) << (2 * bits);
-  if (w) GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, wb, m, 0, end_bit, s));
-  else GBX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, m, 0, end_bit, s));
-  {
-    Tmp<uint8_t> t(tb, s);
-    if (w) GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kb, wb, m, 0, end_bit, s));
-    else GBX_CUDA(cub::DeviceRadixSort::SortKeys(t.p, tb, kb, m, 0, end_bit, s));
-  }
+  if (w) radix_sort_pairs(s, kb, wb, m, 0, end_bit);
+  else radix_sort_keys(s, kb, m, 0, end_bit);
   Tmp<uint8_t> flag(m, s);
   Tmp<int32_t> wmin(w ? m : 0, s);
   k_run_heads<<<ceil_div(m, 256), 256, 0, s>>>(kb.Current(), w ? wb.Current() : nullptr, m,
@@ -565,7 +543,7 @@ static void keys_to_graph(gbx_graph* g, int64_t n, int bits, uint64_t* keys, int
   GBX_LAUNCHED();
   Tmp<uint64_t> uk(m, s);
   Tmp<int64_t> nsel(1, s);
-  tb = 0;
+  size_t tb = 0;
   GBX_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, kb.Current(), flag.p, uk.p, nsel.p, m, s));
   int64_t nnz = 0;
   {

@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "sort.cuh"
 
 namespace gbx {
 
@@ -241,19 +242,14 @@ void build_from_coo(gbx_graph* g, int64_t nrows, int64_t ncols, int64_t m, const
   // stable sort of the keys carrying the tuple index
   cub::DoubleBuffer<uint64_t> kb(k0.p, k1.p);
   cub::DoubleBuffer<int64_t> ib(i0.p, i1.p);
-  size_t tb = 0;
-  GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, ib, m, 0, 2 * bits, s));
-  {
-    Tmp<uint8_t> t(tb, s);
-    GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kb, ib, m, 0, 2 * bits, s));
-  }
+  radix_sort_pairs(s, kb, ib, m, 0, 2 * bits);
   const uint64_t* keys = kb.Current();
   const int64_t* idx = ib.Current();
   Tmp<int32_t> head(m, s);
   Tmp<int64_t> seg(m, s);
   k_run_heads<<<ceil_div(m, 256), 256, 0, s>>>(keys, m, head.p);
   GBX_LAUNCHED();
-  tb = 0;
+  size_t tb = 0;
   GBX_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, head.p, seg.p, m, s));
   {
     Tmp<uint8_t> t(tb, s);

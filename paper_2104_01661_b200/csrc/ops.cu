@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "sort.cuh"
 
 namespace gbx {
 
@@ -307,12 +308,7 @@ void ensure_transpose(gbx_mat* A) {
     GBX_LAUNCHED();
     cub::DoubleBuffer<uint64_t> kb(k0.p, k1.p);
     cub::DoubleBuffer<int64_t> pb(p0.p, p1.p);
-    size_t tb = 0;
-    GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, pb, m, 0, 2 * bits, s));
-    {
-      Tmp<uint8_t> t(tb, s);
-      GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kb, pb, m, 0, 2 * bits, s));
-    }
+    radix_sort_pairs(s, kb, pb, m, 0, 2 * bits);
     rowptr_from_sorted_keys(s, A->ncols, bits, kb.Current(), m, A->trp.p, A->tcol.p);
     k_gather_u64<<<ceil_div(m, kT), kT, 0, s>>>(A->val.p, pb.Current(), m, A->tval.p);
     GBX_LAUNCHED();
@@ -828,12 +824,7 @@ void mxm_op(gbx_mat* out, gbx_mat* C, const gbx_desc* desc, int sr, int sdom, gb
       k_expand<<<ceil_div(nr, kT), kT, 0, st>>>(Av, Bv, off.p, s, bits, k0.p, v0.p);
       GBX_LAUNCHED();
       cub::DoubleBuffer<uint64_t> kb(k0.p, k1.p), vb(v0.p, v1.p);
-      tb = 0;
-      GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, np, 0, 2 * bits, st));
-      {
-        Tmp<uint8_t> t(tb, st);
-        GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kb, vb, np, 0, 2 * bits, st));
-      }
+      radix_sort_pairs(st, kb, vb, np, 0, 2 * bits);
       Tmp<int32_t> head(np, st);
       Tmp<int64_t> seg(np, st);
       k_heads64<<<ceil_div(np, kT), kT, 0, st>>>(kb.Current(), np, head.p);
@@ -882,12 +873,7 @@ void mxm_op(gbx_mat* out, gbx_mat* C, const gbx_desc* desc, int sr, int sdom, gb
   }
   cub::DoubleBuffer<uint64_t> kb(k0.p, k1.p);
   cub::DoubleBuffer<int64_t> rb(r0.p, r1.p);
-  size_t tb = 0;
-  GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, rb, m, 0, 2 * bits, st));
-  {
-    Tmp<uint8_t> t(tb, st);
-    GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kb, rb, m, 0, 2 * bits, st));
-  }
+  radix_sort_pairs(st, kb, rb, m, 0, 2 * bits);
   Tmp<uint8_t> keep(m, st);
   Tmp<uint64_t> ov(m, st);
   k_post_mat<<<ceil_div(m, kT), kT, 0, st>>>(
@@ -898,7 +884,7 @@ void mxm_op(gbx_mat* out, gbx_mat* C, const gbx_desc* desc, int sr, int sdom, gb
   Tmp<uint64_t> ok(m, st);
   Tmp<int64_t> cnt(1, st);
   out->val.alloc(m);
-  tb = 0;
+  size_t tb = 0;
   GBX_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, kb.Current(), keep.p, ok.p, cnt.p, m, st));
   {
     Tmp<uint8_t> t(tb, st);

@@ -37,6 +37,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "sort.cuh"
 #include "plans.cuh"
 
 namespace gbx {
@@ -817,8 +818,24 @@ __global__ void k_pr_gather_a_short(const int64_t* arp, const int32_t* acol,
   }
 }
 
+// plan phases on stderr (option pagerank.trace; synchronises per phase)
+struct PlanTimer {
+  cudaStream_t s;
+  bool on;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    GBX_CUDA(cudaStreamSynchronize(s));
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "pagerank plan: %-28s %8.1f us\n", what,
+                 std::chrono::duration<double, std::micro>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 // relabeled AT (rows by descending in-degree) + relabeled out-degree
 static void build_relabeled(gbx_graph* g, PrPlan& P) {
+  PlanTimer tm{g->stream, option(kOptPrTrace) != 0};
   cudaStream_t s = g->stream;
   const Csr& A = g->A;
   const int64_t n = A.n, nnz = A.nnz;
@@ -837,7 +854,9 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
   } else {
     compute_degrees(s, A, len, false);
   }
+  tm.mark("in-degrees");
   sort_ids_by_key(s, len.p, n, false, P.new2old);
+  tm.mark("relabel sort");
   P.old2new.alloc(std::max<int64_t>(n, 1));
   P.deg.alloc(std::max<int64_t>(n, 1));
   if (n) {
@@ -890,17 +909,17 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
     k_pr_gather_a_short<<<device_sms() * 8, 256, 0, s>>>(A.rp.p, A.col.p, P.new2old.p,
                                                           P.old2new.p, prp.p, n, kc.p, vr.p);
     GBX_LAUNCHED();
-    size_t tb = 0;
-    GBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kc.p, kc2.p, vr.p,
-                                             reinterpret_cast<uint32_t*>(P.tcol.p), nnz, 0, bits,
-                                             s));
-    {
-      Tmp<uint8_t> t(tb, s);
-      GBX_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kc.p, kc2.p, vr.p,
-                                               reinterpret_cast<uint32_t*>(P.tcol.p), nnz, 0,
-                                               bits, s));
-    }
-    rowptr_from_sorted_rows32(s, n, kc2.p, nnz, P.trp.p);
+    tm.mark("gather A rows (new order)");
+    // double buffers (the value alternate is the plan's own tcol) and a 32-bit item count
+    cub::DoubleBuffer<uint32_t> kb(kc.p, kc2.p);
+    cub::DoubleBuffer<uint32_t> vb(vr.p, reinterpret_cast<uint32_t*>(P.tcol.p));
+    radix_sort_pairs(s, kb, vb, nnz, 0, bits);
+    if (vb.Current() != reinterpret_cast<uint32_t*>(P.tcol.p))
+      GBX_CUDA(cudaMemcpyAsync(P.tcol.p, vb.Current(), nnz * 4, cudaMemcpyDeviceToDevice, s));
+    const uint32_t* sorted_rows = kb.Current();
+    tm.mark("radix sort by new column");
+    rowptr_from_sorted_rows32(s, n, sorted_rows, nnz, P.trp.p);
+    tm.mark("row pointers");
   } else {
     GBX_CUDA(cudaMemsetAsync(P.trp.p, 0, (n + 1) * sizeof(int64_t), s));
   }
@@ -929,13 +948,17 @@ void pagerank_prepare(gbx_graph* g) {
   require_rowdeg(g, "pagerank_gap");
   if (g->pr) return;
   auto P = std::make_unique<PrPlan>();
+  PlanTimer tm{g->stream, option(kOptPrTrace) != 0};
   build_relabeled(g, *P);
+  tm.mark("relabeled AT (total)");
   plan_rows(g, *P, 0, P->n);
+  tm.mark("work units / bins");
   for (int b = 0; b < 2; ++b) {
     P->r[b].alloc(std::max<int64_t>(g->A.n, 1));
     P->x[b].alloc(std::max<int64_t>(g->A.n, 1));
   }
   P->out.alloc(std::max<int64_t>(g->A.n, 1));
+  tm.mark("vectors");
   g->pr = std::move(P);
 }
 
