@@ -74,7 +74,8 @@ enum Opt : int {
   kOptBfsMgPushDiv,      // "bfs_mg.push_div": multi-GPU BFS pushes while the frontier < n/div
   kOptBcAlpha,           // "bc.alpha"
   kOptBcTrace,           // "bc.trace": per-depth host timing on stderr
-  kOptSsspTrace,         // "sssp.trace": per-phase %globaltimer log to stderr
+  kOptSsspTrace,         // "sssp.trace": per-phase %globaltimer log to stderr (2: + device printf)
+  kOptSsspPullPct,       // "sssp.pull_pct": heavy pass by pull when pops*100 > pct*unpopped (0: never)
   kOptCount
 };
 int64_t option(Opt o);

@@ -28,7 +28,8 @@ constexpr OptDef kDefs[kOptCount] = {
     {"bfs_mg.push_div", 0, 0, 1 << 30},        // 0: Beamer's edge rule (bfs.alpha); else bfs.cpp:77-78's vertex rule
     {"bc.alpha", 14, 1, 1 << 20},
     {"bc.trace", 0, 0, 1},
-    {"sssp.trace", 0, 0, 1},
+    {"sssp.trace", 0, 0, 2},
+    {"sssp.pull_pct", 100, 0, 1 << 20},
 };
 
 std::atomic<int64_t> g_val[kOptCount] = {};

@@ -136,8 +136,6 @@ struct SsspLane {
   DevArray<uint32_t> bbits;
   DevArray<int> bcnt;
   int nb_alloc = 0;
-  DevArray<int32_t> sq;            // settled list of the current bucket
-  DevArray<uint32_t> sbits;        // its membership bitmap
   DevArray<double> out;            // fp64 copy of the distances for the host
   cudaStream_t stream = nullptr;   // owned (lanes > 0)
   ~SsspLane() {
@@ -165,6 +163,10 @@ struct SsspPlan {
   // per-vertex edge ranges {begin, light end, end, 0} (nnz < 2^32): one 16-byte
   // load per popped vertex instead of row_ptr[u], row_ptr[u+1] and nlight[u]
   DevArray<uint4> vmeta;
+  // heavy in-edges (w > split_delta) of every vertex, packed (u:24 | w:8) and
+  // ascending in w within a row: the pull form of a bucket's heavy pass
+  // (packed plans only; empty when nnz >= 2^32)
+  DevArray<uint32_t> hin_rp, hin;
   std::vector<std::unique_ptr<SsspLane>> lanes;  // [0]: the single-source call's
 };
 

@@ -35,6 +35,7 @@
 
 #include "common.cuh"
 #include "plans.cuh"
+#include "sort.cuh"
 #include "warpqueue.cuh"
 
 namespace cg = cooperative_groups;
@@ -373,15 +374,19 @@ struct SsspBArgs {
   unsigned long long* relax;
   // light/heavy split (Delta-stepping proper, sssp.cpp:30-33, 66-106): every
   // row holds its light edges (w <= delta) first, nl[u] of them.  Near
-  // iterations relax light edges only; each vertex that entered the bucket is
-  // recorded once in the settled list sq (dedup bitmap sbits) and, when the
-  // bucket drains, its heavy edges are relaxed ONCE from its final distance
-  // (they always land in a later bucket).  nl == nullptr: every edge in the
-  // near phase (label-correcting).
+  // iterations relax light edges only and, when the bucket drains, the heavy
+  // edges of every vertex it settled are relaxed ONCE from their final
+  // distances (they always land in a later bucket).  nl == nullptr: every edge
+  // in the near phase (label-correcting).
   const int32_t* nl;
   const uint4* vm;     // {begin, light end, end, 0} per vertex, or nullptr
-  int32_t* sq;
-  uint32_t* sbits;
+  // pull form of the heavy pass (packed edges): every still-unsettled vertex
+  // scans its heavy in-edges in ascending weight until lo_k + w >= its
+  // distance; chosen for a bucket when its pops * 100 > pull_pct * (vertices
+  // not yet popped), i.e. when the settled set outweighs what is left
+  const uint32_t* hrp;
+  const uint32_t* hin;
+  int pull_pct;
   int light_group;     // lanes per vertex in the light (near) phase: 1, 2 or 4
   int trace;
   unsigned long long* tlog;  // optional: [2i] %globaltimer, [2i+1] kind<<32 | size (debug)
@@ -474,6 +479,9 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
   const bool tl = a.tlog && blockIdx.x == 0 && threadIdx.x == 0;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   int tn = 0;
+  // pops of the current bucket / of all buckets so far (every thread reads each
+  // near iteration's count, so every thread takes the same push / pull decision)
+  int64_t popped_k = 0, popped_all = 0;
   // relax the edges of the vertices list[0, cnt): phase 0 all edges, 1 light
   // edges (and record the vertex in the settled list), 2 heavy edges.  4 lanes
   // per vertex (8 vertices per warp), each lane 4 edges per round: 4
@@ -611,6 +619,81 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
       }
     }
   };
+  // pull form of the heavy pass (packed plans, u32 distances): the unsettled
+  // vertices win[0, c) (distances in win[128 + i]) scan their heavy in-edges in
+  // ascending weight, 4 lanes per vertex, 4 edges per lane and round.  Only a
+  // source settled in bucket <= k counts -- its improvement then
+  // lands within nb-1 buckets, as a push would -- and the scan stops at the
+  // first weight with lo + w >= the lane's best (weights ascend, every settled
+  // source of bucket k has du >= lo, earlier buckets already pushed).  The
+  // vertex is written by its own group only (no atomics): plain store of the
+  // minimum, queued in its bucket unless its old distance was already there.
+  auto pull_local = [&](const int32_t* win, int c, uint32_t lo, unsigned long long& nrel) {
+    for (int base = 0; base < c; base += 8) {
+      const int qi = base + g4;
+      bool active = qi < c;
+      const int32_t v = active ? win[qi] : 0;
+      const uint32_t dv = active ? static_cast<uint32_t>(win[128 + qi]) : 0u;
+      uint32_t p = 0, e = 0;
+      if (active) {
+        p = __ldg(a.hrp + v);
+        e = __ldg(a.hrp + v + 1);
+      }
+      if (p >= e) active = false;
+      uint32_t best = dv;
+      while (__any_sync(kFullW, active)) {
+        uint32_t x[4];
+        bool ok[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint32_t q = p + s4 + 4 * q4;
+          ok[q4] = active && q < e;
+          x[q4] = 0;
+          if (ok[q4])
+            asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(x[q4]) : "l"(a.hin + q));
+        }
+        bool stop = !active;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          if (ok[q4] && static_cast<uint64_t>(lo) + (x[q4] & 0xffu) >= best) {
+            ok[q4] = false;
+            stop = true;
+          }
+        uint32_t du[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          GBX_DCHECK(!ok[q4] || static_cast<int64_t>(x[q4] >> 8) < a.n, "sssp in-edge source", x[q4] >> 8);
+          du[q4] = ok[q4] ? __ldcg(reinterpret_cast<const uint32_t*>(a.dist) + (x[q4] >> 8))
+                          : 0xffffffffu;
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          if (ok[q4]) {
+            ++nrel;
+            if (du[q4] != 0xffffffffu && bucket_k<D>(static_cast<D>(du[q4]), a) <= k) {
+              const uint32_t nd = du[q4] + (x[q4] & 0xffu);
+              best = nd < best ? nd : best;
+            }
+          }
+        p += 16;
+        if (stop || p >= e) active = false;
+      }
+      // the group's minimum (4 lanes, uniform shuffles)
+      uint32_t o = __shfl_xor_sync(kFullW, best, 1);
+      best = o < best ? o : best;
+      o = __shfl_xor_sync(kFullW, best, 2);
+      best = o < best ? o : best;
+      bool push = false;
+      int bidx = 0;
+      if (qi < c && s4 == 0 && best < dv) {
+        reinterpret_cast<uint32_t*>(a.dist)[v] = best;
+        const int64_t kb = bucket_k<D>(static_cast<D>(best), a);
+        bidx = static_cast<int>(kb & nbm);
+        push = dv == 0xffffffffu || bucket_k<D>(static_cast<D>(dv), a) != kb;
+      }
+      bucq.push(push, v, bidx, a.bq, a.cap, a.bcnt, a.nb);
+    }
+  };
   for (int guard = 0;; ++guard) {
     if (guard > (1 << 28)) break;
     // ---------------- near iterations inside bucket k
@@ -623,6 +706,7 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
         ++tn;
       }
       if (nq == 0) break;
+      popped_k += nq;
       if (leader) {
         a.ctl[(t + 2) % 3] = 0;
         a.ctl[4] += 1;
@@ -659,7 +743,55 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
     // final distance lies in bucket k -- cheaper than recording them (one more
     // atomic per near visit); each warp compacts its 32-vertex window into
     // shared memory and relaxes the heavy edges 8 vertices at a time
-    if (a.nl) {
+    popped_all += popped_k;
+    const bool pull = a.hin != nullptr &&
+                      popped_k * 100 > static_cast<int64_t>(a.pull_pct) * (a.n - popped_all);
+    popped_k = 0;
+    if (tl && tn < a.tlog_cap) {
+      a.tlog[2 * tn] = sssp_gtimer();
+      a.tlog[2 * tn + 1] = (1ull << 62) | (pull ? 1ull : 0ull);
+      ++tn;
+    }
+    if (a.nl && pull) {
+      if constexpr (std::is_same<D, uint32_t>::value) {
+        unsigned long long nrel = 0;
+        int32_t* win = s_settle[threadIdx.x >> 5];
+        // a lower bound of bucket k's distances (exact for an integral delta;
+        // one below the rounded product otherwise: the pruning stays safe)
+        const double lod = a.idelta ? static_cast<double>(k) * a.idelta
+                                    : floor(static_cast<double>(k) * a.delta) - 1.0;
+        const uint32_t lo = lod <= 0.0 ? 0u
+                            : lod >= 4294967295.0 ? 0xffffffffu : static_cast<uint32_t>(lod);
+        for (int64_t base = gwarp * 128; base < a.n; base += nwarps * 128) {
+          uint32_t dv[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int64_t v = base + 32 * j + lane;
+            dv[j] = v < a.n ? __ldcg(reinterpret_cast<const uint32_t*>(a.dist) + v) : 0u;
+          }
+          int c = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            // unsettled (a later bucket) or unreached
+            const bool in = base + 32 * j + lane < a.n &&
+                            (dv[j] == 0xffffffffu || bucket_k<D>(static_cast<D>(dv[j]), a) > k);
+            const unsigned m = __ballot_sync(kFullW, in);
+            if (in) {
+              const int pos = c + __popc(m & ((1u << lane) - 1));
+              win[pos] = static_cast<int32_t>(base + 32 * j + lane);
+              win[128 + pos] = static_cast<int32_t>(dv[j]);
+            }
+            c += __popc(m);
+          }
+          __syncwarp();
+          if (c) pull_local(win, c, lo, nrel);
+          __syncwarp();
+        }
+        bucq.flush(a.bq, a.cap, a.bcnt, a.nb);
+        sssp_count_relax(a.relax, nrel);
+        grid.sync();
+      }
+    } else if (a.nl) {
       unsigned long long nrel = 0;
       int32_t* win = s_settle[threadIdx.x >> 5];
       for (int64_t base = gwarp * 128; base < a.n; base += nwarps * 128) {
@@ -857,6 +989,83 @@ __global__ void k_vmeta(const int64_t* rp, const int32_t* nl, int64_t n, uint4* 
   vm[u] = make_uint4(b, b + static_cast<uint32_t>(nl[u]), static_cast<uint32_t>(rp[u + 1]), 0u);
 }
 
+// heavy in-edges for the pull form of the heavy pass: (v:24 | w:8) keys with
+// the source u as value, one thread per (light-first) row
+__global__ void k_heavy_in_keys(const int64_t* rp, const int32_t* nl, int64_t n,
+                                const uint32_t* pe, const int64_t* hoff, uint32_t* key,
+                                uint32_t* src) {
+  const int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (u >= n) return;
+  int64_t q = hoff[u];
+  for (int64_t p = rp[u] + nl[u]; p < rp[u + 1]; ++p, ++q) {
+    const uint32_t x = pe[p];
+    key[q] = ((x >> 8) << 8) | (x & 0xffu);
+    src[q] = static_cast<uint32_t>(u);
+  }
+}
+__global__ void k_heavy_count(const int64_t* rp, const int32_t* nl, int64_t n, int64_t* cnt) {
+  const int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (u < n) cnt[u] = rp[u + 1] - rp[u] - nl[u];
+  if (u == n) cnt[u] = 0;
+}
+__global__ void k_heavy_in_rows(const uint32_t* key, int64_t h, uint32_t* cnt) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < h) atomicAdd(&cnt[key[i] >> 8], 1u);
+}
+__global__ void k_heavy_in_pack(const uint32_t* key, const uint32_t* src, int64_t h,
+                                uint32_t* hin) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < h) hin[i] = (src[i] << 8) | (key[i] & 0xffu);
+}
+
+// heavy in-edge CSR of the packed plan for its split delta: rows by target,
+// every row ascending in (w, u) -- a stable sort of (v, w) keys generated in
+// source order
+static void build_heavy_in(gbx_graph* g, SsspPlan& P) {
+  cudaStream_t s = g->stream;
+  const Csr& A = g->A;
+  const int64_t n = A.n;
+  P.hin_rp.release();
+  P.hin.release();
+  if (!P.packed || n == 0 || A.nnz == 0 || A.nnz >= (int64_t(1) << 32)) return;
+  Tmp<int64_t> hoff(n + 1, s);
+  {
+    Tmp<int64_t> hc(n + 1, s);
+    k_heavy_count<<<ceil_div(n + 1, 256), 256, 0, s>>>(A.rp.p, P.nlight.p, n, hc.p);
+    GBX_LAUNCHED();
+    size_t tb = 0;
+    GBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, hc.p, hoff.p, n + 1, s));
+    Tmp<uint8_t> t(tb, s);
+    GBX_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, hc.p, hoff.p, n + 1, s));
+  }
+  int64_t h = 0;
+  GBX_CUDA(cudaMemcpyAsync(&h, hoff.p + n, 8, cudaMemcpyDeviceToHost, s));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  P.hin_rp.alloc(n + 1);
+  P.hin.alloc(std::max<int64_t>(h, 1));
+  Tmp<uint32_t> cnt(n + 1, s);
+  GBX_CUDA(cudaMemsetAsync(cnt.p, 0, (n + 1) * 4, s));
+  if (h > 0) {
+    Tmp<uint32_t> k0(h, s), k1(h, s), v0(h, s), v1(h, s);
+    k_heavy_in_keys<<<ceil_div(n, 256), 256, 0, s>>>(A.rp.p, P.nlight.p, n, P.packed_edges.p,
+                                                     hoff.p, k0.p, v0.p);
+    GBX_LAUNCHED();
+    cub::DoubleBuffer<uint32_t> kb(k0.p, k1.p), vb(v0.p, v1.p);
+    radix_sort_pairs(s, kb, vb, h, 0, 32);
+    k_heavy_in_rows<<<ceil_div(h, 256), 256, 0, s>>>(kb.Current(), h, cnt.p);
+    GBX_LAUNCHED();
+    k_heavy_in_pack<<<ceil_div(h, 256), 256, 0, s>>>(kb.Current(), vb.Current(), h, P.hin.p);
+    GBX_LAUNCHED();
+  }
+  {
+    size_t tb = 0;
+    GBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, P.hin_rp.p, n + 1, s));
+    Tmp<uint8_t> t(tb, s);
+    GBX_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, cnt.p, P.hin_rp.p, n + 1, s));
+  }
+  GBX_CUDA(cudaStreamSynchronize(s));
+}
+
 // (re)partition the plan's edges for delta; any row order is valid for the
 // label-correcting sweep, so the packed edges are partitioned in place of the
 // plan's own copy and re-partitioned when delta changes
@@ -906,6 +1115,7 @@ static void ensure_split(gbx_graph* g, SsspPlan& P, double delta) {
     GBX_LAUNCHED();
   }
   GBX_CUDA(cudaStreamSynchronize(s));
+  build_heavy_in(g, P);
   P.split_delta = delta;
 }
 
@@ -926,8 +1136,6 @@ static SsspLane& ensure_lane(gbx_graph* g, SsspPlan& P, int i) {
   L->ctl.alloc(10);
   L->lohi.alloc(3);
   L->relax.alloc(1);
-  L->sq.alloc(n1 + 1);
-  L->sbits.alloc((n1 + 31) / 32);
   if (i > 0) GBX_CUDA(cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking));
   P.lanes[i] = std::move(L);
   return *P.lanes[i];
@@ -1085,11 +1293,13 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, SsspLane& L, cudaStream_t s, 
       b.light_group = 2;  // 2 lanes per vertex in the light phase (1 / 4: 128 / 124 vs 121 ms)
       b.nl = P.nlight.p;
       b.vm = P.vmeta.p;
-      b.sq = L.sq.p;
-      b.sbits = L.sbits.p;
-      GBX_CUDA(cudaMemsetAsync(L.sbits.p, 0, L.sbits.bytes(), s));
+      if (P.hin.p && option(kOptSsspPullPct) > 0) {
+        b.hrp = P.hin_rp.p;
+        b.hin = P.hin.p;
+        b.pull_pct = static_cast<int>(option(kOptSsspPullPct));
+      }
     }
-    b.trace = option(kOptSsspTrace) ? 1 : 0;
+    b.trace = option(kOptSsspTrace) >= 2 ? 1 : 0;
     const bool tlog_on = option(kOptSsspTrace) != 0;
     DevArray<unsigned long long> tlog;
     if (tlog_on) {
@@ -1113,8 +1323,12 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, SsspLane& L, cudaStream_t s, 
       for (int i = 0; i + 1 < 4096 && t[2 * i + 2]; ++i) {
         const unsigned long long tag = t[2 * i + 1];
         const double us = (t[2 * i + 2] - t[2 * i]) / 1e3;
-        if (tag >> 63)
+        if ((tag >> 62) == 2)
           std::fprintf(stderr, "sssp jump  cnt=%u %.1fus\n", static_cast<unsigned>(tag), us);
+        else if ((tag >> 62) == 1)
+          std::fprintf(stderr, "sssp heavy %s %.1fus\n", (tag & 1) ? "pull" : "push", us);
+        else if ((tag >> 62) == 3)
+          break;
         else
           std::fprintf(stderr, "sssp near k=%llu nq=%u %.1fus\n", tag >> 32,
                        static_cast<unsigned>(tag), us);

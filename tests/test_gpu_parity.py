@@ -1,5 +1,6 @@
 """Parity of the CUDA library (through the C ABI) against the reference's own
 outputs (tests/golden) and the oracle restatement.  Needs a B200."""
+import ctypes as C
 import numpy as np
 import pytest
 
@@ -320,6 +321,32 @@ def test_sssp_er_vs_oracle(logn):
         for delta in (64.0, 16.0, 1000.0):
             got = algo.sssp_delta_stepping(g, int(s), delta).dist
             assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("pct", [1, 100, 0])
+def test_sssp_heavy_pull_vs_oracle(pct):
+    """the pull form of the heavy pass (sssp.pull_pct; 1: nearly every bucket,
+    0: never) on uniform, sparse (unreachable vertices) and skewed graphs, with
+    integral, power-of-two and non-integral deltas: distances equal Dijkstra"""
+    from paper_2104_01661_b200.graph import call
+    rng = np.random.default_rng(5)
+    graphs = [P.generate_er(13, 16, seed=7), P.generate_er(12, 2, seed=8)]
+    r0 = P.generate_rmat(12, 8, seed=9)
+    rp0, col0, _ = r0.export()
+    graphs.append(P.graph_new(rp0, col0, rng.integers(1, 256, len(col0)).astype(np.float64)))
+    call("gbx_set_option", b"sssp.pull_pct", C.c_int64(pct))
+    try:
+        for g in graphs:
+            rp, col, w = g.export()
+            n = len(rp) - 1
+            P.property_rowdegree(g)
+            for s in P.pick_sources(g.row_degree(), 2, 4):
+                want = O.dijkstra(n, rp, col, w.astype(np.float64), int(s))
+                for delta in (64.0, 16.0, 37.5, 200.0, 3.0):
+                    got = algo.sssp_delta_stepping(g, int(s), delta).dist
+                    assert np.array_equal(got, want), (n, delta)
+    finally:
+        call("gbx_reset_option", b"sssp.pull_pct")
 
 
 def test_sssp_fp64_weights_vs_oracle():
