@@ -58,7 +58,13 @@ constexpr int kPrB0Ipl = GBX_PR_B0IPL;  // gathers per lane per step in warp-per
 #define GBX_PR_LONG 1024
 #endif
 constexpr int64_t kPrLong = GBX_PR_LONG;  // rows longer than this are chunked
-constexpr int64_t kPrShort = 32;    // rows up to this length: thread per row, exact-length bins
+#ifndef GBX_PR_SHORT
+// measured: 32 / 48 / 64 / 66 / 72 / 80 / 96 / 128 / 158 -> 204.6 / 194.0 / 192.3 / 185.7 /
+// 183.6 / 183.8 / 183.9 / 189.6 / 191.8 us per iteration
+#define GBX_PR_SHORT 80
+#endif
+constexpr int64_t kPrShort = GBX_PR_SHORT;  // rows up to this length: thread per row, exact-length bins
+static_assert(GBX_PR_SHORT + 2 <= kPrBinsMax, "one bin per exact length + the warp-per-row bin");
 constexpr int64_t kPrChunk = 2048;  // nonzeros per chunk unit
 constexpr unsigned kWarp = 0xffffffffu;
 constexpr int kPrMaxPeers = 8;     // ranks of the fused P2P exchange (one NVSwitch box)
@@ -88,6 +94,7 @@ struct PrArgs {
   int* ctl;            // [0] completed iterations [1] done [2] peer timeout (fused exchange)
   unsigned long long* ktime;  // [128][8]: per iteration, min CTA start / max CTA end of the row phase (%globaltimer); trace: [2] min after barrier 1, [3] max finish end, [4] min after barrier 2, [5] max fold end
   int trace;
+  unsigned long long* cta_end;  // trace: every CTA's row-phase end in iteration 5
   unsigned* fin_cnt;
   int64_t l1hot;       // x[0, l1hot) gathered with L1 evict_last, the rest no_allocate
   int64_t nx;          // entries of x (device checks)
@@ -188,12 +195,16 @@ __device__ __forceinline__ double pr_finish_row(const PrArgs<V>& a, V* r_nxt, V*
 template <typename V>
 __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k, int cta, int ncta,
                                                 typename cub::BlockReduce<double, kPrThreads>::TempStorage& red,
-                                                PrBin* s_bins) {
+                                                PrBinS* s_bins) {
   using BlockReduce = cub::BlockReduce<double, kPrThreads>;
   const V *x_cur, *r_cur;
   V *x_nxt, *r_nxt;
   pr_buffers(a, k, x_cur, r_cur, x_nxt, r_nxt);
-  for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_bins[i] = a.bins[i];
+  for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) {
+    const PrBin b = a.bins[i];
+    s_bins[i] = PrBinS{b.p0, static_cast<int32_t>(b.unit0), static_cast<int32_t>(b.row0),
+                       static_cast<int32_t>(b.row1), b.len};
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (cta * int64_t(kPrThreads) + threadIdx.x) >> 5;
@@ -229,7 +240,7 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k, int c
   int bk = 0;
   for (int64_t u = gwarp; u < a.nunits; u += nwarps) {
     while (bk + 1 < a.nbins && u >= s_bins[bk + 1].unit0) ++bk;
-    const PrBin& B = s_bins[bk];
+    const PrBinS& B = s_bins[bk];
     if (B.len < 0) {
       // one warp per row (kPrShort < len <= kPrLong): coalesced column loads,
       // kPrB0Ipl gathers in flight per lane; the next group of columns is
@@ -340,7 +351,7 @@ template <typename V>
 __global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_rows(PrArgs<V> a) {
   using BlockReduce = cub::BlockReduce<double, kPrThreads>;
   __shared__ typename BlockReduce::TempStorage red;
-  __shared__ PrBin s_bins[kPrBinsMax];
+  __shared__ PrBinS s_bins[kPrBinsMax];
   if (!a.fixed && *(volatile int*)&a.ctl[1]) return;  // converged (host-looped path)
   const int k = *(volatile int*)&a.ctl[0];
   if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 8], pr_gtimer());
@@ -368,7 +379,7 @@ __global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist(PrArgs<V
   cg::grid_group grid = cg::this_grid();
   using BlockReduce = cub::BlockReduce<double, kPrThreads>;
   __shared__ typename BlockReduce::TempStorage red;
-  __shared__ PrBin s_bins[kPrBinsMax];
+  __shared__ PrBinS s_bins[kPrBinsMax];
   __shared__ int s_stop;
   const int ncta = gridDim.x;
   for (int k = 0;; ++k) {
@@ -377,6 +388,7 @@ __global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist(PrArgs<V
     if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 8], pr_gtimer());
     const double blk = pr_rows_phase<V>(a, k, blockIdx.x, ncta, red, s_bins);
     if (threadIdx.x == 0 && a.ktime) atomicMax(&a.ktime[(k % 128) * 8 + 1], pr_gtimer());
+    if (a.trace && k == 5 && threadIdx.x == 0) a.cta_end[blockIdx.x] = pr_gtimer();
     grid.sync();
     unsigned long long* kt = a.ktime + (k % 128) * 8;
     if (a.trace && threadIdx.x == 0) atomicMin(kt + 2, pr_gtimer());
@@ -441,7 +453,7 @@ struct PrP2p {
 __device__ __forceinline__ void pr_p2p_body(const PrArgs<float>& a, const PrP2p& m, int cta,
                                             int ncta, cooperative_groups::grid_group& grid,
                                             cub::BlockReduce<double, kPrThreads>::TempStorage& red,
-                                            PrBin* s_bins, int& s_stop) {
+                                            PrBinS* s_bins, int& s_stop) {
   using BlockReduce = cub::BlockReduce<double, kPrThreads>;
   for (int k = 0;; ++k) {
     if (a.ktime && threadIdx.x == 0) atomicMin(&a.ktime[(k % 128) * 8], pr_gtimer());
@@ -508,7 +520,7 @@ __global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist_p2p(PrAr
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ cub::BlockReduce<double, kPrThreads>::TempStorage red;
-  __shared__ PrBin s_bins[kPrBinsMax];
+  __shared__ PrBinS s_bins[kPrBinsMax];
   __shared__ int s_stop;
   pr_p2p_body(a, m, blockIdx.x, gridDim.x, grid, red, s_bins, s_stop);
 }
@@ -520,7 +532,7 @@ __global__ void __launch_bounds__(kPrThreads, GBX_PR_MINB) k_pr_persist_p2p_virt
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ cub::BlockReduce<double, kPrThreads>::TempStorage red;
-  __shared__ PrBin s_bins[kPrBinsMax];
+  __shared__ PrBinS s_bins[kPrBinsMax];
   __shared__ int s_stop;
   __shared__ PrArgs<float> sa;
   __shared__ PrP2p sm;
@@ -656,7 +668,7 @@ static void build_units(PrPlan& P, int64_t row0, int64_t row1, cudaStream_t s) {
   {
     DevArray<int64_t> dthr(nt), drow(nt), dp(nt);
     GBX_CUDA(cudaMemcpyAsync(dthr.p, thr.data(), nt * 8, cudaMemcpyHostToDevice, s));
-    k_pr_bounds<<<1, 64, 0, s>>>(P.trp.p, row0, row1, dthr.p, nt, drow.p, dp.p);
+    k_pr_bounds<<<(nt + 63) / 64, 64, 0, s>>>(P.trp.p, row0, row1, dthr.p, nt, drow.p, dp.p);
     GBX_LAUNCHED();
     GBX_CUDA(cudaMemcpyAsync(brow.data(), drow.p, nt * 8, cudaMemcpyDeviceToHost, s));
     GBX_CUDA(cudaMemcpyAsync(bp.data(), dp.p, nt * 8, cudaMemcpyDeviceToHost, s));
@@ -1045,6 +1057,8 @@ static PrArgs<V> make_args(PrPlan& P, double damping, double tol, int itermax) {
   a.ctl = P.ctl.p;
   a.ktime = P.ktime.p;
   a.trace = static_cast<int>(option(kOptPrTrace));
+  if (a.trace && !P.cta_end.p) P.cta_end.alloc(static_cast<size_t>(device_sms()) * 32);
+  a.cta_end = P.cta_end.p;
   a.fin_cnt = P.blk_cnt.p;
   a.row0 = 0;
   a.l1hot = std::min<int64_t>(P.n, l1_hot_bytes() / static_cast<int64_t>(sizeof(V)));
@@ -1095,6 +1109,7 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
     GBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_pr_persist<V>),
                                          dim3(pa.grid_rows), dim3(kPrThreads), args, 0, s));
     P.last_persist = true;
+    P.grid = pa.grid_rows;
   } else {
     // one row launch + one finish launch per iteration, checked on the host
     // every 4 iterations (the finish kernels of a converged run return at once)
@@ -1143,10 +1158,21 @@ static int pagerank_loop(gbx_graph* g, PrPlan& P, double damping, double tol, in
       }
     }
     P.last_rows_ms = cnt ? sum / cnt * 1e-6 : 0.0;
+    if (option(kOptPrTrace) && cnt && P.last_persist && it > 5 && P.cta_end.p) {
+      // spread of the CTAs' row-phase end times in iteration 5 (static unit assignment)
+      std::vector<unsigned long long> ce(P.grid);
+      GBX_CUDA(cudaMemcpy(ce.data(), P.cta_end.p, ce.size() * 8, cudaMemcpyDeviceToHost));
+      std::vector<double> d;
+      for (unsigned long long t : ce) d.push_back(static_cast<double>(t - kt[8 * 5]) * 1e-3);
+      std::sort(d.begin(), d.end());
+      std::fprintf(stderr, "pagerank trace: CTA row-phase ends (iteration 5): min %.1f p10 %.1f p50 %.1f "
+                           "p90 %.1f max %.1f us\n",
+                   d.front(), d[d.size() / 10], d[d.size() / 2], d[d.size() * 9 / 10], d.back());
+    }
     if (option(kOptPrTrace) && cnt)
-      std::fprintf(stderr, "pagerank trace: %d iterations, rows %.2f us, barrier1 %.2f us, finish "
+      std::fprintf(stderr, "pagerank trace: grid %d, %d iterations, rows %.2f us, barrier1 %.2f us, finish "
                            "%.2f us, barrier2 %.2f us, fold %.2f us (means)\n",
-                   it, sum / cnt * 1e-3, ph[0] / cnt * 1e-3, ph[1] / cnt * 1e-3,
+                   P.grid, it, sum / cnt * 1e-3, ph[0] / cnt * 1e-3, ph[1] / cnt * 1e-3,
                    ph[2] / cnt * 1e-3, ph[3] / cnt * 1e-3);
   }
   if (iters) *iters = it;

@@ -10,11 +10,17 @@ namespace gbx {
 // A PageRank work bin: warp units [unit0, next bin's unit0) cover rows
 // [row0, row1), 32/2^lg rows per unit with 2^lg lanes per row.  len >= 0: every
 // row has exactly len nonzeros starting at p0 + (row - row0) * len.
-constexpr int kPrBinsMax = 96;
+constexpr int kPrBinsMax = 160;
 struct PrBin {
   int64_t unit0, row0, row1, p0;
   int32_t len;
   int32_t lg;
+};
+// the copy the row kernels stage in shared memory (24 bytes; units and rows fit
+// 32 bits: column ids are int32)
+struct PrBinS {
+  int64_t p0;
+  int32_t unit0, row0, row1, len;
 };
 
 // PageRank pull plan (pagerank.cu): AT relabeled by descending in-degree,
@@ -43,6 +49,7 @@ struct PrPlan {
   DevArray<double> l1_block, l1_fin, l1_hist;
   DevArray<int> ctl;            // [0] completed iterations, [1] done, [2] peer timeout
   DevArray<unsigned long long> ktime;  // k_pr_rows launch spans (%globaltimer)
+  DevArray<unsigned long long> cta_end;  // trace: per-CTA row-phase end times
   double last_rows_ms = 0.0;
   bool last_persist = false;       // the last run used k_pr_persist
   DevArray<unsigned> blk_cnt;
