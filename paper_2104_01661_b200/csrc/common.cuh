@@ -179,6 +179,10 @@ struct gbx_graph {
   bool at_pending = false;
   bool has_rowdeg = false, has_coldeg = false;
   gbx::DevArray<int32_t> rowdeg, coldeg;
+  // column counts of A taken while the host CSR was uploaded (graph.cu); not a
+  // property cache: the PageRank plan reads them instead of recounting
+  bool has_colcount = false;
+  gbx::DevArray<int32_t> colcount;
   int symmetric = GBX_UNKNOWN;
   int64_t ndiag = -1;
   // derived device layouts (plans), rebuilt after delete_properties

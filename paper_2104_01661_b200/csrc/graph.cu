@@ -107,12 +107,18 @@ __global__ void k_convert_cols(const int64_t* c64, int32_t* c32, int64_t nnz, in
   c32[p] = static_cast<int32_t>(c);
 }
 
-__global__ void k_validate_cols(const int32_t* col, const uint8_t* head, int64_t nnz,
-                                int64_t n, int* bad) {
-  int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (p >= nnz) return;
-  int32_t c = col[p];
-  if (c < 0 || c >= n) atomicOr(bad, 2);
+// entries [p0, p1): range and strictly-ascending-within-row checks; count != 0
+// also counts the columns (in-degrees)
+__global__ void k_validate_cols(const int32_t* col, const uint8_t* head, int64_t p0, int64_t p1,
+                                int64_t nnz, int64_t n, int* bad, int32_t* count) {
+  const int64_t p = p0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p >= p1) return;
+  const int32_t c = col[p];
+  if (c < 0 || c >= n) {
+    atomicOr(bad, 2);
+  } else if (count) {
+    atomicAdd(&count[c], 1);
+  }
   if (p > 0 && !head[p] && col[p - 1] >= c) atomicOr(bad, 4);
 }
 
@@ -147,8 +153,6 @@ void build_from_host(gbx_graph* g, int64_t n, const int64_t* rp, const int64_t* 
       GBX_CUDA(cudaMemcpyAsync(c64.p, col64, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, s));
       k_convert_cols<<<ceil_div(nnz, 256), 256, 0, s>>>(c64.p, A.col.p, nnz, n, bad.p);
       GBX_LAUNCHED();
-    } else {
-      GBX_CUDA(cudaMemcpyAsync(A.col.p, col32, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     }
   }
   if (vals && nnz > 0) {
@@ -161,9 +165,45 @@ void build_from_host(gbx_graph* g, int64_t n, const int64_t* rp, const int64_t* 
     GBX_CUDA(cudaMemsetAsync(head.p, 0, std::max<int64_t>(nnz, 1), s));
     k_validate_rows<<<ceil_div(n, 256), 256, 0, s>>>(A.rp.p, n, nnz, head.p, bad.p);
     GBX_LAUNCHED();
-    if (nnz > 0) {
-      k_validate_cols<<<ceil_div(nnz, 256), 256, 0, s>>>(A.col.p, head.p, nnz, n, bad.p);
+    if (nnz > 0 && col64) {
+      k_validate_cols<<<ceil_div(nnz, 256), 256, 0, s>>>(A.col.p, head.p, 0, nnz, nnz, n, bad.p,
+                                                         nullptr);
       GBX_LAUNCHED();
+    } else if (nnz > 0) {
+      // int32 columns: the stream goes up in chunks on a copy stream while the
+      // graph's stream validates the chunks that have arrived and counts the
+      // columns (= in-degrees, kept for the PageRank plan) -- both hide behind
+      // the PCIe transfer instead of following it
+      g->colcount.alloc(n);
+      GBX_CUDA(cudaMemsetAsync(g->colcount.p, 0, n * sizeof(int32_t), s));
+      cudaStream_t cs = nullptr;
+      GBX_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      const int64_t chunk = int64_t(8) << 20;  // entries (32 MB)
+      std::vector<cudaEvent_t> ev;
+      cudaError_t err = cudaSuccess;
+      for (int64_t off = 0; off < nnz && err == cudaSuccess; off += chunk) {
+        const int64_t len = std::min(chunk, nnz - off);
+        cudaEvent_t e = nullptr;
+        err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (err != cudaSuccess) break;
+        ev.push_back(e);
+        err = cudaMemcpyAsync(A.col.p + off, col32 + off, len * sizeof(int32_t),
+                              cudaMemcpyHostToDevice, cs);
+        if (err == cudaSuccess) err = cudaEventRecord(e, cs);
+        if (err == cudaSuccess) err = cudaStreamWaitEvent(s, e, 0);
+        if (err != cudaSuccess) break;
+        // the chunk's first entry is compared with its predecessor, which an
+        // earlier chunk brought (stream order)
+        k_validate_cols<<<ceil_div(len, 256), 256, 0, s>>>(A.col.p, head.p, off, off + len, nnz, n,
+                                                         bad.p, g->colcount.p);
+        err = cudaGetLastError();
+      }
+      if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+      (void)cudaStreamSynchronize(cs);
+      for (cudaEvent_t e : ev) (void)cudaEventDestroy(e);
+      (void)cudaStreamDestroy(cs);
+      GBX_CUDA(err);
+      g->has_colcount = true;
     }
   }
   int hbad = 0;

@@ -627,16 +627,32 @@ __global__ void k_gather_i32(const int32_t* src, const int32_t* idx, int64_t n, 
   if (i < n) dst[i] = src[idx[i]];
 }
 
-// exact-length bin [row0, row0 + nrows) of length L, row-major -> unit-
-// interleaved (32-row units; element j of unit row l at unit*32*L + j*m + l)
-__global__ void k_pr_interleave(const int32_t* src, int32_t* dst, int64_t nrows, int L) {
-  const int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (p >= nrows * L) return;
-  const int64_t i = p / L;
-  const int j = static_cast<int>(p - i * L);
-  const int64_t u = i >> 5;
-  const int m = static_cast<int>(min(int64_t(32), nrows - u * 32));
-  dst[u * 32 * L + int64_t(j) * m + (i & 31)] = src[p];
+// exact-length bins (bins[b0..nbins), ascending p0), row-major -> unit-
+// interleaved (32-row units; element j of unit row l at unit*32*L + j*m + l):
+// one launch over the bins' whole nonzero range [q0, q1)
+__global__ void k_pr_interleave(const int32_t* src, int32_t* dst, const PrBin* bins, int b0,
+                                int nbins, int64_t q0, int64_t q1) {
+  __shared__ int64_t s_p0[kPrBinsMax + 1];
+  for (int i = threadIdx.x; i < nbins - b0; i += blockDim.x) s_p0[i] = bins[b0 + i].p0;
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t p = q0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < q1; p += stride) {
+    int lo = 0, hi = nbins - b0 - 1;  // last bin with p0 <= p
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_p0[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    const PrBin& B = bins[b0 + lo];
+    const int L = B.len;
+    if (L <= 0) continue;
+    const int64_t nrows = B.row1 - B.row0;
+    const int64_t q = p - B.p0;
+    const int64_t i = q / L;
+    const int j = static_cast<int>(q - i * L);
+    const int64_t u = i >> 5;
+    const int m = static_cast<int>(min(int64_t(32), nrows - u * 32));
+    dst[B.p0 + u * 32 * L + int64_t(j) * m + (i & 31)] = src[q + (B.p0 - q0)];
+  }
 }
 
 // first row r in [row0, row1) with length(r) <= thr[t] (lengths are
@@ -721,31 +737,36 @@ static void build_units(PrPlan& P, int64_t row0, int64_t row1, cudaStream_t s) {
     units += (r1 - r0 + 31) / 32;
   }
   if (bins.size() > static_cast<size_t>(kPrBinsMax)) fail(GBX_CUDA_ERROR, "pagerank: too many bins");
-  // exact-length bins: columns to the unit-interleaved layout k_pr_rows reads
-  {
-    int64_t q0 = -1, q1 = -1;
-    for (const PrBin& b : bins)
-      if (b.len > 0) {
-        if (q0 < 0) q0 = b.p0;
-        q1 = b.p0 + (b.row1 - b.row0) * b.len;
-      }
-    if (q0 >= 0 && q1 > q0) {
-      Tmp<int32_t> cp(q1 - q0, s);
-      GBX_CUDA(cudaMemcpyAsync(cp.p, P.tcol.p + q0, (q1 - q0) * 4, cudaMemcpyDeviceToDevice, s));
-      for (const PrBin& b : bins) {
-        const int64_t cnt = (b.row1 - b.row0) * b.len;
-        if (b.len <= 0 || cnt == 0) continue;
-        k_pr_interleave<<<ceil_div(cnt, 256), 256, 0, s>>>(cp.p + (b.p0 - q0), P.tcol.p + b.p0,
-                                                           b.row1 - b.row0, b.len);
-        GBX_LAUNCHED();
-      }
-    }
-  }
   P.nbins = static_cast<int>(bins.size());
   P.bins.alloc(std::max<size_t>(bins.size(), 1));
   if (!bins.empty())
     GBX_CUDA(cudaMemcpyAsync(P.bins.p, bins.data(), bins.size() * sizeof(PrBin),
                              cudaMemcpyHostToDevice, s));
+  // exact-length bins: columns to the unit-interleaved layout k_pr_rows reads
+  // (the bins with len > 0 are contiguous in the bin list and in tcol)
+  {
+    int64_t q0 = -1, q1 = -1;
+    int b0 = -1;
+    for (size_t i = 0; i < bins.size(); ++i) {
+      const PrBin& b = bins[i];
+      if (b.len > 0) {
+        if (q0 < 0) {
+          q0 = b.p0;
+          b0 = static_cast<int>(i);
+        }
+        q1 = b.p0 + (b.row1 - b.row0) * b.len;
+      }
+    }
+    if (q0 >= 0 && q1 > q0) {
+      Tmp<int32_t> cp(q1 - q0, s);
+      GBX_CUDA(cudaMemcpyAsync(cp.p, P.tcol.p + q0, (q1 - q0) * 4, cudaMemcpyDeviceToDevice, s));
+      // bins after the last positive length (len 0) hold no nonzeros
+      int b1 = b0;
+      while (b1 < static_cast<int>(bins.size()) && bins[b1].len > 0) ++b1;
+      k_pr_interleave<<<device_sms() * 8, 256, 0, s>>>(cp.p, P.tcol.p, P.bins.p, b0, b1, q0, q1);
+      GBX_LAUNCHED();
+    }
+  }
   P.nunits = units;
   P.nchunks = static_cast<int64_t>(chunks.size() / 2);
   P.nlong = static_cast<int64_t>(lrow.size());
@@ -771,6 +792,10 @@ __global__ void k_pr_newlen(const int64_t* atrp, const int32_t* new2old, int64_t
   } else if (r == n) {
     len[r] = 0;
   }
+}
+__global__ void k_pr_gather_len(const int32_t* len, const int32_t* new2old, int64_t n, int64_t* out) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r <= n) out[r] = r < n ? len[new2old[r]] : 0;
 }
 constexpr int64_t kPrGatherLong = 256;
 // rows of A in the new order, as (new column, new row) pairs: the pairs come
@@ -863,6 +888,9 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
       k_neg_len<<<ceil_div(n, 256), 256, 0, s>>>(A.rp.p, n, len.p);
       GBX_LAUNCHED();
     }
+  } else if (g->has_colcount) {
+    len = std::move(g->colcount);  // counted while the host CSR was uploaded
+    g->has_colcount = false;
   } else {
     compute_degrees(s, A, len, false);
   }
@@ -928,9 +956,17 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
     radix_sort_pairs(s, kb, vb, nnz, 0, bits);
     if (vb.Current() != reinterpret_cast<uint32_t*>(P.tcol.p))
       GBX_CUDA(cudaMemcpyAsync(P.tcol.p, vb.Current(), nnz * 4, cudaMemcpyDeviceToDevice, s));
-    const uint32_t* sorted_rows = kb.Current();
     tm.mark("radix sort by new column");
-    rowptr_from_sorted_rows32(s, n, sorted_rows, nnz, P.trp.p);
+    // row pointers of the relabeled AT: the exclusive scan of the in-degrees in
+    // the new order (no pass over the sorted keys)
+    k_pr_gather_len<<<ceil_div(n + 1, 256), 256, 0, s>>>(len.p, P.new2old.p, n, P.trp.p);
+    GBX_LAUNCHED();
+    {
+      size_t tb = 0;
+      GBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, P.trp.p, P.trp.p, n + 1, s));
+      Tmp<uint8_t> t(tb, s);
+      GBX_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, P.trp.p, P.trp.p, n + 1, s));
+    }
     tm.mark("row pointers");
   } else {
     GBX_CUDA(cudaMemsetAsync(P.trp.p, 0, (n + 1) * sizeof(int64_t), s));
