@@ -64,6 +64,10 @@ constexpr int64_t kPrLong = GBX_PR_LONG;  // rows longer than this are chunked
 #define GBX_PR_SHORT 80
 #endif
 constexpr int64_t kPrShort = GBX_PR_SHORT;  // rows up to this length: thread per row, exact-length bins
+#ifndef GBX_PR_ZBLK
+#define GBX_PR_ZBLK 1024
+#endif
+constexpr int64_t kPrZeroBlk = GBX_PR_ZBLK;  // rows without in-edges: rows per dynamically claimed block
 static_assert(GBX_PR_SHORT + 2 <= kPrBinsMax, "one bin per exact length + the warp-per-row bin");
 constexpr int64_t kPrChunk = 2048;  // nonzeros per chunk unit
 constexpr unsigned kWarp = 0xffffffffu;
@@ -96,6 +100,8 @@ struct PrArgs {
   int trace;
   unsigned long long* cta_end;  // trace: every CTA's row-phase end in iteration 5
   unsigned* fin_cnt;
+  unsigned* dyn_cnt;   // [4] block counters of the rows without in-edges, by iteration & 3
+  int64_t zrow0, zrow1;  // rows without in-edges, claimed in blocks of kPrZeroBlk
   int64_t l1hot;       // x[0, l1hot) gathered with L1 evict_last, the rest no_allocate
   int64_t nx;          // entries of x (device checks)
   int64_t row0;        // first row of this plan (shards); outputs indexed row - row0
@@ -312,6 +318,26 @@ __device__ __forceinline__ double pr_rows_phase(const PrArgs<V>& a, int k, int c
       }
     }
   }
+  // 3) rows without in-edges (r = teleport; the same arithmetic as an exact-
+  //    length unit of length 0), claimed in blocks from the iteration's
+  //    counter: the CTAs' static shares end up to ~7% apart (measured), and
+  //    whoever is done first takes more of this cheap tail (row phase 171 ->
+  //    165 us; blocks of 256 / 1024 / 4096 rows: 166 / 165 / 190 us).  Claiming
+  //    the shortest exact-length bins the same way costs the main loops
+  //    registers (spills) and lost: 168 us.
+  if (a.zrow1 > a.zrow0) {
+    unsigned* const dyn = a.dyn_cnt + (k & 3);
+    for (;;) {
+      unsigned blk = 0;
+      if (lane == 0) blk = atomicAdd(dyn, 1u);
+      blk = __shfl_sync(kWarp, blk, 0);
+      const int64_t z0 = a.zrow0 + int64_t(blk) * kPrZeroBlk;
+      if (z0 >= a.zrow1) break;
+      const int64_t z1 = min(z0 + kPrZeroBlk, a.zrow1);
+      for (int64_t row = z0 + lane; row < z1; row += 32)
+        l1 += pr_finish_row(a, r_nxt, x_nxt, row, 0.0, r_cur[row - a.row0], a.inv[row]);
+    }
+  }
   __syncthreads();  // red may still be in use by a previous reduction
   return BlockReduce(red).Sum(l1);
 }
@@ -330,6 +356,8 @@ __device__ __forceinline__ double pr_long_phase(const PrArgs<V>& a, int k, int c
   const int64_t gwarp = (cta * int64_t(kPrThreads) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(ncta) * kPrThreads) >> 5;
   double l1 = 0.0;
+  // the zero-row block counter iteration k + 2 will use (last read in k - 2)
+  if (cta == 0 && threadIdx.x == 0) a.dyn_cnt[(k + 2) & 3] = 0u;
   for (int64_t i = gwarp; i < a.nlong; i += nwarps) {
     const int64_t q0 = a.long_slot[i], q1 = a.long_slot[i + 1];
     double s = 0.0;
@@ -590,7 +618,7 @@ __global__ void k_pr_init(V* r, V* x, V* inv, const int32_t* outdeg, int64_t n, 
   // the run's control words and launch-span table (one kernel instead of
   // three memsets / resets before the persistent launch)
   if (i < 4) ctl[i] = 0;
-  if (i == 0) *fin_cnt = 0;
+  if (i < 8) fin_cnt[i] = 0;  // the finish counter and the zero-row block counters
   if (ktime && i < 128 * 8) ktime[i] = (i & 1) ? 0ull : ~0ull;
   if (i >= n) return;
   const double r0 = 1.0 / static_cast<double>(n);
@@ -711,6 +739,7 @@ static void build_units(PrPlan& P, int64_t row0, int64_t row1, cudaStream_t s) {
   lslot.push_back(static_cast<int64_t>(chunks.size() / 2));
   std::vector<PrBin> bins;
   int64_t units = 0;
+  P.zrow0 = P.zrow1 = 0;
   {
     // bin 0: kPrShort < len <= kPrLong, one warp (unit) per row
     PrBin b{};
@@ -733,6 +762,12 @@ static void build_units(PrPlan& P, int64_t row0, int64_t row1, cudaStream_t s) {
     b.row1 = r1;
     b.p0 = bp[t];
     b.len = static_cast<int32_t>(len);
+    if (len == 0) {
+      // the rows without in-edges are not warp units: claimed in blocks
+      P.zrow0 = r0;
+      P.zrow1 = r1;
+      continue;
+    }
     bins.push_back(b);
     units += (r1 - r0 + 31) / 32;
   }
@@ -987,7 +1022,7 @@ static void plan_rows(gbx_graph* g, PrPlan& P, int64_t row0, int64_t row1) {
   P.l1_hist.alloc(128);
   P.ktime.alloc(128 * 8);
   P.ctl.alloc(4);
-  P.blk_cnt.alloc(1);
+  P.blk_cnt.alloc(8);  // [0] finish counter, [4..7] zero-row block counters
 }
 
 void pagerank_prepare(gbx_graph* g) {
@@ -1096,6 +1131,9 @@ static PrArgs<V> make_args(PrPlan& P, double damping, double tol, int itermax) {
   if (a.trace && !P.cta_end.p) P.cta_end.alloc(static_cast<size_t>(device_sms()) * 32);
   a.cta_end = P.cta_end.p;
   a.fin_cnt = P.blk_cnt.p;
+  a.dyn_cnt = P.blk_cnt.p + 4;
+  a.zrow0 = P.zrow0;
+  a.zrow1 = P.zrow1;
   a.row0 = 0;
   a.l1hot = std::min<int64_t>(P.n, l1_hot_bytes() / static_cast<int64_t>(sizeof(V)));
   a.nx = P.n;
@@ -1115,7 +1153,7 @@ __global__ void k_pr_ktime_reset(unsigned long long* t) {
 
 static void reset_state(cudaStream_t s, PrPlan& P) {
   GBX_CUDA(cudaMemsetAsync(P.ctl.p, 0, P.ctl.n * sizeof(int), s));
-  GBX_CUDA(cudaMemsetAsync(P.blk_cnt.p, 0, sizeof(unsigned), s));
+  GBX_CUDA(cudaMemsetAsync(P.blk_cnt.p, 0, 8 * sizeof(unsigned), s));
   if (P.ktime.p) k_pr_ktime_reset<<<1, 256, 0, s>>>(P.ktime.p);
 }
 
@@ -1414,7 +1452,7 @@ void pr_shard_step(gbx_graph* g, const float* x_full, const float* r_prev, float
   a.row0 = P.row0;
   a.grid_rows = resident_grid(reinterpret_cast<const void*>(k_pr_rows<float>));
   GBX_CUDA(cudaMemsetAsync(P.ctl.p, 0, 2 * sizeof(int), s));
-  GBX_CUDA(cudaMemsetAsync(P.blk_cnt.p, 0, sizeof(unsigned), s));
+  GBX_CUDA(cudaMemsetAsync(P.blk_cnt.p, 0, 8 * sizeof(unsigned), s));
   launch_rows<float>(a, s);
   k_pr_finish<float><<<P.grid_fin, kPrThreads, 0, s>>>(a);
   GBX_LAUNCHED();

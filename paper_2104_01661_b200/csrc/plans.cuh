@@ -34,6 +34,7 @@ struct PrPlan {
   DevArray<PrBin> bins;            // warp units by bin
   int nbins = 0;
   int64_t nunits = 0;
+  int64_t zrow0 = 0, zrow1 = 0;    // rows without in-edges
   DevArray<int64_t> chunk_p;       // [2 * nchunks] nonzero ranges of long rows
   int64_t nchunks = 0;
   DevArray<int32_t> long_row;
