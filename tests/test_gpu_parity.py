@@ -216,6 +216,44 @@ def test_graph_new_rejects_corrupt_matrix():
     assert e.value.code == P.ErrCode.InvalidMatrix
 
 
+def test_graph_new32_chunked_upload():
+    """graph_new (graph.cpp:16-28) from a host CSR larger than one upload chunk
+    (8 Mi int32 columns): the chunks are validated and counted as they arrive
+    (csrc/graph.cu build_from_host).  The round trip is exact, a fault ON a chunk
+    boundary is found (containers.cpp:104-124), and PageRank on the uploaded
+    graph equals PageRank on the same graph built on the device bit for bit (its
+    plan reuses the column counts taken during the upload)."""
+    gd = P.generate_rmat(20, 16, seed=5, kind=P.Kind.DirectedAdjacency)
+    rp, col, _ = gd.export()
+    col = np.ascontiguousarray(col, np.int32)
+    chunk = 8 << 20
+    assert len(col) > chunk + 1
+    gh = P.graph_new(rp, col)
+    rp2, col2, _ = gh.export()
+    assert np.array_equal(rp2, rp) and np.array_equal(col2, col)
+    for g in (gd, gh):
+        P.property_at(g)
+        P.property_rowdegree(g)
+    a, b = algo.pagerank_gap(gd), algo.pagerank_gap(gh)
+    assert a.iterations == b.iterations and np.array_equal(a.rank, b.rank)
+    # entry `chunk` is the first of the second chunk: make it repeat its
+    # predecessor inside one row, then point it out of range
+    row = int(np.searchsorted(rp, chunk, side="right")) - 1
+    if rp[row] == chunk:  # it starts a row: use the next entry pair inside a row instead
+        row = next(r for r in range(row, len(rp) - 1) if rp[r + 1] - rp[r] >= 2 and rp[r] >= chunk)
+    bad = col.copy()
+    k = max(int(rp[row]) + 1, chunk)
+    bad[k] = bad[k - 1]
+    with pytest.raises(P.Error) as e:
+        P.graph_new(rp, bad)
+    assert e.value.code == P.ErrCode.InvalidMatrix
+    bad = col.copy()
+    bad[chunk] = len(rp) - 1  # == n: out of range
+    with pytest.raises(P.Error) as e:
+        P.graph_new(rp, bad)
+    assert e.value.code == P.ErrCode.InvalidMatrix
+
+
 @pytest.mark.parametrize("name", case_ids("sort_by_degree"))
 def test_sort_by_degree_golden(name):
     c = CASES[name]
