@@ -54,6 +54,10 @@ constexpr int kSsspThreads = 256;
 #endif
 constexpr int kSsspWarps = kSsspThreads / 32;
 constexpr int kSsspBuf = 256;  // staged pushes per warp and queue
+#ifndef GBX_SSSP_SMALL
+#define GBX_SSSP_SMALL 262144  // 0 / 4096 / 32768 / 262144 -> 67.0 / 66.0 / 65.5 / 64.9 ms per 16 sources (ER 2^24)
+#endif
+constexpr int64_t kSsspSmallBucket = GBX_SSSP_SMALL;  // pops per bucket up to which the heavy pass walks a log
 constexpr unsigned kFullW = 0xffffffffu;
 
 template <typename D> struct DistTraits;
@@ -388,6 +392,13 @@ struct SsspBArgs {
   const uint32_t* hin;
   int pull_pct;
   int light_group;     // lanes per vertex in the light (near) phase: 1, 2 or 4
+  // small buckets: while a bucket has popped <= slog_cap vertices its near
+  // iterations log them (ctl[8] entries, a vertex popped twice is listed
+  // twice: its heavy edges are then relaxed twice from the same final
+  // distance), and the heavy pass walks the log instead of the dense pass
+  // over dist (~25 us per bucket at 2^24 vertices)
+  int32_t* slog;
+  int slog_cap;
   int trace;
   unsigned long long* tlog;  // optional: [2i] %globaltimer, [2i+1] kind<<32 | size (debug)
   int tlog_cap;
@@ -482,6 +493,7 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
   // pops of the current bucket / of all buckets so far (every thread reads each
   // near iteration's count, so every thread takes the same push / pull decision)
   int64_t popped_k = 0, popped_all = 0;
+  bool log_pops = false;  // this near iteration logs its pops (the bucket is still small)
   // relax the edges of the vertices list[0, cnt): phase 0 all edges, 1 light
   // edges (and record the vertex in the settled list), 2 heavy edges.  4 lanes
   // per vertex (8 vertices per warp), each lane 4 edges per round: 4
@@ -498,6 +510,7 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
       const int32_t u = active ? list[qi] : 0;
       const uint32_t ubit = 1u << (u & 31);
       if (active && si == 0 && pop_bits) atomicAnd(&pop_bits[u >> 5], ~ubit);
+      if (active && si == 0 && log_pops) a.slog[atomicAdd(&a.ctl[8], 1)] = u;
       int64_t p = 0, e = 0;
       if (a.vm) {
         if (active) {
@@ -713,6 +726,7 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
         if (zero_bucket >= 0) a.bcnt[zero_bucket] = 0;
       }
       zero_bucket = -1;
+      log_pops = a.nl && a.slog && popped_k <= a.slog_cap;
       const int32_t* qc = (t & 1) ? a.q1 : a.q0;
       int32_t* qn = (t & 1) ? a.q0 : a.q1;
       uint32_t* pop_bits = a.qbits[t & 1];
@@ -744,15 +758,27 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
     // atomic per near visit); each warp compacts its 32-vertex window into
     // shared memory and relaxes the heavy edges 8 vertices at a time
     popped_all += popped_k;
-    const bool pull = a.hin != nullptr &&
+    // every near iteration of the bucket logged its pops: walk the log
+    const bool small = a.nl && a.slog && popped_k <= a.slog_cap;
+    const bool pull = !small && a.hin != nullptr &&
                       popped_k * 100 > static_cast<int64_t>(a.pull_pct) * (a.n - popped_all);
     popped_k = 0;
+    log_pops = false;
     if (tl && tn < a.tlog_cap) {
       a.tlog[2 * tn] = sssp_gtimer();
       a.tlog[2 * tn + 1] = (1ull << 62) | (pull ? 1ull : 0ull);
       ++tn;
     }
-    if (a.nl && pull) {
+    if (small) {
+      unsigned long long nrel = 0;
+      const int cnt = *(volatile int*)&a.ctl[8];
+      if (cnt) {
+        relax(std::integral_constant<int, 4>{}, a.slog, cnt, 2, nullptr, nullptr, nrel);
+        bucq.flush(a.bq, a.cap, a.bcnt, a.nb);
+        sssp_count_relax(a.relax, nrel);
+        grid.sync();  // before the leader below re-zeroes ctl[8]
+      }
+    } else if (a.nl && pull) {
       if constexpr (std::is_same<D, uint32_t>::value) {
         unsigned long long nrel = 0;
         int32_t* win = s_settle[threadIdx.x >> 5];
@@ -1298,6 +1324,10 @@ static void sssp_launch(gbx_graph* g, SsspPlan& P, SsspLane& L, cudaStream_t s, 
         b.hin = P.hin.p;
         b.pull_pct = static_cast<int>(option(kOptSsspPullPct));
       }
+    }
+    if (split) {
+      b.slog = L.far[0].p;  // (the far piles belong to the unbucketed kernel)
+      b.slog_cap = static_cast<int>(std::min<int64_t>(kSsspSmallBucket, n));
     }
     b.trace = option(kOptSsspTrace) >= 2 ? 1 : 0;
     const bool tlog_on = option(kOptSsspTrace) != 0;
