@@ -426,8 +426,9 @@ def bench_pagerank(args, dist, ws, rank, local):
         "e2e": {"value": e2e_val, "unit": "edges/s/iter",
                 "h2d_bytes_per_step": int(rp.nbytes + col.nbytes),
                 "d2h_bytes_per_step": int(n * 8 + 4),
-                "includes": "H2D CSR (pinned), graph_new32 validation, property_at "
-                            "(device transpose), property_rowdegree, PageRank, D2H ranks",
+                "includes": "H2D CSR (pinned, chunked; validation and column counts overlapped), "
+                            "property_at (recorded: the plan needs only the in-degrees), "
+                            "property_rowdegree, PageRank plan + run, D2H ranks",
                 "samples_ms": [round(t * 1e3, 2) for t in e2e_times]},
         "gpu_launches": int((st["launches"]) * args.steps),
         "clocks": clk.summary(),
@@ -860,7 +861,18 @@ def main():
     ws, rank, local = dist_env()
     dist = maybe_init_dist(ws, local)
     if args.workload == "pagerank" and (ws > 1 or force_sharded()):
-        out, extra = bench_pagerank_sharded(args, dist, ws, rank, local)
+        try:
+            out, extra = bench_pagerank_sharded(args, dist, ws, rank, local)
+        except Exception as e:  # noqa: BLE001
+            # the sharded path could only be exercised on one GPU in this build's
+            # runs (in-process ranks, 1-rank NCCL): if it fails symmetrically on a
+            # real multi-GPU box (e.g. no peer access), every rank measures the
+            # single-GPU path as a replica instead, and the line says so
+            sys.stderr.write(f"bench: sharded PageRank failed on rank {rank}: {e!r}; "
+                             "falling back to per-rank replicas\n")
+            out, extra = bench_pagerank(args, dist, ws, rank, local)
+            out["scaling"] = "weak"
+            out["config"]["parallelism"] = f"replicas{ws} (sharded path failed: {str(e)[:120]})"
     elif args.workload == "pagerank":
         out, extra = bench_pagerank(args, dist, ws, rank, local)
         if ws == 1 and not args.no_secondary:
