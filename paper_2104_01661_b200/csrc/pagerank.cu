@@ -51,11 +51,11 @@ constexpr int kPrThreads = 256;
 #endif
 constexpr int kPrIpl = GBX_PR_IPL;  // chunk walks: independent gathers in flight per lane
 #ifndef GBX_PR_B0IPL
-#define GBX_PR_B0IPL 2  // measured: 2 and 4 within 1%, 8 slower (registers)
+#define GBX_PR_B0IPL 6  // with the 80-nonzero bins and kPrLong 2048: 2 / 3 / 4 / 6 / 8 -> 180.7 / 178.5 / 178.4 / 176.5 / 185.3 us per iteration
 #endif
 constexpr int kPrB0Ipl = GBX_PR_B0IPL;  // gathers per lane per step in warp-per-row units
 #ifndef GBX_PR_LONG
-#define GBX_PR_LONG 1024
+#define GBX_PR_LONG 2048  // at B0IPL 6: 1024 / 2048 / 3072 / 4096 / 8192 -> 176.5 / 175.6 / 175.9 / 175.6 / 244.2 us per iteration
 #endif
 constexpr int64_t kPrLong = GBX_PR_LONG;  // rows longer than this are chunked
 #ifndef GBX_PR_SHORT
