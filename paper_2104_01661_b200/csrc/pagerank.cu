@@ -47,7 +47,7 @@ constexpr int kPrThreads = 256;
 #define GBX_PR_MINB 6  // resident CTAs per SM the rows kernel is compiled for
 #endif
 #ifndef GBX_PR_IPL
-#define GBX_PR_IPL 16  // measured: 4 / 8 / 16 -> 219.1 / 215.8 / 215.0 us per iteration
+#define GBX_PR_IPL 8  // round 1 (2048-nonzero chunks): 4 / 8 / 16 -> 219.1 / 215.8 / 215.0; with 1024-nonzero chunks: 8 / 16 -> 172.9 / 173.5 us per iteration
 #endif
 constexpr int kPrIpl = GBX_PR_IPL;  // chunk walks: independent gathers in flight per lane
 #ifndef GBX_PR_B0IPL
@@ -69,7 +69,10 @@ constexpr int64_t kPrShort = GBX_PR_SHORT;  // rows up to this length: thread pe
 #endif
 constexpr int64_t kPrZeroBlk = GBX_PR_ZBLK;  // rows without in-edges: rows per dynamically claimed block
 static_assert(GBX_PR_SHORT + 2 <= kPrBinsMax, "one bin per exact length + the warp-per-row bin");
-constexpr int64_t kPrChunk = 2048;  // nonzeros per chunk unit
+#ifndef GBX_PR_CHUNK
+#define GBX_PR_CHUNK 1024  // 512 / 768 / 1024 / 1280 / 2048 / 3072 / 4096 -> 176.2 / 174.0 / 173.5 / 178.9 / 175.8 / 181.9 / 194.1 us per iteration
+#endif
+constexpr int64_t kPrChunk = GBX_PR_CHUNK;  // nonzeros per chunk unit
 constexpr unsigned kWarp = 0xffffffffu;
 constexpr int kPrMaxPeers = 8;     // ranks of the fused P2P exchange (one NVSwitch box)
 
