@@ -876,19 +876,72 @@ __global__ void k_pr_gather_a_long(const int64_t* arp, const int32_t* acol, cons
     }
   }
 }
-__global__ void k_pr_gather_a_short(const int64_t* arp, const int32_t* acol,
+// rows of up to kPrGatherLong entries: a warp takes 32 consecutive new rows
+// (lane l holds row l's source pointer, destination and length), then walks
+// the concatenation of their entries one per lane -- the owner row of an
+// entry by a shuffle binary search over the lanes' prefix sums -- four
+// entries per lane in flight (column, then its new id), coalesced stores
+__global__ void __launch_bounds__(256) k_pr_gather_a_short(const int64_t* arp, const int32_t* acol,
                                     const int32_t* new2old, const int32_t* old2new,
                                     const int64_t* prp, int64_t n, uint32_t* key, uint32_t* val) {
+  constexpr unsigned kAllW = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t r = gw * 4 + (lane >> 3); r < n; r += nw * 4) {
-    const int64_t d = prp[r], len = prp[r + 1] - d;
-    if (len > kPrGatherLong) continue;
-    const int64_t src = arp[new2old[r]];
-    for (int64_t p = lane & 7; p < len; p += 8) {
-      key[d + p] = static_cast<uint32_t>(old2new[acol[src + p]]);
-      val[d + p] = static_cast<uint32_t>(r);
+  for (int64_t r0 = gw * 32; r0 < n; r0 += nw * 32) {
+    const int64_t r = r0 + lane;
+    int64_t d = 0, src = 0;
+    int len = 0;
+    if (r < n) {
+      d = prp[r];
+      const int64_t l = prp[r + 1] - d;
+      if (l <= kPrGatherLong) {
+        len = static_cast<int>(l);
+        src = arp[new2old[r]];
+      }
+    }
+    int inc = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(kAllW, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const int total = __shfl_sync(kAllW, inc, 31);
+    const int exc = inc - len;
+    for (int base = 0; base < total; base += 128) {
+      int64_t at[4], to[4];
+      int row[4];
+      bool ok[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int q = base + 32 * k + lane;
+        ok[k] = q < total;
+        int lo = 0;  // last lane whose exclusive prefix is <= q (an empty row never wins: the
+                     // next lane has the same prefix)
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int e = __shfl_sync(kAllW, exc, (lo + step) & 31);
+          if (lo + step < 32 && e <= q) lo += step;
+        }
+        const int e = __shfl_sync(kAllW, exc, lo);
+        const int64_t sj = __shfl_sync(kAllW, src, lo);
+        const int64_t dj = __shfl_sync(kAllW, d, lo);
+        at[k] = sj + (q - e);
+        to[k] = dj + (q - e);
+        row[k] = lo;
+      }
+      int32_t c[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) c[k] = ok[k] ? __ldg(acol + at[k]) : 0;
+      int32_t nc[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) nc[k] = ok[k] ? __ldg(old2new + c[k]) : 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (ok[k]) {
+          key[to[k]] = static_cast<uint32_t>(nc[k]);
+          val[to[k]] = static_cast<uint32_t>(r0 + row[k]);
+        }
     }
   }
 }
