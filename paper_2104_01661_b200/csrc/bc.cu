@@ -726,6 +726,61 @@ static BcWork& ensure_work(gbx_graph* g) {
   return W;
 }
 
+__global__ void k_bc_degree_key(const int64_t* rp, const int32_t* colcount, int64_t n, int32_t* key) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) key[i] = static_cast<int32_t>(rp[i + 1] - rp[i]) + (colcount ? colcount[i] : 0);
+}
+__global__ void k_bc_inverse(const int32_t* new2old, int64_t n, int32_t* old2new) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) old2new[new2old[i]] = static_cast<int32_t>(i);
+}
+__global__ void k_bc_map_sources(int32_t* src, int ns, const int32_t* old2new) {
+  if (threadIdx.x < ns) src[threadIdx.x] = old2new[src[threadIdx.x]];
+}
+__global__ void k_bc_unpermute(const double* cent_new, const int32_t* old2new, int64_t n, double* cent) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) cent[i] = cent_new[old2new[i]];
+}
+
+// the degree-sorted copy (BcWork::ra / rat), built once per graph
+static void ensure_relabel(gbx_graph* g, BcWork& W) {
+  const Csr& A = g->A;
+  if (W.relabel_key == A.rp.p && W.relabel_nnz == A.nnz && W.rat.rp.p) return;
+  cudaStream_t s = g->stream;
+  const int64_t n = A.n, nnz = A.nnz;
+  const bool directed = g->kind != GBX_UNDIRECTED;
+  DevArray<int32_t> rowlen, colcount, key(std::max<int64_t>(n, 1));
+  compute_degrees(s, A, rowlen, true);
+  if (directed) compute_degrees(s, A, colcount, false);
+  k_bc_degree_key<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, s>>>(
+      A.rp.p, directed ? colcount.p : nullptr, n, key.p);
+  GBX_LAUNCHED();
+  sort_ids_by_key(s, key.p, n, false, W.new2old);
+  W.old2new.alloc(std::max<int64_t>(n, 1));
+  k_bc_inverse<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, s>>>(W.new2old.p, n, W.old2new.p);
+  GBX_LAUNCHED();
+  // relabeled AT = the transpose of A under the relabeling; an undirected
+  // graph's relabeled A is the same matrix
+  W.rat.n = n;
+  W.rat.nnz = nnz;
+  W.rat.rp.alloc(n + 1);
+  W.rat.col.alloc(std::max<int64_t>(nnz, 1));
+  relabeled_transpose(s, A, W.new2old.p, W.old2new.p, directed ? colcount.p : rowlen.p,
+                      W.rat.rp.p, W.rat.col.p);
+  if (directed) {
+    const Csr& AT = g->AT();
+    W.ra.n = n;
+    W.ra.nnz = nnz;
+    W.ra.rp.alloc(n + 1);
+    W.ra.col.alloc(std::max<int64_t>(nnz, 1));
+    relabeled_transpose(s, AT, W.new2old.p, W.old2new.p, rowlen.p, W.ra.rp.p, W.ra.col.p);
+  }
+  W.cent_new.alloc(std::max<int64_t>(n, 1));
+  GBX_CUDA(cudaStreamSynchronize(s));
+  W.relabel_key = A.rp.p;
+  W.relabel_nnz = nnz;
+}
+
 void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrality) {
   NvtxRange nvtx_("gbx.bc");
   const int64_t n = g->A.n;
@@ -734,8 +789,14 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       fail(GBX_SOURCE_OUT_OF_RANGE, "source " + std::to_string(sources[b]));
   BcWork& W = ensure_work(g);
   cudaStream_t s = g->stream;
-  const Csr& A = g->A;
-  const Csr& AT = g->AT();
+  // large graphs run on the degree-sorted copy: sources mapped in, the
+  // centrality mapped back at the end (same sums, another fp64 rounding order)
+  const int64_t rmin = option(kOptBcRelabelMinN);
+  const bool relabeled = rmin >= 0 && n >= rmin && g->A.nnz > 0;
+  if (relabeled) ensure_relabel(g, W);
+  const Csr& AT = relabeled ? W.rat : g->AT();
+  const Csr& A = relabeled ? (g->kind == GBX_UNDIRECTED ? W.rat : W.ra) : g->A;
+  double* const cent_acc = relabeled ? W.cent_new.p : W.cent.p;
   const int64_t n1 = std::max<int64_t>(n, 1);
   const size_t map_bytes = (n1 / 8 + 1) * sizeof(uint32_t);
   build_hubs(s, A, W.hub_a);
@@ -748,7 +809,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     W.allbin_key = AT.rp.p;
     W.allbin_nnz = AT.nnz;
   }
-  GBX_CUDA(cudaMemsetAsync(W.cent.p, 0, n1 * 8, s));
+  GBX_CUDA(cudaMemsetAsync(cent_acc, 0, n1 * 8, s));
   const int grid = device_sms() * 8;
   const int alpha = static_cast<int>(option(kOptBcAlpha));
   int* ctl = W.ctl.p;
@@ -760,6 +821,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     int32_t hs[4];
     for (int b = 0; b < nb; ++b) hs[b] = static_cast<int32_t>(sources[b0 + b]);
     GBX_CUDA(cudaMemcpyAsync(W.src.p, hs, nb * 4, cudaMemcpyHostToDevice, s));
+    if (relabeled) k_bc_map_sources<<<1, 32, 0, s>>>(W.src.p, nb, W.old2new.p);
     k_bc_init<<<ceil_div(n1 * 4, 256), 256, 0, s>>>(W.level.p, W.lv8.p, W.sigma.p, W.mark.p, n);
     GBX_CUDA(cudaMemsetAsync(W.map[0].p, 0, map_bytes, s));
     GBX_CUDA(cudaMemsetAsync(W.map[1].p, 0, map_bytes, s));
@@ -888,7 +950,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       a.lv8 = W.lv8.p;
       a.sigma = W.sigma.p;
       a.coef = W.delta.p;
-      a.cent = W.cent.p;
+      a.cent = cent_acc;
       a.hv = W.hub_a.hv.p;
       a.hent = W.hub_a.hent.p;
       a.nhv = W.hub_a.nhv;
@@ -920,6 +982,11 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       }
     }
     edges += A.nnz;
+  }
+  if (relabeled) {
+    k_bc_unpermute<<<ceil_div(n1, 256), 256, 0, s>>>(W.cent_new.p, W.old2new.p, n, W.cent.p);
+    GBX_LAUNCHED();
+    ++launches;
   }
   if (centrality) {
     GBX_CUDA(cudaMemcpyAsync(centrality, W.cent.p, n * 8, cudaMemcpyDeviceToHost, s));

@@ -74,6 +74,7 @@ enum Opt : int {
   kOptBfsMgPushDiv,      // "bfs_mg.push_div": multi-GPU BFS pushes while the frontier < n/div
   kOptBcAlpha,           // "bc.alpha"
   kOptBcTrace,           // "bc.trace": per-depth host timing on stderr
+  kOptBcRelabelMinN,     // "bc.relabel_min_n": graphs of at least this many vertices run Brandes on a degree-sorted copy (-1: never)
   kOptSsspTrace,         // "sssp.trace": per-phase %globaltimer log to stderr (2: + device printf)
   kOptSsspPullPct,       // "sssp.pull_pct": heavy pass by pull when pops*100 > pct*unpopped (0: never)
   kOptCount
@@ -288,6 +289,10 @@ void sort_ids_by_key(cudaStream_t s, const int32_t* key, int64_t n, bool ascendi
 // row ids per nonzero (max-scan over row starts)
 void expand_rows(cudaStream_t s, const Csr& A, DevArray<int32_t>& rowid);
 void expand_rows_into(cudaStream_t s, const Csr& A, int32_t* rowid);  // nnz entries
+// transpose of A under a relabeling, rows ascending in the new ids (pagerank.cu)
+void relabeled_transpose(cudaStream_t s, const Csr& A, const int32_t* new2old,
+                         const int32_t* old2new, const int32_t* colcount, int64_t* trp,
+                         int32_t* tcol);
 
 // Stream-ordered temporary from the device pool (freed on the stream when it
 // goes out of scope).

@@ -961,6 +961,84 @@ struct PlanTimer {
   }
 };
 
+// The transpose of A under a relabeling (plans.cuh / common.cuh): row r of the
+// result holds the new ids of the rows of A that have (old) column new2old[r],
+// ascending.  A's rows are gathered in the new order as (new column, new row)
+// pairs -- ordered by new row -- then ONE stable 32-bit radix sort by new column
+// (two sorts took 4.4 ms at scale 22, this ~2.4 ms); the row pointers are the
+// scan of A's column counts in the new order.  trp: n + 1, tcol: nnz entries.
+void relabeled_transpose(cudaStream_t s, const Csr& A, const int32_t* new2old,
+                         const int32_t* old2new, const int32_t* colcount, int64_t* trp,
+                         int32_t* tcol) {
+  PlanTimer tm{s, option(kOptPrTrace) != 0};
+  const int64_t n = A.n, nnz = A.nnz;
+  // relabeled AT, every row's columns ascending in the new ids (the thread-
+  // per-row bins then read the hub end of x together at each step): A's rows
+  // gathered in the new order as (new column, new row) pairs -- ordered by new
+  // row -- then ONE stable 32-bit radix sort by new column (two sorts took
+  // 4.4 ms at scale 22, this ~2.4 ms)
+  const int bits = bits_for(std::max<int64_t>(n, 2));
+  if (nnz) {
+    DevArray<int64_t> prp(n + 1);
+    k_pr_newlen<<<ceil_div(n + 1, 256), 256, 0, s>>>(A.rp.p, new2old, n, prp.p);
+    GBX_LAUNCHED();
+    {
+      size_t tb = 0;
+      GBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, prp.p, prp.p, n + 1, s));
+      Tmp<uint8_t> t(tb, s);
+      GBX_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, prp.p, prp.p, n + 1, s));
+    }
+    Tmp<uint32_t> kc(nnz, s), kc2(nnz, s), vr(nnz, s);
+    {
+      Tmp<int32_t> list(n, s);
+      Tmp<int> cnt(1, s);
+      GBX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), s));
+      k_pr_list_long<<<ceil_div(n, 256), 256, 0, s>>>(prp.p, n, list.p, cnt.p);
+      GBX_LAUNCHED();
+      int m = 0;
+      GBX_CUDA(cudaMemcpyAsync(&m, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      GBX_CUDA(cudaStreamSynchronize(s));
+      if (m > 0) {
+        Tmp<int64_t> nch(m, s);
+        k_pr_long_chunks<<<ceil_div(m, 256), 256, 0, s>>>(prp.p, list.p, m, nch.p);
+        size_t tb2 = 0;
+        GBX_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb2, nch.p, nch.p, m, s));
+        {
+          Tmp<uint8_t> t(tb2, s);
+          GBX_CUDA(cub::DeviceScan::InclusiveSum(t.p, tb2, nch.p, nch.p, m, s));
+        }
+        k_pr_gather_a_long<<<device_sms() * 8, 256, 0, s>>>(A.rp.p, A.col.p, new2old,
+                                                             old2new, prp.p, list.p, nch.p, m,
+                                                             kc.p, vr.p);
+      }
+    }
+    k_pr_gather_a_short<<<device_sms() * 8, 256, 0, s>>>(A.rp.p, A.col.p, new2old,
+                                                          old2new, prp.p, n, kc.p, vr.p);
+    GBX_LAUNCHED();
+    tm.mark("gather A rows (new order)");
+    // double buffers (the value alternate is the plan's own tcol) and a 32-bit item count
+    cub::DoubleBuffer<uint32_t> kb(kc.p, kc2.p);
+    cub::DoubleBuffer<uint32_t> vb(vr.p, reinterpret_cast<uint32_t*>(tcol));
+    radix_sort_pairs(s, kb, vb, nnz, 0, bits);
+    if (vb.Current() != reinterpret_cast<uint32_t*>(tcol))
+      GBX_CUDA(cudaMemcpyAsync(tcol, vb.Current(), nnz * 4, cudaMemcpyDeviceToDevice, s));
+    tm.mark("radix sort by new column");
+    // row pointers of the relabeled AT: the exclusive scan of the in-degrees in
+    // the new order (no pass over the sorted keys)
+    k_pr_gather_len<<<ceil_div(n + 1, 256), 256, 0, s>>>(colcount, new2old, n, trp);
+    GBX_LAUNCHED();
+    {
+      size_t tb = 0;
+      GBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, trp, trp, n + 1, s));
+      Tmp<uint8_t> t(tb, s);
+      GBX_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, trp, trp, n + 1, s));
+    }
+    tm.mark("row pointers");
+  } else {
+    GBX_CUDA(cudaMemsetAsync(trp, 0, (n + 1) * sizeof(int64_t), s));
+  }
+}
+
 // relabeled AT (rows by descending in-degree) + relabeled out-degree
 static void build_relabeled(gbx_graph* g, PrPlan& P) {
   PlanTimer tm{g->stream, option(kOptPrTrace) != 0};
@@ -996,72 +1074,10 @@ static void build_relabeled(gbx_graph* g, PrPlan& P) {
     GBX_LAUNCHED();
   }
   // relabeled AT, every row's columns ascending in the new ids (the thread-
-  // per-row bins then read the hub end of x together at each step): A's rows
-  // gathered in the new order as (new column, new row) pairs -- ordered by new
-  // row -- then ONE stable 32-bit radix sort by new column (two sorts took
-  // 4.4 ms at scale 22, this ~2.4 ms)
-  const int bits = bits_for(std::max<int64_t>(n, 2));
+  // per-row bins then read the hub end of x together at each step)
   P.trp.alloc(n + 1);
   P.tcol.alloc(std::max<int64_t>(nnz, 1));
-  if (nnz) {
-    DevArray<int64_t> prp(n + 1);
-    k_pr_newlen<<<ceil_div(n + 1, 256), 256, 0, s>>>(A.rp.p, P.new2old.p, n, prp.p);
-    GBX_LAUNCHED();
-    {
-      size_t tb = 0;
-      GBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, prp.p, prp.p, n + 1, s));
-      Tmp<uint8_t> t(tb, s);
-      GBX_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, prp.p, prp.p, n + 1, s));
-    }
-    Tmp<uint32_t> kc(nnz, s), kc2(nnz, s), vr(nnz, s);
-    {
-      Tmp<int32_t> list(n, s);
-      Tmp<int> cnt(1, s);
-      GBX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), s));
-      k_pr_list_long<<<ceil_div(n, 256), 256, 0, s>>>(prp.p, n, list.p, cnt.p);
-      GBX_LAUNCHED();
-      int m = 0;
-      GBX_CUDA(cudaMemcpyAsync(&m, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-      GBX_CUDA(cudaStreamSynchronize(s));
-      if (m > 0) {
-        Tmp<int64_t> nch(m, s);
-        k_pr_long_chunks<<<ceil_div(m, 256), 256, 0, s>>>(prp.p, list.p, m, nch.p);
-        size_t tb2 = 0;
-        GBX_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb2, nch.p, nch.p, m, s));
-        {
-          Tmp<uint8_t> t(tb2, s);
-          GBX_CUDA(cub::DeviceScan::InclusiveSum(t.p, tb2, nch.p, nch.p, m, s));
-        }
-        k_pr_gather_a_long<<<device_sms() * 8, 256, 0, s>>>(A.rp.p, A.col.p, P.new2old.p,
-                                                             P.old2new.p, prp.p, list.p, nch.p, m,
-                                                             kc.p, vr.p);
-      }
-    }
-    k_pr_gather_a_short<<<device_sms() * 8, 256, 0, s>>>(A.rp.p, A.col.p, P.new2old.p,
-                                                          P.old2new.p, prp.p, n, kc.p, vr.p);
-    GBX_LAUNCHED();
-    tm.mark("gather A rows (new order)");
-    // double buffers (the value alternate is the plan's own tcol) and a 32-bit item count
-    cub::DoubleBuffer<uint32_t> kb(kc.p, kc2.p);
-    cub::DoubleBuffer<uint32_t> vb(vr.p, reinterpret_cast<uint32_t*>(P.tcol.p));
-    radix_sort_pairs(s, kb, vb, nnz, 0, bits);
-    if (vb.Current() != reinterpret_cast<uint32_t*>(P.tcol.p))
-      GBX_CUDA(cudaMemcpyAsync(P.tcol.p, vb.Current(), nnz * 4, cudaMemcpyDeviceToDevice, s));
-    tm.mark("radix sort by new column");
-    // row pointers of the relabeled AT: the exclusive scan of the in-degrees in
-    // the new order (no pass over the sorted keys)
-    k_pr_gather_len<<<ceil_div(n + 1, 256), 256, 0, s>>>(len.p, P.new2old.p, n, P.trp.p);
-    GBX_LAUNCHED();
-    {
-      size_t tb = 0;
-      GBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, P.trp.p, P.trp.p, n + 1, s));
-      Tmp<uint8_t> t(tb, s);
-      GBX_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, P.trp.p, P.trp.p, n + 1, s));
-    }
-    tm.mark("row pointers");
-  } else {
-    GBX_CUDA(cudaMemsetAsync(P.trp.p, 0, (n + 1) * sizeof(int64_t), s));
-  }
+  relabeled_transpose(s, A, P.new2old.p, P.old2new.p, len.p, P.trp.p, P.tcol.p);
   GBX_CUDA(cudaStreamSynchronize(s));
 }
 

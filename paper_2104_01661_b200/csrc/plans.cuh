@@ -238,6 +238,16 @@ struct BcWork {
   DevArray<double> cent;
   DevArray<int> ctl;
   BcHubs hub_a, hub_t;       // hub rows of A (backward) and AT (forward pull)
+  // degree-sorted copy of the graph (bc_run on large graphs): vertices
+  // relabeled by descending degree, rows ascending in the new ids.  A BFS
+  // depth is then (nearly) a contiguous id range: the sigma / coef sectors a
+  // depth's edges gather are dense in L2 instead of one per 128-byte line, and
+  // the rows of a degree bin are adjacent in memory.
+  Csr ra, rat;               // relabeled A and AT (undirected: rat only, ra unused)
+  DevArray<int32_t> new2old, old2new;
+  DevArray<double> cent_new; // centrality in the new ids (cent: original ids)
+  const void* relabel_key = nullptr;
+  int64_t relabel_nnz = -1;
   std::unique_ptr<BcShard> shard;
 };
 

@@ -7,6 +7,7 @@ import pytest
 import oracle as O
 import paper_2104_01661_b200 as P
 from paper_2104_01661_b200 import algo
+from paper_2104_01661_b200.graph import call
 from tests.golden_util import Golden, case_ids
 from tests.gpu_util import graph_of, rel_l1
 
@@ -491,6 +492,67 @@ def test_bc_deep_path_and_components():
         got = algo.betweenness_centrality(g, srcs).centrality
         want = O.bc(n, rp, col, trp, tcol, np.asarray(srcs, np.int64))
         assert np.max(np.abs(got - want)) <= 1e-9 * max(1.0, np.abs(want).max())
+
+
+class _bc_relabeled:
+    """bc.relabel_min_n = 0: every graph runs Brandes on its degree-sorted copy
+    (csrc/bc.cu ensure_relabel; the default only does so from 2^18 vertices)."""
+
+    def __enter__(self):
+        call("gbx_set_option", b"bc.relabel_min_n", C.c_int64(0))
+
+    def __exit__(self, *exc):
+        call("gbx_reset_option", b"bc.relabel_min_n")
+
+
+@pytest.mark.parametrize("name", case_ids("bc"))
+def test_bc_golden_on_degree_sorted_copy(name):
+    c = CASES[name]
+    g = graph_of(c)
+    P.property_at(g)
+    with _bc_relabeled():
+        got = algo.betweenness_centrality(g, c.params["sources"]).centrality
+    assert np.max(np.abs(got - c.out["centrality"]), initial=0.0) <= 1e-9
+
+
+@pytest.mark.parametrize("und", [True, False])
+@pytest.mark.parametrize("scale,nsrc", [(14, 6), (16, 4)])
+def test_bc_rmat_on_degree_sorted_copy(und, scale, nsrc):
+    """The degree-sorted copy against the oracle and against the run on the
+    original ids (same sums in another fp64 order), directed and undirected,
+    with hub rows (scale 16) and two batches (6 sources)."""
+    kind = P.Kind.UndirectedAdjacency if und else P.Kind.DirectedAdjacency
+    g = P.generate_rmat(scale, 16, seed=8, kind=kind)
+    P.property_at(g)
+    P.property_rowdegree(g)
+    rp, col, _ = g.export()
+    n = len(rp) - 1
+    trp, tcol, _ = O.transpose(n, rp, col)
+    srcs = P.pick_sources(g.row_degree(), nsrc, 8)
+    plain = algo.betweenness_centrality(g, srcs).centrality
+    with _bc_relabeled():
+        got = algo.betweenness_centrality(g, srcs).centrality
+        again = algo.betweenness_centrality(g, srcs[:3]).centrality  # the copy is cached
+    want = O.bc(n, rp, col, trp, tcol, srcs)
+    assert rel_l1(got, want) <= 1e-9
+    assert rel_l1(got, plain) <= 1e-12
+    assert rel_l1(again, O.bc(n, rp, col, trp, tcol, srcs[:3])) <= 1e-9
+
+
+def test_bc_deep_path_on_degree_sorted_copy():
+    n_path = 700
+    edges = [(i, i + 1) for i in range(n_path - 1)]
+    base = n_path
+    edges += [(base, base + k) for k in range(1, 40)] + [(base + 39, base + 40)]
+    n = base + 42
+    rp, col = _undirected(n, edges)
+    g = P.graph_new(rp, col, kind=P.Kind.UndirectedAdjacency)
+    P.property_at(g)
+    with _bc_relabeled():
+        for srcs in ([0, 350, base + 5, 699], [3, base], [base + 41]):
+            got = algo.betweenness_centrality(g, srcs).centrality
+            want = O.bc(n, rp, col, rp, col, np.asarray(srcs, np.int64))
+            assert np.max(np.abs(got - want)) <= 1e-9 * max(1.0, np.abs(want).max())
 
 
 # ---------------------------------------------------------------- multi-GPU shard kernels
