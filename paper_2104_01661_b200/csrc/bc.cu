@@ -149,11 +149,11 @@ __device__ __forceinline__ void warp_reduce(double s[4]) {
 }
 
 #ifndef GBX_BC_UNROLL
-#define GBX_BC_UNROLL 4
+#define GBX_BC_UNROLL 8  // on the degree-sorted copy, 4 CTAs/SM: 4 / 6 / 8 / 10 / 12 / 16 -> 10.03 / 9.98 / 9.69 / 9.92 / 10.17 / 10.47 ms (scale 24, batch of 4)
 #endif
 constexpr int kBcUnroll = GBX_BC_UNROLL;  // loads in flight per lane, group/hub rows
 #ifndef GBX_BC_MINB
-#define GBX_BC_MINB 5
+#define GBX_BC_MINB 4  // on the degree-sorted copy: 3 / 4 / 5 / 6 -> 10.7 / 10.03 / 10.3 / 11.2 ms
 #endif
 constexpr int kBcMinBlocks = GBX_BC_MINB;  // resident 256-thread blocks per SM asked of ptxas
 
