@@ -100,7 +100,11 @@ const char* gbx_version(void);
  *   sssp.pull_pct          100    heavy pass of a bucket by pull (heavy in-edges, ascending
  *                                 weight, pruned) when its pops*100 > pct * vertices not yet
  *                                 popped; 0: always push
- *   bc.alpha               14     as bfs.alpha for the Brandes forward sweep */
+ *   bc.alpha               14     as bfs.alpha for the Brandes forward sweep
+ *   bc.trace               0      1: per-depth host timing on stderr
+ *   bc.relabel_min_n       262144 graphs of at least this many vertices run the batched
+ *                                 Brandes on a degree-sorted copy built once per graph
+ *                                 (sources mapped in, centrality mapped back); -1: never */
 int gbx_set_option(const char* name, int64_t value, char msg[GBX_MSG_LEN]);
 int gbx_reset_option(const char* name, char msg[GBX_MSG_LEN]);
 int gbx_get_option(const char* name, int64_t* value, char msg[GBX_MSG_LEN]);
