@@ -57,7 +57,11 @@ constexpr int kSsspBuf = 256;  // staged pushes per warp and queue
 #ifndef GBX_SSSP_SMALL
 #define GBX_SSSP_SMALL 262144  // 0 / 4096 / 32768 / 262144 -> 67.0 / 66.0 / 65.5 / 64.9 ms per 16 sources (ER 2^24)
 #endif
-constexpr int64_t kSsspSmallBucket = GBX_SSSP_SMALL;  // pops per bucket up to which the heavy pass walks a log
+constexpr int64_t kSsspSmallBucket = GBX_SSSP_SMALL;
+#ifndef GBX_SSSP_ORDERED
+#define GBX_SSSP_ORDERED 4  // 0 (never) / 4 / 16 / 64 / 256 -> 65.4 / 64.3 / 66.7 / 73.7 / 78.0 ms per 16 sources (ER 2^24)
+#endif
+constexpr int64_t kSsspOrdered = GBX_SSSP_ORDERED;  // near queues above n / this are walked in vertex order (0: never)  // pops per bucket up to which the heavy pass walks a log
 constexpr unsigned kFullW = 0xffffffffu;
 
 template <typename D> struct DistTraits;
@@ -499,12 +503,15 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
   // per vertex (8 vertices per warp), each lane 4 edges per round: 4
   // independent edge -> dist -> atomicMin chains.  pop_bits: the list's
   // membership bitmap, released as entries are taken.
+  // local: the list is this warp's own (shared memory window), walked by the
+  // warp alone; else the grid shares it warp-strided
   auto relax = [&](auto gsz, const int32_t* list, int cnt, int phase, uint32_t* pop_bits,
-                   uint32_t* push_bits, unsigned long long& nrel) {
+                   uint32_t* push_bits, unsigned long long& nrel, bool local = false) {
     constexpr int G = decltype(gsz)::value;  // lanes per vertex
     constexpr int VPW = 32 / G;              // vertices per warp step
     const int gi = lane / G, si = lane % G;
-    for (int64_t base = gwarp * VPW; base < cnt; base += nwarps * VPW) {
+    const int64_t first = local ? 0 : gwarp * VPW, stride = local ? VPW : nwarps * VPW;
+    for (int64_t base = first; base < cnt; base += stride) {
       const int64_t qi = base + gi;
       bool active = qi < cnt;
       const int32_t u = active ? list[qi] : 0;
@@ -736,13 +743,42 @@ __global__ void __launch_bounds__(kSsspThreads, GBX_SSSP_MINB) k_sssp_b(SsspBArg
       // large queues release their dedup bitmap wholesale (coalesced stores;
       // the next push into it is two barriers away) instead of one atomicAnd
       // per popped entry
-      const bool dense_clear = static_cast<int64_t>(nq) * 8 > a.words;
+      // big queues (> n / kSsspOrdered of the vertices, split plans) are walked in
+      // VERTEX order through their membership bitmap instead of in push order:
+      // the vertex records and the light edges of the popped vertices are then
+      // read front to back (DRAM pages, shared sectors) instead of one random
+      // sector each; the warp clears the bitmap words it has read
+      const bool ordered = a.nl && a.light_group == 2 && kSsspOrdered > 0 &&
+                           static_cast<int64_t>(nq) * kSsspOrdered > a.n;
+      const bool dense_clear = !ordered && static_cast<int64_t>(nq) * 8 > a.words;
       if (dense_clear)
         for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.words;
              i += int64_t(gridDim.x) * blockDim.x)
           pop_bits[i] = 0u;
       uint32_t* pb = dense_clear ? nullptr : pop_bits;
-      if (!a.nl) relax(std::integral_constant<int, 4>{}, qc, nq, 0, pb, push_bits, nrel);
+      if (ordered) {
+        int32_t* win = s_settle[threadIdx.x >> 5];
+        for (int64_t base = gwarp * 128; base < a.n; base += nwarps * 128) {
+          // 4 bitmap words = 128 vertices per step; lane l tests bit l of each
+          uint32_t wd[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int64_t wi = (base >> 5) + j;
+            wd[j] = wi < a.words ? *(volatile uint32_t*)&pop_bits[wi] : 0u;
+          }
+          int c = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const bool in = (wd[j] >> lane) & 1u;
+            if (in) win[c + __popc(wd[j] & ((1u << lane) - 1))] = static_cast<int32_t>(base + 32 * j + lane);
+            c += __popc(wd[j]);
+          }
+          if (lane < 4 && (base >> 5) + lane < a.words && wd[lane]) pop_bits[(base >> 5) + lane] = 0u;
+          __syncwarp();
+          if (c) relax(std::integral_constant<int, 2>{}, win, c, 1, nullptr, push_bits, nrel, true);
+          __syncwarp();
+        }
+      } else if (!a.nl) relax(std::integral_constant<int, 4>{}, qc, nq, 0, pb, push_bits, nrel);
       else if (a.light_group == 1) relax(std::integral_constant<int, 1>{}, qc, nq, 1, pb, push_bits, nrel);
       else if (a.light_group == 2) relax(std::integral_constant<int, 2>{}, qc, nq, 1, pb, push_bits, nrel);
       else relax(std::integral_constant<int, 4>{}, qc, nq, 1, pb, push_bits, nrel);
