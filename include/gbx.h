@@ -102,6 +102,10 @@ const char* gbx_version(void);
  *                                 popped; 0: always push
  *   bc.alpha               14     as bfs.alpha for the Brandes forward sweep
  *   bc.trace               0      1: per-depth host timing on stderr
+ *   bc.back_push           2      a backward depth runs in push form (children add into
+ *                                 their parents' sums, fp64 atomics) when its children's
+ *                                 rows hold <= 1/this of the parents' edges; 0: always pull
+ *   bc.back_push_min_depth 3      ... and the depth is at least this (hub levels pull)
  *   bc.relabel_min_n       262144 graphs of at least this many vertices run the batched
  *                                 Brandes on a degree-sorted copy built once per graph
  *                                 (sources mapped in, centrality mapped back); -1: never */

@@ -182,6 +182,7 @@ struct BcArgs {
   double* coef;
   double* cent;
   double* hacc;          // [nheavy][4] hub-row partial sums (zero between uses)
+  double* bacc;          // [n][4] backward push sums (zero between uses)
   int32_t* mark;         // push: last level that listed the vertex
   int32_t* list_out;     // vertices of the level being built
   const int32_t* list_in;
@@ -548,6 +549,86 @@ __global__ void k_bc_back_hub_fin(BcArgs a) {
   if (m) a.cent[u] += c;
 }
 
+// Backward in PUSH form (depth d from depth d+1): the children list (depth
+// d+1, binned by in-degree) adds every child's finished coefficient into
+// bacc[v] of its depth-d in-neighbours v (fp64 atomics, map_in = level map of
+// depth d); k_bc_back_fin then finalises the depth-d list from bacc and
+// re-zeroes it.  The children's rows hold far fewer edges than the parents'
+// once the BFS is past its hub levels (scale 24: depth 4 has 25 M edges, depth
+// 3 has 100 M), so this scans less than the pull form above.
+__device__ __forceinline__ void push_row(const BcArgs& a, int64_t p, int64_t e, int st, unsigned mw,
+                                         const double cw[4]) {
+  for (; p < e; p += kBcUnroll * st) {
+    int32_t v[kBcUnroll];
+#pragma unroll
+    for (int k = 0; k < kBcUnroll; ++k) {
+      v[k] = p + k * st < e ? ld_col(a.tcol + p + k * st) : -1;
+      GBX_DCHECK(v[k] < a.n, "bc back-push column", v[k]);
+    }
+    unsigned h[kBcUnroll];
+#pragma unroll
+    for (int k = 0; k < kBcUnroll; ++k) h[k] = v[k] >= 0 ? (nib(a.map_in, v[k]) & mw) : 0u;
+#pragma unroll
+    for (int k = 0; k < kBcUnroll; ++k)
+      if (h[k]) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if ((h[k] >> b) & 1u) atomicAdd(&a.bacc[static_cast<int64_t>(v[k]) * 4 + b], cw[b]);
+      }
+  }
+}
+
+__global__ void __launch_bounds__(256, kBcMinBlocks) k_bc_back_push(BcArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int grp = lane >> 3, sub = lane & 7;
+  const int64_t gwarp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int32_t* L = a.bins.list;
+  const int n0 = a.bins.cnt[0], n1 = a.bins.cnt[1], n23 = a.bins.cnt[2] + a.bins.cnt[3];
+  const int64_t s0 = (n0 + 31) / 32, s1 = (n1 + 3) / 4, tot = s0 + s1 + n23;
+  const int dc = a.d + 1;  // the children's depth
+  for (int64_t t = gwarp; t < tot; t += nwarps) {
+    int64_t w = -1;
+    int64_t p = 0, e = 0;
+    int st = 1;
+    if (t < s0) {  // a row per lane
+      const int64_t i = t * 32 + lane;
+      if (i < n0) w = L[i];
+      if (w >= 0) { p = a.trp[w]; e = a.trp[w + 1]; }
+    } else if (t < s0 + s1) {  // 8 lanes per row
+      const int64_t i = n0 + (t - s0) * 4 + grp;
+      if (i < n0 + n1) w = L[i];
+      if (w >= 0) { p = a.trp[w] + sub; e = a.trp[w + 1]; }
+      st = 8;
+    } else {  // a warp per row (hub rows too: few children are hubs)
+      w = L[n0 + n1 + (t - s0 - s1)];
+      p = a.trp[w] + lane;
+      e = a.trp[w + 1];
+      st = 32;
+    }
+    if (w < 0) continue;
+    const unsigned mw = lanes_on(a.lv8[w], dc, a.lanes, a.level, w);
+    if (!mw) continue;
+    double cw[4];
+    ld_sector(a.coef + w * 4, cw);
+    push_row(a, p, e, st, mw, cw);
+  }
+}
+
+__global__ void k_bc_back_fin(BcArgs a) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= a.n_list) return;
+  const int64_t u = a.list_in[i];
+  const unsigned m = lanes_on(a.lv8[u], a.d, a.lanes, a.level, u);
+  double acc[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    acc[b] = a.bacc[u * 4 + b];
+    if (acc[b] != 0.0) a.bacc[u * 4 + b] = 0.0;
+  }
+  if (m) bc_final(a, u, m, acc);
+}
+
 // level map of depth d from its list (backward)
 __global__ void k_bc_map(const int32_t* list, int nlist, int d, unsigned lanes,
                          const int32_t* level, const uint32_t* lv8, uint32_t* map) {
@@ -831,10 +912,12 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     launches += 2;
     // ---- forward sweep
     std::vector<int64_t> off = {0};
+    std::vector<unsigned long long> lev_edges;  // out-edges of the vertices of each depth
     struct Hc { int c[4]; unsigned long long e; } hc;
     GBX_CUDA(cudaMemcpyAsync(&hc, W.ctl.p, sizeof hc, cudaMemcpyDeviceToHost, s));
     GBX_CUDA(cudaStreamSynchronize(s));
     off.push_back(hc.c[0]);
+    lev_edges.push_back(hc.e);
     int n_ent = hc.c[1];
     unsigned long long fe = hc.e;
     unsigned live = static_cast<unsigned>(hc.c[3]);
@@ -911,6 +994,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       GBX_CUDA(cudaMemcpyAsync(&hc, W.ctl.p, sizeof hc, cudaMemcpyDeviceToHost, s));
       GBX_CUDA(cudaStreamSynchronize(s));
       off.push_back(off.back() + hc.c[0]);
+      lev_edges.push_back(hc.e);
       n_ent = hc.c[1];
       fe = hc.e;
       live = static_cast<unsigned>(hc.c[3]);
@@ -958,27 +1042,57 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       a.hacc = W.hub_a.hacc.p;
       a.d = d;
       a.lanes = all;
-      // level map of depth d+1 (the successors' depth) from its list
       const int nl1 = static_cast<int>(off[d + 2] - off[d + 1]);
+      // push form when the children's rows hold at most 1/bc.back_push of the
+      // parents' edges (and the depth is past the hub levels, whose parents
+      // would serialise the atomics)
+      const int64_t bp = option(kOptBcBackPush);
+      const bool push_back = bp > 0 && d >= option(kOptBcBackPushMinDepth) && nl1 > 0 &&
+                             lev_edges[d + 1] * static_cast<unsigned long long>(bp) <= lev_edges[d];
       GBX_CUDA(cudaMemsetAsync(W.map[0].p, 0, map_bytes, s));
-      k_bc_map<<<ceil_div(std::max(nl1, 1), 256), 256, 0, s>>>(W.order.p + off[d + 1], nl1, d + 1,
-                                                               all, W.level.p, W.lv8.p, W.map[0].p);
       a.map_in = W.map[0].p;
-      // the level-d list binned by out-degree
-      bin_list(s, W, W.order.p + off[d], nl, A, W.border.p + off[d], W.lcnt.p + 4 * d);
-      a.bins = BcBins{W.border.p + off[d], W.lcnt.p + 4 * d};
-      k_bc_back<<<grid, 256, 0, s>>>(a);
-      GBX_LAUNCHED();
-      launches += 4;
-      if (W.hub_a.nhv) {
-        k_bc_back_hub<<<grid, 256, 0, s>>>(a);
-        k_bc_back_hub_fin<<<ceil_div(W.hub_a.nhv, 256), 256, 0, s>>>(a);
+      if (push_back) {
+        // level map of depth d (the parents'), children binned by in-degree
+        k_bc_map<<<ceil_div(nl, 256), 256, 0, s>>>(W.order.p + off[d], nl, d, all, W.level.p,
+                                                   W.lv8.p, W.map[0].p);
+        bin_list(s, W, W.order.p + off[d + 1], nl1, AT, W.border.p + off[d + 1],
+                 W.lcnt.p + 4 * (d + 1));
+        a.bins = BcBins{W.border.p + off[d + 1], W.lcnt.p + 4 * (d + 1)};
+        a.trp = AT.rp.p;
+        a.tcol = AT.col.p;
+        if (!W.bacc.p) {
+          W.bacc.alloc(n1 * 4);
+          GBX_CUDA(cudaMemsetAsync(W.bacc.p, 0, W.bacc.bytes(), s));
+        }
+        a.bacc = W.bacc.p;
+        a.list_in = W.order.p + off[d];
+        a.n_list = nl;
+        k_bc_back_push<<<grid, 256, 0, s>>>(a);
+        k_bc_back_fin<<<ceil_div(nl, 256), 256, 0, s>>>(a);
         GBX_LAUNCHED();
-        launches += 2;
+        launches += 5;
+      } else {
+        // level map of depth d+1 (the successors' depth) from its list
+        k_bc_map<<<ceil_div(std::max(nl1, 1), 256), 256, 0, s>>>(W.order.p + off[d + 1], nl1, d + 1,
+                                                                 all, W.level.p, W.lv8.p, W.map[0].p);
+        // the level-d list binned by out-degree
+        bin_list(s, W, W.order.p + off[d], nl, A, W.border.p + off[d], W.lcnt.p + 4 * d);
+        a.bins = BcBins{W.border.p + off[d], W.lcnt.p + 4 * d};
+        k_bc_back<<<grid, 256, 0, s>>>(a);
+        GBX_LAUNCHED();
+        launches += 4;
+        if (W.hub_a.nhv) {
+          k_bc_back_hub<<<grid, 256, 0, s>>>(a);
+          k_bc_back_hub_fin<<<ceil_div(W.hub_a.nhv, 256), 256, 0, s>>>(a);
+          GBX_LAUNCHED();
+          launches += 2;
+        }
       }
       if (trace) {
         GBX_CUDA(cudaStreamSynchronize(s));
-        std::fprintf(stderr, "bc backward depth %d: %d vertices, %.1f us\n", d, nl, us(t0, tnow()));
+        std::fprintf(stderr, "bc backward depth %d %s: %d vertices (%llu edges; %llu below), %.1f us\n",
+                     d, push_back ? "push" : "pull", nl, lev_edges[d], lev_edges[d + 1],
+                     us(t0, tnow()));
       }
     }
     edges += A.nnz;

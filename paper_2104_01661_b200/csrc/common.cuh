@@ -74,6 +74,8 @@ enum Opt : int {
   kOptBfsMgPushDiv,      // "bfs_mg.push_div": multi-GPU BFS pushes while the frontier < n/div
   kOptBcAlpha,           // "bc.alpha"
   kOptBcTrace,           // "bc.trace": per-depth host timing on stderr
+  kOptBcBackPush,        // "bc.back_push": backward depth in push form when its children hold <= 1/this of the parents' edges (0: never)
+  kOptBcBackPushMinDepth,  // "bc.back_push_min_depth"
   kOptBcRelabelMinN,     // "bc.relabel_min_n": graphs of at least this many vertices run Brandes on a degree-sorted copy (-1: never)
   kOptSsspTrace,         // "sssp.trace": per-phase %globaltimer log to stderr (2: + device printf)
   kOptSsspPullPct,       // "sssp.pull_pct": heavy pass by pull when pops*100 > pct*unpopped (0: never)

@@ -28,6 +28,8 @@ constexpr OptDef kDefs[kOptCount] = {
     {"bfs_mg.push_div", 0, 0, 1 << 30},        // 0: Beamer's edge rule (bfs.alpha); else bfs.cpp:77-78's vertex rule
     {"bc.alpha", 14, 1, 1 << 20},
     {"bc.trace", 0, 0, 1},
+    {"bc.back_push", 2, 0, 1 << 20},
+    {"bc.back_push_min_depth", 3, 1, 1 << 20},
     {"bc.relabel_min_n", 1 << 18, -1, int64_t(1) << 40},  // scale 24: 16.4 -> see DESIGN (degree-sorted copy)
     {"sssp.trace", 0, 0, 2},
     {"sssp.pull_pct", 100, 0, 1 << 20},

@@ -246,6 +246,7 @@ struct BcWork {
   Csr ra, rat;               // relabeled A and AT (undirected: rat only, ra unused)
   DevArray<int32_t> new2old, old2new;
   DevArray<double> cent_new; // centrality in the new ids (cent: original ids)
+  DevArray<double> bacc;     // [n][4] sums of the backward push form (zero between uses)
   const void* relabel_key = nullptr;
   int64_t relabel_nnz = -1;
   std::unique_ptr<BcShard> shard;

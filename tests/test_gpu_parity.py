@@ -539,6 +539,45 @@ def test_bc_rmat_on_degree_sorted_copy(und, scale, nsrc):
     assert rel_l1(again, O.bc(n, rp, col, trp, tcol, srcs[:3])) <= 1e-9
 
 
+@pytest.mark.parametrize("relabel", [False, True])
+def test_bc_backward_push_form(relabel):
+    """The backward sweep in push form (csrc/bc.cu k_bc_back_push: children add
+    their coefficients into their parents' sums) forced at every depth
+    (bc.back_push = 1 accepts any edge ratio >= 1, min depth 1), against the
+    oracle and the pull form: goldens, R-MAT 14 / 16 directed and undirected."""
+    try:
+        call("gbx_set_option", b"bc.back_push", C.c_int64(1))
+        call("gbx_set_option", b"bc.back_push_min_depth", C.c_int64(1))
+        if relabel:
+            call("gbx_set_option", b"bc.relabel_min_n", C.c_int64(0))
+        for name in case_ids("bc"):
+            c = CASES[name]
+            g = graph_of(c)
+            P.property_at(g)
+            got = algo.betweenness_centrality(g, c.params["sources"]).centrality
+            assert np.max(np.abs(got - c.out["centrality"]), initial=0.0) <= 1e-9, name
+        for scale, und in ((14, True), (14, False), (16, True), (16, False)):
+            kind = P.Kind.UndirectedAdjacency if und else P.Kind.DirectedAdjacency
+            g = P.generate_rmat(scale, 16, seed=8, kind=kind)
+            P.property_at(g)
+            P.property_rowdegree(g)
+            rp, col, _ = g.export()
+            n = len(rp) - 1
+            trp, tcol, _ = O.transpose(n, rp, col)
+            srcs = P.pick_sources(g.row_degree(), 6, 8)
+            got = algo.betweenness_centrality(g, srcs).centrality
+            st = g.last_stats()
+            assert rel_l1(got, O.bc(n, rp, col, trp, tcol, srcs)) <= 1e-9, (scale, und)
+            call("gbx_set_option", b"bc.back_push", C.c_int64(0))
+            pull = algo.betweenness_centrality(g, srcs).centrality
+            assert g.last_stats()["launches"] != st["launches"]  # the push form did run
+            call("gbx_set_option", b"bc.back_push", C.c_int64(1))
+            assert rel_l1(got, pull) <= 1e-12, (scale, und)
+    finally:
+        for o in (b"bc.back_push", b"bc.back_push_min_depth", b"bc.relabel_min_n"):
+            call("gbx_reset_option", o)
+
+
 def test_bc_deep_path_on_degree_sorted_copy():
     n_path = 700
     edges = [(i, i + 1) for i in range(n_path - 1)]

@@ -16,6 +16,9 @@ g = P.generate_rmat(scale, 16, seed=1, kind=P.Kind.UndirectedAdjacency)
 P.property_at(g)
 P.property_rowdegree(g)
 s = np.ascontiguousarray(P.pick_sources(g.row_degree(), 4, 1), np.uint64)
+for kv in sys.argv[2:]:
+    k, v = kv.split("=")
+    call("gbx_set_option", k.encode(), C.c_int64(int(v)))
 for _ in range(3):
     call("gbx_betweenness", None, g.handle, s.ctypes.data, 4)
 call("gbx_set_option", b"bc.trace", C.c_int64(1))
