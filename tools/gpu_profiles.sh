@@ -27,7 +27,7 @@ python tools/prof_pr.py 22 4 pagerank.host_loop=1 > $OUT/pr_plain.log 2>&1 && \
 $FULL -k regex:'^k_pr_rows' -s 4 -c 1 -o $OUT/pagerank_k_pr_rows -f \
   python tools/prof_pr.py 22 4 pagerank.host_loop=1 > $OUT/pr.log 2>&1; echo pr rc=$?
 [ "$WHAT" = "pr" ] && { echo done; exit 0; }
-for w in "tc 22 ^k_tc_warp$ 0" "bc 24 ^k_bc_pull$ 0" "bc 24 ^k_bc_back$ 4" "sssp 24 ^k_sssp_b 0" "bfs 22 ^k_bfs1$ 0" "bfs64 16 ^k_bfs64$ 0"; do
+for w in "tc 22 ^k_tc_warp$ 0" "bc 24 ^k_bc_pull$ 0" "bc 24 ^k_bc_back$ 0" "bc 24 ^k_bc_back_push$ 2" "sssp 24 ^k_sssp_b 0" "bfs 22 ^k_bfs1$ 0" "bfs64 16 ^k_bfs64$ 0"; do
   set -- $w
   python tools/prof_algo.py $1 $2 > $OUT/${1}_plain.log 2>&1 && \
   $FULL -k regex:"$3" -s $4 -c 1 -o $OUT/${1}_$(echo $3 | tr -d '^$') -f python tools/prof_algo.py $1 $2 \
