@@ -42,8 +42,14 @@ namespace gbx {
 
 constexpr int kBcLanes = 4;
 constexpr int64_t kBcChunk = 256;    // push entries: edges per warp
-constexpr int64_t kBcHeavy = 2048;   // rows longer than this are chunked
-constexpr int64_t kBcHChunk = 2048;  // edges per hub-row chunk
+#ifndef GBX_BC_HEAVY
+#define GBX_BC_HEAVY 2048
+#endif
+#ifndef GBX_BC_HCHUNK
+#define GBX_BC_HCHUNK 1024
+#endif
+constexpr int64_t kBcHeavy = GBX_BC_HEAVY;    // rows longer than this are chunked
+constexpr int64_t kBcHChunk = GBX_BC_HCHUNK;  // edges per hub-row chunk
 constexpr int kBcBuf = 256;
 constexpr unsigned kAll = 0xffffffffu;
 
@@ -161,7 +167,13 @@ constexpr int kBcMinBlocks = GBX_BC_MINB;  // resident 256-thread blocks per SM 
 // so a warp step handles rows of one shape -- bin 0 (<= kBin0 edges): one
 // row per lane; bin 1 (<= kBin1): 8-lane groups, 4 rows per warp; bin 2
 // (<= kBcHeavy): one row per warp; bin 3 (hubs): the chunked side passes.
-constexpr int64_t kBin0 = 8, kBin1 = 64;
+#ifndef GBX_BC_BIN0
+#define GBX_BC_BIN0 16  // on the degree-sorted copy (scale 24): 4 / 8 / 16 -> 8.38 / 8.13 / 8.03 ms
+#endif
+#ifndef GBX_BC_BIN1
+#define GBX_BC_BIN1 256  // 32 / 64 / 128 / 256 / 512 -> 8.17 / 8.13 / 7.77 / 7.61 / 7.60 ms; with bin 0 <= 16 and 1024-edge hub chunks: 7.52
+#endif
+constexpr int64_t kBin0 = GBX_BC_BIN0, kBin1 = GBX_BC_BIN1;
 __device__ __forceinline__ uint8_t deg_bin(int64_t deg) {
   return deg <= kBin0 ? 0 : deg <= kBin1 ? 1 : deg <= kBcHeavy ? 2 : 3;
 }
