@@ -114,7 +114,7 @@ def sharded_pagerank_p2p(backend, dist, damping=0.85, tol=1e-4, itermax=100, to_
     """GAP PageRank over `world` ranks with the exchange FUSED into the iteration
     kernel (gbx_pr_shard_run_p2p): one cooperative launch per rank runs every
     iteration; each row epilogue stores its contribution straight into every
-    rank's x over NVLink (symmetric-memory peer pointers), the L1 partials go
+    rank's x over NVLink (peer pointers), the L1 partials go
     to every rank's slot table, and a device-side signal barrier separates
     iterations -- no host round trip and no NCCL call per iteration.  One NCCL
     all-gather of the local ranks at the end.  Same results and iteration
@@ -257,7 +257,7 @@ def sharded_betweenness_rows(backend, dist, sources):
     return total.cpu().numpy().copy()
 
 
-# symmetric buffers of the fused P2P PageRank, keyed by (world, chunk, device)
+# buffers of the fused P2P PageRank (one-rank torch driver), keyed by (world, chunk, device)
 _P2P_BUFFERS = {}
 
 
@@ -334,26 +334,31 @@ class GpuShardBackend:
 
     def x_new_slice(self):
         return self._xs
-    # ---- fused P2P run (gbx_pr_shard_run_p2p) over symmetric memory
+    # ---- fused P2P run (gbx_pr_shard_run_p2p)
     def p2p_setup(self, dist):
-        """Symmetric x0 / x1 / slot table / signal buffers, rendezvoused over the
-        world group; their peer pointers go to the kernel."""
+        """x0 / x1 / slot table / signal buffers and the table of every rank's
+        pointers to them.  This torch driver only serves a ONE-rank group (plain
+        device buffers, the rank is its own peer): with more ranks the peer
+        buffers come from the library's own communicator (CUDA IPC handles
+        exchanged over gbx_comm), i.e. mg.Comm / DGraph.pagerank -- the C++ path
+        -- so no private torch API is involved."""
         import torch
-        import torch.distributed._symmetric_memory as symm_mem
+        if self.world != 1:
+            raise NotImplementedError(
+                "the torch driver of the fused exchange serves one rank; multi-rank runs go "
+                "through paper_2104_01661_b200.mg (gbx_comm_init + gbx_pagerank_mg)")
         if getattr(self, "_p2p_world", None) == (self.world, self.chunk):
             return
-        group = dist.group.WORLD
         dev = self.device
         key = (self.world, self.chunk, str(dev))
-        if key not in _P2P_BUFFERS:  # allocation + rendezvous once per layout
-            bufs = [symm_mem.empty(self.world * self.chunk, dtype=torch.float32, device=dev),
-                    symm_mem.empty(self.world * self.chunk, dtype=torch.float32, device=dev),
-                    symm_mem.empty(2 * self.world, dtype=torch.float64, device=dev),
-                    symm_mem.empty(4, dtype=torch.int32, device=dev)]
-            hdl = [symm_mem.rendezvous(t, group) for t in bufs]
-            ptr = [np.ascontiguousarray([int(p) for p in h.buffer_ptrs], np.uint64) for h in hdl]
+        if key not in _P2P_BUFFERS:  # allocated once per layout
+            bufs = [torch.empty(self.world * self.chunk, dtype=torch.float32, device=dev),
+                    torch.empty(self.world * self.chunk, dtype=torch.float32, device=dev),
+                    torch.empty(2 * self.world, dtype=torch.float64, device=dev),
+                    torch.empty(4, dtype=torch.int32, device=dev)]
+            ptr = [np.ascontiguousarray([t.data_ptr()], np.uint64) for t in bufs]
             _P2P_BUFFERS.clear()
-            _P2P_BUFFERS[key] = (bufs, hdl, ptr)
+            _P2P_BUFFERS[key] = (bufs, None, ptr)
         self._pbufs, self._phdl, self._pptr = _P2P_BUFFERS[key]
         for a in self._pptr:
             assert len(a) == self.world

@@ -1,6 +1,6 @@
 """The fused multi-GPU PageRank (gbx_pr_shard_run_p2p: x stored into every
 rank's copy over peer pointers, device-side signal barrier per iteration) on a
-one-rank NCCL group: the kernel, the symmetric-memory plumbing and the driver
+one-rank NCCL group: the kernel, the peer-pointer plumbing and the driver
 (dist.sharded_pagerank_p2p) against the single-GPU PageRank and the NCCL-
 exchange driver.  (Ranks > 1 need one GPU each: the kernels wait on each
 other, so they are not simulated on one GPU.)"""
