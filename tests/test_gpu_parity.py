@@ -676,6 +676,36 @@ def test_tc_partition_rows_sum():
     assert sum(parts) == algo.basic.triangle_count(g)
 
 
+@pytest.mark.parametrize("with_zero_rows", [True, False])
+def test_pagerank_bin_boundary_lengths(with_zero_rows):
+    """In-degrees ON the plan's class boundaries (csrc/pagerank.cu: thread-per-row
+    bins up to 80 nonzeros, warp-per-row up to 2048, 1024-nonzero chunks beyond;
+    rows without in-edges claimed dynamically) against the oracle
+    (pagerank.cpp:8-81): same iteration count, rel. L1 <= 1e-4 -- with and
+    without empty rows, fp32 and fp64 storage."""
+    rng = np.random.default_rng(11)
+    n = 4096
+    lens = [1, 2, 3, 4, 5, 31, 32, 33, 63, 64, 65, 79, 80, 81, 82, 127, 128, 129, 255, 256, 257,
+            1023, 1024, 1025, 2047, 2048, 2049, 2050, 3071, 3072, 3073, 4000]
+    if with_zero_rows:
+        lens += [0] * 7
+    indeg = np.array([lens[i % len(lens)] for i in range(n)], np.int64)
+    # AT row i = indeg[i] distinct sources, ascending; A = its transpose
+    trp = np.concatenate([[0], np.cumsum(indeg)])
+    tcol = np.concatenate([np.sort(rng.choice(n, size=int(k), replace=False)) for k in indeg]
+                          + [np.empty(0, np.int64)]).astype(np.int32)
+    rp, col, _ = O.transpose(n, trp, tcol)
+    g = P.graph_new(rp, col, kind=P.Kind.DirectedAdjacency)
+    P.property_at(g)
+    P.property_rowdegree(g)
+    outdeg = np.diff(rp)
+    for tol in (1e-4, 1e-9):  # fp32 and fp64 storage
+        want, iters = O.pagerank(n, trp, tcol, outdeg, 0.85, tol, 100)
+        r = algo.pagerank_gap(g, 0.85, tol, 100)
+        assert r.iterations == iters, (tol, r.iterations, iters)
+        assert rel_l1(r.rank, want) <= (1e-4 if tol == 1e-4 else 1e-9), tol
+
+
 def test_pagerank_nonpositive_itermax_passes_through():
     """pagerank.cpp:52-75: iterations = min(k, itermax) with k = 1 when the loop
     never runs -- a non-positive itermax comes back unchanged, ranks stay 1/n."""
