@@ -249,6 +249,7 @@ struct BcWork {
   DevArray<double> bacc;     // [n][4] sums of the backward push form (zero between uses)
   const void* relabel_key = nullptr;
   int64_t relabel_nnz = -1;
+  int64_t relabel_nz = 0;    // vertices with edges (ids [0, relabel_nz) of the copy)
   std::unique_ptr<BcShard> shard;
 };
 
