@@ -23,6 +23,9 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
 #include "common.cuh"
 #include "plans.cuh"
 #include "warpqueue.cuh"
@@ -76,6 +79,8 @@ struct Bfs1Args {
   int32_t* ul1;
   const int32_t* heavy;  // in-degree > kBfsHeavy: pulled by whole warps, never listed
   int64_t nheavy;
+  const int32_t* unz;    // vertices with in-edges, ascending: what the FIRST pull scans
+  int64_t nunz;          // (vertices without in-edges can never be pulled)
   int* ctl;  // [5] levels done [6] push levels; slot j = ctl + 16 + 8 * (j & 3) describes
              // the frontier level j produced: [0] queue entries [1] vertices [2:4) u64
              // frontier edges [4] unvisited-list size (-1: not built) [5] list parity
@@ -230,17 +235,26 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
     } else {
       // scan every vertex the first time, afterwards only the ones a previous
       // pull left unvisited (vertices with no in-edges never enter the list)
-      const int32_t* ucur = upar ? a.ul1 : a.ul0;
+      // the first pull scans the (per-graph) list of vertices WITH in-edges --
+      // on an R-MAT graph 45% of the vertices have none and would cost a step
+      // slot, a level word and two row pointers each in a latency-bound level
+      const int32_t* ucur = ucnt < 0 ? a.unz : (upar ? a.ul1 : a.ul0);
       uq.reset(upar ? a.ul0 : a.ul1, &sn[4]);
-      const int64_t range = ucnt < 0 ? a.n : ucnt;
+      const int64_t range = ucnt < 0 ? a.nunz : ucnt;
       const int grp = lane >> 3, sub = lane & 7;
       // 32 vertices per warp step, one per lane: the level/row-pointer loads
       // coalesce and every lane scans its own row 4 edges per round (the 4
       // neighbour and 4 bitmap loads are independent); rows still unresolved
       // after kThreadRounds rounds go to 8-lane groups, 4 rows at a time.
+      // (the next step's list entry is loaded a step ahead: one register, one
+      //  round trip less per step)
+      int32_t wnext = gwarp * 32 + lane < range ? ucur[gwarp * 32 + lane] : -1;
       for (int64_t vb = gwarp * 32; vb < range; vb += nwarps * 32) {
-        const int64_t i = vb + lane;
-        const int64_t w = i < range ? (ucnt < 0 ? i : ucur[i]) : a.n;
+        const int64_t w = wnext >= 0 ? wnext : a.n;
+        {
+          const int64_t i = vb + nwarps * 32 + lane;
+          wnext = i < range ? ucur[i] : -1;
+        }
         // the row pointers are loaded together with the level (not behind its
         // test): one round trip less per 32-vertex step of a latency-bound level
         // (26 steps per warp at scale 22, each a chain vertex -> level / row
@@ -391,6 +405,11 @@ static int coop_grid(const void* fn, int threads) {
   return device_sms() * per_sm;
 }
 
+struct HasInEdges {
+  const int64_t* trp;
+  __device__ __forceinline__ bool operator()(int32_t v) const { return trp[v + 1] > trp[v]; }
+};
+
 __global__ void k_bfs_heavy(const int64_t* trp, int64_t n, int32_t* out, int* cnt) {
   int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (v < n && trp[v + 1] - trp[v] > kBfsHeavy) out[atomicAdd(cnt, 1)] = static_cast<int32_t>(v);
@@ -412,6 +431,21 @@ static void ensure_heavy(gbx_graph* g, const Csr& AT) {
   GBX_CUDA(cudaMemcpyAsync(&c, W.heavy_cnt.p, sizeof c, cudaMemcpyDeviceToHost, s));
   GBX_CUDA(cudaStreamSynchronize(s));
   W.nheavy = c;
+  // vertices with in-edges, ascending (the first pull's work list)
+  W.unz.alloc(std::max<int64_t>(n, 1));
+  {
+    Tmp<int64_t> nsel(1, s);
+    size_t tb = 0;
+    HasInEdges pred{AT.rp.p};
+    thrust::counting_iterator<int32_t> ids(0);
+    GBX_CUDA(cub::DeviceSelect::If(nullptr, tb, ids, W.unz.p, nsel.p, static_cast<int>(n), pred, s));
+    Tmp<uint8_t> t(tb, s);
+    GBX_CUDA(cub::DeviceSelect::If(t.p, tb, ids, W.unz.p, nsel.p, static_cast<int>(n), pred, s));
+    int64_t h = 0;
+    GBX_CUDA(cudaMemcpyAsync(&h, nsel.p, sizeof h, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+    W.nunz = h;
+  }
   W.heavy_key = AT.rp.p;
   W.heavy_nnz = AT.nnz;
 }
@@ -487,6 +521,8 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
   a.ul1 = W.ulist[1].p;
   a.heavy = W.heavy.p;
   a.nheavy = W.nheavy;
+  a.unz = AT ? W.unz.p : nullptr;
+  a.nunz = AT ? W.nunz : 0;
   a.divisor = push_divisor == 0 ? 1 : static_cast<int64_t>(push_divisor);
   a.level = W.level.p;
   a.parent = W.parent.p;

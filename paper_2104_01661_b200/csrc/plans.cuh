@@ -106,6 +106,8 @@ struct BfsWork {
   DevArray<int32_t> heavy;
   DevArray<int> heavy_cnt;
   int64_t nheavy = 0;
+  DevArray<int32_t> unz;                    // vertices with in-edges, ascending (first pull)
+  int64_t nunz = 0;
   const void* heavy_key = nullptr;
   int64_t heavy_nnz = -1;
 };
