@@ -598,6 +598,8 @@ struct Bfs64Args {
   int pull_div;               // pull once frontier edges >= nnz / pull_div
   const int32_t* heavy;       // vertices with in-degree > kBfsHeavy
   int64_t nheavy;
+  const int32_t* unz;         // vertices with in-edges, ascending: what a pull level scans
+  int64_t nunz;
 };
 
 
@@ -710,8 +712,9 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs64(Bfs64Args a) {
     } else {
       const int grp = lane >> 3, sub = lane & 7;
       const unsigned gmask = 0xffu << (grp * 8);
-      for (int64_t vb = gwarp * 4; vb < a.n; vb += nwarps * 4) {
-        const int64_t w = vb + grp;
+      // (only the vertices with in-edges: the others can never be pulled)
+      for (int64_t vb = gwarp * 4; vb < a.nunz; vb += nwarps * 4) {
+        const int64_t w = vb + grp < a.nunz ? a.unz[vb + grp] : a.n;
         unsigned long long need = w < a.n ? (~(a.seen[w] | fc[w]) & a.lanes) : 0ull;
         bool active = need != 0ull;
         int64_t pp = active ? a.trp[w] : 0, pe = active ? a.trp[w + 1] : 0;
@@ -947,6 +950,8 @@ void bfs_batch_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, int64_t* 
     const int pull_div = static_cast<int>(option(kOptBfs64PullDiv));
     a.pull_div = pull_div;
     a.heavy = W.heavy.p;
+    a.unz = W.unz.p;
+    a.nunz = W.nunz;
     a.nheavy = W.nheavy;
     const bool tlog_on = option(kOptBfsTrace) != 0;
     if (tlog_on) {
