@@ -200,6 +200,48 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
       int S = 1;
       while (S < 8 && static_cast<int64_t>(qe) * S * 2 <= nwarps) S <<= 1;
       const int64_t sub = kChunk / S;
+      // many entries with few edges each (the traversal's late levels: ~5 edges
+      // per frontier vertex): four entries per warp step, 8 lanes each -- a warp
+      // per entry leaves most lanes idle and walks the entries one dependent
+      // chain after the other
+      const bool grouped = S == 1 && fe < 16ull * static_cast<unsigned long long>(qe);
+      if (grouped) {
+        const int grp = lane >> 3, sl = lane & 7;
+        for (int64_t e4 = gwarp * 4; e4 < qe; e4 += nwarps * 4) {
+          const int64_t e = e4 + grp;
+          int32_t v = 0;
+          int64_t q = 0, e0 = 0;
+          if (e < qe) {
+            const int64_t ent = qc[e];
+            v = static_cast<int32_t>(ent & 0xffffffff);
+            const int64_t c = ent >> 32;
+            const int64_t cb = a.rp[v] + c * kChunk;
+            e0 = min(a.rp[v + 1], cb + kChunk);
+            q = cb + sl;
+          }
+          bool active = q < e0;
+          while (__any_sync(kFull, active)) {
+            bool has = false;
+            int32_t w = 0;
+            if (active) {
+              w = __ldg(a.col + q);
+              GBX_DCHECK(w >= 0 && w < a.n, "bfs push column", w);
+              const int lw = *(volatile int32_t*)&a.level[w];
+              const int32_t pw = *(volatile int32_t*)&a.parent[w];
+              if ((lw == -1 || lw == d) && v < pw) {
+                atomicMin(&a.parent[w], v);
+                if (lw == -1 && atomicCAS(&a.level[w], -1, d) == -1) {
+                  has = true;
+                  atomicOr(&bn[w >> 5], 1u << (w & 31));
+                }
+              }
+              q += 8;
+              if (q >= e0) active = false;
+            }
+            fq.push(has, w);
+          }
+        }
+      } else
       for (int64_t e2 = gwarp; e2 < static_cast<int64_t>(qe) * S; e2 += nwarps) {
         const int64_t e = e2 / S;
         const int part = static_cast<int>(e2 - e * S);
@@ -392,6 +434,7 @@ static void dump_tlog(BfsWork& W, const char* tag) {
   std::vector<unsigned long long> t(4 * 256);
   GBX_CUDA(cudaMemcpy(t.data(), W.tlog.p, t.size() * 8, cudaMemcpyDeviceToHost));
   if (t[0] && t[1]) std::fprintf(stderr, "%s kernel %.1fus\n", tag, (t[1] - t[0]) / 1e3);
+  if (t[0] && t[4]) std::fprintf(stderr, "%s initial state %.1fus\n", tag, (t[4] - t[0]) / 1e3);
   for (int d = 1; d < 256 && t[4 * d]; ++d)
     std::fprintf(stderr, "%s level %d %s qv=%llu work=%.1fus finalize=%.1fus\n", tag, d,
                  (t[4 * d + 3] & 1) ? "push" : "pull", t[4 * d + 3] >> 8,
