@@ -42,9 +42,25 @@ constexpr int kBfsBuf = 256;  // staged frontier vertices per warp
 constexpr int64_t kChunk = GBX_BFS_CHUNK;  // push: edges per warp entry (latency-bound steps)
 constexpr unsigned kFull = 0xffffffffu;
 // In-degree above which a pull row goes to a whole warp instead of 8 lanes.
-constexpr int64_t kBfsHeavy = 256;
+// The 64-lane batch has to find a parent for every lane, so its hubs are
+// scanned far (256); a single-source pull stops at the first frontier hit,
+// which a hub meets within its first in-edges: a separate pass over them only
+// costs (scale 22, 8 sources: 256 / 512 / 1024 / 2048 / 4096 / 8192 / none ->
+// 2.16 / 1.91 / 1.86 / 1.85 / 1.83 / 1.83 / 1.82 ms; 8192 keeps a bound on what
+// one lane group may have to walk).
+#ifndef GBX_BFS_HEAVY
+#define GBX_BFS_HEAVY 256
+#endif
+#ifndef GBX_BFS1_HEAVY
+#define GBX_BFS1_HEAVY 8192
+#endif
+constexpr int64_t kBfsHeavy = GBX_BFS_HEAVY;
+constexpr int64_t kBfs1Heavy = GBX_BFS1_HEAVY;
 // Pull: 4-edge rounds a lane scans its own row before handing it to a group.
-constexpr int kThreadRounds = 2;
+#ifndef GBX_BFS_ROUNDS
+#define GBX_BFS_ROUNDS 2
+#endif
+constexpr int kThreadRounds = GBX_BFS_ROUNDS;
 
 __device__ __forceinline__ int n_chunks(int64_t deg) {
   return deg <= kChunk ? 1 : static_cast<int>((deg + kChunk - 1) / kChunk);
@@ -308,7 +324,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs1(Bfs1Args a) {
         int64_t pp = inr ? a.trp[w] : 0, pe = inr ? a.trp[w + 1] : 0;
         bool active = inr && lw0 == -1;
         if (!active) pp = pe = 0;
-        if (pe - pp > kBfsHeavy) active = false;  // hub: the warp pass below
+        if (pe - pp > kBfs1Heavy) active = false;  // hub: the warp pass below
         const bool cand = active && pe > pp;
         active = cand;
         int32_t found = -1;
@@ -453,9 +469,9 @@ struct HasInEdges {
   __device__ __forceinline__ bool operator()(int32_t v) const { return trp[v + 1] > trp[v]; }
 };
 
-__global__ void k_bfs_heavy(const int64_t* trp, int64_t n, int32_t* out, int* cnt) {
+__global__ void k_bfs_heavy(const int64_t* trp, int64_t n, int64_t thr, int32_t* out, int* cnt) {
   int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (v < n && trp[v + 1] - trp[v] > kBfsHeavy) out[atomicAdd(cnt, 1)] = static_cast<int32_t>(v);
+  if (v < n && trp[v + 1] - trp[v] > thr) out[atomicAdd(cnt, 1)] = static_cast<int32_t>(v);
 }
 
 // hub list for the pull passes, rebuilt when the transpose changes
@@ -464,16 +480,20 @@ static void ensure_heavy(gbx_graph* g, const Csr& AT) {
   if (W.heavy_key == AT.rp.p && W.heavy_nnz == AT.nnz && W.heavy.p) return;
   const int64_t n = AT.n;
   cudaStream_t s = g->stream;
-  W.heavy.alloc(std::max<int64_t>(n, 1));
   if (!W.heavy_cnt.p) W.heavy_cnt.alloc(1);
-  GBX_CUDA(cudaMemsetAsync(W.heavy_cnt.p, 0, sizeof(int), s));
-  k_bfs_heavy<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, s>>>(AT.rp.p, n, W.heavy.p,
-                                                                    W.heavy_cnt.p);
-  GBX_LAUNCHED();
-  int c = 0;
-  GBX_CUDA(cudaMemcpyAsync(&c, W.heavy_cnt.p, sizeof c, cudaMemcpyDeviceToHost, s));
-  GBX_CUDA(cudaStreamSynchronize(s));
-  W.nheavy = c;
+  // two hub lists: the 64-lane batch's (kBfsHeavy) and the single source's (kBfs1Heavy)
+  for (int which = 0; which < 2; ++which) {
+    DevArray<int32_t>& list = which ? W.heavy1 : W.heavy;
+    list.alloc(std::max<int64_t>(n, 1));
+    GBX_CUDA(cudaMemsetAsync(W.heavy_cnt.p, 0, sizeof(int), s));
+    k_bfs_heavy<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, s>>>(
+        AT.rp.p, n, which ? kBfs1Heavy : kBfsHeavy, list.p, W.heavy_cnt.p);
+    GBX_LAUNCHED();
+    int c = 0;
+    GBX_CUDA(cudaMemcpyAsync(&c, W.heavy_cnt.p, sizeof c, cudaMemcpyDeviceToHost, s));
+    GBX_CUDA(cudaStreamSynchronize(s));
+    (which ? W.nheavy1 : W.nheavy) = c;
+  }
   // vertices with in-edges, ascending (the first pull's work list)
   W.unz.alloc(std::max<int64_t>(n, 1));
   {
@@ -562,8 +582,8 @@ void bfs_run(gbx_graph* g, uint64_t source, int direction, uint64_t push_divisor
   a.alpha = alpha;
   a.ul0 = W.ulist[0].p;
   a.ul1 = W.ulist[1].p;
-  a.heavy = W.heavy.p;
-  a.nheavy = W.nheavy;
+  a.heavy = W.heavy1.p;
+  a.nheavy = W.nheavy1;
   a.unz = AT ? W.unz.p : nullptr;
   a.nunz = AT ? W.nunz : 0;
   a.divisor = push_divisor == 0 ? 1 : static_cast<int64_t>(push_divisor);

@@ -103,9 +103,9 @@ struct BfsWork {
   DevArray<int32_t> msrc;                   // batch lanes + distinct sources
   DevArray<unsigned long long> tlog;
   // pull-mode hubs (in-degree > kBfsHeavy) handled warp-per-vertex
-  DevArray<int32_t> heavy;
+  DevArray<int32_t> heavy, heavy1;          // the 64-lane batch's hubs / the single source's
   DevArray<int> heavy_cnt;
-  int64_t nheavy = 0;
+  int64_t nheavy = 0, nheavy1 = 0;
   DevArray<int32_t> unz;                    // vertices with in-edges, ascending (first pull)
   int64_t nunz = 0;
   const void* heavy_key = nullptr;
