@@ -97,7 +97,7 @@ const char* gbx_version(void);
  *   bfs_mg.push_div        0      gbx_bfs_mg: 0 = push while frontier edges < nnz/bfs.alpha,
  *                                 else push while the frontier < n/div (bfs.cpp:77-78)
  *   bfs.trace / sssp.trace 0      1: per-level %globaltimer log on stderr (sssp 2: + device printf)
- *   sssp.pull_pct          100    heavy pass of a bucket by pull (heavy in-edges, ascending
+  *   sssp.pull_pct          50     heavy pass of a bucket by pull (heavy in-edges, ascending
  *                                 weight, pruned) when its pops*100 > pct * vertices not yet
  *                                 popped; 0: always push
  *   bc.alpha               14     as bfs.alpha for the Brandes forward sweep

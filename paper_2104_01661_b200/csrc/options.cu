@@ -32,7 +32,7 @@ constexpr OptDef kDefs[kOptCount] = {
     {"bc.back_push_min_depth", 3, 1, 1 << 20},
     {"bc.relabel_min_n", 1 << 18, -1, int64_t(1) << 40},  // scale 24: 16.4 -> see DESIGN (degree-sorted copy)
     {"sssp.trace", 0, 0, 2},
-    {"sssp.pull_pct", 100, 0, 1 << 20},
+    {"sssp.pull_pct", 50, 0, 1 << 20},  // 25 / 50 / 100 / 200 / 400 -> 62.8 / 62.7 / 63.8 / 64.2 / 65.4 ms (ER 2^24, 16 sources)
 };
 
 std::atomic<int64_t> g_val[kOptCount] = {};
