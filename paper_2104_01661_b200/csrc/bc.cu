@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(256) k_bc_pull_hub_fin(BcArgs a) {
   unsigned found = 0;
   for (int64_t base = gwarp * 32; base < a.nhv; base += nwarps * 32) {
     const int64_t slot = base + lane;
-    bool has = false;
+    bool has = false, still = false;
     int32_t v = 0;
     if (slot < a.nhv) {
       v = a.hv[slot];
@@ -454,8 +454,13 @@ __global__ void __launch_bounds__(256) k_bc_pull_hub_fin(BcArgs a) {
         found |= nm;
         has = true;
       }
+      still = (um & ~nm) != 0;
     }
     fq.push(has, v);
+    // hubs still unreached in a live lane: while there are none, the next
+    // pulls skip the hub passes (a walk over every hub chunk otherwise)
+    const unsigned sb = __ballot_sync(kAll, still);
+    if (lane == 0 && sb) atomicAdd(&a.cnt[6], __popc(sb));
   }
   fq.flush();
 #pragma unroll
@@ -943,7 +948,8 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
     // ---- forward sweep
     std::vector<int64_t> off = {0};
     std::vector<unsigned long long> lev_edges;  // out-edges of the vertices of each depth
-    struct Hc { int c[4]; unsigned long long e; } hc;
+    struct Hc { int c[4]; unsigned long long e; int hubs_left; int pad; } hc;
+    bool hubs_left = true;  // some hub row is unreached in a live lane (unknown before a pull)
     GBX_CUDA(cudaMemcpyAsync(&hc, W.ctl.p, sizeof hc, cudaMemcpyDeviceToHost, s));
     GBX_CUDA(cudaStreamSynchronize(s));
     off.push_back(hc.c[0]);
@@ -961,6 +967,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       if (off.back() == off[off.size() - 2]) break;
       const auto t0 = tnow();
       GBX_CUDA(cudaMemsetAsync(W.ctl.p, 0, sizeof hc, s));
+      bool pulled_hubs = false;
       BcArgs a{};
       a.own0 = 0;
       a.own1 = n;
@@ -1014,7 +1021,8 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
         k_bc_pull<<<grid, 256, 0, s>>>(a);
         GBX_LAUNCHED();
         ++launches;
-        if (HT.nhv) {
+        pulled_hubs = HT.nhv && hubs_left;
+        if (pulled_hubs) {
           k_bc_pull_hub<<<grid, 256, 0, s>>>(a);
           k_bc_pull_hub_fin<<<ceil_div(HT.nhv, 256), 256, 0, s>>>(a);
           GBX_LAUNCHED();
@@ -1029,6 +1037,7 @@ void bc_run(gbx_graph* g, const uint64_t* sources, uint64_t ns, double* centrali
       fe = hc.e;
       live = static_cast<unsigned>(hc.c[3]);
       if (!push) ucnt = hc.c[2];
+      if (pulled_hubs) hubs_left = hc.hubs_left > 0;
       GBX_CUDA(cudaMemsetAsync(W.map[cur].p, 0, map_bytes, s));  // depth d-1 map retired
       cur ^= 1;
       if (trace)
