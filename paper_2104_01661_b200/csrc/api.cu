@@ -19,6 +19,7 @@ gbx_graph::~gbx_graph() {
     cudaSetDevice(device);
     cudaStreamSynchronize(stream);
   }
+  gbx::ReleaseScope all_idle;  // one device synchronisation for every array below
   pr.reset();
   tc.reset();
   sssp.reset();

@@ -100,6 +100,23 @@ int device_sms();
 // from the device's stream-ordered pool (kept cached: see Scope) so building
 // and freeing graphs does not remap hundreds of MB through cudaMalloc/cudaFree
 // each time; allocation and release both synchronise, like cudaMalloc/cudaFree.
+// While a ReleaseScope is alive on this thread the device has been
+// synchronised and nothing new is launched: DevArray::release skips its own
+// cudaDeviceSynchronize (a graph handle owns ~30 arrays).
+inline int& release_scope_depth() {
+  static thread_local int depth = 0;
+  return depth;
+}
+struct ReleaseScope {
+  ReleaseScope() {
+    cudaDeviceSynchronize();
+    ++release_scope_depth();
+  }
+  ~ReleaseScope() { --release_scope_depth(); }
+  ReleaseScope(const ReleaseScope&) = delete;
+  ReleaseScope& operator=(const ReleaseScope&) = delete;
+};
+
 template <typename T>
 struct DevArray {
   T* p = nullptr;
@@ -132,7 +149,9 @@ struct DevArray {
   void ensure(size_t count) { if (n < count) alloc(count); }
   void release() {
     if (p) {
-      cudaDeviceSynchronize();  // every stream's work on p is done
+      // every stream's work on p is done (a handle's destructor synchronises
+      // the device once for all of its arrays: ReleaseScope)
+      if (!release_scope_depth()) cudaDeviceSynchronize();
       cudaFreeAsync(p, 0);
     }
     p = nullptr;
